@@ -1,0 +1,188 @@
+/*
+ * equil_b200.h -- C ABI of the B200 equilibration hot path (libequil_b200.so).
+ *
+ * Drop-in boundary for the reference's algorithm-level entry points
+ * (SURVEY.md §8(b)).  Each function names the reference interface it replaces.
+ * Plain pointers and sizes only; host pointers unless stated otherwise.
+ * Reference paths are relative to the reference's proj/ tree.
+ *
+ * Error convention (include/equil/common.hpp:16-22): precondition failures
+ * (detail::require -> std::invalid_argument) return EQUIL_EINVAL, runtime
+ * failures (detail::check -> std::runtime_error) return EQUIL_ERUNTIME; CUDA /
+ * NCCL / allocation failures have their own codes.  The message of the last
+ * failure on the calling thread is available from equil_last_error().
+ */
+#ifndef EQUIL_B200_H
+#define EQUIL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EQUIL_OK = 0,
+  EQUIL_EINVAL = 1,   /* std::invalid_argument */
+  EQUIL_ERUNTIME = 2, /* std::runtime_error */
+  EQUIL_ECUDA = 3,
+  EQUIL_ENCCL = 4,
+  EQUIL_ENOMEM = 5
+} equil_status;
+
+/* Opaque device-resident matrix: CSR(A), CSR(A^T) built on device, traversal
+ * plans, workspaces.  Replaces ExplicitMatrix (include/equil/explicit_matrix.hpp:13-86)
+ * as the operand of the entry points below. */
+typedef struct equil_matrix equil_matrix;
+
+/* EquilibrationParams (include/equil/params.hpp:14-23).  alpha/beta == 0 means
+ * "auto" (src/params.cpp:7-33). */
+typedef struct {
+  double alpha;
+  double beta;
+  double gamma;
+  double max_log_scale;
+  int iterations;
+  uint64_t seed;
+} equil_params;
+
+/* Device placement.  world_size > 1 row-shards A and A^T across one process per
+ * GPU and all-gathers e.*s and d.*w with NCCL each iteration; nccl_id points to
+ * the 128-byte ncclUniqueId shared by all ranks (ignored when world_size == 1). */
+typedef struct {
+  int device;
+  int rank;
+  int world_size;
+  const void* nccl_id;
+} equil_device_cfg;
+
+/* DiagnosticsConfig (include/equil/equilibrate.hpp:63-67): history at t = 0
+ * and every `stride` iterations; condition numbers are out of scope. */
+typedef struct {
+  int stride; /* 0 disables history */
+  int want_objective;
+  int want_rms;
+} equil_diag_cfg;
+
+/* ScalingResult (include/equil/equilibrate.hpp:69-78).  Caller-allocated
+ * buffers; u,d have m entries and v,e n entries (full length on every rank).
+ * hist_* have capacity hist_cap (>= iterations/stride + 1). */
+typedef struct {
+  double* u;
+  double* v;
+  double* d;
+  double* e;
+  int outputs_on_device; /* nonzero: u,v,d,e are device pointers */
+  double alpha, beta;
+  int box_feasible;
+  int iterate_bound_ok;
+  long long apply_count;
+  long long adjoint_count;
+  int* hist_iter;
+  double* hist_objective;
+  double* hist_rms;
+  int hist_cap;
+  int hist_len;
+} equil_scaling_out;
+
+/* LsqrRun (include/equil/lsqr.hpp:10-23).  x has n entries; residual_history
+ * capacity residual_cap (>= max_iters + 1, + iterations for preconditioned). */
+typedef struct {
+  double* x;
+  double* residual_history;
+  int residual_cap;
+  int hist_len;
+  int iterations;
+  int equil_iterations;
+  int reached_tol;
+  int breakdown;
+  long long apply_count;
+  long long adjoint_count;
+} equil_lsqr_out;
+
+/* ---- defaults / params (src/params.cpp) -------------------------------- */
+void equil_params_default(equil_params* p); /* params.hpp:14-23 defaults */
+/* resolve_targets (src/params.cpp:7-33) */
+equil_status equil_resolve_targets(const equil_params* p, int64_t rows,
+                                   int64_t cols, double* alpha, double* beta);
+/* validate_params (src/params.cpp:35-44) */
+equil_status equil_validate_params(const equil_params* p);
+
+/* ---- matrix store ------------------------------------------------------- */
+/* ExplicitMatrix::sparse (src/explicit_matrix.cpp:19-57) for input that is
+ * already canonical CSR (rows ascending, columns strictly ascending): uploads,
+ * validates on device, and builds CSR(A^T) on device bit-identically to
+ * ExplicitMatrix::transposed() (:117-125).  Non-canonical input -> EINVAL. */
+equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                                     const int32_t* col, const double* val,
+                                     const equil_device_cfg* cfg,
+                                     equil_matrix** out);
+/* ExplicitMatrix::dense (src/explicit_matrix.cpp:8-17); input row-major. */
+equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowmajor,
+                                       const equil_device_cfg* cfg,
+                                       equil_matrix** out);
+void equil_matrix_destroy(equil_matrix* A);
+equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
+                                int64_t* nnz);
+/* The cudaStream_t all work on this handle is issued on (for event timing). */
+void* equil_matrix_stream(equil_matrix* A);
+
+/* LinearOperator::apply / apply_adjoint (include/equil/linop.hpp:13-25,
+ * src/explicit_matrix.cpp:67-93): y = A x or x = A^T y, host vectors. */
+equil_status equil_apply(equil_matrix* A, const double* x, double* y, int adjoint);
+
+/* ---- the hot path -------------------------------------------------------- */
+/* sgd_equilibrate(op, params, diag) (include/equil/equilibrate.hpp:89-91,
+ * src/equilibrate.cpp:138-221).  diag may be NULL. */
+equil_status equil_sgd_equilibrate(equil_matrix* A, const equil_params* p,
+                                   const equil_diag_cfg* diag,
+                                   equil_scaling_out* out);
+/* lsqr(op, b, max_iters, tol) (include/equil/lsqr.hpp:30-31, src/lsqr.cpp:85-103) */
+equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
+                        equil_lsqr_out* out);
+/* lsqr_preconditioned(op, b, params, max_iters, tol)
+ * (include/equil/lsqr.hpp:38-40, src/lsqr.cpp:105-138) */
+equil_status equil_lsqr_preconditioned(equil_matrix* A, const double* b,
+                                       const equil_params* p, int max_iters,
+                                       double tol, equil_lsqr_out* out);
+
+/* One-shot convenience for callers that only hold host CSR: create + equilibrate
+ * + destroy (all host<->device traffic inside the call). */
+equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                                       const int32_t* col, const double* val,
+                                       const equil_params* p,
+                                       const equil_device_cfg* cfg,
+                                       equil_scaling_out* out);
+
+/* ---- verification hooks -------------------------------------------------- */
+/* Sign bits of SeededRng(seed, stream) outputs [start, start+count), generated
+ * on device (K1); bit k of the packed u32 words = MSB of output start+k. */
+equil_status equil_sign_bits(uint64_t seed, uint64_t stream, uint64_t start,
+                             uint64_t count, uint32_t* bits_out, int device);
+/* CSR(A^T) as built on device (K2); arrays sized n+1, nnz, nnz. */
+equil_status equil_export_transpose(equil_matrix* A, int64_t* t_row_ptr,
+                                    int32_t* t_col, double* t_val);
+/* det_exp evaluated on device, elementwise (numerics contract). */
+equil_status equil_det_exp_device(const double* x, double* y, int64_t n, int device);
+/* Host side of the same contract (for ABI tests without a GPU). */
+double equil_det_exp_host(double x);
+/* Canonical sum of squares on device. */
+equil_status equil_canon_sumsq_device(const double* x, int64_t n, double* out,
+                                      int device);
+/* Row partition used for world_size > 1: splits [0, rows) into `parts`
+ * contiguous ranges balanced by nnz + rows; bounds has parts + 1 entries. */
+equil_status equil_partition_rows(const int64_t* row_ptr, int64_t rows, int parts,
+                                  int64_t* bounds);
+
+/* ncclGetUniqueId for rank 0 of a multi-GPU run (128 bytes). */
+equil_status equil_nccl_unique_id(void* out128);
+
+const char* equil_last_error(void);
+const char* equil_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EQUIL_B200_H */

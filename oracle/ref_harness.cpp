@@ -1,0 +1,236 @@
+// ref_harness.cpp -- extern "C" wrapper over the REFERENCE's own hot-path
+// translation units (TEST INFRASTRUCTURE).  oracle/Makefile compiles
+// /root/reference/proj/src/{rng,params,linop,estimator,explicit_matrix,
+// equilibrate,lsqr,metrics}.cpp unmodified against oracle/eigen_lite and links
+// this file, producing oracle/_ref/libequil_ref.so.  Tests use it to pin the C
+// restatement (equil_oracle.c) and bench.py --impl reference times it.
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "equil/equilibrate.hpp"
+#include "equil/explicit_matrix.hpp"
+#include "equil/lsqr.hpp"
+#include "equil/metrics.hpp"
+#include "equil/rng.hpp"
+
+using namespace equil;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+Vec to_vec(const double* p, int64_t n) {
+  Vec v(n);
+  std::memcpy(v.data(), p, static_cast<std::size_t>(n) * sizeof(double));
+  return v;
+}
+void from_vec(const Vec& v, double* p) {
+  if (p) std::memcpy(p, v.data(), static_cast<std::size_t>(v.size()) * sizeof(double));
+}
+}  // namespace
+
+extern "C" {
+
+const char* er_last_error() { return g_err.c_str(); }
+
+void er_rng_outputs(uint64_t seed, uint64_t stream, uint64_t count, uint64_t* out) {
+  SeededRng r(seed, stream);
+  for (uint64_t k = 0; k < count; ++k) out[k] = r.next_u64();
+}
+
+void er_rng_draws(uint64_t seed, uint64_t stream, int kind, uint64_t count,
+                  double* out) {
+  SeededRng r(seed, stream);
+  for (uint64_t k = 0; k < count; ++k)
+    out[k] = kind == 0 ? r.uniform01() : (kind == 1 ? r.normal() : r.sign());
+}
+
+// Matrix handle: ExplicitMatrix::sparse from the CSR arrays (construction is
+// the reference's own sort + duplicate check, explicit_matrix.cpp:19-57).
+int er_matrix_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                  const int32_t* col, const double* val, void** out) {
+  return guarded([&] {
+    std::vector<ExplicitMatrix::Entry> ent;
+    ent.reserve(static_cast<std::size_t>(row_ptr[m]));
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+        ent.push_back({i, static_cast<Index>(col[k]), val[k]});
+    *out = new ExplicitMatrix(ExplicitMatrix::sparse(m, n, std::move(ent)));
+  });
+}
+
+int er_matrix_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                  const int64_t* cols, const double* vals, void** out) {
+  return guarded([&] {
+    std::vector<ExplicitMatrix::Entry> ent(static_cast<std::size_t>(nnz));
+    for (int64_t k = 0; k < nnz; ++k) ent[k] = {rows[k], cols[k], vals[k]};
+    *out = new ExplicitMatrix(ExplicitMatrix::sparse(m, n, std::move(ent)));
+  });
+}
+
+int er_matrix_dense(int64_t m, int64_t n, const double* rowmajor, void** out) {
+  return guarded([&] {
+    Mat A(m, n);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) A(i, j) = rowmajor[i * n + j];
+    *out = new ExplicitMatrix(ExplicitMatrix::dense(std::move(A)));
+  });
+}
+
+void er_matrix_free(void* h) { delete static_cast<ExplicitMatrix*>(h); }
+
+int64_t er_matrix_nnz(void* h) {
+  return static_cast<ExplicitMatrix*>(h)->stored_entries();
+}
+
+// CSR export (for_each_entry order = CSR order); row_ptr m+1.
+void er_matrix_export(void* h, int64_t* row_ptr, int32_t* col, double* val) {
+  const auto& A = *static_cast<ExplicitMatrix*>(h);
+  int64_t k = 0;
+  row_ptr[0] = 0;
+  Index last = 0;
+  A.for_each_entry([&](Index i, Index j, double v) {
+    while (last < i) row_ptr[++last] = k;
+    col[k] = static_cast<int32_t>(j);
+    val[k] = v;
+    ++k;
+  });
+  while (last < A.rows()) row_ptr[++last] = k;
+}
+
+void* er_matrix_transposed(void* h) {
+  return new ExplicitMatrix(static_cast<ExplicitMatrix*>(h)->transposed());
+}
+
+int er_apply(void* h, const double* x, double* y, int adjoint) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    if (adjoint)
+      from_vec(A.apply_adjoint(to_vec(x, A.rows())), y);
+    else
+      from_vec(A.apply(to_vec(x, A.cols())), y);
+  });
+}
+
+struct er_sgd_out {
+  double* u;
+  double* v;
+  double* d;
+  double* e;
+  double alpha, beta;
+  int box_feasible, iterate_bound_ok;
+  long long apply_count, adjoint_count;
+  int* hist_iter;
+  double* hist_objective;
+  double* hist_rms;
+  int hist_len;
+};
+
+int er_sgd_equilibrate(void* h, double alpha, double beta, double gamma,
+                       double max_log_scale, int iterations, uint64_t seed,
+                       int diag_stride, er_sgd_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    EquilibrationParams p;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.gamma = gamma;
+    p.max_log_scale = max_log_scale;
+    p.iterations = iterations;
+    p.seed = seed;
+    DiagnosticsConfig diag;
+    if (diag_stride > 0) {
+      diag.matrix = &A;
+      diag.stride = diag_stride;
+    }
+    const ScalingResult r = sgd_equilibrate(A, p, diag);
+    from_vec(r.u, out->u);
+    from_vec(r.v, out->v);
+    from_vec(r.d, out->d);
+    from_vec(r.e, out->e);
+    out->alpha = r.alpha;
+    out->beta = r.beta;
+    out->box_feasible = r.box_feasible;
+    out->iterate_bound_ok = r.iterate_bound_ok;
+    out->apply_count = r.apply_count;
+    out->adjoint_count = r.adjoint_count;
+    out->hist_len = static_cast<int>(r.history.size());
+    for (std::size_t k = 0; k < r.history.size(); ++k) {
+      if (out->hist_iter) out->hist_iter[k] = r.history[k].iter;
+      if (out->hist_objective)
+        out->hist_objective[k] = r.history[k].objective.value_or(0.0);
+      if (out->hist_rms) out->hist_rms[k] = r.history[k].rms.value_or(0.0);
+    }
+  });
+}
+
+struct er_lsqr_out {
+  double* x;
+  double* residual_history;  // capacity given by caller
+  int hist_len;
+  int iterations, equil_iterations, reached_tol, breakdown;
+  long long apply_count, adjoint_count;
+};
+
+static void copy_run(const LsqrRun& r, er_lsqr_out* out) {
+  from_vec(r.x, out->x);
+  out->hist_len = static_cast<int>(r.residual_history.size());
+  std::memcpy(out->residual_history, r.residual_history.data(),
+              r.residual_history.size() * sizeof(double));
+  out->iterations = r.iterations;
+  out->equil_iterations = r.equil_iterations;
+  out->reached_tol = r.reached_tol;
+  out->breakdown = r.breakdown;
+  out->apply_count = r.apply_count;
+  out->adjoint_count = r.adjoint_count;
+}
+
+int er_lsqr(void* h, const double* b, int max_iters, double tol,
+            er_lsqr_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    copy_run(lsqr(A, to_vec(b, A.rows()), max_iters, tol), out);
+  });
+}
+
+int er_lsqr_preconditioned(void* h, const double* b, double alpha, double beta,
+                           double gamma, double max_log_scale, int iterations,
+                           uint64_t seed, int max_iters, double tol,
+                           er_lsqr_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    EquilibrationParams p;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.gamma = gamma;
+    p.max_log_scale = max_log_scale;
+    p.iterations = iterations;
+    p.seed = seed;
+    copy_run(lsqr_preconditioned(A, to_vec(b, A.rows()), p, max_iters, tol),
+             out);
+  });
+}
+
+double er_rms_error(void* h, const double* u, const double* v, double alpha,
+                    double beta) {
+  const auto& A = *static_cast<ExplicitMatrix*>(h);
+  return rms_error(A, to_vec(u, A.rows()), to_vec(v, A.cols()), alpha, beta);
+}
+
+}  // extern "C"

@@ -1,0 +1,20 @@
+"""B200-native stochastic matrix-free equilibration (arXiv 1602.06621 hot path).
+
+The product is libequil_b200.so (hand-written sm_100a CUDA + C++ host engine,
+C ABI in include/equil_b200.h); this package is the Python mirror of the
+reference's interface over that ABI.  See DESIGN.md.
+"""
+from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
+                  DiagnosticsConfig, EquilibrationParams, EquilRuntimeError,
+                  ExplicitMatrix, InvalidArgument, IterationRecord, LsqrRun,
+                  ScalingResult, canon_sumsq_device, det_exp_device, lsqr,
+                  lsqr_preconditioned, nccl_unique_id, partition_rows,
+                  resolve_targets, sgd_equilibrate, sign_bits, validate_params)
+
+__all__ = [
+    "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "DiagnosticsConfig",
+    "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",
+    "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",
+    "lsqr", "lsqr_preconditioned", "nccl_unique_id", "partition_rows", "resolve_targets",
+    "sgd_equilibrate", "sign_bits", "validate_params",
+]

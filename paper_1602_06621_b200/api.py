@@ -1,0 +1,342 @@
+"""Python mirror of the reference's interface for the equilibration hot path.
+
+Same names, argument meaning and error behaviour as the reference's C++ API
+(include/equil/{params,explicit_matrix,equilibrate,lsqr}.hpp); every call goes
+through the C ABI of libequil_b200.so (include/equil_b200.h) and runs on the
+GPU.  ``InvalidArgument`` stands for std::invalid_argument (detail::require),
+``EquilRuntimeError`` for std::runtime_error (detail::check).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+K_AUTO_TARGET = 0.0
+DEFAULT_MAX_LOG_SCALE = 9.210340371976184  # log(1e4), include/equil/params.hpp:20
+SGD_PROBE_STREAM = 17                      # include/equil/streams.hpp:17
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument (include/equil/common.hpp:16-18)."""
+
+
+class EquilRuntimeError(RuntimeError):
+    """std::runtime_error (include/equil/common.hpp:20-22) and CUDA/NCCL failures."""
+
+
+def _check(rc: int) -> None:
+    if rc == L.EQUIL_OK:
+        return
+    msg = L.load().equil_last_error().decode()
+    if rc == L.EQUIL_EINVAL:
+        raise InvalidArgument(msg)
+    raise EquilRuntimeError(f"[status {rc}] {msg}")
+
+
+@dataclass
+class EquilibrationParams:
+    """include/equil/params.hpp:14-23."""
+    alpha: float = K_AUTO_TARGET
+    beta: float = K_AUTO_TARGET
+    gamma: float = 0.1
+    max_log_scale: float = DEFAULT_MAX_LOG_SCALE
+    iterations: int = 1000
+    seed: int = 0
+
+    def _c(self) -> L.Params:
+        return L.Params(self.alpha, self.beta, self.gamma, self.max_log_scale,
+                        int(self.iterations), int(self.seed))
+
+
+@dataclass
+class DiagnosticsConfig:
+    """include/equil/equilibrate.hpp:63-67 (``matrix`` is implicit: the
+    operator being equilibrated; condition numbers are out of scope)."""
+    stride: int = 1
+    want_objective: bool = True
+    want_rms: bool = True
+
+
+@dataclass
+class IterationRecord:
+    """include/equil/equilibrate.hpp:51-56."""
+    iter: int
+    objective: Optional[float] = None
+    rms: Optional[float] = None
+    cond: Optional[float] = None
+
+
+@dataclass
+class ScalingResult:
+    """include/equil/equilibrate.hpp:69-78."""
+    u: np.ndarray
+    v: np.ndarray
+    d: np.ndarray
+    e: np.ndarray
+    alpha: float = 0.0
+    beta: float = 0.0
+    history: list = field(default_factory=list)
+    box_feasible: bool = True
+    iterate_bound_ok: bool = True
+    apply_count: int = 0
+    adjoint_count: int = 0
+
+
+@dataclass
+class LsqrRun:
+    """include/equil/lsqr.hpp:10-23."""
+    x: np.ndarray
+    residual_history: list
+    iterations: int = 0
+    equil_iterations: int = 0
+    reached_tol: bool = False
+    breakdown: bool = False
+    apply_count: int = 0
+    adjoint_count: int = 0
+
+
+def resolve_targets(params: EquilibrationParams, rows: int, cols: int):
+    """src/params.cpp:7-33 -> (alpha, beta)."""
+    a, b = C.c_double(), C.c_double()
+    p = params._c()
+    _check(L.load().equil_resolve_targets(C.byref(p), rows, cols, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def validate_params(params: EquilibrationParams) -> None:
+    """src/params.cpp:35-44."""
+    p = params._c()
+    _check(L.load().equil_validate_params(C.byref(p)))
+
+
+class ExplicitMatrix:
+    """Device-resident matrix behind the reference's ExplicitMatrix interface
+    (include/equil/explicit_matrix.hpp:13-86): CSR(A) and CSR(A^T) (built on
+    the device), or dense row-major.  Also the LinearOperator plugin
+    (rows/cols/apply/apply_adjoint, include/equil/linop.hpp:13-25)."""
+
+    def __init__(self, handle, m, n, nnz, dense):
+        self._h = handle
+        self._m, self._n, self._nnz, self._dense = m, n, nnz, dense
+
+    # -- construction ------------------------------------------------------
+    @staticmethod
+    def from_csr(rows: int, cols: int, row_ptr, col, val, device: int = 0,
+                 rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None):
+        """Canonical CSR (columns strictly ascending per row); validated and
+        transposed on the device."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col, dtype=np.int32)
+        va = np.ascontiguousarray(val, dtype=np.float64)
+        if rp.size != rows + 1 and rows > 0:
+            raise InvalidArgument("ExplicitMatrix::sparse: row_ptr must have rows + 1 entries")
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        cfg = L.DeviceCfg(device, rank, world_size,
+                          C.cast(idbuf, C.c_void_p) if idbuf is not None else None)
+        h = C.c_void_p()
+        _check(L.load().equil_matrix_create_csr(rows, cols, L.ptr(rp, L._i64p),
+                                                L.ptr(ci, L._i32p), L.ptr(va, L._dp),
+                                                C.byref(cfg), C.byref(h)))
+        return ExplicitMatrix(h, rows, cols, int(rp[-1]) if rows > 0 else 0, False)
+
+    @staticmethod
+    def sparse(rows: int, cols: int, entries, device: int = 0):
+        """ExplicitMatrix::sparse (src/explicit_matrix.cpp:19-57): entries are
+        (row, col, value) triples in any order; range check, sort by (row, col),
+        duplicate rejection, then CSR."""
+        if not (rows > 0 and cols > 0):
+            raise InvalidArgument("ExplicitMatrix::sparse: dimensions must be positive")
+        if isinstance(entries, tuple) and len(entries) == 3 and hasattr(entries[0], "__len__"):
+            r = np.asarray(entries[0], dtype=np.int64)
+            c = np.asarray(entries[1], dtype=np.int64)
+            v = np.asarray(entries[2], dtype=np.float64)
+        else:
+            ent = list(entries)
+            r = np.array([e[0] for e in ent], dtype=np.int64)
+            c = np.array([e[1] for e in ent], dtype=np.int64)
+            v = np.array([e[2] for e in ent], dtype=np.float64)
+        bad = (r < 0) | (r >= rows) | (c < 0) | (c >= cols)
+        if bad.any():
+            k = int(np.argmax(bad))
+            raise InvalidArgument(
+                f"ExplicitMatrix::sparse: entry ({r[k]}, {c[k]}) out of range")
+        order = np.lexsort((c, r))
+        r, c, v = r[order], c[order], v[order]
+        if r.size > 1:
+            dup = (r[1:] == r[:-1]) & (c[1:] == c[:-1])
+            if dup.any():
+                k = int(np.argmax(dup)) + 1
+                raise InvalidArgument(
+                    f"ExplicitMatrix::sparse: duplicate entry ({r[k]}, {c[k]})")
+        rp = np.zeros(rows + 1, dtype=np.int64)
+        np.add.at(rp, r + 1, 1)
+        rp = np.cumsum(rp)
+        return ExplicitMatrix.from_csr(rows, cols, rp, c.astype(np.int32), v, device)
+
+    @staticmethod
+    def dense(values, device: int = 0):
+        """ExplicitMatrix::dense (src/explicit_matrix.cpp:8-17)."""
+        a = np.ascontiguousarray(values, dtype=np.float64)
+        if a.ndim != 2 or a.shape[0] <= 0 or a.shape[1] <= 0:
+            raise InvalidArgument("ExplicitMatrix::dense: dimensions must be positive")
+        cfg = L.DeviceCfg(device, 0, 1, None)
+        h = C.c_void_p()
+        _check(L.load().equil_matrix_create_dense(a.shape[0], a.shape[1], L.ptr(a, L._dp),
+                                                  C.byref(cfg), C.byref(h)))
+        return ExplicitMatrix(h, a.shape[0], a.shape[1], a.size, True)
+
+    @staticmethod
+    def identity(n: int, device: int = 0):
+        """ExplicitMatrix::identity (src/explicit_matrix.cpp:59-65)."""
+        if n <= 0:
+            raise InvalidArgument("ExplicitMatrix::identity: n must be positive")
+        return ExplicitMatrix.from_csr(n, n, np.arange(n + 1), np.arange(n), np.ones(n), device)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            L.load().equil_matrix_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- LinearOperator ----------------------------------------------------
+    def rows(self) -> int:
+        return self._m
+
+    def cols(self) -> int:
+        return self._n
+
+    def is_sparse(self) -> bool:
+        return not self._dense
+
+    def stored_entries(self) -> int:
+        return self._nnz
+
+    def apply(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.size != self._n:
+            raise InvalidArgument("ExplicitMatrix::apply: size mismatch")
+        y = np.zeros(self._m)
+        _check(L.load().equil_apply(self._h, L.ptr(x, L._dp), L.ptr(y, L._dp), 0))
+        return y
+
+    def apply_adjoint(self, y) -> np.ndarray:
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if y.size != self._m:
+            raise InvalidArgument("ExplicitMatrix::apply_adjoint: size mismatch")
+        x = np.zeros(self._n)
+        _check(L.load().equil_apply(self._h, L.ptr(y, L._dp), L.ptr(x, L._dp), 1))
+        return x
+
+    def transposed_csr(self):
+        """CSR(A^T) exactly as built on the device (verification hook)."""
+        trp = np.zeros(self._n + 1, np.int64)
+        tc = np.zeros(max(self._nnz, 1), np.int32)
+        tv = np.zeros(max(self._nnz, 1), np.float64)
+        _check(L.load().equil_export_transpose(self._h, L.ptr(trp, L._i64p),
+                                               L.ptr(tc, L._i32p), L.ptr(tv, L._dp)))
+        return trp, tc[: self._nnz], tv[: self._nnz]
+
+
+def sgd_equilibrate(op: ExplicitMatrix, params: EquilibrationParams | None = None,
+                    diag: DiagnosticsConfig | None = None) -> ScalingResult:
+    """sgd_equilibrate (include/equil/equilibrate.hpp:89-91)."""
+    params = params or EquilibrationParams()
+    m, n = op.rows(), op.cols()
+    u, v, d, e = np.zeros(m), np.zeros(n), np.zeros(m), np.zeros(n)
+    cap = (max(int(params.iterations), 0) // diag.stride + 1) if diag and diag.stride > 0 else 1
+    hi = np.zeros(cap, np.int32)
+    ho = np.zeros(cap)
+    hr = np.zeros(cap)
+    out = L.ScalingOut(L.ptr(u, L._dp), L.ptr(v, L._dp), L.ptr(d, L._dp), L.ptr(e, L._dp), 0,
+                       0.0, 0.0, 0, 0, 0, 0, L.ptr(hi, L._ip), L.ptr(ho, L._dp),
+                       L.ptr(hr, L._dp), cap, 0)
+    p = params._c()
+    dc = L.DiagCfg(diag.stride, int(diag.want_objective), int(diag.want_rms)) if diag else None
+    _check(L.load().equil_sgd_equilibrate(op._h, C.byref(p),
+                                          C.byref(dc) if dc is not None else None,
+                                          C.byref(out)))
+    hist = [IterationRecord(int(hi[k]), float(ho[k]) if diag.want_objective else None,
+                            float(hr[k]) if diag.want_rms else None)
+            for k in range(out.hist_len)] if diag else []
+    return ScalingResult(u, v, d, e, out.alpha, out.beta, hist, bool(out.box_feasible),
+                         bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
+
+
+def _lsqr_run(x, h, out) -> LsqrRun:
+    return LsqrRun(x, list(h[: out.hist_len]), out.iterations, out.equil_iterations,
+                   bool(out.reached_tol), bool(out.breakdown), out.apply_count,
+                   out.adjoint_count)
+
+
+def lsqr(op: ExplicitMatrix, b, max_iters: int, rel_residual_tol: float) -> LsqrRun:
+    """lsqr (include/equil/lsqr.hpp:30-31)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.size != op.rows():
+        raise InvalidArgument("lsqr: rhs length mismatch")
+    x = np.zeros(op.cols())
+    h = np.zeros(max(max_iters, 0) + 1)
+    out = L.LsqrOut(L.ptr(x, L._dp), L.ptr(h, L._dp), h.size, 0, 0, 0, 0, 0, 0, 0)
+    _check(L.load().equil_lsqr(op._h, L.ptr(b, L._dp), int(max_iters), float(rel_residual_tol),
+                               C.byref(out)))
+    return _lsqr_run(x, h, out)
+
+
+def lsqr_preconditioned(op: ExplicitMatrix, b, equil_params: EquilibrationParams,
+                        max_iters: int, rel_residual_tol: float) -> LsqrRun:
+    """lsqr_preconditioned (include/equil/lsqr.hpp:38-40)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.size != op.rows():
+        raise InvalidArgument("lsqr_preconditioned: rhs length mismatch")
+    x = np.zeros(op.cols())
+    h = np.zeros(max(max_iters, 0) + max(int(equil_params.iterations), 0) + 2)
+    out = L.LsqrOut(L.ptr(x, L._dp), L.ptr(h, L._dp), h.size, 0, 0, 0, 0, 0, 0, 0)
+    p = equil_params._c()
+    _check(L.load().equil_lsqr_preconditioned(op._h, L.ptr(b, L._dp), C.byref(p),
+                                              int(max_iters), float(rel_residual_tol),
+                                              C.byref(out)))
+    return _lsqr_run(x, h, out)
+
+
+def sign_bits(seed: int, stream: int, start: int, count: int, device: int = 0) -> np.ndarray:
+    """Device-generated probe sign bits (verification hook, K1)."""
+    out = np.zeros((count + 31) // 32 + 1, np.uint32)
+    _check(L.load().equil_sign_bits(seed, stream, start, count, L.ptr(out, L._u32p), device))
+    return out[: (count + 31) // 32]
+
+
+def det_exp_device(x, device: int = 0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(x)
+    _check(L.load().equil_det_exp_device(L.ptr(x, L._dp), L.ptr(y, L._dp), x.size, device))
+    return y
+
+
+def canon_sumsq_device(x, device: int = 0) -> float:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = C.c_double()
+    _check(L.load().equil_canon_sumsq_device(L.ptr(x, L._dp), x.size, C.byref(out), device))
+    return out.value
+
+
+def partition_rows(row_ptr, parts: int) -> np.ndarray:
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    b = np.zeros(parts + 1, np.int64)
+    _check(L.load().equil_partition_rows(L.ptr(rp, L._i64p), rp.size - 1, parts,
+                                         L.ptr(b, L._i64p)))
+    return b
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(L.load().equil_nccl_unique_id(buf))
+    return buf.raw

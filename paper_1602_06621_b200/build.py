@@ -1,0 +1,83 @@
+"""Build libequil_b200.so in-tree (nvcc, sm_100a).
+
+    python -m paper_1602_06621_b200.build          # incremental
+    python -m paper_1602_06621_b200.build --force
+
+The library is the product: CUDA kernels + the host engine + the C ABI declared
+in include/equil_b200.h.  It is compiled with --fmad=false and
+-ffp-contract=off because the trajectory must reproduce the reference's
+separately rounded multiply/add sequence bit for bit.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(CSRC, "build")
+LIB = os.path.join(HERE, "libequil_b200.so")
+GEN_LIB = os.path.join(HERE, "libequil_gen.so")  # synthetic inputs (bench/tests)
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+CU_SOURCES = ["kernels.cu", "engine.cu"]
+CXX_SOURCES = ["mt64_host.cpp"]
+HEADERS = ["det_math.cuh", "internal.h", "mt64_host.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xptxas", "-v",
+           "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-I", CSRC,
+           "-I", os.path.join(ROOT, "include")]
+CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+            "-I", CSRC]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str], log: str | None = None) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if log:
+        with open(log, "w") as f:
+            f.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ...")
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "equil_b200.h")]
+    objs = []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src + ".o")
+        if force or _stale(o, [s, *hdrs]):
+            if verbose:
+                print("nvcc", src, flush=True)
+            _run([NVCC, *ARCH, *NVFLAGS, "-c", s, "-o", o], log=o + ".ptxas.log")
+        objs.append(o)
+    for src in CXX_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src + ".o")
+        if force or _stale(o, [s, *hdrs]):
+            if verbose:
+                print("g++", src, flush=True)
+            _run(["g++", *CXXFLAGS, "-c", s, "-o", o])
+        objs.append(o)
+    if force or _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lpthread"])
+    gsrc = os.path.join(CSRC, "gen.cpp")
+    if force or _stale(GEN_LIB, [gsrc]):
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", gsrc, "-o", GEN_LIB])
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

@@ -1,0 +1,1278 @@
+// engine.cu -- host engine and C ABI (include/equil_b200.h).
+//
+// Owns the device-resident matrix (CSR(A), CSR(A^T) shards or dense A), the
+// traversal plans, the sign stream and the SGD / LSQR drivers.  The T-iteration
+// SGD loop is captured once as a CUDA graph per (T, targets, gamma, M) and
+// replayed; LSQR keeps its scalar recurrence on the host (std::hypot, exactly
+// as src/lsqr.cpp:58-64) with one device->host round trip per iteration.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/equil_b200.h"
+#include "internal.h"
+#include "mt64_host.h"
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (the process that drives us -- e.g. torch -- has
+// usually loaded libnccl.so.2 already; dlopen then returns that copy).
+// ---------------------------------------------------------------------------
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int ncclUint8 = 1, ncclUint32 = 3, ncclFloat64 = 8, ncclMax = 2;
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
+             api.AllReduce;
+  });
+  return api;
+}
+
+thread_local std::string g_err;
+
+struct Fail {
+  equil_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(equil_status c, const std::string& m) { throw Fail{c, m}; }
+void require(bool c, const std::string& m) {
+  if (!c) fail(EQUIL_EINVAL, m);
+}
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? EQUIL_ENOMEM : EQUIL_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) cuda_check((x), #x)
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != 0) {
+    const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
+    fail(EQUIL_ENCCL, std::string(what) + ": " + s);
+  }
+}
+
+template <class F>
+equil_status guarded(F&& f) {
+  try {
+    f();
+    return EQUIL_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return EQUIL_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return EQUIL_ERUNTIME;
+  }
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n || !p) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---- params (src/params.cpp:7-44) -----------------------------------------
+void resolve_targets(const equil_params& p, int64_t rows, int64_t cols,
+                     double& alpha, double& beta) {
+  require(rows > 0 && cols > 0, "resolve_targets: dimensions must be positive");
+  require(p.alpha >= 0.0 && p.beta >= 0.0,
+          "resolve_targets: targets must be positive (or 0 for auto)");
+  const double m = static_cast<double>(rows);
+  const double n = static_cast<double>(cols);
+  alpha = p.alpha;
+  beta = p.beta;
+  if (alpha == 0.0 && beta == 0.0) {
+    alpha = std::pow(n / m, 0.25);
+    beta = std::pow(m / n, 0.25);
+  } else if (beta == 0.0) {
+    beta = alpha * std::sqrt(m / n);
+  } else if (alpha == 0.0) {
+    alpha = beta * std::sqrt(n / m);
+  } else {
+    const double lhs = m * alpha * alpha;
+    const double rhs = n * beta * beta;
+    require(std::abs(lhs - rhs) <= 1e-8 * std::max(lhs, rhs),
+            "resolve_targets: m*alpha^2 == n*beta^2 violated");
+  }
+}
+
+void validate_params(const equil_params& p) {
+  require(p.gamma > 0.0, "params: gamma must be positive");
+  require(p.max_log_scale > 0.0, "params: max_log_scale must be positive");
+  require(p.iterations >= 0, "params: iterations must be nonnegative");
+  require(std::isfinite(p.gamma) && std::isfinite(p.max_log_scale),
+          "params: gamma and max_log_scale must be finite");
+}
+
+// ---- traversal plan ---------------------------------------------------------
+constexpr int kMaxRowsPerTile = 2048;
+
+void plan_tiles(const std::vector<int64_t>& rp, int mat, std::vector<eqb::Tile>& lng,
+                std::vector<eqb::Tile>& packed) {
+  const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
+  int64_t i = 0;
+  std::vector<std::pair<int64_t, int64_t>> longs;
+  while (i < rows) {
+    const int64_t len = rp[i + 1] - rp[i];
+    if (len > eqb::kTileNnz) {
+      longs.push_back({len, i});
+      ++i;
+      continue;
+    }
+    const int64_t start = i;
+    int64_t acc = 0;
+    while (i < rows && i - start < kMaxRowsPerTile) {
+      const int64_t l = rp[i + 1] - rp[i];
+      if (l > eqb::kTileNnz || acc + l > eqb::kTileNnz) break;
+      acc += l;
+      ++i;
+    }
+    packed.push_back({static_cast<int32_t>(start), static_cast<int32_t>(i), 0,
+                      static_cast<int16_t>(mat), 0});
+  }
+  std::stable_sort(longs.begin(), longs.end(),
+                   [](auto& a, auto& b) { return a.first > b.first; });
+  for (auto& [len, r] : longs)
+    lng.push_back({static_cast<int32_t>(r), static_cast<int32_t>(r + 1), 1,
+                   static_cast<int16_t>(mat), 0});
+}
+
+std::vector<int64_t> partition_rows(const int64_t* rp, int64_t rows, int parts) {
+  // contiguous ranges balanced by (nnz + rows): boundary g at the first row
+  // whose prefix cost reaches g/parts of the total
+  std::vector<int64_t> b(parts + 1, rows);
+  b[0] = 0;
+  const double total = static_cast<double>(rp[rows] + rows);
+  int g = 1;
+  for (int64_t i = 0; i <= rows && g < parts; ++i) {
+    const double cost = static_cast<double>(rp[i] + i);
+    while (g < parts && cost >= total * g / parts) b[g++] = i;
+  }
+  while (g < parts) b[g++] = rows;
+  b[parts] = rows;
+  return b;
+}
+
+__global__ void remap_cols_kernel(int32_t* col, int64_t nnz, const int64_t* bounds,
+                                  int parts, int64_t maxcnt) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nnz) return;
+  const int64_t j = col[k];
+  int g = 0;
+  while (g + 1 < parts && bounds[g + 1] <= j) ++g;
+  col[k] = static_cast<int32_t>(g * maxcnt + (j - bounds[g]));
+}
+
+__global__ void rebase_rowptr_kernel(int64_t* dst, const int64_t* src, int64_t cnt,
+                                     int64_t base) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < cnt) dst[k] = src[k] - base;
+}
+
+__global__ void unpad_kernel(double* dst, const double* src, const int64_t* bounds,
+                             int parts, int64_t maxcnt, int64_t len) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= len) return;
+  int g = 0;
+  while (g + 1 < parts && bounds[g + 1] <= k) ++g;
+  dst[k] = src[g * maxcnt + (k - bounds[g])];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct equil_matrix {
+  int device = 0, rank = 0, world = 1;
+  bool dense = false;
+  int64_t m = 0, n = 0, nnz = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  ncclComm_t comm = nullptr;
+
+  // sparse shards (local rows, columns in padded coordinates)
+  eqb::DevCsr A, AT;
+  DevBuf<int64_t> a_rp, t_rp;
+  DevBuf<int32_t> a_ci, t_ci;
+  DevBuf<double> a_va, t_va;
+  std::vector<int64_t> a_bounds, t_bounds;  // partitions of rows / columns
+  int64_t a_max = 0, t_max = 0;             // padded slice sizes
+  DevBuf<int64_t> a_bounds_d, t_bounds_d;
+  DevBuf<eqb::Tile> tiles_sgd, tiles_a, tiles_t;
+  int n_sgd = 0, n_a = 0, n_t = 0;
+
+  // dense
+  DevBuf<double> Ad, colpart;
+
+  // workspaces
+  DevBuf<double> xs[2], xw[2];  // padded gathered vectors
+  DevBuf<double> u, ub, v, vb;  // local
+  DevBuf<uint32_t> signs;
+  DevBuf<unsigned char> sign_scratch;
+  DevBuf<unsigned> flags;
+  DevBuf<double> red_part;
+  DevBuf<unsigned> red_counter;
+  DevBuf<double> scal;  // small device scalars
+  DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
+
+  // graph cache for the SGD loop
+  cudaGraphExec_t graph = nullptr;
+  struct Key {
+    int T = -1;
+    double alpha = 0, beta = 0, gamma = 0, M = 0;
+    bool operator==(const Key& o) const {
+      return T == o.T && alpha == o.alpha && beta == o.beta && gamma == o.gamma && M == o.M;
+    }
+  } graph_key;
+
+  int64_t m_loc() const { return dense ? m : a_bounds[rank + 1] - a_bounds[rank]; }
+  int64_t n_loc() const { return dense ? n : t_bounds[rank + 1] - t_bounds[rank]; }
+  int64_t a_goff() const { return dense ? 0 : a_bounds[rank]; }
+  int64_t t_goff() const { return dense ? 0 : t_bounds[rank]; }
+  int64_t m_pad() const { return world == 1 ? m : a_max * world; }
+  int64_t n_pad() const { return world == 1 ? n : t_max * world; }
+
+  ~equil_matrix() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
+  M->device = cfg ? cfg->device : 0;
+  M->rank = cfg ? cfg->rank : 0;
+  M->world = cfg ? std::max(1, cfg->world_size) : 1;
+  require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  require(M->device >= 0 && M->device < ndev, "device cfg: no such CUDA device");
+  CK(cudaSetDevice(M->device));
+  CK(cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking));
+  if (M->world > 1) {
+    require(cfg->nccl_id != nullptr, "device cfg: world_size > 1 needs nccl_id");
+    if (!nccl().ok) fail(EQUIL_ENCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof id);
+    nccl_check(nccl().CommInitRank(&M->comm, M->world, id, M->rank), "ncclCommInitRank");
+  }
+  M->flags.alloc(1);
+  M->red_counter.alloc(1);
+  CK(cudaMemset(M->red_counter.p, 0, sizeof(unsigned)));
+  M->scal.alloc(64);
+  CK(cudaMemset(M->scal.p, 0, 64 * sizeof(double)));
+}
+
+void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
+  if (M->world == 1) return;
+  nccl_check(nccl().AllGather(buf + M->rank * maxcnt, buf, static_cast<size_t>(maxcnt),
+                              ncclFloat64, M->comm, M->stream),
+             "ncclAllGather");
+}
+
+// Build local shards from the full device CSR(A) and CSR(A^T).
+void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
+                  const std::vector<int64_t>& rpA_host,
+                  const std::vector<int64_t>& rpT_host) {
+  const int G = M->world, r = M->rank;
+  M->a_bounds = G == 1 ? std::vector<int64_t>{0, M->m}
+                       : partition_rows(rpA_host.data(), M->m, G);
+  M->t_bounds = G == 1 ? std::vector<int64_t>{0, M->n}
+                       : partition_rows(rpT_host.data(), M->n, G);
+  M->a_max = 0;
+  M->t_max = 0;
+  for (int g = 0; g < G; ++g) {
+    M->a_max = std::max(M->a_max, M->a_bounds[g + 1] - M->a_bounds[g]);
+    M->t_max = std::max(M->t_max, M->t_bounds[g + 1] - M->t_bounds[g]);
+  }
+  M->a_bounds_d.alloc(G + 1);
+  M->t_bounds_d.alloc(G + 1);
+  CK(cudaMemcpy(M->a_bounds_d.p, M->a_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(M->t_bounds_d.p, M->t_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+
+  auto take = [&](eqb::DevCsr& full, const std::vector<int64_t>& rph,
+                  const std::vector<int64_t>& bounds, const std::vector<int64_t>& colb,
+                  int64_t colmax, eqb::DevCsr& out, DevBuf<int64_t>& rp,
+                  DevBuf<int32_t>& ci, DevBuf<double>& va) {
+    const int64_t r0 = bounds[r], r1 = bounds[r + 1];
+    const int64_t k0 = rph[r0], k1 = rph[r1];
+    out.rows = r1 - r0;
+    out.cols = full.cols;
+    out.nnz = k1 - k0;
+    rp.alloc(out.rows + 1);
+    ci.alloc(out.nnz);
+    va.alloc(out.nnz);
+    rebase_rowptr_kernel<<<static_cast<unsigned>((out.rows + 1 + 255) / 256), 256, 0,
+                           M->stream>>>(rp.p, full.row_ptr + r0, out.rows + 1, k0);
+    CK(cudaGetLastError());
+    if (out.nnz) {
+      CK(cudaMemcpyAsync(ci.p, full.col + k0, out.nnz * 4, cudaMemcpyDeviceToDevice, M->stream));
+      CK(cudaMemcpyAsync(va.p, full.val + k0, out.nnz * 8, cudaMemcpyDeviceToDevice, M->stream));
+      if (G > 1) {
+        DevBuf<int64_t> cb;
+        cb.alloc(G + 1);
+        CK(cudaMemcpy(cb.p, colb.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+        remap_cols_kernel<<<static_cast<unsigned>((out.nnz + 255) / 256), 256, 0,
+                            M->stream>>>(ci.p, out.nnz, cb.p, G, colmax);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(M->stream));
+      }
+    }
+    out.row_ptr = rp.p;
+    out.col = ci.p;
+    out.val = va.p;
+  };
+  take(fullA, rpA_host, M->a_bounds, M->t_bounds, M->t_max, M->A, M->a_rp, M->a_ci, M->a_va);
+  take(fullT, rpT_host, M->t_bounds, M->a_bounds, M->a_max, M->AT, M->t_rp, M->t_ci, M->t_va);
+  CK(cudaStreamSynchronize(M->stream));
+
+  // traversal plans on the local shards
+  auto local_rp = [&](const std::vector<int64_t>& rph, const std::vector<int64_t>& b) {
+    std::vector<int64_t> out(rph.begin() + b[r], rph.begin() + b[r + 1] + 1);
+    const int64_t base = out[0];
+    for (auto& x : out) x -= base;
+    return out;
+  };
+  std::vector<eqb::Tile> la, pa, lt, pt;
+  plan_tiles(local_rp(rpA_host, M->a_bounds), 0, la, pa);
+  plan_tiles(local_rp(rpT_host, M->t_bounds), 1, lt, pt);
+  std::vector<eqb::Tile> sgd;
+  // long rows first (longest first), then packed tiles
+  std::vector<eqb::Tile> lng = la;
+  lng.insert(lng.end(), lt.begin(), lt.end());
+  auto lenof = [&](const eqb::Tile& t) {
+    const auto& rph = t.mat ? rpT_host : rpA_host;
+    const auto& b = t.mat ? M->t_bounds : M->a_bounds;
+    return rph[b[r] + t.r0 + 1] - rph[b[r] + t.r0];
+  };
+  std::stable_sort(lng.begin(), lng.end(),
+                   [&](const eqb::Tile& x, const eqb::Tile& y) { return lenof(x) > lenof(y); });
+  sgd = lng;
+  sgd.insert(sgd.end(), pa.begin(), pa.end());
+  sgd.insert(sgd.end(), pt.begin(), pt.end());
+  std::vector<eqb::Tile> ta = la, tt = lt;
+  ta.insert(ta.end(), pa.begin(), pa.end());
+  tt.insert(tt.end(), pt.begin(), pt.end());
+  auto upload = [&](DevBuf<eqb::Tile>& d, const std::vector<eqb::Tile>& h, int& cnt) {
+    d.alloc(h.size());
+    if (!h.empty())
+      CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(eqb::Tile), cudaMemcpyHostToDevice));
+    cnt = static_cast<int>(h.size());
+  };
+  upload(M->tiles_sgd, sgd, M->n_sgd);
+  upload(M->tiles_a, ta, M->n_a);
+  upload(M->tiles_t, tt, M->n_t);
+}
+
+void alloc_workspaces(equil_matrix* M) {
+  for (int b = 0; b < 2; ++b) {
+    M->xs[b].alloc(M->n_pad());
+    M->xw[b].alloc(M->m_pad());
+  }
+  M->u.alloc(M->m_loc());
+  M->ub.alloc(M->m_loc());
+  M->v.alloc(M->n_loc());
+  M->vb.alloc(M->n_loc());
+  const int64_t big = std::max(M->m_pad(), M->n_pad());
+  M->red_part.alloc((big + eqb::kChunk - 1) / eqb::kChunk + 1);
+  M->tmp_m.alloc(M->m_pad());
+  M->tmp_n.alloc(M->n_pad());
+  M->tmp_m2.alloc(M->m_pad());
+  M->tmp_n2.alloc(M->n_pad());
+  if (M->dense) M->colpart.alloc(((M->m + eqb::kChunk - 1) / eqb::kChunk) * M->n);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* equil_last_error(void) { return g_err.c_str(); }
+const char* equil_version(void) { return "equil_b200 0.1 (sm_100a)"; }
+
+void equil_params_default(equil_params* p) {
+  p->alpha = 0.0;
+  p->beta = 0.0;
+  p->gamma = 0.1;
+  p->max_log_scale = 9.210340371976184;
+  p->iterations = 1000;
+  p->seed = 0;
+}
+
+equil_status equil_resolve_targets(const equil_params* p, int64_t rows, int64_t cols,
+                                   double* alpha, double* beta) {
+  return guarded([&] {
+    require(p != nullptr, "resolve_targets: null params");
+    resolve_targets(*p, rows, cols, *alpha, *beta);
+  });
+}
+
+equil_status equil_validate_params(const equil_params* p) {
+  return guarded([&] {
+    require(p != nullptr, "validate_params: null params");
+    validate_params(*p);
+  });
+}
+
+double equil_det_exp_host(double x) { return eqb::det_exp(x); }
+
+equil_status equil_partition_rows(const int64_t* row_ptr, int64_t rows, int parts,
+                                  int64_t* bounds) {
+  return guarded([&] {
+    require(parts > 0 && rows >= 0, "partition_rows: bad arguments");
+    const auto b = partition_rows(row_ptr, rows, parts);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+equil_status equil_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    if (!nccl().ok) fail(EQUIL_ENCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                                     const int32_t* col, const double* val,
+                                     const equil_device_cfg* cfg, equil_matrix** out) {
+  return guarded([&] {
+    require(out != nullptr, "ExplicitMatrix::sparse: null output handle");
+    *out = nullptr;
+    require(m > 0 && n > 0, "ExplicitMatrix::sparse: dimensions must be positive");
+    require(row_ptr != nullptr, "ExplicitMatrix::sparse: null row_ptr");
+    require(n < (1LL << 31) && m < (1LL << 31), "ExplicitMatrix::sparse: dimension too large");
+    const int64_t nnz = row_ptr[m];
+    require(nnz >= 0 && nnz < (1LL << 31), "ExplicitMatrix::sparse: bad nnz");
+    require(nnz == 0 || (col && val), "ExplicitMatrix::sparse: null col/val");
+    auto M = std::make_unique<equil_matrix>();
+    setup_common(M.get(), cfg);
+    M->m = m;
+    M->n = n;
+    M->nnz = nnz;
+    DeviceGuard dg(M->device);
+    cudaStream_t s = M->stream;
+    // full A on device (uploaded once; shards are sliced from it)
+    DevBuf<int64_t> rp;
+    DevBuf<int32_t> ci;
+    DevBuf<double> va;
+    rp.alloc(m + 1);
+    ci.alloc(nnz);
+    va.alloc(nnz);
+    CK(cudaMemcpyAsync(rp.p, row_ptr, (m + 1) * 8, cudaMemcpyHostToDevice, s));
+    if (nnz) {
+      CK(cudaMemcpyAsync(ci.p, col, nnz * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(va.p, val, nnz * 8, cudaMemcpyHostToDevice, s));
+    }
+    eqb::DevCsr fullA{m, n, nnz, rp.p, ci.p, va.p};
+    // validation (explicit_matrix.cpp:21-39 for canonical CSR)
+    DevBuf<int64_t> where;
+    where.alloc(2);
+    CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(where.p, 0, 16, s));
+    CK(eqb::launch_validate_csr(fullA, reinterpret_cast<int*>(M->flags.p), where.p, s));
+    int errc = 0;
+    int64_t wh = 0;
+    CK(cudaMemcpyAsync(&errc, M->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&wh, where.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (errc) {
+      if (errc == 1) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: malformed row_ptr at row " + std::to_string(wh));
+      // locate the row of entry wh on the host
+      const int64_t k = wh;
+      const int64_t i = std::upper_bound(row_ptr, row_ptr + m + 1, k) - row_ptr - 1;
+      const std::string at = "(" + std::to_string(i) + ", " + std::to_string(col[k]) + ")";
+      if (errc == 2) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry " + at + " out of range");
+      if (errc == 3) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry " + at);
+      fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: columns not ascending at entry " + at +
+                             " (canonical CSR required)");
+    }
+    // K2: CSR(A^T) on device
+    DevBuf<int64_t> trp;
+    DevBuf<int32_t> tci;
+    DevBuf<double> tva;
+    trp.alloc(n + 1);
+    tci.alloc(nnz);
+    tva.alloc(nnz);
+    eqb::DevCsr fullT{n, m, nnz, trp.p, tci.p, tva.p};
+    CK(eqb::transpose_csr(fullA, fullT, s));
+    std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1), rpT(n + 1);
+    CK(cudaMemcpyAsync(rpT.data(), trp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (M->world == 1) {
+      // adopt the full arrays as the shard (no copy)
+      M->a_bounds = {0, m};
+      M->t_bounds = {0, n};
+      M->a_max = m;
+      M->t_max = n;
+      std::swap(M->a_rp.p, rp.p); std::swap(M->a_rp.n, rp.n);
+      std::swap(M->a_ci.p, ci.p); std::swap(M->a_ci.n, ci.n);
+      std::swap(M->a_va.p, va.p); std::swap(M->a_va.n, va.n);
+      std::swap(M->t_rp.p, trp.p); std::swap(M->t_rp.n, trp.n);
+      std::swap(M->t_ci.p, tci.p); std::swap(M->t_ci.n, tci.n);
+      std::swap(M->t_va.p, tva.p); std::swap(M->t_va.n, tva.n);
+      M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
+      M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
+      std::vector<eqb::Tile> la, pa, lt, pt;
+      plan_tiles(rpA, 0, la, pa);
+      plan_tiles(rpT, 1, lt, pt);
+      std::vector<eqb::Tile> lng = la;
+      lng.insert(lng.end(), lt.begin(), lt.end());
+      auto lenof = [&](const eqb::Tile& t) {
+        const auto& rph = t.mat ? rpT : rpA;
+        return rph[t.r0 + 1] - rph[t.r0];
+      };
+      std::stable_sort(lng.begin(), lng.end(), [&](const eqb::Tile& x, const eqb::Tile& y) {
+        return lenof(x) > lenof(y);
+      });
+      std::vector<eqb::Tile> sgd = lng;
+      sgd.insert(sgd.end(), pa.begin(), pa.end());
+      sgd.insert(sgd.end(), pt.begin(), pt.end());
+      std::vector<eqb::Tile> ta = la, tt = lt;
+      ta.insert(ta.end(), pa.begin(), pa.end());
+      tt.insert(tt.end(), pt.begin(), pt.end());
+      auto upload = [&](DevBuf<eqb::Tile>& d, const std::vector<eqb::Tile>& h, int& cnt) {
+        d.alloc(h.size());
+        if (!h.empty())
+          CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(eqb::Tile), cudaMemcpyHostToDevice));
+        cnt = static_cast<int>(h.size());
+      };
+      upload(M->tiles_sgd, sgd, M->n_sgd);
+      upload(M->tiles_a, ta, M->n_a);
+      upload(M->tiles_t, tt, M->n_t);
+    } else {
+      shard_sparse(M.get(), fullA, fullT, rpA, rpT);
+    }
+    alloc_workspaces(M.get());
+    CK(cudaStreamSynchronize(s));
+    *out = M.release();
+  });
+}
+
+equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowmajor,
+                                       const equil_device_cfg* cfg, equil_matrix** out) {
+  return guarded([&] {
+    require(out != nullptr, "ExplicitMatrix::dense: null output handle");
+    *out = nullptr;
+    require(m > 0 && n > 0, "ExplicitMatrix::dense: dimensions must be positive");
+    require(rowmajor != nullptr, "ExplicitMatrix::dense: null data");
+    require(cfg == nullptr || cfg->world_size <= 1,
+            "ExplicitMatrix::dense: the dense path runs on one GPU");
+    require(n <= static_cast<int64_t>(eqb::kChunk) * 4096, "dense: n too large");
+    require((m + eqb::kChunk - 1) / eqb::kChunk <= 64, "dense: m too large (<= 131072)");
+    auto M = std::make_unique<equil_matrix>();
+    setup_common(M.get(), cfg);
+    M->dense = true;
+    M->m = m;
+    M->n = n;
+    M->nnz = m * n;
+    DeviceGuard dg(M->device);
+    M->Ad.alloc(m * n);
+    CK(cudaMemcpyAsync(M->Ad.p, rowmajor, m * n * 8, cudaMemcpyHostToDevice, M->stream));
+    M->a_bounds = {0, m};
+    M->t_bounds = {0, n};
+    alloc_workspaces(M.get());
+    CK(cudaStreamSynchronize(M->stream));
+    *out = M.release();
+  });
+}
+
+void equil_matrix_destroy(equil_matrix* A) {
+  if (!A) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(A->device);
+  cudaStreamSynchronize(A->stream);
+  delete A;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+void* equil_matrix_stream(equil_matrix* A) {
+  return A ? static_cast<void*>(A->stream) : nullptr;
+}
+
+equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
+                                int64_t* nnz) {
+  return guarded([&] {
+    require(A != nullptr, "matrix: null handle");
+    if (m) *m = A->m;
+    if (n) *n = A->n;
+    if (nnz) *nnz = A->nnz;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// SGD driver
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DiagPlan {
+  int stride = 0;
+  bool obj = false, rms = false;
+};
+
+// canonical reduction of x[0, len) into *out (device): kind 0 sum of squares,
+// 1 plain sum, 2 sum of coef * x; optional sqrt of the result
+void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, int kind,
+                  double coef = 0.0, bool sqrt_out = false) {
+  CK(eqb::launch_canon_reduce(x, len, kind, coef, M->red_part.p, M->red_counter.p, out,
+                              sqrt_out ? 1 : 0, M->stream));
+}
+
+}  // namespace
+
+extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_params* p,
+                                              const equil_diag_cfg* diag,
+                                              equil_scaling_out* out) {
+  return guarded([&] {
+    require(M != nullptr && p != nullptr && out != nullptr, "sgd_equilibrate: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    double alpha = 0, beta = 0;
+    resolve_targets(*p, M->m, M->n, alpha, beta);  // src/equilibrate.cpp:216
+    validate_params(*p);                            // :142
+    DiagPlan dp;
+    if (diag && diag->stride > 0) {
+      dp.stride = diag->stride;
+      dp.obj = diag->want_objective != 0;
+      dp.rms = diag->want_rms != 0;
+      require(M->world == 1, "sgd_equilibrate: history is single-GPU in this build");
+      require(!M->dense, "sgd_equilibrate: history is implemented for sparse matrices");
+      require(out->hist_cap >= p->iterations / dp.stride + 1,
+              "sgd_equilibrate: history capacity too small");
+    } else if (diag && diag->stride < 0) {
+      fail(EQUIL_EINVAL, "sgd_row_col: stride must be positive");
+    }
+    cudaStream_t s = M->stream;
+    const int T = p->iterations;
+    const int64_t m = M->m, n = M->n;
+    const uint64_t per_iter = static_cast<uint64_t>(m + n);
+    const uint64_t total = per_iter * static_cast<uint64_t>(T);
+    const double lin_u = alpha * alpha, lin_v = beta * beta;
+    const double gamma = p->gamma, Mx = p->max_log_scale;
+    auto block_const = [&](double lin) {
+      eqb::SgdBlockConst c;
+      c.lin = lin;
+      c.gamma = gamma;
+      c.M = Mx;
+      const double cap = lin / gamma;
+      c.thresh = cap + 1e-9 * std::max(1.0, std::abs(cap));
+      return c;
+    };
+    const eqb::SgdBlockConst cu = block_const(lin_u), cv = block_const(lin_v);
+
+    // K1: all T*(n+m) signs up front (never depends on the iterate)
+    if (total > 0) {
+      M->signs.ensure((total + 31) / 32 + 1);
+      const size_t sb = eqb::sign_stream_scratch_bytes(total);
+      M->sign_scratch.ensure(sb);
+      CK(eqb::sign_stream_generate(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb, s));
+    }
+    // init: u = v = 0, ubar = vbar = 0, xs = s_1, xw = w_1
+    CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
+    const int64_t a_poff = M->world == 1 ? M->a_goff() : M->rank * M->a_max;
+    const int64_t t_poff = M->world == 1 ? M->t_goff() : M->rank * M->t_max;
+    if (T > 0) {
+      CK(eqb::launch_sgd_init(M->xs[0].p, M->xw[0].p, M->u.p, M->ub.p, M->v.p, M->vb.p,
+                              M->n_pad(), M->m_pad(), M->signs.p, M->m_loc(), M->n_loc(),
+                              M->a_goff(), M->t_goff(), a_poff, t_poff, m, n, s));
+      allgather_padded(M, M->xs[0].p, M->t_max);
+      allgather_padded(M, M->xw[0].p, M->a_max);
+    } else {
+      CK(cudaMemsetAsync(M->ub.p, 0, M->m_loc() * 8, s));
+      CK(cudaMemsetAsync(M->vb.p, 0, M->n_loc() * 8, s));
+    }
+
+    // history (src/equilibrate.cpp:174-195) into device slots, read at the end:
+    // per record [rms_acc, quad, lin_u.u, lin_v.v, |u|^2, |v|^2]
+    constexpr int kRec = 6;
+    const int nrec = dp.stride ? T / dp.stride + 1 : 0;
+    DevBuf<double> hist, terms;
+    if (nrec) {
+      hist.alloc(kRec * nrec);
+      CK(cudaMemsetAsync(hist.p, 0, kRec * nrec * 8, s));
+      terms.alloc(m + n);
+    }
+    int rec = 0;
+    auto record = [&](int) {
+      double* slot = hist.p + kRec * rec;
+      if (dp.rms) {  // rms_error (src/metrics.cpp:41-56)
+        double* eu = M->tmp_m.p;
+        double* ev = M->tmp_n.p;
+        CK(eqb::launch_exp(M->ub.p, eu, m, 2.0, s));
+        CK(eqb::launch_exp(M->vb.p, ev, n, 2.0, s));
+        CK(eqb::launch_rms_terms(0, M->A, eu, ev, terms.p, 0, alpha, s));
+        CK(eqb::launch_rms_terms(1, M->AT, eu, ev, terms.p + m, 0, beta, s));
+        canon_reduce(M, terms.p, m + n, slot + 0, 1);
+      }
+      if (dp.obj) {  // objective_weighted (src/equilibrate.cpp:10-22)
+        CK(eqb::launch_obj_terms(M->A, M->ub.p, M->vb.p, terms.p, s));
+        canon_reduce(M, terms.p, m, slot + 1, 1);
+        canon_reduce(M, M->ub.p, m, slot + 2, 2, lin_u);
+        canon_reduce(M, M->vb.p, n, slot + 3, 2, lin_v);
+        canon_reduce(M, M->ub.p, m, slot + 4, 0);
+        canon_reduce(M, M->vb.p, n, slot + 5, 0);
+      }
+      ++rec;
+    };
+    if (dp.stride) record(0);
+
+    auto host_step = [&](int t) {
+      eqb::SgdStep st;
+      st.step = 2.0 / (gamma * static_cast<double>(t + 1));  // :106
+      st.aw = 2.0 / (static_cast<double>(t) + 2.0);           // :107
+      st.aw1 = 1.0 - st.aw;
+      st.pad = 0;
+      return st;
+    };
+    auto iter_args = [&](int t) {
+      eqb::SgdIterArgs a{};
+      for (int k = 0; k < 2; ++k) {
+        const eqb::DevCsr& C = k ? M->AT : M->A;
+        a.rp[k] = C.row_ptr;
+        a.ci[k] = C.col;
+        a.va[k] = C.val;
+      }
+      a.tiles = M->tiles_sgd.p;
+      a.xs_cur = M->xs[(t - 1) & 1].p;
+      a.xw_cur = M->xw[(t - 1) & 1].p;
+      a.xs_next = M->xs[t & 1].p;
+      a.xw_next = M->xw[t & 1].p;
+      a.x[0] = M->u.p;
+      a.x[1] = M->v.p;
+      a.avg[0] = M->ub.p;
+      a.avg[1] = M->vb.p;
+      a.goff[0] = M->a_goff();
+      a.goff[1] = M->t_goff();
+      a.poff[0] = a_poff;
+      a.poff[1] = t_poff;
+      a.signs = M->signs.p;
+      a.sign_next[0] = static_cast<int64_t>(t) * (m + n) + n + M->a_goff();
+      a.sign_next[1] = static_cast<int64_t>(t) * (m + n) + M->t_goff();
+      a.has_next = t < T;
+      a.c[0] = cu;
+      a.c[1] = cv;
+      a.st = host_step(t);
+      a.flags = M->flags.p;
+      return a;
+    };
+    auto dense_args = [&](int t) {
+      eqb::DenseIterArgs a{};
+      a.A = M->Ad.p;
+      a.m = m;
+      a.n = n;
+      a.xs_cur = M->xs[(t - 1) & 1].p;
+      a.xw_cur = M->xw[(t - 1) & 1].p;
+      a.xs_next = M->xs[t & 1].p;
+      a.xw_next = M->xw[t & 1].p;
+      a.u = M->u.p;
+      a.ub = M->ub.p;
+      a.v = M->v.p;
+      a.vb = M->vb.p;
+      a.signs = M->signs.p;
+      a.sign_next_w = static_cast<int64_t>(t) * (m + n) + n;
+      a.sign_next_s = static_cast<int64_t>(t) * (m + n);
+      a.has_next = t < T;
+      a.cu = cu;
+      a.cv = cv;
+      a.st = host_step(t);
+      a.flags = M->flags.p;
+      a.colpart = M->colpart.p;
+      return a;
+    };
+    auto one_iter = [&](int t) {
+      if (M->dense) {
+        CK(eqb::launch_dense_sgd_iter(dense_args(t), s));
+      } else {
+        CK(eqb::launch_sgd_iter(iter_args(t), M->n_sgd, s));
+        if (t < T) {
+          allgather_padded(M, M->xs[t & 1].p, M->t_max);
+          allgather_padded(M, M->xw[t & 1].p, M->a_max);
+        }
+      }
+    };
+
+    if (dp.stride == 0 && T > 0) {
+      // capture the whole T loop once per (T, targets, gamma, M) and replay it
+      equil_matrix::Key key{T, alpha, beta, gamma, Mx};
+      if (!M->graph || !(M->graph_key == key)) {
+        if (M->graph) {
+          cudaGraphExecDestroy(M->graph);
+          M->graph = nullptr;
+        }
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+          for (int t = 1; t <= T; ++t) one_iter(t);
+        } catch (...) {
+          cudaStreamEndCapture(s, &g);
+          throw;
+        }
+        CK(cudaStreamEndCapture(s, &g));
+        CK(cudaGraphInstantiate(&M->graph, g, 0));
+        cudaGraphDestroy(g);
+        M->graph_key = key;
+      }
+      CK(cudaGraphLaunch(M->graph, s));
+    } else {
+      for (int t = 1; t <= T; ++t) {
+        one_iter(t);
+        if (dp.stride && t % dp.stride == 0) record(t);
+      }
+    }
+
+    // finalize: u = ubar, v = vbar, d = exp(ubar), e = exp(vbar) (:201-204)
+    const int64_t ml = M->m_loc(), nl = M->n_loc();
+    double* dloc = M->tmp_m.p;
+    double* eloc = M->tmp_n.p;
+    CK(eqb::launch_exp(M->ub.p, dloc, ml, 1.0, s));
+    CK(eqb::launch_exp(M->vb.p, eloc, nl, 1.0, s));
+    unsigned flags = 0;
+    if (M->world > 1) {
+      nccl_check(nccl().AllReduce(M->flags.p, M->flags.p, 1, ncclUint32, ncclMax, M->comm, s),
+                 "ncclAllReduce");
+    }
+    CK(cudaMemcpyAsync(&flags, M->flags.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    const cudaMemcpyKind kind =
+        out->outputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (M->world == 1) {
+      if (out->u) CK(cudaMemcpyAsync(out->u, M->ub.p, ml * 8, kind, s));
+      if (out->v) CK(cudaMemcpyAsync(out->v, M->vb.p, nl * 8, kind, s));
+      if (out->d) CK(cudaMemcpyAsync(out->d, dloc, ml * 8, kind, s));
+      if (out->e) CK(cudaMemcpyAsync(out->e, eloc, nl * 8, kind, s));
+    } else {
+      // gather the four vectors in padded coordinates, then un-pad
+      auto gather_out = [&](const double* loc, int64_t cnt, int64_t maxcnt, int64_t full,
+                            const DevBuf<int64_t>& bd, double* dst) {
+        DevBuf<double> pad, flat;
+        pad.alloc(maxcnt * M->world);
+        flat.alloc(full);
+        CK(cudaMemcpyAsync(pad.p + M->rank * maxcnt, loc, cnt * 8, cudaMemcpyDeviceToDevice, s));
+        allgather_padded(M, pad.p, maxcnt);
+        unpad_kernel<<<static_cast<unsigned>((full + 255) / 256), 256, 0, s>>>(
+            flat.p, pad.p, bd.p, M->world, maxcnt, full);
+        CK(cudaGetLastError());
+        if (dst) CK(cudaMemcpyAsync(dst, flat.p, full * 8, kind, s));
+        CK(cudaStreamSynchronize(s));
+      };
+      gather_out(M->ub.p, ml, M->a_max, m, M->a_bounds_d, out->u);
+      gather_out(M->vb.p, nl, M->t_max, n, M->t_bounds_d, out->v);
+      gather_out(dloc, ml, M->a_max, m, M->a_bounds_d, out->d);
+      gather_out(eloc, nl, M->t_max, n, M->t_bounds_d, out->e);
+    }
+    std::vector<double> hh(kRec * static_cast<size_t>(std::max(nrec, 1)));
+    if (nrec)
+      CK(cudaMemcpyAsync(hh.data(), hist.p, kRec * nrec * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out->alpha = alpha;
+    out->beta = beta;
+    out->iterate_bound_ok = (flags & 1u) ? 0 : 1;
+    out->box_feasible = (flags & 2u) ? 0 : 1;
+    out->apply_count = T;
+    out->adjoint_count = T;
+    out->hist_len = nrec;
+    for (int h = 0; h < nrec; ++h) {
+      const double* r = hh.data() + kRec * h;
+      if (out->hist_iter) out->hist_iter[h] = h * dp.stride;
+      if (out->hist_objective)
+        out->hist_objective[h] =
+            dp.obj ? 0.5 * r[1] - r[2] - r[3] + 0.5 * gamma * (r[4] + r[5]) : 0.0;
+      if (out->hist_rms)
+        out->hist_rms[h] = dp.rms ? std::sqrt(r[0] / static_cast<double>(m + n)) : 0.0;
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// LSQR (src/lsqr.cpp:17-138).  Device vectors, canonical norms, host scalar
+// recurrence with std::hypot.
+// ---------------------------------------------------------------------------
+namespace {
+
+// one matvec pass of B (scaled by scale when non-null) in the given mode
+void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
+                const double* scale, const double* prev, const double* coef) {
+  if (M->dense) {
+    eqb::DensePassArgs a{};
+    a.A = M->Ad.p;
+    a.m = M->m;
+    a.n = M->n;
+    a.adjoint = adjoint ? 1 : 0;
+    a.xg = xg;
+    a.out = out;
+    a.scale = scale;
+    a.prev = prev;
+    a.coef = coef;
+    a.mode = mode;
+    a.colpart = M->colpart.p;
+    CK(eqb::launch_dense_pass(a, M->stream));
+    return;
+  }
+  eqb::PassArgs a{};
+  const eqb::DevCsr& C = adjoint ? M->AT : M->A;
+  a.rp = C.row_ptr;
+  a.ci = C.col;
+  a.va = C.val;
+  a.tiles = adjoint ? M->tiles_t.p : M->tiles_a.p;
+  a.xg = xg;
+  a.out = out;
+  a.scale = scale;
+  a.prev = prev;
+  a.coef = coef;
+  a.mode = mode;
+  CK(eqb::launch_pass(a, adjoint ? M->n_t : M->n_a, M->stream));
+}
+
+double read_scalar(equil_matrix* M, const double* dev) {
+  double h = 0;
+  CK(cudaMemcpyAsync(&h, dev, 8, cudaMemcpyDeviceToHost, M->stream));
+  CK(cudaStreamSynchronize(M->stream));
+  return h;
+}
+
+struct LsqrState {
+  int hist_len = 0;
+  int iterations = 0;
+  bool reached_tol = false, breakdown = false;
+  long long applies = 0, adjoints = 0;
+};
+
+// lsqr_core (:17-81) on B = diag(d) A diag(e) (d, e device or null) with rhs c
+void lsqr_core(equil_matrix* M, const double* c, const double* b_d, double bnorm,
+               const double* d, const double* e, int max_iters, double tol,
+               double* hist, int hist_cap, LsqrState& st, DevBuf<double>& x) {
+  cudaStream_t s = M->stream;
+  const int64_t m = M->m, n = M->n;
+  DevBuf<double> u, un, v, vn, w, du, ev, ex, r;
+  u.alloc(m); un.alloc(m); du.alloc(m); r.alloc(m);
+  v.alloc(n); vn.alloc(n); w.alloc(n); ev.alloc(n); ex.alloc(n);
+  x.alloc(n);
+  CK(cudaMemsetAsync(x.p, 0, n * 8, s));
+  double* sc = M->scal.p;  // [0] beta, [1] alpha, [2] residual norm
+  int* dummy = reinterpret_cast<int*>(sc + 8);
+
+  canon_reduce(M, c, m, sc + 0, 0, 0.0, true);  // beta = |c|
+  CK(eqb::launch_lsqr_normalize(u.p, c, sc + 0, du.p, d, m, nullptr, nullptr, s));
+  apply_pass(M, true, du.p, v.p, eqb::kPassScaled, e, nullptr, nullptr);  // v = B^T u
+  ++st.adjoints;
+  canon_reduce(M, v.p, n, sc + 1, 0, 0.0, true);
+  double beta = read_scalar(M, sc + 0);
+  double alpha = read_scalar(M, sc + 1);
+  if (alpha == 0.0) {
+    st.breakdown = true;
+    return;
+  }
+  CK(eqb::launch_lsqr_normalize(v.p, v.p, sc + 1, ev.p, e, n, dummy, nullptr, s));
+  CK(cudaMemcpyAsync(w.p, v.p, n * 8, cudaMemcpyDeviceToDevice, s));
+  double phibar = beta, rhobar = alpha;
+
+  for (int t = 1; t <= max_iters; ++t) {
+    bool invariant = false;
+    apply_pass(M, false, ev.p, un.p, eqb::kPassLsqrU, d, u.p, sc + 1);  // Bv - alpha u
+    ++st.applies;
+    canon_reduce(M, un.p, m, sc + 0, 0, 0.0, true);
+    beta = read_scalar(M, sc + 0);
+    if (beta > 0.0) {
+      CK(eqb::launch_lsqr_normalize(u.p, un.p, sc + 0, du.p, d, m, nullptr, nullptr, s));
+    } else {
+      invariant = true;
+    }
+    alpha = 0.0;
+    if (!invariant) {
+      apply_pass(M, true, du.p, vn.p, eqb::kPassLsqrV, e, v.p, sc + 0);  // B^T u - beta v
+      ++st.adjoints;
+      canon_reduce(M, vn.p, n, sc + 1, 0, 0.0, true);
+      alpha = read_scalar(M, sc + 1);
+      if (alpha > 0.0) {
+        CK(eqb::launch_lsqr_normalize(v.p, vn.p, sc + 1, ev.p, e, n, nullptr, nullptr, s));
+      } else {
+        invariant = true;
+      }
+    }
+    const double rho = std::hypot(rhobar, beta);  // :58-64
+    const double cs = rhobar / rho;
+    const double sn = beta / rho;
+    const double theta = sn * alpha;
+    rhobar = -cs * alpha;
+    const double phi = cs * phibar;
+    phibar = sn * phibar;
+    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, ex.p, n, s));
+    st.iterations = t;
+    apply_pass(M, false, ex.p, r.p, eqb::kPassResid, nullptr, b_d, nullptr);
+    canon_reduce(M, r.p, m, sc + 2, 0, 0.0, true);
+    const double rel = read_scalar(M, sc + 2) / bnorm;
+    if (st.hist_len < hist_cap) hist[st.hist_len] = rel;
+    ++st.hist_len;
+    if (rel <= tol) {
+      st.reached_tol = true;
+      break;
+    }
+    if (invariant) {
+      st.breakdown = true;
+      break;
+    }
+  }
+}
+
+void lsqr_common(equil_matrix* M, const double* b, const equil_params* p, int max_iters,
+                 double tol, equil_lsqr_out* out, const char* who) {
+  require(M != nullptr && out != nullptr, std::string(who) + ": null argument");
+  require(b != nullptr, std::string(who) + ": rhs length mismatch");
+  std::lock_guard<std::mutex> lk(M->mu);
+  DeviceGuard dg(M->device);
+  require(M->world == 1, std::string(who) + ": multi-GPU LSQR is not in this build");
+  cudaStream_t s = M->stream;
+  const int64_t m = M->m, n = M->n;
+  DevBuf<double> b_d;
+  b_d.alloc(m);
+  CK(cudaMemcpyAsync(b_d.p, b, m * 8, cudaMemcpyHostToDevice, s));
+  canon_reduce(M, b_d.p, m, M->scal.p + 3, 0, 0.0, true);
+  const double bnorm = read_scalar(M, M->scal.p + 3);
+  require(bnorm > 0.0, std::string(who) + ": rhs must be nonzero");
+  require(max_iters >= 0, std::string(who) + ": max_iters must be nonnegative");
+  const int T = p ? p->iterations : 0;
+  require(out->residual_history != nullptr &&
+              out->residual_cap >= max_iters + 1 + (p ? std::max(T, 0) : 0),
+          std::string(who) + ": residual_history capacity too small");
+  LsqrState st;
+  DevBuf<double> dd, ed, c, x;
+  const double* c_ptr = b_d.p;
+  if (p) {
+    // sgd_equilibrate on the charged operator (:115-116), d, e kept on device
+    dd.alloc(m);
+    ed.alloc(n);
+    equil_scaling_out so{};
+    so.u = nullptr;
+    so.v = nullptr;
+    so.d = dd.p;
+    so.e = ed.p;
+    so.outputs_on_device = 1;
+    M->mu.unlock();
+    const equil_status rc = equil_sgd_equilibrate(M, p, nullptr, &so);
+    M->mu.lock();
+    if (rc != EQUIL_OK) fail(rc, g_err);
+    st.applies = so.apply_count;
+    st.adjoints = so.adjoint_count;
+    for (int t = 0; t <= T; ++t) out->residual_history[st.hist_len++] = 1.0;  // :121-123
+    c.alloc(m);
+    CK(eqb::launch_mul(c.p, dd.p, b_d.p, m, s));  // c = d .* b (:126)
+    c_ptr = c.p;
+  } else {
+    out->residual_history[st.hist_len++] = 1.0;  // :94
+  }
+  lsqr_core(M, c_ptr, b_d.p, bnorm, p ? dd.p : nullptr, p ? ed.p : nullptr, max_iters,
+            tol, out->residual_history, out->residual_cap, st, x);
+  // x = e .* x_scaled (:134)
+  if (p) CK(eqb::launch_mul(x.p, ed.p, x.p, n, s));
+  if (out->x) CK(cudaMemcpyAsync(out->x, x.p, n * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out->hist_len = st.hist_len;
+  out->iterations = st.iterations;
+  out->equil_iterations = p ? T : 0;
+  out->reached_tol = st.reached_tol;
+  out->breakdown = st.breakdown;
+  out->apply_count = st.applies;
+  out->adjoint_count = st.adjoints;
+}
+
+}  // namespace
+
+extern "C" {
+
+equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
+                        equil_lsqr_out* out) {
+  return guarded([&] { lsqr_common(A, b, nullptr, max_iters, tol, out, "lsqr"); });
+}
+
+equil_status equil_lsqr_preconditioned(equil_matrix* A, const double* b,
+                                       const equil_params* p, int max_iters, double tol,
+                                       equil_lsqr_out* out) {
+  return guarded([&] {
+    require(p != nullptr, "lsqr_preconditioned: null params");
+    lsqr_common(A, b, p, max_iters, tol, out, "lsqr_preconditioned");
+  });
+}
+
+equil_status equil_apply(equil_matrix* M, const double* x, double* y, int adjoint) {
+  return guarded([&] {
+    require(M != nullptr && x != nullptr && y != nullptr, "apply: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    require(M->world == 1, "apply: single-GPU matrices only");
+    const int64_t nin = adjoint ? M->m : M->n, nout = adjoint ? M->n : M->m;
+    DevBuf<double> xi, yo;
+    xi.alloc(nin);
+    yo.alloc(nout);
+    CK(cudaMemcpyAsync(xi.p, x, nin * 8, cudaMemcpyHostToDevice, M->stream));
+    apply_pass(M, adjoint != 0, xi.p, yo.p, eqb::kPassPlain, nullptr, nullptr, nullptr);
+    CK(cudaMemcpyAsync(y, yo.p, nout * 8, cudaMemcpyDeviceToHost, M->stream));
+    CK(cudaStreamSynchronize(M->stream));
+  });
+}
+
+equil_status equil_export_transpose(equil_matrix* M, int64_t* t_row_ptr, int32_t* t_col,
+                                    double* t_val) {
+  return guarded([&] {
+    require(M != nullptr, "export_transpose: null handle");
+    require(!M->dense && M->world == 1, "export_transpose: single-GPU sparse matrices only");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    CK(cudaMemcpy(t_row_ptr, M->AT.row_ptr, (M->n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (M->nnz) {
+      CK(cudaMemcpy(t_col, M->AT.col, M->nnz * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(t_val, M->AT.val, M->nnz * 8, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+equil_status equil_sign_bits(uint64_t seed, uint64_t stream, uint64_t start,
+                             uint64_t count, uint32_t* bits_out, int device) {
+  return guarded([&] {
+    require(bits_out != nullptr || count == 0, "sign_bits: null output");
+    if (count == 0) return;
+    DeviceGuard dg(device);
+    const uint64_t total = start + count;
+    DevBuf<uint32_t> bits;
+    DevBuf<unsigned char> scratch;
+    bits.alloc((total + 31) / 32 + 1);
+    const size_t sb = eqb::sign_stream_scratch_bytes(total);
+    scratch.alloc(sb);
+    CK(eqb::sign_stream_generate(seed, stream, total, bits.p, scratch.p, sb, 0));
+    std::vector<uint32_t> all((total + 31) / 32 + 1, 0);
+    CK(cudaMemcpy(all.data(), bits.p, ((total + 31) / 32) * 4, cudaMemcpyDeviceToHost));
+    const uint64_t nw = (count + 31) / 32;
+    for (uint64_t w = 0; w < nw; ++w) {
+      uint32_t word = 0;
+      for (int k = 0; k < 32; ++k) {
+        const uint64_t o = w * 32 + k;
+        if (o >= count) break;
+        const uint64_t g = start + o;
+        if ((all[g >> 5] >> (g & 31)) & 1u) word |= 1u << k;
+      }
+      bits_out[w] = word;
+    }
+  });
+}
+
+equil_status equil_det_exp_device(const double* x, double* y, int64_t n, int device) {
+  return guarded([&] {
+    if (n <= 0) return;
+    DeviceGuard dg(device);
+    DevBuf<double> a, b;
+    a.alloc(n);
+    b.alloc(n);
+    CK(cudaMemcpy(a.p, x, n * 8, cudaMemcpyHostToDevice));
+    CK(eqb::launch_exp(a.p, b.p, n, 1.0, 0));
+    CK(cudaMemcpy(y, b.p, n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+equil_status equil_canon_sumsq_device(const double* x, int64_t n, double* out, int device) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    DevBuf<double> a, part, res;
+    DevBuf<unsigned> cnt;
+    a.alloc(std::max<int64_t>(n, 1));
+    part.alloc((n + eqb::kChunk - 1) / eqb::kChunk + 1);
+    res.alloc(1);
+    cnt.alloc(1);
+    CK(cudaMemset(cnt.p, 0, 4));
+    if (n > 0) CK(cudaMemcpy(a.p, x, n * 8, cudaMemcpyHostToDevice));
+    CK(eqb::launch_canon_reduce(a.p, n, 0, 0.0, part.p, cnt.p, res.p, 0, 0));
+    CK(cudaMemcpy(out, res.p, 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                                       const int32_t* col, const double* val,
+                                       const equil_params* p, const equil_device_cfg* cfg,
+                                       equil_scaling_out* out) {
+  equil_matrix* M = nullptr;
+  equil_status rc = equil_matrix_create_csr(m, n, row_ptr, col, val, cfg, &M);
+  if (rc != EQUIL_OK) return rc;
+  rc = equil_sgd_equilibrate(M, p, nullptr, out);
+  equil_matrix_destroy(M);
+  return rc;
+}
+
+}  // extern "C"

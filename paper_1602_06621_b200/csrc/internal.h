@@ -1,0 +1,163 @@
+// internal.h -- shared declarations between the kernels and the host engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "det_math.cuh"
+
+namespace eqb {
+
+// Sparse traversal tile.  kind 0: rows [r0, r1) fully inside one tile
+// (nnz <= kTileNnz); kind 1: a single long row r0 streamed in kTileNnz chunks.
+// mat 0 = A (u block), mat 1 = A^T (v block).
+struct Tile {
+  int32_t r0, r1;
+  int16_t kind, mat;
+  int32_t pad;
+};
+constexpr int kTileNnz = 2048;
+constexpr int kTileThreads = 256;
+
+// CSR slice resident on the device (int64 row_ptr, int32 col, fp64 val).
+struct DevCsr {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int64_t* row_ptr = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+};
+
+struct SgdIterArgs {
+  const int64_t* rp[2];
+  const int32_t* ci[2];
+  const double* va[2];
+  const Tile* tiles;
+  const double* xs_cur;  // gathered e.*s (n, padded coords)
+  const double* xw_cur;  // gathered d.*w (m, padded coords)
+  double* xs_next;
+  double* xw_next;
+  double* x[2];    // u (local rows of A), v (local rows of A^T)
+  double* avg[2];  // ubar, vbar
+  int64_t goff[2];   // global index of local row 0 (A rows, A^T rows)
+  int64_t poff[2];   // padded index of local row 0 (into xw / xs)
+  const uint32_t* signs;  // packed sign bits
+  int64_t sign_next[2];   // bit index of (local row 0) for iteration t+1: w, s
+  int has_next;
+  SgdBlockConst c[2];
+  SgdStep st;
+  unsigned* flags;
+};
+
+enum PassMode : int {
+  kPassPlain = 0,    // y = acc
+  kPassLsqrU = 1,    // out = s_i*acc - alpha*u_i   (s = d or 1)
+  kPassLsqrV = 2,    // out = s_j*acc - beta*v_j    (s = e or 1)
+  kPassResid = 3,    // out = b_i - acc
+  kPassScaled = 4,   // out = s_i*acc (s = scale or 1)
+};
+
+struct PassArgs {
+  const int64_t* rp;
+  const int32_t* ci;
+  const double* va;
+  const Tile* tiles;
+  const double* xg;     // gathered vector (padded coords)
+  double* out;          // local rows
+  const double* scale;  // d or e (local rows) or nullptr
+  const double* prev;   // u or v (local rows), or b for kPassResid
+  const double* coef;   // device scalar (alpha or beta) or nullptr
+  const int* skip;      // device flag: when nonzero the pass is a no-op
+  int mode;
+};
+
+// LSQR device scalars
+struct LsqrDev {
+  double alpha, beta, rel;
+  double rnorm2;
+  int invariant;
+  int pad;
+};
+
+// -------------------- launchers (kernels.cu) ------------------------------
+cudaError_t launch_validate_csr(const DevCsr& A, int* err, int64_t* where,
+                                cudaStream_t s);
+cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s);
+cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
+                            double* v, double* vb, int64_t n_pad_len,
+                            int64_t m_pad_len, const uint32_t* signs,
+                            int64_t m_loc, int64_t n_loc, int64_t a_goff,
+                            int64_t at_goff, int64_t a_poff, int64_t at_poff,
+                            int64_t m_glob, int64_t n_glob, cudaStream_t s);
+cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s);
+cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
+                       cudaStream_t s);
+cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s);
+
+// canonical reduction (det_math.cuh) of terms x*x (kind 0), x (kind 1) or
+// coef*x (kind 2); *out (device) = result, or its sqrt when sqrt_out
+cudaError_t launch_canon_reduce(const double* x, int64_t len, int kind, double coef,
+                                double* partials, unsigned* counter, double* out,
+                                int sqrt_out, cudaStream_t s);
+
+// signs: MT19937-64 device generation
+cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
+                                 uint32_t* bits, void* scratch,
+                                 size_t scratch_bytes, cudaStream_t s);
+size_t sign_stream_scratch_bytes(uint64_t total);
+
+// dense
+struct DenseIterArgs {
+  const double* A;  // row-major m x n
+  int64_t m, n;
+  const double* xs_cur;
+  const double* xw_cur;
+  double* xs_next;
+  double* xw_next;
+  double* u;
+  double* ub;
+  double* v;
+  double* vb;
+  const uint32_t* signs;
+  int64_t sign_next_w, sign_next_s;
+  int has_next;
+  SgdBlockConst cu, cv;
+  SgdStep st;
+  unsigned* flags;
+  double* colpart;  // scratch: nchunks_m x n
+};
+cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s);
+struct DensePassArgs {
+  const double* A;
+  int64_t m, n;
+  int adjoint;
+  const double* xg;
+  double* out;
+  const double* scale;
+  const double* prev;
+  const double* coef;
+  const int* skip;
+  int mode;
+  double* colpart;
+};
+cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s);
+
+// LSQR elementwise helpers
+cudaError_t launch_lsqr_normalize(double* dst, const double* src,
+                                  const double* norm_dev, double* scaled_out,
+                                  const double* scale, int64_t len,
+                                  int* invariant, int* skip_in,
+                                  cudaStream_t s);
+cudaError_t launch_lsqr_xw_update(double* x, double* w, const double* v,
+                                  double c1, double c2, const double* e,
+                                  double* ex, int64_t n, cudaStream_t s);
+cudaError_t launch_rms_terms(int mat, const DevCsr& M, const double* eu,
+                             const double* ev, double* out, int64_t goff,
+                             double target, cudaStream_t s);
+
+cudaError_t launch_obj_terms(const DevCsr& A, const double* u, const double* v,
+                             double* out, cudaStream_t s);
+cudaError_t launch_mul(double* out, const double* a, const double* b, int64_t n,
+                       cudaStream_t s);
+
+}  // namespace eqb

@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors.  Bit-exact for signs, transpose and the whole
+SGD / LSQR trajectories (SURVEY.md §0 fact 4 explains why nothing weaker
+survives the chaotic recurrence); diagnostics to 1e-12 relative (no feedback,
+different summation order and exp)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1602_06621_b200 as eq
+from conftest import csr_from_golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["sp", "lr", "dn"]
+
+
+def device_matrix(A: oracle.CsrArrays):
+    if A.dense is not None:
+        return eq.ExplicitMatrix.dense(A.dense)
+    return eq.ExplicitMatrix.from_csr(A.m, A.n, A.row_ptr, A.col, A.val)
+
+
+def bits_of(raw, start, count):
+    return np.array([(int(raw[start + k]) >> 63) for k in range(count)], np.uint8)
+
+
+def unpack(words, count):
+    return np.array([(int(words[k >> 5]) >> (k & 31)) & 1 for k in range(count)], np.uint8)
+
+
+# ---------------------------------------------------------------- K1 signs
+def test_sign_stream_matches_reference_outputs(golden):
+    raw = golden["raw_0_17"]
+    for start, count in [(0, 20000), (1, 31), (312, 5000), (7777, 3333)]:
+        got = unpack(eq.sign_bits(0, 17, start, count), count)
+        assert np.array_equal(got, bits_of(raw, start, count)), (start, count)
+    raw1 = golden["raw_1_17"]
+    assert np.array_equal(unpack(eq.sign_bits(1, 17, 0, 20000), 20000), bits_of(raw1, 0, 20000))
+
+
+@pytest.mark.parametrize("seed,start,count", [(0, 1_000_000 - 5, 4096), (0, 3_000_000, 2048),
+                                              (7, 12_345_678, 1000), (99, 0, 2_000_000)])
+def test_sign_stream_far_positions_match_oracle(C, seed, start, count):
+    """jump-ahead (many segments, several levels) vs sequential generation"""
+    got = eq.sign_bits(seed, 17, start, count)
+    want = C.sign_bits(seed, 17, start, count)
+    assert np.array_equal(got, want)
+
+
+def test_sign_stream_survey_kats():
+    # output [1e6] of (0,17) has MSB 1 (+), [3e8] of (0,17) +, (1,17)[3e8] +
+    assert unpack(eq.sign_bits(0, 17, 1_000_000, 1), 1)[0] == 1
+    assert unpack(eq.sign_bits(0, 17, 3_000_000, 1), 1)[0] == 0
+    assert unpack(eq.sign_bits(0, 17, 10_000_000, 1), 1)[0] == 0
+
+
+# ---------------------------------------------------------------- K2 transpose
+@pytest.mark.parametrize("key", ["sp", "lr"])
+def test_transpose_bit_exact_vs_reference(golden, key):
+    A = csr_from_golden(golden, key)
+    M = device_matrix(A)
+    trp, tc, tv = M.transposed_csr()
+    assert np.array_equal(trp, golden[f"{key}_t_rp"])
+    assert np.array_equal(tc, golden[f"{key}_t_col"])
+    assert np.array_equal(tv.view(np.uint64), golden[f"{key}_t_val"].view(np.uint64))
+
+
+def test_transpose_bit_exact_config1(C):
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(1)
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    T = C.transpose(A)
+    trp, tc, tv = device_matrix(A).transposed_csr()
+    assert np.array_equal(trp, T.row_ptr) and np.array_equal(tc, T.col)
+    assert np.array_equal(tv.view(np.uint64), T.val.view(np.uint64))
+
+
+# ---------------------------------------------------------------- numerics contract
+def test_det_exp_device_equals_oracle(C):
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.uniform(-20, 20, 200_000), rng.standard_normal(50_000) * 1e-3,
+                        np.array([0.0, -0.0, 9.210340371976184, -9.210340371976184, 709.0,
+                                  -707.0, 1e-300, -1e-300])])
+    got = eq.det_exp_device(x)
+    want = C.det_exp(x)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("n", [0, 1, 255, 2048, 2049, 100_000, 2048 * 1024 + 17])
+def test_canonical_reduction_device_equals_oracle(C, n):
+    x = np.random.default_rng(n).standard_normal(n) * 3.0
+    assert eq.canon_sumsq_device(x) == C.canon_sumsq(x)
+
+
+# ---------------------------------------------------------------- apply / adjoint
+@pytest.mark.parametrize("key", CASES)
+def test_apply_and_adjoint_bit_exact(C, golden, key):
+    A = csr_from_golden(golden, key)
+    M = device_matrix(A)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(A.n)
+    y = rng.standard_normal(A.m)
+    assert np.array_equal(M.apply(x), C.apply(A, x))
+    assert np.array_equal(M.apply_adjoint(y), C.apply(A, y, adjoint=True))
+
+
+# ---------------------------------------------------------------- SGD trajectory
+@pytest.mark.parametrize("key", CASES)
+def test_sgd_bit_exact_vs_reference_golden(golden, key):
+    A = csr_from_golden(golden, key)
+    M = device_matrix(A)
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=40, seed=5))
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), golden[f"{key}_sgd_{k}"]), k
+    box, bound, ap, ad = golden[f"{key}_sgd_flags"]
+    assert (r.box_feasible, r.iterate_bound_ok, r.apply_count, r.adjoint_count) == \
+        (bool(box), bool(bound), ap, ad)
+
+
+def test_sgd_history_within_tolerance(golden):
+    A = csr_from_golden(golden, "sp")
+    M = device_matrix(A)
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=40, seed=5),
+                           eq.DiagnosticsConfig(stride=10))
+    assert [h.iter for h in r.history] == [0, 10, 20, 30, 40]
+    rms = np.array([h.rms for h in r.history])
+    obj = np.array([h.objective for h in r.history])
+    np.testing.assert_allclose(rms, golden["sp_sgd_hist_rms"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(obj, golden["sp_sgd_hist_obj"], rtol=1e-12, atol=0)
+    for k in "uvde":  # history must not perturb the trajectory
+        assert np.array_equal(getattr(r, k), golden[f"sp_sgd_{k}"])
+
+
+def test_sgd_config1_bit_exact_vs_oracle(C):
+    """BASELINE config 1 (10000x5000, 1%, T=50, seed 0, beta=1, alpha=sqrt(n/m))."""
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(1)
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    want = C.sgd_equilibrate(A, alpha=inst.alpha, beta=inst.beta, iterations=50, seed=0)
+    M = device_matrix(A)
+    p = eq.EquilibrationParams(alpha=inst.alpha, beta=inst.beta, iterations=50, seed=0)
+    got = eq.sgd_equilibrate(M, p)
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    # graph replay on the same handle is bit-identical (determinism, :229-245)
+    again = eq.sgd_equilibrate(M, p)
+    assert np.array_equal(again.d, got.d) and np.array_equal(again.e, got.e)
+    other = eq.sgd_equilibrate(M, eq.EquilibrationParams(alpha=inst.alpha, beta=inst.beta,
+                                                          iterations=50, seed=1))
+    assert not np.array_equal(other.u, got.u)
+
+
+def test_sgd_identity_fixed_point():
+    """test_equilibrate.cpp:183-198"""
+    M = eq.ExplicitMatrix.identity(5)
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(alpha=1.0, beta=1.0, iterations=50),
+                           eq.DiagnosticsConfig(stride=1))
+    assert np.all(r.u == 0) and np.all(r.v == 0) and np.all(r.d == 1) and np.all(r.e == 1)
+    assert all(abs(h.objective - 2.5) <= 2.5e-15 for h in r.history)
+    assert all(abs(h.rms) <= 1e-15 for h in r.history)
+
+
+def test_sgd_scalar_and_zero_known_answers(C):
+    """test_equilibrate.cpp:200-227 (1x1 [2]) and :302-331 (zero matrix)"""
+    one = oracle.CsrArrays(1, 1, dense=np.array([[2.0]]))
+    p = eq.EquilibrationParams(alpha=1.0, beta=1.0, gamma=0.1, max_log_scale=10.0,
+                               iterations=10000)
+    r = eq.sgd_equilibrate(eq.ExplicitMatrix.dense(one.dense), p)
+    w = C.sgd_equilibrate(one, alpha=1.0, beta=1.0, gamma=0.1, max_log_scale=10.0,
+                          iterations=10000)
+    assert np.array_equal(r.u, w.u) and np.array_equal(r.v, w.v)
+    assert r.box_feasible and r.iterate_bound_ok
+    z = eq.ExplicitMatrix.from_csr(1, 1, np.array([0, 1]), np.array([0]), np.array([0.0]))
+    r = eq.sgd_equilibrate(z, eq.EquilibrationParams(alpha=1.0, beta=1.0, iterations=57))
+    w = C.sgd_equilibrate(oracle.CsrArrays(1, 1, np.array([0, 1]), np.array([0]),
+                                           np.array([0.0])), alpha=1.0, beta=1.0,
+                          iterations=57)
+    assert np.array_equal(r.u, w.u)
+
+
+@pytest.mark.parametrize("T", [0, 1, 2])
+def test_sgd_tiny_budgets(C, golden, T):
+    A = csr_from_golden(golden, "sp")
+    r = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(iterations=T, seed=2))
+    w = C.sgd_equilibrate(A, iterations=T, seed=2)
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), getattr(w, k))
+    assert r.apply_count == T and r.adjoint_count == T
+
+
+def test_sgd_random_shapes_vs_oracle(C):
+    rng = np.random.default_rng(21)
+    for m, n, dens in [(1, 7, 0.9), (7, 1, 0.9), (513, 257, 0.02), (2, 3000, 0.8)]:
+        mask = rng.random((m, n)) < dens
+        a = rng.standard_normal((m, n)) * np.exp(2 * rng.standard_normal((m, 1)))
+        rp = np.concatenate([[0], np.cumsum(mask.sum(1))])
+        A = oracle.CsrArrays(m, n, rp, np.nonzero(mask)[1], a[mask])
+        p = dict(iterations=33, seed=int(rng.integers(1 << 30)))
+        w = C.sgd_equilibrate(A, **p)
+        r = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(**p))
+        for k in "uvde":
+            assert np.array_equal(getattr(r, k), getattr(w, k)), (m, n, k)
+        Ad = oracle.CsrArrays(m, n, dense=np.where(mask, a, 0.0))
+        w = C.sgd_equilibrate(Ad, **p)
+        r = eq.sgd_equilibrate(device_matrix(Ad), eq.EquilibrationParams(**p))
+        for k in "uvde":
+            assert np.array_equal(getattr(r, k), getattr(w, k)), ("dense", m, n, k)
+
+
+# ---------------------------------------------------------------- LSQR
+@pytest.mark.parametrize("key", CASES)
+def test_lsqr_bit_exact_vs_reference_golden(golden, key):
+    A = csr_from_golden(golden, key)
+    M = device_matrix(A)
+    b = golden[f"{key}_b"]
+    run = eq.lsqr(M, b, 30, 0.0)
+    assert np.array_equal(np.array(run.residual_history), golden[f"{key}_lsqr_res"])
+    assert np.array_equal(run.x, golden[f"{key}_lsqr_x"])
+    assert [run.iterations, run.reached_tol, run.breakdown, run.apply_count,
+            run.adjoint_count] == list(golden[f"{key}_lsqr_meta"])
+    pre = eq.lsqr_preconditioned(M, b, eq.EquilibrationParams(iterations=15, seed=3), 30, 0.0)
+    assert np.array_equal(np.array(pre.residual_history), golden[f"{key}_plsqr_res"])
+    assert np.array_equal(pre.x, golden[f"{key}_plsqr_x"])
+    assert [pre.iterations, pre.reached_tol, pre.breakdown, pre.apply_count,
+            pre.adjoint_count] == list(golden[f"{key}_plsqr_meta"])
+
+
+def test_lsqr_reference_cases():
+    """test_itersolvers.cpp:36-56, :88-121, :123-142"""
+    rng = np.random.default_rng(81)
+    b = rng.standard_normal(6)
+    run = eq.lsqr(eq.ExplicitMatrix.identity(6), b, 10, 1e-12)
+    assert run.reached_tol and run.iterations == 1 and len(run.residual_history) == 2
+    assert run.residual_history[0] == 1.0 and run.residual_history[1] <= 1e-12
+    assert np.linalg.norm(run.x - b) <= 1e-12 * np.linalg.norm(b)
+    D = np.diag(np.arange(1.0, 6.0))
+    run = eq.lsqr(eq.ExplicitMatrix.dense(D), D @ np.ones(5), 10, 1e-13)
+    assert run.reached_tol and run.iterations <= 5
+    assert np.abs(run.x - 1).max() <= 1e-10
+    with pytest.raises(eq.InvalidArgument):
+        eq.lsqr(eq.ExplicitMatrix.identity(3), np.zeros(3), 5, 1e-6)
+    A = np.zeros((2, 2)); A[0, 0] = 1.0
+    run = eq.lsqr(eq.ExplicitMatrix.dense(A), np.array([0.0, 1.0]), 20, 1e-10)
+    assert run.breakdown and not run.reached_tol and run.iterations == 0
+    assert np.linalg.norm(run.x) == 0 and run.residual_history == [1.0]
+    run = eq.lsqr(eq.ExplicitMatrix.dense(A), np.array([1.0, 1.0]), 20, 1e-10)
+    assert not run.reached_tol and abs(run.x[0] - 1) < 1e-12 and abs(run.x[1]) < 1e-12
+    assert run.residual_history[-1] == pytest.approx(1 / np.sqrt(2), rel=1e-12)
+    b = np.random.default_rng(84).standard_normal(7)
+    I7 = eq.ExplicitMatrix.identity(7)
+    plain = eq.lsqr(I7, b, 50, 1e-12)
+    pre = eq.lsqr_preconditioned(I7, b, eq.EquilibrationParams(iterations=9), 50, 1e-12)
+    assert pre.equil_iterations == 9 and np.array_equal(pre.x, plain.x)
+    assert pre.residual_history[:10] == [1.0] * 10
+    assert pre.residual_history[10:] == plain.residual_history[1:]
+    assert pre.apply_count == plain.apply_count + 9
+    assert pre.adjoint_count == plain.adjoint_count + 9
+
+
+# ---------------------------------------------------------------- errors
+def test_errors_mirror_reference():
+    with pytest.raises(eq.InvalidArgument, match="duplicate"):
+        eq.ExplicitMatrix.from_csr(2, 2, [0, 2, 2], [1, 1], [1.0, 2.0])
+    with pytest.raises(eq.InvalidArgument, match="out of range"):
+        eq.ExplicitMatrix.from_csr(2, 2, [0, 1, 1], [5], [1.0])
+    with pytest.raises(eq.InvalidArgument, match="duplicate"):
+        eq.ExplicitMatrix.sparse(2, 2, [(0, 1, 1.0), (0, 1, 2.0)])
+    M = eq.ExplicitMatrix.identity(3)
+    with pytest.raises(eq.InvalidArgument, match="gamma"):
+        eq.sgd_equilibrate(M, eq.EquilibrationParams(gamma=-1.0, iterations=1))
+    with pytest.raises(eq.InvalidArgument, match="violated"):
+        eq.sgd_equilibrate(M, eq.EquilibrationParams(alpha=1.0, beta=2.0, iterations=1))
+    with pytest.raises(eq.InvalidArgument, match="nonnegative"):
+        eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=-1))
