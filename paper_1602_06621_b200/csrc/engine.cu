@@ -179,36 +179,47 @@ void validate_params(const equil_params& p) {
 }
 
 // ---- traversal plan ---------------------------------------------------------
-constexpr int kMaxRowsPerTile = 2048;
+// Rows longer than kTileNnz become kind-1 tiles (one warp streams the row);
+// all other rows are grouped into kind-2 slices: within windows of
+// kSliceWindow consecutive rows, rows are sorted by length (longest first) and
+// cut into groups of 32, so the lanes of a slice have similar chain lengths and
+// the epilogue's scattered writes stay inside one window.  The row order never
+// affects results: each row is an independent sequential sum.
+struct Plan {
+  std::vector<eqb::Tile> lng, slices;
+  std::vector<int32_t> rowlist;
+};
 
-void plan_tiles(const std::vector<int64_t>& rp, int mat, std::vector<eqb::Tile>& lng,
-                std::vector<eqb::Tile>& packed) {
+Plan plan_tiles(const std::vector<int64_t>& rp, int mat) {
+  Plan P;
   const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
-  int64_t i = 0;
   std::vector<std::pair<int64_t, int64_t>> longs;
-  while (i < rows) {
-    const int64_t len = rp[i + 1] - rp[i];
-    if (len > eqb::kTileNnz) {
-      longs.push_back({len, i});
-      ++i;
-      continue;
+  std::vector<std::pair<int64_t, int32_t>> win;
+  for (int64_t w0 = 0; w0 < rows; w0 += eqb::kSliceWindow) {
+    const int64_t w1 = std::min<int64_t>(rows, w0 + eqb::kSliceWindow);
+    win.clear();
+    for (int64_t i = w0; i < w1; ++i) {
+      const int64_t len = rp[i + 1] - rp[i];
+      if (len > eqb::kTileNnz)
+        longs.push_back({len, i});
+      else
+        win.push_back({len, static_cast<int32_t>(i)});
     }
-    const int64_t start = i;
-    int64_t acc = 0;
-    while (i < rows && i - start < kMaxRowsPerTile) {
-      const int64_t l = rp[i + 1] - rp[i];
-      if (l > eqb::kTileNnz || acc + l > eqb::kTileNnz) break;
-      acc += l;
-      ++i;
+    std::stable_sort(win.begin(), win.end(),
+                     [](const auto& a, const auto& b) { return a.first > b.first; });
+    for (size_t q = 0; q < win.size(); q += eqb::kSliceRows) {
+      const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, win.size() - q));
+      P.slices.push_back({static_cast<int32_t>(P.rowlist.size()), cnt, 2,
+                          static_cast<int16_t>(mat), 0});
+      for (int k = 0; k < cnt; ++k) P.rowlist.push_back(win[q + k].second);
     }
-    packed.push_back({static_cast<int32_t>(start), static_cast<int32_t>(i), 0,
-                      static_cast<int16_t>(mat), 0});
   }
   std::stable_sort(longs.begin(), longs.end(),
-                   [](auto& a, auto& b) { return a.first > b.first; });
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
   for (auto& [len, r] : longs)
-    lng.push_back({static_cast<int32_t>(r), static_cast<int32_t>(r + 1), 1,
-                   static_cast<int16_t>(mat), 0});
+    P.lng.push_back({static_cast<int32_t>(r), static_cast<int32_t>(r + 1), 1,
+                     static_cast<int16_t>(mat), 0});
+  return P;
 }
 
 std::vector<int64_t> partition_rows(const int64_t* rp, int64_t rows, int parts) {
@@ -272,13 +283,19 @@ struct equil_matrix {
   int64_t a_max = 0, t_max = 0;             // padded slice sizes
   DevBuf<int64_t> a_bounds_d, t_bounds_d;
   DevBuf<eqb::Tile> tiles_sgd, tiles_a, tiles_t;
+  DevBuf<int32_t> rowlist_a, rowlist_t;
   int n_sgd = 0, n_a = 0, n_t = 0;
 
   // dense
   DevBuf<double> Ad, colpart;
 
   // workspaces
-  DevBuf<double> xs[2], xw[2];  // padded gathered vectors
+  // padded gathered vectors e.*s (xs) and d.*w (xw), double-buffered, in one
+  // allocation so a single L2 persisting window covers every gather target
+  struct Slot {
+    double* p = nullptr;
+  } xs[2], xw[2];
+  DevBuf<double> xbuf;
   DevBuf<double> u, ub, v, vb;  // local
   DevBuf<uint32_t> signs;
   DevBuf<unsigned char> sign_scratch;
@@ -336,6 +353,39 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   CK(cudaMemset(M->red_counter.p, 0, sizeof(unsigned)));
   M->scal.alloc(64);
   CK(cudaMemset(M->scal.p, 0, 64 * sizeof(double)));
+}
+
+// Upload the traversal plans of the local CSR(A) / CSR(A^T) shards.  The SGD
+// launch covers both matrices: every long row (longest first, so the longest
+// sequential chains start first), then the slices of A and of A^T.
+void build_plans(equil_matrix* M, const std::vector<int64_t>& rpA,
+                 const std::vector<int64_t>& rpT) {
+  Plan pa = plan_tiles(rpA, 0), pt = plan_tiles(rpT, 1);
+  auto lenof = [&](const eqb::Tile& t) {
+    const auto& rph = t.mat ? rpT : rpA;
+    return rph[t.r0 + 1] - rph[t.r0];
+  };
+  std::vector<eqb::Tile> sgd = pa.lng;
+  sgd.insert(sgd.end(), pt.lng.begin(), pt.lng.end());
+  std::stable_sort(sgd.begin(), sgd.end(), [&](const eqb::Tile& x, const eqb::Tile& y) {
+    return lenof(x) > lenof(y);
+  });
+  sgd.insert(sgd.end(), pa.slices.begin(), pa.slices.end());
+  sgd.insert(sgd.end(), pt.slices.begin(), pt.slices.end());
+  std::vector<eqb::Tile> ta = pa.lng, tt = pt.lng;
+  ta.insert(ta.end(), pa.slices.begin(), pa.slices.end());
+  tt.insert(tt.end(), pt.slices.begin(), pt.slices.end());
+  auto upload = [&](auto& d, const auto& h) {
+    d.alloc(h.size());
+    if (!h.empty())
+      CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+    return static_cast<int>(h.size());
+  };
+  M->n_sgd = upload(M->tiles_sgd, sgd);
+  M->n_a = upload(M->tiles_a, ta);
+  M->n_t = upload(M->tiles_t, tt);
+  upload(M->rowlist_a, pa.rowlist);
+  upload(M->rowlist_t, pt.rowlist);
 }
 
 void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
@@ -401,48 +451,42 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   take(fullT, rpT_host, M->t_bounds, M->a_bounds, M->a_max, M->AT, M->t_rp, M->t_ci, M->t_va);
   CK(cudaStreamSynchronize(M->stream));
 
-  // traversal plans on the local shards
   auto local_rp = [&](const std::vector<int64_t>& rph, const std::vector<int64_t>& b) {
     std::vector<int64_t> out(rph.begin() + b[r], rph.begin() + b[r + 1] + 1);
     const int64_t base = out[0];
     for (auto& x : out) x -= base;
     return out;
   };
-  std::vector<eqb::Tile> la, pa, lt, pt;
-  plan_tiles(local_rp(rpA_host, M->a_bounds), 0, la, pa);
-  plan_tiles(local_rp(rpT_host, M->t_bounds), 1, lt, pt);
-  std::vector<eqb::Tile> sgd;
-  // long rows first (longest first), then packed tiles
-  std::vector<eqb::Tile> lng = la;
-  lng.insert(lng.end(), lt.begin(), lt.end());
-  auto lenof = [&](const eqb::Tile& t) {
-    const auto& rph = t.mat ? rpT_host : rpA_host;
-    const auto& b = t.mat ? M->t_bounds : M->a_bounds;
-    return rph[b[r] + t.r0 + 1] - rph[b[r] + t.r0];
-  };
-  std::stable_sort(lng.begin(), lng.end(),
-                   [&](const eqb::Tile& x, const eqb::Tile& y) { return lenof(x) > lenof(y); });
-  sgd = lng;
-  sgd.insert(sgd.end(), pa.begin(), pa.end());
-  sgd.insert(sgd.end(), pt.begin(), pt.end());
-  std::vector<eqb::Tile> ta = la, tt = lt;
-  ta.insert(ta.end(), pa.begin(), pa.end());
-  tt.insert(tt.end(), pt.begin(), pt.end());
-  auto upload = [&](DevBuf<eqb::Tile>& d, const std::vector<eqb::Tile>& h, int& cnt) {
-    d.alloc(h.size());
-    if (!h.empty())
-      CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(eqb::Tile), cudaMemcpyHostToDevice));
-    cnt = static_cast<int>(h.size());
-  };
-  upload(M->tiles_sgd, sgd, M->n_sgd);
-  upload(M->tiles_a, ta, M->n_a);
-  upload(M->tiles_t, tt, M->n_t);
+  build_plans(M, local_rp(rpA_host, M->a_bounds), local_rp(rpT_host, M->t_bounds));
 }
 
 void alloc_workspaces(equil_matrix* M) {
+  const int64_t np = M->n_pad(), mp = M->m_pad();
+  M->xbuf.alloc(2 * (np + mp));
   for (int b = 0; b < 2; ++b) {
-    M->xs[b].alloc(M->n_pad());
-    M->xw[b].alloc(M->m_pad());
+    M->xs[b].p = M->xbuf.p + b * np;
+    M->xw[b].p = M->xbuf.p + 2 * np + b * mp;
+  }
+  // Keep the gather targets resident in L2 while CSR(A)/CSR(A^T) stream past.
+  int dev = 0, max_persist = 0, max_window = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  const size_t bytes = static_cast<size_t>(2 * (np + mp)) * sizeof(double);
+  if (max_persist > 0 && max_window > 0) {
+    const size_t win = std::min(bytes, static_cast<size_t>(max_window));
+    const size_t carve = std::min(win, static_cast<size_t>(max_persist));
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+      cudaStreamAttrValue attr{};
+      attr.accessPolicyWindow.base_ptr = M->xbuf.p;
+      attr.accessPolicyWindow.num_bytes = win;
+      attr.accessPolicyWindow.hitRatio =
+          static_cast<float>(std::min(1.0, static_cast<double>(carve) / win));
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(M->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+    }
+    cudaGetLastError();  // the window is a hint; never fail on it
   }
   M->u.alloc(M->m_loc());
   M->ub.alloc(M->m_loc());
@@ -591,33 +635,7 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
       std::swap(M->t_va.p, tva.p); std::swap(M->t_va.n, tva.n);
       M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
       M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
-      std::vector<eqb::Tile> la, pa, lt, pt;
-      plan_tiles(rpA, 0, la, pa);
-      plan_tiles(rpT, 1, lt, pt);
-      std::vector<eqb::Tile> lng = la;
-      lng.insert(lng.end(), lt.begin(), lt.end());
-      auto lenof = [&](const eqb::Tile& t) {
-        const auto& rph = t.mat ? rpT : rpA;
-        return rph[t.r0 + 1] - rph[t.r0];
-      };
-      std::stable_sort(lng.begin(), lng.end(), [&](const eqb::Tile& x, const eqb::Tile& y) {
-        return lenof(x) > lenof(y);
-      });
-      std::vector<eqb::Tile> sgd = lng;
-      sgd.insert(sgd.end(), pa.begin(), pa.end());
-      sgd.insert(sgd.end(), pt.begin(), pt.end());
-      std::vector<eqb::Tile> ta = la, tt = lt;
-      ta.insert(ta.end(), pa.begin(), pa.end());
-      tt.insert(tt.end(), pt.begin(), pt.end());
-      auto upload = [&](DevBuf<eqb::Tile>& d, const std::vector<eqb::Tile>& h, int& cnt) {
-        d.alloc(h.size());
-        if (!h.empty())
-          CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(eqb::Tile), cudaMemcpyHostToDevice));
-        cnt = static_cast<int>(h.size());
-      };
-      upload(M->tiles_sgd, sgd, M->n_sgd);
-      upload(M->tiles_a, ta, M->n_a);
-      upload(M->tiles_t, tt, M->n_t);
+      build_plans(M.get(), rpA, rpT);
     } else {
       shard_sparse(M.get(), fullA, fullT, rpA, rpT);
     }
@@ -812,6 +830,7 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
         a.rp[k] = C.row_ptr;
         a.ci[k] = C.col;
         a.va[k] = C.val;
+        a.rl[k] = k ? M->rowlist_t.p : M->rowlist_a.p;
       }
       a.tiles = M->tiles_sgd.p;
       a.xs_cur = M->xs[(t - 1) & 1].p;
@@ -994,6 +1013,7 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
   a.ci = C.col;
   a.va = C.val;
   a.tiles = adjoint ? M->tiles_t.p : M->tiles_a.p;
+  a.rl = adjoint ? M->rowlist_t.p : M->rowlist_a.p;
   a.xg = xg;
   a.out = out;
   a.scale = scale;

@@ -9,16 +9,33 @@
 
 namespace eqb {
 
-// Sparse traversal tile.  kind 0: rows [r0, r1) fully inside one tile
-// (nnz <= kTileNnz); kind 1: a single long row r0 streamed in kTileNnz chunks.
+// Sparse traversal tile, one per warp.  kind 0: rows [r0, r1) fully inside one
+// tile (nnz <= kTileNnz); kind 1: a single long row r0 streamed in kTileNnz
+// chunks; kind 2: a slice of r1 (<= 32) rows listed at rowlist[r0 ...], sorted
+// by length (longest first), summed one row per lane in lock-step chunks.
 // mat 0 = A (u block), mat 1 = A^T (v block).
 struct Tile {
   int32_t r0, r1;
   int16_t kind, mat;
   int32_t pad;
 };
-constexpr int kTileNnz = 2048;
-constexpr int kTileThreads = 256;
+constexpr int kTileNnz = 512;    // products staged per warp tile (kinds 0, 1)
+constexpr int kSliceChunk = 16;  // products per row per lock-step round (kind 2)
+constexpr int kSliceStride = 18; // padded row stride (doubles): conflict-free LDS.128
+constexpr int kSliceBatch = 8;   // row pairs staged per batch (loads in flight)
+constexpr int kSliceRows = 32;
+constexpr int kSliceWindow = 4096;  // rows are length-sorted within windows
+constexpr int kWarpSmem = kTileNnz > 32 * kSliceStride ? kTileNnz : 32 * kSliceStride;
+constexpr int kTileWarps = 4;    // independent warps per CTA
+constexpr int kTileThreads = 32 * kTileWarps;
+
+struct SliceMeta {
+  int64_t start[32];  // chunk-aligned base of each row's CSR range
+  int32_t k0[32];     // row start relative to start
+  int32_t len[32];    // row end relative to start
+};
+constexpr int kTileMinBlocks = 8;   // 32 warps/SM: <= 64 registers per thread
+constexpr int kStageUnroll = 4;     // independent loads in flight per lane
 
 // CSR slice resident on the device (int64 row_ptr, int32 col, fp64 val).
 struct DevCsr {
@@ -32,6 +49,7 @@ struct SgdIterArgs {
   const int64_t* rp[2];
   const int32_t* ci[2];
   const double* va[2];
+  const int32_t* rl[2];  // slice row lists
   const Tile* tiles;
   const double* xs_cur;  // gathered e.*s (n, padded coords)
   const double* xw_cur;  // gathered d.*w (m, padded coords)
@@ -61,6 +79,7 @@ struct PassArgs {
   const int64_t* rp;
   const int32_t* ci;
   const double* va;
+  const int32_t* rl;    // slice row list
   const Tile* tiles;
   const double* xg;     // gathered vector (padded coords)
   double* out;          // local rows

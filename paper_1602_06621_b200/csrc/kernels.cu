@@ -350,24 +350,38 @@ cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 namespace {
 
+// read-only load that does not allocate in L1 (streamed CSR arrays)
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_na(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ bool sign_bit(const uint32_t* bits, int64_t b) {
   return (__ldg(bits + (b >> 5)) >> (b & 31)) & 1u;
 }
 
-// products p[k - k0] = val[k] * xg[col[k]] for k in [k0, k1), threads [t0, nt)
-__device__ __forceinline__ void stage_products(const int32_t* __restrict__ ci,
-                                               const double* __restrict__ va,
-                                               const double* __restrict__ xg,
-                                               int64_t k0, int64_t k1,
-                                               double* __restrict__ sp, int t,
-                                               int nt) {
-  constexpr int U = 4;
-  for (int64_t kb = k0 + t; kb < k1; kb += static_cast<int64_t>(nt) * U) {
+// Products p[k - k0] = val[k] * xg[col[k]] for k in [k0, k1), one warp,
+// coalesced streaming loads of val/col, gathers through the read-only path.
+// The product is one rounded multiply whoever computes it, so staging it in
+// any order leaves the sequential sum below bit-identical to the reference.
+__device__ __forceinline__ void warp_stage(const int32_t* __restrict__ ci,
+                                           const double* __restrict__ va,
+                                           const double* __restrict__ xg,
+                                           int64_t k0, int64_t k1,
+                                           double* __restrict__ sp, int lane) {
+  constexpr int U = kStageUnroll;
+  for (int64_t kb = k0 + lane; kb < k1; kb += 32 * U) {
     int32_t c[U];
     double v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t k = kb + static_cast<int64_t>(u) * nt;
+      const int64_t k = kb + 32 * u;
       if (k < k1) {
         c[u] = __ldcs(ci + k);
         v[u] = __ldcs(va + k);
@@ -375,24 +389,44 @@ __device__ __forceinline__ void stage_products(const int32_t* __restrict__ ci,
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t k = kb + static_cast<int64_t>(u) * nt;
+      const int64_t k = kb + 32 * u;
       if (k < k1) sp[k - k0] = __dmul_rn(v[u], __ldg(xg + c[u]));
     }
   }
 }
 
-// sequential CSR-order sum of sp[b, e) onto acc (explicit_matrix.cpp:73-75)
+// Sequential CSR-order sum of sp[b, e) onto acc (explicit_matrix.cpp:73-75).
+// The adds form one dependent chain; the shared-memory loads feeding it are
+// software-pipelined 8 products ahead (16-byte LDS) so the chain runs at add
+// latency instead of load latency.
 __device__ __forceinline__ double chain_sum(double acc, const double* sp, int b,
                                             int e) {
   int k = b;
-  for (; k + 4 <= e; k += 4) {
-    const double p0 = sp[k], p1 = sp[k + 1], p2 = sp[k + 2], p3 = sp[k + 3];
-    acc = __dadd_rn(acc, p0);
-    acc = __dadd_rn(acc, p1);
-    acc = __dadd_rn(acc, p2);
-    acc = __dadd_rn(acc, p3);
+  if ((k & 1) && k < e) acc = __dadd_rn(acc, sp[k++]);
+  const double2* s2 = reinterpret_cast<const double2*>(sp);  // sp is 16B aligned
+  int k2 = k >> 1;
+  const int e2 = e >> 1;
+  if (k2 + 4 <= e2) {
+    double2 c0 = s2[k2], c1 = s2[k2 + 1], c2 = s2[k2 + 2], c3 = s2[k2 + 3];
+    for (k2 += 4; k2 + 4 <= e2; k2 += 4) {
+      const double2 n0 = s2[k2], n1 = s2[k2 + 1], n2 = s2[k2 + 2], n3 = s2[k2 + 3];
+      acc = __dadd_rn(acc, c0.x); acc = __dadd_rn(acc, c0.y);
+      acc = __dadd_rn(acc, c1.x); acc = __dadd_rn(acc, c1.y);
+      acc = __dadd_rn(acc, c2.x); acc = __dadd_rn(acc, c2.y);
+      acc = __dadd_rn(acc, c3.x); acc = __dadd_rn(acc, c3.y);
+      c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    acc = __dadd_rn(acc, c0.x); acc = __dadd_rn(acc, c0.y);
+    acc = __dadd_rn(acc, c1.x); acc = __dadd_rn(acc, c1.y);
+    acc = __dadd_rn(acc, c2.x); acc = __dadd_rn(acc, c2.y);
+    acc = __dadd_rn(acc, c3.x); acc = __dadd_rn(acc, c3.y);
   }
-  for (; k < e; ++k) acc = __dadd_rn(acc, sp[k]);
+  for (; k2 < e2; ++k2) {
+    const double2 c = s2[k2];
+    acc = __dadd_rn(acc, c.x);
+    acc = __dadd_rn(acc, c.y);
+  }
+  if ((e & 1) && e - 1 >= k) acc = __dadd_rn(acc, sp[e - 1]);
   return acc;
 }
 
@@ -415,48 +449,116 @@ __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
   }
 }
 
-__global__ void __launch_bounds__(kTileThreads)
-sgd_iter_kernel(const SgdIterArgs a) {
-  __shared__ double sp[2][kTileNnz];
-  const Tile t = a.tiles[blockIdx.x];
-  const int mat = t.mat;
-  const int64_t* __restrict__ rp = a.rp[mat];
-  const int32_t* __restrict__ ci = a.ci[mat];
-  const double* __restrict__ va = a.va[mat];
-  const double* __restrict__ xg = mat ? a.xw_cur : a.xs_cur;
-  const int tid = threadIdx.x;
-  unsigned fl = 0;
-  if (t.kind == 0) {
-    const int64_t k0 = rp[t.r0], k1 = rp[t.r1];
-    stage_products(ci, va, xg, k0, k1, sp[0], tid, kTileThreads);
-    __syncthreads();
-    for (int64_t r = t.r0 + tid; r < t.r1; r += kTileThreads) {
-      const double acc = chain_sum(0.0, sp[0], static_cast<int>(rp[r] - k0),
-                                   static_cast<int>(rp[r + 1] - k0));
-      sgd_epilogue(a, mat, r, acc, fl);
+// One warp runs one tile; warps never wait on each other, so on an SM the
+// memory-bound staging of some warps overlaps the latency-bound sequential
+// chains of others.  kind 0: every lane sums whole rows of the tile; kind 1: a
+// row longer than a tile is staged chunk by chunk and lane 0 carries the
+// running sum across chunks (the order stays the CSR order).
+template <class Epi>
+__device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restrict__ rp,
+                                         const int32_t* __restrict__ ci,
+                                         const double* __restrict__ va,
+                                         const double* __restrict__ xg,
+                                         const int32_t* __restrict__ rowlist, double* sp,
+                                         SliceMeta& sm, int lane, Epi& epi) {
+  if (t.kind == 2) {
+    // Slice: up to 32 rows (sorted by length, longest first), one per lane, in
+    // lock-step rounds of kSliceChunk products per row.  Each round the warp
+    // stages the rows' next chunks with coalesced half-warp loads into a padded
+    // [row][kSliceStride] buffer (conflict-free 16B reads), then every lane
+    // extends its own row's sequential sum.
+    // Chunks are aligned to kSliceChunk elements in absolute CSR position, so a
+    // 128-byte line of values / 64 bytes of columns is fetched once per row
+    // (the first and last chunk of a row are partial).
+    const int cnt = t.r1;
+    const int myrow = lane < cnt ? rowlist[t.r0 + lane] : -1;
+    const int64_t k0 = myrow >= 0 ? rp[myrow] : 0;
+    const int64_t k1 = myrow >= 0 ? rp[myrow + 1] : 0;
+    const int64_t kb = k0 & ~static_cast<int64_t>(kSliceChunk - 1);
+    const int rounds = k1 > k0 ? static_cast<int>((k1 - kb + kSliceChunk - 1) / kSliceChunk) : 0;
+    sm.start[lane] = kb;
+    sm.k0[lane] = static_cast<int32_t>(k0 - kb);
+    sm.len[lane] = static_cast<int32_t>(k1 - kb);
+    const int maxr = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(rounds)));
+    __syncwarp();
+    const int half = lane >> 4, e = lane & 15;
+    double acc = 0.0;
+    for (int b = 0; b < maxr; ++b) {
+      const int off = b * kSliceChunk;
+      // rows still active this round (rows are length-sorted, so nearly a prefix)
+      const int act = 32 - __clz(__ballot_sync(0xffffffffu, rounds > b));
+      for (int q0 = 0; q0 < act; q0 += 2 * kSliceBatch) {
+        int32_t c[kSliceBatch];
+        double v[kSliceBatch];
+        bool ok[kSliceBatch];
+#pragma unroll
+        for (int u = 0; u < kSliceBatch; ++u) {
+          const int q = q0 + 2 * u + half;
+          const int rel = off + e;  // position relative to the row's aligned base
+          ok[u] = q < act && rel >= sm.k0[q] && rel < sm.len[q];
+          if (ok[u]) {
+            const int64_t k = sm.start[q] + rel;
+            c[u] = ld_na(ci + k);
+            v[u] = ld_na(va + k);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kSliceBatch; ++u) {
+          const int q = q0 + 2 * u + half;
+          if (ok[u]) sp[q * kSliceStride + e] = __dmul_rn(v[u], __ldg(xg + c[u]));
+        }
+      }
+      __syncwarp();
+      if (rounds > b) {
+        const int lo = max(0, sm.k0[lane] - off);
+        const int hi = min(kSliceChunk, sm.len[lane] - off);
+        acc = chain_sum(acc, sp + lane * kSliceStride, lo, hi);
+      }
+      __syncwarp();
     }
+    if (myrow >= 0) epi(myrow, acc);
+  } else if (t.kind == 0) {
+    const int64_t k0 = rp[t.r0], k1 = rp[t.r1];
+    warp_stage(ci, va, xg, k0, k1, sp, lane);
+    __syncwarp();
+    for (int64_t r = t.r0 + lane; r < t.r1; r += 32)
+      epi(r, chain_sum(0.0, sp, static_cast<int>(rp[r] - k0),
+                       static_cast<int>(rp[r + 1] - k0)));
   } else {
-    // long row: warp 0 lane 0 chains chunk c while warps 1.. stage chunk c+1
     const int64_t r = t.r0;
     const int64_t k0 = rp[r], k1 = rp[r + 1];
-    const int64_t nch = (k1 - k0 + kTileNnz - 1) / kTileNnz;
-    stage_products(ci, va, xg, k0, min(k1, k0 + kTileNnz), sp[0], tid, kTileThreads);
-    __syncthreads();
     double acc = 0.0;
-    for (int64_t c = 0; c < nch; ++c) {
-      const int64_t cb = k0 + c * kTileNnz;
-      if (c + 1 < nch && tid >= 32) {
-        const int64_t nb = cb + kTileNnz;
-        stage_products(ci, va, xg, nb, min(k1, nb + kTileNnz), sp[(c + 1) & 1],
-                       tid - 32, kTileThreads - 32);
-      }
-      if (tid == 0)
-        acc = chain_sum(acc, sp[c & 1], 0, static_cast<int>(imin64(kTileNnz, k1 - cb)));
-      __syncthreads();
+    for (int64_t cb = k0, ce; cb < k1; cb = ce) {  // chunks aligned to kTileNnz
+      ce = imin64(k1, (cb & ~static_cast<int64_t>(kTileNnz - 1)) + kTileNnz);
+      warp_stage(ci, va, xg, cb, ce, sp, lane);
+      __syncwarp();
+      if (lane == 0) acc = chain_sum(acc, sp, 0, static_cast<int>(ce - cb));
+      __syncwarp();
     }
-    if (tid == 0) sgd_epilogue(a, mat, r, acc, fl);
+    if (lane == 0) epi(r, acc);
   }
-  if (fl) atomicOr(a.flags, fl);
+}
+
+struct SgdEpi {
+  const SgdIterArgs& a;
+  int mat;
+  unsigned fl;
+  __device__ void operator()(int64_t r, double acc) { sgd_epilogue(a, mat, r, acc, fl); }
+};
+
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+sgd_iter_kernel(const SgdIterArgs a, int ntiles) {
+  __shared__ __align__(16) double sp[kTileWarps][kWarpSmem];
+  __shared__ SliceMeta sm[kTileWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = blockIdx.x * kTileWarps + warp;
+  if (tid >= ntiles) return;
+  const Tile t = a.tiles[tid];
+  const int mat = t.mat;
+  SgdEpi epi{a, mat, 0u};
+  run_tile(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur, a.rl[mat],
+           sp[warp], sm[warp], lane, epi);
+  if (epi.fl) atomicOr(a.flags, epi.fl);
 }
 
 __global__ void sgd_init_kernel(double* xs, double* xw, double* u, double* ub,
@@ -501,7 +603,7 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
 
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  sgd_iter_kernel<<<ntiles, kTileThreads, 0, s>>>(a);
+  sgd_iter_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles);
   return cudaGetLastError();
 }
 
@@ -538,47 +640,27 @@ __device__ __forceinline__ void pass_epilogue(const PassArgs& a, int64_t r,
   }
 }
 
-__global__ void __launch_bounds__(kTileThreads) pass_kernel(const PassArgs a) {
-  __shared__ double sp[2][kTileNnz];
+struct PassEpi {
+  const PassArgs& a;
+  __device__ void operator()(int64_t r, double acc) { pass_epilogue(a, r, acc); }
+};
+
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) pass_kernel(const PassArgs a, int ntiles) {
+  __shared__ __align__(16) double sp[kTileWarps][kWarpSmem];
+  __shared__ SliceMeta sm[kTileWarps];
   if (a.skip && *a.skip) return;
-  const Tile t = a.tiles[blockIdx.x];
-  const int tid = threadIdx.x;
-  if (t.kind == 0) {
-    const int64_t k0 = a.rp[t.r0], k1 = a.rp[t.r1];
-    stage_products(a.ci, a.va, a.xg, k0, k1, sp[0], tid, kTileThreads);
-    __syncthreads();
-    for (int64_t r = t.r0 + tid; r < t.r1; r += kTileThreads)
-      pass_epilogue(a, r,
-                    chain_sum(0.0, sp[0], static_cast<int>(a.rp[r] - k0),
-                              static_cast<int>(a.rp[r + 1] - k0)));
-  } else {
-    const int64_t r = t.r0;
-    const int64_t k0 = a.rp[r], k1 = a.rp[r + 1];
-    const int64_t nch = (k1 - k0 + kTileNnz - 1) / kTileNnz;
-    stage_products(a.ci, a.va, a.xg, k0, min(k1, k0 + kTileNnz), sp[0], tid,
-                   kTileThreads);
-    __syncthreads();
-    double acc = 0.0;
-    for (int64_t c = 0; c < nch; ++c) {
-      const int64_t cb = k0 + c * kTileNnz;
-      if (c + 1 < nch && tid >= 32) {
-        const int64_t nb = cb + kTileNnz;
-        stage_products(a.ci, a.va, a.xg, nb, min(k1, nb + kTileNnz), sp[(c + 1) & 1],
-                       tid - 32, kTileThreads - 32);
-      }
-      if (tid == 0)
-        acc = chain_sum(acc, sp[c & 1], 0, static_cast<int>(imin64(kTileNnz, k1 - cb)));
-      __syncthreads();
-    }
-    if (tid == 0) pass_epilogue(a, r, acc);
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = blockIdx.x * kTileWarps + warp;
+  if (tid >= ntiles) return;
+  PassEpi epi{a};
+  run_tile(a.tiles[tid], a.rp, a.ci, a.va, a.xg, a.rl, sp[warp], sm[warp], lane, epi);
 }
 
 }  // namespace
 
 cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  pass_kernel<<<ntiles, kTileThreads, 0, s>>>(a);
+  pass_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles);
   return cudaGetLastError();
 }
 
