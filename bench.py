@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- equilibration throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (config.workload): BASELINE.json configs[2] ("c3"): sparse CSR A,
+m = 2e6, n = 1e6, Zipf(1.5) row lengths on [1, 1e4] (nnz = 1.535e8), entries
+N(0,1) with row/column scalings exp(N(0,1.5)); auto targets, T = 100
+stochastic iterations, seed 0.  It is the config BASELINE's metric is quoted on
+at 1/2/4/8 GPUs.  A "step" is one complete sgd_equilibrate call: all T*(n+m)
+probe signs generated on device, T fused SGD passes over CSR(A) and CSR(A^T),
+final exp.  value = whole-job iterations per second (strong scaling: the same
+matrix is row-sharded over N GPUs).
+
+Our arm prints one JSON line with value (matrix resident in HBM), e2e (one-shot
+C-ABI call from pinned host CSR: upload + device transpose + T iterations +
+download), roofline (live CUDA-event time of the fused iteration kernel), the
+CPU baseline (oracle C port, single thread, bounded sample), clocks and the
+number of our kernels launched.  --impl reference times the reference's own
+sources (oracle/_ref, built from /root/reference against eigen-lite) on the
+host: rank 0 only, single thread (the reference has no threading).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "equilibration iters/sec and achieved HBM GB/s (fraction of 8 TB/s) at 1/2/4/8 B200"
+UNIT = "iterations/s"
+CONFIG_ID = 3
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def algorithmic_bytes(inst) -> float:
+    """Bytes one SGD iteration must move:
+    A and A^T values + int32 columns (24 B/nnz), both row pointers, the two
+    gathered vectors once, u/ubar/v/vbar read+write, next e.*s / d.*w written,
+    the sign bits."""
+    m, n, nnz = inst.m, inst.n, inst.nnz
+    return 24.0 * nnz + 52.125 * (m + n) + 8.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per sgd_iter_kernel launch from the committed ncu --set full
+    capture (profiles/ncu_summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["sgd_iter_kernel"]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_baseline(inst, iters: int):
+    import numpy as np  # noqa: F401
+    import oracle
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    O = oracle.c_oracle()
+    t0 = time.perf_counter()
+    O.sgd_equilibrate(A, alpha=inst.alpha, beta=inst.beta, iterations=iters, seed=inst.seed)
+    dt = time.perf_counter() - t0
+    return {"value": iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{iters} SGD iterations of the full c3 matrix (oracle/equil_oracle.c, "
+                      f"bit-identical to the reference's sources), 1 thread, {dt:.2f} s"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1602_06621_b200 as eq
+    from paper_1602_06621_b200 import configs
+
+    rank, world, local = dist_env()
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        raise SystemExit("run N>1 under torch.distributed.run (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    inst = configs.config(CONFIG_ID)
+    T = inst.iterations
+    nccl_id = None
+    if world > 1:
+        obj = [eq.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    M = eq.ExplicitMatrix.from_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val,
+                                   device=local, rank=rank, world_size=world, nccl_id=nccl_id)
+    p = eq.EquilibrationParams(alpha=inst.alpha, beta=inst.beta, iterations=T, seed=inst.seed)
+    dev = torch.device("cuda", local)
+    u = torch.empty(inst.m, dtype=torch.float64, device=dev)
+    v = torch.empty(inst.n, dtype=torch.float64, device=dev)
+    d = torch.empty(inst.m, dtype=torch.float64, device=dev)
+    e = torch.empty(inst.n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(eq._lib.load().equil_matrix_stream(M._h))
+
+    def step():
+        return eq.sgd_equilibrate_device(M, p, u.data_ptr(), v.data_ptr(), d.data_ptr(),
+                                         e.data_ptr())
+
+    for _ in range(args.warmup):
+        res = step()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    barrier()
+    clocks.start()
+    l0 = eq.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    loop_ms = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+        loop_ms.append(eq.last_loop_ms(M)[0])
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    launches = eq.kernel_launches() - l0
+    clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    value = T * args.steps / elapsed
+
+    # ---- roofline of the dominant kernel (fused SGD pass), live CUDA events
+    B = algorithmic_bytes(inst)
+    kern_s = statistics.mean(loop_ms) / 1e3 / T  # per launch (loop of T launches)
+    per_gpu_bytes = B / world
+    achieved = per_gpu_bytes / kern_s / 1e9
+    peak, peak_src = peaks()
+    traffic = ncu_traffic()
+
+    # ---- e2e through the one-shot C ABI from pinned host memory
+    e2e = None
+    if world == 1:
+        pin_rp = torch.from_numpy(inst.row_ptr).pin_memory()
+        pin_c = torch.from_numpy(inst.col).pin_memory()
+        pin_v = torch.from_numpy(inst.val).pin_memory()
+        eq.sgd_equilibrate_csr(inst.m, inst.n, pin_rp.numpy(), pin_c.numpy(), pin_v.numpy(),
+                               p, device=local)  # warm (module load, jump polys)
+        ts = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            r = eq.sgd_equilibrate_csr(inst.m, inst.n, pin_rp.numpy(), pin_c.numpy(),
+                                       pin_v.numpy(), p, device=local)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = statistics.mean(ts)
+        h2d = int(inst.row_ptr.nbytes + inst.col.nbytes + inst.val.nbytes)
+        d2h = int(8 * 2 * (inst.m + inst.n))
+        e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "s_per_step": e2e_s,
+               "path": "equil_sgd_equilibrate_csr (upload, device transpose, T iterations, "
+                       "download)"}
+        del r
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(inst, args.cpu_iters)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator restating BASELINE configs[2])",
+            "config": {"workload": "c3: sparse CSR 2e6 x 1e6, Zipf(1.5) rows on [1,1e4], "
+                                   "exp(N(0,1.5)) scalings, T=100, seed 0, auto targets",
+                       "m": inst.m, "n": inst.n, "nnz": inst.nnz, "iterations_per_step": T,
+                       "l2": "inputs larger than L2 (CSR(A)+CSR(A^T) = 3.7 GB >> 126 MB)",
+                       "parallelism": f"rows of A and A^T sharded over {world} GPU(s)"},
+            "ms_per_iteration": elapsed / args.steps / T * 1e3,
+            "achieved_GBps": B * value / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "sgd_iter_kernel (fused A/A^T pass + u/v epilogue)",
+                         "bytes_per_launch": per_gpu_bytes, "launch_ms": kern_s * 1e3,
+                         "peak_source": peak_src},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
+            "flags": {"box_feasible": res.box_feasible, "iterate_bound_ok": res.iterate_bound_ok},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from paper_1602_06621_b200 import configs
+    if not os.path.exists(oracle.REF_PATH):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libequil_ref.so was "
+                          "not built (needs /root/reference at build time)"}))
+        return
+    inst = configs.config(CONFIG_ID)
+    R = oracle.ref_oracle()
+    t0 = time.perf_counter()
+    RM = R.matrix(oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val))
+    build_s = time.perf_counter() - t0
+    T = 1  # one SGD iteration of the full matrix per step (bounded sample)
+    for _ in range(args.warmup):
+        RM.sgd_equilibrate(alpha=inst.alpha, beta=inst.beta, iterations=T, seed=inst.seed)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        RM.sgd_equilibrate(alpha=inst.alpha, beta=inst.beta, iterations=T, seed=inst.seed)
+    dt = time.perf_counter() - t0
+    value = T * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator restating BASELINE configs[2])",
+        "config": {"workload": "c3: sparse CSR 2e6 x 1e6, Zipf(1.5) rows on [1,1e4], "
+                               "exp(N(0,1.5)) scalings, T=100, seed 0, auto targets",
+                   "m": inst.m, "n": inst.n, "nnz": inst.nnz},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"sgd_equilibrate with T={T} per step on the full c3 matrix; "
+                                   "reference sources (oracle/_ref) on eigen-lite, 1 thread "
+                                   f"(ExplicitMatrix::sparse build {build_s:.1f} s untimed)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

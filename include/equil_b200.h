@@ -127,6 +127,11 @@ equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
                                 int64_t* nnz);
 /* The cudaStream_t all work on this handle is issued on (for event timing). */
 void* equil_matrix_stream(equil_matrix* A);
+/* Device time (CUDA events on the handle's stream) of the T-iteration loop of
+ * the last equil_sgd_equilibrate call; *iterations receives T. */
+double equil_last_loop_ms(equil_matrix* A, int* iterations);
+/* Number of this library's kernels launched so far in the process. */
+long long equil_kernel_launches(void);
 
 /* LinearOperator::apply / apply_adjoint (include/equil/linop.hpp:13-25,
  * src/explicit_matrix.cpp:67-93): y = A x or x = A^T y, host vectors. */

@@ -7,14 +7,16 @@ reference's interface over that ABI.  See DESIGN.md.
 from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   DiagnosticsConfig, EquilibrationParams, EquilRuntimeError,
                   ExplicitMatrix, InvalidArgument, IterationRecord, LsqrRun,
-                  ScalingResult, canon_sumsq_device, det_exp_device, lsqr,
-                  lsqr_preconditioned, nccl_unique_id, partition_rows,
-                  resolve_targets, sgd_equilibrate, sign_bits, validate_params)
+                  ScalingResult, canon_sumsq_device, det_exp_device, kernel_launches,
+                  last_loop_ms, lsqr, lsqr_preconditioned, nccl_unique_id,
+                  partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
+                  sgd_equilibrate_device, sign_bits, validate_params)
 
 __all__ = [
     "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "DiagnosticsConfig",
     "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",
     "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",
-    "lsqr", "lsqr_preconditioned", "nccl_unique_id", "partition_rows", "resolve_targets",
-    "sgd_equilibrate", "sign_bits", "validate_params",
+    "kernel_launches", "last_loop_ms", "lsqr", "lsqr_preconditioned", "nccl_unique_id",
+    "partition_rows", "resolve_targets", "sgd_equilibrate", "sgd_equilibrate_csr",
+    "sgd_equilibrate_device", "sign_bits", "validate_params",
 ]

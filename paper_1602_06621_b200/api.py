@@ -272,6 +272,49 @@ def sgd_equilibrate(op: ExplicitMatrix, params: EquilibrationParams | None = Non
                          bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
 
 
+def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,
+                           u_ptr: int, v_ptr: int, d_ptr: int, e_ptr: int) -> ScalingResult:
+    """sgd_equilibrate with u, v, d, e written to caller-owned DEVICE buffers
+    (raw pointers, e.g. torch tensors' data_ptr()); the vectors in the returned
+    record are empty."""
+    p = params._c()
+    dp = C.POINTER(C.c_double)
+    out = L.ScalingOut(C.cast(u_ptr, dp), C.cast(v_ptr, dp), C.cast(d_ptr, dp),
+                       C.cast(e_ptr, dp), 1, 0.0, 0.0, 0, 0, 0, 0, None, None, None, 0, 0)
+    _check(L.load().equil_sgd_equilibrate(op._h, C.byref(p), None, C.byref(out)))
+    z = np.zeros(0)
+    return ScalingResult(z, z, z, z, out.alpha, out.beta, [], bool(out.box_feasible),
+                         bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
+
+
+def sgd_equilibrate_csr(rows: int, cols: int, row_ptr, col, val,
+                        params: EquilibrationParams, device: int = 0) -> ScalingResult:
+    """One-shot C-ABI entry (equil_sgd_equilibrate_csr): host CSR in, host
+    scaling out; upload, device transpose, equilibration and download inside."""
+    u, v, d, e = np.zeros(rows), np.zeros(cols), np.zeros(rows), np.zeros(cols)
+    out = L.ScalingOut(L.ptr(u, L._dp), L.ptr(v, L._dp), L.ptr(d, L._dp), L.ptr(e, L._dp), 0,
+                       0.0, 0.0, 0, 0, 0, 0, None, None, None, 0, 0)
+    p = params._c()
+    cfg = L.DeviceCfg(device, 0, 1, None)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    _check(L.load().equil_sgd_equilibrate_csr(
+        rows, cols, L.ptr(rp, L._i64p), col.ctypes.data_as(L._i32p),
+        val.ctypes.data_as(L._dp), C.byref(p), C.byref(cfg), C.byref(out)))
+    return ScalingResult(u, v, d, e, out.alpha, out.beta, [], bool(out.box_feasible),
+                         bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
+
+
+def last_loop_ms(op: ExplicitMatrix):
+    """(device ms of the last call's T-iteration loop, T)"""
+    it = C.c_int()
+    ms = L.load().equil_last_loop_ms(op._h, C.byref(it))
+    return ms, it.value
+
+
+def kernel_launches() -> int:
+    return int(L.load().equil_kernel_launches())
+
+
 def _lsqr_run(x, h, out) -> LsqrRun:
     return LsqrRun(x, list(h[: out.hist_len]), out.iterations, out.equil_iterations,
                    bool(out.reached_tol), bool(out.breakdown), out.apply_count,

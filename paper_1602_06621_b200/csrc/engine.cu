@@ -322,7 +322,15 @@ struct equil_matrix {
   int64_t m_pad() const { return world == 1 ? m : a_max * world; }
   int64_t n_pad() const { return world == 1 ? n : t_max * world; }
 
+  // events bracketing the T-iteration loop of the last sgd call (also inside
+  // the captured graph), for the live per-kernel roofline in bench.py
+  cudaEvent_t ev_loop0 = nullptr, ev_loop1 = nullptr;
+  double last_loop_ms = 0.0;
+  int last_loop_iters = 0;
+
   ~equil_matrix() {
+    if (ev_loop0) cudaEventDestroy(ev_loop0);
+    if (ev_loop1) cudaEventDestroy(ev_loop1);
     if (graph) cudaGraphExecDestroy(graph);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
@@ -352,6 +360,8 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   M->red_counter.alloc(1);
   CK(cudaMemset(M->red_counter.p, 0, sizeof(unsigned)));
   M->scal.alloc(64);
+  CK(cudaEventCreate(&M->ev_loop0));
+  CK(cudaEventCreate(&M->ev_loop1));
   CK(cudaMemset(M->scal.p, 0, 64 * sizeof(double)));
 }
 
@@ -687,6 +697,14 @@ void* equil_matrix_stream(equil_matrix* A) {
   return A ? static_cast<void*>(A->stream) : nullptr;
 }
 
+double equil_last_loop_ms(equil_matrix* A, int* iterations) {
+  if (!A) return 0.0;
+  if (iterations) *iterations = A->last_loop_iters;
+  return A->last_loop_ms;
+}
+
+long long equil_kernel_launches(void) { return eqb::launch_count(); }
+
 equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
                                 int64_t* nnz) {
   return guarded([&] {
@@ -902,7 +920,9 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         try {
+          CK(cudaEventRecord(M->ev_loop0, s));
           for (int t = 1; t <= T; ++t) one_iter(t);
+          CK(cudaEventRecord(M->ev_loop1, s));
         } catch (...) {
           cudaStreamEndCapture(s, &g);
           throw;
@@ -913,12 +933,16 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
         M->graph_key = key;
       }
       CK(cudaGraphLaunch(M->graph, s));
+      eqb::note_launches(T);
     } else {
+      CK(cudaEventRecord(M->ev_loop0, s));
       for (int t = 1; t <= T; ++t) {
         one_iter(t);
         if (dp.stride && t % dp.stride == 0) record(t);
       }
+      CK(cudaEventRecord(M->ev_loop1, s));
     }
+    M->last_loop_iters = T;
 
     // finalize: u = ubar, v = vbar, d = exp(ubar), e = exp(vbar) (:201-204)
     const int64_t ml = M->m_loc(), nl = M->n_loc();
@@ -963,6 +987,13 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
     if (nrec)
       CK(cudaMemcpyAsync(hh.data(), hist.p, kRec * nrec * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    M->last_loop_ms = 0.0;
+    if (T > 0) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, M->ev_loop0, M->ev_loop1) == cudaSuccess)
+        M->last_loop_ms = ms;
+      cudaGetLastError();
+    }
     out->alpha = alpha;
     out->beta = beta;
     out->iterate_bound_ok = (flags & 1u) ? 0 : 1;

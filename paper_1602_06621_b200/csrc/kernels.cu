@@ -14,6 +14,7 @@
 // Every floating-point operation that feeds the trajectory is an explicit
 // round-to-nearest intrinsic; the library is also built with --fmad=false.
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -25,6 +26,20 @@ namespace eqb {
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) {
   return a < b ? a : b;
+}
+
+// Kernel-launch accounting for bench.py's "gpu_launches" (launches issued while
+// a stream is being captured are counted when the graph is replayed instead).
+static std::atomic<long long> g_launches{0};
+void note_launches(long long n) { g_launches += n; }
+long long launch_count() { return g_launches.load(); }
+static void count_launch(cudaStream_t s, int n = 1) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+    cudaGetLastError();
+    st = cudaStreamCaptureStatusNone;
+  }
+  if (st == cudaStreamCaptureStatusNone) g_launches += n;
 }
 
 #define EQ_CUDA_TRY(x)                   \
@@ -216,11 +231,11 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
     const uint64_t lo = 1ULL << a;
     const uint64_t cnt = std::min(lo, G - lo);
     mt_jump_kernel<<<static_cast<unsigned>(cnt), kMtThreads, smem, s>>>(
-        windows, 0, static_cast<int>(lo), polys + a * mt::kPolyWords);
+        windows, 0, static_cast<int>(lo), polys + a * mt::kPolyWords); count_launch(s);
     EQ_CUDA_TRY(cudaGetLastError());
   }
   mt_gen_kernel<<<static_cast<unsigned>(G), kMtThreads, 0, s>>>(windows, L, total,
-                                                                bits);
+                                                                bits); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -261,10 +276,10 @@ cudaError_t launch_validate_csr(const DevCsr& A, int* err, int64_t* where,
                                 cudaStream_t s) {
   const int bs = 256;
   validate_rows_kernel<<<static_cast<unsigned>((A.rows + 1 + bs - 1) / bs), bs, 0, s>>>(
-      A.row_ptr, A.rows, A.nnz, err, where);
+      A.row_ptr, A.rows, A.nnz, err, where); count_launch(s);
   EQ_CUDA_TRY(cudaGetLastError());
   validate_cols_kernel<<<static_cast<unsigned>((A.rows + bs - 1) / bs), bs, 0, s>>>(
-      A.row_ptr, A.col, A.rows, A.cols, err, where);
+      A.row_ptr, A.col, A.rows, A.cols, err, where); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -321,7 +336,7 @@ cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
       e = cudaMallocAsync(&perm_in, nnz * sizeof(int32_t), s); if (e) break;
       e = cudaMallocAsync(&perm_out, nnz * sizeof(int32_t), s); if (e) break;
       e = cudaMallocAsync(&keys_out, nnz * sizeof(int32_t), s); if (e) break;
-      iota_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(perm_in, nnz);
+      iota_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(perm_in, nnz); count_launch(s);
       e = cudaGetLastError(); if (e) break;
       e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, A.col, keys_out, perm_in,
                                           perm_out, nnz, 0, end_bit, s);
@@ -331,11 +346,11 @@ cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
                                           perm_out, nnz, 0, end_bit, s);
       if (e) break;
       transpose_gather_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
-          A.row_ptr, A.rows, A.val, perm_out, nnz, AT.col, AT.val);
+          A.row_ptr, A.rows, A.val, perm_out, nnz, AT.col, AT.val); count_launch(s);
       e = cudaGetLastError(); if (e) break;
     }
     transpose_rowptr_kernel<<<static_cast<unsigned>((nnz + 1 + 255) / 256), 256, 0, s>>>(
-        keys_out, nnz, A.cols, AT.row_ptr);
+        keys_out, nnz, A.cols, AT.row_ptr); count_launch(s);
     e = cudaGetLastError();
   } while (0);
   if (temp) cudaFreeAsync(temp, s);
@@ -597,20 +612,20 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
   if (nmax == 0) return cudaSuccess;
   sgd_init_kernel<<<static_cast<unsigned>((nmax + 255) / 256), 256, 0, s>>>(
       xs, xw, u, ub, v, vb, signs, m_loc, n_loc, a_goff, at_goff, a_poff, at_poff,
-      n_glob);
+      n_glob); count_launch(s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  sgd_iter_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles);
+  sgd_iter_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles); count_launch(s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  exp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, y, n, scale);
+  exp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, y, n, scale); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -660,7 +675,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) pass_kernel(cons
 
 cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  pass_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles);
+  pass_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -726,7 +741,7 @@ cudaError_t launch_canon_reduce(const double* x, int64_t len, int kind, double c
                                 int sqrt_out, cudaStream_t s) {
   const int64_t nc = std::max<int64_t>(1, (len + kChunk - 1) / kChunk);
   canon_reduce_kernel<<<static_cast<unsigned>(nc), 256, 0, s>>>(
-      x, len, kind, coef, partials, counter, out, sqrt_out);
+      x, len, kind, coef, partials, counter, out, sqrt_out); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -773,7 +788,7 @@ cudaError_t launch_lsqr_normalize(double* dst, const double* src,
                                   int* invariant, int* skip_in, cudaStream_t s) {
   const int64_t nb = std::max<int64_t>(1, (len + 255) / 256);
   lsqr_normalize_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(
-      dst, src, norm_dev, scaled_out, scale, len, invariant, skip_in);
+      dst, src, norm_dev, scaled_out, scale, len, invariant, skip_in); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -782,7 +797,7 @@ cudaError_t launch_lsqr_xw_update(double* x, double* w, const double* v,
                                   double* ex, int64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   lsqr_xw_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, w, v, c1, c2,
-                                                                        e, ex, n);
+                                                                        e, ex, n); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -960,30 +975,30 @@ static cudaError_t dense_cols_partial(const double* A, int64_t m, int64_t n,
   }
   const dim3 grid(static_cast<unsigned>((n + 31) / 32),
                   static_cast<unsigned>((m + kChunk - 1) / kChunk));
-  dense_cols_partial_kernel<<<grid, 256, smem, s>>>(A, m, n, w, colpart);
+  dense_cols_partial_kernel<<<grid, 256, smem, s>>>(A, m, n, w, colpart); count_launch(s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s) {
   if (a.n > static_cast<int64_t>(kChunk) * kMaxDenseChunks) return cudaErrorInvalidValue;
-  dense_sgd_rows_kernel<<<static_cast<unsigned>(a.m), 256, 0, s>>>(a);
+  dense_sgd_rows_kernel<<<static_cast<unsigned>(a.m), 256, 0, s>>>(a); count_launch(s);
   EQ_CUDA_TRY(cudaGetLastError());
   EQ_CUDA_TRY(dense_cols_partial(a.A, a.m, a.n, a.xw_cur, a.colpart, s));
-  dense_sgd_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
+  dense_sgd_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a); count_launch(s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s) {
   if (!a.adjoint) {
     if (a.n > static_cast<int64_t>(kChunk) * kMaxDenseChunks) return cudaErrorInvalidValue;
-    dense_pass_rows_kernel<<<static_cast<unsigned>(a.m), 256, 0, s>>>(a);
+    dense_pass_rows_kernel<<<static_cast<unsigned>(a.m), 256, 0, s>>>(a); count_launch(s);
     return cudaGetLastError();
   }
   // A^T y: columns of the row-major m x n matrix
   EQ_CUDA_TRY(dense_cols_partial(a.A, a.m, a.n, a.xg, a.colpart, s));
   DensePassArgs b = a;
   b.m = a.m;
-  dense_pass_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(b);
+  dense_pass_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(b); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -1019,7 +1034,7 @@ cudaError_t launch_rms_terms(int mat, const DevCsr& M, const double* eu,
                              double target, cudaStream_t s) {
   if (M.rows == 0) return cudaSuccess;
   rms_terms_kernel<<<static_cast<unsigned>((M.rows + 255) / 256), 256, 0, s>>>(
-      mat, M.row_ptr, M.col, M.val, M.rows, eu, ev, out, goff, target);
+      mat, M.row_ptr, M.col, M.val, M.rows, eu, ev, out, goff, target); count_launch(s);
   return cudaGetLastError();
 }
 
@@ -1057,13 +1072,13 @@ cudaError_t launch_obj_terms(const DevCsr& A, const double* u, const double* v,
                              double* out, cudaStream_t s) {
   if (A.rows == 0) return cudaSuccess;
   obj_terms_kernel<<<static_cast<unsigned>((A.rows + 255) / 256), 256, 0, s>>>(
-      A.row_ptr, A.col, A.val, A.rows, u, v, out);
+      A.row_ptr, A.col, A.val, A.rows, u, v, out); count_launch(s);
   return cudaGetLastError();
 }
 cudaError_t launch_mul(double* out, const double* a, const double* b, int64_t n,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  mul_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(out, a, b, n);
+  mul_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(out, a, b, n); count_launch(s);
   return cudaGetLastError();
 }
 }  // namespace eqb
