@@ -219,7 +219,7 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (fused SGD pass), live CUDA events
     B = algorithmic_bytes(inst)
-    kern_s = statistics.mean(loop_ms) / 1e3 / T  # per launch (loop of T launches)
+    kern_s = max(statistics.mean(loop_ms), 1e-9) / 1e3 / T  # per launch (T launches)
     per_gpu_bytes = B / world
     achieved = per_gpu_bytes / kern_s / 1e9
     peak, peak_src = peaks()

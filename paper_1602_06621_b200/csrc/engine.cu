@@ -920,9 +920,10 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         try {
-          CK(cudaEventRecord(M->ev_loop0, s));
+          // external event-record nodes: the graph itself timestamps the loop
+          CK(cudaEventRecordWithFlags(M->ev_loop0, s, cudaEventRecordExternal));
           for (int t = 1; t <= T; ++t) one_iter(t);
-          CK(cudaEventRecord(M->ev_loop1, s));
+          CK(cudaEventRecordWithFlags(M->ev_loop1, s, cudaEventRecordExternal));
         } catch (...) {
           cudaStreamEndCapture(s, &g);
           throw;
