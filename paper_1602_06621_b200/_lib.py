@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libequil_b200.so")
+LIB_PATH = os.environ.get("EQUIL_LIB") or os.path.join(HERE, "libequil_b200.so")
 
 EQUIL_OK, EQUIL_EINVAL, EQUIL_ERUNTIME, EQUIL_ECUDA, EQUIL_ENCCL, EQUIL_ENOMEM = range(6)
 

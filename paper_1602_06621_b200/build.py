@@ -17,8 +17,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(CSRC, "build")
-LIB = os.path.join(HERE, "libequil_b200.so")
+# EQUIL_TAG / EQUIL_DEFS build tuning variants side by side (development only):
+#   EQUIL_TAG=b4 EQUIL_DEFS="-DEQ_SLICE_BATCH=4" python -m paper_1602_06621_b200.build
+# produces libequil_b200_b4.so; EQUIL_LIB=<path> makes _lib load it.
+TAG = os.environ.get("EQUIL_TAG", "")
+DEFS = os.environ.get("EQUIL_DEFS", "").split()
+OBJ = os.path.join(CSRC, "build" + (f"_{TAG}" if TAG else ""))
+LIB = os.path.join(HERE, "libequil_b200" + (f"_{TAG}" if TAG else "") + ".so")
 GEN_LIB = os.path.join(HERE, "libequil_gen.so")  # synthetic inputs (bench/tests)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -60,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _stale(o, [s, *hdrs]):
             if verbose:
                 print("nvcc", src, flush=True)
-            _run([NVCC, *ARCH, *NVFLAGS, "-c", s, "-o", o], log=o + ".ptxas.log")
+            _run([NVCC, *ARCH, *NVFLAGS, *DEFS, "-c", s, "-o", o], log=o + ".ptxas.log")
         objs.append(o)
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)

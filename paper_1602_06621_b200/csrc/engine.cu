@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/equil_b200.h"
@@ -113,6 +115,23 @@ equil_status guarded(F&& f) {
   }
 }
 
+// EQUIL_VERBOSE=1: per-phase wall times of setup calls (synchronizing; debug only)
+struct PhaseTimer {
+  const char* what;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(const char* w)
+      : what(w), on(getenv("EQUIL_VERBOSE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(cudaStream_t s, const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[equil] %s %-14s %8.2f ms\n", what, phase,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -179,46 +198,80 @@ void validate_params(const equil_params& p) {
 }
 
 // ---- traversal plan ---------------------------------------------------------
-// Rows longer than kTileNnz become kind-1 tiles (one warp streams the row);
-// all other rows are grouped into kind-2 slices: within windows of
+// Rows longer than kTileNnz become kind-3 long slices (32 length-sorted rows
+// per CTA); all other rows are grouped into kind-2 slices: within windows of
 // kSliceWindow consecutive rows, rows are sorted by length (longest first) and
 // cut into groups of 32, so the lanes of a slice have similar chain lengths and
 // the epilogue's scattered writes stay inside one window.  The row order never
-// affects results: each row is an independent sequential sum.
+// affects results: each row is an independent sequential sum.  Windows are
+// planned in parallel host threads; the result does not depend on the thread
+// count (parts are concatenated in window order, ties keep row order).
 struct Plan {
   std::vector<eqb::Tile> lng, slices;
   std::vector<int32_t> rowlist;
 };
 
-Plan plan_tiles(const std::vector<int64_t>& rp, int mat) {
+Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   Plan P;
-  const int64_t rows = static_cast<int64_t>(rp.size()) - 1;
+  const int64_t nwin = (rows + eqb::kSliceWindow - 1) / eqb::kSliceWindow;
+  const int nth = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), nwin / 8)));
+  struct Part {
+    std::vector<eqb::Tile> slices;
+    std::vector<int32_t> rowlist;
+    std::vector<std::pair<int64_t, int64_t>> longs;
+  };
+  std::vector<Part> parts(nth);
+  auto work = [&](int t) {
+    Part& pt = parts[t];
+    const int64_t wa = nwin * t / nth, wb = nwin * (t + 1) / nth;
+    std::vector<std::pair<int64_t, int32_t>> win;
+    for (int64_t w = wa; w < wb; ++w) {
+      const int64_t w0 = w * eqb::kSliceWindow;
+      const int64_t w1 = std::min<int64_t>(rows, w0 + eqb::kSliceWindow);
+      win.clear();
+      for (int64_t i = w0; i < w1; ++i) {
+        const int64_t len = rp[i + 1] - rp[i];
+        if (len > eqb::kTileNnz)
+          pt.longs.push_back({len, i});
+        else
+          win.push_back({len, static_cast<int32_t>(i)});
+      }
+      std::stable_sort(win.begin(), win.end(),
+                       [](const auto& a, const auto& b) { return a.first > b.first; });
+      for (size_t q = 0; q < win.size(); q += eqb::kSliceRows) {
+        const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, win.size() - q));
+        pt.slices.push_back({static_cast<int32_t>(pt.rowlist.size()), cnt, 2,
+                             static_cast<int16_t>(mat), 0});
+        for (int k = 0; k < cnt; ++k) pt.rowlist.push_back(win[q + k].second);
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nth; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
   std::vector<std::pair<int64_t, int64_t>> longs;
-  std::vector<std::pair<int64_t, int32_t>> win;
-  for (int64_t w0 = 0; w0 < rows; w0 += eqb::kSliceWindow) {
-    const int64_t w1 = std::min<int64_t>(rows, w0 + eqb::kSliceWindow);
-    win.clear();
-    for (int64_t i = w0; i < w1; ++i) {
-      const int64_t len = rp[i + 1] - rp[i];
-      if (len > eqb::kTileNnz)
-        longs.push_back({len, i});
-      else
-        win.push_back({len, static_cast<int32_t>(i)});
+  for (Part& pt : parts) {
+    const int32_t base = static_cast<int32_t>(P.rowlist.size());
+    for (eqb::Tile s : pt.slices) {
+      s.r0 += base;
+      P.slices.push_back(s);
     }
-    std::stable_sort(win.begin(), win.end(),
-                     [](const auto& a, const auto& b) { return a.first > b.first; });
-    for (size_t q = 0; q < win.size(); q += eqb::kSliceRows) {
-      const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, win.size() - q));
-      P.slices.push_back({static_cast<int32_t>(P.rowlist.size()), cnt, 2,
-                          static_cast<int16_t>(mat), 0});
-      for (int k = 0; k < cnt; ++k) P.rowlist.push_back(win[q + k].second);
-    }
+    P.rowlist.insert(P.rowlist.end(), pt.rowlist.begin(), pt.rowlist.end());
+    longs.insert(longs.end(), pt.longs.begin(), pt.longs.end());
   }
+  // rows longer than a tile: CTA-cooperative long slices of 32 length-sorted
+  // rows (kind 3), each replicated once per warp of the CTA
   std::stable_sort(longs.begin(), longs.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-  for (auto& [len, r] : longs)
-    P.lng.push_back({static_cast<int32_t>(r), static_cast<int32_t>(r + 1), 1,
-                     static_cast<int16_t>(mat), 0});
+  for (size_t q = 0; q < longs.size(); q += eqb::kSliceRows) {
+    const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, longs.size() - q));
+    const eqb::Tile t{static_cast<int32_t>(P.rowlist.size()), cnt, 3,
+                      static_cast<int16_t>(mat), 0};
+    for (int k = 0; k < cnt; ++k) P.rowlist.push_back(static_cast<int32_t>(longs[q + k].second));
+    for (int w = 0; w < eqb::kTileWarps; ++w) P.lng.push_back(t);
+  }
   return P;
 }
 
@@ -349,6 +402,14 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   require(M->device >= 0 && M->device < ndev, "device cfg: no such CUDA device");
   CK(cudaSetDevice(M->device));
   CK(cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking));
+  {  // keep stream-ordered scratch (transpose, reductions) cached across calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, M->device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   if (M->world > 1) {
     require(cfg->nccl_id != nullptr, "device cfg: world_size > 1 needs nccl_id");
     if (!nccl().ok) fail(EQUIL_ENCCL, "libnccl.so.2 could not be loaded");
@@ -368,18 +429,10 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
 // Upload the traversal plans of the local CSR(A) / CSR(A^T) shards.  The SGD
 // launch covers both matrices: every long row (longest first, so the longest
 // sequential chains start first), then the slices of A and of A^T.
-void build_plans(equil_matrix* M, const std::vector<int64_t>& rpA,
-                 const std::vector<int64_t>& rpT) {
-  Plan pa = plan_tiles(rpA, 0), pt = plan_tiles(rpT, 1);
-  auto lenof = [&](const eqb::Tile& t) {
-    const auto& rph = t.mat ? rpT : rpA;
-    return rph[t.r0 + 1] - rph[t.r0];
-  };
+void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
+  // kind-3 groups (4 entries each) first, so every group starts on a CTA
   std::vector<eqb::Tile> sgd = pa.lng;
   sgd.insert(sgd.end(), pt.lng.begin(), pt.lng.end());
-  std::stable_sort(sgd.begin(), sgd.end(), [&](const eqb::Tile& x, const eqb::Tile& y) {
-    return lenof(x) > lenof(y);
-  });
   sgd.insert(sgd.end(), pa.slices.begin(), pa.slices.end());
   sgd.insert(sgd.end(), pt.slices.begin(), pt.slices.end());
   std::vector<eqb::Tile> ta = pa.lng, tt = pt.lng;
@@ -467,7 +520,10 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
     for (auto& x : out) x -= base;
     return out;
   };
-  build_plans(M, local_rp(rpA_host, M->a_bounds), local_rp(rpT_host, M->t_bounds));
+  const std::vector<int64_t> la = local_rp(rpA_host, M->a_bounds);
+  const std::vector<int64_t> lt = local_rp(rpT_host, M->t_bounds);
+  upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
+               plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
 }
 
 void alloc_workspaces(equil_matrix* M) {
@@ -577,6 +633,7 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     const int64_t nnz = row_ptr[m];
     require(nnz >= 0 && nnz < (1LL << 31), "ExplicitMatrix::sparse: bad nnz");
     require(nnz == 0 || (col && val), "ExplicitMatrix::sparse: null col/val");
+    PhaseTimer pt("create_csr");
     auto M = std::make_unique<equil_matrix>();
     setup_common(M.get(), cfg);
     M->m = m;
@@ -584,6 +641,7 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     M->nnz = nnz;
     DeviceGuard dg(M->device);
     cudaStream_t s = M->stream;
+    pt.mark(s, "setup");
     // full A on device (uploaded once; shards are sliced from it)
     DevBuf<int64_t> rp;
     DevBuf<int32_t> ci;
@@ -597,6 +655,17 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
       CK(cudaMemcpyAsync(va.p, val, nnz * 8, cudaMemcpyHostToDevice, s));
     }
     eqb::DevCsr fullA{m, n, nnz, rp.p, ci.p, va.p};
+    // plan CSR(A) on the host while the device validates and transposes
+    Plan planA;
+    std::thread planner;
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{planner};
+    if (M->world == 1) planner = std::thread([&] { planA = plan_tiles(row_ptr, m, 0); });
+    pt.mark(s, "upload");
     // validation (explicit_matrix.cpp:21-39 for canonical CSR)
     DevBuf<int64_t> where;
     where.alloc(2);
@@ -608,6 +677,7 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     CK(cudaMemcpyAsync(&errc, M->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&wh, where.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    pt.mark(s, "validate");
     if (errc) {
       if (errc == 1) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: malformed row_ptr at row " + std::to_string(wh));
       // locate the row of entry wh on the host
@@ -628,9 +698,11 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     tva.alloc(nnz);
     eqb::DevCsr fullT{n, m, nnz, trp.p, tci.p, tva.p};
     CK(eqb::transpose_csr(fullA, fullT, s));
-    std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1), rpT(n + 1);
+    pt.mark(s, "transpose");
+    std::vector<int64_t> rpT(n + 1);
     CK(cudaMemcpyAsync(rpT.data(), trp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    pt.mark(s, "rowptr copy");
     if (M->world == 1) {
       // adopt the full arrays as the shard (no copy)
       M->a_bounds = {0, m};
@@ -645,12 +717,17 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
       std::swap(M->t_va.p, tva.p); std::swap(M->t_va.n, tva.n);
       M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
       M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
-      build_plans(M.get(), rpA, rpT);
+      const Plan planT = plan_tiles(rpT.data(), n, 1);
+      planner.join();
+      upload_plans(M.get(), planA, planT);
     } else {
+      const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
       shard_sparse(M.get(), fullA, fullT, rpA, rpT);
     }
+    pt.mark(s, "plan");
     alloc_workspaces(M.get());
     CK(cudaStreamSynchronize(s));
+    pt.mark(s, "workspaces");
     *out = M.release();
   });
 }

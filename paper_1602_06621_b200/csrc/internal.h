@@ -19,22 +19,38 @@ struct Tile {
   int16_t kind, mat;
   int32_t pad;
 };
-constexpr int kTileNnz = 512;    // products staged per warp tile (kinds 0, 1)
+#ifndef EQ_SLICE_BATCH
+#define EQ_SLICE_BATCH 4
+#endif
+#ifndef EQ_LONG_BATCH
+#define EQ_LONG_BATCH 4
+#endif
+#ifndef EQ_LONG_THRESH
+#define EQ_LONG_THRESH 512
+#endif
+constexpr int kTileNnz = EQ_LONG_THRESH;  // longest row of a slice; longer rows: kind 3
 constexpr int kSliceChunk = 16;  // products per row per lock-step round (kind 2)
 constexpr int kSliceStride = 18; // padded row stride (doubles): conflict-free LDS.128
-constexpr int kSliceBatch = 8;   // row pairs staged per batch (loads in flight)
+constexpr int kSliceBatch = EQ_SLICE_BATCH;  // row pairs staged per batch (loads in flight)
 constexpr int kSliceRows = 32;
 constexpr int kSliceWindow = 4096;  // rows are length-sorted within windows
 constexpr int kWarpSmem = kTileNnz > 32 * kSliceStride ? kTileNnz : 32 * kSliceStride;
 constexpr int kTileWarps = 4;    // independent warps per CTA
 constexpr int kTileThreads = 32 * kTileWarps;
 
-struct SliceMeta {
-  int64_t start[32];  // chunk-aligned base of each row's CSR range
-  int32_t k0[32];     // row start relative to start
-  int32_t len[32];    // row end relative to start
+struct __align__(16) RowMeta {
+  int64_t start;  // chunk-aligned base of the row's CSR range
+  int32_t k0;     // row start relative to start
+  int32_t len;    // row end relative to start
 };
-constexpr int kTileMinBlocks = 8;   // 32 warps/SM: <= 64 registers per thread
+constexpr int kLongChunk = 64;    // products per row per round (kind 3)
+constexpr int kLongStride = 66;   // padded row stride (doubles): conflict-free LDS.128
+constexpr int kLongBatch = EQ_LONG_BATCH;  // rows per staging batch per warp
+struct SliceMeta {
+  RowMeta r[32];
+  int maxr;  // long slices: rounds of the longest row
+};
+constexpr int kTileMinBlocks = 6;   // 24 warps/SM: <= 80 registers (no spills)
 constexpr int kStageUnroll = 4;     // independent loads in flight per lane
 
 // CSR slice resident on the device (int64 row_ptr, int32 col, fp64 val).

@@ -74,15 +74,18 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
 }
 
 // One CTA per jump: W[dst0 + b] = sum_i r_i W_{p+i}, p = position of W[src0 + b].
+// The set bits of r are given as a host-expanded list of positions (uint16,
+// padded to a multiple of 8 with kJumpWords, whose window reads zeros).
 __global__ void __launch_bounds__(kMtThreads)
 mt_jump_kernel(uint64_t* __restrict__ windows, int src0, int dst0,
-               const uint64_t* __restrict__ poly) {
-  extern __shared__ uint64_t sx[];  // kJumpWords + kPolyWords
-  uint64_t* spoly = sx + kJumpWords;
+               const uint4* __restrict__ pos8, int npos8) {
+  extern __shared__ uint64_t sx[];  // kJumpWords + kN zero words
   const int tid = threadIdx.x;
   const uint64_t* src = windows + static_cast<size_t>(src0 + blockIdx.x) * mt::kN;
-  for (int j = tid; j < mt::kN; j += blockDim.x) sx[j] = src[j];
-  for (int j = tid; j < mt::kPolyWords; j += blockDim.x) spoly[j] = poly[j];
+  for (int j = tid; j < mt::kN; j += blockDim.x) {
+    sx[j] = src[j];
+    sx[kJumpWords + j] = 0;
+  }
   __syncthreads();
   for (int q = 0; q + mt::kN < kJumpWords; q += mt::kN) {
     const int j = tid;
@@ -94,16 +97,20 @@ mt_jump_kernel(uint64_t* __restrict__ windows, int src0, int dst0,
     __syncthreads();
   }
   if (tid < mt::kN) {
-    uint64_t acc = 0;
-    for (int w = 0; w < mt::kPolyWords; ++w) {
-      uint64_t word = spoly[w];
-      while (word) {
-        const int b = __ffsll(static_cast<long long>(word)) - 1;
-        word &= word - 1;
-        acc ^= sx[64 * w + b + tid];
-      }
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    const uint64_t* x = sx + tid;
+    for (int q = 0; q < npos8; ++q) {
+      const uint4 p = __ldg(pos8 + q);  // 8 positions, warp-uniform (broadcast)
+      a0 ^= x[p.x & 0xffff];
+      a1 ^= x[p.x >> 16];
+      a2 ^= x[p.y & 0xffff];
+      a3 ^= x[p.y >> 16];
+      a0 ^= x[p.z & 0xffff];
+      a1 ^= x[p.z >> 16];
+      a2 ^= x[p.w & 0xffff];
+      a3 ^= x[p.w >> 16];
     }
-    windows[static_cast<size_t>(dst0 + blockIdx.x) * mt::kN + tid] = acc;
+    windows[static_cast<size_t>(dst0 + blockIdx.x) * mt::kN + tid] = (a0 ^ a1) ^ (a2 ^ a3);
   }
 }
 
@@ -123,22 +130,24 @@ mt_gen_kernel(const uint64_t* __restrict__ windows, uint64_t seg_len,
   // local word index p (p >= 312) lives at ring[p % 624]; output k = p - 312.
   for (uint64_t base = 0; base < len; base += kPackOutputs) {
     const uint64_t blen = min(static_cast<uint64_t>(kPackOutputs), len - base);
-    for (uint64_t b = 0; b < blen; b += mt::kN) {
-      const uint64_t p0 = base + b + mt::kN;  // first word of this batch
+    for (int b = 0; b < static_cast<int>(blen); b += mt::kN) {
+      // base is a multiple of 624, so the batch's first word p0 = base + b + 312
+      // sits in ring slot 312 on even batches and slot 0 on odd ones
       const int j = tid;
+      const int s0 = ((b / mt::kN) & 1) ? 0 : mt::kN;  // slot of p0
+      const int sp = s0 + j;                             // slot of p = p0 + j
+      const int sm312 = mt::kN - s0 + j;                 // slot of p - 312
+      const int sm311 = sm312 + 1 == 2 * mt::kN ? 0 : sm312 + 1;
+      const int sm156 = sp >= mt::kM ? sp - mt::kM : sp + 2 * mt::kN - mt::kM;
       if (j < mt::kM) {
-        const uint64_t p = p0 + j;
-        const uint64_t w = mt_next(ring[(p - 312) % 624], ring[(p - 311) % 624],
-                                   ring[(p - 156) % 624]);
-        ring[p % 624] = w;
+        const uint64_t w = mt_next(ring[sm312], ring[sm311], ring[sm156]);
+        ring[sp] = w;
         sbit[b + j] = static_cast<uint8_t>(mt_temper(w) >> 63);
       }
       __syncthreads();
       if (j >= mt::kM && j < mt::kN) {
-        const uint64_t p = p0 + j;
-        const uint64_t w = mt_next(ring[(p - 312) % 624], ring[(p - 311) % 624],
-                                   ring[(p - 156) % 624]);
-        ring[p % 624] = w;
+        const uint64_t w = mt_next(ring[sm312], ring[sm311], ring[sm156]);
+        ring[sp] = w;
         sbit[b + j] = static_cast<uint8_t>(mt_temper(w) >> 63);
       }
       __syncthreads();
@@ -186,13 +195,15 @@ int choose_seg_log2(uint64_t total) {
 
 }  // namespace
 
+constexpr int kPosCap = 20000;  // >= 19937 set bits, padded to a multiple of 8
+
 size_t sign_stream_scratch_bytes(uint64_t total) {
   if (total == 0) return 0;
   const int k = choose_seg_log2(total);
   const uint64_t G = (total + (1ULL << k) - 1) >> k;
   const int levels = ceil_log2(G);
-  return (G * mt::kN + static_cast<size_t>(levels + 1) * mt::kPolyWords) *
-         sizeof(uint64_t);
+  return G * mt::kN * sizeof(uint64_t) +
+         static_cast<size_t>(levels + 1) * kPosCap * sizeof(uint16_t);
 }
 
 cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
@@ -205,21 +216,28 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
   const uint64_t G = (total + L - 1) / L;
   const int levels = ceil_log2(G);
   uint64_t* windows = static_cast<uint64_t*>(scratch);
-  uint64_t* polys = windows + G * mt::kN;
-  // host: seeding state and the jump polynomials x^(2^(k+a)) mod phi
-  static thread_local std::vector<uint64_t> host;
-  host.assign(mt::kN + static_cast<size_t>(levels) * mt::kPolyWords, 0);
-  mt::seed_state(seed, stream, host.data());
-  for (int a = 0; a < levels; ++a)
-    if (!mt::jump_poly_pow2(k + a, host.data() + mt::kN + a * mt::kPolyWords))
-      return cudaErrorUnknown;
-  EQ_CUDA_TRY(cudaMemcpyAsync(windows, host.data(), mt::kN * sizeof(uint64_t),
+  uint16_t* pos = reinterpret_cast<uint16_t*>(windows + G * mt::kN);
+  // host: seeding state and, per tree level, the set-bit positions of the
+  // jump polynomial x^(2^(k+a)) mod phi
+  static thread_local std::vector<uint64_t> seedw(mt::kN), poly(mt::kPolyWords);
+  static thread_local std::vector<uint16_t> hpos;
+  std::vector<int> npos8(levels);
+  hpos.assign(static_cast<size_t>(levels) * kPosCap, static_cast<uint16_t>(kJumpWords));
+  mt::seed_state(seed, stream, seedw.data());
+  for (int a = 0; a < levels; ++a) {
+    if (!mt::jump_poly_pow2(k + a, poly.data())) return cudaErrorUnknown;
+    uint16_t* dst = hpos.data() + static_cast<size_t>(a) * kPosCap;
+    int cnt = 0;
+    for (int i = 0; i < mt::kDegree; ++i)
+      if ((poly[i >> 6] >> (i & 63)) & 1ULL) dst[cnt++] = static_cast<uint16_t>(i);
+    npos8[a] = (cnt + 7) / 8;  // tail slots keep the zero-window sentinel
+  }
+  EQ_CUDA_TRY(cudaMemcpyAsync(windows, seedw.data(), mt::kN * sizeof(uint64_t),
                               cudaMemcpyHostToDevice, s));
   if (levels > 0)
-    EQ_CUDA_TRY(cudaMemcpyAsync(polys, host.data() + mt::kN,
-                                static_cast<size_t>(levels) * mt::kPolyWords * 8,
+    EQ_CUDA_TRY(cudaMemcpyAsync(pos, hpos.data(), hpos.size() * sizeof(uint16_t),
                                 cudaMemcpyHostToDevice, s));
-  const size_t smem = (kJumpWords + mt::kPolyWords) * sizeof(uint64_t);
+  const size_t smem = (kJumpWords + mt::kN) * sizeof(uint64_t);
   static bool attr = false;
   if (!attr) {
     EQ_CUDA_TRY(cudaFuncSetAttribute(mt_jump_kernel,
@@ -231,7 +249,9 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
     const uint64_t lo = 1ULL << a;
     const uint64_t cnt = std::min(lo, G - lo);
     mt_jump_kernel<<<static_cast<unsigned>(cnt), kMtThreads, smem, s>>>(
-        windows, 0, static_cast<int>(lo), polys + a * mt::kPolyWords); count_launch(s);
+        windows, 0, static_cast<int>(lo),
+        reinterpret_cast<const uint4*>(pos + static_cast<size_t>(a) * kPosCap), npos8[a]);
+    count_launch(s);
     EQ_CUDA_TRY(cudaGetLastError());
   }
   mt_gen_kernel<<<static_cast<unsigned>(G), kMtThreads, 0, s>>>(windows, L, total,
@@ -293,7 +313,26 @@ __global__ void iota_kernel(int32_t* v, int64_t n) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k < n) v[k] = static_cast<int32_t>(k);
 }
-__global__ void transpose_gather_kernel(const int64_t* __restrict__ rp, int64_t rows,
+// row index of every entry: each thread binary-searches the row of its first
+// entry, then walks 32 consecutive entries (streaming writes)
+constexpr int kExpand = 32;
+__global__ void expand_rows_kernel(const int64_t* __restrict__ rp, int64_t rows, int64_t nnz,
+                                   int32_t* __restrict__ rowidx) {
+  const int64_t k0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * kExpand;
+  if (k0 >= nnz) return;
+  int64_t lo = 0, hi = rows;  // rp[lo] <= k0 < rp[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rp[mid] <= k0) lo = mid; else hi = mid;
+  }
+  int64_t next = rp[lo + 1];
+  const int64_t k1 = imin64(nnz, k0 + kExpand);
+  for (int64_t k = k0; k < k1; ++k) {
+    while (k >= next) next = rp[++lo + 1];  // skips empty rows
+    rowidx[k] = static_cast<int32_t>(lo);
+  }
+}
+__global__ void transpose_gather_kernel(const int32_t* __restrict__ rowidx,
                                         const double* __restrict__ val,
                                         const int32_t* __restrict__ perm,
                                         int64_t nnz, int32_t* __restrict__ tcol,
@@ -301,13 +340,7 @@ __global__ void transpose_gather_kernel(const int64_t* __restrict__ rp, int64_t 
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (p >= nnz) return;
   const int64_t k = perm[p];
-  // row of entry k: largest i with rp[i] <= k
-  int64_t lo = 0, hi = rows;  // rp[lo] <= k < rp[hi]
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (rp[mid] <= k) lo = mid; else hi = mid;
-  }
-  tcol[p] = static_cast<int32_t>(lo);
+  tcol[p] = rowidx[k];
   tval[p] = val[k];
 }
 __global__ void transpose_rowptr_kernel(const int32_t* __restrict__ skey, int64_t nnz,
@@ -345,8 +378,12 @@ cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
       e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, A.col, keys_out, perm_in,
                                           perm_out, nnz, 0, end_bit, s);
       if (e) break;
+      // perm_in is free once the sort has run: reuse it for the row index of each entry
+      const int64_t nexp = (nnz + kExpand - 1) / kExpand;
+      expand_rows_kernel<<<static_cast<unsigned>((nexp + 255) / 256), 256, 0, s>>>(
+          A.row_ptr, A.rows, nnz, perm_in); count_launch(s);
       transpose_gather_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
-          A.row_ptr, A.rows, A.val, perm_out, nnz, AT.col, AT.val); count_launch(s);
+          perm_in, A.val, perm_out, nnz, AT.col, AT.val); count_launch(s);
       e = cudaGetLastError(); if (e) break;
     }
     transpose_rowptr_kernel<<<static_cast<unsigned>((nnz + 1 + 255) / 256), 256, 0, s>>>(
@@ -469,6 +506,79 @@ __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
 // chains of others.  kind 0: every lane sums whole rows of the tile; kind 1: a
 // row longer than a tile is staged chunk by chunk and lane 0 carries the
 // running sum across chunks (the order stays the CSR order).
+//
+// kind 3 (run_long_slice) is CTA-cooperative: the 4 warps of a CTA own the same
+// "long slice" of up to 32 rows longer than kTileNnz (length-sorted).  Each
+// round all 128 threads stage the next kLongChunk products of every active row
+// (coalesced, aligned chunks) into a padded [32][kLongStride] buffer, then warp
+// 0's 32 lanes each extend one row's sequential sum with conflict-free 16-byte
+// reads -- 32 chains in parallel instead of one lane-0 chain per warp.
+template <class Epi>
+__device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __restrict__ rp,
+                                               const int32_t* __restrict__ ci,
+                                               const double* __restrict__ va,
+                                               const double* __restrict__ xg,
+                                               const int32_t* __restrict__ rowlist,
+                                               double* sp, SliceMeta& sm, Epi& epi) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cnt = t.r1;
+  int myrow = -1, mk0 = 0, mlen = 0, rounds = 0;
+  if (warp == 0) {
+    myrow = lane < cnt ? rowlist[t.r0 + lane] : -1;
+    const int64_t k0 = myrow >= 0 ? rp[myrow] : 0;
+    const int64_t k1 = myrow >= 0 ? rp[myrow + 1] : 0;
+    const int64_t kb = k0 & ~static_cast<int64_t>(kLongChunk - 1);
+    rounds = k1 > k0 ? static_cast<int>((k1 - kb + kLongChunk - 1) / kLongChunk) : 0;
+    mk0 = static_cast<int>(k0 - kb);
+    mlen = static_cast<int>(k1 - kb);
+    sm.r[lane] = RowMeta{kb, mk0, mlen};
+    const int maxr = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(rounds)));
+    if (lane == 0) sm.maxr = maxr;
+  }
+  __syncthreads();
+  const int maxr = sm.maxr;
+  double acc = 0.0;
+  for (int b = 0; b < maxr; ++b) {
+    const int off = b * kLongChunk;
+    // warp w stages rows w, w+4, ... : 2 products per lane per row
+#pragma unroll 1
+    for (int q0 = warp; q0 < cnt; q0 += 4 * kLongBatch) {
+      int32_t c[2 * kLongBatch];
+      double v[2 * kLongBatch];
+      bool ok[2 * kLongBatch];
+#pragma unroll
+      for (int u = 0; u < kLongBatch; ++u) {
+        const int q = q0 + 4 * u;
+        RowMeta rm{0, 1, 0};
+        if (q < cnt) rm = sm.r[q];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rel = off + lane + 32 * h;
+          const int i = 2 * u + h;
+          ok[i] = rel >= rm.k0 && rel < rm.len;
+          if (ok[i]) {
+            c[i] = ld_na(ci + rm.start + rel);
+            v[i] = ld_na(va + rm.start + rel);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kLongBatch; ++u)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (ok[2 * u + h])
+            sp[(q0 + 4 * u) * kLongStride + lane + 32 * h] =
+                __dmul_rn(v[2 * u + h], __ldg(xg + c[2 * u + h]));
+    }
+    __syncthreads();
+    if (warp == 0 && rounds > b)
+      acc = chain_sum(acc, sp + lane * kLongStride, max(0, mk0 - off),
+                      min(kLongChunk, mlen - off));
+    __syncthreads();
+  }
+  if (warp == 0 && myrow >= 0) epi(myrow, acc);
+}
+
 template <class Epi>
 __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restrict__ rp,
                                          const int32_t* __restrict__ ci,
@@ -491,9 +601,8 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
     const int64_t k1 = myrow >= 0 ? rp[myrow + 1] : 0;
     const int64_t kb = k0 & ~static_cast<int64_t>(kSliceChunk - 1);
     const int rounds = k1 > k0 ? static_cast<int>((k1 - kb + kSliceChunk - 1) / kSliceChunk) : 0;
-    sm.start[lane] = kb;
-    sm.k0[lane] = static_cast<int32_t>(k0 - kb);
-    sm.len[lane] = static_cast<int32_t>(k1 - kb);
+    const int mk0 = static_cast<int>(k0 - kb), mlen = static_cast<int>(k1 - kb);
+    sm.r[lane] = RowMeta{kb, mk0, mlen};
     const int maxr = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(rounds)));
     __syncwarp();
     const int half = lane >> 4, e = lane & 15;
@@ -510,9 +619,11 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
         for (int u = 0; u < kSliceBatch; ++u) {
           const int q = q0 + 2 * u + half;
           const int rel = off + e;  // position relative to the row's aligned base
-          ok[u] = q < act && rel >= sm.k0[q] && rel < sm.len[q];
+          RowMeta rm{0, 1, 0};
+          if (q < act) rm = sm.r[q];  // one 16-byte shared load per row chunk
+          ok[u] = rel >= rm.k0 && rel < rm.len;
           if (ok[u]) {
-            const int64_t k = sm.start[q] + rel;
+            const int64_t k = rm.start + rel;
             c[u] = ld_na(ci + k);
             v[u] = ld_na(va + k);
           }
@@ -525,8 +636,8 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
       }
       __syncwarp();
       if (rounds > b) {
-        const int lo = max(0, sm.k0[lane] - off);
-        const int hi = min(kSliceChunk, sm.len[lane] - off);
+        const int lo = max(0, mk0 - off);
+        const int hi = min(kSliceChunk, mlen - off);
         acc = chain_sum(acc, sp + lane * kSliceStride, lo, hi);
       }
       __syncwarp();
@@ -561,7 +672,8 @@ struct SgdEpi {
   __device__ void operator()(int64_t r, double acc) { sgd_epilogue(a, mat, r, acc, fl); }
 };
 
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+template <int MINB>
+__global__ void __launch_bounds__(kTileThreads, MINB)
 sgd_iter_kernel(const SgdIterArgs a, int ntiles) {
   __shared__ __align__(16) double sp[kTileWarps][kWarpSmem];
   __shared__ SliceMeta sm[kTileWarps];
@@ -571,8 +683,12 @@ sgd_iter_kernel(const SgdIterArgs a, int ntiles) {
   const Tile t = a.tiles[tid];
   const int mat = t.mat;
   SgdEpi epi{a, mat, 0u};
-  run_tile(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur, a.rl[mat],
-           sp[warp], sm[warp], lane, epi);
+  if (t.kind == 3)  // CTA-cooperative (all 4 warps hold this tile)
+    run_long_slice(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
+                   a.rl[mat], &sp[0][0], sm[0], epi);
+  else
+    run_tile(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur, a.rl[mat],
+             sp[warp], sm[warp], lane, epi);
   if (epi.fl) atomicOr(a.flags, epi.fl);
 }
 
@@ -618,7 +734,23 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
 
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  sgd_iter_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles); count_launch(s);
+  // occupancy variant (CTAs/SM bound); EQUIL_MINB selects one for tuning runs
+  static const int minb = [] {
+    const char* e = getenv("EQUIL_MINB");
+    return e ? atoi(e) : kTileMinBlocks;
+  }();
+  const unsigned grid = (ntiles + kTileWarps - 1) / kTileWarps;
+  if (minb >= 12)
+    sgd_iter_kernel<12><<<grid, kTileThreads, 0, s>>>(a, ntiles);
+  else if (minb >= 10)
+    sgd_iter_kernel<10><<<grid, kTileThreads, 0, s>>>(a, ntiles);
+  else if (minb >= 8)
+    sgd_iter_kernel<8><<<grid, kTileThreads, 0, s>>>(a, ntiles);
+  else if (minb <= 4)
+    sgd_iter_kernel<4><<<grid, kTileThreads, 0, s>>>(a, ntiles);
+  else
+    sgd_iter_kernel<6><<<grid, kTileThreads, 0, s>>>(a, ntiles);
+  count_launch(s);
   return cudaGetLastError();
 }
 
@@ -668,7 +800,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) pass_kernel(cons
   const int tid = blockIdx.x * kTileWarps + warp;
   if (tid >= ntiles) return;
   PassEpi epi{a};
-  run_tile(a.tiles[tid], a.rp, a.ci, a.va, a.xg, a.rl, sp[warp], sm[warp], lane, epi);
+  const Tile t = a.tiles[tid];
+  if (t.kind == 3)
+    run_long_slice(t, a.rp, a.ci, a.va, a.xg, a.rl, &sp[0][0], sm[0], epi);
+  else
+    run_tile(t, a.rp, a.ci, a.va, a.xg, a.rl, sp[warp], sm[warp], lane, epi);
 }
 
 }  // namespace
