@@ -741,7 +741,7 @@ equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowma
     require(rowmajor != nullptr, "ExplicitMatrix::dense: null data");
     require(cfg == nullptr || cfg->world_size <= 1,
             "ExplicitMatrix::dense: the dense path runs on one GPU");
-    require(n <= static_cast<int64_t>(eqb::kChunk) * 4096, "dense: n too large");
+    require(n <= static_cast<int64_t>(eqb::kChunk) * 32, "dense: n too large (<= 65536)");
     require((m + eqb::kChunk - 1) / eqb::kChunk <= 64, "dense: m too large (<= 131072)");
     auto M = std::make_unique<equil_matrix>();
     setup_common(M.get(), cfg);

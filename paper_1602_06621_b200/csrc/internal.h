@@ -117,6 +117,7 @@ struct LsqrDev {
 // -------------------- launchers (kernels.cu) ------------------------------
 void note_launches(long long n);
 long long launch_count();
+void count_launch(cudaStream_t s, int n = 1);  // skipped while s is capturing
 cudaError_t launch_validate_csr(const DevCsr& A, int* err, int64_t* where,
                                 cudaStream_t s);
 cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s);

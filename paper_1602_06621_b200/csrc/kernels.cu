@@ -33,7 +33,7 @@ __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) {
 static std::atomic<long long> g_launches{0};
 void note_launches(long long n) { g_launches += n; }
 long long launch_count() { return g_launches.load(); }
-static void count_launch(cudaStream_t s, int n = 1) {
+void count_launch(cudaStream_t s, int n) {
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
     cudaGetLastError();
@@ -934,207 +934,6 @@ cudaError_t launch_lsqr_xw_update(double* x, double* w, const double* v,
   if (n == 0) return cudaSuccess;
   lsqr_xw_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, w, v, c1, c2,
                                                                         e, ex, n); count_launch(s);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// K5: dense GEMV pair in the canonical order (row-major A)
-//   rows: y_i = canon_j A_ij x_j      one CTA per row
-//   cols: z_j = canon_i A_ij w_i      CTA per (32-column strip, 2048-row chunk)
-// ---------------------------------------------------------------------------
-namespace {
-
-// level 1+2 canonical dot of row i with x; valid in thread 0 (blockDim 256)
-__device__ double dense_row_dot(const double* __restrict__ Arow,
-                                const double* __restrict__ x, int64_t n,
-                                double* s, double* part) {
-  const int l = threadIdx.x;
-  const int64_t nc = (n + kChunk - 1) / kChunk;
-  for (int64_t c = 0; c < nc; ++c) {
-    const int64_t base = c * kChunk;
-    const int64_t clen = imin64(kChunk, n - base);
-    double acc = 0.0;
-    for (int64_t k = l; k < clen; k += kLanes1)
-      acc = __dadd_rn(acc, __dmul_rn(__ldcs(Arow + base + k), __ldg(x + base + k)));
-    s[l] = acc;
-    __syncthreads();
-    const double p = block_fold(s, kLanes1);
-    if (l == 0) part[c] = p;
-    __syncthreads();
-  }
-  if (nc == 1) return part[0];
-  for (int q = l; q < kLanes2; q += blockDim.x) {
-    double a2 = 0.0;
-    for (int64_t k = q; k < nc; k += kLanes2) a2 = __dadd_rn(a2, part[k]);
-    s[q] = a2;
-  }
-  __syncthreads();
-  return block_fold(s, kLanes2);
-}
-
-constexpr int kMaxDenseChunks = 4096;  // n <= 2048 * 4096
-
-__global__ void __launch_bounds__(256)
-dense_sgd_rows_kernel(const DenseIterArgs a) {
-  __shared__ double s[kLanes2];
-  __shared__ double part[kMaxDenseChunks];
-  const int64_t i = blockIdx.x;
-  const double acc = dense_row_dot(a.A + i * a.n, a.xs_cur, a.n, s, part);
-  if (threadIdx.x == 0) {
-    unsigned fl = 0;
-    const double d = fabs(a.xw_cur[i]);
-    const double y = __dmul_rn(d, acc);
-    const double est = __dmul_rn(y, y);
-    double avg = a.ub[i];
-    const double xn = sgd_coord(est, a.u[i], a.cu, a.st, avg, fl);
-    a.u[i] = xn;
-    a.ub[i] = avg;
-    if (a.has_next) {
-      const double dn = det_exp(xn);
-      a.xw_next[i] = sign_bit(a.signs, a.sign_next_w + i) ? dn : -dn;
-    }
-    if (fl) atomicOr(a.flags, fl);
-  }
-}
-
-// partial column sums of one (strip, chunk): colpart[c * n + j]
-__global__ void __launch_bounds__(256)
-dense_cols_partial_kernel(const double* __restrict__ A, int64_t m, int64_t n,
-                          const double* __restrict__ w, double* __restrict__ colpart) {
-  extern __shared__ double sc[];  // [kLanes1][32]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + lane;
-  const int64_t c = blockIdx.y;
-  const int64_t base = c * kChunk;
-  const int64_t clen = imin64(kChunk, m - base);
-  for (int q = 0; q < kLanes1 / 8; ++q) {
-    const int l = warp + 8 * q;
-    double acc = 0.0;
-    if (j < n)
-      for (int64_t k = l; k < clen; k += kLanes1)
-        acc = __dadd_rn(acc, __dmul_rn(__ldcs(A + (base + k) * n + j), __ldg(w + base + k)));
-    sc[l * 32 + lane] = acc;
-  }
-  __syncthreads();
-  for (int h = kLanes1 / 2; h >= 1; h >>= 1) {
-    for (int e = threadIdx.x; e < h * 32; e += blockDim.x) {
-      const int l = e >> 5, cc = e & 31;
-      sc[l * 32 + cc] = __dadd_rn(sc[l * 32 + cc], sc[(l + h) * 32 + cc]);
-    }
-    __syncthreads();
-  }
-  if (warp == 0 && j < n) colpart[c * n + j] = sc[lane];
-}
-
-// level 2 over chunk partials for column j, serial emulation of the 1024-lane fold
-__device__ double dense_col_level2(const double* colpart, int64_t nc, int64_t n,
-                                   int64_t j) {
-  if (nc == 1) return colpart[j];
-  // nc <= 64 (enforced at matrix creation): lanes >= nc are +0.0, so the
-  // 1024-lane fold equals the fold over the next power of two >= nc
-  double s[64];
-  int lanes = 1;
-  while (lanes < nc) lanes <<= 1;
-  for (int q = 0; q < lanes; ++q) {
-    double a2 = 0.0;
-    for (int64_t k = q; k < nc; k += kLanes2) a2 = __dadd_rn(a2, colpart[k * n + j]);
-    s[q] = a2;
-  }
-  for (int h = lanes / 2; h >= 1; h >>= 1)
-    for (int q = 0; q < h; ++q) s[q] = __dadd_rn(s[q], s[q + h]);
-  return s[0];
-}
-
-__global__ void dense_sgd_cols_final_kernel(const DenseIterArgs a) {
-  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (j >= a.n) return;
-  const int64_t nc = (a.m + kChunk - 1) / kChunk;
-  const double acc = dense_col_level2(a.colpart, nc, a.n, j);
-  unsigned fl = 0;
-  const double e = fabs(a.xs_cur[j]);
-  const double z = __dmul_rn(e, acc);
-  const double est = __dmul_rn(z, z);
-  double avg = a.vb[j];
-  const double xn = sgd_coord(est, a.v[j], a.cv, a.st, avg, fl);
-  a.v[j] = xn;
-  a.vb[j] = avg;
-  if (a.has_next) {
-    const double dn = det_exp(xn);
-    a.xs_next[j] = sign_bit(a.signs, a.sign_next_s + j) ? dn : -dn;
-  }
-  if (fl) atomicOr(a.flags, fl);
-}
-
-__device__ __forceinline__ void dense_pass_epi(const DensePassArgs& a, int64_t r,
-                                               double acc) {
-  switch (a.mode) {
-    case kPassPlain: a.out[r] = acc; break;
-    case kPassLsqrU:
-    case kPassLsqrV: {
-      const double bv = a.scale ? __dmul_rn(a.scale[r], acc) : acc;
-      a.out[r] = __dsub_rn(bv, __dmul_rn(*a.coef, a.prev[r]));
-      break;
-    }
-    case kPassResid: a.out[r] = __dsub_rn(a.prev[r], acc); break;
-    case kPassScaled: a.out[r] = a.scale ? __dmul_rn(a.scale[r], acc) : acc; break;
-  }
-}
-
-__global__ void __launch_bounds__(256) dense_pass_rows_kernel(const DensePassArgs a) {
-  __shared__ double s[kLanes2];
-  __shared__ double part[kMaxDenseChunks];
-  if (a.skip && *a.skip) return;
-  const int64_t i = blockIdx.x;
-  const double acc = dense_row_dot(a.A + i * a.n, a.xg, a.n, s, part);
-  if (threadIdx.x == 0) dense_pass_epi(a, i, acc);
-}
-
-__global__ void dense_pass_cols_final_kernel(const DensePassArgs a) {
-  if (a.skip && *a.skip) return;
-  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (j >= a.n) return;
-  const int64_t nc = (a.m + kChunk - 1) / kChunk;
-  dense_pass_epi(a, j, dense_col_level2(a.colpart, nc, a.n, j));
-}
-
-}  // namespace
-
-static cudaError_t dense_cols_partial(const double* A, int64_t m, int64_t n,
-                                      const double* w, double* colpart, cudaStream_t s) {
-  const size_t smem = kLanes1 * 32 * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    EQ_CUDA_TRY(cudaFuncSetAttribute(dense_cols_partial_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-    attr = true;
-  }
-  const dim3 grid(static_cast<unsigned>((n + 31) / 32),
-                  static_cast<unsigned>((m + kChunk - 1) / kChunk));
-  dense_cols_partial_kernel<<<grid, 256, smem, s>>>(A, m, n, w, colpart); count_launch(s);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s) {
-  if (a.n > static_cast<int64_t>(kChunk) * kMaxDenseChunks) return cudaErrorInvalidValue;
-  dense_sgd_rows_kernel<<<static_cast<unsigned>(a.m), 256, 0, s>>>(a); count_launch(s);
-  EQ_CUDA_TRY(cudaGetLastError());
-  EQ_CUDA_TRY(dense_cols_partial(a.A, a.m, a.n, a.xw_cur, a.colpart, s));
-  dense_sgd_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a); count_launch(s);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s) {
-  if (!a.adjoint) {
-    if (a.n > static_cast<int64_t>(kChunk) * kMaxDenseChunks) return cudaErrorInvalidValue;
-    dense_pass_rows_kernel<<<static_cast<unsigned>(a.m), 256, 0, s>>>(a); count_launch(s);
-    return cudaGetLastError();
-  }
-  // A^T y: columns of the row-major m x n matrix
-  EQ_CUDA_TRY(dense_cols_partial(a.A, a.m, a.n, a.xg, a.colpart, s));
-  DensePassArgs b = a;
-  b.m = a.m;
-  dense_pass_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(b); count_launch(s);
   return cudaGetLastError();
 }
 
