@@ -338,6 +338,7 @@ struct equil_matrix {
   DevBuf<eqb::Tile> tiles_sgd, tiles_a, tiles_t;
   DevBuf<int32_t> rowlist_a, rowlist_t;
   int n_sgd = 0, n_a = 0, n_t = 0;
+  int n_sgd_long = 0;  // leading kind-3 entries of tiles_sgd
 
   // dense
   DevBuf<double> Ad, colpart;
@@ -445,6 +446,7 @@ void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
     return static_cast<int>(h.size());
   };
   M->n_sgd = upload(M->tiles_sgd, sgd);
+  M->n_sgd_long = static_cast<int>(pa.lng.size() + pt.lng.size());
   M->n_a = upload(M->tiles_a, ta);
   M->n_t = upload(M->tiles_t, tt);
   upload(M->rowlist_a, pa.rowlist);
@@ -928,6 +930,7 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
         a.rl[k] = k ? M->rowlist_t.p : M->rowlist_a.p;
       }
       a.tiles = M->tiles_sgd.p;
+      a.n_long = M->n_sgd_long;
       a.xs_cur = M->xs[(t - 1) & 1].p;
       a.xw_cur = M->xw[(t - 1) & 1].p;
       a.xs_next = M->xs[t & 1].p;

@@ -67,6 +67,7 @@ struct SgdIterArgs {
   const double* va[2];
   const int32_t* rl[2];  // slice row lists
   const Tile* tiles;
+  int n_long;            // leading kind-3 entries of tiles
   const double* xs_cur;  // gathered e.*s (n, padded coords)
   const double* xw_cur;  // gathered d.*w (m, padded coords)
   double* xs_next;

@@ -672,21 +672,23 @@ struct SgdEpi {
   __device__ void operator()(int64_t r, double acc) { sgd_epilogue(a, mat, r, acc, fl); }
 };
 
-template <int MINB>
+// KINDS: bit 0 = warp tiles (kinds 0-2), bit 1 = CTA long slices (kind 3);
+// tile_base offsets into the tile list (for launches over a sub-range).
+template <int MINB, int KINDS>
 __global__ void __launch_bounds__(kTileThreads, MINB)
-sgd_iter_kernel(const SgdIterArgs a, int ntiles) {
+sgd_iter_kernel(const SgdIterArgs a, int tile_base, int ntiles) {
   __shared__ __align__(16) double sp[kTileWarps][kWarpSmem];
   __shared__ SliceMeta sm[kTileWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = blockIdx.x * kTileWarps + warp;
   if (tid >= ntiles) return;
-  const Tile t = a.tiles[tid];
+  const Tile t = a.tiles[tile_base + tid];
   const int mat = t.mat;
   SgdEpi epi{a, mat, 0u};
-  if (t.kind == 3)  // CTA-cooperative (all 4 warps hold this tile)
+  if ((KINDS & 2) && t.kind == 3)  // CTA-cooperative (all 4 warps hold this tile)
     run_long_slice(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
                    a.rl[mat], &sp[0][0], sm[0], epi);
-  else
+  else if (KINDS & 1)
     run_tile(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur, a.rl[mat],
              sp[warp], sm[warp], lane, epi);
   if (epi.fl) atomicOr(a.flags, epi.fl);
@@ -735,22 +737,33 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
   // occupancy variant (CTAs/SM bound); EQUIL_MINB selects one for tuning runs
-  static const int minb = [] {
-    const char* e = getenv("EQUIL_MINB");
-    return e ? atoi(e) : kTileMinBlocks;
-  }();
-  const unsigned grid = (ntiles + kTileWarps - 1) / kTileWarps;
-  if (minb >= 12)
-    sgd_iter_kernel<12><<<grid, kTileThreads, 0, s>>>(a, ntiles);
-  else if (minb >= 10)
-    sgd_iter_kernel<10><<<grid, kTileThreads, 0, s>>>(a, ntiles);
-  else if (minb >= 8)
-    sgd_iter_kernel<8><<<grid, kTileThreads, 0, s>>>(a, ntiles);
-  else if (minb <= 4)
-    sgd_iter_kernel<4><<<grid, kTileThreads, 0, s>>>(a, ntiles);
+  // tuning knobs (development): EQUIL_SPLIT=1 launches the CTA long slices and
+  // the warp tiles as two kernels with their own occupancy points
+  static const int split = getenv("EQUIL_SPLIT") ? atoi(getenv("EQUIL_SPLIT")) : 0;
+  static const int minb_s = getenv("EQUIL_MINB_S") ? atoi(getenv("EQUIL_MINB_S")) : 8;
+  static const int minb_l = getenv("EQUIL_MINB_L") ? atoi(getenv("EQUIL_MINB_L")) : 6;
+  auto grid = [](int n) { return static_cast<unsigned>((n + kTileWarps - 1) / kTileWarps); };
+  if (!split || a.n_long == 0 || a.n_long == ntiles) {
+    sgd_iter_kernel<kTileMinBlocks, 3><<<grid(ntiles), kTileThreads, 0, s>>>(a, 0, ntiles);
+    count_launch(s);
+    return cudaGetLastError();
+  }
+  const int nl = a.n_long, ns = ntiles - a.n_long;
+  if (minb_l >= 8)
+    sgd_iter_kernel<8, 2><<<grid(nl), kTileThreads, 0, s>>>(a, 0, nl);
+  else if (minb_l <= 4)
+    sgd_iter_kernel<4, 2><<<grid(nl), kTileThreads, 0, s>>>(a, 0, nl);
   else
-    sgd_iter_kernel<6><<<grid, kTileThreads, 0, s>>>(a, ntiles);
-  count_launch(s);
+    sgd_iter_kernel<6, 2><<<grid(nl), kTileThreads, 0, s>>>(a, 0, nl);
+  if (minb_s >= 12)
+    sgd_iter_kernel<12, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
+  else if (minb_s >= 10)
+    sgd_iter_kernel<10, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
+  else if (minb_s >= 8)
+    sgd_iter_kernel<8, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
+  else
+    sgd_iter_kernel<6, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
+  count_launch(s, 2);
   return cudaGetLastError();
 }
 

@@ -273,3 +273,59 @@ def test_errors_mirror_reference():
         eq.sgd_equilibrate(M, eq.EquilibrationParams(alpha=1.0, beta=2.0, iterations=1))
     with pytest.raises(eq.InvalidArgument, match="nonnegative"):
         eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=-1))
+
+
+# ---------------------------------------------------------------- larger scales
+def test_sgd_scaled_config3_bit_exact(C):
+    """c3's generator at 2% scale (40000 x 20000, Zipf rows up to 1e4: long-row
+    CTA slices, slices, empty columns) -- full trajectory bit-exact."""
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(3, scale=0.02)
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    assert np.diff(inst.row_ptr).max() > 2048
+    want = C.sgd_equilibrate(A, iterations=20, seed=7)
+    got = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(iterations=20, seed=7))
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert (got.box_feasible, got.iterate_bound_ok) == (want.box_feasible, want.iterate_bound_ok)
+
+
+def test_lsqr_config1_bit_exact(C):
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(1)
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    b = configs.rhs(inst)
+    M = device_matrix(A)
+    run = eq.lsqr(M, b, 25, 0.0)
+    ref = C.lsqr(A, b, 25, 0.0)
+    assert np.array_equal(np.array(run.residual_history), ref.residual_history)
+    assert np.array_equal(run.x, ref.x)
+    pre = eq.lsqr_preconditioned(M, b, eq.EquilibrationParams(iterations=10, seed=2), 25, 0.0)
+    pref = C.lsqr_preconditioned(A, b, 25, 0.0, iterations=10, seed=2)
+    assert np.array_equal(np.array(pre.residual_history), pref.residual_history)
+    assert np.array_equal(pre.x, pref.x)
+    assert (pre.apply_count, pre.adjoint_count) == (pref.apply_count, pref.adjoint_count)
+
+
+def test_full_size_config3_properties(C):
+    """BASELINE size (2e6 x 1e6, nnz 1.5e8): size-independent properties --
+    bit-for-bit determinism across handles and entry points, d = det_exp(u)
+    exactly, the box, and the reference's flags."""
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(3)
+    p = eq.EquilibrationParams(iterations=5, seed=0)
+    M = eq.ExplicitMatrix.from_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    r1 = eq.sgd_equilibrate(M, p)
+    r2 = eq.sgd_equilibrate(M, p)
+    r3 = eq.sgd_equilibrate_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val, p)
+    for k in "uvde":
+        assert np.array_equal(getattr(r1, k), getattr(r2, k))
+        assert np.array_equal(getattr(r1, k), getattr(r3, k))
+    idx = np.random.default_rng(0).integers(0, inst.m, 20000)
+    assert np.array_equal(r1.d[idx], C.det_exp(r1.u[idx]))
+    assert np.abs(r1.u).max() <= p.max_log_scale and np.abs(r1.v).max() <= p.max_log_scale
+    assert r1.box_feasible and r1.iterate_bound_ok
+    # the transpose of the full matrix is a permutation of A's entries by column
+    trp, tc, tv = M.transposed_csr()
+    assert trp[-1] == inst.nnz and np.all(np.diff(trp) >= 0)
+    assert np.array_equal(np.diff(trp), np.bincount(inst.col, minlength=inst.n))

@@ -32,6 +32,25 @@ def main():
     res = {}
     for k in which:
         k = int(k)
+        if k == 4:  # LSQR on c3 (config 4): per-iteration time, plain and preconditioned
+            inst = configs.config(4)
+            b = configs.rhs(inst)
+            M = eq.ExplicitMatrix.from_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+            out = {}
+            for name, fn in [("lsqr", lambda it: eq.lsqr(M, b, it, 0.0)),
+                             ("lsqr_pre", lambda it: eq.lsqr_preconditioned(
+                                 M, b, eq.EquilibrationParams(iterations=50), it, 0.0))]:
+                fn(5)
+                t0 = time.perf_counter()
+                r10 = fn(10)
+                t1 = time.perf_counter()
+                r110 = fn(110)
+                t2 = time.perf_counter()
+                out[name] = {"ms_per_lsqr_iter": ((t2 - t1) - (t1 - t0)) / 100 * 1e3,
+                             "final_residual_110": r110.residual_history[-1]}
+            print(json.dumps({4: out}), flush=True)
+            del M
+            continue
         t0 = time.time()
         inst = configs.config(k)
         tg = time.time() - t0
