@@ -118,6 +118,13 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
                                      const int32_t* col, const double* val,
                                      const equil_device_cfg* cfg,
                                      equil_matrix** out);
+/* ExplicitMatrix::sparse(rows, cols, entries) (src/explicit_matrix.cpp:19-57)
+ * from COO triplets in any order, on device: range check in input order, sort
+ * by (row, col), duplicate rejection in sorted order (same messages), CSR. */
+equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz,
+                                     const int64_t* rows, const int64_t* cols,
+                                     const double* vals, const equil_device_cfg* cfg,
+                                     equil_matrix** out);
 /* ExplicitMatrix::dense (src/explicit_matrix.cpp:8-17); input row-major. */
 equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowmajor,
                                        const equil_device_cfg* cfg,

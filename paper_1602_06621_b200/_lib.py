@@ -61,6 +61,8 @@ SIGNATURES = {
     "equil_validate_params": (C.c_int, [C.POINTER(Params)]),
     "equil_matrix_create_csr": (C.c_int, [C.c_int64, C.c_int64, _i64p, _i32p, _dp,
                                           C.POINTER(DeviceCfg), C.POINTER(C.c_void_p)]),
+    "equil_matrix_create_coo": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, _dp,
+                                          C.POINTER(DeviceCfg), C.POINTER(C.c_void_p)]),
     "equil_matrix_create_dense": (C.c_int, [C.c_int64, C.c_int64, _dp,
                                             C.POINTER(DeviceCfg), C.POINTER(C.c_void_p)]),
     "equil_matrix_destroy": (None, [C.c_void_p]),

@@ -147,36 +147,24 @@ class ExplicitMatrix:
     @staticmethod
     def sparse(rows: int, cols: int, entries, device: int = 0):
         """ExplicitMatrix::sparse (src/explicit_matrix.cpp:19-57): entries are
-        (row, col, value) triples in any order; range check, sort by (row, col),
-        duplicate rejection, then CSR."""
-        if not (rows > 0 and cols > 0):
-            raise InvalidArgument("ExplicitMatrix::sparse: dimensions must be positive")
+        (row, col, value) triples in any order (or a (rows, cols, vals) tuple of
+        arrays).  On the device: range check in input order, sort by (row, col),
+        duplicate rejection in sorted order, CSR, then CSR(A^T)."""
         if isinstance(entries, tuple) and len(entries) == 3 and hasattr(entries[0], "__len__"):
-            r = np.asarray(entries[0], dtype=np.int64)
-            c = np.asarray(entries[1], dtype=np.int64)
-            v = np.asarray(entries[2], dtype=np.float64)
+            r = np.ascontiguousarray(entries[0], dtype=np.int64)
+            c = np.ascontiguousarray(entries[1], dtype=np.int64)
+            v = np.ascontiguousarray(entries[2], dtype=np.float64)
         else:
             ent = list(entries)
             r = np.array([e[0] for e in ent], dtype=np.int64)
             c = np.array([e[1] for e in ent], dtype=np.int64)
             v = np.array([e[2] for e in ent], dtype=np.float64)
-        bad = (r < 0) | (r >= rows) | (c < 0) | (c >= cols)
-        if bad.any():
-            k = int(np.argmax(bad))
-            raise InvalidArgument(
-                f"ExplicitMatrix::sparse: entry ({r[k]}, {c[k]}) out of range")
-        order = np.lexsort((c, r))
-        r, c, v = r[order], c[order], v[order]
-        if r.size > 1:
-            dup = (r[1:] == r[:-1]) & (c[1:] == c[:-1])
-            if dup.any():
-                k = int(np.argmax(dup)) + 1
-                raise InvalidArgument(
-                    f"ExplicitMatrix::sparse: duplicate entry ({r[k]}, {c[k]})")
-        rp = np.zeros(rows + 1, dtype=np.int64)
-        np.add.at(rp, r + 1, 1)
-        rp = np.cumsum(rp)
-        return ExplicitMatrix.from_csr(rows, cols, rp, c.astype(np.int32), v, device)
+        cfg = L.DeviceCfg(device, 0, 1, None)
+        h = C.c_void_p()
+        _check(L.load().equil_matrix_create_coo(rows, cols, r.size, L.ptr(r, L._i64p),
+                                                L.ptr(c, L._i64p), L.ptr(v, L._dp),
+                                                C.byref(cfg), C.byref(h)))
+        return ExplicitMatrix(h, rows, cols, int(r.size), False)
 
     @staticmethod
     def dense(values, device: int = 0):

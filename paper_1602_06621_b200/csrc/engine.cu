@@ -528,6 +528,60 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
                plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
 }
 
+void alloc_workspaces(equil_matrix* M);
+
+// From a validated device CSR(A) (ownership taken) and its host row_ptr: build
+// CSR(A^T) on device (K2), plan the traversal (planA may already be running on
+// `planner`), shard for world_size > 1, allocate workspaces.
+void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
+                   DevBuf<double>& va, const int64_t* row_ptr, PhaseTimer& pt, Plan* planA,
+                   std::thread* planner) {
+  const int64_t m = M->m, n = M->n, nnz = M->nnz;
+  cudaStream_t s = M->stream;
+  eqb::DevCsr fullA{m, n, nnz, rp.p, ci.p, va.p};
+  DevBuf<int64_t> trp;
+  DevBuf<int32_t> tci;
+  DevBuf<double> tva;
+  trp.alloc(n + 1);
+  tci.alloc(nnz);
+  tva.alloc(nnz);
+  eqb::DevCsr fullT{n, m, nnz, trp.p, tci.p, tva.p};
+  CK(eqb::transpose_csr(fullA, fullT, s));
+  pt.mark(s, "transpose");
+  std::vector<int64_t> rpT(n + 1);
+  CK(cudaMemcpyAsync(rpT.data(), trp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  pt.mark(s, "rowptr copy");
+  if (M->world == 1) {
+    // adopt the full arrays as the shard (no copy)
+    M->a_bounds = {0, m};
+    M->t_bounds = {0, n};
+    M->a_max = m;
+    M->t_max = n;
+    std::swap(M->a_rp.p, rp.p); std::swap(M->a_rp.n, rp.n);
+    std::swap(M->a_ci.p, ci.p); std::swap(M->a_ci.n, ci.n);
+    std::swap(M->a_va.p, va.p); std::swap(M->a_va.n, va.n);
+    std::swap(M->t_rp.p, trp.p); std::swap(M->t_rp.n, trp.n);
+    std::swap(M->t_ci.p, tci.p); std::swap(M->t_ci.n, tci.n);
+    std::swap(M->t_va.p, tva.p); std::swap(M->t_va.n, tva.n);
+    M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
+    M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
+    const Plan planT = plan_tiles(rpT.data(), n, 1);
+    if (planner && planner->joinable()) planner->join();
+    if (planA)  // computed concurrently by the caller
+      upload_plans(M, *planA, planT);
+    else
+      upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
+  } else {
+    const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
+    shard_sparse(M, fullA, fullT, rpA, rpT);
+  }
+  pt.mark(s, "plan");
+  alloc_workspaces(M);
+  CK(cudaStreamSynchronize(s));
+  pt.mark(s, "workspaces");
+}
+
 void alloc_workspaces(equil_matrix* M) {
   const int64_t np = M->n_pad(), mp = M->m_pad();
   M->xbuf.alloc(2 * (np + mp));
@@ -634,6 +688,11 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     require(n < (1LL << 31) && m < (1LL << 31), "ExplicitMatrix::sparse: dimension too large");
     const int64_t nnz = row_ptr[m];
     require(nnz >= 0 && nnz < (1LL << 31), "ExplicitMatrix::sparse: bad nnz");
+    // row_ptr is checked on the host before anything reads the arrays by it
+    require(row_ptr[0] == 0, "ExplicitMatrix::sparse: row_ptr[0] must be 0");
+    for (int64_t i = 0; i < m; ++i)
+      if (row_ptr[i + 1] < row_ptr[i])
+        fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: row_ptr decreases at row " + std::to_string(i));
     require(nnz == 0 || (col && val), "ExplicitMatrix::sparse: null col/val");
     PhaseTimer pt("create_csr");
     auto M = std::make_unique<equil_matrix>();
@@ -668,68 +727,83 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     } joiner{planner};
     if (M->world == 1) planner = std::thread([&] { planA = plan_tiles(row_ptr, m, 0); });
     pt.mark(s, "upload");
-    // validation (explicit_matrix.cpp:21-39 for canonical CSR)
-    DevBuf<int64_t> where;
-    where.alloc(2);
+    // validation (explicit_matrix.cpp:21-39 for canonical CSR); the deterministic
+    // first error: out of range, then duplicate, then unsorted columns
+    DevBuf<unsigned long long> where;
+    where.alloc(1);
     CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
-    CK(cudaMemsetAsync(where.p, 0, 16, s));
+    CK(cudaMemsetAsync(where.p, 0xff, 8, s));
     CK(eqb::launch_validate_csr(fullA, reinterpret_cast<int*>(M->flags.p), where.p, s));
-    int errc = 0;
-    int64_t wh = 0;
-    CK(cudaMemcpyAsync(&errc, M->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    unsigned long long wh = ~0ULL;
     CK(cudaMemcpyAsync(&wh, where.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     pt.mark(s, "validate");
-    if (errc) {
-      if (errc == 1) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: malformed row_ptr at row " + std::to_string(wh));
-      // locate the row of entry wh on the host
-      const int64_t k = wh;
+    if (wh != ~0ULL) {
+      const int cls = static_cast<int>(wh >> 40);
+      const int64_t k = static_cast<int64_t>(wh & ((1ULL << 40) - 1));
       const int64_t i = std::upper_bound(row_ptr, row_ptr + m + 1, k) - row_ptr - 1;
       const std::string at = "(" + std::to_string(i) + ", " + std::to_string(col[k]) + ")";
-      if (errc == 2) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry " + at + " out of range");
-      if (errc == 3) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry " + at);
+      if (cls == 0) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry " + at + " out of range");
+      if (cls == 1) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry " + at);
       fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: columns not ascending at entry " + at +
                              " (canonical CSR required)");
     }
-    // K2: CSR(A^T) on device
-    DevBuf<int64_t> trp;
-    DevBuf<int32_t> tci;
-    DevBuf<double> tva;
-    trp.alloc(n + 1);
-    tci.alloc(nnz);
-    tva.alloc(nnz);
-    eqb::DevCsr fullT{n, m, nnz, trp.p, tci.p, tva.p};
-    CK(eqb::transpose_csr(fullA, fullT, s));
-    pt.mark(s, "transpose");
-    std::vector<int64_t> rpT(n + 1);
-    CK(cudaMemcpyAsync(rpT.data(), trp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    pt.mark(s, "rowptr copy");
-    if (M->world == 1) {
-      // adopt the full arrays as the shard (no copy)
-      M->a_bounds = {0, m};
-      M->t_bounds = {0, n};
-      M->a_max = m;
-      M->t_max = n;
-      std::swap(M->a_rp.p, rp.p); std::swap(M->a_rp.n, rp.n);
-      std::swap(M->a_ci.p, ci.p); std::swap(M->a_ci.n, ci.n);
-      std::swap(M->a_va.p, va.p); std::swap(M->a_va.n, va.n);
-      std::swap(M->t_rp.p, trp.p); std::swap(M->t_rp.n, trp.n);
-      std::swap(M->t_ci.p, tci.p); std::swap(M->t_ci.n, tci.n);
-      std::swap(M->t_va.p, tva.p); std::swap(M->t_va.n, tva.n);
-      M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
-      M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
-      const Plan planT = plan_tiles(rpT.data(), n, 1);
-      planner.join();
-      upload_plans(M.get(), planA, planT);
-    } else {
-      const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
-      shard_sparse(M.get(), fullA, fullT, rpA, rpT);
+    finish_sparse(M.get(), rp, ci, va, row_ptr, pt, &planA, &planner);
+    *out = M.release();
+  });
+}
+
+equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                                     const int64_t* cols, const double* vals,
+                                     const equil_device_cfg* cfg, equil_matrix** out) {
+  return guarded([&] {
+    require(out != nullptr, "ExplicitMatrix::sparse: null output handle");
+    *out = nullptr;
+    require(m > 0 && n > 0, "ExplicitMatrix::sparse: dimensions must be positive");
+    require(n < (1LL << 31) && m < (1LL << 31), "ExplicitMatrix::sparse: dimension too large");
+    require(nnz >= 0 && nnz < (1LL << 31), "ExplicitMatrix::sparse: bad nnz");
+    require(nnz == 0 || (rows && cols && vals), "ExplicitMatrix::sparse: null entries");
+    PhaseTimer pt("create_coo");
+    auto M = std::make_unique<equil_matrix>();
+    setup_common(M.get(), cfg);
+    M->m = m;
+    M->n = n;
+    M->nnz = nnz;
+    DeviceGuard dg(M->device);
+    cudaStream_t s = M->stream;
+    DevBuf<int64_t> dr, dc, rp;
+    DevBuf<double> dv, va;
+    DevBuf<int32_t> ci;
+    dr.alloc(nnz);
+    dc.alloc(nnz);
+    dv.alloc(nnz);
+    rp.alloc(m + 1);
+    ci.alloc(nnz);
+    va.alloc(nnz);
+    if (nnz) {
+      CK(cudaMemcpyAsync(dr.p, rows, nnz * 8, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dc.p, cols, nnz * 8, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(dv.p, vals, nnz * 8, cudaMemcpyHostToDevice, s));
     }
-    pt.mark(s, "plan");
-    alloc_workspaces(M.get());
+    eqb::DevCsr A{m, n, nnz, rp.p, ci.p, va.p};
+    unsigned long long bad = 0;
+    int kind = 0;
+    CK(eqb::coo_to_csr(m, n, nnz, dr.p, dc.p, dv.p, A, &bad, &kind, s));
+    if (kind == 1)  // explicit_matrix.cpp:23-27
+      fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry (" + std::to_string(rows[bad]) + ", " +
+                             std::to_string(cols[bad]) + ") out of range");
+    if (kind == 2)  // explicit_matrix.cpp:33-38
+      fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry (" +
+                             std::to_string(bad / static_cast<uint64_t>(n)) + ", " +
+                             std::to_string(bad % static_cast<uint64_t>(n)) + ")");
+    dr.release();
+    dc.release();
+    dv.release();
+    std::vector<int64_t> rph(m + 1);
+    CK(cudaMemcpyAsync(rph.data(), rp.p, (m + 1) * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    pt.mark(s, "workspaces");
+    pt.mark(s, "coo->csr");
+    finish_sparse(M.get(), rp, ci, va, rph.data(), pt, nullptr, nullptr);
     *out = M.release();
   });
 }

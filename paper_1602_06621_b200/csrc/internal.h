@@ -119,9 +119,18 @@ struct LsqrDev {
 void note_launches(long long n);
 long long launch_count();
 void count_launch(cudaStream_t s, int n = 1);  // skipped while s is capturing
-cudaError_t launch_validate_csr(const DevCsr& A, int* err, int64_t* where,
+// where: min over (class << 40 | entry), class 0 out of range, 1 duplicate,
+// 2 columns not ascending; must be preset to ~0
+cudaError_t launch_validate_csr(const DevCsr& A, int* err, unsigned long long* where,
                                 cudaStream_t s);
 cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s);
+// ExplicitMatrix::sparse on device from COO (rows/cols int64, device); out
+// arrays preallocated (row_ptr m+1, col/val nnz).  On a precondition failure
+// *bad_kind = 1 (out of range: *bad = first entry index in input order) or
+// 2 (duplicate: *bad = row * n + col of the first duplicate in sorted order).
+cudaError_t coo_to_csr(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                       const int64_t* cols, const double* vals, DevCsr& out,
+                       unsigned long long* bad, int* bad_kind, cudaStream_t s);
 cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
                             double* v, double* vb, int64_t n_pad_len,
                             int64_t m_pad_len, const uint32_t* signs,

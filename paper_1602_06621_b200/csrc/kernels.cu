@@ -264,42 +264,50 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
 // restated for canonical CSR input: rows ascending, columns strictly ascending)
 // ---------------------------------------------------------------------------
 namespace {
-__global__ void validate_rows_kernel(const int64_t* rp, int64_t rows, int64_t nnz,
-                                     int* err, int64_t* where) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i > rows) return;
-  bool bad = false;
-  if (i == 0 && rp[0] != 0) bad = true;
-  if (i == rows && rp[rows] != nnz) bad = true;
-  if (i < rows && rp[i + 1] < rp[i]) bad = true;
-  if (bad && atomicCAS(err, 0, 1) == 0) *where = i;
-}
+// (row_ptr itself is validated on the host before upload, so these reads
+// stay inside the arrays.)  One warp per row, coalesced.  The reported error is deterministic and follows
+// the reference's order of checks: the first out-of-range entry
+// (explicit_matrix.cpp:23-28) before the first duplicate (:33-39); a column
+// order violation (only possible for non-canonical CSR) ranks last.  `where`
+// receives min over (class << 40 | entry index).
 __global__ void validate_cols_kernel(const int64_t* rp, const int32_t* ci,
                                      int64_t rows, int64_t cols, int* err,
-                                     int64_t* where) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+                                     unsigned long long* where) {
+  const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= rows) return;
-  for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-    const int32_t c = ci[k];
-    int code = 0;
-    if (c < 0 || c >= cols) code = 2;
-    else if (k > rp[i] && ci[k - 1] >= c) code = (ci[k - 1] == c) ? 3 : 4;
-    if (code) {
-      if (atomicCAS(err, 0, code) == 0) *where = k;
-      return;
+  const int64_t k0 = rp[i], k1 = rp[i + 1];
+  unsigned long long best = ~0ULL;
+  for (int64_t k = k0 + lane; k < k1; k += 32) {
+    const int32_t c = __ldg(ci + k);
+    unsigned long long key = ~0ULL;
+    if (c < 0 || c >= cols) {
+      key = static_cast<unsigned long long>(k);
+    } else if (k > k0) {
+      const int32_t p = __ldg(ci + k - 1);
+      if (p == c) key = (1ULL << 40) | static_cast<unsigned long long>(k);
+      else if (p > c && p >= 0 && p < cols) key = (2ULL << 40) | static_cast<unsigned long long>(k);
     }
+    best = key < best ? key : best;
+  }
+  for (int h = 16; h >= 1; h >>= 1) {
+    const unsigned long long o = __shfl_down_sync(0xffffffffu, best, h);
+    best = o < best ? o : best;
+  }
+  if (lane == 0 && best != ~0ULL) {
+    atomicMin(where, best);
+    *err = 1;
   }
 }
 }  // namespace
 
-cudaError_t launch_validate_csr(const DevCsr& A, int* err, int64_t* where,
+cudaError_t launch_validate_csr(const DevCsr& A, int* err, unsigned long long* where,
                                 cudaStream_t s) {
-  const int bs = 256;
-  validate_rows_kernel<<<static_cast<unsigned>((A.rows + 1 + bs - 1) / bs), bs, 0, s>>>(
-      A.row_ptr, A.rows, A.nnz, err, where); count_launch(s);
-  EQ_CUDA_TRY(cudaGetLastError());
-  validate_cols_kernel<<<static_cast<unsigned>((A.rows + bs - 1) / bs), bs, 0, s>>>(
-      A.row_ptr, A.col, A.rows, A.cols, err, where); count_launch(s);
+  if (A.rows == 0) return cudaSuccess;
+  const int bs = 256;  // 8 rows per CTA
+  validate_cols_kernel<<<static_cast<unsigned>((A.rows * 32 + bs - 1) / bs), bs, 0, s>>>(
+      A.row_ptr, A.col, A.rows, A.cols, err, where);
+  count_launch(s);
   return cudaGetLastError();
 }
 
@@ -394,6 +402,108 @@ cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
   if (perm_in) cudaFreeAsync(perm_in, s);
   if (perm_out) cudaFreeAsync(perm_out, s);
   if (keys_out) cudaFreeAsync(keys_out, s);
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// COO ingest = ExplicitMatrix::sparse (src/explicit_matrix.cpp:19-57) on device:
+// range check in input order (:21-28), sort by (row, col) (:28-31), duplicate
+// rejection in sorted order (:32-39), CSR by counting (:41-56).
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void coo_range_kernel(const int64_t* __restrict__ r, const int64_t* __restrict__ c,
+                                 int64_t nnz, int64_t m, int64_t n,
+                                 unsigned long long* first_bad, uint64_t* key,
+                                 int32_t* perm) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= nnz) return;
+  const int64_t i = r[k], j = c[k];
+  const bool ok = i >= 0 && i < m && j >= 0 && j < n;
+  if (!ok) atomicMin(first_bad, static_cast<unsigned long long>(k));
+  key[k] = ok ? static_cast<uint64_t>(i) * static_cast<uint64_t>(n) + static_cast<uint64_t>(j) : 0;
+  perm[k] = static_cast<int32_t>(k);
+}
+__global__ void coo_build_kernel(const uint64_t* __restrict__ skey,
+                                 const int32_t* __restrict__ sperm,
+                                 const double* __restrict__ v, int64_t nnz, int64_t n,
+                                 unsigned long long* first_dup, int32_t* __restrict__ col,
+                                 double* __restrict__ val) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= nnz) return;
+  const uint64_t key = skey[p];
+  if (p > 0 && skey[p - 1] == key) atomicMin(first_dup, static_cast<unsigned long long>(p));
+  col[p] = static_cast<int32_t>(key % static_cast<uint64_t>(n));
+  val[p] = v[sperm[p]];
+}
+__global__ void coo_rowptr_kernel(const uint64_t* __restrict__ skey, int64_t nnz, int64_t n,
+                                  int64_t m, int64_t* __restrict__ rp) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p > nnz) return;
+  const int64_t prev = p == 0 ? -1 : static_cast<int64_t>(skey[p - 1] / static_cast<uint64_t>(n));
+  const int64_t cur = p == nnz ? m : static_cast<int64_t>(skey[p] / static_cast<uint64_t>(n));
+  for (int64_t i = prev + 1; i <= cur && i <= m; ++i) rp[i] = p;
+}
+}  // namespace
+
+cudaError_t coo_to_csr(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                       const int64_t* cols, const double* vals, DevCsr& out,
+                       unsigned long long* bad, int* bad_kind, cudaStream_t s) {
+  *bad_kind = 0;
+  uint64_t *key = nullptr, *skey = nullptr;
+  int32_t *perm = nullptr, *sperm = nullptr;
+  unsigned long long* flags = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  const int end_bit = std::max(1, ceil_log2(static_cast<uint64_t>(m) * static_cast<uint64_t>(n)));
+  const unsigned nb = static_cast<unsigned>((nnz + 255) / 256);
+  cudaError_t e = cudaSuccess;
+  unsigned long long h[2] = {~0ULL, ~0ULL};
+  do {
+    e = cudaMallocAsync(&flags, 2 * sizeof(unsigned long long), s); if (e) break;
+    e = cudaMemsetAsync(flags, 0xff, 2 * sizeof(unsigned long long), s); if (e) break;
+    if (nnz > 0) {
+      e = cudaMallocAsync(&key, nnz * 8, s); if (e) break;
+      e = cudaMallocAsync(&skey, nnz * 8, s); if (e) break;
+      e = cudaMallocAsync(&perm, nnz * 4, s); if (e) break;
+      e = cudaMallocAsync(&sperm, nnz * 4, s); if (e) break;
+      coo_range_kernel<<<nb, 256, 0, s>>>(rows, cols, nnz, m, n, flags, key, perm);
+      count_launch(s);
+      e = cudaMemcpyAsync(h, flags, 8, cudaMemcpyDeviceToHost, s); if (e) break;
+      e = cudaStreamSynchronize(s); if (e) break;
+      if (h[0] != ~0ULL) {  // first out-of-range entry in input order
+        *bad = h[0];
+        *bad_kind = 1;
+        break;
+      }
+      e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, key, skey, perm, sperm, nnz, 0,
+                                          end_bit, s);
+      if (e) break;
+      e = cudaMallocAsync(&temp, temp_bytes, s); if (e) break;
+      e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, perm, sperm, nnz, 0,
+                                          end_bit, s);
+      if (e) break;
+      coo_build_kernel<<<nb, 256, 0, s>>>(skey, sperm, vals, nnz, n, flags + 1, out.col,
+                                          out.val);
+      count_launch(s);
+    }
+    coo_rowptr_kernel<<<static_cast<unsigned>((nnz + 1 + 255) / 256), 256, 0, s>>>(
+        skey, nnz, n, m, out.row_ptr);
+    count_launch(s);
+    e = cudaMemcpyAsync(h + 1, flags + 1, 8, cudaMemcpyDeviceToHost, s); if (e) break;
+    e = cudaStreamSynchronize(s); if (e) break;
+    if (h[1] != ~0ULL) {  // first duplicate in sorted order: report its key
+      uint64_t dk = 0;
+      e = cudaMemcpy(&dk, skey + h[1], 8, cudaMemcpyDeviceToHost); if (e) break;
+      *bad = dk;
+      *bad_kind = 2;
+    }
+  } while (0);
+  if (temp) cudaFreeAsync(temp, s);
+  if (key) cudaFreeAsync(key, s);
+  if (skey) cudaFreeAsync(skey, s);
+  if (perm) cudaFreeAsync(perm, s);
+  if (sperm) cudaFreeAsync(sperm, s);
+  if (flags) cudaFreeAsync(flags, s);
   return e;
 }
 

@@ -329,3 +329,45 @@ def test_full_size_config3_properties(C):
     trp, tc, tv = M.transposed_csr()
     assert trp[-1] == inst.nnz and np.all(np.diff(trp) >= 0)
     assert np.array_equal(np.diff(trp), np.bincount(inst.col, minlength=inst.n))
+
+
+# ---------------------------------------------------------------- COO ingest (f2)
+def test_coo_ingest_equals_reference_construction(golden):
+    """ExplicitMatrix::sparse from shuffled COO triplets on device: same CSR
+    (hence same CSR(A^T) and trajectory) as the reference's construction."""
+    A = csr_from_golden(golden, "lr")
+    rows = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    perm = np.random.default_rng(5).permutation(rows.size)
+    M = eq.ExplicitMatrix.sparse(A.m, A.n, (rows[perm], A.col[perm].astype(np.int64),
+                                            A.val[perm]))
+    trp, tc, tv = M.transposed_csr()
+    assert np.array_equal(trp, golden["lr_t_rp"]) and np.array_equal(tc, golden["lr_t_col"])
+    assert np.array_equal(tv.view(np.uint64), golden["lr_t_val"].view(np.uint64))
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=40, seed=5))
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), golden[f"lr_sgd_{k}"])
+
+
+def test_coo_errors_match_reference_messages():
+    cases = [
+        (3, 3, [(0, 0, 1.0), (5, 1, 1.0), (3, 3, 2.0)]),          # first bad in input order
+        (3, 3, [(2, 2, 1.0), (0, 1, 2.0), (2, 2, 3.0), (0, 1, 4.0)]),  # first dup after sort
+        (2, 4, [(1, -1, 1.0)]),
+    ]
+    want = ["ExplicitMatrix::sparse: entry (5, 1) out of range",
+            "ExplicitMatrix::sparse: duplicate entry (0, 1)",
+            "ExplicitMatrix::sparse: entry (1, -1) out of range"]
+    for (m, n, ent), msg in zip(cases, want):
+        with pytest.raises(eq.InvalidArgument) as ei:
+            eq.ExplicitMatrix.sparse(m, n, ent)
+        assert str(ei.value) == msg
+        if oracle.ref_available():  # the reference's own construction agrees
+            r, c, v = (np.array(x) for x in zip(*ent))
+            with pytest.raises(oracle.OracleError) as er:
+                oracle.ref_oracle().matrix_coo(m, n, r, c, v)
+            assert str(er.value) == msg
+    # empty rows/columns and an empty matrix are fine
+    M = eq.ExplicitMatrix.sparse(4, 3, [])
+    assert M.stored_entries() == 0
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(alpha=1.0, iterations=3))
+    assert np.all(r.u < 0) or np.all(r.u != 0)
