@@ -150,6 +150,13 @@ equil_status equil_apply(equil_matrix* A, const double* x, double* y, int adjoin
 equil_status equil_sgd_equilibrate(equil_matrix* A, const equil_params* p,
                                    const equil_diag_cfg* diag,
                                    equil_scaling_out* out);
+/* sgd_equilibrate_targets(op, r, c, params, diag) (include/equil/variants.hpp:24-27,
+ * src/variants.cpp:105-118): per-row squared-norm targets r (m entries) and
+ * per-column targets c (n entries), positive, sum(r) == sum(c) to 1e-8; the
+ * same engine with per-coordinate linear terms (history: objective only). */
+equil_status equil_sgd_equilibrate_targets(equil_matrix* A, const double* r, const double* c,
+                                           const equil_params* p, const equil_diag_cfg* diag,
+                                           equil_scaling_out* out);
 /* lsqr(op, b, max_iters, tol) (include/equil/lsqr.hpp:30-31, src/lsqr.cpp:85-103) */
 equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
                         equil_lsqr_out* out);

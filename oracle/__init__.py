@@ -183,6 +183,8 @@ class _COracle:
         L.eo_last_error.restype = C.c_char_p
         L.eo_sgd_equilibrate.argtypes = [C.POINTER(_Matrix), C.POINTER(_Params), C.c_int,
                                          C.POINTER(_Scaling)]
+        L.eo_sgd_equilibrate_targets.argtypes = [C.POINTER(_Matrix), _dp, _dp, C.POINTER(_Params),
+                                                 C.c_int, C.POINTER(_Scaling)]
         L.eo_objective.restype = C.c_double
         L.eo_objective.argtypes = [C.POINTER(_Matrix), _dp, _dp, C.c_double, C.c_double, C.c_double]
         L.eo_rms_error.restype = C.c_double
@@ -288,6 +290,29 @@ class _COracle:
                        bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
                        hi[:k].copy(), ho[:k].copy(), hr[:k].copy(), tu, tv)
 
+    def sgd_equilibrate_targets(self, A: CsrArrays, r, c, gamma=0.1,
+                                max_log_scale=9.210340371976184, iterations=1000, seed=0,
+                                diag_stride=0) -> Scaling:
+        r = np.ascontiguousarray(r, np.float64)
+        c = np.ascontiguousarray(c, np.float64)
+        m, n = A.m, A.n
+        u, v, d, e = np.zeros(m), np.zeros(n), np.zeros(m), np.zeros(n)
+        nh = iterations // diag_stride + 1 if diag_stride > 0 else 1
+        hi, ho, hr = np.zeros(nh, np.int32), np.zeros(nh), np.zeros(nh)
+        s = _Scaling(ptr(u, _dp), ptr(v, _dp), ptr(d, _dp), ptr(e, _dp), 0, 0, 0, 0, 0, 0,
+                     ptr(hi, _ip), ptr(ho, _dp), ptr(hr, _dp), 0, ptr(None, _dp),
+                     ptr(None, _dp))
+        p = _Params(0.0, 0.0, gamma, max_log_scale, iterations, seed)
+        mat = A._struct()
+        rc = self.L.eo_sgd_equilibrate_targets(C.byref(mat), ptr(r, _dp), ptr(c, _dp),
+                                               C.byref(p), diag_stride, C.byref(s))
+        if rc:
+            self._err(rc)
+        k = s.hist_len
+        return Scaling(u, v, d, e, s.alpha, s.beta, bool(s.box_feasible),
+                       bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
+                       hi[:k].copy(), ho[:k].copy(), hr[:k].copy())
+
     def objective(self, A, u, v, alpha2, beta2, gamma):
         mat = A._struct()
         return self.L.eo_objective(C.byref(mat), ptr(np.ascontiguousarray(u, np.float64), _dp),
@@ -360,6 +385,8 @@ class _RefOracle:
         L.er_sgd_equilibrate.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_int, C.c_uint64, C.c_int,
                                          C.POINTER(_RefSgd)]
+        L.er_sgd_targets.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_int,
+                                     C.c_uint64, C.c_int, C.POINTER(_RefSgd)]
         L.er_lsqr.argtypes = [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(_RefLsqr)]
         L.er_lsqr_preconditioned.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double,
                                              C.c_double, C.c_double, C.c_int, C.c_uint64,
@@ -444,6 +471,24 @@ class RefMatrix:
                     ptr(hi, _ip), ptr(ho, _dp), ptr(hr, _dp), 0)
         rc = self.R.L.er_sgd_equilibrate(self.h, alpha, beta, gamma, max_log_scale,
                                          iterations, seed, diag_stride, C.byref(s))
+        if rc:
+            self.R._err(rc)
+        k = s.hist_len
+        return Scaling(u, v, d, e, s.alpha, s.beta, bool(s.box_feasible),
+                       bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
+                       hi[:k].copy(), ho[:k].copy(), hr[:k].copy())
+
+    def sgd_equilibrate_targets(self, r, c, gamma=0.1, max_log_scale=9.210340371976184,
+                                iterations=1000, seed=0, diag_stride=0) -> Scaling:
+        r = np.ascontiguousarray(r, np.float64)
+        c = np.ascontiguousarray(c, np.float64)
+        u, v, d, e = np.zeros(self.m), np.zeros(self.n), np.zeros(self.m), np.zeros(self.n)
+        nh = iterations // diag_stride + 1 if diag_stride > 0 else 1
+        hi, ho, hr = np.zeros(nh, np.int32), np.zeros(nh), np.zeros(nh)
+        s = _RefSgd(ptr(u, _dp), ptr(v, _dp), ptr(d, _dp), ptr(e, _dp), 0, 0, 0, 0, 0, 0,
+                    ptr(hi, _ip), ptr(ho, _dp), ptr(hr, _dp), 0)
+        rc = self.R.L.er_sgd_targets(self.h, ptr(r, _dp), ptr(c, _dp), gamma, max_log_scale,
+                                     iterations, seed, diag_stride, C.byref(s))
         if rc:
             self.R._err(rc)
         k = s.hist_len

@@ -380,23 +380,30 @@ int eo_validate_params(const eo_params* p) {
     }                                                                       \
   } while (0)
 
-double eo_objective(const eo_matrix* A, const double* u, const double* v,
-                    double alpha2, double beta2, double gamma) {
+/* objective_weighted with vector linear terms (src/equilibrate.cpp:10-22) */
+static double objective_lin(const eo_matrix* A, const double* u, const double* v,
+                            const double* lu, const double* lv, double gamma) {
   double quad = 0.0;
   FOR_EACH_ENTRY(A, {
     if (ea != 0.0) quad += ea * ea * exp(2.0 * (u[ei] + v[ej]));
   });
+  double du = eo_canon_dot(lu, u, A->m);
+  double dv = eo_canon_dot(lv, v, A->n);
+  double su = eo_canon_sumsq(u, A->m), sv = eo_canon_sumsq(v, A->n);
+  return 0.5 * quad - du - dv + 0.5 * gamma * (su + sv);
+}
+
+double eo_objective(const eo_matrix* A, const double* u, const double* v,
+                    double alpha2, double beta2, double gamma) {
   /* lin_u.dot(u) with lin_u = alpha^2 * 1 */
   double* lu = (double*)malloc((size_t)A->m * sizeof(double));
   double* lv = (double*)malloc((size_t)A->n * sizeof(double));
   for (int64_t i = 0; i < A->m; ++i) lu[i] = alpha2;
   for (int64_t j = 0; j < A->n; ++j) lv[j] = beta2;
-  double du = eo_canon_dot(lu, u, A->m);
-  double dv = eo_canon_dot(lv, v, A->n);
-  double su = eo_canon_sumsq(u, A->m), sv = eo_canon_sumsq(v, A->n);
+  const double r = objective_lin(A, u, v, lu, lv, gamma);
   free(lu);
   free(lv);
-  return 0.5 * quad - du - dv + 0.5 * gamma * (su + sv);
+  return r;
 }
 
 double eo_rms_error(const eo_matrix* A, const double* u, const double* v,
@@ -435,9 +442,10 @@ double eo_rms_error(const eo_matrix* A, const double* u, const double* v,
 
 /* One block update, run_projected_sgd :109-129. */
 static void sgd_block(int64_t dim, double* x, double* avg, const double* est,
-                      double lin, double gamma, double M, double step,
+                      const double* lins, double gamma, double M, double step,
                       double aw, int* bound_ok, int* box_ok) {
   for (int64_t i = 0; i < dim; ++i) {
+    const double lin = lins[i];
     const double g = est[i] - lin + gamma * x[i];
     double xi = x[i] - step * g;
     double lo = (xi < -M) ? -M : xi; /* std::max(xi, -M) */
@@ -453,14 +461,46 @@ static void sgd_block(int64_t dim, double* x, double* avg, const double* est,
   for (int64_t i = 0; i < dim; ++i) avg[i] = aw * x[i] + w1 * avg[i];
 }
 
+/* internal::sgd_row_col (src/equilibrate.cpp:138-210) with per-coordinate
+ * linear terms; alpha, beta > 0 enable the RMS diagnostic. */
+static int sgd_row_col(const eo_matrix* A, const eo_params* p, const double* lin_u,
+                       const double* lin_v, double alpha, double beta, int diag_stride,
+                       eo_scaling* out);
+
 int eo_sgd_equilibrate(const eo_matrix* A, const eo_params* p, int diag_stride,
                        eo_scaling* out) {
   double alpha, beta;
   if (eo_resolve_targets(p, A->m, A->n, &alpha, &beta)) return 1; /* :216 */
-  if (eo_validate_params(p)) return 1;                            /* :142 */
+  double* lu = (double*)malloc((size_t)A->m * sizeof(double));
+  double* lv = (double*)malloc((size_t)A->n * sizeof(double));
+  for (int64_t i = 0; i < A->m; ++i) lu[i] = alpha * alpha; /* :218-220 */
+  for (int64_t j = 0; j < A->n; ++j) lv[j] = beta * beta;
+  const int rc = sgd_row_col(A, p, lu, lv, alpha, beta, diag_stride, out);
+  free(lu);
+  free(lv);
+  return rc;
+}
+
+/* sgd_equilibrate_targets (src/variants.cpp:105-118) */
+int eo_sgd_equilibrate_targets(const eo_matrix* A, const double* r, const double* c,
+                               const eo_params* p, int diag_stride, eo_scaling* out) {
+  for (int64_t i = 0; i < A->m; ++i)
+    if (!(r[i] > 0.0)) return fail("sgd_equilibrate_targets: targets must be positive");
+  for (int64_t j = 0; j < A->n; ++j)
+    if (!(c[j] > 0.0)) return fail("sgd_equilibrate_targets: targets must be positive");
+  const double sr = eo_canon_sum(r, A->m), sc = eo_canon_sum(c, A->n);
+  const double mx = sr < sc ? sc : sr;
+  if (!(fabs(sr - sc) <= 1e-8 * mx))
+    return fail("sgd_equilibrate_targets: sum(r) == sum(c) violated");
+  return sgd_row_col(A, p, r, c, 0.0, 0.0, diag_stride, out);
+}
+
+static int sgd_row_col(const eo_matrix* A, const eo_params* p, const double* lin_u,
+                       const double* lin_v, double alpha, double beta, int diag_stride,
+                       eo_scaling* out) {
+  if (eo_validate_params(p)) return 1; /* :142 */
   if (diag_stride < 0) return fail("sgd_row_col: stride must be positive");
   const int64_t m = A->m, n = A->n;
-  const double lin_u = alpha * alpha, lin_v = beta * beta; /* :218-220 */
   const double gamma = p->gamma, M = p->max_log_scale;
   const int T = p->iterations;
 
@@ -485,8 +525,10 @@ int eo_sgd_equilibrate(const eo_matrix* A, const eo_params* p, int diag_stride,
       int h = out->hist_len++;                                            \
       if (out->hist_iter) out->hist_iter[h] = (t);                        \
       if (out->hist_objective)                                            \
-        out->hist_objective[h] = eo_objective(A, ub, vb, lin_u, lin_v, gamma); \
-      if (out->hist_rms) out->hist_rms[h] = eo_rms_error(A, ub, vb, alpha, beta); \
+        out->hist_objective[h] = objective_lin(A, ub, vb, lin_u, lin_v, gamma); \
+      if (out->hist_rms)                                                  \
+        out->hist_rms[h] = (alpha > 0.0 && beta > 0.0)                    \
+                               ? eo_rms_error(A, ub, vb, alpha, beta) : 0.0; \
     }                                                                     \
   } while (0)
 

@@ -120,6 +120,9 @@ typedef struct {
   double* traj_v;
 } eo_scaling;
 
+/* sgd_equilibrate_targets (src/variants.cpp:105-118): r (m), c (n) */
+int eo_sgd_equilibrate_targets(const eo_matrix* A, const double* r, const double* c,
+                               const eo_params* p, int diag_stride, eo_scaling* out);
 int eo_sgd_equilibrate(const eo_matrix* A, const eo_params* p, int diag_stride,
                        eo_scaling* out);
 

@@ -15,6 +15,7 @@
 #include "equil/lsqr.hpp"
 #include "equil/metrics.hpp"
 #include "equil/rng.hpp"
+#include "equil/variants.hpp"
 
 using namespace equil;
 
@@ -176,6 +177,43 @@ int er_sgd_equilibrate(void* h, double alpha, double beta, double gamma,
       if (out->hist_objective)
         out->hist_objective[k] = r.history[k].objective.value_or(0.0);
       if (out->hist_rms) out->hist_rms[k] = r.history[k].rms.value_or(0.0);
+    }
+  });
+}
+
+// sgd_equilibrate_targets (include/equil/variants.hpp:24-27)
+int er_sgd_targets(void* h, const double* r, const double* c, double gamma,
+                   double max_log_scale, int iterations, uint64_t seed, int diag_stride,
+                   er_sgd_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    EquilibrationParams p;
+    p.gamma = gamma;
+    p.max_log_scale = max_log_scale;
+    p.iterations = iterations;
+    p.seed = seed;
+    DiagnosticsConfig diag;
+    if (diag_stride > 0) {
+      diag.matrix = &A;
+      diag.stride = diag_stride;
+    }
+    const ScalingResult res =
+        sgd_equilibrate_targets(A, to_vec(r, A.rows()), to_vec(c, A.cols()), p, diag);
+    from_vec(res.u, out->u);
+    from_vec(res.v, out->v);
+    from_vec(res.d, out->d);
+    from_vec(res.e, out->e);
+    out->alpha = res.alpha;
+    out->beta = res.beta;
+    out->box_feasible = res.box_feasible;
+    out->iterate_bound_ok = res.iterate_bound_ok;
+    out->apply_count = res.apply_count;
+    out->adjoint_count = res.adjoint_count;
+    out->hist_len = static_cast<int>(res.history.size());
+    for (std::size_t k = 0; k < res.history.size(); ++k) {
+      if (out->hist_iter) out->hist_iter[k] = res.history[k].iter;
+      if (out->hist_objective) out->hist_objective[k] = res.history[k].objective.value_or(0.0);
+      if (out->hist_rms) out->hist_rms[k] = res.history[k].rms.value_or(0.0);
     }
   });
 }

@@ -10,6 +10,7 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   ScalingResult, canon_sumsq_device, det_exp_device, kernel_launches,
                   last_loop_ms, lsqr, lsqr_preconditioned, nccl_unique_id,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
+                  sgd_equilibrate_targets,
                   sgd_equilibrate_device, sign_bits, validate_params)
 
 __all__ = [
@@ -18,5 +19,5 @@ __all__ = [
     "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",
     "kernel_launches", "last_loop_ms", "lsqr", "lsqr_preconditioned", "nccl_unique_id",
     "partition_rows", "resolve_targets", "sgd_equilibrate", "sgd_equilibrate_csr",
-    "sgd_equilibrate_device", "sign_bits", "validate_params",
+    "sgd_equilibrate_device", "sgd_equilibrate_targets", "sign_bits", "validate_params",
 ]

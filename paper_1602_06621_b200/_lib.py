@@ -73,6 +73,8 @@ SIGNATURES = {
     "equil_apply": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int]),
     "equil_sgd_equilibrate": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(DiagCfg),
                                         C.POINTER(ScalingOut)]),
+    "equil_sgd_equilibrate_targets": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params),
+                                                C.POINTER(DiagCfg), C.POINTER(ScalingOut)]),
     "equil_lsqr": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(LsqrOut)]),
     "equil_lsqr_preconditioned": (C.c_int, [C.c_void_p, _dp, C.POINTER(Params), C.c_int,
                                             C.c_double, C.POINTER(LsqrOut)]),

@@ -260,6 +260,35 @@ def sgd_equilibrate(op: ExplicitMatrix, params: EquilibrationParams | None = Non
                          bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
 
 
+def sgd_equilibrate_targets(op: ExplicitMatrix, r, c, params: EquilibrationParams | None = None,
+                            diag: DiagnosticsConfig | None = None) -> ScalingResult:
+    """sgd_equilibrate_targets (include/equil/variants.hpp:24-27): row i aims
+    at squared norm r_i, column j at c_j; history carries the objective only
+    (alpha/beta of the result are 0, as in the reference)."""
+    params = params or EquilibrationParams()
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    if r.size != op.rows() or c.size != op.cols():
+        raise InvalidArgument("sgd_equilibrate_targets: target length mismatch")
+    m, n = op.rows(), op.cols()
+    u, v, d, e = np.zeros(m), np.zeros(n), np.zeros(m), np.zeros(n)
+    cap = (max(int(params.iterations), 0) // diag.stride + 1) if diag and diag.stride > 0 else 1
+    hi, ho, hr = np.zeros(cap, np.int32), np.zeros(cap), np.zeros(cap)
+    out = L.ScalingOut(L.ptr(u, L._dp), L.ptr(v, L._dp), L.ptr(d, L._dp), L.ptr(e, L._dp), 0,
+                       0.0, 0.0, 0, 0, 0, 0, L.ptr(hi, L._ip), L.ptr(ho, L._dp),
+                       L.ptr(hr, L._dp), cap, 0)
+    p = params._c()
+    dc = L.DiagCfg(diag.stride, int(diag.want_objective), 0) if diag else None
+    _check(L.load().equil_sgd_equilibrate_targets(op._h, L.ptr(r, L._dp), L.ptr(c, L._dp),
+                                                  C.byref(p),
+                                                  C.byref(dc) if dc is not None else None,
+                                                  C.byref(out)))
+    hist = [IterationRecord(int(hi[k]), float(ho[k]) if diag.want_objective else None, None)
+            for k in range(out.hist_len)] if diag else []
+    return ScalingResult(u, v, d, e, out.alpha, out.beta, hist, bool(out.box_feasible),
+                         bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
+
+
 def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,
                            u_ptr: int, v_ptr: int, d_ptr: int, e_ptr: int) -> ScalingResult:
     """sgd_equilibrate with u, v, d, e written to caller-owned DEVICE buffers

@@ -94,7 +94,8 @@ dense_sgd_rows_kernel(const DenseIterArgs a) {
     const double y = __dmul_rn(d, acc);
     const double est = __dmul_rn(y, y);
     double avg = a.ub[i];
-    const double xn = sgd_coord(est, a.u[i], a.cu, a.st, avg, fl);
+    const double xn = a.lin_u ? sgd_coord_lin(est, a.u[i], a.lin_u[i], a.cu, a.st, avg, fl)
+                              : sgd_coord(est, a.u[i], a.cu, a.st, avg, fl);
     a.u[i] = xn;
     a.ub[i] = avg;
     if (a.has_next) {
@@ -182,7 +183,8 @@ __global__ void dense_sgd_cols_final_kernel(const DenseIterArgs a) {
   const double z = __dmul_rn(e, acc);
   const double est = __dmul_rn(z, z);
   double avg = a.vb[j];
-  const double xn = sgd_coord(est, a.v[j], a.cv, a.st, avg, fl);
+  const double xn = a.lin_v ? sgd_coord_lin(est, a.v[j], a.lin_v[j], a.cv, a.st, avg, fl)
+                            : sgd_coord(est, a.v[j], a.cv, a.st, avg, fl);
   a.v[j] = xn;
   a.vb[j] = avg;
   if (a.has_next) {

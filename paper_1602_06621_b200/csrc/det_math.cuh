@@ -136,4 +136,22 @@ EQ_HD double sgd_coord(double est, double x, const SgdBlockConst& c,
   return xi;
 }
 
+// The same update with a per-coordinate linear term lin_i (nonuniform targets,
+// src/variants.cpp:105-118 -> sgd_row_col); the iterate-bound threshold is
+// formed per coordinate exactly as run_projected_sgd does (:122-125).
+EQ_HD double sgd_coord_lin(double est, double x, double lin, const SgdBlockConst& c,
+                           const SgdStep& s, double& avg, unsigned& flags) {
+  const double g = rn_add(rn_sub(est, lin), rn_mul(c.gamma, x));
+  double xi = rn_sub(x, rn_mul(s.step, g));
+  const double negM = -c.M;
+  xi = (xi < negM) ? negM : xi;
+  xi = (c.M < xi) ? c.M : xi;
+  const double cap = rn_div(lin, c.gamma);
+  const double acap = fabs(cap);
+  if (xi > rn_add(cap, rn_mul(1e-9, (1.0 < acap) ? acap : 1.0))) flags |= 1u;
+  if (fabs(xi) > c.M) flags |= 2u;
+  avg = rn_add(rn_mul(s.aw, xi), rn_mul(s.aw1, avg));
+  return xi;
+}
+
 }  // namespace eqb

@@ -358,14 +358,17 @@ struct equil_matrix {
   DevBuf<unsigned> red_counter;
   DevBuf<double> scal;  // small device scalars
   DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
+  DevBuf<double> lin_u, lin_v;  // per-coordinate targets (sgd_equilibrate_targets)
 
   // graph cache for the SGD loop
   cudaGraphExec_t graph = nullptr;
   struct Key {
     int T = -1;
     double alpha = 0, beta = 0, gamma = 0, M = 0;
+    bool vec_lin = false;
     bool operator==(const Key& o) const {
-      return T == o.T && alpha == o.alpha && beta == o.beta && gamma == o.gamma && M == o.M;
+      return T == o.T && alpha == o.alpha && beta == o.beta && gamma == o.gamma && M == o.M &&
+             vec_lin == o.vec_lin;
     }
   } graph_key;
 
@@ -890,16 +893,28 @@ void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, in
 
 }  // namespace
 
-extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_params* p,
-                                              const equil_diag_cfg* diag,
-                                              equil_scaling_out* out) {
-  return guarded([&] {
-    require(M != nullptr && p != nullptr && out != nullptr, "sgd_equilibrate: null argument");
+namespace {
+
+// internal::sgd_row_col (src/equilibrate.cpp:138-210).  Uniform targets
+// (lin = alpha^2, beta^2) when lin_u_host / lin_v_host are null, otherwise the
+// per-coordinate linear terms of sgd_equilibrate_targets (src/variants.cpp:105-118);
+// alpha, beta > 0 enable the RMS diagnostic (alpha_for_rms, beta_for_rms).
+void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* diag,
+                 equil_scaling_out* out, double alpha, double beta,
+                 const double* lin_u_host, const double* lin_v_host) {
+  {
     std::lock_guard<std::mutex> lk(M->mu);
     DeviceGuard dg(M->device);
-    double alpha = 0, beta = 0;
-    resolve_targets(*p, M->m, M->n, alpha, beta);  // src/equilibrate.cpp:216
-    validate_params(*p);                            // :142
+    validate_params(*p);  // :142
+    const bool vec_lin = lin_u_host != nullptr;
+    if (vec_lin) {  // local slices of the per-coordinate linear terms
+      M->lin_u.ensure(M->m_loc());
+      M->lin_v.ensure(M->n_loc());
+      CK(cudaMemcpyAsync(M->lin_u.p, lin_u_host + M->a_goff(), M->m_loc() * 8,
+                         cudaMemcpyHostToDevice, M->stream));
+      CK(cudaMemcpyAsync(M->lin_v.p, lin_v_host + M->t_goff(), M->n_loc() * 8,
+                         cudaMemcpyHostToDevice, M->stream));
+    }
     DiagPlan dp;
     if (diag && diag->stride > 0) {
       dp.stride = diag->stride;
@@ -965,7 +980,7 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
     int rec = 0;
     auto record = [&](int) {
       double* slot = hist.p + kRec * rec;
-      if (dp.rms) {  // rms_error (src/metrics.cpp:41-56)
+      if (dp.rms && alpha > 0.0 && beta > 0.0) {  // rms_error (src/metrics.cpp:41-56)
         double* eu = M->tmp_m.p;
         double* ev = M->tmp_n.p;
         CK(eqb::launch_exp(M->ub.p, eu, m, 2.0, s));
@@ -977,8 +992,15 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
       if (dp.obj) {  // objective_weighted (src/equilibrate.cpp:10-22)
         CK(eqb::launch_obj_terms(M->A, M->ub.p, M->vb.p, terms.p, s));
         canon_reduce(M, terms.p, m, slot + 1, 1);
-        canon_reduce(M, M->ub.p, m, slot + 2, 2, lin_u);
-        canon_reduce(M, M->vb.p, n, slot + 3, 2, lin_v);
+        if (vec_lin) {  // lin_u.dot(u): rounded products, canonical sum
+          CK(eqb::launch_mul(terms.p, M->lin_u.p, M->ub.p, m, s));
+          canon_reduce(M, terms.p, m, slot + 2, 1);
+          CK(eqb::launch_mul(terms.p, M->lin_v.p, M->vb.p, n, s));
+          canon_reduce(M, terms.p, n, slot + 3, 1);
+        } else {
+          canon_reduce(M, M->ub.p, m, slot + 2, 2, lin_u);
+          canon_reduce(M, M->vb.p, n, slot + 3, 2, lin_v);
+        }
         canon_reduce(M, M->ub.p, m, slot + 4, 0);
         canon_reduce(M, M->vb.p, n, slot + 5, 0);
       }
@@ -1023,6 +1045,8 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
       a.has_next = t < T;
       a.c[0] = cu;
       a.c[1] = cv;
+      a.lin[0] = vec_lin ? M->lin_u.p : nullptr;
+      a.lin[1] = vec_lin ? M->lin_v.p : nullptr;
       a.st = host_step(t);
       a.flags = M->flags.p;
       return a;
@@ -1046,6 +1070,8 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
       a.has_next = t < T;
       a.cu = cu;
       a.cv = cv;
+      a.lin_u = vec_lin ? M->lin_u.p : nullptr;
+      a.lin_v = vec_lin ? M->lin_v.p : nullptr;
       a.st = host_step(t);
       a.flags = M->flags.p;
       a.colpart = M->colpart.p;
@@ -1065,7 +1091,7 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
 
     if (dp.stride == 0 && T > 0) {
       // capture the whole T loop once per (T, targets, gamma, M) and replay it
-      equil_matrix::Key key{T, alpha, beta, gamma, Mx};
+      equil_matrix::Key key{T, alpha, beta, gamma, Mx, vec_lin};
       if (!M->graph || !(M->graph_key == key)) {
         if (M->graph) {
           cudaGraphExecDestroy(M->graph);
@@ -1165,6 +1191,64 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
       if (out->hist_rms)
         out->hist_rms[h] = dp.rms ? std::sqrt(r[0] / static_cast<double>(m + n)) : 0.0;
     }
+  }
+}
+
+// canonical sum on the host (det_math.cuh definition; precondition checks only)
+double canon_sum_host(const double* x, int64_t len) {
+  if (len <= 0) return 0.0;
+  const int64_t nc = (len + eqb::kChunk - 1) / eqb::kChunk;
+  std::vector<double> part(nc), s(eqb::kLanes2);
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t base = c * eqb::kChunk, clen = std::min<int64_t>(eqb::kChunk, len - base);
+    for (int l = 0; l < eqb::kLanes1; ++l) {
+      double acc = 0.0;
+      for (int64_t k = l; k < clen; k += eqb::kLanes1) acc = acc + x[base + k];
+      s[l] = acc;
+    }
+    for (int h = eqb::kLanes1 / 2; h >= 1; h >>= 1)
+      for (int l = 0; l < h; ++l) s[l] = s[l] + s[l + h];
+    part[c] = s[0];
+  }
+  for (int l = 0; l < eqb::kLanes2; ++l) {
+    double acc = 0.0;
+    for (int64_t k = l; k < nc; k += eqb::kLanes2) acc = acc + part[k];
+    s[l] = acc;
+  }
+  for (int h = eqb::kLanes2 / 2; h >= 1; h >>= 1)
+    for (int l = 0; l < h; ++l) s[l] = s[l] + s[l + h];
+  return s[0];
+}
+
+}  // namespace
+
+extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_params* p,
+                                              const equil_diag_cfg* diag,
+                                              equil_scaling_out* out) {
+  return guarded([&] {
+    require(M != nullptr && p != nullptr && out != nullptr, "sgd_equilibrate: null argument");
+    double alpha = 0, beta = 0;
+    resolve_targets(*p, M->m, M->n, alpha, beta);  // src/equilibrate.cpp:216
+    sgd_row_col(M, p, diag, out, alpha, beta, nullptr, nullptr);
+  });
+}
+
+extern "C" equil_status equil_sgd_equilibrate_targets(equil_matrix* M, const double* r,
+                                                      const double* c, const equil_params* p,
+                                                      const equil_diag_cfg* diag,
+                                                      equil_scaling_out* out) {
+  return guarded([&] {
+    require(M != nullptr && p != nullptr && out != nullptr,
+            "sgd_equilibrate_targets: null argument");
+    require(r != nullptr && c != nullptr, "sgd_equilibrate_targets: target length mismatch");
+    for (int64_t i = 0; i < M->m; ++i)
+      require(r[i] > 0.0, "sgd_equilibrate_targets: targets must be positive");
+    for (int64_t j = 0; j < M->n; ++j)
+      require(c[j] > 0.0, "sgd_equilibrate_targets: targets must be positive");
+    const double sum_r = canon_sum_host(r, M->m), sum_c = canon_sum_host(c, M->n);
+    require(std::abs(sum_r - sum_c) <= 1e-8 * std::max(sum_r, sum_c),
+            "sgd_equilibrate_targets: sum(r) == sum(c) violated");
+    sgd_row_col(M, p, diag, out, 0.0, 0.0, r, c);  // variants.cpp:117
   });
 }
 

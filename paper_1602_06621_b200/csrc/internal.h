@@ -80,6 +80,7 @@ struct SgdIterArgs {
   int64_t sign_next[2];   // bit index of (local row 0) for iteration t+1: w, s
   int has_next;
   SgdBlockConst c[2];
+  const double* lin[2];  // per-coordinate linear terms (local rows) or nullptr
   SgdStep st;
   unsigned* flags;
 };
@@ -170,6 +171,8 @@ struct DenseIterArgs {
   int64_t sign_next_w, sign_next_s;
   int has_next;
   SgdBlockConst cu, cv;
+  const double* lin_u;  // per-coordinate linear terms or nullptr
+  const double* lin_v;
   SgdStep st;
   unsigned* flags;
   double* colpart;  // scratch: nchunks_m x n

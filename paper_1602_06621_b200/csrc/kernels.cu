@@ -601,7 +601,9 @@ __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
   const double y = __dmul_rn(scl, acc);          // linop.cpp:19 / :25
   const double est = __dmul_rn(y, y);            // estimator.cpp:8
   double avg = a.avg[mat][r];
-  const double xn = sgd_coord(est, a.x[mat][r], a.c[mat], a.st, avg, fl);
+  const double xn = a.lin[mat]
+                        ? sgd_coord_lin(est, a.x[mat][r], a.lin[mat][r], a.c[mat], a.st, avg, fl)
+                        : sgd_coord(est, a.x[mat][r], a.c[mat], a.st, avg, fl);
   a.x[mat][r] = xn;
   a.avg[mat][r] = avg;
   if (a.has_next) {  // next iteration's e.*s (from v) / d.*w (from u)

@@ -94,6 +94,19 @@ def main():
         g[f"{key}_plsqr_res"], g[f"{key}_plsqr_x"] = pp.residual_history, pp.x
         g[f"{key}_plsqr_meta"] = np.array([pp.iterations, pp.reached_tol, pp.breakdown,
                                            pp.apply_count, pp.adjoint_count])
+    # nonuniform targets (src/variants.cpp:105-118) on the sparse case
+    A = cases["sp"]
+    rng = np.random.default_rng(15)
+    r = rng.uniform(0.5, 2.0, A.m)
+    c = rng.uniform(0.5, 2.0, A.n)
+    c = c * (r.sum() / c.sum())
+    s = R.matrix(A).sgd_equilibrate_targets(r, c, iterations=30, seed=4, diag_stride=10)
+    g["tg_r"], g["tg_c"] = r, c
+    for k in "uvde":
+        g[f"tg_sgd_{k}"] = getattr(s, k)
+    g["tg_sgd_hist_obj"] = s.hist_objective
+    g["tg_sgd_flags"] = np.array([s.box_feasible, s.iterate_bound_ok, s.apply_count,
+                                  s.adjoint_count])
     np.savez_compressed(OUT, **g)
     print(OUT, os.path.getsize(OUT), "bytes")
 

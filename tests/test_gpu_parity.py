@@ -331,6 +331,46 @@ def test_full_size_config3_properties(C):
     assert np.array_equal(np.diff(trp), np.bincount(inst.col, minlength=inst.n))
 
 
+# ---------------------------------------------------------------- targets variant (f4)
+def test_targets_variant_bit_exact_vs_reference_golden(golden):
+    A = csr_from_golden(golden, "sp")
+    M = device_matrix(A)
+    r = eq.sgd_equilibrate_targets(M, golden["tg_r"], golden["tg_c"],
+                                   eq.EquilibrationParams(iterations=30, seed=4),
+                                   eq.DiagnosticsConfig(stride=10))
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), golden[f"tg_sgd_{k}"]), k
+    np.testing.assert_allclose([h.objective for h in r.history], golden["tg_sgd_hist_obj"],
+                               rtol=1e-12)
+    assert all(h.rms is None for h in r.history) and (r.alpha, r.beta) == (0.0, 0.0)
+    box, bound, ap, ad = golden["tg_sgd_flags"]
+    assert (r.box_feasible, r.iterate_bound_ok, r.apply_count) == (bool(box), bool(bound), ap)
+    # without history the graph path gives the same trajectory
+    r2 = eq.sgd_equilibrate_targets(M, golden["tg_r"], golden["tg_c"],
+                                    eq.EquilibrationParams(iterations=30, seed=4))
+    assert np.array_equal(r2.u, r.u) and np.array_equal(r2.e, r.e)
+    # and the uniform path on the same handle is unaffected afterwards
+    u = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=40, seed=5))
+    assert np.array_equal(u.u, golden["sp_sgd_u"])
+    with pytest.raises(eq.InvalidArgument, match="sum"):
+        eq.sgd_equilibrate_targets(M, golden["tg_r"], 2 * golden["tg_c"])
+    with pytest.raises(eq.InvalidArgument, match="positive"):
+        eq.sgd_equilibrate_targets(M, -golden["tg_r"], golden["tg_c"])
+
+
+def test_targets_variant_dense_vs_oracle(C, golden):
+    A = csr_from_golden(golden, "dn")
+    rng = np.random.default_rng(8)
+    rr = rng.uniform(0.2, 3.0, A.m)
+    cc = rng.uniform(0.2, 3.0, A.n)
+    cc *= rr.sum() / cc.sum()
+    want = C.sgd_equilibrate_targets(A, rr, cc, iterations=25, seed=9)
+    got = eq.sgd_equilibrate_targets(device_matrix(A), rr, cc,
+                                     eq.EquilibrationParams(iterations=25, seed=9))
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+
+
 # ---------------------------------------------------------------- COO ingest (f2)
 def test_coo_ingest_equals_reference_construction(golden):
     """ExplicitMatrix::sparse from shuffled COO triplets on device: same CSR

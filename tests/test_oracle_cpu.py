@@ -124,6 +124,26 @@ def test_oracle_matches_reference_golden(C, golden, key):
             pp.adjoint_count] == list(golden[f"{key}_plsqr_meta"])
 
 
+def test_oracle_targets_variant_matches_reference_golden(C, golden):
+    """sgd_equilibrate_targets (src/variants.cpp:105-118) on the oracle vs the
+    reference's own sources (golden)."""
+    A = csr_from_golden(golden, "sp")
+    s = C.sgd_equilibrate_targets(A, golden["tg_r"], golden["tg_c"], iterations=30, seed=4,
+                                  diag_stride=10)
+    for k in "uvde":
+        assert np.array_equal(getattr(s, k), golden[f"tg_sgd_{k}"])
+    assert np.array_equal(s.hist_objective, golden["tg_sgd_hist_obj"])
+    # uniform targets reproduce sgd_equilibrate bit for bit (test_variants.cpp:97-110)
+    al = (A.n / A.m) ** 0.25
+    be = (A.m / A.n) ** 0.25
+    a, b = C.sgd_equilibrate(A, iterations=40, seed=5), C.sgd_equilibrate_targets(
+        A, np.full(A.m, al * al), np.full(A.n, be * be), iterations=40, seed=5)
+    import math
+    if (al, be) == (math.pow(A.n / A.m, 0.25), math.pow(A.m / A.n, 0.25)):
+        for k in "uvde":
+            assert np.array_equal(getattr(a, k), getattr(b, k))
+
+
 @pytest.mark.skipif(not oracle.ref_available(), reason="reference sources absent")
 def test_oracle_matches_live_reference_random():
     """Live: C restatement vs the reference's own sources on fresh inputs."""
