@@ -33,7 +33,10 @@ constexpr int kSliceChunk = 16;  // products per row per lock-step round (kind 2
 constexpr int kSliceStride = 18; // padded row stride (doubles): conflict-free LDS.128
 constexpr int kSliceBatch = EQ_SLICE_BATCH;  // row pairs staged per batch (loads in flight)
 constexpr int kSliceRows = 32;
-constexpr int kSliceWindow = 4096;  // rows are length-sorted within windows
+#ifndef EQ_SLICE_WINDOW
+#define EQ_SLICE_WINDOW 4096
+#endif
+constexpr int kSliceWindow = EQ_SLICE_WINDOW;  // rows are length-sorted within windows
 constexpr int kWarpSmem = kTileNnz > 32 * kSliceStride ? kTileNnz : 32 * kSliceStride;
 constexpr int kTileWarps = 4;    // independent warps per CTA
 constexpr int kTileThreads = 32 * kTileWarps;
@@ -43,8 +46,11 @@ struct __align__(16) RowMeta {
   int32_t k0;     // row start relative to start
   int32_t len;    // row end relative to start
 };
-constexpr int kLongChunk = 64;    // products per row per round (kind 3)
-constexpr int kLongStride = 66;   // padded row stride (doubles): conflict-free LDS.128
+#ifndef EQ_LONG_CHUNK
+#define EQ_LONG_CHUNK 64
+#endif
+constexpr int kLongChunk = EQ_LONG_CHUNK;      // products per row per round (kind 3)
+constexpr int kLongStride = kLongChunk + 2;    // padded stride: conflict-free LDS.128
 constexpr int kLongBatch = EQ_LONG_BATCH;  // rows per staging batch per warp
 struct SliceMeta {
   RowMeta r[32];

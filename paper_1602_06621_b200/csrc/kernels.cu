@@ -652,21 +652,22 @@ __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __r
   double acc = 0.0;
   for (int b = 0; b < maxr; ++b) {
     const int off = b * kLongChunk;
-    // warp w stages rows w, w+4, ... : 2 products per lane per row
+    // warp w stages rows w, w+4, ... : kLongChunk / 32 products per lane per row
+    constexpr int kPer = kLongChunk / 32;
 #pragma unroll 1
     for (int q0 = warp; q0 < cnt; q0 += 4 * kLongBatch) {
-      int32_t c[2 * kLongBatch];
-      double v[2 * kLongBatch];
-      bool ok[2 * kLongBatch];
+      int32_t c[kPer * kLongBatch];
+      double v[kPer * kLongBatch];
+      bool ok[kPer * kLongBatch];
 #pragma unroll
       for (int u = 0; u < kLongBatch; ++u) {
         const int q = q0 + 4 * u;
         RowMeta rm{0, 1, 0};
         if (q < cnt) rm = sm.r[q];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kPer; ++h) {
           const int rel = off + lane + 32 * h;
-          const int i = 2 * u + h;
+          const int i = kPer * u + h;
           ok[i] = rel >= rm.k0 && rel < rm.len;
           if (ok[i]) {
             c[i] = ld_na(ci + rm.start + rel);
@@ -677,10 +678,10 @@ __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __r
 #pragma unroll
       for (int u = 0; u < kLongBatch; ++u)
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (ok[2 * u + h])
+        for (int h = 0; h < kPer; ++h)
+          if (ok[kPer * u + h])
             sp[(q0 + 4 * u) * kLongStride + lane + 32 * h] =
-                __dmul_rn(v[2 * u + h], __ldg(xg + c[2 * u + h]));
+                __dmul_rn(v[kPer * u + h], __ldg(xg + c[kPer * u + h]));
     }
     __syncthreads();
     if (warp == 0 && rounds > b)
