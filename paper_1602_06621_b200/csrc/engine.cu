@@ -142,6 +142,11 @@ struct DevBuf {
     CK(cudaMalloc(&p, count * sizeof(T)));
     n = count;
   }
+  void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'ed array
+    release();
+    p = q;
+    n = count;
+  }
   void ensure(size_t count) {
     if (count > n || !p) alloc(count);
   }
@@ -339,6 +344,16 @@ struct equil_matrix {
   DevBuf<int32_t> rowlist_a, rowlist_t;
   int n_sgd = 0, n_a = 0, n_t = 0;
   int n_sgd_long = 0;  // leading kind-3 entries of tiles_sgd
+  // column-panel layout of the local A / A^T shards (panel.cu), built when
+  // EQUIL_PANEL=1 at creation; n_pbands == 0 selects the row-slice traversal
+  // above (the default: faster on B200)
+  bool use_panels = false;
+  DevBuf<double> pval[2];
+  DevBuf<uint16_t> pcol[2];
+  DevBuf<uint32_t> pruns[2];
+  DevBuf<eqb::PanelChunk> pchunks[2];
+  DevBuf<eqb::PanelBand> pbands;
+  int n_pbands = 0;
 
   // dense
   DevBuf<double> Ad, colpart;
@@ -400,6 +415,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   M->device = cfg ? cfg->device : 0;
   M->rank = cfg ? cfg->rank : 0;
   M->world = cfg ? std::max(1, cfg->world_size) : 1;
+  if (const char* e = getenv("EQUIL_PANEL")) M->use_panels = atoi(e) != 0;  // A/B knob
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -461,6 +477,65 @@ void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
   nccl_check(nccl().AllGather(buf + M->rank * maxcnt, buf, static_cast<size_t>(maxcnt),
                               ncclFloat64, M->comm, M->stream),
              "ncclAllGather");
+}
+
+// Bands for the column-panel traversal: consecutive rows, closed before a row
+// that would push the band past `target` entries or kBandRows rows.
+std::vector<int64_t> plan_bands(const int64_t* rp, int64_t rows, int64_t target) {
+  std::vector<int64_t> b{0};
+  for (int64_t i = 0; i < rows; ++i) {
+    const int64_t r0 = b.back();
+    if (i > r0 && (i - r0 >= eqb::kBandRows || rp[i + 1] - rp[r0] > target)) b.push_back(i);
+  }
+  if (rows > 0) b.push_back(rows);
+  return b;
+}
+
+// Panel-major copies of the local A / A^T shards and the band list of the SGD
+// launch (both matrices, largest bands first).  Band size targets about
+// EQUIL_BANDS_PER_SM (default 2) bands per SM over the whole launch.
+void build_panel_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT) {
+  M->n_pbands = 0;
+  if (!M->use_panels) return;
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double per_sm = 2.0;
+  if (const char* e = getenv("EQUIL_BANDS_PER_SM")) per_sm = std::max(0.1, atof(e));
+  const int64_t total = M->A.nnz + M->AT.nnz;
+  const int64_t target = std::max<int64_t>(1, static_cast<int64_t>(total / (per_sm * sms)));
+  std::vector<std::pair<int64_t, eqb::PanelBand>> all;
+  for (int mat = 0; mat < 2; ++mat) {
+    const eqb::DevCsr& C = mat ? M->AT : M->A;
+    const int64_t* rp = mat ? rpT : rpA;
+    const std::vector<int64_t> bounds = plan_bands(rp, C.rows, target);
+    const int nb = static_cast<int>(bounds.size()) - 1;
+    if (nb <= 0) continue;
+    M->pval[mat].alloc(C.nnz);
+    M->pcol[mat].alloc(C.nnz);
+    eqb::PanelChunk* ch = nullptr;
+    uint32_t* runs = nullptr;
+    int64_t nch = 0, nruns = 0;
+    std::vector<int64_t> bc;
+    CK(eqb::build_panels(C, mat ? M->m_pad() : M->n_pad(), bounds, M->pval[mat].p,
+                         M->pcol[mat].p, &runs, &nruns, &ch, &nch, &bc, M->stream));
+    M->pchunks[mat].adopt(ch, static_cast<size_t>(std::max<int64_t>(1, nch)));
+    M->pruns[mat].adopt(runs, static_cast<size_t>(std::max<int64_t>(1, nruns)));
+    for (int b = 0; b < nb; ++b) {
+      eqb::PanelBand pb{static_cast<int32_t>(bounds[b]),
+                        static_cast<int32_t>(bounds[b + 1] - bounds[b]),
+                        static_cast<int32_t>(bc[b]), static_cast<int32_t>(bc[b + 1]), mat, 0};
+      all.push_back({rp[bounds[b + 1]] - rp[bounds[b]], pb});
+    }
+  }
+  std::stable_sort(all.begin(), all.end(),
+                   [](const auto& x, const auto& y) { return x.first > y.first; });
+  std::vector<eqb::PanelBand> h;
+  for (const auto& x : all) h.push_back(x.second);
+  M->pbands.alloc(h.size());
+  if (!h.empty())
+    CK(cudaMemcpy(M->pbands.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+  M->n_pbands = static_cast<int>(h.size());
 }
 
 // Build local shards from the full device CSR(A) and CSR(A^T).
@@ -529,6 +604,7 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   const std::vector<int64_t> lt = local_rp(rpT_host, M->t_bounds);
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
                plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
+  build_panel_layout(M, la.data(), lt.data());
 }
 
 void alloc_workspaces(equil_matrix* M);
@@ -575,6 +651,7 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
       upload_plans(M, *planA, planT);
     else
       upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
+    build_panel_layout(M, row_ptr, rpT.data());
   } else {
     const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
     shard_sparse(M, fullA, fullT, rpA, rpT);
@@ -586,8 +663,11 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
 }
 
 void alloc_workspaces(equil_matrix* M) {
-  const int64_t np = M->n_pad(), mp = M->m_pad();
+  // each vector padded to whole panels (the panel traversal bulk-copies them)
+  auto whole = [](int64_t x) { return (x + eqb::kPanelW - 1) / eqb::kPanelW * eqb::kPanelW; };
+  const int64_t np = whole(M->n_pad()), mp = whole(M->m_pad());
   M->xbuf.alloc(2 * (np + mp));
+  CK(cudaMemset(M->xbuf.p, 0, 2 * (np + mp) * sizeof(double)));
   for (int b = 0; b < 2; ++b) {
     M->xs[b].p = M->xbuf.p + b * np;
     M->xw[b].p = M->xbuf.p + 2 * np + b * mp;
@@ -1051,6 +1131,14 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       a.flags = M->flags.p;
       return a;
     };
+    eqb::PanelArgs panel_args{};
+    panel_args.bands = M->pbands.p;
+    for (int k = 0; k < 2; ++k) {
+      panel_args.chunks[k] = M->pchunks[k].p;
+      panel_args.val[k] = M->pval[k].p;
+      panel_args.col[k] = M->pcol[k].p;
+      panel_args.runs[k] = M->pruns[k].p;
+    }
     auto dense_args = [&](int t) {
       eqb::DenseIterArgs a{};
       a.A = M->Ad.p;
@@ -1081,7 +1169,10 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       if (M->dense) {
         CK(eqb::launch_dense_sgd_iter(dense_args(t), s));
       } else {
-        CK(eqb::launch_sgd_iter(iter_args(t), M->n_sgd, s));
+        if (M->n_pbands)
+          CK(eqb::launch_sgd_panel(iter_args(t), panel_args, M->n_pbands, s));
+        else
+          CK(eqb::launch_sgd_iter(iter_args(t), M->n_sgd, s));
         if (t < T) {
           allgather_padded(M, M->xs[t & 1].p, M->t_max);
           allgather_padded(M, M->xw[t & 1].p, M->a_max);

@@ -1,0 +1,122 @@
+// sgd_common.cuh -- device helpers shared by the SGD traversals (kernels.cu:
+// warp tiles / long slices, panel.cu: column panels): streamed loads, the
+// sequential row sum and the fused u/v epilogue.
+#pragma once
+
+#include "internal.h"
+
+namespace eqb {
+
+// read-only load that does not allocate in L1 (streamed CSR arrays)
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_na(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ bool sign_bit(const uint32_t* bits, int64_t b) {
+  return (__ldg(bits + (b >> 5)) >> (b & 31)) & 1u;
+}
+
+// Products p[k - k0] = val[k] * xg[col[k]] for k in [k0, k1), one warp,
+// coalesced streaming loads of val/col, gathers through the read-only path.
+// The product is one rounded multiply whoever computes it, so staging it in
+// any order leaves the sequential sum below bit-identical to the reference.
+__device__ __forceinline__ void warp_stage(const int32_t* __restrict__ ci,
+                                           const double* __restrict__ va,
+                                           const double* __restrict__ xg,
+                                           int64_t k0, int64_t k1,
+                                           double* __restrict__ sp, int lane) {
+  constexpr int U = kStageUnroll;
+  for (int64_t kb = k0 + lane; kb < k1; kb += 32 * U) {
+    int32_t c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = kb + 32 * u;
+      if (k < k1) {
+        c[u] = __ldcs(ci + k);
+        v[u] = __ldcs(va + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = kb + 32 * u;
+      if (k < k1) sp[k - k0] = __dmul_rn(v[u], __ldg(xg + c[u]));
+    }
+  }
+}
+
+// Sequential CSR-order sum of sp[b, e) onto acc (explicit_matrix.cpp:73-75).
+// The adds form one dependent chain; the shared-memory loads feeding it are
+// software-pipelined 8 products ahead (16-byte LDS) so the chain runs at add
+// latency instead of load latency.
+__device__ __forceinline__ double chain_sum(double acc, const double* sp, int b,
+                                            int e) {
+  int k = b;
+  if ((k & 1) && k < e) acc = __dadd_rn(acc, sp[k++]);
+  const double2* s2 = reinterpret_cast<const double2*>(sp);  // sp is 16B aligned
+  int k2 = k >> 1;
+  const int e2 = e >> 1;
+  if (k2 + 4 <= e2) {
+    double2 c0 = s2[k2], c1 = s2[k2 + 1], c2 = s2[k2 + 2], c3 = s2[k2 + 3];
+    for (k2 += 4; k2 + 4 <= e2; k2 += 4) {
+      const double2 n0 = s2[k2], n1 = s2[k2 + 1], n2 = s2[k2 + 2], n3 = s2[k2 + 3];
+      acc = __dadd_rn(acc, c0.x); acc = __dadd_rn(acc, c0.y);
+      acc = __dadd_rn(acc, c1.x); acc = __dadd_rn(acc, c1.y);
+      acc = __dadd_rn(acc, c2.x); acc = __dadd_rn(acc, c2.y);
+      acc = __dadd_rn(acc, c3.x); acc = __dadd_rn(acc, c3.y);
+      c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    acc = __dadd_rn(acc, c0.x); acc = __dadd_rn(acc, c0.y);
+    acc = __dadd_rn(acc, c1.x); acc = __dadd_rn(acc, c1.y);
+    acc = __dadd_rn(acc, c2.x); acc = __dadd_rn(acc, c2.y);
+    acc = __dadd_rn(acc, c3.x); acc = __dadd_rn(acc, c3.y);
+  }
+  for (; k2 < e2; ++k2) {
+    const double2 c = s2[k2];
+    acc = __dadd_rn(acc, c.x);
+    acc = __dadd_rn(acc, c.y);
+  }
+  if ((e & 1) && e - 1 >= k) acc = __dadd_rn(acc, sp[e - 1]);
+  return acc;
+}
+
+__device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
+                                             int64_t r, double acc,
+                                             unsigned& fl) {
+  const int64_t pi = a.poff[mat] + r;
+  // |d_i w_i| = d_i exactly (w = +-1): this iteration's d (mat 0) or e (mat 1)
+  const double scl = fabs(mat ? a.xs_cur[pi] : a.xw_cur[pi]);
+  const double y = __dmul_rn(scl, acc);          // linop.cpp:19 / :25
+  const double est = __dmul_rn(y, y);            // estimator.cpp:8
+  double avg = a.avg[mat][r];
+  const double xn = a.lin[mat]
+                        ? sgd_coord_lin(est, a.x[mat][r], a.lin[mat][r], a.c[mat], a.st, avg, fl)
+                        : sgd_coord(est, a.x[mat][r], a.c[mat], a.st, avg, fl);
+  a.x[mat][r] = xn;
+  a.avg[mat][r] = avg;
+  if (a.has_next) {  // next iteration's e.*s (from v) / d.*w (from u)
+    const double dn = det_exp(xn);
+    const bool pos = sign_bit(a.signs, a.sign_next[mat] + r);
+    (mat ? a.xs_next : a.xw_next)[pi] = pos ? dn : -dn;
+  }
+}
+__device__ __forceinline__ uint32_t ld_na(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint16_t ld_na(const uint16_t* p) {
+  unsigned short v;
+  asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+
+}  // namespace eqb

@@ -290,6 +290,27 @@ def test_sgd_scaled_config3_bit_exact(C):
     assert (got.box_feasible, got.iterate_bound_ok) == (want.box_feasible, want.iterate_bound_ok)
 
 
+@pytest.mark.parametrize("case", ["sp", "lr", "c3"])
+def test_panel_traversal_bit_exact(C, golden, monkeypatch, case):
+    """The opt-in column-panel traversal (panel.cu, EQUIL_PANEL=1): same
+    trajectory bit for bit -- golden cases (rows crossing panels and rounds)
+    and c3's generator at 2% scale (bands, many panels, long rows)."""
+    monkeypatch.setenv("EQUIL_PANEL", "1")
+    if case == "c3":
+        from paper_1602_06621_b200 import configs
+        inst = configs.config(3, scale=0.02)
+        A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+        want = C.sgd_equilibrate(A, iterations=20, seed=7)
+        got = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(iterations=20, seed=7))
+        want = {k: getattr(want, k) for k in "uvde"}
+    else:
+        A = csr_from_golden(golden, case)
+        got = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(iterations=40, seed=5))
+        want = {k: golden[f"{case}_sgd_{k}"] for k in "uvde"}
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), want[k]), k
+
+
 def test_lsqr_config1_bit_exact(C):
     from paper_1602_06621_b200 import configs
     inst = configs.config(1)
