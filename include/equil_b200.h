@@ -48,8 +48,12 @@ typedef struct {
 } equil_params;
 
 /* Device placement.  world_size > 1 row-shards A and A^T across one process per
- * GPU and all-gathers e.*s and d.*w with NCCL each iteration; nccl_id points to
- * the 128-byte ncclUniqueId shared by all ranks (ignored when world_size == 1). */
+ * GPU and all-gathers e.*s and d.*w with NCCL each iteration (SGD), and the
+ * gathered LSQR vectors after every update (LSQR; norms are reduced over the
+ * whole vector in global order, so every rank sees the single-GPU scalars);
+ * nccl_id points to the 128-byte ncclUniqueId shared by all ranks (ignored
+ * when world_size == 1).  Every rank calls every entry point collectively and
+ * receives the full-length results. */
 typedef struct {
   int device;
   int rank;

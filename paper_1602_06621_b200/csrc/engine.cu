@@ -1000,7 +1000,6 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       dp.stride = diag->stride;
       dp.obj = diag->want_objective != 0;
       dp.rms = diag->want_rms != 0;
-      require(M->world == 1, "sgd_equilibrate: history is single-GPU in this build");
       require(!M->dense, "sgd_equilibrate: history is implemented for sparse matrices");
       require(out->hist_cap >= p->iterations / dp.stride + 1,
               "sgd_equilibrate: history capacity too small");
@@ -1048,41 +1047,105 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     }
 
     // history (src/equilibrate.cpp:174-195) into device slots, read at the end:
-    // per record [rms_acc, quad, lin_u.u, lin_v.v, |u|^2, |v|^2]
+    // per record [rms_acc, quad, lin_u.u, lin_v.v, |u|^2, |v|^2].  Every term
+    // vector is reduced in global order; with world > 1 the local terms are
+    // written into the padded layout, all-gathered and un-padded first, so the
+    // record is identical for any number of GPUs.
     constexpr int kRec = 6;
     const int nrec = dp.stride ? T / dp.stride + 1 : 0;
-    DevBuf<double> hist, terms;
+    const bool multi = M->world > 1;
+    const int64_t ml = M->m_loc(), nl = M->n_loc();
+    DevBuf<double> hist, terms, eu_p, ev_p, ta_p, tt_p, ub_f, vb_f, vb_p;
     if (nrec) {
       hist.alloc(kRec * nrec);
       CK(cudaMemsetAsync(hist.p, 0, kRec * nrec * 8, s));
       terms.alloc(m + n);
+      eu_p.alloc(M->m_pad());
+      ev_p.alloc(M->n_pad());
+      if (multi) {
+        ta_p.alloc(M->m_pad());
+        tt_p.alloc(M->n_pad());
+        ub_f.alloc(m);
+        vb_f.alloc(n);
+        vb_p.alloc(M->n_pad());
+      }
     }
+    // local slice -> padded buffer (gathered); world 1: the slice is the vector
+    auto to_padded = [&](const double* loc, int64_t cnt, bool mside, double* pad) {
+      if (!multi) return;
+      const int64_t off = mside ? a_poff : t_poff;
+      if (loc != pad + off)
+        CK(cudaMemcpyAsync(pad + off, loc, cnt * 8, cudaMemcpyDeviceToDevice, s));
+      allgather_padded(M, pad, mside ? M->a_max : M->t_max);
+    };
+    auto unpad_to = [&](const double* pad, bool mside, double* dst) {
+      const int64_t full = mside ? m : n;
+      const int64_t maxcnt = mside ? M->a_max : M->t_max;
+      unpad_kernel<<<static_cast<unsigned>((full + 255) / 256), 256, 0, s>>>(
+          dst, pad, (mside ? M->a_bounds_d : M->t_bounds_d).p, M->world, maxcnt, full);
+      CK(cudaGetLastError());
+    };
     int rec = 0;
     auto record = [&](int) {
       double* slot = hist.p + kRec * rec;
       if (dp.rms && alpha > 0.0 && beta > 0.0) {  // rms_error (src/metrics.cpp:41-56)
-        double* eu = M->tmp_m.p;
-        double* ev = M->tmp_n.p;
-        CK(eqb::launch_exp(M->ub.p, eu, m, 2.0, s));
-        CK(eqb::launch_exp(M->vb.p, ev, n, 2.0, s));
-        CK(eqb::launch_rms_terms(0, M->A, eu, ev, terms.p, 0, alpha, s));
-        CK(eqb::launch_rms_terms(1, M->AT, eu, ev, terms.p + m, 0, beta, s));
+        CK(eqb::launch_exp(M->ub.p, eu_p.p + a_poff, ml, 2.0, s));
+        CK(eqb::launch_exp(M->vb.p, ev_p.p + t_poff, nl, 2.0, s));
+        to_padded(eu_p.p + a_poff, ml, true, eu_p.p);
+        to_padded(ev_p.p + t_poff, nl, false, ev_p.p);
+        double* ta = multi ? ta_p.p + a_poff : terms.p;
+        double* tt = multi ? tt_p.p + t_poff : terms.p + m;
+        CK(eqb::launch_rms_terms(0, M->A, eu_p.p, ev_p.p, ta, a_poff, alpha, s));
+        CK(eqb::launch_rms_terms(1, M->AT, eu_p.p, ev_p.p, tt, t_poff, beta, s));
+        if (multi) {
+          to_padded(ta, ml, true, ta_p.p);
+          to_padded(tt, nl, false, tt_p.p);
+          unpad_to(ta_p.p, true, terms.p);
+          unpad_to(tt_p.p, false, terms.p + m);
+        }
         canon_reduce(M, terms.p, m + n, slot + 0, 1);
       }
       if (dp.obj) {  // objective_weighted (src/equilibrate.cpp:10-22)
-        CK(eqb::launch_obj_terms(M->A, M->ub.p, M->vb.p, terms.p, s));
+        const double* ubf = M->ub.p;  // whole ubar / vbar in global order
+        const double* vbf = M->vb.p;
+        const double* vbp = M->vb.p;  // vbar in padded coordinates (gathered)
+        if (multi) {
+          to_padded(M->ub.p, ml, true, ta_p.p);
+          unpad_to(ta_p.p, true, ub_f.p);
+          to_padded(M->vb.p, nl, false, vb_p.p);
+          unpad_to(vb_p.p, false, vb_f.p);
+          ubf = ub_f.p;
+          vbf = vb_f.p;
+          vbp = vb_p.p;
+        }
+        double* ot = multi ? ta_p.p + a_poff : terms.p;
+        CK(eqb::launch_obj_terms(M->A, M->ub.p, vbp, ot, s));
+        if (multi) {
+          to_padded(ot, ml, true, ta_p.p);
+          unpad_to(ta_p.p, true, terms.p);
+        }
         canon_reduce(M, terms.p, m, slot + 1, 1);
         if (vec_lin) {  // lin_u.dot(u): rounded products, canonical sum
-          CK(eqb::launch_mul(terms.p, M->lin_u.p, M->ub.p, m, s));
+          double* pu = multi ? ta_p.p + a_poff : terms.p;
+          CK(eqb::launch_mul(pu, M->lin_u.p, M->ub.p, ml, s));
+          if (multi) {
+            to_padded(pu, ml, true, ta_p.p);
+            unpad_to(ta_p.p, true, terms.p);
+          }
           canon_reduce(M, terms.p, m, slot + 2, 1);
-          CK(eqb::launch_mul(terms.p, M->lin_v.p, M->vb.p, n, s));
+          double* pv = multi ? tt_p.p + t_poff : terms.p;
+          CK(eqb::launch_mul(pv, M->lin_v.p, M->vb.p, nl, s));
+          if (multi) {
+            to_padded(pv, nl, false, tt_p.p);
+            unpad_to(tt_p.p, false, terms.p);
+          }
           canon_reduce(M, terms.p, n, slot + 3, 1);
         } else {
-          canon_reduce(M, M->ub.p, m, slot + 2, 2, lin_u);
-          canon_reduce(M, M->vb.p, n, slot + 3, 2, lin_v);
+          canon_reduce(M, ubf, m, slot + 2, 2, lin_u);
+          canon_reduce(M, vbf, n, slot + 3, 2, lin_v);
         }
-        canon_reduce(M, M->ub.p, m, slot + 4, 0);
-        canon_reduce(M, M->vb.p, n, slot + 5, 0);
+        canon_reduce(M, ubf, m, slot + 4, 0);
+        canon_reduce(M, vbf, n, slot + 5, 0);
       }
       ++rec;
     };
@@ -1217,8 +1280,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     M->last_loop_iters = T;
 
     // finalize: u = ubar, v = vbar, d = exp(ubar), e = exp(vbar) (:201-204)
-    const int64_t ml = M->m_loc(), nl = M->n_loc();
-    double* dloc = M->tmp_m.p;
+        double* dloc = M->tmp_m.p;
     double* eloc = M->tmp_n.p;
     CK(eqb::launch_exp(M->ub.p, dloc, ml, 1.0, s));
     CK(eqb::launch_exp(M->vb.p, eloc, nl, 1.0, s));
@@ -1398,54 +1460,109 @@ struct LsqrState {
   long long applies = 0, adjoints = 0;
 };
 
-// lsqr_core (:17-81) on B = diag(d) A diag(e) (d, e device or null) with rhs c
-void lsqr_core(equil_matrix* M, const double* c, const double* b_d, double bnorm,
+// Row-sharded LSQR vectors.  m-side vectors (u, the residual) live as local
+// slices of A's rows, n-side ones (v, w, x) as local slices of A^T's rows;
+// the vectors a pass gathers from (d.*u, e.*v, e.*x) are kept in the padded
+// layout of the SGD loop and all-gathered after every update.  A norm is the
+// canonical reduction of the whole vector in global order: the padded buffer
+// is all-gathered and un-padded first, so every rank computes the identical
+// scalar for any world size (world 1: no copies).
+struct LsqrLayout {
+  equil_matrix* M;
+  int64_t mL, nL, mP, nP, pa, pt;
+  DevBuf<double> flat_m, flat_n;
+  explicit LsqrLayout(equil_matrix* m_) : M(m_) {
+    mL = M->m_loc();
+    nL = M->n_loc();
+    mP = M->m_pad();
+    nP = M->n_pad();
+    pa = M->world == 1 ? 0 : M->rank * M->a_max;
+    pt = M->world == 1 ? 0 : M->rank * M->t_max;
+    if (M->world > 1) {
+      flat_m.alloc(M->m);
+      flat_n.alloc(M->n);
+    }
+  }
+  void gather(double* pad, bool mside) {
+    allgather_padded(M, pad, mside ? M->a_max : M->t_max);
+  }
+  // out_dev = |v| for the padded vector whose local slice was just written
+  void norm(double* pad, bool mside, double* out_dev) {
+    const int64_t full = mside ? M->m : M->n;
+    if (M->world == 1) {
+      canon_reduce(M, pad, full, out_dev, 0, 0.0, true);
+      return;
+    }
+    const int64_t maxcnt = mside ? M->a_max : M->t_max;
+    double* flat = mside ? flat_m.p : flat_n.p;
+    gather(pad, mside);
+    unpad_kernel<<<static_cast<unsigned>((full + 255) / 256), 256, 0, M->stream>>>(
+        flat, pad, (mside ? M->a_bounds_d : M->t_bounds_d).p, M->world, maxcnt, full);
+    CK(cudaGetLastError());
+    canon_reduce(M, flat, full, out_dev, 0, 0.0, true);
+  }
+};
+
+// lsqr_core (:17-81) on B = diag(d) A diag(e) (d, e local slices or null) with
+// local rhs slice c; x receives the local slice of the solution
+void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bnorm,
                const double* d, const double* e, int max_iters, double tol,
                double* hist, int hist_cap, LsqrState& st, DevBuf<double>& x) {
   cudaStream_t s = M->stream;
-  const int64_t m = M->m, n = M->n;
-  DevBuf<double> u, un, v, vn, w, du, ev, ex, r;
-  u.alloc(m); un.alloc(m); du.alloc(m); r.alloc(m);
-  v.alloc(n); vn.alloc(n); w.alloc(n); ev.alloc(n); ex.alloc(n);
-  x.alloc(n);
-  CK(cudaMemsetAsync(x.p, 0, n * 8, s));
+  LsqrLayout L(M);
+  DevBuf<double> u, v, w, un, du, vn, ev, ex, r;
+  u.alloc(L.mL); v.alloc(L.nL); w.alloc(L.nL); x.alloc(L.nL);
+  un.alloc(L.mP); du.alloc(L.mP); r.alloc(L.mP);
+  vn.alloc(L.nP); ev.alloc(L.nP); ex.alloc(L.nP);
+  double* unL = un.p + L.pa;
+  double* duL = du.p + L.pa;
+  double* rL = r.p + L.pa;
+  double* vnL = vn.p + L.pt;
+  double* evL = ev.p + L.pt;
+  double* exL = ex.p + L.pt;
+  CK(cudaMemsetAsync(x.p, 0, L.nL * 8, s));
   double* sc = M->scal.p;  // [0] beta, [1] alpha, [2] residual norm
   int* dummy = reinterpret_cast<int*>(sc + 8);
 
-  canon_reduce(M, c, m, sc + 0, 0, 0.0, true);  // beta = |c|
-  CK(eqb::launch_lsqr_normalize(u.p, c, sc + 0, du.p, d, m, nullptr, nullptr, s));
-  apply_pass(M, true, du.p, v.p, eqb::kPassScaled, e, nullptr, nullptr);  // v = B^T u
+  CK(cudaMemcpyAsync(unL, c, L.mL * 8, cudaMemcpyDeviceToDevice, s));
+  L.norm(un.p, true, sc + 0);  // beta = |c|
+  CK(eqb::launch_lsqr_normalize(u.p, c, sc + 0, duL, d, L.mL, nullptr, nullptr, s));
+  L.gather(du.p, true);
+  apply_pass(M, true, du.p, vnL, eqb::kPassScaled, e, nullptr, nullptr);  // v = B^T u
   ++st.adjoints;
-  canon_reduce(M, v.p, n, sc + 1, 0, 0.0, true);
+  L.norm(vn.p, false, sc + 1);
   double beta = read_scalar(M, sc + 0);
   double alpha = read_scalar(M, sc + 1);
   if (alpha == 0.0) {
     st.breakdown = true;
     return;
   }
-  CK(eqb::launch_lsqr_normalize(v.p, v.p, sc + 1, ev.p, e, n, dummy, nullptr, s));
-  CK(cudaMemcpyAsync(w.p, v.p, n * 8, cudaMemcpyDeviceToDevice, s));
+  CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, dummy, nullptr, s));
+  L.gather(ev.p, false);
+  CK(cudaMemcpyAsync(w.p, v.p, L.nL * 8, cudaMemcpyDeviceToDevice, s));
   double phibar = beta, rhobar = alpha;
 
   for (int t = 1; t <= max_iters; ++t) {
     bool invariant = false;
-    apply_pass(M, false, ev.p, un.p, eqb::kPassLsqrU, d, u.p, sc + 1);  // Bv - alpha u
+    apply_pass(M, false, ev.p, unL, eqb::kPassLsqrU, d, u.p, sc + 1);  // Bv - alpha u
     ++st.applies;
-    canon_reduce(M, un.p, m, sc + 0, 0, 0.0, true);
+    L.norm(un.p, true, sc + 0);
     beta = read_scalar(M, sc + 0);
     if (beta > 0.0) {
-      CK(eqb::launch_lsqr_normalize(u.p, un.p, sc + 0, du.p, d, m, nullptr, nullptr, s));
+      CK(eqb::launch_lsqr_normalize(u.p, unL, sc + 0, duL, d, L.mL, nullptr, nullptr, s));
+      L.gather(du.p, true);
     } else {
       invariant = true;
     }
     alpha = 0.0;
     if (!invariant) {
-      apply_pass(M, true, du.p, vn.p, eqb::kPassLsqrV, e, v.p, sc + 0);  // B^T u - beta v
+      apply_pass(M, true, du.p, vnL, eqb::kPassLsqrV, e, v.p, sc + 0);  // B^T u - beta v
       ++st.adjoints;
-      canon_reduce(M, vn.p, n, sc + 1, 0, 0.0, true);
+      L.norm(vn.p, false, sc + 1);
       alpha = read_scalar(M, sc + 1);
       if (alpha > 0.0) {
-        CK(eqb::launch_lsqr_normalize(v.p, vn.p, sc + 1, ev.p, e, n, nullptr, nullptr, s));
+        CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, nullptr, nullptr, s));
+        L.gather(ev.p, false);
       } else {
         invariant = true;
       }
@@ -1457,10 +1574,11 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_d, double bnorm
     rhobar = -cs * alpha;
     const double phi = cs * phibar;
     phibar = sn * phibar;
-    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, ex.p, n, s));
+    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, exL, L.nL, s));
+    L.gather(ex.p, false);
     st.iterations = t;
-    apply_pass(M, false, ex.p, r.p, eqb::kPassResid, nullptr, b_d, nullptr);
-    canon_reduce(M, r.p, m, sc + 2, 0, 0.0, true);
+    apply_pass(M, false, ex.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr);
+    L.norm(r.p, true, sc + 2);
     const double rel = read_scalar(M, sc + 2) / bnorm;
     if (st.hist_len < hist_cap) hist[st.hist_len] = rel;
     ++st.hist_len;
@@ -1481,10 +1599,10 @@ void lsqr_common(equil_matrix* M, const double* b, const equil_params* p, int ma
   require(b != nullptr, std::string(who) + ": rhs length mismatch");
   std::lock_guard<std::mutex> lk(M->mu);
   DeviceGuard dg(M->device);
-  require(M->world == 1, std::string(who) + ": multi-GPU LSQR is not in this build");
   cudaStream_t s = M->stream;
   const int64_t m = M->m, n = M->n;
-  DevBuf<double> b_d;
+  const int64_t mL = M->m_loc(), nL = M->n_loc();
+  DevBuf<double> b_d;  // the whole rhs on every rank (its norm is global)
   b_d.alloc(m);
   CK(cudaMemcpyAsync(b_d.p, b, m * 8, cudaMemcpyHostToDevice, s));
   canon_reduce(M, b_d.p, m, M->scal.p + 3, 0, 0.0, true);
@@ -1495,11 +1613,14 @@ void lsqr_common(equil_matrix* M, const double* b, const equil_params* p, int ma
   require(out->residual_history != nullptr &&
               out->residual_cap >= max_iters + 1 + (p ? std::max(T, 0) : 0),
           std::string(who) + ": residual_history capacity too small");
+  const double* b_loc = b_d.p + M->a_goff();
   LsqrState st;
   DevBuf<double> dd, ed, c, x;
-  const double* c_ptr = b_d.p;
+  const double* c_ptr = b_loc;
+  const double* d_loc = nullptr;
+  const double* e_loc = nullptr;
   if (p) {
-    // sgd_equilibrate on the charged operator (:115-116), d, e kept on device
+    // sgd_equilibrate on the charged operator (:115-116); full d, e on device
     dd.alloc(m);
     ed.alloc(n);
     equil_scaling_out so{};
@@ -1515,17 +1636,33 @@ void lsqr_common(equil_matrix* M, const double* b, const equil_params* p, int ma
     st.applies = so.apply_count;
     st.adjoints = so.adjoint_count;
     for (int t = 0; t <= T; ++t) out->residual_history[st.hist_len++] = 1.0;  // :121-123
-    c.alloc(m);
-    CK(eqb::launch_mul(c.p, dd.p, b_d.p, m, s));  // c = d .* b (:126)
+    d_loc = dd.p + M->a_goff();
+    e_loc = ed.p + M->t_goff();
+    c.alloc(mL);
+    CK(eqb::launch_mul(c.p, d_loc, b_loc, mL, s));  // c = d .* b (:126)
     c_ptr = c.p;
   } else {
     out->residual_history[st.hist_len++] = 1.0;  // :94
   }
-  lsqr_core(M, c_ptr, b_d.p, bnorm, p ? dd.p : nullptr, p ? ed.p : nullptr, max_iters,
-            tol, out->residual_history, out->residual_cap, st, x);
+  lsqr_core(M, c_ptr, b_loc, bnorm, d_loc, e_loc, max_iters, tol, out->residual_history,
+            out->residual_cap, st, x);
   // x = e .* x_scaled (:134)
-  if (p) CK(eqb::launch_mul(x.p, ed.p, x.p, n, s));
-  if (out->x) CK(cudaMemcpyAsync(out->x, x.p, n * 8, cudaMemcpyDeviceToHost, s));
+  if (p) CK(eqb::launch_mul(x.p, e_loc, x.p, nL, s));
+  if (out->x) {
+    if (M->world == 1) {
+      CK(cudaMemcpyAsync(out->x, x.p, n * 8, cudaMemcpyDeviceToHost, s));
+    } else {  // gather the slices, un-pad, copy out
+      DevBuf<double> pad, flat;
+      pad.alloc(M->n_pad());
+      flat.alloc(n);
+      CK(cudaMemcpyAsync(pad.p + M->rank * M->t_max, x.p, nL * 8, cudaMemcpyDeviceToDevice, s));
+      allgather_padded(M, pad.p, M->t_max);
+      unpad_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+          flat.p, pad.p, M->t_bounds_d.p, M->world, M->t_max, n);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(out->x, flat.p, n * 8, cudaMemcpyDeviceToHost, s));
+    }
+  }
   CK(cudaStreamSynchronize(s));
   out->hist_len = st.hist_len;
   out->iterations = st.iterations;

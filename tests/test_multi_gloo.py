@@ -151,3 +151,104 @@ def test_sharded_trajectory_bit_identical_world2(golden):
 def test_det_exp_numpy_restatement_matches_oracle(C):
     x = np.random.default_rng(2).uniform(-30, 30, 5000)
     assert np.array_equal(det_exp_np(x), C.det_exp(x))
+
+
+def _lsqr_worker(rank, world, port, A_arrays, b, iters, out_q):
+    """Row-sharded LSQR exactly as engine.cu lsqr_core runs it for world > 1:
+    local slices of u / r (rows of A) and v / w / x (rows of A^T), the gathered
+    d.*u, e.*v, e.*x exchanged after every update, every norm the canonical
+    reduction of the whole (gathered) vector."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    import paper_1602_06621_b200 as eq
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, n, rp, col, val = A_arrays
+    O = oracle.c_oracle()
+    A = oracle.CsrArrays(m, n, rp, col, val)
+    AT = O.transpose(A)
+    ab = eq.partition_rows(rp, world)
+    tb = eq.partition_rows(AT.row_ptr, world)
+    amax, tmax = int(np.max(np.diff(ab))), int(np.max(np.diff(tb)))
+
+    def local(C, bd):
+        r0, r1 = bd[rank], bd[rank + 1]
+        k0, k1 = C.row_ptr[r0], C.row_ptr[r1]
+        return oracle.CsrArrays(r1 - r0, C.n, C.row_ptr[r0:r1 + 1] - k0, C.col[k0:k1],
+                                C.val[k0:k1]), r0, r1
+
+    Al, a0, a1 = local(A, ab)
+    Tl, t0, t1 = local(AT, tb)
+
+    def gather(loc, mx, bounds, full):
+        pad = torch.zeros(mx, dtype=torch.float64)
+        pad[:loc.size] = torch.from_numpy(loc)
+        parts = [torch.zeros(mx, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        outv = np.zeros(full)
+        for g in range(world):
+            outv[bounds[g]:bounds[g + 1]] = parts[g].numpy()[:bounds[g + 1] - bounds[g]]
+        return outv
+
+    def gnorm(loc, mside):
+        full = gather(loc, amax, ab, m) if mside else gather(loc, tmax, tb, n)
+        return np.sqrt(O.canon_sumsq(full))
+
+    bnorm = np.sqrt(O.canon_sumsq(b))
+    bl = b[a0:a1]
+    hist = [1.0]
+    x = np.zeros(t1 - t0)
+    beta = gnorm(bl, True)
+    u = bl / beta
+    v = O.apply(Tl, gather(u, amax, ab, m))
+    alpha = gnorm(v, False)
+    v = v / alpha
+    w = v.copy()
+    phibar, rhobar = beta, alpha
+    for _ in range(iters):
+        un = O.apply(Al, gather(v, tmax, tb, n)) - alpha * u
+        beta = gnorm(un, True)
+        u = un / beta
+        vn = O.apply(Tl, gather(u, amax, ab, m)) - beta * v
+        alpha = gnorm(vn, False)
+        v = vn / alpha
+        rho = float(np.hypot(rhobar, beta))
+        cs, sn = rhobar / rho, beta / rho
+        theta = sn * alpha
+        rhobar = -cs * alpha
+        phi = cs * phibar
+        phibar = sn * phibar
+        x = x + (phi / rho) * w
+        w = v - (theta / rho) * w
+        r = bl - O.apply(Al, gather(x, tmax, tb, n))
+        hist.append(gnorm(r, True) / bnorm)
+    X = gather(x, tmax, tb, n)
+    if rank == 0:
+        out_q.put((np.array(hist), X))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_lsqr_bit_identical_world2(golden):
+    from conftest import csr_from_golden
+    import oracle
+    A = csr_from_golden(golden, "sp")
+    b = golden["sp_b"]
+    iters = 12
+    want = oracle.c_oracle().lsqr(A, b, iters, 0.0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lsqr_worker,
+                         args=(r, 2, port, (A.m, A.n, A.row_ptr, A.col, A.val), b, iters, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    hist, X = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(hist, want.residual_history)
+    assert np.array_equal(X, want.x)
