@@ -161,6 +161,21 @@ equil_status equil_sgd_equilibrate(equil_matrix* A, const equil_params* p,
 equil_status equil_sgd_equilibrate_targets(equil_matrix* A, const double* r, const double* c,
                                            const equil_params* p, const equil_diag_cfg* diag,
                                            equil_scaling_out* out);
+/* sgd_equilibrate_symmetric(op, params, diag) (include/equil/variants.hpp:16-18,
+ * src/variants.cpp:35-103): square symmetric A, one scaling u = v on both
+ * sides, one apply and no adjoint per iteration; the symmetry spot check of
+ * :14-33 runs first.  Single GPU. */
+equil_status equil_sgd_equilibrate_symmetric(equil_matrix* A, const equil_params* p,
+                                             const equil_diag_cfg* diag,
+                                             equil_scaling_out* out);
+/* sgd_equilibrate_block(op, BlockStructure, params, diag)
+ * (include/equil/variants.hpp:30-50, src/variants.cpp:120-240): row i shares
+ * u_{row_block[i]}, column j shares v_{col_block[j]}; results expanded to full
+ * length.  Single GPU. */
+equil_status equil_sgd_equilibrate_block(equil_matrix* A, const int64_t* row_block,
+                                         const int64_t* col_block, int64_t row_blocks,
+                                         int64_t col_blocks, const equil_params* p,
+                                         const equil_diag_cfg* diag, equil_scaling_out* out);
 /* lsqr(op, b, max_iters, tol) (include/equil/lsqr.hpp:30-31, src/lsqr.cpp:85-103) */
 equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
                         equil_lsqr_out* out);

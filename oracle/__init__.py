@@ -185,6 +185,11 @@ class _COracle:
                                          C.POINTER(_Scaling)]
         L.eo_sgd_equilibrate_targets.argtypes = [C.POINTER(_Matrix), _dp, _dp, C.POINTER(_Params),
                                                  C.c_int, C.POINTER(_Scaling)]
+        L.eo_sgd_equilibrate_symmetric.argtypes = [C.POINTER(_Matrix), C.POINTER(_Params),
+                                                   C.c_int, C.POINTER(_Scaling)]
+        L.eo_sgd_equilibrate_block.argtypes = [C.POINTER(_Matrix), _i64p, _i64p, C.c_int64,
+                                               C.c_int64, C.POINTER(_Params), C.c_int,
+                                               C.POINTER(_Scaling)]
         L.eo_objective.restype = C.c_double
         L.eo_objective.argtypes = [C.POINTER(_Matrix), _dp, _dp, C.c_double, C.c_double, C.c_double]
         L.eo_rms_error.restype = C.c_double
@@ -313,6 +318,42 @@ class _COracle:
                        bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
                        hi[:k].copy(), ho[:k].copy(), hr[:k].copy())
 
+    def _variant(self, call, m, n, iterations, diag_stride):
+        u, v, d, e = np.zeros(m), np.zeros(n), np.zeros(m), np.zeros(n)
+        nh = iterations // diag_stride + 1 if diag_stride > 0 else 1
+        hi, ho, hr = np.zeros(nh, np.int32), np.zeros(nh), np.zeros(nh)
+        s = _Scaling(ptr(u, _dp), ptr(v, _dp), ptr(d, _dp), ptr(e, _dp), 0, 0, 0, 0, 0, 0,
+                     ptr(hi, _ip), ptr(ho, _dp), ptr(hr, _dp), 0, ptr(None, _dp),
+                     ptr(None, _dp))
+        rc = call(C.byref(s))
+        if rc:
+            self._err(rc)
+        k = s.hist_len
+        return Scaling(u, v, d, e, s.alpha, s.beta, bool(s.box_feasible),
+                       bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
+                       hi[:k].copy(), ho[:k].copy(), hr[:k].copy())
+
+    def sgd_equilibrate_symmetric(self, A: CsrArrays, alpha=0.0, beta=0.0, gamma=0.1,
+                                  max_log_scale=9.210340371976184, iterations=1000, seed=0,
+                                  diag_stride=0) -> Scaling:
+        """src/variants.cpp:35-103"""
+        p = _Params(alpha, beta, gamma, max_log_scale, iterations, seed)
+        mat = A._struct()
+        return self._variant(lambda s: self.L.eo_sgd_equilibrate_symmetric(
+            C.byref(mat), C.byref(p), diag_stride, s), A.m, A.n, iterations, diag_stride)
+
+    def sgd_equilibrate_block(self, A: CsrArrays, row_block, col_block, row_blocks, col_blocks,
+                              gamma=0.1, max_log_scale=9.210340371976184, iterations=1000,
+                              seed=0, diag_stride=0) -> Scaling:
+        """src/variants.cpp:156-240"""
+        rb = np.ascontiguousarray(row_block, np.int64)
+        cb = np.ascontiguousarray(col_block, np.int64)
+        p = _Params(0.0, 0.0, gamma, max_log_scale, iterations, seed)
+        mat = A._struct()
+        return self._variant(lambda s: self.L.eo_sgd_equilibrate_block(
+            C.byref(mat), ptr(rb, _i64p), ptr(cb, _i64p), row_blocks, col_blocks, C.byref(p),
+            diag_stride, s), A.m, A.n, iterations, diag_stride)
+
     def objective(self, A, u, v, alpha2, beta2, gamma):
         mat = A._struct()
         return self.L.eo_objective(C.byref(mat), ptr(np.ascontiguousarray(u, np.float64), _dp),
@@ -387,6 +428,11 @@ class _RefOracle:
                                          C.POINTER(_RefSgd)]
         L.er_sgd_targets.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_int,
                                      C.c_uint64, C.c_int, C.POINTER(_RefSgd)]
+        L.er_sgd_symmetric.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_int, C.c_uint64, C.c_int,
+                                       C.POINTER(_RefSgd)]
+        L.er_sgd_block.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int64, C.c_int64, C.c_double,
+                                   C.c_double, C.c_int, C.c_uint64, C.c_int, C.POINTER(_RefSgd)]
         L.er_lsqr.argtypes = [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(_RefLsqr)]
         L.er_lsqr_preconditioned.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double,
                                              C.c_double, C.c_double, C.c_int, C.c_uint64,
@@ -495,6 +541,36 @@ class RefMatrix:
         return Scaling(u, v, d, e, s.alpha, s.beta, bool(s.box_feasible),
                        bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
                        hi[:k].copy(), ho[:k].copy(), hr[:k].copy())
+
+    def _variant(self, call, iterations, diag_stride):
+        u, v, d, e = np.zeros(self.m), np.zeros(self.n), np.zeros(self.m), np.zeros(self.n)
+        nh = iterations // diag_stride + 1 if diag_stride > 0 else 1
+        hi, ho, hr = np.zeros(nh, np.int32), np.zeros(nh), np.zeros(nh)
+        s = _RefSgd(ptr(u, _dp), ptr(v, _dp), ptr(d, _dp), ptr(e, _dp), 0, 0, 0, 0, 0, 0,
+                    ptr(hi, _ip), ptr(ho, _dp), ptr(hr, _dp), 0)
+        rc = call(C.byref(s))
+        if rc:
+            self.R._err(rc)
+        k = s.hist_len
+        return Scaling(u, v, d, e, s.alpha, s.beta, bool(s.box_feasible),
+                       bool(s.iterate_bound_ok), s.apply_count, s.adjoint_count,
+                       hi[:k].copy(), ho[:k].copy(), hr[:k].copy())
+
+    def sgd_equilibrate_symmetric(self, alpha=0.0, beta=0.0, gamma=0.1,
+                                  max_log_scale=9.210340371976184, iterations=1000, seed=0,
+                                  diag_stride=0) -> Scaling:
+        return self._variant(lambda s: self.R.L.er_sgd_symmetric(
+            self.h, alpha, beta, gamma, max_log_scale, iterations, seed, diag_stride, s),
+            iterations, diag_stride)
+
+    def sgd_equilibrate_block(self, row_block, col_block, row_blocks, col_blocks, gamma=0.1,
+                              max_log_scale=9.210340371976184, iterations=1000, seed=0,
+                              diag_stride=0) -> Scaling:
+        rb = np.ascontiguousarray(row_block, np.int64)
+        cb = np.ascontiguousarray(col_block, np.int64)
+        return self._variant(lambda s: self.R.L.er_sgd_block(
+            self.h, ptr(rb, _i64p), ptr(cb, _i64p), row_blocks, col_blocks, gamma,
+            max_log_scale, iterations, seed, diag_stride, s), iterations, diag_stride)
 
     def lsqr(self, b, max_iters, tol) -> LsqrRun:
         b = np.ascontiguousarray(b, np.float64)

@@ -574,6 +574,217 @@ static int sgd_row_col(const eo_matrix* A, const eo_params* p, const double* lin
   return 0;
 }
 
+/* sgd_equilibrate_symmetric (src/variants.cpp:35-103).  check_symmetry
+ * (:14-33): three probes of normals drawn on stream 18 (kSymmetryCheck),
+ * <Ax, y> vs <x, Ay> with Eigen dot/norm -> canonical reductions. */
+int eo_sgd_equilibrate_symmetric(const eo_matrix* A, const eo_params* p, int diag_stride,
+                                 eo_scaling* out) {
+  if (eo_validate_params(p)) return 1; /* :38 */
+  if (A->m != A->n) return fail("sgd_equilibrate_symmetric: operator must be square");
+  const int64_t n = A->n;
+  {
+    double* x = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+    double* y = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+    double* ax = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+    double* ay = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+    eo_rng r;
+    eo_rng_init(&r, p->seed, 18);
+    int ok = 1;
+    for (int probe = 0; probe < 3 && ok; ++probe) {
+      for (int64_t i = 0; i < n; ++i) x[i] = eo_rng_normal(&r);
+      for (int64_t i = 0; i < n; ++i) y[i] = eo_rng_normal(&r);
+      mat_apply(A, x, ax);
+      mat_apply(A, y, ay);
+      const double lhs = eo_canon_dot(ax, y, n);
+      const double rhs = eo_canon_dot(x, ay, n);
+      const double scale = sqrt(eo_canon_sumsq(ax, n)) * sqrt(eo_canon_sumsq(y, n)) +
+                           sqrt(eo_canon_sumsq(x, n)) * sqrt(eo_canon_sumsq(ay, n)) + 1e-30;
+      if (!(fabs(lhs - rhs) <= 1e-10 * scale)) ok = 0;
+    }
+    free(x); free(y); free(ax); free(ay);
+    if (!ok) return fail("sgd_equilibrate_symmetric: operator failed symmetry check");
+  }
+  double alpha, beta;
+  if (eo_resolve_targets(p, n, n, &alpha, &beta)) return 1; /* :41 */
+  {
+    const double mx = alpha < beta ? beta : alpha;
+    if (!(fabs(alpha - beta) <= 1e-12 * mx))
+      return fail("sgd_equilibrate_symmetric: targets must coincide");
+  }
+  if (diag_stride < 0) return fail("sgd_equilibrate_symmetric: stride must be positive");
+  const double gamma = p->gamma, M = p->max_log_scale;
+  const int T = p->iterations;
+  double* u = (double*)calloc((size_t)(n ? n : 1), sizeof(double));
+  double* ub = (double*)calloc((size_t)(n ? n : 1), sizeof(double));
+  double* d = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* xs = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* yu = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* lin = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  for (int64_t i = 0; i < n; ++i) lin[i] = alpha * alpha; /* :56 */
+  eo_rng rng;
+  eo_rng_init(&rng, p->seed, 17);
+  int bound_ok = 1, box_ok = 1;
+  out->hist_len = 0;
+#define SYM_RECORD(t)                                                         \
+  do {                                                                        \
+    if (diag_stride > 0 && ((t) == 0 || (t) % diag_stride == 0)) {            \
+      int h = out->hist_len++;                                                \
+      if (out->hist_iter) out->hist_iter[h] = (t);                            \
+      if (out->hist_objective) /* :75-78, each unordered pair once */          \
+        out->hist_objective[h] = 0.5 * objective_lin(A, ub, ub, lin, lin, gamma); \
+      if (out->hist_rms) out->hist_rms[h] = eo_rms_error(A, ub, ub, alpha, alpha); \
+    }                                                                         \
+  } while (0)
+  SYM_RECORD(0);
+  for (int t = 1; t <= T; ++t) {
+    /* estimator :60-64: d = exp(u); est = (d .* A (d .* s))^2, n draws */
+    for (int64_t i = 0; i < n; ++i) d[i] = eo_det_exp(u[i]);
+    for (int64_t j = 0; j < n; ++j) xs[j] = d[j] * eo_rng_sign(&rng);
+    mat_apply(A, xs, yu);
+    for (int64_t i = 0; i < n; ++i) {
+      const double yy = d[i] * yu[i];
+      yu[i] = yy * yy;
+    }
+    const double step = 2.0 / (gamma * (double)(t + 1));
+    const double aw = 2.0 / ((double)t + 2.0);
+    sgd_block(n, u, ub, yu, lin, gamma, M, step, aw, &bound_ok, &box_ok);
+    SYM_RECORD(t);
+  }
+#undef SYM_RECORD
+  memcpy(out->u, ub, (size_t)n * 8); /* :93-96 */
+  memcpy(out->v, ub, (size_t)n * 8);
+  for (int64_t i = 0; i < n; ++i) out->d[i] = eo_det_exp(ub[i]);
+  memcpy(out->e, out->d, (size_t)n * 8);
+  out->alpha = alpha;
+  out->beta = alpha;
+  out->box_feasible = box_ok;
+  out->iterate_bound_ok = bound_ok;
+  out->apply_count = T;
+  out->adjoint_count = 0;
+  free(u); free(ub); free(d); free(xs); free(yu); free(lin);
+  return 0;
+}
+
+/* sgd_equilibrate_block (src/variants.cpp:156-240) with BlockStructure::validate
+ * (:131-154).  Block estimates sum the members' row (column) estimates in
+ * ascending index order starting from 0.0 (:190-193). */
+int eo_sgd_equilibrate_block(const eo_matrix* A, const int64_t* rb, const int64_t* cb,
+                             int64_t R, int64_t C, const eo_params* p, int diag_stride,
+                             eo_scaling* out) {
+  if (eo_validate_params(p)) return 1;
+  const int64_t m = A->m, n = A->n;
+  if (!(R > 0 && C > 0)) return fail("BlockStructure: block counts must be positive");
+  for (int64_t i = 0; i < m; ++i)
+    if (rb[i] < 0 || rb[i] >= R) return fail("BlockStructure: row block index out of range");
+  for (int64_t j = 0; j < n; ++j)
+    if (cb[j] < 0 || cb[j] >= C) return fail("BlockStructure: col block index out of range");
+  double* rc = (double*)calloc((size_t)R, sizeof(double));
+  double* cc = (double*)calloc((size_t)C, sizeof(double));
+  for (int64_t i = 0; i < m; ++i) rc[rb[i]] += 1.0;
+  for (int64_t j = 0; j < n; ++j) cc[cb[j]] += 1.0;
+  for (int64_t b = 0; b < R; ++b)
+    if (rc[b] == 0.0) {
+      free(rc); free(cc);
+      return fail("BlockStructure: empty row block");
+    }
+  for (int64_t b = 0; b < C; ++b)
+    if (cc[b] == 0.0) {
+      free(rc); free(cc);
+      return fail("BlockStructure: empty col block");
+    }
+  double alpha, beta;
+  if (eo_resolve_targets(p, m, n, &alpha, &beta)) {
+    free(rc); free(cc);
+    return 1;
+  }
+  if (diag_stride < 0) {
+    free(rc); free(cc);
+    return fail("sgd_equilibrate_block: stride must be positive");
+  }
+  const double gamma = p->gamma, M = p->max_log_scale;
+  const int T = p->iterations;
+  double* lu = (double*)malloc((size_t)R * sizeof(double));
+  double* lv = (double*)malloc((size_t)C * sizeof(double));
+  for (int64_t b = 0; b < R; ++b) lu[b] = (alpha * alpha) * rc[b]; /* :172-173 */
+  for (int64_t b = 0; b < C; ++b) lv[b] = (beta * beta) * cc[b];
+  double* xu = (double*)calloc((size_t)R, sizeof(double));
+  double* xub = (double*)calloc((size_t)R, sizeof(double));
+  double* xv = (double*)calloc((size_t)C, sizeof(double));
+  double* xvb = (double*)calloc((size_t)C, sizeof(double));
+  double* eu = (double*)malloc((size_t)R * sizeof(double));
+  double* ev = (double*)malloc((size_t)C * sizeof(double));
+  double* d = (double*)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double* e = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* xs = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* xw = (double*)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double* yu = (double*)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double* zv = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* uf = (double*)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double* vf = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  double* l1 = (double*)malloc((size_t)(m ? m : 1) * sizeof(double));
+  double* l2 = (double*)malloc((size_t)(n ? n : 1) * sizeof(double));
+  for (int64_t i = 0; i < m; ++i) l1[i] = alpha * alpha;
+  for (int64_t j = 0; j < n; ++j) l2[j] = beta * beta;
+  eo_rng rng;
+  eo_rng_init(&rng, p->seed, 17);
+  int bound_ok = 1, box_ok = 1;
+  out->hist_len = 0;
+#define BLK_RECORD(t)                                                         \
+  do {                                                                        \
+    if (diag_stride > 0 && ((t) == 0 || (t) % diag_stride == 0)) {            \
+      for (int64_t i = 0; i < m; ++i) uf[i] = xub[rb[i]];                     \
+      for (int64_t j = 0; j < n; ++j) vf[j] = xvb[cb[j]];                     \
+      int h = out->hist_len++;                                                \
+      if (out->hist_iter) out->hist_iter[h] = (t);                            \
+      if (out->hist_objective)                                                \
+        out->hist_objective[h] = objective_lin(A, uf, vf, l1, l2, gamma);     \
+      if (out->hist_rms) out->hist_rms[h] = eo_rms_error(A, uf, vf, alpha, beta); \
+    }                                                                         \
+  } while (0)
+  BLK_RECORD(0);
+  for (int t = 1; t <= T; ++t) {
+    /* estimator :181-194 */
+    for (int64_t i = 0; i < m; ++i) d[i] = eo_det_exp(xu[rb[i]]);
+    for (int64_t j = 0; j < n; ++j) e[j] = eo_det_exp(xv[cb[j]]);
+    for (int64_t j = 0; j < n; ++j) xs[j] = e[j] * eo_rng_sign(&rng);
+    mat_apply(A, xs, yu);
+    for (int64_t i = 0; i < m; ++i) {
+      const double yy = d[i] * yu[i];
+      yu[i] = yy * yy;
+    }
+    for (int64_t i = 0; i < m; ++i) xw[i] = d[i] * eo_rng_sign(&rng);
+    mat_adjoint(A, xw, zv);
+    for (int64_t j = 0; j < n; ++j) {
+      const double z = e[j] * zv[j];
+      zv[j] = z * z;
+    }
+    for (int64_t b = 0; b < R; ++b) eu[b] = 0.0;
+    for (int64_t b = 0; b < C; ++b) ev[b] = 0.0;
+    for (int64_t i = 0; i < m; ++i) eu[rb[i]] += yu[i];
+    for (int64_t j = 0; j < n; ++j) ev[cb[j]] += zv[j];
+    const double step = 2.0 / (gamma * (double)(t + 1));
+    const double aw = 2.0 / ((double)t + 2.0);
+    sgd_block(R, xu, xub, eu, lu, gamma, M, step, aw, &bound_ok, &box_ok);
+    sgd_block(C, xv, xvb, ev, lv, gamma, M, step, aw, &bound_ok, &box_ok);
+    BLK_RECORD(t);
+  }
+#undef BLK_RECORD
+  for (int64_t i = 0; i < m; ++i) out->u[i] = xub[rb[i]]; /* :226-229 */
+  for (int64_t j = 0; j < n; ++j) out->v[j] = xvb[cb[j]];
+  for (int64_t i = 0; i < m; ++i) out->d[i] = eo_det_exp(out->u[i]);
+  for (int64_t j = 0; j < n; ++j) out->e[j] = eo_det_exp(out->v[j]);
+  out->alpha = alpha;
+  out->beta = beta;
+  out->box_feasible = box_ok;
+  out->iterate_bound_ok = bound_ok;
+  out->apply_count = T;
+  out->adjoint_count = T;
+  free(rc); free(cc); free(lu); free(lv); free(xu); free(xub); free(xv); free(xvb);
+  free(eu); free(ev); free(d); free(e); free(xs); free(xw); free(yu); free(zv);
+  free(uf); free(vf); free(l1); free(l2);
+  return 0;
+}
+
 /* ========================================================================== */
 /* LSQR (src/lsqr.cpp:17-138)                                                 */
 /* ========================================================================== */

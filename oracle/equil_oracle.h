@@ -125,6 +125,15 @@ int eo_sgd_equilibrate_targets(const eo_matrix* A, const double* r, const double
                                const eo_params* p, int diag_stride, eo_scaling* out);
 int eo_sgd_equilibrate(const eo_matrix* A, const eo_params* p, int diag_stride,
                        eo_scaling* out);
+/* sgd_equilibrate_symmetric (src/variants.cpp:35-103): square A, one scaling
+ * u applied on both sides; symmetry spot check on stream 18 (:14-33). */
+int eo_sgd_equilibrate_symmetric(const eo_matrix* A, const eo_params* p, int diag_stride,
+                                 eo_scaling* out);
+/* sgd_equilibrate_block (src/variants.cpp:156-240): row i shares u_{rb[i]},
+ * column j shares v_{cb[j]}; R row blocks, C column blocks. */
+int eo_sgd_equilibrate_block(const eo_matrix* A, const int64_t* rb, const int64_t* cb,
+                             int64_t R, int64_t C, const eo_params* p, int diag_stride,
+                             eo_scaling* out);
 
 /* diagnostics at (u, v): src/equilibrate.cpp:10-22 and src/metrics.cpp:24-56 */
 double eo_objective(const eo_matrix* A, const double* u, const double* v,

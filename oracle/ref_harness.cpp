@@ -218,6 +218,71 @@ int er_sgd_targets(void* h, const double* r, const double* c, double gamma,
   });
 }
 
+static void copy_scaling(const ScalingResult& res, er_sgd_out* out) {
+  from_vec(res.u, out->u);
+  from_vec(res.v, out->v);
+  from_vec(res.d, out->d);
+  from_vec(res.e, out->e);
+  out->alpha = res.alpha;
+  out->beta = res.beta;
+  out->box_feasible = res.box_feasible;
+  out->iterate_bound_ok = res.iterate_bound_ok;
+  out->apply_count = res.apply_count;
+  out->adjoint_count = res.adjoint_count;
+  out->hist_len = static_cast<int>(res.history.size());
+  for (std::size_t k = 0; k < res.history.size(); ++k) {
+    if (out->hist_iter) out->hist_iter[k] = res.history[k].iter;
+    if (out->hist_objective) out->hist_objective[k] = res.history[k].objective.value_or(0.0);
+    if (out->hist_rms) out->hist_rms[k] = res.history[k].rms.value_or(0.0);
+  }
+}
+
+// sgd_equilibrate_symmetric (include/equil/variants.hpp:16-18)
+int er_sgd_symmetric(void* h, double alpha, double beta, double gamma, double max_log_scale,
+                     int iterations, uint64_t seed, int diag_stride, er_sgd_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    EquilibrationParams p;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.gamma = gamma;
+    p.max_log_scale = max_log_scale;
+    p.iterations = iterations;
+    p.seed = seed;
+    DiagnosticsConfig diag;
+    if (diag_stride > 0) {
+      diag.matrix = &A;
+      diag.stride = diag_stride;
+    }
+    copy_scaling(sgd_equilibrate_symmetric(A, p, diag), out);
+  });
+}
+
+// sgd_equilibrate_block (include/equil/variants.hpp:47-50)
+int er_sgd_block(void* h, const int64_t* rb, const int64_t* cb, int64_t R, int64_t C,
+                 double gamma, double max_log_scale, int iterations, uint64_t seed,
+                 int diag_stride, er_sgd_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    EquilibrationParams p;
+    p.gamma = gamma;
+    p.max_log_scale = max_log_scale;
+    p.iterations = iterations;
+    p.seed = seed;
+    BlockStructure bs;
+    bs.row_block.assign(rb, rb + A.rows());
+    bs.col_block.assign(cb, cb + A.cols());
+    bs.row_blocks = R;
+    bs.col_blocks = C;
+    DiagnosticsConfig diag;
+    if (diag_stride > 0) {
+      diag.matrix = &A;
+      diag.stride = diag_stride;
+    }
+    copy_scaling(sgd_equilibrate_block(A, bs, p, diag), out);
+  });
+}
+
 struct er_lsqr_out {
   double* x;
   double* residual_history;  // capacity given by caller

@@ -5,19 +5,21 @@ C ABI in include/equil_b200.h); this package is the Python mirror of the
 reference's interface over that ABI.  See DESIGN.md.
 """
 from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
-                  DiagnosticsConfig, EquilibrationParams, EquilRuntimeError,
+                  BlockStructure, DiagnosticsConfig, EquilibrationParams, EquilRuntimeError,
                   ExplicitMatrix, InvalidArgument, IterationRecord, LsqrRun,
                   ScalingResult, canon_sumsq_device, det_exp_device, kernel_launches,
                   last_loop_ms, lsqr, lsqr_preconditioned, nccl_unique_id,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
-                  sgd_equilibrate_targets,
+                  sgd_equilibrate_block, sgd_equilibrate_symmetric, sgd_equilibrate_targets,
                   sgd_equilibrate_device, sign_bits, validate_params)
 
 __all__ = [
-    "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "DiagnosticsConfig",
+    "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "BlockStructure",
+    "DiagnosticsConfig",
     "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",
     "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",
     "kernel_launches", "last_loop_ms", "lsqr", "lsqr_preconditioned", "nccl_unique_id",
     "partition_rows", "resolve_targets", "sgd_equilibrate", "sgd_equilibrate_csr",
-    "sgd_equilibrate_device", "sgd_equilibrate_targets", "sign_bits", "validate_params",
+    "sgd_equilibrate_block", "sgd_equilibrate_device", "sgd_equilibrate_symmetric",
+    "sgd_equilibrate_targets", "sign_bits", "validate_params",
 ]

@@ -75,6 +75,11 @@ SIGNATURES = {
                                         C.POINTER(ScalingOut)]),
     "equil_sgd_equilibrate_targets": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params),
                                                 C.POINTER(DiagCfg), C.POINTER(ScalingOut)]),
+    "equil_sgd_equilibrate_symmetric": (C.c_int, [C.c_void_p, C.POINTER(Params),
+                                                  C.POINTER(DiagCfg), C.POINTER(ScalingOut)]),
+    "equil_sgd_equilibrate_block": (C.c_int, [C.c_void_p, _i64p, _i64p, C.c_int64, C.c_int64,
+                                              C.POINTER(Params), C.POINTER(DiagCfg),
+                                              C.POINTER(ScalingOut)]),
     "equil_lsqr": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(LsqrOut)]),
     "equil_lsqr_preconditioned": (C.c_int, [C.c_void_p, _dp, C.POINTER(Params), C.c_int,
                                             C.c_double, C.POINTER(LsqrOut)]),

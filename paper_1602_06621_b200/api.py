@@ -289,6 +289,66 @@ def sgd_equilibrate_targets(op: ExplicitMatrix, r, c, params: EquilibrationParam
                          bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
 
 
+@dataclass
+class BlockStructure:
+    """BlockStructure (include/equil/variants.hpp:30-39): row i belongs to row
+    block row_block[i], column j to column block col_block[j]."""
+    row_block: np.ndarray
+    col_block: np.ndarray
+    row_blocks: int
+    col_blocks: int
+
+    @staticmethod
+    def trivial(rows: int, cols: int) -> "BlockStructure":
+        """One row (column) per block (src/variants.cpp:120-129)."""
+        return BlockStructure(np.arange(rows, dtype=np.int64), np.arange(cols, dtype=np.int64),
+                              int(rows), int(cols))
+
+
+def _variant_call(op, params, diag, call):
+    m, n = op.rows(), op.cols()
+    u, v, d, e = np.zeros(m), np.zeros(n), np.zeros(m), np.zeros(n)
+    cap = (max(int(params.iterations), 0) // diag.stride + 1) if diag and diag.stride > 0 else 1
+    hi, ho, hr = np.zeros(cap, np.int32), np.zeros(cap), np.zeros(cap)
+    out = L.ScalingOut(L.ptr(u, L._dp), L.ptr(v, L._dp), L.ptr(d, L._dp), L.ptr(e, L._dp), 0,
+                       0.0, 0.0, 0, 0, 0, 0, L.ptr(hi, L._ip), L.ptr(ho, L._dp),
+                       L.ptr(hr, L._dp), cap, 0)
+    p = params._c()
+    dc = L.DiagCfg(diag.stride, int(diag.want_objective), int(diag.want_rms)) if diag else None
+    _check(call(C.byref(p), C.byref(dc) if dc is not None else None, C.byref(out)))
+    hist = [IterationRecord(int(hi[k]), float(ho[k]) if diag.want_objective else None,
+                            float(hr[k]) if diag.want_rms else None)
+            for k in range(out.hist_len)] if diag else []
+    return ScalingResult(u, v, d, e, out.alpha, out.beta, hist, bool(out.box_feasible),
+                         bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
+
+
+def sgd_equilibrate_symmetric(op: ExplicitMatrix, params: EquilibrationParams | None = None,
+                              diag: DiagnosticsConfig | None = None) -> ScalingResult:
+    """sgd_equilibrate_symmetric (include/equil/variants.hpp:16-18): one
+    scaling on both sides of a symmetric matrix; u == v and d == e."""
+    params = params or EquilibrationParams()
+    return _variant_call(op, params, diag, lambda p, dc, out: L.load()
+                         .equil_sgd_equilibrate_symmetric(op._h, p, dc, out))
+
+
+def sgd_equilibrate_block(op: ExplicitMatrix, structure: BlockStructure,
+                          params: EquilibrationParams | None = None,
+                          diag: DiagnosticsConfig | None = None) -> ScalingResult:
+    """sgd_equilibrate_block (include/equil/variants.hpp:47-50): rows (columns)
+    of one block share a scaling; results expanded to full length."""
+    params = params or EquilibrationParams()
+    rb = np.ascontiguousarray(structure.row_block, dtype=np.int64)
+    cb = np.ascontiguousarray(structure.col_block, dtype=np.int64)
+    if rb.size != op.rows() or cb.size != op.cols():
+        raise InvalidArgument("BlockStructure: assignment length mismatch")
+    return _variant_call(op, params, diag, lambda p, dc, out: L.load()
+                         .equil_sgd_equilibrate_block(op._h, L.ptr(rb, L._i64p),
+                                                      L.ptr(cb, L._i64p),
+                                                      int(structure.row_blocks),
+                                                      int(structure.col_blocks), p, dc, out))
+
+
 def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,
                            u_ptr: int, v_ptr: int, d_ptr: int, e_ptr: int) -> ScalingResult:
     """sgd_equilibrate with u, v, d, e written to caller-owned DEVICE buffers

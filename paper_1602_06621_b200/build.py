@@ -27,7 +27,7 @@ LIB = os.path.join(HERE, "libequil_b200" + (f"_{TAG}" if TAG else "") + ".so")
 GEN_LIB = os.path.join(HERE, "libequil_gen.so")  # synthetic inputs (bench/tests)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["kernels.cu", "panel.cu", "dense.cu", "engine.cu"]
+CU_SOURCES = ["kernels.cu", "panel.cu", "variants.cu", "dense.cu", "engine.cu"]
 CXX_SOURCES = ["mt64_host.cpp"]
 HEADERS = ["det_math.cuh", "internal.h", "mt64_host.h", "sgd_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -205,6 +205,11 @@ __device__ __forceinline__ void dense_pass_epi(const DensePassArgs& a, int64_t r
     }
     case kPassResid: a.out[r] = __dsub_rn(a.prev[r], acc); break;
     case kPassScaled: a.out[r] = a.scale ? __dmul_rn(a.scale[r], acc) : acc; break;
+    case kPassEst: {  // estimate_row_norms_sq (src/estimator.cpp:5-9)
+      const double y = __dmul_rn(a.scale[r], acc);
+      a.out[r] = __dmul_rn(y, y);
+      break;
+    }
   }
 }
 

@@ -1280,7 +1280,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     M->last_loop_iters = T;
 
     // finalize: u = ubar, v = vbar, d = exp(ubar), e = exp(vbar) (:201-204)
-        double* dloc = M->tmp_m.p;
+    double* dloc = M->tmp_m.p;
     double* eloc = M->tmp_n.p;
     CK(eqb::launch_exp(M->ub.p, dloc, ml, 1.0, s));
     CK(eqb::launch_exp(M->vb.p, eloc, nl, 1.0, s));
@@ -1791,6 +1791,328 @@ equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_
   rc = equil_sgd_equilibrate(M, p, nullptr, out);
   equil_matrix_destroy(M);
   return rc;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Engine variants (src/variants.cpp): symmetric (:35-103) and block
+// (:156-240) equilibration.  Same sign stream, the same projected-SGD update
+// (run_projected_sgd) and the same estimator arithmetic as sgd_row_col, but
+// the passes run as generic pass kernels (kPassEst) between small kernels that
+// form the scalings, sum estimates over blocks and update the block iterates.
+// Single GPU; sparse and dense matrices (history for sparse ones).
+// ---------------------------------------------------------------------------
+namespace {
+
+// SeededRng (src/rng.cpp:9-49) on the host: the symmetry check's probe
+// normals (Box-Muller with the spare kept; glibc log/sin/cos like the
+// reference build).
+struct HostRng {
+  uint64_t mt[eqb::mt::kN];
+  int i = eqb::mt::kN;
+  bool has_spare = false;
+  double spare = 0.0;
+  HostRng(uint64_t seed, uint64_t stream) { eqb::mt::seed_state(seed, stream, mt); }
+  uint64_t next() {
+    if (i >= eqb::mt::kN) {
+      constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL;
+      for (int k = 0; k < eqb::mt::kN; ++k) {
+        const uint64_t x = (mt[k] & kUpper) | (mt[(k + 1) % eqb::mt::kN] & kLower);
+        uint64_t xa = x >> 1;
+        if (x & 1u) xa ^= 0xB5026F5AA96619E9ULL;
+        mt[k] = mt[(k + eqb::mt::kM) % eqb::mt::kN] ^ xa;
+      }
+      i = 0;
+    }
+    return eqb::mt::temper(mt[i++]);
+  }
+  double uniform01() { return (static_cast<double>(next() >> 11) + 0.5) * 0x1.0p-53; }
+  double normal() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    const double u1 = uniform01(), u2 = uniform01();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(theta);
+    has_spare = true;
+    return r * std::cos(theta);
+  }
+};
+
+enum class Variant { kSymmetric, kBlock };
+
+// check_symmetry (src/variants.cpp:14-33) with device applies and canonical
+// dots / norms; the probes come from stream 18 (streams::kSymmetryCheck).
+void check_symmetry(equil_matrix* M, uint64_t seed) {
+  const int64_t n = M->n;
+  cudaStream_t s = M->stream;
+  HostRng rng(seed, 18);
+  std::vector<double> x(n), y(n);
+  DevBuf<double> xd, yd, ax, ay, t;
+  xd.alloc(n); yd.alloc(n); ax.alloc(n); ay.alloc(n); t.alloc(n);
+  double* sc = M->scal.p + 32;
+  for (int probe = 0; probe < 3; ++probe) {
+    for (int64_t i = 0; i < n; ++i) x[i] = rng.normal();
+    for (int64_t i = 0; i < n; ++i) y[i] = rng.normal();
+    CK(cudaMemcpyAsync(xd.p, x.data(), n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(yd.p, y.data(), n * 8, cudaMemcpyHostToDevice, s));
+    apply_pass(M, false, xd.p, ax.p, eqb::kPassPlain, nullptr, nullptr, nullptr);
+    apply_pass(M, false, yd.p, ay.p, eqb::kPassPlain, nullptr, nullptr, nullptr);
+    CK(eqb::launch_mul(t.p, ax.p, yd.p, n, s));
+    canon_reduce(M, t.p, n, sc + 0, 1);  // ax.dot(y)
+    CK(eqb::launch_mul(t.p, xd.p, ay.p, n, s));
+    canon_reduce(M, t.p, n, sc + 1, 1);  // x.dot(ay)
+    canon_reduce(M, ax.p, n, sc + 2, 0, 0.0, true);
+    canon_reduce(M, yd.p, n, sc + 3, 0, 0.0, true);
+    canon_reduce(M, xd.p, n, sc + 4, 0, 0.0, true);
+    canon_reduce(M, ay.p, n, sc + 5, 0, 0.0, true);
+    double r[6];
+    CK(cudaMemcpyAsync(r, sc, sizeof r, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double scale = r[2] * r[3] + r[4] * r[5] + 1e-30;
+    require(std::abs(r[0] - r[1]) <= 1e-10 * scale,
+            "sgd_equilibrate_symmetric: operator failed symmetry check");
+  }
+}
+
+void sgd_variant(equil_matrix* M, Variant kind, const equil_params* p,
+                 const equil_diag_cfg* diag, equil_scaling_out* out, const int64_t* rb_host,
+                 const int64_t* cb_host, int64_t R, int64_t C) {
+  std::lock_guard<std::mutex> lk(M->mu);
+  DeviceGuard dg(M->device);
+  const bool sym = kind == Variant::kSymmetric;
+  const char* who = sym ? "sgd_equilibrate_symmetric" : "sgd_equilibrate_block";
+  require(M->world == 1, std::string(who) + ": single-GPU matrices only in this build");
+  validate_params(*p);
+  const int64_t m = M->m, n = M->n;
+  double alpha = 0, beta = 0;
+  std::vector<int32_t> rbm, cbm;
+  std::vector<double> rcount, ccount;
+  if (sym) {
+    require(m == n, "sgd_equilibrate_symmetric: operator must be square");
+    check_symmetry(M, p->seed);
+    resolve_targets(*p, n, n, alpha, beta);
+    require(std::abs(alpha - beta) <= 1e-12 * std::max(alpha, beta),
+            "sgd_equilibrate_symmetric: targets must coincide");
+    R = n;
+    C = 0;
+  } else {  // BlockStructure::validate (src/variants.cpp:131-154)
+    require(rb_host != nullptr && cb_host != nullptr, "BlockStructure: assignment length mismatch");
+    require(R > 0 && C > 0, "BlockStructure: block counts must be positive");
+    require(R < (1LL << 31) && C < (1LL << 31), "BlockStructure: too many blocks");
+    rcount.assign(R, 0.0);
+    ccount.assign(C, 0.0);
+    rbm.resize(m);
+    cbm.resize(n);
+    for (int64_t i = 0; i < m; ++i) {
+      require(rb_host[i] >= 0 && rb_host[i] < R, "BlockStructure: row block index out of range");
+      rbm[i] = static_cast<int32_t>(rb_host[i]);
+    }
+    for (int64_t j = 0; j < n; ++j) {
+      require(cb_host[j] >= 0 && cb_host[j] < C, "BlockStructure: col block index out of range");
+      cbm[j] = static_cast<int32_t>(cb_host[j]);
+    }
+    for (int64_t i = 0; i < m; ++i) rcount[rbm[i]] += 1.0;  // :165-169
+    for (int64_t j = 0; j < n; ++j) ccount[cbm[j]] += 1.0;
+    for (int64_t b = 0; b < R; ++b) require(rcount[b] != 0.0, "BlockStructure: empty row block");
+    for (int64_t b = 0; b < C; ++b) require(ccount[b] != 0.0, "BlockStructure: empty col block");
+    resolve_targets(*p, m, n, alpha, beta);
+  }
+  const int stride = diag ? diag->stride : 0;
+  require(stride >= 0, std::string(who) + ": stride must be positive");
+  const int T = p->iterations;
+  const int nrec = stride ? T / stride + 1 : 0;
+  if (stride) {
+    require(!M->dense, std::string(who) + ": history is implemented for sparse matrices");
+    require(out->hist_cap >= nrec, std::string(who) + ": history capacity too small");
+  }
+  cudaStream_t s = M->stream;
+  const double gamma = p->gamma, Mx = p->max_log_scale;
+
+  // signs: n per iteration (symmetric: one probe) or n + m (s then w)
+  const uint64_t per_iter = static_cast<uint64_t>(sym ? n : n + m);
+  const uint64_t total = per_iter * static_cast<uint64_t>(T);
+  if (total > 0) {
+    M->signs.ensure((total + 31) / 32 + 1);
+    const size_t sb = eqb::sign_stream_scratch_bytes(total);
+    M->sign_scratch.ensure(sb);
+    CK(eqb::sign_stream_generate(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb, s));
+  }
+  // block iterates, linear terms, scalings, probes, estimates
+  DevBuf<double> xu, xub, xv, xvb, lu, lv, d, e, xs, xw, er, ec, ebu, ebv;
+  DevBuf<int32_t> rbd, cbd, memr, memc;
+  DevBuf<int64_t> offr, offc;
+  xu.alloc(R); xub.alloc(R); lu.alloc(R);
+  d.alloc(m); e.alloc(n); xs.alloc(n); xw.alloc(m); er.alloc(m); ec.alloc(n);
+  CK(cudaMemsetAsync(xu.p, 0, R * 8, s));
+  CK(cudaMemsetAsync(xub.p, 0, R * 8, s));
+  {
+    std::vector<double> l(R);
+    for (int64_t b = 0; b < R; ++b) l[b] = sym ? alpha * alpha : (alpha * alpha) * rcount[b];
+    CK(cudaMemcpyAsync(lu.p, l.data(), R * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  if (!sym) {
+    xv.alloc(C); xvb.alloc(C); lv.alloc(C); ebu.alloc(R); ebv.alloc(C);
+    CK(cudaMemsetAsync(xv.p, 0, C * 8, s));
+    CK(cudaMemsetAsync(xvb.p, 0, C * 8, s));
+    std::vector<double> l(C);
+    for (int64_t b = 0; b < C; ++b) l[b] = (beta * beta) * ccount[b];
+    CK(cudaMemcpy(lv.p, l.data(), C * 8, cudaMemcpyHostToDevice));
+    // members of every block in ascending index order (stable counting sort)
+    auto members = [](const std::vector<int32_t>& map, int64_t nb, DevBuf<int32_t>& mem,
+                      DevBuf<int64_t>& off) {
+      std::vector<int64_t> o(nb + 1, 0);
+      for (int32_t b : map) ++o[b + 1];
+      for (int64_t b = 0; b < nb; ++b) o[b + 1] += o[b];
+      std::vector<int32_t> list(map.size());
+      std::vector<int64_t> pos(o.begin(), o.end() - 1);
+      for (size_t i = 0; i < map.size(); ++i) list[pos[map[i]]++] = static_cast<int32_t>(i);
+      mem.alloc(list.size());
+      off.alloc(o.size());
+      if (!list.empty())
+        CK(cudaMemcpy(mem.p, list.data(), list.size() * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(off.p, o.data(), o.size() * 8, cudaMemcpyHostToDevice));
+    };
+    members(rbm, R, memr, offr);
+    members(cbm, C, memc, offc);
+    rbd.alloc(m);
+    cbd.alloc(n);
+    if (m) CK(cudaMemcpy(rbd.p, rbm.data(), m * 4, cudaMemcpyHostToDevice));
+    if (n) CK(cudaMemcpy(cbd.p, cbm.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
+  eqb::SgdBlockConst c{};
+  c.gamma = gamma;
+  c.M = Mx;
+
+  // history (src/variants.cpp:66-86, :197-214) at the expanded averages
+  constexpr int kRec = 6;
+  DevBuf<double> hist, terms, uf, vf, eu, ev;
+  if (nrec) {
+    hist.alloc(kRec * nrec);
+    terms.alloc(m + n);
+    uf.alloc(m); vf.alloc(n); eu.alloc(m); ev.alloc(n);
+  }
+  const double a2 = alpha * alpha, b2 = sym ? alpha * alpha : beta * beta;
+  const double beta_rms = sym ? alpha : beta;
+  auto expand_avg = [&]() {
+    if (sym) {
+      CK(cudaMemcpyAsync(uf.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(vf.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+      CK(eqb::launch_gather_map(xub.p, rbd.p, m, uf.p, s));
+      CK(eqb::launch_gather_map(xvb.p, cbd.p, n, vf.p, s));
+    }
+  };
+  int rec = 0;
+  auto record = [&]() {
+    double* slot = hist.p + kRec * rec;
+    expand_avg();
+    CK(eqb::launch_exp(uf.p, eu.p, m, 2.0, s));
+    CK(eqb::launch_exp(vf.p, ev.p, n, 2.0, s));
+    CK(eqb::launch_rms_terms(0, M->A, eu.p, ev.p, terms.p, 0, alpha, s));
+    CK(eqb::launch_rms_terms(1, M->AT, eu.p, ev.p, terms.p + m, 0, beta_rms, s));
+    canon_reduce(M, terms.p, m + n, slot + 0, 1);
+    CK(eqb::launch_obj_terms(M->A, uf.p, vf.p, terms.p, s));
+    canon_reduce(M, terms.p, m, slot + 1, 1);
+    canon_reduce(M, uf.p, m, slot + 2, 2, a2);
+    canon_reduce(M, vf.p, n, slot + 3, 2, b2);
+    canon_reduce(M, uf.p, m, slot + 4, 0);
+    canon_reduce(M, vf.p, n, slot + 5, 0);
+    ++rec;
+  };
+  if (stride) record();
+  for (int t = 1; t <= T; ++t) {
+    eqb::SgdStep st;
+    st.step = 2.0 / (gamma * static_cast<double>(t + 1));
+    st.aw = 2.0 / (static_cast<double>(t) + 2.0);
+    st.aw1 = 1.0 - st.aw;
+    st.pad = 0;
+    const int64_t base = static_cast<int64_t>(t - 1) * static_cast<int64_t>(per_iter);
+    if (sym) {  // d = exp(u); est = (d .* A (d .* s))^2 (:60-64)
+      CK(eqb::launch_expand_scale(xu.p, nullptr, n, M->signs.p, base, d.p, xs.p, s));
+      apply_pass(M, false, xs.p, er.p, eqb::kPassEst, d.p, nullptr, nullptr);
+      CK(eqb::launch_sgd_update(xu.p, xub.p, er.p, lu.p, c, st, n, M->flags.p, s));
+    } else {  // :181-194
+      CK(eqb::launch_expand_scale(xv.p, cbd.p, n, M->signs.p, base, e.p, xs.p, s));
+      CK(eqb::launch_expand_scale(xu.p, rbd.p, m, M->signs.p, base + n, d.p, xw.p, s));
+      apply_pass(M, false, xs.p, er.p, eqb::kPassEst, d.p, nullptr, nullptr);
+      apply_pass(M, true, xw.p, ec.p, eqb::kPassEst, e.p, nullptr, nullptr);
+      CK(eqb::launch_block_sum(er.p, memr.p, offr.p, R, ebu.p, s));
+      CK(eqb::launch_block_sum(ec.p, memc.p, offc.p, C, ebv.p, s));
+      CK(eqb::launch_sgd_update(xu.p, xub.p, ebu.p, lu.p, c, st, R, M->flags.p, s));
+      CK(eqb::launch_sgd_update(xv.p, xvb.p, ebv.p, lv.p, c, st, C, M->flags.p, s));
+    }
+    if (stride && t % stride == 0) record();
+  }
+  // result: expanded averages and their exponentials (:93-96, :226-229)
+  DevBuf<double> ufin, vfin, dfin, efin;
+  ufin.alloc(m); vfin.alloc(n); dfin.alloc(m); efin.alloc(n);
+  if (sym) {
+    CK(cudaMemcpyAsync(ufin.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(vfin.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
+  } else {
+    CK(eqb::launch_gather_map(xub.p, rbd.p, m, ufin.p, s));
+    CK(eqb::launch_gather_map(xvb.p, cbd.p, n, vfin.p, s));
+  }
+  CK(eqb::launch_exp(ufin.p, dfin.p, m, 1.0, s));
+  CK(eqb::launch_exp(vfin.p, efin.p, n, 1.0, s));
+  const cudaMemcpyKind k =
+      out->outputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (out->u) CK(cudaMemcpyAsync(out->u, ufin.p, m * 8, k, s));
+  if (out->v) CK(cudaMemcpyAsync(out->v, vfin.p, n * 8, k, s));
+  if (out->d) CK(cudaMemcpyAsync(out->d, dfin.p, m * 8, k, s));
+  if (out->e) CK(cudaMemcpyAsync(out->e, efin.p, n * 8, k, s));
+  unsigned flags = 0;
+  CK(cudaMemcpyAsync(&flags, M->flags.p, sizeof flags, cudaMemcpyDeviceToHost, s));
+  std::vector<double> hh(kRec * static_cast<size_t>(std::max(nrec, 1)));
+  if (nrec) CK(cudaMemcpyAsync(hh.data(), hist.p, kRec * nrec * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out->alpha = alpha;
+  out->beta = sym ? alpha : beta;
+  out->iterate_bound_ok = (flags & 1u) ? 0 : 1;
+  out->box_feasible = (flags & 2u) ? 0 : 1;
+  out->apply_count = T;
+  out->adjoint_count = sym ? 0 : T;
+  out->hist_len = nrec;
+  for (int h = 0; h < nrec; ++h) {
+    const double* r = hh.data() + kRec * h;
+    const double obj = 0.5 * r[1] - r[2] - r[3] + 0.5 * gamma * (r[4] + r[5]);
+    if (out->hist_iter) out->hist_iter[h] = h * stride;
+    if (out->hist_objective)  // symmetric: each unordered pair once (:75-78)
+      out->hist_objective[h] = (diag->want_objective ? (sym ? 0.5 * obj : obj) : 0.0);
+    if (out->hist_rms)
+      out->hist_rms[h] = diag->want_rms ? std::sqrt(r[0] / static_cast<double>(m + n)) : 0.0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+equil_status equil_sgd_equilibrate_symmetric(equil_matrix* M, const equil_params* p,
+                                             const equil_diag_cfg* diag,
+                                             equil_scaling_out* out) {
+  return guarded([&] {
+    require(M != nullptr && p != nullptr && out != nullptr,
+            "sgd_equilibrate_symmetric: null argument");
+    sgd_variant(M, Variant::kSymmetric, p, diag, out, nullptr, nullptr, 0, 0);
+  });
+}
+
+equil_status equil_sgd_equilibrate_block(equil_matrix* M, const int64_t* row_block,
+                                         const int64_t* col_block, int64_t row_blocks,
+                                         int64_t col_blocks, const equil_params* p,
+                                         const equil_diag_cfg* diag, equil_scaling_out* out) {
+  return guarded([&] {
+    require(M != nullptr && p != nullptr && out != nullptr,
+            "sgd_equilibrate_block: null argument");
+    sgd_variant(M, Variant::kBlock, p, diag, out, row_block, col_block, row_blocks, col_blocks);
+  });
 }
 
 }  // extern "C"

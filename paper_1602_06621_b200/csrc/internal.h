@@ -150,6 +150,7 @@ enum PassMode : int {
   kPassLsqrV = 2,    // out = s_j*acc - beta*v_j    (s = e or 1)
   kPassResid = 3,    // out = b_i - acc
   kPassScaled = 4,   // out = s_i*acc (s = scale or 1)
+  kPassEst = 5,      // out = (s_i*acc)^2 (row-norm estimate, s = scale)
 };
 
 struct PassArgs {
@@ -251,6 +252,22 @@ struct DensePassArgs {
   double* colpart;
 };
 cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s);
+
+// engine variants (variants.cu): symmetric / block equilibration
+// scale_i = exp(x[map ? map[i] : i]); signed_out_i = +-scale_i by sign bit sign0 + i
+cudaError_t launch_expand_scale(const double* x, const int32_t* map, int64_t len,
+                                const uint32_t* signs, int64_t sign0, double* scale,
+                                double* signed_out, cudaStream_t s);
+// out[b] = sequential sum of est over members[off[b] .. off[b+1]) (ascending)
+cudaError_t launch_block_sum(const double* est, const int32_t* members, const int64_t* off,
+                             int64_t nblocks, double* out, cudaStream_t s);
+// projected SGD update of len coordinates with per-coordinate linear terms
+cudaError_t launch_sgd_update(double* x, double* avg, const double* est, const double* lin,
+                              const SgdBlockConst& c, const SgdStep& st, int64_t len,
+                              unsigned* flags, cudaStream_t s);
+// out_i = x[map[i]]
+cudaError_t launch_gather_map(const double* x, const int32_t* map, int64_t len, double* out,
+                              cudaStream_t s);
 
 // LSQR elementwise helpers
 cudaError_t launch_lsqr_normalize(double* dst, const double* src,

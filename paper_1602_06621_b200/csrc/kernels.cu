@@ -810,6 +810,11 @@ __device__ __forceinline__ void pass_epilogue(const PassArgs& a, int64_t r,
     case kPassScaled:
       a.out[r] = a.scale ? __dmul_rn(a.scale[r], acc) : acc;
       break;
+    case kPassEst: {  // estimate_row_norms_sq: y = s_i * acc, y * y (estimator.cpp:5-9)
+      const double y = __dmul_rn(a.scale[r], acc);
+      a.out[r] = __dmul_rn(y, y);
+      break;
+    }
   }
 }
 

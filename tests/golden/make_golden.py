@@ -107,6 +107,39 @@ def main():
     g["tg_sgd_hist_obj"] = s.hist_objective
     g["tg_sgd_flags"] = np.array([s.box_feasible, s.iterate_bound_ok, s.apply_count,
                                   s.adjoint_count])
+    # symmetric variant (src/variants.cpp:35-103) on an exactly symmetric matrix
+    rng = np.random.default_rng(16)
+    ns = 120
+    mask = rng.random((ns, ns)) < 0.05
+    mask |= mask.T
+    np.fill_diagonal(mask, True)
+    sc = np.exp(rng.standard_normal(ns))
+    a = rng.standard_normal((ns, ns)) * sc[:, None] * sc[None, :]
+    a = np.triu(a) + np.triu(a, 1).T
+    rows, cols = np.nonzero(mask)
+    S = oracle.CsrArrays(ns, ns, np.concatenate([[0], np.cumsum(mask.sum(1))]).astype(np.int64),
+                         cols.astype(np.int32), a[mask])
+    g["sy_shape"] = np.array([ns, ns])
+    g["sy_rp"], g["sy_col"], g["sy_val"] = S.row_ptr, S.col, S.val
+    s = R.matrix(S).sgd_equilibrate_symmetric(iterations=40, seed=6, diag_stride=10)
+    for k in "uvde":
+        g[f"sy_sgd_{k}"] = getattr(s, k)
+    g["sy_sgd_hist_obj"], g["sy_sgd_hist_rms"] = s.hist_objective, s.hist_rms
+    g["sy_sgd_flags"] = np.array([s.box_feasible, s.iterate_bound_ok, s.apply_count,
+                                  s.adjoint_count])
+    # block variant (src/variants.cpp:156-240) on the sparse case
+    A = cases["sp"]
+    rb = rng.integers(0, 17, A.m)
+    rb[:17] = np.arange(17)
+    cb = np.arange(A.n) // 9
+    s = R.matrix(A).sgd_equilibrate_block(rb, cb, 17, int(cb.max()) + 1, iterations=30, seed=8,
+                                          diag_stride=10)
+    g["bl_rb"], g["bl_cb"] = rb, cb
+    for k in "uvde":
+        g[f"bl_sgd_{k}"] = getattr(s, k)
+    g["bl_sgd_hist_obj"], g["bl_sgd_hist_rms"] = s.hist_objective, s.hist_rms
+    g["bl_sgd_flags"] = np.array([s.box_feasible, s.iterate_bound_ok, s.apply_count,
+                                  s.adjoint_count])
     np.savez_compressed(OUT, **g)
     print(OUT, os.path.getsize(OUT), "bytes")
 

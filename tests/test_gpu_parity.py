@@ -432,3 +432,85 @@ def test_coo_errors_match_reference_messages():
     assert M.stored_entries() == 0
     r = eq.sgd_equilibrate(M, eq.EquilibrationParams(alpha=1.0, iterations=3))
     assert np.all(r.u < 0) or np.all(r.u != 0)
+
+
+# ---------------------------------------------------------------- engine variants
+def test_symmetric_variant_bit_exact_vs_reference_golden(golden):
+    """sgd_equilibrate_symmetric (src/variants.cpp:35-103) on the device."""
+    S = csr_from_golden(golden, "sy")
+    r = eq.sgd_equilibrate_symmetric(device_matrix(S), eq.EquilibrationParams(iterations=40,
+                                                                              seed=6),
+                                     eq.DiagnosticsConfig(stride=10))
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), golden[f"sy_sgd_{k}"]), k
+    box, bound, ap, ad = golden["sy_sgd_flags"]
+    assert (r.box_feasible, r.iterate_bound_ok, r.apply_count, r.adjoint_count) == \
+        (bool(box), bool(bound), ap, ad)
+    np.testing.assert_allclose([h.objective for h in r.history], golden["sy_sgd_hist_obj"],
+                               rtol=1e-12, atol=0)
+    np.testing.assert_allclose([h.rms for h in r.history], golden["sy_sgd_hist_rms"],
+                               rtol=1e-12, atol=0)
+
+
+def test_block_variant_bit_exact_vs_reference_golden(golden):
+    """sgd_equilibrate_block (src/variants.cpp:156-240) on the device."""
+    A = csr_from_golden(golden, "sp")
+    rb, cb = golden["bl_rb"], golden["bl_cb"]
+    st = eq.BlockStructure(rb, cb, 17, int(cb.max()) + 1)
+    r = eq.sgd_equilibrate_block(device_matrix(A), st, eq.EquilibrationParams(iterations=30,
+                                                                              seed=8),
+                                 eq.DiagnosticsConfig(stride=10))
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), golden[f"bl_sgd_{k}"]), k
+    np.testing.assert_allclose([h.objective for h in r.history], golden["bl_sgd_hist_obj"],
+                               rtol=1e-12, atol=0)
+    np.testing.assert_allclose([h.rms for h in r.history], golden["bl_sgd_hist_rms"],
+                               rtol=1e-12, atol=0)
+
+
+def test_variants_dense_and_known_answers_vs_oracle(C):
+    """Dense operands, singleton blocks == the plain solver, identity fixed
+    point, and the reference's rejections (test_variants.cpp:36-61, :165-176,
+    :234-249)."""
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((48, 48)) * np.exp(rng.standard_normal((48, 1)))
+    Sd = np.triu(X) + np.triu(X, 1).T
+    A = oracle.CsrArrays(48, 48, dense=Sd)
+    want = C.sgd_equilibrate_symmetric(A, iterations=60, seed=2)
+    got = eq.sgd_equilibrate_symmetric(eq.ExplicitMatrix.dense(Sd),
+                                       eq.EquilibrationParams(iterations=60, seed=2))
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    D = rng.standard_normal((40, 25)) * np.exp(2 * rng.standard_normal((40, 1)))
+    B = oracle.CsrArrays(40, 25, dense=D)
+    rb, cb = np.arange(40) % 6, np.arange(25) // 5
+    want = C.sgd_equilibrate_block(B, rb, cb, 6, 5, iterations=50, seed=3)
+    got = eq.sgd_equilibrate_block(eq.ExplicitMatrix.dense(D), eq.BlockStructure(rb, cb, 6, 5),
+                                   eq.EquilibrationParams(iterations=50, seed=3))
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    M = eq.ExplicitMatrix.dense(D)
+    plain = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=40, seed=11))
+    blk = eq.sgd_equilibrate_block(M, eq.BlockStructure.trivial(40, 25),
+                                   eq.EquilibrationParams(iterations=40, seed=11))
+    for k in "uvde":
+        assert np.array_equal(getattr(plain, k), getattr(blk, k)), k
+    r = eq.sgd_equilibrate_symmetric(eq.ExplicitMatrix.identity(4),
+                                     eq.EquilibrationParams(alpha=1.0, beta=1.0,
+                                                            iterations=100))
+    assert np.all(r.u == 0) and np.array_equal(r.d, r.e) and (r.apply_count,
+                                                               r.adjoint_count) == (100, 0)
+    with pytest.raises(eq.InvalidArgument, match="symmetry check"):
+        eq.sgd_equilibrate_symmetric(eq.ExplicitMatrix.dense(rng.standard_normal((5, 5))),
+                                     eq.EquilibrationParams(alpha=1.0, beta=1.0))
+    with pytest.raises(eq.InvalidArgument, match="must be square"):
+        eq.sgd_equilibrate_symmetric(eq.ExplicitMatrix.dense(np.ones((3, 4))),
+                                     eq.EquilibrationParams(alpha=1.0, beta=1.0))
+    Bm = eq.ExplicitMatrix.dense(rng.standard_normal((3, 2)) + 1.5)
+    for rbx, cbx, R, Cb, msg in [([0, 0, 1], [0, 1], 3, 2, "empty row block"),
+                                 ([0, 0, 1], [0, 1], 1, 2, "row block index out of range"),
+                                 ([0, 0, 1], [0, -1], 2, 2, "col block index out of range"),
+                                 ([0, 0, 1, 1], [0, 1], 2, 2, "assignment length mismatch")]:
+        with pytest.raises(eq.InvalidArgument, match=msg):
+            eq.sgd_equilibrate_block(Bm, eq.BlockStructure(np.array(rbx), np.array(cbx), R, Cb),
+                                     eq.EquilibrationParams(iterations=3))

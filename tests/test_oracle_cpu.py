@@ -198,3 +198,54 @@ def test_oracle_errors(C):
         C.sgd_equilibrate(A, alpha=1.0, beta=2.0, iterations=1)
     with pytest.raises(oracle.OracleError, match="nonzero"):
         C.lsqr(A, np.zeros(2), 5, 0.0)
+
+
+def test_oracle_symmetric_and_block_variants_match_reference_golden(C, golden):
+    """sgd_equilibrate_symmetric (src/variants.cpp:35-103) and
+    sgd_equilibrate_block (:156-240) on the oracle vs the reference's own
+    sources (golden), history included."""
+    S = csr_from_golden(golden, "sy")
+    s = C.sgd_equilibrate_symmetric(S, iterations=40, seed=6, diag_stride=10)
+    for k in "uvde":
+        assert np.array_equal(getattr(s, k), golden[f"sy_sgd_{k}"]), k
+    assert np.array_equal(s.hist_objective, golden["sy_sgd_hist_obj"])
+    assert np.array_equal(s.hist_rms, golden["sy_sgd_hist_rms"])
+    assert [s.box_feasible, s.iterate_bound_ok, s.apply_count, s.adjoint_count] == \
+        list(golden["sy_sgd_flags"])
+    A = csr_from_golden(golden, "sp")
+    rb, cb = golden["bl_rb"], golden["bl_cb"]
+    b = C.sgd_equilibrate_block(A, rb, cb, 17, int(cb.max()) + 1, iterations=30, seed=8,
+                                diag_stride=10)
+    for k in "uvde":
+        assert np.array_equal(getattr(b, k), golden[f"bl_sgd_{k}"]), k
+    assert np.array_equal(b.hist_objective, golden["bl_sgd_hist_obj"])
+    assert np.array_equal(b.hist_rms, golden["bl_sgd_hist_rms"])
+
+
+def test_oracle_variant_known_answers(C):
+    """test_variants.cpp:36-61, :165-176, :234-249 restated on the oracle."""
+    eye = oracle.CsrArrays(4, 4, np.arange(5), np.arange(4), np.ones(4))
+    s = C.sgd_equilibrate_symmetric(eye, alpha=1.0, beta=1.0, iterations=100)
+    assert np.all(s.u == 0) and np.array_equal(s.u, s.v) and np.array_equal(s.d, s.e)
+    assert (s.apply_count, s.adjoint_count) == (100, 0)
+    rng = np.random.default_rng(61)
+    ns = oracle.CsrArrays(5, 5, dense=rng.standard_normal((5, 5)))
+    with pytest.raises(oracle.OracleError, match="symmetry check"):
+        C.sgd_equilibrate_symmetric(ns, alpha=1.0, beta=1.0, iterations=5)
+    with pytest.raises(oracle.OracleError, match="must be square"):
+        C.sgd_equilibrate_symmetric(oracle.CsrArrays(3, 4, dense=np.ones((3, 4))), alpha=1.0,
+                                    beta=1.0, iterations=5)
+    A = oracle.CsrArrays(5, 7, dense=rng.standard_normal((5, 7)))
+    plain = C.sgd_equilibrate(A, iterations=300, seed=11)
+    blk = C.sgd_equilibrate_block(A, np.arange(5), np.arange(7), 5, 7, iterations=300, seed=11)
+    for k in "uvde":
+        assert np.array_equal(getattr(plain, k), getattr(blk, k))
+    B = oracle.CsrArrays(3, 2, dense=rng.standard_normal((3, 2)) + 1.5)
+    for rb, cb, R, Cb, msg in [([0, 0, 1], [0, 1], 3, 2, "empty row block"),
+                               ([0, 0, 1], [0, 1], 1, 2, "row block index out of range"),
+                               ([0, 0, 1], [0, -1], 2, 2, "col block index out of range"),
+                               ([0, 0, 1], [0, 1], 0, 2, "block counts must be positive")]:
+        with pytest.raises(oracle.OracleError, match=msg):
+            C.sgd_equilibrate_block(B, rb, cb, R, Cb, iterations=3)
+    one = C.sgd_equilibrate_block(B, [0, 0, 0], [0, 0], 1, 1, iterations=50)
+    assert one.u[0] == one.u[1] == one.u[2] and one.v[0] == one.v[1]
