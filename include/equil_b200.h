@@ -176,6 +176,49 @@ equil_status equil_sgd_equilibrate_block(equil_matrix* A, const int64_t* row_blo
                                          const int64_t* col_block, int64_t row_blocks,
                                          int64_t col_blocks, const equil_params* p,
                                          const equil_diag_cfg* diag, equil_scaling_out* out);
+/* CcpOptions / CcpRun (include/equil/ccp.hpp:24-48).  tau, sigma <= 0 select
+ * the automatic 0.9 / |K|_2; p_star NaN disables the gap history.  Histories
+ * are caller-allocated with capacity hist_cap >= max_iters + 1 (+ iterations
+ * of the equilibration for the preconditioned run). */
+typedef struct {
+  int max_iters;
+  double tau;
+  double sigma;
+  double theta;
+  double p_star;
+  double gap_tol;
+} equil_ccp_options;
+typedef struct {
+  double* x; /* n */
+  double* objective_history;
+  double* gap_history; /* required when p_star is finite */
+  int hist_cap;
+  int hist_len;
+  int gap_len;
+  double tau, sigma, theta;
+  int iterations;
+  int equil_iterations;
+  int reached_tol;
+  long long apply_count;
+  long long adjoint_count;
+} equil_ccp_out;
+/* ccp_lasso(LassoProblem{A, b, lambda}, options) (include/equil/ccp.hpp:57,
+ * src/ccp.cpp:125-132): min |Ax - b|^2/sqrt(lambda) + sqrt(lambda)|x|_1.  Single GPU. */
+equil_status equil_ccp_lasso(equil_matrix* A, const double* b, double lambda,
+                             const equil_ccp_options* options, equil_ccp_out* out);
+/* ccp_lasso_preconditioned (include/equil/ccp.hpp:65-67, src/ccp.cpp:134-141) */
+equil_status equil_ccp_lasso_preconditioned(equil_matrix* A, const double* b, double lambda,
+                                            const equil_params* p,
+                                            const equil_ccp_options* options,
+                                            equil_ccp_out* out);
+/* spectral_norm(op, max_iters, rel_tol, seed) (include/equil/lsqr.hpp:44-48,
+ * src/lsqr.cpp:140-163): power iteration, normals on stream 19. */
+equil_status equil_spectral_norm(equil_matrix* A, int max_iters, double rel_tol, uint64_t seed,
+                                 double* out);
+/* lasso_objective(LassoProblem{A, b, lambda}, x) (include/equil/ccp.hpp:21,
+ * src/ccp.cpp:115-123) */
+equil_status equil_lasso_objective(equil_matrix* A, const double* b, double lambda,
+                                   const double* x, double* out);
 /* lsqr(op, b, max_iters, tol) (include/equil/lsqr.hpp:30-31, src/lsqr.cpp:85-103) */
 equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
                         equil_lsqr_out* out);

@@ -124,6 +124,43 @@ class LsqrRun:
     e: np.ndarray | None = None
 
 
+class _CcpOpts(C.Structure):
+    _fields_ = [("max_iters", C.c_int), ("tau", C.c_double), ("sigma", C.c_double),
+                ("theta", C.c_double), ("p_star", C.c_double), ("gap_tol", C.c_double)]
+
+
+class _CcpRun(C.Structure):  # eo_ccp_run and er_ccp_out share this layout
+    _fields_ = [("x", _dp), ("obj_hist", _dp), ("gap_hist", _dp), ("hist_len", C.c_int),
+                ("gap_len", C.c_int), ("tau", C.c_double), ("sigma", C.c_double),
+                ("theta", C.c_double), ("iterations", C.c_int),
+                ("equil_iterations", C.c_int), ("reached_tol", C.c_int),
+                ("apply_count", C.c_longlong), ("adjoint_count", C.c_longlong)]
+
+
+@dataclass
+class CcpRun:
+    x: np.ndarray
+    objective_history: np.ndarray
+    gap_history: np.ndarray
+    tau: float
+    sigma: float
+    theta: float
+    iterations: int
+    equil_iterations: int
+    reached_tol: bool
+    apply_count: int
+    adjoint_count: int
+
+
+def _ccp_call(n, cap, fn):
+    x, oh, gh = np.zeros(n), np.zeros(cap), np.zeros(cap)
+    r = _CcpRun(ptr(x, _dp), ptr(oh, _dp), ptr(gh, _dp), 0, 0, 0.0, 0.0, 0.0, 0, 0, 0, 0, 0)
+    rc = fn(C.byref(r))
+    return rc, CcpRun(x, oh[:r.hist_len].copy(), gh[:r.gap_len].copy(), r.tau, r.sigma, r.theta,
+                      r.iterations, r.equil_iterations, bool(r.reached_tol), r.apply_count,
+                      r.adjoint_count)
+
+
 class OracleError(Exception):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
@@ -190,6 +227,14 @@ class _COracle:
         L.eo_sgd_equilibrate_block.argtypes = [C.POINTER(_Matrix), _i64p, _i64p, C.c_int64,
                                                C.c_int64, C.POINTER(_Params), C.c_int,
                                                C.POINTER(_Scaling)]
+        L.eo_spectral_norm.argtypes = [C.POINTER(_Matrix), C.c_int, C.c_double, C.c_uint64, _dp]
+        L.eo_lasso_objective.restype = C.c_double
+        L.eo_lasso_objective.argtypes = [C.POINTER(_Matrix), _dp, C.c_double, _dp]
+        L.eo_ccp_lasso.argtypes = [C.POINTER(_Matrix), _dp, C.c_double, C.POINTER(_CcpOpts),
+                                   C.POINTER(_CcpRun)]
+        L.eo_ccp_lasso_preconditioned.argtypes = [C.POINTER(_Matrix), _dp, C.c_double,
+                                                  C.POINTER(_Params), C.POINTER(_CcpOpts),
+                                                  C.POINTER(_CcpRun)]
         L.eo_objective.restype = C.c_double
         L.eo_objective.argtypes = [C.POINTER(_Matrix), _dp, _dp, C.c_double, C.c_double, C.c_double]
         L.eo_rms_error.restype = C.c_double
@@ -354,6 +399,43 @@ class _COracle:
             C.byref(mat), ptr(rb, _i64p), ptr(cb, _i64p), row_blocks, col_blocks, C.byref(p),
             diag_stride, s), A.m, A.n, iterations, diag_stride)
 
+    def spectral_norm(self, A: CsrArrays, max_iters=100, rel_tol=1e-9, seed=0) -> float:
+        """src/lsqr.cpp:140-163"""
+        out = C.c_double(0.0)
+        mat = A._struct()
+        rc = self.L.eo_spectral_norm(C.byref(mat), max_iters, rel_tol, seed, C.byref(out))
+        if rc:
+            self._err(rc)
+        return out.value
+
+    def lasso_objective(self, A: CsrArrays, b, lam, x) -> float:
+        mat = A._struct()
+        return self.L.eo_lasso_objective(C.byref(mat), ptr(np.ascontiguousarray(b, np.float64),
+                                                            _dp), lam,
+                                         ptr(np.ascontiguousarray(x, np.float64), _dp))
+
+    def ccp_lasso(self, A: CsrArrays, b, lam, max_iters=1000, tau=0.0, sigma=0.0, theta=1.0,
+                  p_star=float("nan"), gap_tol=0.0, params=None) -> CcpRun:
+        """ccp_lasso / ccp_lasso_preconditioned (src/ccp.cpp:125-141);
+        params = dict of EquilibrationParams fields selects the latter."""
+        b = np.ascontiguousarray(b, np.float64)
+        o = _CcpOpts(max_iters, tau, sigma, theta, p_star, gap_tol)
+        mat = A._struct()
+        T = params.get("iterations", 1000) if params is not None else 0
+        cap = max(max_iters, 0) + 1 + max(T, 0)
+        if params is None:
+            rc, run = _ccp_call(A.n, cap, lambda r: self.L.eo_ccp_lasso(
+                C.byref(mat), ptr(b, _dp), lam, C.byref(o), r))
+        else:
+            p = _Params(params.get("alpha", 0.0), params.get("beta", 0.0),
+                        params.get("gamma", 0.1), params.get("max_log_scale", 9.210340371976184),
+                        T, params.get("seed", 0))
+            rc, run = _ccp_call(A.n, cap, lambda r: self.L.eo_ccp_lasso_preconditioned(
+                C.byref(mat), ptr(b, _dp), lam, C.byref(p), C.byref(o), r))
+        if rc:
+            self._err(rc)
+        return run
+
     def objective(self, A, u, v, alpha2, beta2, gamma):
         mat = A._struct()
         return self.L.eo_objective(C.byref(mat), ptr(np.ascontiguousarray(u, np.float64), _dp),
@@ -433,6 +515,16 @@ class _RefOracle:
                                        C.POINTER(_RefSgd)]
         L.er_sgd_block.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int64, C.c_int64, C.c_double,
                                    C.c_double, C.c_int, C.c_uint64, C.c_int, C.POINTER(_RefSgd)]
+        L.er_ccp_lasso.argtypes = [C.c_void_p, _dp, C.c_double, C.c_int, C.c_double,
+                                   C.c_double, C.c_double, C.c_double, C.c_double,
+                                   C.POINTER(_CcpRun)]
+        L.er_ccp_lasso_preconditioned.argtypes = [
+            C.c_void_p, _dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+            C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+            C.c_double, C.POINTER(_CcpRun)]
+        L.er_spectral_norm.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_uint64, _dp]
+        L.er_lasso_objective.argtypes = [C.c_void_p, _dp, C.c_double, _dp, _dp]
+        L.er_lasso_fista.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double, C.c_int, _dp, _dp]
         L.er_lsqr.argtypes = [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(_RefLsqr)]
         L.er_lsqr_preconditioned.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double,
                                              C.c_double, C.c_double, C.c_int, C.c_uint64,
@@ -571,6 +663,47 @@ class RefMatrix:
         return self._variant(lambda s: self.R.L.er_sgd_block(
             self.h, ptr(rb, _i64p), ptr(cb, _i64p), row_blocks, col_blocks, gamma,
             max_log_scale, iterations, seed, diag_stride, s), iterations, diag_stride)
+
+    def ccp_lasso(self, b, lam, max_iters=1000, tau=0.0, sigma=0.0, theta=1.0,
+                  p_star=float("nan"), gap_tol=0.0, params=None) -> CcpRun:
+        b = np.ascontiguousarray(b, np.float64)
+        T = params.get("iterations", 1000) if params is not None else 0
+        cap = max(max_iters, 0) + 1 + max(T, 0)
+        if params is None:
+            rc, run = _ccp_call(self.n, cap, lambda r: self.R.L.er_ccp_lasso(
+                self.h, ptr(b, _dp), lam, max_iters, tau, sigma, theta, p_star, gap_tol, r))
+        else:
+            rc, run = _ccp_call(self.n, cap, lambda r: self.R.L.er_ccp_lasso_preconditioned(
+                self.h, ptr(b, _dp), lam, params.get("alpha", 0.0), params.get("beta", 0.0),
+                params.get("gamma", 0.1), params.get("max_log_scale", 9.210340371976184), T,
+                params.get("seed", 0), max_iters, tau, sigma, theta, p_star, gap_tol, r))
+        if rc:
+            self.R._err(rc)
+        return run
+
+    def spectral_norm(self, max_iters=100, rel_tol=1e-9, seed=0) -> float:
+        out = C.c_double(0.0)
+        rc = self.R.L.er_spectral_norm(self.h, max_iters, rel_tol, seed, C.byref(out))
+        if rc:
+            self.R._err(rc)
+        return out.value
+
+    def lasso_objective(self, b, lam, x) -> float:
+        out = C.c_double(0.0)
+        rc = self.R.L.er_lasso_objective(self.h, ptr(np.ascontiguousarray(b, np.float64), _dp),
+                                         lam, ptr(np.ascontiguousarray(x, np.float64), _dp),
+                                         C.byref(out))
+        if rc:
+            self.R._err(rc)
+        return out.value
+
+    def lasso_fista(self, b, lam, grad_map_tol=1e-12, max_iters=500000):
+        x, ps = np.zeros(self.n), C.c_double(0.0)
+        rc = self.R.L.er_lasso_fista(self.h, ptr(np.ascontiguousarray(b, np.float64), _dp), lam,
+                                     grad_map_tol, max_iters, ptr(x, _dp), C.byref(ps))
+        if rc:
+            self.R._err(rc)
+        return x, ps.value
 
     def lsqr(self, b, max_iters, tol) -> LsqrRun:
         b = np.ascontiguousarray(b, np.float64)

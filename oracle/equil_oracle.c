@@ -966,3 +966,194 @@ int eo_lsqr_preconditioned(const eo_matrix* A, const double* b,
   free(su); free(sv); free(d); free(e);
   return 0;
 }
+
+/* ========================================================================== */
+/* spectral_norm (src/lsqr.cpp:140-163) and ccp_lasso (src/ccp.cpp:28-160)     */
+/* ========================================================================== */
+
+/* power iteration on B = diag(d) A diag(e) (d == NULL: A), uncharged */
+static int spectral_norm_op(const eo_matrix* A, const double* d, const double* e,
+                            int max_iters, double rel_tol, uint64_t seed, double* out) {
+  if (max_iters <= 0) return fail("spectral_norm: max_iters must be positive");
+  const int64_t m = A->m, n = A->n;
+  double* x = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* y = (double*)malloc((size_t)(m ? m : 1) * 8);
+  double* z = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* tn = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* tm = (double*)malloc((size_t)(m ? m : 1) * 8);
+  lsqr_op B = {A, d, e, tn, tm, 0, 0};
+  eo_rng r;
+  eo_rng_init(&r, seed, 19); /* streams::kPowerIteration */
+  for (int64_t j = 0; j < n; ++j) x[j] = eo_rng_normal(&r);
+  const double xn = sqrt(eo_canon_sumsq(x, n));
+  int rc = 0;
+  double lambda = 0.0;
+  if (!(xn > 0.0)) {
+    rc = fail("spectral_norm: degenerate start");
+  } else {
+    for (int64_t j = 0; j < n; ++j) x[j] = x[j] / xn;
+    for (int t = 0; t < max_iters; ++t) {
+      B_apply(&B, x, y);
+      const double next = eo_canon_sumsq(y, m); /* Rayleigh quotient of A^T A */
+      if (next == 0.0) {
+        lambda = 0.0;
+        break;
+      }
+      const int settled = fabs(next - lambda) <= rel_tol * next;
+      lambda = next;
+      if (settled) break;
+      B_adjoint(&B, y, z);
+      const double zn = sqrt(eo_canon_sumsq(z, n));
+      if (zn == 0.0) break;
+      for (int64_t j = 0; j < n; ++j) x[j] = z[j] / zn;
+    }
+  }
+  *out = sqrt(lambda);
+  free(x); free(y); free(z); free(tn); free(tm);
+  return rc;
+}
+
+int eo_spectral_norm(const eo_matrix* A, int max_iters, double rel_tol, uint64_t seed,
+                     double* out) {
+  return spectral_norm_op(A, NULL, NULL, max_iters, rel_tol, seed, out);
+}
+
+/* |A x - b|^2 / sqrt(lambda) + sqrt(lambda) |x|_1 (src/ccp.cpp:115-123) */
+double eo_lasso_objective(const eo_matrix* A, const double* b, double lambda, const double* x) {
+  const int64_t m = A->m, n = A->n;
+  const double sl = sqrt(lambda);
+  double* r = (double*)malloc((size_t)(m ? m : 1) * 8);
+  double* ax = (double*)malloc((size_t)(n ? n : 1) * 8);
+  mat_apply(A, x, r);
+  for (int64_t i = 0; i < m; ++i) r[i] = r[i] - b[i];
+  for (int64_t j = 0; j < n; ++j) ax[j] = fabs(x[j]);
+  const double f = eo_canon_sumsq(r, m) / sl + sl * eo_canon_sum(ax, n);
+  free(r);
+  free(ax);
+  return f;
+}
+
+static double soft_threshold(double q, double t) { /* src/ccp.cpp:19-23 */
+  if (q > t) return q - t;
+  if (q < -t) return q + t;
+  return 0.0;
+}
+
+static int ccp_validate(const eo_matrix* A, const double* b, double lambda,
+                        const eo_ccp_options* o, const char* who) { /* :11-17 */
+  if (!(lambda > 0.0)) return fail("lasso: lambda must be positive");
+  if (!(sqrt(eo_canon_sumsq(b, A->m)) > 0.0)) return fail("lasso: rhs must be nonzero");
+  if (o->max_iters < 0) {
+    static char msg[128];
+    snprintf(msg, sizeof msg, "%s: max_iters must be nonnegative", who);
+    return fail(msg);
+  }
+  return 0;
+}
+
+/* ccp_core (src/ccp.cpp:27-110); d == NULL: plain run (d = e = 1) */
+static int ccp_core(const eo_matrix* A, const double* b, double lambda, const double* d,
+                    const double* e, int equil_iters, long long applies0, long long adjoints0,
+                    const eo_ccp_options* o, eo_ccp_run* out) {
+  const int64_t m = A->m, n = A->n;
+  const double sl = sqrt(lambda);
+  double tau, sigma;
+  if (o->tau > 0.0 && o->sigma > 0.0) {
+    tau = o->tau;
+    sigma = o->sigma;
+  } else {
+    double norm2;
+    if (spectral_norm_op(A, d, e, 100, 1e-9, 0, &norm2)) return 1;
+    if (!(norm2 > 0.0)) return fail("ccp_lasso: zero operator");
+    tau = 0.9 / norm2;
+    sigma = 0.9 / norm2;
+  }
+  out->tau = tau;
+  out->sigma = sigma;
+  out->theta = o->theta;
+  out->equil_iterations = equil_iters;
+  out->iterations = 0;
+  out->reached_tol = 0;
+  out->hist_len = 0;
+  out->gap_len = 0;
+  double* zero = (double*)calloc((size_t)(n ? n : 1), 8);
+  const double f0 = eo_lasso_objective(A, b, lambda, zero);
+  const int track = isfinite(o->p_star);
+#define CCP_PUSH(f)                                                   \
+  do {                                                                \
+    out->obj_hist[out->hist_len++] = (f);                             \
+    if (track) out->gap_hist[out->gap_len++] = ((f) - o->p_star) / f0; \
+  } while (0)
+  for (int t = 0; t <= equil_iters; ++t) CCP_PUSH(f0);
+  if (track && o->gap_tol > 0.0 && out->gap_hist[out->gap_len - 1] <= o->gap_tol)
+    out->reached_tol = 1;
+  double* y = (double*)calloc((size_t)(m ? m : 1), 8);
+  double* kz = (double*)malloc((size_t)(m ? m : 1) * 8);
+  double* z = (double*)calloc((size_t)(n ? n : 1), 8);
+  double* zt = (double*)calloc((size_t)(n ? n : 1), 8);
+  double* zn = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* g = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* x = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* tn = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* tm = (double*)malloc((size_t)(m ? m : 1) * 8);
+  lsqr_op K = {A, d, e, tn, tm, 0, 0};
+  for (int t = 1; t <= o->max_iters && !out->reached_tol; ++t) {
+    /* dual: y = (y + sigma K z~ - sigma d b) / (1 + 0.5 sigma d d sqrt(lambda)) */
+    B_apply(&K, zt, kz);
+    for (int64_t i = 0; i < m; ++i) {
+      const double di = d ? d[i] : 1.0;
+      const double yh = y[i] + sigma * kz[i];
+      y[i] = (yh - sigma * di * b[i]) / (1.0 + 0.5 * sigma * di * di * sl);
+    }
+    /* primal: weighted shrinkage, extrapolation */
+    B_adjoint(&K, y, g);
+    for (int64_t j = 0; j < n; ++j) {
+      const double ej = e ? e[j] : 1.0;
+      zn[j] = soft_threshold(z[j] - tau * g[j], tau * sl * ej);
+    }
+    for (int64_t j = 0; j < n; ++j) {
+      zt[j] = zn[j] + o->theta * (zn[j] - z[j]);
+      z[j] = zn[j];
+    }
+    out->iterations = t;
+    for (int64_t j = 0; j < n; ++j) x[j] = (e ? e[j] : 1.0) * z[j];
+    const double f = eo_lasso_objective(A, b, lambda, x);
+    CCP_PUSH(f);
+    if (track && o->gap_tol > 0.0 && out->gap_hist[out->gap_len - 1] <= o->gap_tol)
+      out->reached_tol = 1;
+  }
+#undef CCP_PUSH
+  for (int64_t j = 0; j < n; ++j) out->x[j] = (e ? e[j] : 1.0) * z[j];
+  out->apply_count = applies0 + K.applies;
+  out->adjoint_count = adjoints0 + K.adjoints;
+  free(zero); free(y); free(kz); free(z); free(zt); free(zn); free(g); free(x);
+  free(tn); free(tm);
+  return 0;
+}
+
+int eo_ccp_lasso(const eo_matrix* A, const double* b, double lambda, const eo_ccp_options* o,
+                 eo_ccp_run* out) {
+  if (ccp_validate(A, b, lambda, o, "ccp_lasso")) return 1;
+  return ccp_core(A, b, lambda, NULL, NULL, 0, 0, 0, o, out);
+}
+
+int eo_ccp_lasso_preconditioned(const eo_matrix* A, const double* b, double lambda,
+                                const eo_params* p, const eo_ccp_options* o, eo_ccp_run* out) {
+  if (ccp_validate(A, b, lambda, o, "ccp_lasso_preconditioned")) return 1;
+  const int64_t m = A->m, n = A->n;
+  double* u = (double*)malloc((size_t)(m ? m : 1) * 8);
+  double* v = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* d = (double*)malloc((size_t)(m ? m : 1) * 8);
+  double* e = (double*)malloc((size_t)(n ? n : 1) * 8);
+  eo_scaling s;
+  memset(&s, 0, sizeof s);
+  s.u = u;
+  s.v = v;
+  s.d = d;
+  s.e = e;
+  int rc = eo_sgd_equilibrate(A, p, 0, &s); /* :139 */
+  if (!rc) rc = ccp_core(A, b, lambda, d, e, p->iterations, s.apply_count, s.adjoint_count, o,
+                         out);
+  free(u); free(v); free(d); free(e);
+  return rc;
+}

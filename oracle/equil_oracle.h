@@ -158,6 +158,31 @@ int eo_lsqr_preconditioned(const eo_matrix* A, const double* b,
                            const eo_params* p, int max_iters, double tol,
                            eo_lsqr_run* out);
 
+/* ---- spectral_norm (src/lsqr.cpp:140-163) and the Chambolle-Pock lasso
+ * (src/ccp.cpp:28-160) --------------------------------------------------- */
+int eo_spectral_norm(const eo_matrix* A, int max_iters, double rel_tol, uint64_t seed,
+                     double* out);
+double eo_lasso_objective(const eo_matrix* A, const double* b, double lambda, const double* x);
+typedef struct {
+  int max_iters;
+  double tau, sigma, theta; /* tau, sigma <= 0: auto 0.9 / |K|_2 */
+  double p_star;            /* NaN: no gap history */
+  double gap_tol;
+} eo_ccp_options;
+typedef struct {
+  double* x;        /* n */
+  double* obj_hist; /* capacity max_iters + 1 (+ T) */
+  double* gap_hist; /* same capacity, or NULL */
+  int hist_len, gap_len;
+  double tau, sigma, theta;
+  int iterations, equil_iterations, reached_tol;
+  long long apply_count, adjoint_count;
+} eo_ccp_run;
+int eo_ccp_lasso(const eo_matrix* A, const double* b, double lambda, const eo_ccp_options* o,
+                 eo_ccp_run* out);
+int eo_ccp_lasso_preconditioned(const eo_matrix* A, const double* b, double lambda,
+                                const eo_params* p, const eo_ccp_options* o, eo_ccp_run* out);
+
 #ifdef __cplusplus
 }
 #endif

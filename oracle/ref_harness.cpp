@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "equil/ccp.hpp"
 #include "equil/equilibrate.hpp"
 #include "equil/explicit_matrix.hpp"
 #include "equil/lsqr.hpp"
@@ -280,6 +281,102 @@ int er_sgd_block(void* h, const int64_t* rb, const int64_t* cb, int64_t R, int64
       diag.stride = diag_stride;
     }
     copy_scaling(sgd_equilibrate_block(A, bs, p, diag), out);
+  });
+}
+
+// ---- ccp_lasso / ccp_lasso_preconditioned / spectral_norm / lasso_fista
+struct er_ccp_out {
+  double* x;          // n
+  double* obj_hist;   // capacity max_iters + 1 (+ T)
+  double* gap_hist;   // same capacity (may be unused)
+  int hist_len, gap_len;
+  double tau, sigma, theta;
+  int iterations, equil_iterations, reached_tol;
+  long long apply_count, adjoint_count;
+};
+
+static void copy_ccp(const CcpRun& r, er_ccp_out* out) {
+  from_vec(r.x, out->x);
+  out->hist_len = static_cast<int>(r.objective_history.size());
+  std::memcpy(out->obj_hist, r.objective_history.data(),
+              r.objective_history.size() * sizeof(double));
+  out->gap_len = static_cast<int>(r.gap_history.size());
+  if (out->gap_hist && !r.gap_history.empty())
+    std::memcpy(out->gap_hist, r.gap_history.data(), r.gap_history.size() * sizeof(double));
+  out->tau = r.tau;
+  out->sigma = r.sigma;
+  out->theta = r.theta;
+  out->iterations = r.iterations;
+  out->equil_iterations = r.equil_iterations;
+  out->reached_tol = r.reached_tol;
+  out->apply_count = r.apply_count;
+  out->adjoint_count = r.adjoint_count;
+}
+
+static CcpOptions ccp_opts(int max_iters, double tau, double sigma, double theta, double p_star,
+                           double gap_tol) {
+  CcpOptions o;
+  o.max_iters = max_iters;
+  o.tau = tau;
+  o.sigma = sigma;
+  o.theta = theta;
+  o.p_star = p_star;
+  o.gap_tol = gap_tol;
+  return o;
+}
+
+int er_ccp_lasso(void* h, const double* b, double lambda, int max_iters, double tau,
+                 double sigma, double theta, double p_star, double gap_tol, er_ccp_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    LassoProblem prob{&A, to_vec(b, A.rows()), lambda};
+    copy_ccp(ccp_lasso(prob, ccp_opts(max_iters, tau, sigma, theta, p_star, gap_tol)), out);
+  });
+}
+
+int er_ccp_lasso_preconditioned(void* h, const double* b, double lambda, double alpha,
+                                double beta, double gamma, double max_log_scale,
+                                int iterations, uint64_t seed, int max_iters, double tau,
+                                double sigma, double theta, double p_star, double gap_tol,
+                                er_ccp_out* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    LassoProblem prob{&A, to_vec(b, A.rows()), lambda};
+    EquilibrationParams p;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.gamma = gamma;
+    p.max_log_scale = max_log_scale;
+    p.iterations = iterations;
+    p.seed = seed;
+    copy_ccp(ccp_lasso_preconditioned(prob, p,
+                                      ccp_opts(max_iters, tau, sigma, theta, p_star, gap_tol)),
+             out);
+  });
+}
+
+int er_spectral_norm(void* h, int max_iters, double rel_tol, uint64_t seed, double* out) {
+  return guarded([&] {
+    *out = spectral_norm(*static_cast<ExplicitMatrix*>(h), max_iters, rel_tol, seed);
+  });
+}
+
+int er_lasso_objective(void* h, const double* b, double lambda, const double* x, double* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    LassoProblem prob{&A, to_vec(b, A.rows()), lambda};
+    *out = lasso_objective(prob, to_vec(x, A.cols()));
+  });
+}
+
+int er_lasso_fista(void* h, const double* b, double lambda, double grad_map_tol, int max_iters,
+                   double* x, double* p_star) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    LassoProblem prob{&A, to_vec(b, A.rows()), lambda};
+    const FistaResult r = lasso_fista(prob, grad_map_tol, max_iters);
+    from_vec(r.x, x);
+    *p_star = r.p_star;
   });
 }
 

@@ -5,9 +5,11 @@ C ABI in include/equil_b200.h); this package is the Python mirror of the
 reference's interface over that ABI.  See DESIGN.md.
 """
 from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
-                  BlockStructure, DiagnosticsConfig, EquilibrationParams, EquilRuntimeError,
-                  ExplicitMatrix, InvalidArgument, IterationRecord, LsqrRun,
-                  ScalingResult, canon_sumsq_device, det_exp_device, kernel_launches,
+                  BlockStructure, CcpOptions, CcpRun, DiagnosticsConfig,
+                  EquilibrationParams, EquilRuntimeError,
+                  ExplicitMatrix, InvalidArgument, IterationRecord, LassoProblem, LsqrRun,
+                  ScalingResult, canon_sumsq_device, ccp_lasso, ccp_lasso_preconditioned,
+                  lasso_objective, spectral_norm, det_exp_device, kernel_launches,
                   last_loop_ms, lsqr, lsqr_preconditioned, nccl_unique_id,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
                   sgd_equilibrate_block, sgd_equilibrate_symmetric, sgd_equilibrate_targets,
@@ -15,6 +17,8 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
 
 __all__ = [
     "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "BlockStructure",
+    "CcpOptions", "CcpRun", "LassoProblem", "ccp_lasso", "ccp_lasso_preconditioned",
+    "lasso_objective", "spectral_norm",
     "DiagnosticsConfig",
     "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",
     "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",

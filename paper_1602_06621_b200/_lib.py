@@ -54,6 +54,20 @@ class LsqrOut(C.Structure):
                 ("adjoint_count", C.c_longlong)]
 
 
+class CcpOptions(C.Structure):
+    _fields_ = [("max_iters", C.c_int), ("tau", C.c_double), ("sigma", C.c_double),
+                ("theta", C.c_double), ("p_star", C.c_double), ("gap_tol", C.c_double)]
+
+
+class CcpOut(C.Structure):
+    _fields_ = [("x", _dp), ("objective_history", _dp), ("gap_history", _dp),
+                ("hist_cap", C.c_int), ("hist_len", C.c_int), ("gap_len", C.c_int),
+                ("tau", C.c_double), ("sigma", C.c_double), ("theta", C.c_double),
+                ("iterations", C.c_int), ("equil_iterations", C.c_int),
+                ("reached_tol", C.c_int), ("apply_count", C.c_longlong),
+                ("adjoint_count", C.c_longlong)]
+
+
 # every exported symbol of include/equil_b200.h with (restype, argtypes)
 SIGNATURES = {
     "equil_params_default": (None, [C.POINTER(Params)]),
@@ -80,6 +94,13 @@ SIGNATURES = {
     "equil_sgd_equilibrate_block": (C.c_int, [C.c_void_p, _i64p, _i64p, C.c_int64, C.c_int64,
                                               C.POINTER(Params), C.POINTER(DiagCfg),
                                               C.POINTER(ScalingOut)]),
+    "equil_ccp_lasso": (C.c_int, [C.c_void_p, _dp, C.c_double, C.POINTER(CcpOptions),
+                                  C.POINTER(CcpOut)]),
+    "equil_ccp_lasso_preconditioned": (C.c_int, [C.c_void_p, _dp, C.c_double,
+                                                 C.POINTER(Params), C.POINTER(CcpOptions),
+                                                 C.POINTER(CcpOut)]),
+    "equil_spectral_norm": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, _dp]),
+    "equil_lasso_objective": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp]),
     "equil_lsqr": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(LsqrOut)]),
     "equil_lsqr_preconditioned": (C.c_int, [C.c_void_p, _dp, C.POINTER(Params), C.c_int,
                                             C.c_double, C.POINTER(LsqrOut)]),

@@ -349,6 +349,99 @@ def sgd_equilibrate_block(op: ExplicitMatrix, structure: BlockStructure,
                                                       int(structure.col_blocks), p, dc, out))
 
 
+@dataclass
+class LassoProblem:
+    """LassoProblem (include/equil/ccp.hpp:14-18): min |A x - b|^2 / sqrt(lambda)
+    + sqrt(lambda) |x|_1."""
+    op: ExplicitMatrix
+    b: np.ndarray
+    lam: float
+
+
+@dataclass
+class CcpOptions:
+    """CcpOptions (include/equil/ccp.hpp:24-33)."""
+    max_iters: int = 1000
+    tau: float = 0.0     # 0 = auto 0.9 / |K|_2
+    sigma: float = 0.0
+    theta: float = 1.0
+    p_star: float = float("nan")  # NaN disables gap_history
+    gap_tol: float = 0.0
+
+
+@dataclass
+class CcpRun:
+    """CcpRun (include/equil/ccp.hpp:35-48)."""
+    x: np.ndarray
+    objective_history: list
+    gap_history: list
+    tau: float
+    sigma: float
+    theta: float
+    iterations: int
+    equil_iterations: int
+    reached_tol: bool
+    apply_count: int
+    adjoint_count: int
+
+
+def _ccp(prob: LassoProblem, params, options: CcpOptions | None) -> CcpRun:
+    options = options or CcpOptions()
+    b = np.ascontiguousarray(prob.b, dtype=np.float64)
+    if b.size != prob.op.rows():
+        raise InvalidArgument("lasso: rhs length mismatch")
+    T = max(int(params.iterations), 0) if params is not None else 0
+    cap = max(int(options.max_iters), 0) + 1 + T
+    x, oh, gh = np.zeros(prob.op.cols()), np.zeros(cap), np.zeros(cap)
+    o = L.CcpOptions(int(options.max_iters), float(options.tau), float(options.sigma),
+                     float(options.theta), float(options.p_star), float(options.gap_tol))
+    out = L.CcpOut(L.ptr(x, L._dp), L.ptr(oh, L._dp), L.ptr(gh, L._dp), cap, 0, 0, 0.0, 0.0,
+                   0.0, 0, 0, 0, 0, 0)
+    lib = L.load()
+    if params is None:
+        _check(lib.equil_ccp_lasso(prob.op._h, L.ptr(b, L._dp), float(prob.lam), C.byref(o),
+                                   C.byref(out)))
+    else:
+        p = params._c()
+        _check(lib.equil_ccp_lasso_preconditioned(prob.op._h, L.ptr(b, L._dp), float(prob.lam),
+                                                  C.byref(p), C.byref(o), C.byref(out)))
+    return CcpRun(x, oh[:out.hist_len].tolist(), gh[:out.gap_len].tolist(), out.tau, out.sigma,
+                  out.theta, out.iterations, out.equil_iterations, bool(out.reached_tol),
+                  out.apply_count, out.adjoint_count)
+
+
+def ccp_lasso(prob: LassoProblem, options: CcpOptions | None = None) -> CcpRun:
+    """ccp_lasso (include/equil/ccp.hpp:57, src/ccp.cpp:125-132)."""
+    return _ccp(prob, None, options)
+
+
+def ccp_lasso_preconditioned(prob: LassoProblem, params: EquilibrationParams,
+                             options: CcpOptions | None = None) -> CcpRun:
+    """ccp_lasso_preconditioned (include/equil/ccp.hpp:65-67, src/ccp.cpp:134-141)."""
+    return _ccp(prob, params, options)
+
+
+def spectral_norm(op: ExplicitMatrix, max_iters: int = 100, rel_tol: float = 1e-6,
+                  seed: int = 0) -> float:
+    """spectral_norm (include/equil/lsqr.hpp:44-48, src/lsqr.cpp:140-163)."""
+    out = C.c_double(0.0)
+    _check(L.load().equil_spectral_norm(op._h, int(max_iters), float(rel_tol), int(seed),
+                                        C.byref(out)))
+    return out.value
+
+
+def lasso_objective(prob: LassoProblem, x) -> float:
+    """lasso_objective (include/equil/ccp.hpp:21, src/ccp.cpp:115-123)."""
+    b = np.ascontiguousarray(prob.b, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.size != prob.op.cols():
+        raise InvalidArgument("lasso_objective: x length mismatch")
+    out = C.c_double(0.0)
+    _check(L.load().equil_lasso_objective(prob.op._h, L.ptr(b, L._dp), float(prob.lam),
+                                          L.ptr(x, L._dp), C.byref(out)))
+    return out.value
+
+
 def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,
                            u_ptr: int, v_ptr: int, d_ptr: int, e_ptr: int) -> ScalingResult:
     """sgd_equilibrate with u, v, d, e written to caller-owned DEVICE buffers

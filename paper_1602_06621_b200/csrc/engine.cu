@@ -2116,3 +2116,237 @@ equil_status equil_sgd_equilibrate_block(equil_matrix* M, const int64_t* row_blo
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// spectral_norm (src/lsqr.cpp:140-163) and the Chambolle-Pock lasso
+// (src/ccp.cpp:27-160): the second consumer of the equilibration's d, e.
+// Device vectors, canonical reductions; the lasso objective of every iterate
+// is evaluated on the device into a history array, so a run without an early
+// stop test synchronises only at its end.  Single GPU.
+// ---------------------------------------------------------------------------
+namespace {
+
+// power iteration on diag(d) A diag(e) (d, e null: A), uncharged
+double spectral_norm_dev(equil_matrix* M, const double* d, const double* e, int max_iters,
+                         double rel_tol, uint64_t seed) {
+  require(max_iters > 0, "spectral_norm: max_iters must be positive");
+  const int64_t m = M->m, n = M->n;
+  cudaStream_t s = M->stream;
+  HostRng rng(seed, 19);  // streams::kPowerIteration
+  std::vector<double> xh(n);
+  for (int64_t j = 0; j < n; ++j) xh[j] = rng.normal();
+  DevBuf<double> x, y, z, t;
+  x.alloc(n); y.alloc(m); z.alloc(n); t.alloc(std::max(m, n));
+  double* sc = M->scal.p + 40;
+  CK(cudaMemcpyAsync(x.p, xh.data(), n * 8, cudaMemcpyHostToDevice, s));
+  canon_reduce(M, x.p, n, sc + 0, 0, 0.0, true);
+  const double xn = read_scalar(M, sc + 0);
+  if (!(xn > 0.0)) fail(EQUIL_ERUNTIME, "spectral_norm: degenerate start");
+  CK(eqb::launch_lsqr_normalize(x.p, x.p, sc + 0, nullptr, nullptr, n, nullptr, nullptr, s));
+  double lambda = 0.0;
+  for (int it = 0; it < max_iters; ++it) {
+    const double* xg = x.p;
+    if (e) {
+      CK(eqb::launch_mul(t.p, e, x.p, n, s));
+      xg = t.p;
+    }
+    apply_pass(M, false, xg, y.p, eqb::kPassScaled, d, nullptr, nullptr);
+    canon_reduce(M, y.p, m, sc + 1, 0);
+    const double next = read_scalar(M, sc + 1);
+    if (next == 0.0) return 0.0;
+    const bool settled = std::abs(next - lambda) <= rel_tol * next;
+    lambda = next;
+    if (settled) break;
+    const double* yg = y.p;
+    if (d) {
+      CK(eqb::launch_mul(t.p, d, y.p, m, s));
+      yg = t.p;
+    }
+    apply_pass(M, true, yg, z.p, eqb::kPassScaled, e, nullptr, nullptr);
+    canon_reduce(M, z.p, n, sc + 2, 0, 0.0, true);
+    const double zn = read_scalar(M, sc + 2);
+    if (zn == 0.0) break;
+    CK(eqb::launch_lsqr_normalize(x.p, z.p, sc + 2, nullptr, nullptr, n, nullptr, nullptr, s));
+  }
+  return std::sqrt(lambda);
+}
+
+// lasso_objective (src/ccp.cpp:115-123) of device x into *out (device)
+void lasso_value_dev(equil_matrix* M, const double* b_d, double sqrt_lambda, const double* x,
+                     const double* absx, double* r, double* out) {
+  apply_pass(M, false, x, r, eqb::kPassResid, nullptr, b_d, nullptr);  // b - Ax: same squares
+  double* sc = M->scal.p + 44;
+  canon_reduce(M, r, M->m, sc + 0, 0);
+  canon_reduce(M, absx, M->n, sc + 1, 1);
+  CK(eqb::launch_lasso_value(sc + 0, sc + 1, sqrt_lambda, out, M->stream));
+}
+
+void ccp_common(equil_matrix* M, const double* b, double lambda, const equil_params* p,
+                const equil_ccp_options* o, equil_ccp_out* out, const char* who) {
+  require(M != nullptr && o != nullptr && out != nullptr, std::string(who) + ": null argument");
+  require(b != nullptr, "lasso: rhs length mismatch");
+  std::lock_guard<std::mutex> lk(M->mu);
+  DeviceGuard dg(M->device);
+  require(M->world == 1, std::string(who) + ": single-GPU matrices only in this build");
+  cudaStream_t s = M->stream;
+  const int64_t m = M->m, n = M->n;
+  // validate_problem (:11-17)
+  require(lambda > 0.0, "lasso: lambda must be positive");
+  DevBuf<double> b_d;
+  b_d.alloc(m);
+  CK(cudaMemcpyAsync(b_d.p, b, m * 8, cudaMemcpyHostToDevice, s));
+  canon_reduce(M, b_d.p, m, M->scal.p + 48, 0, 0.0, true);
+  require(read_scalar(M, M->scal.p + 48) > 0.0, "lasso: rhs must be nonzero");
+  require(o->max_iters >= 0, std::string(who) + ": max_iters must be nonnegative");
+  const int T = p ? p->iterations : 0;
+  require(out->objective_history != nullptr &&
+              out->hist_cap >= std::max(o->max_iters, 0) + 1 + std::max(T, 0),
+          std::string(who) + ": history capacity too small");
+  const bool track = std::isfinite(o->p_star);
+  require(!track || out->gap_history != nullptr, std::string(who) + ": gap_history missing");
+
+  long long applies = 0, adjoints = 0;
+  DevBuf<double> dd, ed;
+  const double* d = nullptr;
+  const double* e = nullptr;
+  if (p) {  // sgd_equilibrate on the charged operator (:139)
+    dd.alloc(m);
+    ed.alloc(n);
+    equil_scaling_out so{};
+    so.d = dd.p;
+    so.e = ed.p;
+    so.outputs_on_device = 1;
+    M->mu.unlock();
+    const equil_status rc = equil_sgd_equilibrate(M, p, nullptr, &so);
+    M->mu.lock();
+    if (rc != EQUIL_OK) fail(rc, g_err);
+    applies = so.apply_count;
+    adjoints = so.adjoint_count;
+    d = dd.p;
+    e = ed.p;
+  }
+  // ccp_core (:27-110)
+  const double sl = std::sqrt(lambda);
+  double tau, sigma;
+  if (o->tau > 0.0 && o->sigma > 0.0) {
+    tau = o->tau;
+    sigma = o->sigma;
+  } else {
+    const double norm2 = spectral_norm_dev(M, d, e, 100, 1e-9, 0);
+    if (!(norm2 > 0.0)) fail(EQUIL_ERUNTIME, "ccp_lasso: zero operator");
+    tau = 0.9 / norm2;
+    sigma = 0.9 / norm2;
+  }
+  const double f0 = [&] {
+    DevBuf<double> zero, r, v;
+    zero.alloc(n);
+    r.alloc(m);
+    v.alloc(1);
+    CK(cudaMemsetAsync(zero.p, 0, n * 8, s));
+    lasso_value_dev(M, b_d.p, sl, zero.p, zero.p, r.p, v.p);
+    return read_scalar(M, v.p);
+  }();
+  int hl = 0, gl = 0;
+  bool reached = false;
+  auto push = [&](double f) {
+    out->objective_history[hl++] = f;
+    if (track) out->gap_history[gl++] = (f - o->p_star) / f0;
+  };
+  for (int t = 0; t <= T; ++t) push(f0);
+  if (track && o->gap_tol > 0.0 && out->gap_history[gl - 1] <= o->gap_tol) reached = true;
+
+  DevBuf<double> y, kz, dy, z, ezt, g, x, absx, r, fh;
+  y.alloc(m); kz.alloc(m); dy.alloc(m); r.alloc(m);
+  z.alloc(n); ezt.alloc(n); g.alloc(n); x.alloc(n); absx.alloc(n);
+  const int iters = std::max(o->max_iters, 0);
+  fh.alloc(std::max(iters, 1));
+  CK(cudaMemsetAsync(y.p, 0, m * 8, s));
+  CK(cudaMemsetAsync(z.p, 0, n * 8, s));
+  CK(cudaMemsetAsync(ezt.p, 0, n * 8, s));
+  CK(cudaMemsetAsync(x.p, 0, n * 8, s));
+  const bool early = track && o->gap_tol > 0.0;  // stop test needs f on the host
+  int done = 0;
+  for (int t = 1; t <= iters && !reached; ++t) {
+    apply_pass(M, false, ezt.p, kz.p, eqb::kPassScaled, d, nullptr, nullptr);  // K z~
+    ++applies;
+    CK(eqb::launch_ccp_dual(y.p, kz.p, d, b_d.p, sigma, sl, m, dy.p, s));
+    apply_pass(M, true, dy.p, g.p, eqb::kPassScaled, e, nullptr, nullptr);  // K^T y
+    ++adjoints;
+    CK(eqb::launch_ccp_primal(z.p, ezt.p, g.p, e, tau, tau * sl, o->theta, n, x.p, absx.p, s));
+    lasso_value_dev(M, b_d.p, sl, x.p, absx.p, r.p, fh.p + (t - 1));  // uncharged probe
+    done = t;
+    if (early) {
+      push(read_scalar(M, fh.p + (t - 1)));
+      if (out->gap_history[gl - 1] <= o->gap_tol) reached = true;
+    }
+  }
+  if (!early && done > 0) {
+    std::vector<double> f(done);
+    CK(cudaMemcpyAsync(f.data(), fh.p, done * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (double v : f) push(v);
+  }
+  if (out->x) CK(cudaMemcpyAsync(out->x, x.p, n * 8, cudaMemcpyDeviceToHost, s));  // e .* z
+  CK(cudaStreamSynchronize(s));
+  out->hist_len = hl;
+  out->gap_len = gl;
+  out->tau = tau;
+  out->sigma = sigma;
+  out->theta = o->theta;
+  out->iterations = done;
+  out->equil_iterations = T;
+  out->reached_tol = reached ? 1 : 0;
+  out->apply_count = applies;
+  out->adjoint_count = adjoints;
+}
+
+}  // namespace
+
+extern "C" {
+
+equil_status equil_spectral_norm(equil_matrix* M, int max_iters, double rel_tol, uint64_t seed,
+                                 double* out) {
+  return guarded([&] {
+    require(M != nullptr && out != nullptr, "spectral_norm: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    require(M->world == 1, "spectral_norm: single-GPU matrices only in this build");
+    *out = spectral_norm_dev(M, nullptr, nullptr, max_iters, rel_tol, seed);
+  });
+}
+
+equil_status equil_lasso_objective(equil_matrix* M, const double* b, double lambda,
+                                   const double* x, double* out) {
+  return guarded([&] {
+    require(M != nullptr && b != nullptr && x != nullptr && out != nullptr,
+            "lasso_objective: null argument");
+    require(lambda > 0.0, "lasso_objective: malformed problem");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    require(M->world == 1, "lasso_objective: single-GPU matrices only in this build");
+    cudaStream_t s = M->stream;
+    DevBuf<double> b_d, x_d, ax, r, v;
+    b_d.alloc(M->m); x_d.alloc(M->n); ax.alloc(M->n); r.alloc(M->m); v.alloc(1);
+    CK(cudaMemcpyAsync(b_d.p, b, M->m * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(x_d.p, x, M->n * 8, cudaMemcpyHostToDevice, s));
+    CK(eqb::launch_abs(x_d.p, M->n, ax.p, s));
+    lasso_value_dev(M, b_d.p, std::sqrt(lambda), x_d.p, ax.p, r.p, v.p);
+    *out = read_scalar(M, v.p);
+  });
+}
+
+equil_status equil_ccp_lasso(equil_matrix* M, const double* b, double lambda,
+                             const equil_ccp_options* o, equil_ccp_out* out) {
+  return guarded([&] { ccp_common(M, b, lambda, nullptr, o, out, "ccp_lasso"); });
+}
+
+equil_status equil_ccp_lasso_preconditioned(equil_matrix* M, const double* b, double lambda,
+                                            const equil_params* p, const equil_ccp_options* o,
+                                            equil_ccp_out* out) {
+  return guarded([&] {
+    require(p != nullptr, "ccp_lasso_preconditioned: null params");
+    ccp_common(M, b, lambda, p, o, out, "ccp_lasso_preconditioned");
+  });
+}
+
+}  // extern "C"

@@ -269,6 +269,17 @@ cudaError_t launch_sgd_update(double* x, double* avg, const double* est, const d
 cudaError_t launch_gather_map(const double* x, const int32_t* map, int64_t len, double* out,
                               cudaStream_t s);
 
+// Chambolle-Pock lasso steps (variants.cu; src/ccp.cpp:73-88), d / e may be null (= 1)
+cudaError_t launch_ccp_dual(double* y, const double* kz, const double* d, const double* b,
+                            double sigma, double sqrt_lambda, int64_t m, double* dy,
+                            cudaStream_t s);
+cudaError_t launch_ccp_primal(double* z, double* ezt, const double* g, const double* e,
+                              double tau, double tau_sl, double theta, int64_t n, double* x,
+                              double* absx, cudaStream_t s);
+cudaError_t launch_lasso_value(const double* r2, const double* l1, double sqrt_lambda,
+                               double* out, cudaStream_t s);
+cudaError_t launch_abs(const double* x, int64_t n, double* out, cudaStream_t s);
+
 // LSQR elementwise helpers
 cudaError_t launch_lsqr_normalize(double* dst, const double* src,
                                   const double* norm_dev, double* scaled_out,

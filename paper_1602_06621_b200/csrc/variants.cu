@@ -1,8 +1,10 @@
 // variants.cu -- kernels of the engine variants sharing the SGD loop
 // (src/variants.cpp): symmetric equilibration (:35-103) and block
-// equilibration (:156-240).  The matrix passes themselves are the generic
-// pass kernels (kPassEst epilogue); these kernels form the scalings and the
-// gathered probes, sum row estimates over blocks and update the block iterates.
+// equilibration (:156-240), and of the second consumer of D, E: the
+// Chambolle-Pock lasso (src/ccp.cpp:27-110).  The matrix passes themselves are
+// the generic pass kernels; these kernels form the scalings and the gathered
+// probes, sum row estimates over blocks, update the block iterates, and run
+// the CCP dual / primal steps.
 #include "internal.h"
 #include "sgd_common.cuh"
 
@@ -64,6 +66,60 @@ __global__ void gather_map_kernel(const double* __restrict__ x, const int32_t* _
   if (i < len) out[i] = x[map[i]];
 }
 
+// dual step (src/ccp.cpp:73-78): y = (y + sigma*(K z~)_i - (sigma*d_i)*b_i) /
+// (1 + ((0.5*sigma*d_i)*d_i)*sqrt(lambda)); dy = d .* y feeds K^T
+__global__ void ccp_dual_kernel(double* __restrict__ y, const double* __restrict__ kz,
+                                const double* __restrict__ d, const double* __restrict__ b,
+                                double sigma, double sqrt_lambda, int64_t m,
+                                double* __restrict__ dy) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  const double di = d ? d[i] : 1.0;
+  const double yh = __dadd_rn(y[i], __dmul_rn(sigma, kz[i]));
+  const double num = __dsub_rn(yh, __dmul_rn(__dmul_rn(sigma, di), b[i]));
+  const double den =
+      __dadd_rn(1.0, __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(0.5, sigma), di), di), sqrt_lambda));
+  const double yn = __ddiv_rn(num, den);
+  y[i] = yn;
+  dy[i] = d ? __dmul_rn(di, yn) : yn;
+}
+
+__device__ __forceinline__ double soft_threshold(double q, double t) {  // src/ccp.cpp:19-23
+  if (q > t) return __dsub_rn(q, t);
+  if (q < -t) return __dadd_rn(q, t);
+  return 0.0;
+}
+
+// primal step (:81-88): z' = soft(z - tau*g, (tau*sqrt(lambda))*e_j),
+// z~ = z' + theta*(z' - z); ez~ = e .* z~ feeds K, x = e .* z', |x| for |x|_1
+__global__ void ccp_primal_kernel(double* __restrict__ z, double* __restrict__ ezt,
+                                  const double* __restrict__ g, const double* __restrict__ e,
+                                  double tau, double tau_sl, double theta, int64_t n,
+                                  double* __restrict__ x, double* __restrict__ absx) {
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  const double ej = e ? e[j] : 1.0;
+  const double zo = z[j];
+  const double zn = soft_threshold(__dsub_rn(zo, __dmul_rn(tau, g[j])), __dmul_rn(tau_sl, ej));
+  const double zt = __dadd_rn(zn, __dmul_rn(theta, __dsub_rn(zn, zo)));
+  z[j] = zn;
+  ezt[j] = e ? __dmul_rn(ej, zt) : zt;
+  const double xj = e ? __dmul_rn(ej, zn) : zn;
+  x[j] = xj;
+  absx[j] = fabs(xj);
+}
+
+// lasso objective from its two reductions (:121-122): r2 / sqrt(l) + sqrt(l) * l1
+__global__ void lasso_value_kernel(const double* r2, const double* l1, double sqrt_lambda,
+                                   double* out) {
+  *out = __dadd_rn(__ddiv_rn(*r2, sqrt_lambda), __dmul_rn(sqrt_lambda, *l1));
+}
+
+__global__ void abs_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (j < n) out[j] = fabs(x[j]);
+}
+
 unsigned grid(int64_t n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
@@ -98,6 +154,38 @@ cudaError_t launch_gather_map(const double* x, const int32_t* map, int64_t len, 
                               cudaStream_t s) {
   if (len == 0) return cudaSuccess;
   gather_map_kernel<<<grid(len), 256, 0, s>>>(x, map, len, out);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ccp_dual(double* y, const double* kz, const double* d, const double* b,
+                            double sigma, double sqrt_lambda, int64_t m, double* dy,
+                            cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  ccp_dual_kernel<<<grid(m), 256, 0, s>>>(y, kz, d, b, sigma, sqrt_lambda, m, dy);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ccp_primal(double* z, double* ezt, const double* g, const double* e,
+                              double tau, double tau_sl, double theta, int64_t n, double* x,
+                              double* absx, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ccp_primal_kernel<<<grid(n), 256, 0, s>>>(z, ezt, g, e, tau, tau_sl, theta, n, x, absx);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lasso_value(const double* r2, const double* l1, double sqrt_lambda,
+                               double* out, cudaStream_t s) {
+  lasso_value_kernel<<<1, 1, 0, s>>>(r2, l1, sqrt_lambda, out);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_abs(const double* x, int64_t n, double* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  abs_kernel<<<grid(n), 256, 0, s>>>(x, n, out);
   count_launch(s);
   return cudaGetLastError();
 }

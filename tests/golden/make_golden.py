@@ -140,6 +140,27 @@ def main():
     g["bl_sgd_hist_obj"], g["bl_sgd_hist_rms"] = s.hist_objective, s.hist_rms
     g["bl_sgd_flags"] = np.array([s.box_feasible, s.iterate_bound_ok, s.apply_count,
                                   s.adjoint_count])
+    # spectral_norm (src/lsqr.cpp:140-163) and the Chambolle-Pock lasso
+    # (src/ccp.cpp): plain, preconditioned, early stop on the gap
+    for key in ["sp", "dn"]:
+        A = cases[key]
+        RM = R.matrix(A)
+        b = g[f"{key}_b"]
+        g[f"{key}_snorm"] = np.array([RM.spectral_norm(100, 1e-9, 0),
+                                      RM.spectral_norm(300, 1e-12, 1)])
+        lam = 0.3
+        xf, ps = RM.lasso_fista(b, lam, 1e-10, 200000)
+        g[f"{key}_pstar"] = np.array([ps])
+        for tag, kw in [("ccp", dict(max_iters=150)),
+                        ("pccp", dict(max_iters=150, params=dict(iterations=30, seed=3))),
+                        ("eccp", dict(max_iters=20000, gap_tol=1e-4))]:
+            r = RM.ccp_lasso(b, lam, p_star=ps, **kw)
+            g[f"{key}_{tag}_x"] = r.x
+            g[f"{key}_{tag}_obj"] = r.objective_history
+            g[f"{key}_{tag}_gap"] = r.gap_history
+            g[f"{key}_{tag}_meta"] = np.array([r.iterations, r.equil_iterations, r.reached_tol,
+                                               r.apply_count, r.adjoint_count])
+            g[f"{key}_{tag}_steps"] = np.array([r.tau, r.sigma, r.theta])
     np.savez_compressed(OUT, **g)
     print(OUT, os.path.getsize(OUT), "bytes")
 

@@ -514,3 +514,69 @@ def test_variants_dense_and_known_answers_vs_oracle(C):
         with pytest.raises(eq.InvalidArgument, match=msg):
             eq.sgd_equilibrate_block(Bm, eq.BlockStructure(np.array(rbx), np.array(cbx), R, Cb),
                                      eq.EquilibrationParams(iterations=3))
+
+
+# ---------------------------------------------------------------- CCP lasso
+@pytest.mark.parametrize("key", ["sp", "dn"])
+def test_ccp_and_spectral_norm_bit_exact_vs_reference_golden(golden, key):
+    """spectral_norm (src/lsqr.cpp:140-163), ccp_lasso and
+    ccp_lasso_preconditioned (src/ccp.cpp:27-141) on the device: plain,
+    preconditioned and gap-stopped runs, every history entry bit-exact."""
+    A = csr_from_golden(golden, key)
+    M = device_matrix(A)
+    b = golden[f"{key}_b"]
+    sn = golden[f"{key}_snorm"]
+    assert eq.spectral_norm(M, 100, 1e-9, 0) == sn[0]
+    assert eq.spectral_norm(M, 300, 1e-12, 1) == sn[1]
+    ps = float(golden[f"{key}_pstar"][0])
+    prob = eq.LassoProblem(M, b, 0.3)
+    for tag, opt, params in [
+            ("ccp", eq.CcpOptions(max_iters=150, p_star=ps), None),
+            ("pccp", eq.CcpOptions(max_iters=150, p_star=ps),
+             eq.EquilibrationParams(iterations=30, seed=3)),
+            ("eccp", eq.CcpOptions(max_iters=20000, p_star=ps, gap_tol=1e-4), None)]:
+        r = eq.ccp_lasso(prob, opt) if params is None else eq.ccp_lasso_preconditioned(
+            prob, params, opt)
+        assert np.array_equal(r.x, golden[f"{key}_{tag}_x"]), tag
+        assert np.array_equal(r.objective_history, golden[f"{key}_{tag}_obj"]), tag
+        assert np.array_equal(r.gap_history, golden[f"{key}_{tag}_gap"]), tag
+        assert [r.iterations, r.equil_iterations, r.reached_tol, r.apply_count,
+                r.adjoint_count] == list(golden[f"{key}_{tag}_meta"]), tag
+        assert [r.tau, r.sigma, r.theta] == list(golden[f"{key}_{tag}_steps"]), tag
+
+
+def test_ccp_known_answers_and_errors(C):
+    """test_itersolvers.cpp:173-227, :273-292 on the device."""
+    assert eq.spectral_norm(eq.ExplicitMatrix.dense(np.diag([3.0, 1.0])), 500,
+                            1e-12) == pytest.approx(3.0, rel=1e-8)
+    eye = eq.ExplicitMatrix.identity(2)
+    prob = eq.LassoProblem(eye, np.array([3.0, 0.0]), 4.0)
+    assert eq.lasso_objective(prob, np.zeros(2)) == pytest.approx(4.5, rel=1e-14)
+    assert eq.lasso_objective(prob, np.array([1.0, 0.0])) == pytest.approx(4.0, rel=1e-14)
+    r = eq.ccp_lasso(prob, eq.CcpOptions(max_iters=5000))
+    assert r.x[0] == pytest.approx(1.0, rel=1e-6) and abs(r.x[1]) <= 1e-8
+    assert len(r.objective_history) == r.iterations + 1 and r.gap_history == []
+    assert r.apply_count == r.adjoint_count == r.iterations
+    rng = np.random.default_rng(91)
+    Ad = rng.standard_normal((10, 14))
+    bb = rng.standard_normal(10)
+    M = eq.ExplicitMatrix.dense(Ad)
+    p2 = eq.LassoProblem(M, bb, 0.05)
+    plain = eq.ccp_lasso(p2, eq.CcpOptions(max_iters=500))
+    pre = eq.ccp_lasso_preconditioned(p2, eq.EquilibrationParams(iterations=0),
+                                      eq.CcpOptions(max_iters=500))
+    want = C.ccp_lasso(oracle.CsrArrays(10, 14, dense=Ad), bb, 0.05, max_iters=500)
+    assert np.array_equal(plain.x, want.x) and np.array_equal(plain.objective_history,
+                                                                want.objective_history)
+    assert pre.equil_iterations == 0 and np.array_equal(pre.x, plain.x)
+    x = rng.standard_normal(14)
+    assert eq.lasso_objective(p2, x) == C.lasso_objective(oracle.CsrArrays(10, 14, dense=Ad),
+                                                          bb, 0.05, x)
+    with pytest.raises(eq.InvalidArgument, match="lambda must be positive"):
+        eq.ccp_lasso(eq.LassoProblem(M, bb, 0.0))
+    with pytest.raises(eq.InvalidArgument, match="rhs must be nonzero"):
+        eq.ccp_lasso(eq.LassoProblem(M, np.zeros(10), 0.1))
+    with pytest.raises(eq.InvalidArgument, match="max_iters must be nonnegative"):
+        eq.ccp_lasso(p2, eq.CcpOptions(max_iters=-1))
+    with pytest.raises(eq.InvalidArgument, match="max_iters must be positive"):
+        eq.spectral_norm(M, 0)

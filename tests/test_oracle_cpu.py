@@ -249,3 +249,53 @@ def test_oracle_variant_known_answers(C):
             C.sgd_equilibrate_block(B, rb, cb, R, Cb, iterations=3)
     one = C.sgd_equilibrate_block(B, [0, 0, 0], [0, 0], 1, 1, iterations=50)
     assert one.u[0] == one.u[1] == one.u[2] and one.v[0] == one.v[1]
+
+
+@pytest.mark.parametrize("key", ["sp", "dn"])
+def test_oracle_ccp_and_spectral_norm_match_reference_golden(C, golden, key):
+    """spectral_norm (src/lsqr.cpp:140-163) and ccp_lasso(_preconditioned)
+    (src/ccp.cpp:27-141) on the oracle vs the reference's own sources."""
+    A = csr_from_golden(golden, key)
+    b = golden[f"{key}_b"]
+    sn = golden[f"{key}_snorm"]
+    assert C.spectral_norm(A, 100, 1e-9, 0) == sn[0]
+    assert C.spectral_norm(A, 300, 1e-12, 1) == sn[1]
+    ps = float(golden[f"{key}_pstar"][0])
+    for tag, kw in [("ccp", dict(max_iters=150)),
+                    ("pccp", dict(max_iters=150, params=dict(iterations=30, seed=3))),
+                    ("eccp", dict(max_iters=20000, gap_tol=1e-4))]:
+        r = C.ccp_lasso(A, b, 0.3, p_star=ps, **kw)
+        assert np.array_equal(r.x, golden[f"{key}_{tag}_x"]), tag
+        assert np.array_equal(r.objective_history, golden[f"{key}_{tag}_obj"]), tag
+        assert np.array_equal(r.gap_history, golden[f"{key}_{tag}_gap"]), tag
+        assert [r.iterations, r.equil_iterations, r.reached_tol, r.apply_count,
+                r.adjoint_count] == list(golden[f"{key}_{tag}_meta"]), tag
+        assert [r.tau, r.sigma, r.theta] == list(golden[f"{key}_{tag}_steps"]), tag
+
+
+def test_oracle_ccp_known_answers(C):
+    """test_itersolvers.cpp:173-227, :273-292 restated on the oracle."""
+    D = oracle.CsrArrays(2, 2, dense=np.diag([3.0, 1.0]))
+    assert C.spectral_norm(D, 500, 1e-12) == pytest.approx(3.0, rel=1e-8)
+    eye = oracle.CsrArrays(2, 2, np.arange(3), np.arange(2), np.ones(2))
+    b = np.array([3.0, 0.0])
+    assert C.lasso_objective(eye, b, 4.0, np.zeros(2)) == pytest.approx(4.5, rel=1e-14)
+    assert C.lasso_objective(eye, b, 4.0, np.array([1.0, 0.0])) == pytest.approx(4.0, rel=1e-14)
+    r = C.ccp_lasso(eye, b, 4.0, max_iters=5000)
+    assert r.x[0] == pytest.approx(1.0, rel=1e-6) and abs(r.x[1]) <= 1e-8
+    assert len(r.objective_history) == r.iterations + 1
+    assert r.apply_count == r.adjoint_count == r.iterations
+    assert r.tau * r.sigma <= 0.81 + 1e-12
+    rng = np.random.default_rng(91)
+    A = oracle.CsrArrays(10, 14, dense=rng.standard_normal((10, 14)))
+    bb = rng.standard_normal(10)
+    plain = C.ccp_lasso(A, bb, 0.05, max_iters=500)
+    pre = C.ccp_lasso(A, bb, 0.05, max_iters=500, params=dict(iterations=0))
+    assert pre.equil_iterations == 0 and np.array_equal(pre.x, plain.x)
+    assert np.array_equal(pre.objective_history, plain.objective_history)
+    with pytest.raises(oracle.OracleError, match="lambda must be positive"):
+        C.ccp_lasso(A, bb, 0.0, max_iters=5)
+    with pytest.raises(oracle.OracleError, match="rhs must be nonzero"):
+        C.ccp_lasso(A, np.zeros(10), 0.1, max_iters=5)
+    with pytest.raises(oracle.OracleError, match="max_iters must be nonnegative"):
+        C.ccp_lasso(A, bb, 0.1, max_iters=-1)
