@@ -136,6 +136,37 @@ equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowma
 void equil_matrix_destroy(equil_matrix* A);
 equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
                                 int64_t* nnz);
+/* read_matrix_market_file (include/equil/matrix_market.hpp:17-18,
+ * src/matrix_market.cpp:63-204): real general coordinate or array files;
+ * parse errors are EQUIL_ERUNTIME with the reference's message
+ * "matrix market: line N: ...". */
+equil_status equil_matrix_read_matrix_market(const char* path, const equil_device_cfg* cfg,
+                                             equil_matrix** out);
+/* write_matrix_market_file (include/equil/matrix_market.hpp:20-21,
+ * src/matrix_market.cpp:209-243): "%.17g", byte-identical to the reference. */
+equil_status equil_matrix_write_matrix_market(equil_matrix* A, const char* path);
+/* Binary CSR ("EQBCSR01": int64 m, n, nnz, dense flag; row_ptr int64, col int32,
+ * val f64 -- or m*n f64 row-major): fast reload path, no reference equivalent. */
+equil_status equil_matrix_save_binary(equil_matrix* A, const char* path);
+equil_status equil_matrix_load_binary(const char* path, const equil_device_cfg* cfg,
+                                      equil_matrix** out);
+/* CSR(A) (sparse) or row-major A (dense) back on the host; single GPU. */
+equil_status equil_matrix_export_csr(equil_matrix* A, int64_t* row_ptr, int32_t* col,
+                                     double* val);
+equil_status equil_matrix_export_dense(equil_matrix* A, double* rowmajor);
+int equil_matrix_is_dense(const equil_matrix* A);
+/* Host-only Matrix Market access (no GPU needed): parse a file into an
+ * opaque handle (entries 0-based in file order, with their line numbers; or a
+ * dense row-major array), fetch, free; write a host CSR / dense array. */
+equil_status equil_mm_parse(const char* path, int64_t* m, int64_t* n, int64_t* nnz, int* dense,
+                            void** handle);
+equil_status equil_mm_fetch(void* handle, int64_t* rows, int64_t* cols, double* vals,
+                            int64_t* lines);
+void equil_mm_free(void* handle);
+equil_status equil_mm_write_csr(const char* path, int64_t m, int64_t n, const int64_t* row_ptr,
+                                const int32_t* col, const double* val);
+equil_status equil_mm_write_dense(const char* path, int64_t m, int64_t n,
+                                  const double* rowmajor);
 /* The cudaStream_t all work on this handle is issued on (for event timing). */
 void* equil_matrix_stream(equil_matrix* A);
 /* Device time (CUDA events on the handle's stream) of the T-iteration loop of

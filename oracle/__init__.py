@@ -499,6 +499,10 @@ class _RefOracle:
                                     C.POINTER(C.c_void_p)]
         L.er_matrix_dense.argtypes = [C.c_int64, C.c_int64, _dp, C.POINTER(C.c_void_p)]
         L.er_matrix_free.argtypes = [C.c_void_p]
+        L.er_mm_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), _i64p, _i64p,
+                                 C.POINTER(C.c_int)]
+        L.er_mm_write.argtypes = [C.c_void_p, C.c_char_p]
+        L.er_matrix_to_dense.argtypes = [C.c_void_p, _dp]
         L.er_matrix_nnz.argtypes = [C.c_void_p]
         L.er_matrix_nnz.restype = C.c_int64
         L.er_matrix_export.argtypes = [C.c_void_p, _i64p, _i32p, _dp]
@@ -557,6 +561,15 @@ class _RefOracle:
             self._err(rc)
         return RefMatrix(self, h, A.m, A.n)
 
+    def read_matrix_market(self, path):
+        """(RefMatrix, is_sparse) from the reference's read_matrix_market_file."""
+        h, m, n, sp = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int()
+        rc = self.L.er_mm_read(str(path).encode(), C.byref(h), C.byref(m), C.byref(n),
+                               C.byref(sp))
+        if rc:
+            self._err(rc)
+        return RefMatrix(self, h, m.value, n.value), bool(sp.value)
+
     def matrix_coo(self, m, n, rows, cols, vals):
         rows = np.ascontiguousarray(rows, np.int64)
         cols = np.ascontiguousarray(cols, np.int64)
@@ -572,6 +585,18 @@ class _RefOracle:
 class RefMatrix:
     def __init__(self, R: _RefOracle, h, m, n):
         self.R, self.h, self.m, self.n = R, h, m, n
+
+    def write_matrix_market(self, path):
+        rc = self.R.L.er_mm_write(self.h, str(path).encode())
+        if rc:
+            self.R._err(rc)
+
+    def to_dense(self):
+        out = np.zeros((self.m, self.n))
+        rc = self.R.L.er_matrix_to_dense(self.h, ptr(out, _dp))
+        if rc:
+            self.R._err(rc)
+        return out
 
     def __del__(self):
         try:

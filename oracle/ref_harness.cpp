@@ -14,6 +14,7 @@
 #include "equil/equilibrate.hpp"
 #include "equil/explicit_matrix.hpp"
 #include "equil/lsqr.hpp"
+#include "equil/matrix_market.hpp"
 #include "equil/metrics.hpp"
 #include "equil/rng.hpp"
 #include "equil/variants.hpp"
@@ -377,6 +378,31 @@ int er_lasso_fista(void* h, const double* b, double lambda, double grad_map_tol,
     const FistaResult r = lasso_fista(prob, grad_map_tol, max_iters);
     from_vec(r.x, x);
     *p_star = r.p_star;
+  });
+}
+
+// ---- read_matrix_market_file / write_matrix_market_file (matrix_market.hpp)
+int er_mm_read(const char* path, void** out, int64_t* m, int64_t* n, int* is_sparse) {
+  return guarded([&] {
+    auto* A = new ExplicitMatrix(read_matrix_market_file(path));
+    *out = A;
+    *m = A->rows();
+    *n = A->cols();
+    *is_sparse = A->is_sparse() ? 1 : 0;
+  });
+}
+
+int er_mm_write(void* h, const char* path) {
+  return guarded([&] { write_matrix_market_file(path, *static_cast<ExplicitMatrix*>(h)); });
+}
+
+// dense values (row-major) of any ExplicitMatrix
+int er_matrix_to_dense(void* h, double* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    const Mat d = A.to_dense();
+    for (Index i = 0; i < A.rows(); ++i)
+      for (Index j = 0; j < A.cols(); ++j) out[i * A.cols() + j] = d(i, j);
   });
 }
 

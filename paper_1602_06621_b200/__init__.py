@@ -6,7 +6,8 @@ reference's interface over that ABI.  See DESIGN.md.
 """
 from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   BlockStructure, CcpOptions, CcpRun, DiagnosticsConfig,
-                  EquilibrationParams, EquilRuntimeError,
+                  EquilibrationParams, EquilRuntimeError, MatrixMarketData,
+                  parse_matrix_market, write_matrix_market_csr, write_matrix_market_dense,
                   ExplicitMatrix, InvalidArgument, IterationRecord, LassoProblem, LsqrRun,
                   ScalingResult, canon_sumsq_device, ccp_lasso, ccp_lasso_preconditioned,
                   lasso_objective, spectral_norm, det_exp_device, kernel_launches,
@@ -18,7 +19,8 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
 __all__ = [
     "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "BlockStructure",
     "CcpOptions", "CcpRun", "LassoProblem", "ccp_lasso", "ccp_lasso_preconditioned",
-    "lasso_objective", "spectral_norm",
+    "lasso_objective", "spectral_norm", "MatrixMarketData", "parse_matrix_market",
+    "write_matrix_market_csr", "write_matrix_market_dense",
     "DiagnosticsConfig",
     "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",
     "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",

@@ -101,6 +101,21 @@ SIGNATURES = {
                                                  C.POINTER(CcpOut)]),
     "equil_spectral_norm": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, _dp]),
     "equil_lasso_objective": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp]),
+    "equil_matrix_read_matrix_market": (C.c_int, [C.c_char_p, C.POINTER(DeviceCfg),
+                                                  C.POINTER(C.c_void_p)]),
+    "equil_matrix_write_matrix_market": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "equil_matrix_save_binary": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "equil_matrix_load_binary": (C.c_int, [C.c_char_p, C.POINTER(DeviceCfg),
+                                           C.POINTER(C.c_void_p)]),
+    "equil_matrix_export_csr": (C.c_int, [C.c_void_p, _i64p, _i32p, _dp]),
+    "equil_matrix_export_dense": (C.c_int, [C.c_void_p, _dp]),
+    "equil_matrix_is_dense": (C.c_int, [C.c_void_p]),
+    "equil_mm_parse": (C.c_int, [C.c_char_p, _i64p, _i64p, _i64p, C.POINTER(C.c_int),
+                                 C.POINTER(C.c_void_p)]),
+    "equil_mm_fetch": (C.c_int, [C.c_void_p, _i64p, _i64p, _dp, _i64p]),
+    "equil_mm_free": (None, [C.c_void_p]),
+    "equil_mm_write_csr": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _i64p, _i32p, _dp]),
+    "equil_mm_write_dense": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _dp]),
     "equil_lsqr": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(LsqrOut)]),
     "equil_lsqr_preconditioned": (C.c_int, [C.c_void_p, _dp, C.POINTER(Params), C.c_int,
                                             C.c_double, C.POINTER(LsqrOut)]),

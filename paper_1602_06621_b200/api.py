@@ -185,6 +185,56 @@ class ExplicitMatrix:
             raise InvalidArgument("ExplicitMatrix::identity: n must be positive")
         return ExplicitMatrix.from_csr(n, n, np.arange(n + 1), np.arange(n), np.ones(n), device)
 
+    @staticmethod
+    def _from_handle(h):
+        m, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.load().equil_matrix_shape(h, C.byref(m), C.byref(n), C.byref(nnz)))
+        return ExplicitMatrix(h, m.value, n.value, nnz.value,
+                              bool(L.load().equil_matrix_is_dense(h)))
+
+    @staticmethod
+    def read_matrix_market(path: str, device: int = 0):
+        """read_matrix_market_file (include/equil/matrix_market.hpp:17-18):
+        parsed on host threads, sorted / validated / converted on the device."""
+        cfg = L.DeviceCfg(device, 0, 1, None)
+        h = C.c_void_p()
+        _check(L.load().equil_matrix_read_matrix_market(str(path).encode(), C.byref(cfg),
+                                                        C.byref(h)))
+        return ExplicitMatrix._from_handle(h)
+
+    def write_matrix_market(self, path: str):
+        """write_matrix_market_file (include/equil/matrix_market.hpp:20-21)."""
+        _check(L.load().equil_matrix_write_matrix_market(self._h, str(path).encode()))
+
+    @staticmethod
+    def load_binary(path: str, device: int = 0):
+        """Binary CSR / dense file written by save_binary (fast reload)."""
+        cfg = L.DeviceCfg(device, 0, 1, None)
+        h = C.c_void_p()
+        _check(L.load().equil_matrix_load_binary(str(path).encode(), C.byref(cfg), C.byref(h)))
+        return ExplicitMatrix._from_handle(h)
+
+    def save_binary(self, path: str):
+        _check(L.load().equil_matrix_save_binary(self._h, str(path).encode()))
+
+    def is_sparse(self) -> bool:
+        return not self._dense
+
+    def to_csr(self):
+        """(row_ptr, col, val) of A as stored on the device."""
+        rp = np.zeros(self._m + 1, np.int64)
+        ci = np.zeros(max(self._nnz, 1), np.int32)
+        va = np.zeros(max(self._nnz, 1), np.float64)
+        _check(L.load().equil_matrix_export_csr(self._h, L.ptr(rp, L._i64p), L.ptr(ci, L._i32p),
+                                                L.ptr(va, L._dp)))
+        return rp, ci[: self._nnz], va[: self._nnz]
+
+    def to_dense(self):
+        """Row-major values of a dense matrix."""
+        a = np.zeros((self._m, self._n))
+        _check(L.load().equil_matrix_export_dense(self._h, L.ptr(a, L._dp)))
+        return a
+
     def close(self):
         if self._h is not None and self._h.value:
             L.load().equil_matrix_destroy(self._h)
@@ -440,6 +490,58 @@ def lasso_objective(prob: LassoProblem, x) -> float:
     _check(L.load().equil_lasso_objective(prob.op._h, L.ptr(b, L._dp), float(prob.lam),
                                           L.ptr(x, L._dp), C.byref(out)))
     return out.value
+
+
+@dataclass
+class MatrixMarketData:
+    """A parsed Matrix Market file on the host (no device involved)."""
+    m: int
+    n: int
+    dense: bool
+    rows: np.ndarray   # 0-based, file order (coordinate)
+    cols: np.ndarray
+    vals: np.ndarray   # coordinate values, or row-major m x n (array)
+    lines: np.ndarray  # line number of every coordinate entry
+
+
+def parse_matrix_market(path: str) -> MatrixMarketData:
+    """The host half of read_matrix_market (src/matrix_market.cpp:63-198):
+    header / size / entry rules and their line-numbered errors.  Duplicate
+    detection happens with the device sort in ExplicitMatrix.read_matrix_market."""
+    lib = L.load()
+    m, n, nnz, dn = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+    h = C.c_void_p()
+    _check(lib.equil_mm_parse(str(path).encode(), C.byref(m), C.byref(n), C.byref(nnz),
+                              C.byref(dn), C.byref(h)))
+    try:
+        if dn.value:
+            v = np.zeros((m.value, n.value))
+            _check(lib.equil_mm_fetch(h, None, None, L.ptr(v, L._dp), None))
+            z = np.zeros(0, np.int64)
+            return MatrixMarketData(m.value, n.value, True, z, z, v, z)
+        k = nnz.value
+        r, c, ln = (np.zeros(max(k, 1), np.int64) for _ in range(3))
+        v = np.zeros(max(k, 1))
+        _check(lib.equil_mm_fetch(h, L.ptr(r, L._i64p), L.ptr(c, L._i64p), L.ptr(v, L._dp),
+                                  L.ptr(ln, L._i64p)))
+        return MatrixMarketData(m.value, n.value, False, r[:k], c[:k], v[:k], ln[:k])
+    finally:
+        lib.equil_mm_free(h)
+
+
+def write_matrix_market_csr(path: str, m: int, n: int, row_ptr, col, val):
+    """write_matrix_market (src/matrix_market.cpp:209-233) of a host CSR."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col, dtype=np.int32)
+    va = np.ascontiguousarray(val, dtype=np.float64)
+    _check(L.load().equil_mm_write_csr(str(path).encode(), m, n, L.ptr(rp, L._i64p),
+                                       L.ptr(ci, L._i32p), L.ptr(va, L._dp)))
+
+
+def write_matrix_market_dense(path: str, values):
+    a = np.ascontiguousarray(values, dtype=np.float64)
+    _check(L.load().equil_mm_write_dense(str(path).encode(), a.shape[0], a.shape[1],
+                                         L.ptr(a, L._dp)))
 
 
 def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,

@@ -23,6 +23,7 @@
 
 #include "../../include/equil_b200.h"
 #include "internal.h"
+#include "mmio.h"
 #include "mt64_host.h"
 
 // ---------------------------------------------------------------------------
@@ -836,10 +837,16 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
   });
 }
 
-equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
-                                     const int64_t* cols, const double* vals,
-                                     const equil_device_cfg* cfg, equil_matrix** out) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace {
+// ExplicitMatrix::sparse on the device.  With `lines` (Matrix Market ingest)
+// a duplicate is reported the way read_matrix_market does
+// (src/matrix_market.cpp:142-158): at the line of the later occurrence.
+void create_coo_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                     const int64_t* cols, const double* vals, const int64_t* lines,
+                     const equil_device_cfg* cfg, equil_matrix** out) {
+  {
     require(out != nullptr, "ExplicitMatrix::sparse: null output handle");
     *out = nullptr;
     require(m > 0 && n > 0, "ExplicitMatrix::sparse: dimensions must be positive");
@@ -875,6 +882,17 @@ equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz, const in
     if (kind == 1)  // explicit_matrix.cpp:23-27
       fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry (" + std::to_string(rows[bad]) + ", " +
                              std::to_string(cols[bad]) + ") out of range");
+    if (kind == 2 && lines) {  // matrix_market.cpp:142-158
+      const int64_t r = static_cast<int64_t>(bad / static_cast<uint64_t>(n));
+      const int64_t c = static_cast<int64_t>(bad % static_cast<uint64_t>(n));
+      int seen = 0;
+      int64_t line = 0;
+      for (int64_t k = 0; k < nnz && seen < 2; ++k)
+        if (rows[k] == r && cols[k] == c && ++seen == 2) line = lines[k];
+      throw std::runtime_error("matrix market: line " + std::to_string(line) +
+                               ": duplicate entry (" + std::to_string(r + 1) + ", " +
+                               std::to_string(c + 1) + ")");
+    }
     if (kind == 2)  // explicit_matrix.cpp:33-38
       fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry (" +
                              std::to_string(bad / static_cast<uint64_t>(n)) + ", " +
@@ -888,7 +906,16 @@ equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz, const in
     pt.mark(s, "coo->csr");
     finish_sparse(M.get(), rp, ci, va, rph.data(), pt, nullptr, nullptr);
     *out = M.release();
-  });
+  }
+}
+}  // namespace
+
+extern "C" {
+
+equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                                     const int64_t* cols, const double* vals,
+                                     const equil_device_cfg* cfg, equil_matrix** out) {
+  return guarded([&] { create_coo_impl(m, n, nnz, rows, cols, vals, nullptr, cfg, out); });
 }
 
 equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowmajor,
@@ -2346,6 +2373,228 @@ equil_status equil_ccp_lasso_preconditioned(equil_matrix* M, const double* b, do
   return guarded([&] {
     require(p != nullptr, "ccp_lasso_preconditioned: null params");
     ccp_common(M, b, lambda, p, o, out, "ccp_lasso_preconditioned");
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Matrix store ingest: Matrix Market files
+// (src/matrix_market.cpp) parsed on host threads, sorted / checked / converted
+// to CSR on the device; a binary CSR file for fast reloads; host export.
+// ---------------------------------------------------------------------------
+namespace {
+
+// the local CSR(A) (world 1) or dense A on the host
+void export_host(equil_matrix* M, std::vector<int64_t>& rp, std::vector<int32_t>& ci,
+                 std::vector<double>& va, std::vector<double>& dense) {
+  require(M->world == 1, "export: single-GPU matrices only");
+  cudaStream_t s = M->stream;
+  if (M->dense) {
+    dense.resize(static_cast<size_t>(M->m * M->n));
+    CK(cudaMemcpyAsync(dense.data(), M->Ad.p, M->m * M->n * 8, cudaMemcpyDeviceToHost, s));
+  } else {
+    rp.resize(M->m + 1);
+    ci.resize(static_cast<size_t>(M->nnz));
+    va.resize(static_cast<size_t>(M->nnz));
+    CK(cudaMemcpyAsync(rp.data(), M->A.row_ptr, (M->m + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (M->nnz) {
+      CK(cudaMemcpyAsync(ci.data(), M->A.col, M->nnz * 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(va.data(), M->A.val, M->nnz * 8, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+equil_status equil_matrix_read_matrix_market(const char* path, const equil_device_cfg* cfg,
+                                             equil_matrix** out) {
+  return guarded([&] {
+    require(path != nullptr && out != nullptr, "matrix market: null argument");
+    *out = nullptr;
+    std::string buf;
+    eqb::mm::read_file(path, buf);
+    eqb::mm::Matrix mm;
+    eqb::mm::parse(buf.data(), buf.size(), mm);
+    buf.clear();
+    buf.shrink_to_fit();
+    if (mm.dense) {
+      const equil_status rc =
+          equil_matrix_create_dense(mm.m, mm.n, mm.dense_rowmajor.data(), cfg, out);
+      if (rc != EQUIL_OK) fail(rc, g_err);
+      return;
+    }
+    create_coo_impl(mm.m, mm.n, mm.nnz, mm.row.data(), mm.col.data(), mm.val.data(),
+                    mm.line.data(), cfg, out);
+  });
+}
+
+equil_status equil_matrix_write_matrix_market(equil_matrix* M, const char* path) {
+  return guarded([&] {
+    require(M != nullptr && path != nullptr, "matrix market: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> va, dense;
+    export_host(M, rp, ci, va, dense);
+    if (M->dense)
+      eqb::mm::write_array(path, M->m, M->n, dense.data());
+    else
+      eqb::mm::write_coordinate(path, M->m, M->n, rp.data(), ci.data(), va.data());
+  });
+}
+
+equil_status equil_matrix_save_binary(equil_matrix* M, const char* path) {
+  return guarded([&] {
+    require(M != nullptr && path != nullptr, "binary csr: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> va, dense;
+    export_host(M, rp, ci, va, dense);
+    eqb::mm::write_binary(path, M->m, M->n, M->dense, rp.data(), ci.data(), va.data(),
+                          dense.data());
+  });
+}
+
+equil_status equil_matrix_load_binary(const char* path, const equil_device_cfg* cfg,
+                                      equil_matrix** out) {
+  return guarded([&] {
+    require(path != nullptr && out != nullptr, "binary csr: null argument");
+    *out = nullptr;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw std::runtime_error(std::string("binary csr: cannot open '") + path + "'");
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    int64_t hdr[4];
+    eqb::mm::read_binary_header(f, path, hdr);
+    const int64_t m = hdr[0], n = hdr[1], nnz = hdr[2];
+    // read straight into pinned host buffers (fast H2D in the create call)
+    auto pinned = [](size_t bytes) {
+      void* p = nullptr;
+      CK(cudaMallocHost(&p, std::max<size_t>(bytes, 8)));
+      return p;
+    };
+    struct Pinned {
+      void* p;
+      ~Pinned() { if (p) cudaFreeHost(p); }
+    };
+    equil_status rc;
+    if (hdr[3]) {
+      Pinned a{pinned(static_cast<size_t>(nnz) * 8)};
+      eqb::mm::read_exact(f, a.p, 8, static_cast<size_t>(nnz), path);
+      rc = equil_matrix_create_dense(m, n, static_cast<const double*>(a.p), cfg, out);
+    } else {
+      Pinned rp{pinned(static_cast<size_t>(m + 1) * 8)};
+      Pinned ci{pinned(static_cast<size_t>(nnz) * 4)};
+      Pinned va{pinned(static_cast<size_t>(nnz) * 8)};
+      eqb::mm::read_exact(f, rp.p, 8, static_cast<size_t>(m + 1), path);
+      eqb::mm::read_exact(f, ci.p, 4, static_cast<size_t>(nnz), path);
+      eqb::mm::read_exact(f, va.p, 8, static_cast<size_t>(nnz), path);
+      rc = equil_matrix_create_csr(m, n, static_cast<const int64_t*>(rp.p),
+                                   static_cast<const int32_t*>(ci.p),
+                                   static_cast<const double*>(va.p), cfg, out);
+    }
+    if (rc != EQUIL_OK) fail(rc, g_err);
+  });
+}
+
+equil_status equil_matrix_export_csr(equil_matrix* M, int64_t* row_ptr, int32_t* col,
+                                     double* val) {
+  return guarded([&] {
+    require(M != nullptr && row_ptr != nullptr, "export_csr: null argument");
+    require(!M->dense, "export_csr: dense matrix");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> va, dense;
+    export_host(M, rp, ci, va, dense);
+    std::memcpy(row_ptr, rp.data(), rp.size() * 8);
+    if (M->nnz) {
+      std::memcpy(col, ci.data(), ci.size() * 4);
+      std::memcpy(val, va.data(), va.size() * 8);
+    }
+  });
+}
+
+equil_status equil_matrix_export_dense(equil_matrix* M, double* rowmajor) {
+  return guarded([&] {
+    require(M != nullptr && rowmajor != nullptr, "export_dense: null argument");
+    require(M->dense, "export_dense: sparse matrix");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> va, dense;
+    export_host(M, rp, ci, va, dense);
+    std::memcpy(rowmajor, dense.data(), dense.size() * 8);
+  });
+}
+
+int equil_matrix_is_dense(const equil_matrix* M) { return M && M->dense ? 1 : 0; }
+
+}  // extern "C"
+
+// Host-only Matrix Market access (no device needed): parse into a handle,
+// fetch the entries, write a host CSR / dense array.
+extern "C" {
+
+equil_status equil_mm_parse(const char* path, int64_t* m, int64_t* n, int64_t* nnz, int* dense,
+                            void** handle) {
+  return guarded([&] {
+    require(path && m && n && nnz && dense && handle, "matrix market: null argument");
+    *handle = nullptr;
+    std::string buf;
+    eqb::mm::read_file(path, buf);
+    auto mm = std::make_unique<eqb::mm::Matrix>();
+    eqb::mm::parse(buf.data(), buf.size(), *mm);
+    *m = mm->m;
+    *n = mm->n;
+    *nnz = mm->nnz;
+    *dense = mm->dense ? 1 : 0;
+    *handle = mm.release();
+  });
+}
+
+equil_status equil_mm_fetch(void* handle, int64_t* rows, int64_t* cols, double* vals,
+                            int64_t* lines) {
+  return guarded([&] {
+    require(handle != nullptr, "matrix market: null handle");
+    const auto* mm = static_cast<const eqb::mm::Matrix*>(handle);
+    if (mm->dense) {
+      if (vals) std::memcpy(vals, mm->dense_rowmajor.data(), mm->dense_rowmajor.size() * 8);
+      return;
+    }
+    if (rows) std::memcpy(rows, mm->row.data(), mm->row.size() * 8);
+    if (cols) std::memcpy(cols, mm->col.data(), mm->col.size() * 8);
+    if (vals) std::memcpy(vals, mm->val.data(), mm->val.size() * 8);
+    if (lines) std::memcpy(lines, mm->line.data(), mm->line.size() * 8);
+  });
+}
+
+void equil_mm_free(void* handle) { delete static_cast<eqb::mm::Matrix*>(handle); }
+
+equil_status equil_mm_write_csr(const char* path, int64_t m, int64_t n, const int64_t* row_ptr,
+                                const int32_t* col, const double* val) {
+  return guarded([&] {
+    require(path && row_ptr && m > 0 && n > 0, "matrix market: null argument");
+    eqb::mm::write_coordinate(path, m, n, row_ptr, col, val);
+  });
+}
+
+equil_status equil_mm_write_dense(const char* path, int64_t m, int64_t n,
+                                  const double* rowmajor) {
+  return guarded([&] {
+    require(path && rowmajor && m > 0 && n > 0, "matrix market: null argument");
+    eqb::mm::write_array(path, m, n, rowmajor);
   });
 }
 

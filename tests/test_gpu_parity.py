@@ -580,3 +580,49 @@ def test_ccp_known_answers_and_errors(C):
         eq.ccp_lasso(p2, eq.CcpOptions(max_iters=-1))
     with pytest.raises(eq.InvalidArgument, match="max_iters must be positive"):
         eq.spectral_norm(M, 0)
+
+
+# ---------------------------------------------------------------- matrix store
+def test_matrix_market_and_binary_ingest_on_device(C, golden, tmp_path):
+    """read_matrix_market_file (src/matrix_market.cpp:63-204) through the
+    device COO ingest: same matrix as the reference construction (CSR and
+    CSR(A^T)), duplicates reported at the later line (:142-158), writer bytes
+    equal to what the host writer produces, binary CSR round trip."""
+    A = csr_from_golden(golden, "lr")
+    rows = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    perm = np.random.default_rng(0).permutation(A.nnz)  # any entry order
+    lines = ["%%MatrixMarket matrix coordinate real general\n", "% shuffled\n",
+             f"{A.m} {A.n} {A.nnz}\n"]
+    lines += [f"{rows[k] + 1} {A.col[k] + 1} {float(A.val[k])!r}\n" for k in perm]
+    p = tmp_path / "lr.mtx"
+    p.write_text("".join(lines))
+    M = eq.ExplicitMatrix.read_matrix_market(str(p))
+    rp, ci, va = M.to_csr()
+    assert np.array_equal(rp, A.row_ptr) and np.array_equal(ci, A.col)
+    assert np.array_equal(va, A.val)
+    trp, tci, tva = M.transposed_csr()
+    assert np.array_equal(trp, golden["lr_t_rp"]) and np.array_equal(tva, golden["lr_t_val"])
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=40, seed=5))
+    assert np.array_equal(r.u, golden["lr_sgd_u"])
+    # writer from the device copy == host writer == reference bytes (CPU test)
+    w1, w2 = tmp_path / "w1.mtx", tmp_path / "w2.mtx"
+    M.write_matrix_market(str(w1))
+    eq.write_matrix_market_csr(str(w2), A.m, A.n, A.row_ptr, A.col, A.val)
+    assert w1.read_bytes() == w2.read_bytes()
+    # binary CSR round trip
+    b = tmp_path / "lr.eqb"
+    M.save_binary(str(b))
+    M2 = eq.ExplicitMatrix.load_binary(str(b))
+    assert all(np.array_equal(x, y) for x, y in zip(M2.to_csr(), (A.row_ptr, A.col, A.val)))
+    D = golden["dn_dense"]
+    Md = eq.ExplicitMatrix.dense(D)
+    Md.save_binary(str(b))
+    assert np.array_equal(eq.ExplicitMatrix.load_binary(str(b)).to_dense(), D)
+    Md.write_matrix_market(str(w1))
+    assert np.array_equal(eq.ExplicitMatrix.read_matrix_market(str(w1)).to_dense(), D)
+    # duplicates: the first duplicated (row, col) in sorted order, at its later line
+    dup = ["%%MatrixMarket matrix coordinate real general\n", "3 3 5\n", "3 3 1.0\n",
+           "1 2 1.0\n", "2 2 1.0\n", "% c\n", "1 2 5.0\n", "3 3 2.0\n"]
+    p.write_text("".join(dup))
+    with pytest.raises(eq.EquilRuntimeError, match=r"line 7: duplicate entry \(1, 2\)"):
+        eq.ExplicitMatrix.read_matrix_market(str(p))
