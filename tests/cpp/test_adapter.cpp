@@ -93,6 +93,35 @@ int main() {
     }
     CHECK(threw);
   }
+  {  // variants (test_variants.cpp:36-48, :165-176): symmetric identity fixed
+     // point; singleton blocks reproduce the plain solver exactly
+    EquilibrationParams p;
+    p.alpha = p.beta = 1.0;
+    p.iterations = 100;
+    const ScalingResult s = sgd_equilibrate_symmetric(identity(4), p);
+    for (double x : s.u) CHECK(x == 0.0);
+    CHECK(s.u == s.v && s.d == s.e && s.apply_count == 100 && s.adjoint_count == 0);
+    std::vector<double> a(5 * 7);
+    for (size_t k = 0; k < a.size(); ++k) a[k] = std::cos(0.3 + 0.71 * k) * (1 + k % 3);
+    const DeviceMatrix A = DeviceMatrix::dense_rowmajor(5, 7, a);
+    EquilibrationParams q;
+    q.iterations = 300;
+    q.seed = 11;
+    const ScalingResult plain = sgd_equilibrate(A, q);
+    const ScalingResult blk = sgd_equilibrate_block(A, BlockStructure::trivial(5, 7), q);
+    CHECK(plain.u == blk.u && plain.v == blk.v);
+  }
+  {  // ccp on the identity reaches the soft-threshold solution
+     // (test_itersolvers.cpp:205-225); spectral norm of diag(3, 1)
+    CcpOptions opt;
+    opt.max_iters = 5000;
+    const CcpRun run = ccp_lasso(identity(2), Vec{3.0, 0.0}, 4.0, opt);
+    CHECK(std::abs(run.x[0] - 1.0) <= 1e-6 && std::abs(run.x[1]) <= 1e-8);
+    CHECK(static_cast<int>(run.objective_history.size()) == run.iterations + 1);
+    CHECK(run.apply_count == run.iterations && run.adjoint_count == run.iterations);
+    const DeviceMatrix D = DeviceMatrix::dense_rowmajor(2, 2, {3.0, 0.0, 0.0, 1.0});
+    CHECK(std::abs(spectral_norm(D, 500, 1e-12) - 3.0) <= 3e-8);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
