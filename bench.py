@@ -244,6 +244,7 @@ def run_ours(args):
         d2h = int(8 * 2 * (inst.m + inst.n))
         e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "s_per_step": e2e_s,
+               "samples_s": [round(t, 4) for t in ts],
                "path": "equil_sgd_equilibrate_csr (upload, device transpose, T iterations, "
                        "download)"}
         del r
