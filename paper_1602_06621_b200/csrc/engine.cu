@@ -349,6 +349,12 @@ struct equil_matrix {
   // EQUIL_PANEL=1 at creation; n_pbands == 0 selects the row-slice traversal
   // above (the default: faster on B200)
   bool use_panels = false;
+  // hot-first slot layout of the gathered vectors (build_slot_layout): the SGD
+  // passes read CSR copies whose column indices point at slots, and the
+  // epilogues write each row's next value at its slot
+  bool use_slots = true;
+  bool slots = false;
+  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wslot, sslot;
   DevBuf<double> pval[2];
   DevBuf<uint16_t> pcol[2];
   DevBuf<uint32_t> pruns[2];
@@ -417,6 +423,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   M->rank = cfg ? cfg->rank : 0;
   M->world = cfg ? std::max(1, cfg->world_size) : 1;
   if (const char* e = getenv("EQUIL_PANEL")) M->use_panels = atoi(e) != 0;  // A/B knob
+  if (const char* e = getenv("EQUIL_SLOTS")) M->use_slots = atoi(e) != 0;
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -539,6 +546,67 @@ void build_panel_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT)
   M->n_pbands = static_cast<int>(h.size());
 }
 
+// Hot-first slot layout.  In the A^T pass every entry of A's row i gathers
+// xw[i], so row i is read len(row i) times per iteration; with Zipf row lengths
+// a few thousand rows take most gathers (c3: the 20k longest rows, 156 KB, take
+// 57%).  Scattered over the 16 MB vector, each of them pins its own 128-byte L1
+// line; packed together they fit in L1.  Rows are ordered by decreasing
+// floor(log2(length)) (stable), per rank inside its own padded range, and the
+// same is done for the columns feeding xs.  Only memory placement changes:
+// every row sum keeps its entries and their order.
+void build_slot_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT) {
+  M->slots = false;
+  if (!M->use_slots || M->use_panels) return;
+  cudaStream_t s = M->stream;
+  // slot of every row of a matrix with global row_ptr rp partitioned by bounds
+  auto slots_of = [&](const int64_t* rp, int64_t rows, const std::vector<int64_t>& bounds,
+                      int64_t maxcnt, std::vector<int32_t>& map_pad, int64_t pad_len) {
+    map_pad.assign(static_cast<size_t>(pad_len), 0);
+    const int G = static_cast<int>(bounds.size()) - 1;
+    for (int g = 0; g < G; ++g) {
+      const int64_t b0 = bounds[g], b1 = bounds[g + 1];
+      const int64_t base = M->world == 1 ? 0 : g * maxcnt;
+      // key 0: longest rows (floor(log2(len)) = 63) ... key 63: length 1, key 64: empty
+      auto key = [&](int64_t i) {
+        const int64_t len = rp[i + 1] - rp[i];
+        return len <= 0 ? 64 : __builtin_clzll(static_cast<unsigned long long>(len));
+      };
+      int64_t cnt[65] = {0};
+      for (int64_t i = b0; i < b1; ++i) ++cnt[key(i)];
+      int64_t off[65], acc = 0;
+      for (int q = 0; q < 65; ++q) {
+        off[q] = acc;
+        acc += cnt[q];
+      }
+      for (int64_t i = b0; i < b1; ++i)
+        map_pad[static_cast<size_t>(base + (i - b0))] = static_cast<int32_t>(base + off[key(i)]++);
+    }
+    (void)rows;
+  };
+  std::vector<int32_t> wmap, smap;
+  slots_of(rpA, M->m, M->a_bounds, M->a_max, wmap, M->m_pad());
+  slots_of(rpT, M->n, M->t_bounds, M->t_max, smap, M->n_pad());
+  DevBuf<int32_t> wmap_d, smap_d;
+  wmap_d.alloc(wmap.size());
+  smap_d.alloc(smap.size());
+  CK(cudaMemcpyAsync(wmap_d.p, wmap.data(), wmap.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(smap_d.p, smap.data(), smap.size() * 4, cudaMemcpyHostToDevice, s));
+  M->a_ci_sgd.alloc(M->A.nnz);
+  M->t_ci_sgd.alloc(M->AT.nnz);
+  CK(eqb::launch_remap_cols(M->a_ci_sgd.p, M->A.col, smap_d.p, M->A.nnz, s));
+  CK(eqb::launch_remap_cols(M->t_ci_sgd.p, M->AT.col, wmap_d.p, M->AT.nnz, s));
+  const int64_t pa = M->world == 1 ? 0 : M->rank * M->a_max;
+  const int64_t pt = M->world == 1 ? 0 : M->rank * M->t_max;
+  M->wslot.alloc(M->m_loc());
+  M->sslot.alloc(M->n_loc());
+  if (M->m_loc())
+    CK(cudaMemcpyAsync(M->wslot.p, wmap.data() + pa, M->m_loc() * 4, cudaMemcpyHostToDevice, s));
+  if (M->n_loc())
+    CK(cudaMemcpyAsync(M->sslot.p, smap.data() + pt, M->n_loc() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  M->slots = true;
+}
+
 // Build local shards from the full device CSR(A) and CSR(A^T).
 void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
                   const std::vector<int64_t>& rpA_host,
@@ -606,6 +674,7 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
                plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
   build_panel_layout(M, la.data(), lt.data());
+  build_slot_layout(M, rpA_host.data(), rpT_host.data());
 }
 
 void alloc_workspaces(equil_matrix* M);
@@ -653,6 +722,7 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     else
       upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
     build_panel_layout(M, row_ptr, rpT.data());
+    build_slot_layout(M, row_ptr, rpT.data());
   } else {
     const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
     shard_sparse(M, fullA, fullT, rpA, rpT);
@@ -1065,7 +1135,9 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     if (T > 0) {
       CK(eqb::launch_sgd_init(M->xs[0].p, M->xw[0].p, M->u.p, M->ub.p, M->v.p, M->vb.p,
                               M->n_pad(), M->m_pad(), M->signs.p, M->m_loc(), M->n_loc(),
-                              M->a_goff(), M->t_goff(), a_poff, t_poff, m, n, s));
+                              M->a_goff(), M->t_goff(), a_poff, t_poff, m, n,
+                              M->slots ? M->wslot.p : nullptr,
+                              M->slots ? M->sslot.p : nullptr, s));
       allgather_padded(M, M->xs[0].p, M->t_max);
       allgather_padded(M, M->xw[0].p, M->a_max);
     } else {
@@ -1217,6 +1289,12 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       a.c[1] = cv;
       a.lin[0] = vec_lin ? M->lin_u.p : nullptr;
       a.lin[1] = vec_lin ? M->lin_v.p : nullptr;
+      if (M->slots) {
+        a.ci[0] = M->a_ci_sgd.p;
+        a.ci[1] = M->t_ci_sgd.p;
+        a.slot[0] = M->wslot.p;
+        a.slot[1] = M->sslot.p;
+      }
       a.st = host_step(t);
       a.flags = M->flags.p;
       return a;

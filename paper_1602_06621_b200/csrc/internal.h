@@ -88,6 +88,10 @@ struct SgdIterArgs {
   int has_next;
   SgdBlockConst c[2];
   const double* lin[2];  // per-coordinate linear terms (local rows) or nullptr
+  // slot of local row r in the gathered vector it feeds (xw for A rows, xs for
+  // A^T rows), or nullptr for the plain padded position poff + r.  A layout
+  // with the most-gathered coordinates packed first keeps them L1-resident.
+  const int32_t* slot[2];
   SgdStep st;
   unsigned* flags;
 };
@@ -197,7 +201,11 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
                             int64_t m_pad_len, const uint32_t* signs,
                             int64_t m_loc, int64_t n_loc, int64_t a_goff,
                             int64_t at_goff, int64_t a_poff, int64_t at_poff,
-                            int64_t m_glob, int64_t n_glob, cudaStream_t s);
+                            int64_t m_glob, int64_t n_glob, const int32_t* wslot,
+                            const int32_t* sslot, cudaStream_t s);
+// dst[k] = map[src[k]] (column indices into a slot layout)
+cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* map, int64_t nnz,
+                              cudaStream_t s);
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s);
 cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
                        cudaStream_t s);

@@ -711,18 +711,24 @@ __global__ void sgd_init_kernel(double* xs, double* xw, double* u, double* ub,
                                 double* v, double* vb, const uint32_t* signs,
                                 int64_t m_loc, int64_t n_loc, int64_t a_goff,
                                 int64_t at_goff, int64_t a_poff, int64_t at_poff,
-                                int64_t n_glob) {
+                                int64_t n_glob, const int32_t* wslot, const int32_t* sslot) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k < m_loc) {  // d = exp(0) = 1: xw = w (iteration 1: outputs n + i)
     u[k] = 0.0;
     ub[k] = 0.0;
-    xw[a_poff + k] = sign_bit(signs, n_glob + a_goff + k) ? 1.0 : -1.0;
+    xw[wslot ? wslot[k] : a_poff + k] = sign_bit(signs, n_glob + a_goff + k) ? 1.0 : -1.0;
   }
   if (k < n_loc) {  // e = 1: xs = s (outputs j)
     v[k] = 0.0;
     vb[k] = 0.0;
-    xs[at_poff + k] = sign_bit(signs, at_goff + k) ? 1.0 : -1.0;
+    xs[sslot ? sslot[k] : at_poff + k] = sign_bit(signs, at_goff + k) ? 1.0 : -1.0;
   }
+}
+
+__global__ void remap_cols_by_map_kernel(int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                                         const int32_t* __restrict__ map, int64_t nnz) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nnz) dst[k] = map[src[k]];
 }
 
 __global__ void exp_kernel(const double* __restrict__ x, double* __restrict__ y,
@@ -737,13 +743,22 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
                             double* v, double* vb, int64_t, int64_t,
                             const uint32_t* signs, int64_t m_loc, int64_t n_loc,
                             int64_t a_goff, int64_t at_goff, int64_t a_poff,
-                            int64_t at_poff, int64_t, int64_t n_glob,
-                            cudaStream_t s) {
+                            int64_t at_poff, int64_t, int64_t n_glob, const int32_t* wslot,
+                            const int32_t* sslot, cudaStream_t s) {
   const int64_t nmax = std::max(m_loc, n_loc);
   if (nmax == 0) return cudaSuccess;
   sgd_init_kernel<<<static_cast<unsigned>((nmax + 255) / 256), 256, 0, s>>>(
       xs, xw, u, ub, v, vb, signs, m_loc, n_loc, a_goff, at_goff, a_poff, at_poff,
-      n_glob); count_launch(s);
+      n_glob, wslot, sslot); count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* map, int64_t nnz,
+                              cudaStream_t s) {
+  if (nnz == 0) return cudaSuccess;
+  remap_cols_by_map_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(dst, src, map,
+                                                                                   nnz);
+  count_launch(s);
   return cudaGetLastError();
 }
 

@@ -90,7 +90,7 @@ __device__ __forceinline__ double chain_sum(double acc, const double* sp, int b,
 __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
                                              int64_t r, double acc,
                                              unsigned& fl) {
-  const int64_t pi = a.poff[mat] + r;
+  const int64_t pi = a.slot[mat] ? static_cast<int64_t>(a.slot[mat][r]) : a.poff[mat] + r;
   // |d_i w_i| = d_i exactly (w = +-1): this iteration's d (mat 0) or e (mat 1)
   const double scl = fabs(mat ? a.xs_cur[pi] : a.xw_cur[pi]);
   const double y = __dmul_rn(scl, acc);          // linop.cpp:19 / :25
