@@ -133,29 +133,79 @@ struct PhaseTimer {
   }
 };
 
+// Device buffers come from the device's stream-ordered memory pool (release
+// threshold kept at max), allocated on a private per-device stream and made
+// visible before use, so repeated matrix setups reuse already-mapped memory
+// instead of paying cudaMalloc / cudaFree page mapping every time.  Release
+// keeps cudaFree's semantics: the device is synchronised before the memory goes
+// back to the pool.
+cudaStream_t alloc_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    cudaGetLastError();
+  }
+  return streams[dev];
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  int dev = -1;         // >= 0: pool allocation on alloc_stream(dev)
   void alloc(size_t count) {
     release();
     if (count == 0) count = 1;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    int d = 0;
+    CK(cudaGetDevice(&d));
+    cudaStream_t s = alloc_stream(d);
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    CK(cudaStreamSynchronize(s));
+    dev = d;
     n = count;
   }
   void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'ed array
     release();
     p = q;
     n = count;
+    dev = -1;
   }
   void ensure(size_t count) {
     if (count > n || !p) alloc(count);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (dev >= 0) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        cudaDeviceSynchronize();  // like cudaFree: nothing may still use p
+        cudaFreeAsync(p, alloc_stream(dev));
+        if (cur != dev) cudaSetDevice(cur);
+      } else {
+        cudaFree(p);
+      }
+    }
     p = nullptr;
     n = 0;
+    dev = -1;
   }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(dev, o.dev);
+  }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
 };
 
@@ -354,7 +404,7 @@ struct equil_matrix {
   // epilogues write each row's next value at its slot
   bool use_slots = true;
   bool slots = false;
-  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wslot, sslot;
+  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wmap, smap;  // wmap / smap: padded position -> slot
   DevBuf<double> pval[2];
   DevBuf<uint16_t> pcol[2];
   DevBuf<uint32_t> pruns[2];
@@ -553,56 +603,33 @@ void build_panel_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT)
 // line; packed together they fit in L1.  Rows are ordered by decreasing
 // floor(log2(length)) (stable), per rank inside its own padded range, and the
 // same is done for the columns feeding xs.  Only memory placement changes:
-// every row sum keeps its entries and their order.
-void build_slot_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT) {
+// every row sum keeps its entries and their order.  Built on the device from
+// the global row pointers (a 7-bit stable radix sort per matrix).
+void build_slot_layout(equil_matrix* M, const int64_t* rpA_dev, const int64_t* rpT_dev) {
   M->slots = false;
   if (!M->use_slots || M->use_panels) return;
   cudaStream_t s = M->stream;
-  // slot of every row of a matrix with global row_ptr rp partitioned by bounds
-  auto slots_of = [&](const int64_t* rp, int64_t rows, const std::vector<int64_t>& bounds,
-                      int64_t maxcnt, std::vector<int32_t>& map_pad, int64_t pad_len) {
-    map_pad.assign(static_cast<size_t>(pad_len), 0);
-    const int G = static_cast<int>(bounds.size()) - 1;
-    for (int g = 0; g < G; ++g) {
-      const int64_t b0 = bounds[g], b1 = bounds[g + 1];
-      const int64_t base = M->world == 1 ? 0 : g * maxcnt;
-      // key 0: longest rows (floor(log2(len)) = 63) ... key 63: length 1, key 64: empty
-      auto key = [&](int64_t i) {
-        const int64_t len = rp[i + 1] - rp[i];
-        return len <= 0 ? 64 : __builtin_clzll(static_cast<unsigned long long>(len));
-      };
-      int64_t cnt[65] = {0};
-      for (int64_t i = b0; i < b1; ++i) ++cnt[key(i)];
-      int64_t off[65], acc = 0;
-      for (int q = 0; q < 65; ++q) {
-        off[q] = acc;
-        acc += cnt[q];
-      }
-      for (int64_t i = b0; i < b1; ++i)
-        map_pad[static_cast<size_t>(base + (i - b0))] = static_cast<int32_t>(base + off[key(i)]++);
-    }
-    (void)rows;
-  };
-  std::vector<int32_t> wmap, smap;
-  slots_of(rpA, M->m, M->a_bounds, M->a_max, wmap, M->m_pad());
-  slots_of(rpT, M->n, M->t_bounds, M->t_max, smap, M->n_pad());
-  DevBuf<int32_t> wmap_d, smap_d;
-  wmap_d.alloc(wmap.size());
-  smap_d.alloc(smap.size());
-  CK(cudaMemcpyAsync(wmap_d.p, wmap.data(), wmap.size() * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(smap_d.p, smap.data(), smap.size() * 4, cudaMemcpyHostToDevice, s));
+  const int G = M->world;
+  DevBuf<int64_t> ab, tb;
+  const int64_t* abd = M->a_bounds_d.p;
+  const int64_t* tbd = M->t_bounds_d.p;
+  if (G == 1) {  // bounds {0, rows}
+    ab.alloc(2);
+    tb.alloc(2);
+    const int64_t a2[2] = {0, M->m}, t2[2] = {0, M->n};
+    CK(cudaMemcpy(ab.p, a2, 16, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(tb.p, t2, 16, cudaMemcpyHostToDevice));
+    abd = ab.p;
+    tbd = tb.p;
+  }
+  M->wmap.alloc(M->m_pad());
+  M->smap.alloc(M->n_pad());
+  CK(eqb::launch_slot_map(rpA_dev, M->m, abd, G, M->a_max, M->wmap.p, s));
+  CK(eqb::launch_slot_map(rpT_dev, M->n, tbd, G, M->t_max, M->smap.p, s));
   M->a_ci_sgd.alloc(M->A.nnz);
   M->t_ci_sgd.alloc(M->AT.nnz);
-  CK(eqb::launch_remap_cols(M->a_ci_sgd.p, M->A.col, smap_d.p, M->A.nnz, s));
-  CK(eqb::launch_remap_cols(M->t_ci_sgd.p, M->AT.col, wmap_d.p, M->AT.nnz, s));
-  const int64_t pa = M->world == 1 ? 0 : M->rank * M->a_max;
-  const int64_t pt = M->world == 1 ? 0 : M->rank * M->t_max;
-  M->wslot.alloc(M->m_loc());
-  M->sslot.alloc(M->n_loc());
-  if (M->m_loc())
-    CK(cudaMemcpyAsync(M->wslot.p, wmap.data() + pa, M->m_loc() * 4, cudaMemcpyHostToDevice, s));
-  if (M->n_loc())
-    CK(cudaMemcpyAsync(M->sslot.p, smap.data() + pt, M->n_loc() * 4, cudaMemcpyHostToDevice, s));
+  CK(eqb::launch_remap_cols(M->a_ci_sgd.p, M->A.col, M->smap.p, M->A.nnz, s));
+  CK(eqb::launch_remap_cols(M->t_ci_sgd.p, M->AT.col, M->wmap.p, M->AT.nnz, s));
   CK(cudaStreamSynchronize(s));
   M->slots = true;
 }
@@ -674,10 +701,10 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
                plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
   build_panel_layout(M, la.data(), lt.data());
-  build_slot_layout(M, rpA_host.data(), rpT_host.data());
+  build_slot_layout(M, fullA.row_ptr, fullT.row_ptr);
 }
 
-void alloc_workspaces(equil_matrix* M);
+void alloc_workspaces(equil_matrix* M, PhaseTimer* pt = nullptr);
 
 // From a validated device CSR(A) (ownership taken) and its host row_ptr: build
 // CSR(A^T) on device (K2), plan the traversal (planA may already be running on
@@ -707,38 +734,43 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     M->t_bounds = {0, n};
     M->a_max = m;
     M->t_max = n;
-    std::swap(M->a_rp.p, rp.p); std::swap(M->a_rp.n, rp.n);
-    std::swap(M->a_ci.p, ci.p); std::swap(M->a_ci.n, ci.n);
-    std::swap(M->a_va.p, va.p); std::swap(M->a_va.n, va.n);
-    std::swap(M->t_rp.p, trp.p); std::swap(M->t_rp.n, trp.n);
-    std::swap(M->t_ci.p, tci.p); std::swap(M->t_ci.n, tci.n);
-    std::swap(M->t_va.p, tva.p); std::swap(M->t_va.n, tva.n);
+    M->a_rp.swap(rp);
+    M->a_ci.swap(ci);
+    M->a_va.swap(va);
+    M->t_rp.swap(trp);
+    M->t_ci.swap(tci);
+    M->t_va.swap(tva);
     M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
     M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
     const Plan planT = plan_tiles(rpT.data(), n, 1);
+    pt.mark(s, "plan A^T");
     if (planner && planner->joinable()) planner->join();
+    pt.mark(s, "plan A (join)");
     if (planA)  // computed concurrently by the caller
       upload_plans(M, *planA, planT);
     else
       upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
+    pt.mark(s, "upload plans");
     build_panel_layout(M, row_ptr, rpT.data());
-    build_slot_layout(M, row_ptr, rpT.data());
+    build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);
+    pt.mark(s, "slots");
   } else {
     const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
     shard_sparse(M, fullA, fullT, rpA, rpT);
   }
   pt.mark(s, "plan");
-  alloc_workspaces(M);
+  alloc_workspaces(M, &pt);
   CK(cudaStreamSynchronize(s));
   pt.mark(s, "workspaces");
 }
 
-void alloc_workspaces(equil_matrix* M) {
+void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   // each vector padded to whole panels (the panel traversal bulk-copies them)
   auto whole = [](int64_t x) { return (x + eqb::kPanelW - 1) / eqb::kPanelW * eqb::kPanelW; };
   const int64_t np = whole(M->n_pad()), mp = whole(M->m_pad());
   M->xbuf.alloc(2 * (np + mp));
   CK(cudaMemset(M->xbuf.p, 0, 2 * (np + mp) * sizeof(double)));
+  if (pt) pt->mark(M->stream, "xbuf");
   for (int b = 0; b < 2; ++b) {
     M->xs[b].p = M->xbuf.p + b * np;
     M->xw[b].p = M->xbuf.p + 2 * np + b * mp;
@@ -764,6 +796,7 @@ void alloc_workspaces(equil_matrix* M) {
     }
     cudaGetLastError();  // the window is a hint; never fail on it
   }
+  if (pt) pt->mark(M->stream, "l2 window");
   M->u.alloc(M->m_loc());
   M->ub.alloc(M->m_loc());
   M->v.alloc(M->n_loc());
@@ -1136,8 +1169,8 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       CK(eqb::launch_sgd_init(M->xs[0].p, M->xw[0].p, M->u.p, M->ub.p, M->v.p, M->vb.p,
                               M->n_pad(), M->m_pad(), M->signs.p, M->m_loc(), M->n_loc(),
                               M->a_goff(), M->t_goff(), a_poff, t_poff, m, n,
-                              M->slots ? M->wslot.p : nullptr,
-                              M->slots ? M->sslot.p : nullptr, s));
+                              M->slots ? M->wmap.p + a_poff : nullptr,
+                              M->slots ? M->smap.p + t_poff : nullptr, s));
       allgather_padded(M, M->xs[0].p, M->t_max);
       allgather_padded(M, M->xw[0].p, M->a_max);
     } else {
@@ -1292,8 +1325,8 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       if (M->slots) {
         a.ci[0] = M->a_ci_sgd.p;
         a.ci[1] = M->t_ci_sgd.p;
-        a.slot[0] = M->wslot.p;
-        a.slot[1] = M->sslot.p;
+        a.slot[0] = M->wmap.p + a_poff;  // local row r -> slot
+        a.slot[1] = M->smap.p + t_poff;
       }
       a.st = host_step(t);
       a.flags = M->flags.p;

@@ -21,7 +21,7 @@ struct Tile {
   int32_t pad;
 };
 #ifndef EQ_SLICE_BATCH
-#define EQ_SLICE_BATCH 4
+#define EQ_SLICE_BATCH 6
 #endif
 #ifndef EQ_LONG_BATCH
 #define EQ_LONG_BATCH 4
@@ -34,6 +34,9 @@ constexpr int kSliceChunk = 16;  // products per row per lock-step round (kind 2
 constexpr int kSliceStride = 18; // padded row stride (doubles): conflict-free LDS.128
 constexpr int kSliceBatch = EQ_SLICE_BATCH;  // row pairs staged per batch (loads in flight)
 constexpr int kSliceRows = 32;
+#ifndef EQ_SLICE_PREFETCH
+#define EQ_SLICE_PREFETCH 0  // rounds of L2 prefetch ahead in kind-2 slices (0: off)
+#endif
 #ifndef EQ_SLICE_WINDOW
 #define EQ_SLICE_WINDOW 4096
 #endif
@@ -203,6 +206,11 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
                             int64_t at_goff, int64_t a_poff, int64_t at_poff,
                             int64_t m_glob, int64_t n_glob, const int32_t* wslot,
                             const int32_t* sslot, cudaStream_t s);
+// hot-first slot map of the rows of a (global) matrix partitioned by bounds
+// (G + 1 device values): map_pad[padded position of row i] = its slot, rows
+// of each rank ordered by decreasing floor(log2(length)), stable
+cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* bounds, int G,
+                            int64_t maxcnt, int32_t* map_pad, cudaStream_t s);
 // dst[k] = map[src[k]] (column indices into a slot layout)
 cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* map, int64_t nnz,
                               cudaStream_t s);

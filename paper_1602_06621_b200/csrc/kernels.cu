@@ -622,6 +622,16 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
     double acc = 0.0;
     for (int b = 0; b < maxr; ++b) {
       const int off = b * kSliceChunk;
+#if EQ_SLICE_PREFETCH
+      // pull this lane's row chunk EQ_SLICE_PREFETCH rounds ahead into L2, so the
+      // column-index loads of later rounds (which the gathers depend on) do not
+      // wait on DRAM
+      if (rounds > b + EQ_SLICE_PREFETCH) {
+        const int64_t nx = kb + off + EQ_SLICE_PREFETCH * kSliceChunk;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ci + nx));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(va + nx));
+      }
+#endif
       // rows still active this round (rows are length-sorted, so nearly a prefix)
       const int act = 32 - __clz(__ballot_sync(0xffffffffu, rounds > b));
       for (int q0 = 0; q0 < act; q0 += 2 * kSliceBatch) {
@@ -751,6 +761,67 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
       xs, xw, u, ub, v, vb, signs, m_loc, n_loc, a_goff, at_goff, a_poff, at_poff,
       n_glob, wslot, sslot); count_launch(s);
   return cudaGetLastError();
+}
+
+namespace {
+// key of row i of rank g: g * 128 + (len == 0 ? 64 : clz(len)) -> longest rows first
+__global__ void slot_keys_kernel(const int64_t* __restrict__ rp, int64_t rows,
+                                 const int64_t* __restrict__ bounds, int G,
+                                 uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows) return;
+  int g = 0;
+  while (g + 1 < G && bounds[g + 1] <= i) ++g;
+  const int64_t len = rp[i + 1] - rp[i];
+  key[i] = static_cast<uint32_t>(g) * 128u +
+           (len <= 0 ? 64u : static_cast<uint32_t>(__clzll(static_cast<long long>(len))));
+  idx[i] = static_cast<int32_t>(i);
+}
+// sorted position s holds row perm[s]: map[pad(perm[s])] = g * maxcnt + (s - bounds[g])
+__global__ void slot_map_kernel(const int32_t* __restrict__ perm, int64_t rows,
+                                const int64_t* __restrict__ bounds, int G, int64_t maxcnt,
+                                int32_t* __restrict__ map_pad) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= rows) return;
+  const int64_t i = perm[s];
+  int g = 0;
+  while (g + 1 < G && bounds[g + 1] <= i) ++g;  // rank of row i == rank of position s
+  const int64_t base = G == 1 ? 0 : g * maxcnt;
+  map_pad[base + (i - bounds[g])] = static_cast<int32_t>(base + (s - bounds[g]));
+}
+}  // namespace
+
+cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* bounds, int G,
+                            int64_t maxcnt, int32_t* map_pad, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  uint32_t *k0 = nullptr, *k1 = nullptr;
+  int32_t *i0 = nullptr, *i1 = nullptr;
+  void* temp = nullptr;
+  size_t tb = 0;
+  int bits = 7;
+  while ((1 << (bits - 7)) < G) ++bits;
+  cudaError_t e = cudaSuccess;
+  do {
+    e = cudaMallocAsync(&k0, rows * 4, s); if (e) break;
+    e = cudaMallocAsync(&k1, rows * 4, s); if (e) break;
+    e = cudaMallocAsync(&i0, rows * 4, s); if (e) break;
+    e = cudaMallocAsync(&i1, rows * 4, s); if (e) break;
+    const unsigned grid = static_cast<unsigned>((rows + 255) / 256);
+    slot_keys_kernel<<<grid, 256, 0, s>>>(rp, rows, bounds, G, k0, i0);
+    count_launch(s);
+    e = cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, i1, rows, 0, bits, s);
+    if (e) break;
+    e = cudaMallocAsync(&temp, tb, s); if (e) break;
+    e = cub::DeviceRadixSort::SortPairs(temp, tb, k0, k1, i0, i1, rows, 0, bits, s);  // stable
+    if (e) break;
+    slot_map_kernel<<<grid, 256, 0, s>>>(i1, rows, bounds, G, maxcnt, map_pad);
+    count_launch(s);
+    e = cudaGetLastError();
+  } while (0);
+  for (void* q : {static_cast<void*>(k0), static_cast<void*>(k1), static_cast<void*>(i0),
+                  static_cast<void*>(i1), temp})
+    if (q) cudaFreeAsync(q, s);
+  return e;
 }
 
 cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* map, int64_t nnz,
@@ -898,7 +969,8 @@ canon_reduce_kernel(const double* __restrict__ x, int64_t len, int kind, double 
   if (l == 0) {
     part[blockIdx.x] = p;
     __threadfence();
-    last = (atomicAdd(counter, 1u) == static_cast<unsigned>(nc - 1));
+    // (an empty input still runs one CTA, which must finish the reduction)
+    last = (atomicAdd(counter, 1u) == static_cast<unsigned>((nc > 0 ? nc : 1) - 1));
   }
   __syncthreads();
   if (!last) return;
