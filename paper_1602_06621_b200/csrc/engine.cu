@@ -380,6 +380,8 @@ struct equil_matrix {
   bool dense = false;
   int64_t m = 0, n = 0, nnz = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // uploads that overlap work on `stream`
+  cudaEvent_t ev_vals = nullptr;       // values of A on the device
   std::mutex mu;
   ncclComm_t comm = nullptr;
 
@@ -462,6 +464,8 @@ struct equil_matrix {
     if (ev_loop1) cudaEventDestroy(ev_loop1);
     if (graph) cudaGraphExecDestroy(graph);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
+    if (ev_vals) cudaEventDestroy(ev_vals);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -480,6 +484,8 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   require(M->device >= 0 && M->device < ndev, "device cfg: no such CUDA device");
   CK(cudaSetDevice(M->device));
   CK(cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&M->copy_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&M->ev_vals, cudaEventDisableTiming));
   {  // keep stream-ordered scratch (transpose, reductions) cached across calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, M->device) == cudaSuccess) {
@@ -630,8 +636,7 @@ void build_slot_layout(equil_matrix* M, const int64_t* rpA_dev, const int64_t* r
   M->t_ci_sgd.alloc(M->AT.nnz);
   CK(eqb::launch_remap_cols(M->a_ci_sgd.p, M->A.col, M->smap.p, M->A.nnz, s));
   CK(eqb::launch_remap_cols(M->t_ci_sgd.p, M->AT.col, M->wmap.p, M->AT.nnz, s));
-  CK(cudaStreamSynchronize(s));
-  M->slots = true;
+  M->slots = true;  // complete when `stream` reaches here (setup ends with a sync)
 }
 
 // Build local shards from the full device CSR(A) and CSR(A^T).
@@ -722,11 +727,34 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
   tci.alloc(nnz);
   tva.alloc(nnz);
   eqb::DevCsr fullT{n, m, nnz, trp.p, tci.p, tva.p};
-  CK(eqb::transpose_csr(fullA, fullT, s));
-  pt.mark(s, "transpose");
+  // CSR(A^T)'s row pointers first (column counts), so the host can plan the
+  // A^T traversal while the device transposes
   std::vector<int64_t> rpT(n + 1);
+  CK(eqb::launch_col_rowptr(ci.p, nnz, n, trp.p, s));
   CK(cudaMemcpyAsync(rpT.data(), trp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  cudaEvent_t ev_rp = nullptr;
+  CK(cudaEventCreateWithFlags(&ev_rp, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t e;
+    ~EvGuard() { cudaEventDestroy(e); }
+  } evg{ev_rp};
+  CK(cudaEventRecord(ev_rp, s));
+  Plan planT;
+  std::thread tplanner;
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } tj{tplanner};
+  if (M->world == 1)
+    tplanner = std::thread([&] {
+      if (cudaEventSynchronize(ev_rp) == cudaSuccess) planT = plan_tiles(rpT.data(), n, 1);
+    });
+  CK(eqb::transpose_csr(fullA, fullT, s, M->ev_vals));
+  CK(cudaStreamWaitEvent(s, M->ev_vals, 0));  // every later use of A's values
+  pt.mark(s, "transpose");
+  CK(cudaEventSynchronize(ev_rp));
   pt.mark(s, "rowptr copy");
   if (M->world == 1) {
     // adopt the full arrays as the shard (no copy)
@@ -742,7 +770,8 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     M->t_va.swap(tva);
     M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
     M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
-    const Plan planT = plan_tiles(rpT.data(), n, 1);
+    build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);  // device work
+    if (tplanner.joinable()) tplanner.join();  // planned during the transpose
     pt.mark(s, "plan A^T");
     if (planner && planner->joinable()) planner->join();
     pt.mark(s, "plan A (join)");
@@ -752,8 +781,7 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
       upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
     pt.mark(s, "upload plans");
     build_panel_layout(M, row_ptr, rpT.data());
-    build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);
-    pt.mark(s, "slots");
+    pt.mark(s, "panels");
   } else {
     const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
     shard_sparse(M, fullA, fullT, rpA, rpT);
@@ -897,10 +925,17 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     rp.alloc(m + 1);
     ci.alloc(nnz);
     va.alloc(nnz);
+    // row pointers and columns first: validation and the transpose sort need
+    // only those, and run while the values are still crossing PCIe
     CK(cudaMemcpyAsync(rp.p, row_ptr, (m + 1) * 8, cudaMemcpyHostToDevice, s));
     if (nnz) {
       CK(cudaMemcpyAsync(ci.p, col, nnz * 4, cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(va.p, val, nnz * 8, cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(M->ev_vals, s));  // values follow the columns on the copy stream
+      CK(cudaStreamWaitEvent(M->copy_stream, M->ev_vals, 0));
+      CK(cudaMemcpyAsync(va.p, val, nnz * 8, cudaMemcpyHostToDevice, M->copy_stream));
+      CK(cudaEventRecord(M->ev_vals, M->copy_stream));
+    } else {
+      CK(cudaEventRecord(M->ev_vals, s));
     }
     eqb::DevCsr fullA{m, n, nnz, rp.p, ci.p, va.p};
     // plan CSR(A) on the host while the device validates and transposes

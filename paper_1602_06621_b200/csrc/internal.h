@@ -191,7 +191,13 @@ void count_launch(cudaStream_t s, int n = 1);  // skipped while s is capturing
 // 2 columns not ascending; must be preset to ~0
 cudaError_t launch_validate_csr(const DevCsr& A, int* err, unsigned long long* where,
                                 cudaStream_t s);
-cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s);
+// row pointers of A^T from A's column indices (column counts + scan), available
+// before the transpose itself
+cudaError_t launch_col_rowptr(const int32_t* col, int64_t nnz, int64_t cols, int64_t* rp,
+                              cudaStream_t s);
+// val_ready (optional): event the value gather waits on (values still uploading)
+cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s,
+                          cudaEvent_t val_ready = nullptr);
 // ExplicitMatrix::sparse on device from COO (rows/cols int64, device); out
 // arrays preallocated (row_ptr m+1, col/val nnz).  On a precondition failure
 // *bad_kind = 1 (out of range: *bad = first entry index in input order) or

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "internal.h"
 #include "mt64_host.h"
@@ -362,7 +363,35 @@ __global__ void transpose_rowptr_kernel(const int32_t* __restrict__ skey, int64_
 }
 }  // namespace
 
-cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
+namespace {
+__global__ void col_count_kernel(const int32_t* __restrict__ col, int64_t nnz,
+                                 unsigned long long* __restrict__ cnt) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nnz) atomicAdd(cnt + col[k] + 1, 1ull);
+}
+}  // namespace
+
+cudaError_t launch_col_rowptr(const int32_t* col, int64_t nnz, int64_t cols, int64_t* rp,
+                              cudaStream_t s) {
+  void* temp = nullptr;
+  size_t tb = 0;
+  cudaError_t e = cudaMemsetAsync(rp, 0, (cols + 1) * 8, s);
+  if (e) return e;
+  if (nnz > 0) {
+    col_count_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
+        col, nnz, reinterpret_cast<unsigned long long*>(rp));
+    count_launch(s);
+  }
+  e = cub::DeviceScan::InclusiveSum(nullptr, tb, rp, rp, cols + 1, s);
+  if (e) return e;
+  e = cudaMallocAsync(&temp, tb, s);
+  if (e) return e;
+  e = cub::DeviceScan::InclusiveSum(temp, tb, rp, rp, cols + 1, s);
+  cudaFreeAsync(temp, s);
+  return e;
+}
+
+cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s, cudaEvent_t val_ready) {
   const int64_t nnz = A.nnz;
   AT.rows = A.cols;
   AT.cols = A.rows;
@@ -391,6 +420,9 @@ cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s) {
       const int64_t nexp = (nnz + kExpand - 1) / kExpand;
       expand_rows_kernel<<<static_cast<unsigned>((nexp + 255) / 256), 256, 0, s>>>(
           A.row_ptr, A.rows, nnz, perm_in); count_launch(s);
+      if (val_ready) {
+        e = cudaStreamWaitEvent(s, val_ready, 0); if (e) break;
+      }
       transpose_gather_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
           perm_in, A.val, perm_out, nnz, AT.col, AT.val); count_launch(s);
       e = cudaGetLastError(); if (e) break;
