@@ -382,6 +382,7 @@ struct equil_matrix {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // uploads that overlap work on `stream`
   cudaEvent_t ev_vals = nullptr;       // values of A on the device
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
   ncclComm_t comm = nullptr;
 
@@ -436,6 +437,7 @@ struct equil_matrix {
 
   // graph cache for the SGD loop
   cudaGraphExec_t graph = nullptr;
+  long long graph_launches = 0;  // kernel nodes per replay
   struct Key {
     int T = -1;
     double alpha = 0, beta = 0, gamma = 0, M = 0;
@@ -465,6 +467,8 @@ struct equil_matrix {
     if (graph) cudaGraphExecDestroy(graph);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (ev_vals) cudaEventDestroy(ev_vals);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -486,6 +490,8 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   CK(cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&M->copy_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&M->ev_vals, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&M->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&M->ev_join, cudaEventDisableTiming));
   {  // keep stream-ordered scratch (transpose, reductions) cached across calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, M->device) == cudaSuccess) {
@@ -809,7 +815,8 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
   const size_t bytes = static_cast<size_t>(2 * (np + mp)) * sizeof(double);
-  if (max_persist > 0 && max_window > 0) {
+  static const bool l2win = !getenv("EQUIL_L2WIN") || atoi(getenv("EQUIL_L2WIN")) != 0;
+  if (l2win && max_persist > 0 && max_window > 0) {
     const size_t win = std::min(bytes, static_cast<size_t>(max_window));
     const size_t carve = std::min(win, static_cast<size_t>(max_persist));
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
@@ -1405,10 +1412,25 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       if (M->dense) {
         CK(eqb::launch_dense_sgd_iter(dense_args(t), s));
       } else {
-        if (M->n_pbands)
+        static const int conc = getenv("EQUIL_CONC") ? atoi(getenv("EQUIL_CONC")) : 1;
+        if (M->n_pbands) {
           CK(eqb::launch_sgd_panel(iter_args(t), panel_args, M->n_pbands, s));
-        else
+        } else if (conc && M->n_sgd_long > 0 && M->n_sgd_long < M->n_sgd) {
+          // long-row CTA groups and warp tiles as two concurrent kernels (fork /
+          // join on the copy stream): each kernel gets its own residency on the
+          // SMs instead of one launch sized for both (c3: 4-5% faster)
+          const eqb::SgdIterArgs a = iter_args(t);
+          CK(cudaEventRecord(M->ev_fork, s));
+          CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+          CK(eqb::launch_sgd_iter_part(a, 0, M->n_sgd_long, true, conc >= 2 ? 8 : 6,
+                                       M->copy_stream));
+          CK(eqb::launch_sgd_iter_part(a, M->n_sgd_long, M->n_sgd - M->n_sgd_long, false,
+                                       conc >= 3 ? 8 : 6, s));
+          CK(cudaEventRecord(M->ev_join, M->copy_stream));
+          CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+        } else {
           CK(eqb::launch_sgd_iter(iter_args(t), M->n_sgd, s));
+        }
         if (t < T) {
           allgather_padded(M, M->xs[t & 1].p, M->t_max);
           allgather_padded(M, M->xw[t & 1].p, M->a_max);
@@ -1436,12 +1458,24 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
           throw;
         }
         CK(cudaStreamEndCapture(s, &g));
+        {  // kernel nodes of one replay, for the launch accounting
+          size_t nn = 0;
+          CK(cudaGraphGetNodes(g, nullptr, &nn));
+          std::vector<cudaGraphNode_t> nodes(nn);
+          if (nn) CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+          long long kn = 0;
+          for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++kn;
+          }
+          M->graph_launches = kn;
+        }
         CK(cudaGraphInstantiate(&M->graph, g, 0));
         cudaGraphDestroy(g);
         M->graph_key = key;
       }
       CK(cudaGraphLaunch(M->graph, s));
-      eqb::note_launches(T);
+      eqb::note_launches(M->graph_launches);
     } else {
       CK(cudaEventRecord(M->ev_loop0, s));
       for (int t = 1; t <= T; ++t) {

@@ -221,6 +221,8 @@ cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* boun
 cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* map, int64_t nnz,
                               cudaStream_t s);
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s);
+cudaError_t launch_sgd_iter_part(const SgdIterArgs& a, int tile_base, int ntiles, bool long_part,
+                                 int minb, cudaStream_t s);
 cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
                        cudaStream_t s);
 cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s);

@@ -898,6 +898,23 @@ cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// tiles [tile_base, tile_base + ntiles) of one kind class (long: kind-3 CTA
+// groups, else warp tiles) -- for launching the two classes on separate streams
+cudaError_t launch_sgd_iter_part(const SgdIterArgs& a, int tile_base, int ntiles, bool long_part,
+                                 int minb, cudaStream_t s) {
+  if (ntiles <= 0) return cudaSuccess;
+  const unsigned g = static_cast<unsigned>((ntiles + kTileWarps - 1) / kTileWarps);
+  if (long_part) {
+    if (minb >= 8) sgd_iter_kernel<8, 2><<<g, kTileThreads, 0, s>>>(a, tile_base, ntiles);
+    else sgd_iter_kernel<6, 2><<<g, kTileThreads, 0, s>>>(a, tile_base, ntiles);
+  } else {
+    if (minb >= 8) sgd_iter_kernel<8, 1><<<g, kTileThreads, 0, s>>>(a, tile_base, ntiles);
+    else sgd_iter_kernel<6, 1><<<g, kTileThreads, 0, s>>>(a, tile_base, ntiles);
+  }
+  count_launch(s);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;

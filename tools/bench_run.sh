@@ -1,1 +1,2 @@
-EQUIL_VERBOSE=1 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err || exit 1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err || exit 1
