@@ -41,17 +41,21 @@ def launches(src, dst):
 
 
 def full(rep, dst):
+    """One ncu --set full capture of the launches of ONE SGD iteration (the
+    long-row and slice parts of sgd_iter_kernel); per-launch metrics and the
+    per-iteration DRAM traffic (sum over the parts)."""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
-    h, u, v = r[0], r[1], r[2]
-    get = lambda n: (float(v[h.index(n)].replace(",", "")), u[h.index(n)]) if n in h else (None, "")
+    h, u, rows = r[0], r[1], r[2:]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    rd, ru = get("dram__bytes_read.sum")
-    wr, wu = get("dram__bytes_write.sum")
-    dur, du = get("gpu__time_duration.sum")
-    dur_ms = dur * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1}.get(du, 1)
-    rd_b, wr_b = rd * scale.get(ru, 1), wr * scale.get(wu, 1)
+    tscale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1, "ms": 1}
+
+    def get(v, n, sc):
+        if n not in h:
+            return 0.0
+        return float(v[h.index(n)].replace(",", "")) * sc.get(u[h.index(n)], 1)
+
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "dram__throughput.avg.pct_of_peak_sustained_elapsed",
             "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -59,19 +63,32 @@ def full(rep, dst):
             "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "launch__grid_size",
+            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
             "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
             "lts__t_sectors_srcunit_tex_op_read.sum"]
-    lines = [f"| {k} | {v[h.index(k)]} {u[h.index(k)]} |" for k in keys if k in h]
+    names = [v[h.index("Kernel Name")][:40] if "Kernel Name" in h else f"launch {k}"
+             for k, v in enumerate(rows)]
+    lines = ["| metric | " + " | ".join(names) + " |", "|---|" + "---|" * len(rows)]
+    for k in keys:
+        if k in h:
+            lines.append(f"| {k} ({u[h.index(k)]}) | " +
+                         " | ".join(v[h.index(k)] for v in rows) + " |")
+    rd = sum(get(v, "dram__bytes_read.sum", scale) for v in rows)
+    wr = sum(get(v, "dram__bytes_write.sum", scale) for v in rows)
+    dur = sum(get(v, "gpu__time_duration.sum", tscale) for v in rows)
     with open(dst, "w") as f:
-        f.write(f"ncu --set full --clock-control none, kernel sgd_iter_kernel (c3, one launch)\n"
-                f"source: {rep}\n\n| metric | value |\n|---|---|\n" + "\n".join(lines) + "\n")
+        f.write(f"ncu --set full --clock-control none: the {len(rows)} launches of one SGD "
+                f"iteration on c3 (serialised by ncu)\nsource: {rep}\n\n" +
+                "\n".join(lines) + f"\n\nper iteration: DRAM {rd / 1e9:.3f} GB read + "
+                f"{wr / 1e9:.3f} GB written, {dur:.3f} ms summed\n")
     summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
     d = {}
     if os.path.exists(summ):
         d = json.load(open(summ))
-    d["sgd_iter_kernel"] = {"dram_bytes_per_launch": rd_b + wr_b, "dram_read": rd_b,
-                            "dram_write": wr_b, "duration_ms": dur_ms, "source": dst}
+    d["sgd_iter_kernel"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd,
+                            "dram_write": wr, "duration_ms": dur, "launches": len(rows),
+                            "source": dst}
     json.dump(d, open(summ, "w"), indent=1)
     print("\n".join(lines))
 
