@@ -250,6 +250,30 @@ equil_status equil_spectral_norm(equil_matrix* A, int max_iters, double rel_tol,
  * src/ccp.cpp:115-123) */
 equil_status equil_lasso_objective(equil_matrix* A, const double* b, double lambda,
                                    const double* x, double* out);
+/* Public helpers of include/equil/equilibrate.hpp:15-48 and metrics.hpp:14-15 on the
+ * device matrix (single GPU; sparse, except the estimate).  u (m), v (n), lin_u (m),
+ * lin_v (n), gradients are host arrays.  exp and whole-vector sums follow the
+ * numerics contract, so objective / gradient / rms agree with the
+ * reference to ~1e-12 relative; the estimate is bit-exact. */
+equil_status equil_objective(equil_matrix* A, const double* u, const double* v,
+                             const equil_params* p, double* out);
+equil_status equil_objective_weighted(equil_matrix* A, const double* u, const double* v,
+                                      const double* lin_u, const double* lin_v, double gamma,
+                                      double* out);
+equil_status equil_gradient(equil_matrix* A, const double* u, const double* v,
+                            const equil_params* p, double* grad_u, double* grad_v);
+equil_status equil_gradient_weighted(equil_matrix* A, const double* u, const double* v,
+                                     const double* lin_u, const double* lin_v, double gamma,
+                                     double* grad_u, double* grad_v);
+/* stochastic_gradient_estimate(op, u, v, params, rng, g_u, g_v): the SeededRng is
+ * (seed, stream) advanced by `offset` draws; the call consumes n + m draws. */
+equil_status equil_stochastic_gradient_estimate(equil_matrix* A, const double* u,
+                                                const double* v, const equil_params* p,
+                                                uint64_t seed, uint64_t stream, uint64_t offset,
+                                                double* g_u, double* g_v);
+equil_status equil_rms_error(equil_matrix* A, const double* u, const double* v, double alpha,
+                             double beta, double* out);
+equil_status equil_project_box(const double* x, int64_t n, double bound, double* out);
 /* lsqr(op, b, max_iters, tol) (include/equil/lsqr.hpp:30-31, src/lsqr.cpp:85-103) */
 equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
                         equil_lsqr_out* out);

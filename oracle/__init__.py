@@ -235,6 +235,9 @@ class _COracle:
         L.eo_ccp_lasso_preconditioned.argtypes = [C.POINTER(_Matrix), _dp, C.c_double,
                                                   C.POINTER(_Params), C.POINTER(_CcpOpts),
                                                   C.POINTER(_CcpRun)]
+        L.eo_stochastic_gradient_estimate.argtypes = [C.POINTER(_Matrix), _dp, _dp,
+                                                      C.POINTER(_Params), C.c_uint64, C.c_uint64,
+                                                      C.c_uint64, _dp, _dp]
         L.eo_objective.restype = C.c_double
         L.eo_objective.argtypes = [C.POINTER(_Matrix), _dp, _dp, C.c_double, C.c_double, C.c_double]
         L.eo_rms_error.restype = C.c_double
@@ -399,6 +402,21 @@ class _COracle:
             C.byref(mat), ptr(rb, _i64p), ptr(cb, _i64p), row_blocks, col_blocks, C.byref(p),
             diag_stride, s), A.m, A.n, iterations, diag_stride)
 
+    def stochastic_gradient_estimate(self, A: CsrArrays, u, v, seed, stream, offset, alpha=0.0,
+                                     beta=0.0, gamma=0.1):
+        """src/equilibrate.cpp:60-71"""
+        u = np.ascontiguousarray(u, np.float64)
+        v = np.ascontiguousarray(v, np.float64)
+        gu, gv = np.zeros(A.m), np.zeros(A.n)
+        p = _Params(alpha, beta, gamma, 9.210340371976184, 1, 0)
+        mat = A._struct()
+        rc = self.L.eo_stochastic_gradient_estimate(C.byref(mat), ptr(u, _dp), ptr(v, _dp),
+                                                    C.byref(p), seed, stream, offset,
+                                                    ptr(gu, _dp), ptr(gv, _dp))
+        if rc:
+            self._err(rc)
+        return gu, gv
+
     def spectral_norm(self, A: CsrArrays, max_iters=100, rel_tol=1e-9, seed=0) -> float:
         """src/lsqr.cpp:140-163"""
         out = C.c_double(0.0)
@@ -529,6 +547,11 @@ class _RefOracle:
         L.er_spectral_norm.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_uint64, _dp]
         L.er_lasso_objective.argtypes = [C.c_void_p, _dp, C.c_double, _dp, _dp]
         L.er_lasso_fista.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double, C.c_int, _dp, _dp]
+        L.er_objective.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_double, _dp]
+        L.er_gradient.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_double, _dp,
+                                  _dp]
+        L.er_sge.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_double,
+                             C.c_uint64, C.c_uint64, C.c_uint64, _dp, _dp]
         L.er_lsqr.argtypes = [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(_RefLsqr)]
         L.er_lsqr_preconditioned.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double,
                                              C.c_double, C.c_double, C.c_int, C.c_uint64,
@@ -705,6 +728,34 @@ class RefMatrix:
         if rc:
             self.R._err(rc)
         return run
+
+    def objective(self, u, v, alpha=0.0, beta=0.0, gamma=0.1) -> float:
+        out = C.c_double(0.0)
+        rc = self.R.L.er_objective(self.h, ptr(np.ascontiguousarray(u, np.float64), _dp),
+                                   ptr(np.ascontiguousarray(v, np.float64), _dp), alpha, beta,
+                                   gamma, C.byref(out))
+        if rc:
+            self.R._err(rc)
+        return out.value
+
+    def gradient(self, u, v, alpha=0.0, beta=0.0, gamma=0.1):
+        gu, gv = np.zeros(self.m), np.zeros(self.n)
+        rc = self.R.L.er_gradient(self.h, ptr(np.ascontiguousarray(u, np.float64), _dp),
+                                  ptr(np.ascontiguousarray(v, np.float64), _dp), alpha, beta,
+                                  gamma, ptr(gu, _dp), ptr(gv, _dp))
+        if rc:
+            self.R._err(rc)
+        return gu, gv
+
+    def stochastic_gradient_estimate(self, u, v, seed, stream, offset, alpha=0.0, beta=0.0,
+                                     gamma=0.1):
+        gu, gv = np.zeros(self.m), np.zeros(self.n)
+        rc = self.R.L.er_sge(self.h, ptr(np.ascontiguousarray(u, np.float64), _dp),
+                             ptr(np.ascontiguousarray(v, np.float64), _dp), alpha, beta, gamma,
+                             seed, stream, offset, ptr(gu, _dp), ptr(gv, _dp))
+        if rc:
+            self.R._err(rc)
+        return gu, gv
 
     def spectral_norm(self, max_iters=100, rel_tol=1e-9, seed=0) -> float:
         out = C.c_double(0.0)

@@ -1157,3 +1157,39 @@ int eo_ccp_lasso_preconditioned(const eo_matrix* A, const double* b, double lamb
   free(u); free(v); free(d); free(e);
   return rc;
 }
+
+/* stochastic_gradient_estimate (src/equilibrate.cpp:60-71) */
+int eo_stochastic_gradient_estimate(const eo_matrix* A, const double* u, const double* v,
+                                    const eo_params* p, uint64_t seed, uint64_t stream,
+                                    uint64_t offset, double* g_u, double* g_v) {
+  if (eo_validate_params(p)) return 1;
+  double alpha, beta;
+  if (eo_resolve_targets(p, A->m, A->n, &alpha, &beta)) return 1;
+  const int64_t m = A->m, n = A->n;
+  double* d = (double*)malloc((size_t)(m ? m : 1) * 8);
+  double* e = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* xs = (double*)malloc((size_t)(n ? n : 1) * 8);
+  double* xw = (double*)malloc((size_t)(m ? m : 1) * 8);
+  for (int64_t i = 0; i < m; ++i) d[i] = eo_det_exp(u[i]);
+  for (int64_t j = 0; j < n; ++j) e[j] = eo_det_exp(v[j]);
+  eo_rng r;
+  eo_rng_init(&r, seed, stream);
+  for (uint64_t k = 0; k < offset; ++k) (void)eo_rng_next_u64(&r);
+  for (int64_t j = 0; j < n; ++j) xs[j] = e[j] * eo_rng_sign(&r);
+  mat_apply(A, xs, g_u);
+  for (int64_t i = 0; i < m; ++i) {
+    const double y = d[i] * g_u[i];
+    g_u[i] = y * y;
+  }
+  for (int64_t i = 0; i < m; ++i) xw[i] = d[i] * eo_rng_sign(&r);
+  mat_adjoint(A, xw, g_v);
+  for (int64_t j = 0; j < n; ++j) {
+    const double z = e[j] * g_v[j];
+    g_v[j] = z * z;
+  }
+  const double nla = -alpha * alpha, nlb = -beta * beta;
+  for (int64_t i = 0; i < m; ++i) g_u[i] = g_u[i] + (nla + p->gamma * u[i]);
+  for (int64_t j = 0; j < n; ++j) g_v[j] = g_v[j] + (nlb + p->gamma * v[j]);
+  free(d); free(e); free(xs); free(xw);
+  return 0;
+}

@@ -158,6 +158,12 @@ int eo_lsqr_preconditioned(const eo_matrix* A, const double* b,
                            const eo_params* p, int max_iters, double tol,
                            eo_lsqr_run* out);
 
+/* stochastic_gradient_estimate (src/equilibrate.cpp:60-71): probes are outputs
+ * [offset, offset + n + m) of SeededRng(seed, stream) */
+int eo_stochastic_gradient_estimate(const eo_matrix* A, const double* u, const double* v,
+                                    const eo_params* p, uint64_t seed, uint64_t stream,
+                                    uint64_t offset, double* g_u, double* g_v);
+
 /* ---- spectral_norm (src/lsqr.cpp:140-163) and the Chambolle-Pock lasso
  * (src/ccp.cpp:28-160) --------------------------------------------------- */
 int eo_spectral_norm(const eo_matrix* A, int max_iters, double rel_tol, uint64_t seed,

@@ -406,6 +406,52 @@ int er_matrix_to_dense(void* h, double* out) {
   });
 }
 
+// ---- equilibrate.hpp helpers: objective / gradient (plain and weighted),
+// stochastic_gradient_estimate (rng advanced by `offset` draws)
+static EquilibrationParams mkparams(double alpha, double beta, double gamma, double M) {
+  EquilibrationParams p;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.gamma = gamma;
+  p.max_log_scale = M;
+  return p;
+}
+
+int er_objective(void* h, const double* u, const double* v, double alpha, double beta,
+                 double gamma, double* out) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    *out = objective(A, to_vec(u, A.rows()), to_vec(v, A.cols()),
+                     mkparams(alpha, beta, gamma, 9.210340371976184));
+  });
+}
+
+int er_gradient(void* h, const double* u, const double* v, double alpha, double beta,
+                double gamma, double* gu, double* gv) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    Vec a, b;
+    gradient(A, to_vec(u, A.rows()), to_vec(v, A.cols()),
+             mkparams(alpha, beta, gamma, 9.210340371976184), a, b);
+    from_vec(a, gu);
+    from_vec(b, gv);
+  });
+}
+
+int er_sge(void* h, const double* u, const double* v, double alpha, double beta, double gamma,
+           uint64_t seed, uint64_t stream, uint64_t offset, double* gu, double* gv) {
+  return guarded([&] {
+    const auto& A = *static_cast<ExplicitMatrix*>(h);
+    SeededRng rng(seed, stream);
+    for (uint64_t k = 0; k < offset; ++k) rng.next_u64();
+    Vec a, b;
+    stochastic_gradient_estimate(A, to_vec(u, A.rows()), to_vec(v, A.cols()),
+                                 mkparams(alpha, beta, gamma, 9.210340371976184), rng, a, b);
+    from_vec(a, gu);
+    from_vec(b, gv);
+  });
+}
+
 struct er_lsqr_out {
   double* x;
   double* residual_history;  // capacity given by caller

@@ -11,6 +11,8 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   ExplicitMatrix, InvalidArgument, IterationRecord, LassoProblem, LsqrRun,
                   ScalingResult, canon_sumsq_device, ccp_lasso, ccp_lasso_preconditioned,
                   lasso_objective, spectral_norm, det_exp_device, kernel_launches,
+                  SeededRng, gradient, gradient_weighted, objective, objective_weighted,
+                  project_box, rms_error, stochastic_gradient_estimate,
                   last_loop_ms, lsqr, lsqr_preconditioned, nccl_unique_id,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
                   sgd_equilibrate_block, sgd_equilibrate_symmetric, sgd_equilibrate_targets,
@@ -20,6 +22,8 @@ __all__ = [
     "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "BlockStructure",
     "CcpOptions", "CcpRun", "LassoProblem", "ccp_lasso", "ccp_lasso_preconditioned",
     "lasso_objective", "spectral_norm", "MatrixMarketData", "parse_matrix_market",
+    "SeededRng", "gradient", "gradient_weighted", "objective", "objective_weighted",
+    "project_box", "rms_error", "stochastic_gradient_estimate",
     "write_matrix_market_csr", "write_matrix_market_dense",
     "DiagnosticsConfig",
     "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",

@@ -116,6 +116,16 @@ SIGNATURES = {
     "equil_mm_free": (None, [C.c_void_p]),
     "equil_mm_write_csr": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _i64p, _i32p, _dp]),
     "equil_mm_write_dense": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _dp]),
+    "equil_objective": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params), _dp]),
+    "equil_objective_weighted": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, _dp]),
+    "equil_gradient": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params), _dp, _dp]),
+    "equil_gradient_weighted": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, _dp,
+                                          _dp]),
+    "equil_stochastic_gradient_estimate": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params),
+                                                     C.c_uint64, C.c_uint64, C.c_uint64, _dp,
+                                                     _dp]),
+    "equil_rms_error": (C.c_int, [C.c_void_p, _dp, _dp, C.c_double, C.c_double, _dp]),
+    "equil_project_box": (C.c_int, [_dp, C.c_int64, C.c_double, _dp]),
     "equil_lsqr": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_double, C.POINTER(LsqrOut)]),
     "equil_lsqr_preconditioned": (C.c_int, [C.c_void_p, _dp, C.POINTER(Params), C.c_int,
                                             C.c_double, C.POINTER(LsqrOut)]),

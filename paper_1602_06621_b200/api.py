@@ -544,6 +544,97 @@ def write_matrix_market_dense(path: str, values):
                                          L.ptr(a, L._dp)))
 
 
+class SeededRng:
+    """SeededRng (include/equil/rng.hpp:12-42) as a position in the (seed,
+    stream) output sequence; consumers advance it by the draws they use."""
+
+    def __init__(self, seed: int, stream: int):
+        self.seed, self.stream, self.position = int(seed), int(stream), 0
+
+
+def _vecs(op, u, v):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if u.size != op.rows() or v.size != op.cols():
+        raise InvalidArgument("objective: scaling length mismatch")
+    return u, v
+
+
+def objective(op: ExplicitMatrix, u, v, params: EquilibrationParams | None = None) -> float:
+    """objective (include/equil/equilibrate.hpp:23-24)."""
+    u, v = _vecs(op, u, v)
+    p = (params or EquilibrationParams())._c()
+    out = C.c_double(0.0)
+    _check(L.load().equil_objective(op._h, L.ptr(u, L._dp), L.ptr(v, L._dp), C.byref(p),
+                                    C.byref(out)))
+    return out.value
+
+
+def objective_weighted(op: ExplicitMatrix, u, v, lin_u, lin_v, gamma: float) -> float:
+    """objective_weighted (include/equil/equilibrate.hpp:35-36)."""
+    u, v = _vecs(op, u, v)
+    lu = np.ascontiguousarray(lin_u, dtype=np.float64)
+    lv = np.ascontiguousarray(lin_v, dtype=np.float64)
+    out = C.c_double(0.0)
+    _check(L.load().equil_objective_weighted(op._h, L.ptr(u, L._dp), L.ptr(v, L._dp),
+                                             L.ptr(lu, L._dp), L.ptr(lv, L._dp), float(gamma),
+                                             C.byref(out)))
+    return out.value
+
+
+def gradient(op: ExplicitMatrix, u, v, params: EquilibrationParams | None = None):
+    """gradient (include/equil/equilibrate.hpp:29-30) -> (grad_u, grad_v)."""
+    u, v = _vecs(op, u, v)
+    p = (params or EquilibrationParams())._c()
+    gu, gv = np.zeros(op.rows()), np.zeros(op.cols())
+    _check(L.load().equil_gradient(op._h, L.ptr(u, L._dp), L.ptr(v, L._dp), C.byref(p),
+                                   L.ptr(gu, L._dp), L.ptr(gv, L._dp)))
+    return gu, gv
+
+
+def gradient_weighted(op: ExplicitMatrix, u, v, lin_u, lin_v, gamma: float):
+    """gradient_weighted (include/equil/equilibrate.hpp:37-39)."""
+    u, v = _vecs(op, u, v)
+    lu = np.ascontiguousarray(lin_u, dtype=np.float64)
+    lv = np.ascontiguousarray(lin_v, dtype=np.float64)
+    gu, gv = np.zeros(op.rows()), np.zeros(op.cols())
+    _check(L.load().equil_gradient_weighted(op._h, L.ptr(u, L._dp), L.ptr(v, L._dp),
+                                            L.ptr(lu, L._dp), L.ptr(lv, L._dp), float(gamma),
+                                            L.ptr(gu, L._dp), L.ptr(gv, L._dp)))
+    return gu, gv
+
+
+def stochastic_gradient_estimate(op: ExplicitMatrix, u, v, params: EquilibrationParams,
+                                 rng: SeededRng):
+    """stochastic_gradient_estimate (include/equil/equilibrate.hpp:43-45):
+    consumes n + m draws of rng (s for the apply, then w for the adjoint)."""
+    u, v = _vecs(op, u, v)
+    p = params._c()
+    gu, gv = np.zeros(op.rows()), np.zeros(op.cols())
+    _check(L.load().equil_stochastic_gradient_estimate(
+        op._h, L.ptr(u, L._dp), L.ptr(v, L._dp), C.byref(p), rng.seed, rng.stream,
+        rng.position, L.ptr(gu, L._dp), L.ptr(gv, L._dp)))
+    rng.position += op.rows() + op.cols()
+    return gu, gv
+
+
+def rms_error(op: ExplicitMatrix, u, v, alpha: float, beta: float) -> float:
+    """rms_error (include/equil/metrics.hpp:14-15)."""
+    u, v = _vecs(op, u, v)
+    out = C.c_double(0.0)
+    _check(L.load().equil_rms_error(op._h, L.ptr(u, L._dp), L.ptr(v, L._dp), float(alpha),
+                                    float(beta), C.byref(out)))
+    return out.value
+
+
+def project_box(x, bound: float) -> np.ndarray:
+    """project_box (include/equil/equilibrate.hpp:48)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    _check(L.load().equil_project_box(L.ptr(x, L._dp), x.size, float(bound), L.ptr(out, L._dp)))
+    return out
+
+
 def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,
                            u_ptr: int, v_ptr: int, d_ptr: int, e_ptr: int) -> ScalingResult:
     """sgd_equilibrate with u, v, d, e written to caller-owned DEVICE buffers

@@ -2779,3 +2779,210 @@ equil_status equil_mm_write_dense(const char* path, int64_t m, int64_t n,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Public helpers of include/equil/equilibrate.hpp and metrics.hpp on the device
+// matrix: objective / gradient (weighted and plain), the one-sample stochastic
+// gradient estimate, rms_error, project_box.  Per-row sums follow CSR order
+// (A's rows for u, A^T's rows = ascending original rows for v); whole-vector
+// sums use the canonical reduction; exp is det_exp (the numerics contract).
+// Single GPU, sparse matrices (the estimate also takes dense ones).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct HelperCtx {
+  equil_matrix* M;
+  cudaStream_t s;
+  DevBuf<double> u, v, lu, lv, tm, tn;
+  HelperCtx(equil_matrix* m, const double* uh, const double* vh, const char* who,
+            bool need_csr = true)
+      : M(m), s(m->stream) {
+    require(M->world == 1, std::string(who) + ": single-GPU matrices only in this build");
+    require(!need_csr || !M->dense, std::string(who) + ": sparse matrices only in this build");
+    u.alloc(M->m);
+    v.alloc(M->n);
+    tm.alloc(M->m);
+    tn.alloc(M->n);
+    CK(cudaMemcpyAsync(u.p, uh, M->m * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(v.p, vh, M->n * 8, cudaMemcpyHostToDevice, s));
+  }
+  const double* upload_lin(DevBuf<double>& b, const double* h, int64_t len) {
+    if (!h) return nullptr;
+    b.alloc(len);
+    CK(cudaMemcpyAsync(b.p, h, len * 8, cudaMemcpyHostToDevice, s));
+    return b.p;
+  }
+};
+
+// objective_weighted (src/equilibrate.cpp:10-22); lin arrays null: constants
+double objective_dev(HelperCtx& c, const double* lin_u, double lu_c, const double* lin_v,
+                     double lv_c, double gamma) {
+  equil_matrix* M = c.M;
+  double* sc = M->scal.p + 52;
+  CK(eqb::launch_obj_terms(M->A, c.u.p, c.v.p, c.tm.p, c.s));
+  canon_reduce(M, c.tm.p, M->m, sc + 0, 1);
+  if (lin_u) {
+    CK(eqb::launch_mul(c.tm.p, lin_u, c.u.p, M->m, c.s));
+    canon_reduce(M, c.tm.p, M->m, sc + 1, 1);
+  } else {
+    canon_reduce(M, c.u.p, M->m, sc + 1, 2, lu_c);
+  }
+  if (lin_v) {
+    CK(eqb::launch_mul(c.tn.p, lin_v, c.v.p, M->n, c.s));
+    canon_reduce(M, c.tn.p, M->n, sc + 2, 1);
+  } else {
+    canon_reduce(M, c.v.p, M->n, sc + 2, 2, lv_c);
+  }
+  canon_reduce(M, c.u.p, M->m, sc + 3, 0);
+  canon_reduce(M, c.v.p, M->n, sc + 4, 0);
+  double r[5];
+  CK(cudaMemcpyAsync(r, sc, sizeof r, cudaMemcpyDeviceToHost, c.s));
+  CK(cudaStreamSynchronize(c.s));
+  return 0.5 * r[0] - r[1] - r[2] + 0.5 * gamma * (r[3] + r[4]);
+}
+
+// gradient_weighted (src/equilibrate.cpp:24-37)
+void gradient_dev(HelperCtx& c, const double* lin_u, double lu_c, const double* lin_v,
+                  double lv_c, double gamma, double* gu_h, double* gv_h) {
+  equil_matrix* M = c.M;
+  CK(eqb::launch_obj_terms(M->A, c.u.p, c.v.p, c.tm.p, c.s));   // sum_j a^2 e^{2(u_i+v_j)}
+  CK(eqb::launch_obj_terms(M->AT, c.v.p, c.u.p, c.tn.p, c.s));  // ascending i per column
+  CK(eqb::launch_grad_finish(c.tm.p, c.u.p, lin_u, lu_c, gamma, M->m, c.s));
+  CK(eqb::launch_grad_finish(c.tn.p, c.v.p, lin_v, lv_c, gamma, M->n, c.s));
+  CK(cudaMemcpyAsync(gu_h, c.tm.p, M->m * 8, cudaMemcpyDeviceToHost, c.s));
+  CK(cudaMemcpyAsync(gv_h, c.tn.p, M->n * 8, cudaMemcpyDeviceToHost, c.s));
+  CK(cudaStreamSynchronize(c.s));
+}
+
+}  // namespace
+
+extern "C" {
+
+equil_status equil_objective_weighted(equil_matrix* M, const double* u, const double* v,
+                                      const double* lin_u, const double* lin_v, double gamma,
+                                      double* out) {
+  return guarded([&] {
+    require(M && u && v && lin_u && lin_v && out, "objective: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    HelperCtx c(M, u, v, "objective");
+    const double* lu = c.upload_lin(c.lu, lin_u, M->m);
+    const double* lv = c.upload_lin(c.lv, lin_v, M->n);
+    *out = objective_dev(c, lu, 0.0, lv, 0.0, gamma);
+  });
+}
+
+equil_status equil_objective(equil_matrix* M, const double* u, const double* v,
+                             const equil_params* p, double* out) {
+  return guarded([&] {
+    require(M && u && v && p && out, "objective: null argument");
+    validate_params(*p);
+    double alpha = 0, beta = 0;
+    resolve_targets(*p, M->m, M->n, alpha, beta);
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    HelperCtx c(M, u, v, "objective");
+    *out = objective_dev(c, nullptr, alpha * alpha, nullptr, beta * beta, p->gamma);
+  });
+}
+
+equil_status equil_gradient_weighted(equil_matrix* M, const double* u, const double* v,
+                                     const double* lin_u, const double* lin_v, double gamma,
+                                     double* grad_u, double* grad_v) {
+  return guarded([&] {
+    require(M && u && v && lin_u && lin_v && grad_u && grad_v, "gradient: null argument");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    HelperCtx c(M, u, v, "gradient");
+    const double* lu = c.upload_lin(c.lu, lin_u, M->m);
+    const double* lv = c.upload_lin(c.lv, lin_v, M->n);
+    gradient_dev(c, lu, 0.0, lv, 0.0, gamma, grad_u, grad_v);
+  });
+}
+
+equil_status equil_gradient(equil_matrix* M, const double* u, const double* v,
+                            const equil_params* p, double* grad_u, double* grad_v) {
+  return guarded([&] {
+    require(M && u && v && p && grad_u && grad_v, "gradient: null argument");
+    validate_params(*p);
+    double alpha = 0, beta = 0;
+    resolve_targets(*p, M->m, M->n, alpha, beta);
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    HelperCtx c(M, u, v, "gradient");
+    gradient_dev(c, nullptr, alpha * alpha, nullptr, beta * beta, p->gamma, grad_u, grad_v);
+  });
+}
+
+// stochastic_gradient_estimate (src/equilibrate.cpp:60-71): the probes are
+// outputs [offset, offset + n + m) of SeededRng(seed, stream) (s then w)
+equil_status equil_stochastic_gradient_estimate(equil_matrix* M, const double* u,
+                                                const double* v, const equil_params* p,
+                                                uint64_t seed, uint64_t stream, uint64_t offset,
+                                                double* g_u, double* g_v) {
+  return guarded([&] {
+    require(M && u && v && p && g_u && g_v, "stochastic_gradient_estimate: null argument");
+    validate_params(*p);
+    double alpha = 0, beta = 0;
+    resolve_targets(*p, M->m, M->n, alpha, beta);
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    HelperCtx c(M, u, v, "stochastic_gradient_estimate", false);
+    const int64_t m = M->m, n = M->n;
+    const uint64_t total = offset + static_cast<uint64_t>(m + n);
+    DevBuf<uint32_t> bits;
+    DevBuf<unsigned char> scratch;
+    bits.alloc((total + 31) / 32 + 1);
+    const size_t sb = eqb::sign_stream_scratch_bytes(total);
+    scratch.alloc(sb);
+    CK(eqb::sign_stream_generate(seed, stream, total, bits.p, scratch.p, sb, c.s));
+    DevBuf<double> d, e, xs, xw;
+    d.alloc(m); e.alloc(n); xs.alloc(n); xw.alloc(m);
+    // d = exp(u), e = exp(v); xs = e .* s; xw = d .* w
+    CK(eqb::launch_expand_scale(c.v.p, nullptr, n, bits.p, static_cast<int64_t>(offset), e.p,
+                                xs.p, c.s));
+    CK(eqb::launch_expand_scale(c.u.p, nullptr, m, bits.p, static_cast<int64_t>(offset) + n,
+                                d.p, xw.p, c.s));
+    apply_pass(M, false, xs.p, c.tm.p, eqb::kPassEst, d.p, nullptr, nullptr);
+    apply_pass(M, true, xw.p, c.tn.p, eqb::kPassEst, e.p, nullptr, nullptr);
+    CK(eqb::launch_sge_finish(c.tm.p, c.u.p, -alpha * alpha, p->gamma, m, c.s));
+    CK(eqb::launch_sge_finish(c.tn.p, c.v.p, -beta * beta, p->gamma, n, c.s));
+    CK(cudaMemcpyAsync(g_u, c.tm.p, m * 8, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaMemcpyAsync(g_v, c.tn.p, n * 8, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaStreamSynchronize(c.s));
+  });
+}
+
+// rms_error (src/metrics.cpp:41-56)
+equil_status equil_rms_error(equil_matrix* M, const double* u, const double* v, double alpha,
+                             double beta, double* out) {
+  return guarded([&] {
+    require(M && u && v && out, "rms_error: null argument");
+    require(alpha > 0.0 && beta > 0.0, "rms_error: targets must be positive");
+    std::lock_guard<std::mutex> lk(M->mu);
+    DeviceGuard dg(M->device);
+    HelperCtx c(M, u, v, "rms_error");
+    DevBuf<double> terms;
+    terms.alloc(M->m + M->n);
+    CK(eqb::launch_exp(c.u.p, c.tm.p, M->m, 2.0, c.s));
+    CK(eqb::launch_exp(c.v.p, c.tn.p, M->n, 2.0, c.s));
+    CK(eqb::launch_rms_terms(0, M->A, c.tm.p, c.tn.p, terms.p, 0, alpha, c.s));
+    CK(eqb::launch_rms_terms(1, M->AT, c.tm.p, c.tn.p, terms.p + M->m, 0, beta, c.s));
+    canon_reduce(M, terms.p, M->m + M->n, M->scal.p + 58, 1);
+    *out = std::sqrt(read_scalar(M, M->scal.p + 58) / static_cast<double>(M->m + M->n));
+  });
+}
+
+// project_box (src/equilibrate.cpp:73-76), host
+equil_status equil_project_box(const double* x, int64_t n, double bound, double* out) {
+  return guarded([&] {
+    require(bound >= 0.0, "project_box: bound must be nonnegative");
+    require(n == 0 || (x && out), "project_box: null argument");
+    for (int64_t i = 0; i < n; ++i) {
+      const double lo = x[i] < -bound ? -bound : x[i];  // cwiseMax(-bound)
+      out[i] = bound < lo ? bound : lo;                  // cwiseMin(bound)
+    }
+  });
+}
+
+}  // extern "C"

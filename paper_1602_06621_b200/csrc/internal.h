@@ -303,6 +303,12 @@ cudaError_t launch_ccp_primal(double* z, double* ezt, const double* g, const dou
 cudaError_t launch_lasso_value(const double* r2, const double* l1, double sqrt_lambda,
                                double* out, cudaStream_t s);
 cudaError_t launch_abs(const double* x, int64_t n, double* out, cudaStream_t s);
+// g = est + (neg_lin + gamma x)  (stochastic_gradient_estimate, equilibrate.cpp:69-70)
+cudaError_t launch_sge_finish(double* g, const double* x, double neg_lin, double gamma,
+                              int64_t n, cudaStream_t s);
+// g = g + (gamma x - lin)  (gradient_weighted, equilibrate.cpp:35-36); lin null: lin_c
+cudaError_t launch_grad_finish(double* g, const double* x, const double* lin, double lin_c,
+                               double gamma, int64_t n, cudaStream_t s);
 
 // LSQR elementwise helpers
 cudaError_t launch_lsqr_normalize(double* dst, const double* src,

@@ -120,6 +120,22 @@ __global__ void abs_kernel(const double* __restrict__ x, int64_t n, double* __re
   if (j < n) out[j] = fabs(x[j]);
 }
 
+// stochastic_gradient_estimate (src/equilibrate.cpp:69-70): g = est + (neg_lin + gamma * x)
+__global__ void sge_finish_kernel(double* __restrict__ g, const double* __restrict__ x,
+                                  double neg_lin, double gamma, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) g[i] = __dadd_rn(g[i], __dadd_rn(neg_lin, __dmul_rn(gamma, x[i])));
+}
+
+// gradient_weighted (src/equilibrate.cpp:35-36): g = g + (gamma * x - lin_i)
+__global__ void grad_finish_kernel(double* __restrict__ g, const double* __restrict__ x,
+                                   const double* __restrict__ lin, double lin_c, double gamma,
+                                   int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n)
+    g[i] = __dadd_rn(g[i], __dsub_rn(__dmul_rn(gamma, x[i]), lin ? lin[i] : lin_c));
+}
+
 unsigned grid(int64_t n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
@@ -179,6 +195,22 @@ cudaError_t launch_ccp_primal(double* z, double* ezt, const double* g, const dou
 cudaError_t launch_lasso_value(const double* r2, const double* l1, double sqrt_lambda,
                                double* out, cudaStream_t s) {
   lasso_value_kernel<<<1, 1, 0, s>>>(r2, l1, sqrt_lambda, out);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sge_finish(double* g, const double* x, double neg_lin, double gamma,
+                              int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  sge_finish_kernel<<<grid(n), 256, 0, s>>>(g, x, neg_lin, gamma, n);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grad_finish(double* g, const double* x, const double* lin, double lin_c,
+                               double gamma, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  grad_finish_kernel<<<grid(n), 256, 0, s>>>(g, x, lin, lin_c, gamma, n);
   count_launch(s);
   return cudaGetLastError();
 }

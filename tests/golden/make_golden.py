@@ -161,6 +161,21 @@ def main():
             g[f"{key}_{tag}_meta"] = np.array([r.iterations, r.equil_iterations, r.reached_tol,
                                                r.apply_count, r.adjoint_count])
             g[f"{key}_{tag}_steps"] = np.array([r.tau, r.sigma, r.theta])
+    # equilibrate.hpp / metrics.hpp helpers at a fixed (u, v): objective, gradient,
+    # rms_error (std::exp and sequential sums: tolerance references) and the
+    # stochastic gradient estimate (bit-exact reference)
+    for key in ["sp", "dn"]:
+        A = cases[key]
+        RM = R.matrix(A)
+        rng = np.random.default_rng(17)
+        u, v = 0.3 * rng.standard_normal(A.m), 0.3 * rng.standard_normal(A.n)
+        g[f"{key}_hu"], g[f"{key}_hv"] = u, v
+        g[f"{key}_hobj"] = np.array([RM.objective(u, v), RM.objective(u, v, 0.9, 0.0, 0.3)])
+        gu, gv = RM.gradient(u, v)
+        g[f"{key}_hgu"], g[f"{key}_hgv"] = gu, gv
+        g[f"{key}_hrms"] = np.array([RM.rms_error(u, v, 0.7, 1.1)])
+        su, sv = RM.stochastic_gradient_estimate(u, v, 7, 17, 123)
+        g[f"{key}_hsu"], g[f"{key}_hsv"] = su, sv
     np.savez_compressed(OUT, **g)
     print(OUT, os.path.getsize(OUT), "bytes")
 

@@ -626,3 +626,41 @@ def test_matrix_market_and_binary_ingest_on_device(C, golden, tmp_path):
     p.write_text("".join(dup))
     with pytest.raises(eq.EquilRuntimeError, match=r"line 7: duplicate entry \(1, 2\)"):
         eq.ExplicitMatrix.read_matrix_market(str(p))
+
+
+# ---------------------------------------------------------------- public helpers
+@pytest.mark.parametrize("key", ["sp", "dn"])
+def test_equilibrate_helpers_vs_reference_golden(golden, key):
+    """stochastic_gradient_estimate (src/equilibrate.cpp:60-71) bit-exact on the
+    device; objective / gradient (:10-57) and rms_error (metrics.cpp:41-56) to
+    1e-12 relative (the reference uses std::exp and plain sequential sums)."""
+    A = csr_from_golden(golden, key)
+    M = device_matrix(A)
+    u, v = golden[f"{key}_hu"], golden[f"{key}_hv"]
+    rng = eq.SeededRng(7, 17)
+    rng.position = 123
+    su, sv = eq.stochastic_gradient_estimate(M, u, v, eq.EquilibrationParams(), rng)
+    assert np.array_equal(su, golden[f"{key}_hsu"]) and np.array_equal(sv, golden[f"{key}_hsv"])
+    assert rng.position == 123 + A.m + A.n
+    if A.dense is not None:
+        with pytest.raises(eq.InvalidArgument, match="sparse matrices only"):
+            eq.objective(M, u, v)
+        return
+    obj = eq.objective(M, u, v)
+    assert obj == pytest.approx(golden[f"{key}_hobj"][0], rel=1e-12)
+    obj2 = eq.objective(M, u, v, eq.EquilibrationParams(alpha=0.9, gamma=0.3))
+    assert obj2 == pytest.approx(golden[f"{key}_hobj"][1], rel=1e-12)
+    gu, gv = eq.gradient(M, u, v)
+    np.testing.assert_allclose(gu, golden[f"{key}_hgu"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(gv, golden[f"{key}_hgv"], rtol=1e-12, atol=1e-12)
+    assert eq.rms_error(M, u, v, 0.7, 1.1) == pytest.approx(golden[f"{key}_hrms"][0], rel=1e-12)
+    al, be = eq.resolve_targets(eq.EquilibrationParams(), A.m, A.n)
+    w = eq.objective_weighted(M, u, v, np.full(A.m, al * al), np.full(A.n, be * be), 0.1)
+    assert w == pytest.approx(obj, rel=1e-14)
+    gw = eq.gradient_weighted(M, u, v, np.full(A.m, al * al), np.full(A.n, be * be), 0.1)
+    assert np.array_equal(gw[0], gu) and np.array_equal(gw[1], gv)
+    assert np.array_equal(eq.project_box(np.array([-3.0, 0.5, 2.0]), 1.0), [-1.0, 0.5, 1.0])
+    with pytest.raises(eq.InvalidArgument, match="bound must be nonnegative"):
+        eq.project_box(np.zeros(2), -1.0)
+    with pytest.raises(eq.InvalidArgument, match="targets must be positive"):
+        eq.rms_error(M, u, v, 0.0, 1.0)

@@ -299,3 +299,18 @@ def test_oracle_ccp_known_answers(C):
         C.ccp_lasso(A, np.zeros(10), 0.1, max_iters=5)
     with pytest.raises(oracle.OracleError, match="max_iters must be nonnegative"):
         C.ccp_lasso(A, bb, 0.1, max_iters=-1)
+
+
+@pytest.mark.parametrize("key", ["sp", "dn"])
+def test_oracle_helpers_match_reference_golden(C, golden, key):
+    """stochastic_gradient_estimate (src/equilibrate.cpp:60-71) bit-exact; the
+    objective and rms_error restatements to 1e-12 (the reference uses std::exp
+    and plain sequential sums, src/equilibrate.cpp:10-22, metrics.cpp:24-56)."""
+    A = csr_from_golden(golden, key)
+    u, v = golden[f"{key}_hu"], golden[f"{key}_hv"]
+    su, sv = C.stochastic_gradient_estimate(A, u, v, 7, 17, 123)
+    assert np.array_equal(su, golden[f"{key}_hsu"]) and np.array_equal(sv, golden[f"{key}_hsv"])
+    a2 = (A.n / A.m) ** 0.5  # alpha^2 for auto targets
+    obj = C.objective(A, u, v, a2, (A.m / A.n) ** 0.5, 0.1)
+    assert obj == pytest.approx(golden[f"{key}_hobj"][0], rel=1e-12)
+    assert C.rms_error(A, u, v, 0.7, 1.1) == pytest.approx(golden[f"{key}_hrms"][0], rel=1e-12)
