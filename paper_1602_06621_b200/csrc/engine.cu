@@ -321,8 +321,8 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   // rows (kind 3), each replicated once per warp of the CTA
   std::stable_sort(longs.begin(), longs.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-  for (size_t q = 0; q < longs.size(); q += eqb::kSliceRows) {
-    const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, longs.size() - q));
+  for (size_t q = 0; q < longs.size(); q += eqb::kLongRows) {
+    const int cnt = static_cast<int>(std::min<size_t>(eqb::kLongRows, longs.size() - q));
     const eqb::Tile t{static_cast<int32_t>(P.rowlist.size()), cnt, 3,
                       static_cast<int16_t>(mat), 0};
     for (int k = 0; k < cnt; ++k) P.rowlist.push_back(static_cast<int32_t>(longs[q + k].second));

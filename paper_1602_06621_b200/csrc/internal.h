@@ -56,6 +56,12 @@ struct __align__(16) RowMeta {
 constexpr int kLongChunk = EQ_LONG_CHUNK;      // products per row per round (kind 3)
 constexpr int kLongStride = kLongChunk + 2;    // padded stride: conflict-free LDS.128
 constexpr int kLongBatch = EQ_LONG_BATCH;  // rows per staging batch per warp
+#ifndef EQ_LONG_ROWS
+#define EQ_LONG_ROWS 32
+#endif
+constexpr int kLongRows = EQ_LONG_ROWS;  // rows per CTA-cooperative long slice
+static_assert(kLongRows <= 32 && kLongRows * kLongStride <= kTileWarps * kWarpSmem,
+              "long slice staging must fit the CTA's buffers");
 struct SliceMeta {
   RowMeta r[32];
   int maxr;  // long slices: rounds of the longest row
