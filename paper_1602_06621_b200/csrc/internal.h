@@ -10,11 +10,10 @@
 
 namespace eqb {
 
-// Sparse traversal tile, one per warp.  kind 0: rows [r0, r1) fully inside one
-// tile (nnz <= kTileNnz); kind 1: a single long row r0 streamed in kTileNnz
-// chunks; kind 2: a slice of r1 (<= 32) rows listed at rowlist[r0 ...], sorted
-// by length (longest first), summed one row per lane in lock-step chunks.
-// mat 0 = A (u block), mat 1 = A^T (v block).
+// Sparse traversal tile.  kind 2 (one warp): a slice of r1 (<= 32) rows listed
+// at rowlist[r0 ...], sorted by length (longest first), summed one row per lane
+// in lock-step chunks.  kind 3 (one CTA): a long slice of r1 rows longer than
+// kTileNnz, staged cooperatively.  mat 0 = A (u block), mat 1 = A^T (v block).
 struct Tile {
   int32_t r0, r1;
   int16_t kind, mat;
@@ -67,7 +66,6 @@ struct SliceMeta {
   int maxr;  // long slices: rounds of the longest row
 };
 constexpr int kTileMinBlocks = 6;   // 24 warps/SM: <= 80 registers (no spills)
-constexpr int kStageUnroll = 4;     // independent loads in flight per lane
 
 // CSR slice resident on the device (int64 row_ptr, int32 col, fp64 val).
 struct DevCsr {

@@ -545,11 +545,9 @@ cudaError_t coo_to_csr(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
 // ---------------------------------------------------------------------------
 namespace {
 
-// One warp runs one tile; warps never wait on each other, so on an SM the
-// memory-bound staging of some warps overlaps the latency-bound sequential
-// chains of others.  kind 0: every lane sums whole rows of the tile; kind 1: a
-// row longer than a tile is staged chunk by chunk and lane 0 carries the
-// running sum across chunks (the order stays the CSR order).
+// kind 2 (run_tile): one warp runs one slice; warps never wait on each other,
+// so on an SM the memory-bound staging of some warps overlaps the
+// latency-bound sequential chains of others.
 //
 // kind 3 (run_long_slice) is CTA-cooperative: the 4 warps of a CTA own the same
 // "long slice" of up to 32 rows longer than kTileNnz (length-sorted).  Each
@@ -631,7 +629,7 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
                                          const double* __restrict__ xg,
                                          const int32_t* __restrict__ rowlist, double* sp,
                                          SliceMeta& sm, int lane, Epi& epi) {
-  if (t.kind == 2) {
+  {
     // Slice: up to 32 rows (sorted by length, longest first), one per lane, in
     // lock-step rounds of kSliceChunk products per row.  Each round the warp
     // stages the rows' next chunks with coalesced half-warp loads into a padded
@@ -698,25 +696,6 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
       __syncwarp();
     }
     if (myrow >= 0) epi(myrow, acc);
-  } else if (t.kind == 0) {
-    const int64_t k0 = rp[t.r0], k1 = rp[t.r1];
-    warp_stage(ci, va, xg, k0, k1, sp, lane);
-    __syncwarp();
-    for (int64_t r = t.r0 + lane; r < t.r1; r += 32)
-      epi(r, chain_sum(0.0, sp, static_cast<int>(rp[r] - k0),
-                       static_cast<int>(rp[r + 1] - k0)));
-  } else {
-    const int64_t r = t.r0;
-    const int64_t k0 = rp[r], k1 = rp[r + 1];
-    double acc = 0.0;
-    for (int64_t cb = k0, ce; cb < k1; cb = ce) {  // chunks aligned to kTileNnz
-      ce = imin64(k1, (cb & ~static_cast<int64_t>(kTileNnz - 1)) + kTileNnz);
-      warp_stage(ci, va, xg, cb, ce, sp, lane);
-      __syncwarp();
-      if (lane == 0) acc = chain_sum(acc, sp, 0, static_cast<int>(ce - cb));
-      __syncwarp();
-    }
-    if (lane == 0) epi(r, acc);
   }
 }
 
@@ -727,7 +706,7 @@ struct SgdEpi {
   __device__ void operator()(int64_t r, double acc) { sgd_epilogue(a, mat, r, acc, fl); }
 };
 
-// KINDS: bit 0 = warp tiles (kinds 0-2), bit 1 = CTA long slices (kind 3);
+// KINDS: bit 0 = warp slices (kind 2), bit 1 = CTA long slices (kind 3);
 // tile_base offsets into the tile list (for launches over a sub-range).
 template <int MINB, int KINDS>
 __global__ void __launch_bounds__(kTileThreads, MINB)
@@ -867,34 +846,9 @@ cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* m
 
 cudaError_t launch_sgd_iter(const SgdIterArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  // occupancy variant (CTAs/SM bound); EQUIL_MINB selects one for tuning runs
-  // tuning knobs (development): EQUIL_SPLIT=1 launches the CTA long slices and
-  // the warp tiles as two kernels with their own occupancy points
-  static const int split = getenv("EQUIL_SPLIT") ? atoi(getenv("EQUIL_SPLIT")) : 0;
-  static const int minb_s = getenv("EQUIL_MINB_S") ? atoi(getenv("EQUIL_MINB_S")) : 8;
-  static const int minb_l = getenv("EQUIL_MINB_L") ? atoi(getenv("EQUIL_MINB_L")) : 6;
-  auto grid = [](int n) { return static_cast<unsigned>((n + kTileWarps - 1) / kTileWarps); };
-  if (!split || a.n_long == 0 || a.n_long == ntiles) {
-    sgd_iter_kernel<kTileMinBlocks, 3><<<grid(ntiles), kTileThreads, 0, s>>>(a, 0, ntiles);
-    count_launch(s);
-    return cudaGetLastError();
-  }
-  const int nl = a.n_long, ns = ntiles - a.n_long;
-  if (minb_l >= 8)
-    sgd_iter_kernel<8, 2><<<grid(nl), kTileThreads, 0, s>>>(a, 0, nl);
-  else if (minb_l <= 4)
-    sgd_iter_kernel<4, 2><<<grid(nl), kTileThreads, 0, s>>>(a, 0, nl);
-  else
-    sgd_iter_kernel<6, 2><<<grid(nl), kTileThreads, 0, s>>>(a, 0, nl);
-  if (minb_s >= 12)
-    sgd_iter_kernel<12, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
-  else if (minb_s >= 10)
-    sgd_iter_kernel<10, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
-  else if (minb_s >= 8)
-    sgd_iter_kernel<8, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
-  else
-    sgd_iter_kernel<6, 1><<<grid(ns), kTileThreads, 0, s>>>(a, nl, ns);
-  count_launch(s, 2);
+  const unsigned g = static_cast<unsigned>((ntiles + kTileWarps - 1) / kTileWarps);
+  sgd_iter_kernel<kTileMinBlocks, 3><<<g, kTileThreads, 0, s>>>(a, 0, ntiles);
+  count_launch(s);
   return cudaGetLastError();
 }
 

@@ -23,35 +23,6 @@ __device__ __forceinline__ bool sign_bit(const uint32_t* bits, int64_t b) {
   return (__ldg(bits + (b >> 5)) >> (b & 31)) & 1u;
 }
 
-// Products p[k - k0] = val[k] * xg[col[k]] for k in [k0, k1), one warp,
-// coalesced streaming loads of val/col, gathers through the read-only path.
-// The product is one rounded multiply whoever computes it, so staging it in
-// any order leaves the sequential sum below bit-identical to the reference.
-__device__ __forceinline__ void warp_stage(const int32_t* __restrict__ ci,
-                                           const double* __restrict__ va,
-                                           const double* __restrict__ xg,
-                                           int64_t k0, int64_t k1,
-                                           double* __restrict__ sp, int lane) {
-  constexpr int U = kStageUnroll;
-  for (int64_t kb = k0 + lane; kb < k1; kb += 32 * U) {
-    int32_t c[U];
-    double v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = kb + 32 * u;
-      if (k < k1) {
-        c[u] = __ldcs(ci + k);
-        v[u] = __ldcs(va + k);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = kb + 32 * u;
-      if (k < k1) sp[k - k0] = __dmul_rn(v[u], __ldg(xg + c[u]));
-    }
-  }
-}
-
 // Sequential CSR-order sum of sp[b, e) onto acc (explicit_matrix.cpp:73-75).
 // The adds form one dependent chain; the shared-memory loads feeding it are
 // software-pipelined 8 products ahead (16-byte LDS) so the chain runs at add
