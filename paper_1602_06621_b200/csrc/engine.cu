@@ -1,271 +1,15 @@
-// engine.cu -- host engine and C ABI (include/equil_b200.h).
+// engine.cu -- host engine and C ABI (include/equil_b200.h): matrix creation
+// and sharding, traversal plans, the SGD driver and LSQR.
 //
 // Owns the device-resident matrix (CSR(A), CSR(A^T) shards or dense A), the
 // traversal plans, the sign stream and the SGD / LSQR drivers.  The T-iteration
 // SGD loop is captured once as a CUDA graph per (T, targets, gamma, M) and
 // replayed; LSQR keeps its scalar recurrence on the host (std::hypot, exactly
-// as src/lsqr.cpp:58-64) with one device->host round trip per iteration.
-#include <cuda_runtime.h>
-#include <dlfcn.h>
+// as src/lsqr.cpp:58-64) with one device->host round trip per norm.  The
+// variants, the lasso, the public helpers and file I/O are in engine_ext.cu.
+#include "engine_internal.h"
 
-#include <algorithm>
-#include <chrono>
-#include <cmath>
-#include <cstdio>
-#include <cstring>
-#include <memory>
-#include <mutex>
-#include <new>
-#include <stdexcept>
-#include <string>
-#include <thread>
-#include <vector>
-
-#include "../../include/equil_b200.h"
-#include "internal.h"
-#include "mmio.h"
-#include "mt64_host.h"
-
-// ---------------------------------------------------------------------------
-// NCCL, resolved at run time (the process that drives us -- e.g. torch -- has
-// usually loaded libnccl.so.2 already; dlopen then returns that copy).
-// ---------------------------------------------------------------------------
-namespace {
-typedef struct ncclComm* ncclComm_t;
-typedef struct {
-  char internal[128];
-} ncclUniqueId;
-typedef int ncclResult_t;
-constexpr int ncclUint8 = 1, ncclUint32 = 3, ncclFloat64 = 8, ncclMax = 2;
-
-struct NcclApi {
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-  bool ok = false;
-};
-
-NcclApi& nccl() {
-  static NcclApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* nm : names) {
-      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
-      if (api.h) break;
-    }
-    if (!api.h) return;
-    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
-    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.h, "ncclCommInitRank"));
-    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
-    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
-    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
-    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
-             api.AllReduce;
-  });
-  return api;
-}
-
-thread_local std::string g_err;
-
-struct Fail {
-  equil_status code;
-  std::string msg;
-};
-
-[[noreturn]] void fail(equil_status c, const std::string& m) { throw Fail{c, m}; }
-void require(bool c, const std::string& m) {
-  if (!c) fail(EQUIL_EINVAL, m);
-}
-void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    fail(e == cudaErrorMemoryAllocation ? EQUIL_ENOMEM : EQUIL_ECUDA,
-         std::string(what) + ": " + cudaGetErrorString(e));
-  }
-}
-#define CK(x) cuda_check((x), #x)
-void nccl_check(ncclResult_t r, const char* what) {
-  if (r != 0) {
-    const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
-    fail(EQUIL_ENCCL, std::string(what) + ": " + s);
-  }
-}
-
-template <class F>
-equil_status guarded(F&& f) {
-  try {
-    f();
-    return EQUIL_OK;
-  } catch (const Fail& e) {
-    g_err = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    g_err = "out of host memory";
-    return EQUIL_ENOMEM;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return EQUIL_ERUNTIME;
-  }
-}
-
-// EQUIL_VERBOSE=1: per-phase wall times of setup calls (synchronizing; debug only)
-struct PhaseTimer {
-  const char* what;
-  bool on;
-  std::chrono::steady_clock::time_point t;
-  explicit PhaseTimer(const char* w)
-      : what(w), on(getenv("EQUIL_VERBOSE") != nullptr), t(std::chrono::steady_clock::now()) {}
-  void mark(cudaStream_t s, const char* phase) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[equil] %s %-14s %8.2f ms\n", what, phase,
-            std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
-
-// Device buffers come from the device's stream-ordered memory pool (release
-// threshold kept at max), allocated on a private per-device stream and made
-// visible before use, so repeated matrix setups reuse already-mapped memory
-// instead of paying cudaMalloc / cudaFree page mapping every time.  Release
-// keeps cudaFree's semantics: the device is synchronised before the memory goes
-// back to the pool.
-cudaStream_t alloc_stream(int dev) {
-  static std::mutex mu;
-  static cudaStream_t streams[64] = {};
-  std::lock_guard<std::mutex> lk(mu);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-    cudaGetLastError();
-  }
-  return streams[dev];
-}
-
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  int dev = -1;         // >= 0: pool allocation on alloc_stream(dev)
-  void alloc(size_t count) {
-    release();
-    if (count == 0) count = 1;
-    int d = 0;
-    CK(cudaGetDevice(&d));
-    cudaStream_t s = alloc_stream(d);
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
-    CK(cudaStreamSynchronize(s));
-    dev = d;
-    n = count;
-  }
-  void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'ed array
-    release();
-    p = q;
-    n = count;
-    dev = -1;
-  }
-  void ensure(size_t count) {
-    if (count > n || !p) alloc(count);
-  }
-  void release() {
-    if (p) {
-      if (dev >= 0) {
-        int cur = 0;
-        cudaGetDevice(&cur);
-        if (cur != dev) cudaSetDevice(dev);
-        cudaDeviceSynchronize();  // like cudaFree: nothing may still use p
-        cudaFreeAsync(p, alloc_stream(dev));
-        if (cur != dev) cudaSetDevice(cur);
-      } else {
-        cudaFree(p);
-      }
-    }
-    p = nullptr;
-    n = 0;
-    dev = -1;
-  }
-  void swap(DevBuf& o) {
-    std::swap(p, o.p);
-    std::swap(n, o.n);
-    std::swap(dev, o.dev);
-  }
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() { release(); }
-};
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) CK(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-// ---- params (src/params.cpp:7-44) -----------------------------------------
-void resolve_targets(const equil_params& p, int64_t rows, int64_t cols,
-                     double& alpha, double& beta) {
-  require(rows > 0 && cols > 0, "resolve_targets: dimensions must be positive");
-  require(p.alpha >= 0.0 && p.beta >= 0.0,
-          "resolve_targets: targets must be positive (or 0 for auto)");
-  const double m = static_cast<double>(rows);
-  const double n = static_cast<double>(cols);
-  alpha = p.alpha;
-  beta = p.beta;
-  if (alpha == 0.0 && beta == 0.0) {
-    alpha = std::pow(n / m, 0.25);
-    beta = std::pow(m / n, 0.25);
-  } else if (beta == 0.0) {
-    beta = alpha * std::sqrt(m / n);
-  } else if (alpha == 0.0) {
-    alpha = beta * std::sqrt(n / m);
-  } else {
-    const double lhs = m * alpha * alpha;
-    const double rhs = n * beta * beta;
-    require(std::abs(lhs - rhs) <= 1e-8 * std::max(lhs, rhs),
-            "resolve_targets: m*alpha^2 == n*beta^2 violated");
-  }
-}
-
-void validate_params(const equil_params& p) {
-  require(p.gamma > 0.0, "params: gamma must be positive");
-  require(p.max_log_scale > 0.0, "params: max_log_scale must be positive");
-  require(p.iterations >= 0, "params: iterations must be nonnegative");
-  require(std::isfinite(p.gamma) && std::isfinite(p.max_log_scale),
-          "params: gamma and max_log_scale must be finite");
-}
-
-// ---- traversal plan ---------------------------------------------------------
-// Rows longer than kTileNnz become kind-3 long slices (32 length-sorted rows
-// per CTA); all other rows are grouped into kind-2 slices: within windows of
-// kSliceWindow consecutive rows, rows are sorted by length (longest first) and
-// cut into groups of 32, so the lanes of a slice have similar chain lengths and
-// the epilogue's scattered writes stay inside one window.  The row order never
-// affects results: each row is an independent sequential sum.  Windows are
-// planned in parallel host threads; the result does not depend on the thread
-// count (parts are concatenated in window order, ties keep row order).
-struct Plan {
-  std::vector<eqb::Tile> lng, slices;
-  std::vector<int32_t> rowlist;
-};
+namespace eqe {
 
 Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   Plan P;
@@ -372,109 +116,9 @@ __global__ void unpad_kernel(double* dst, const double* src, const int64_t* boun
   dst[k] = src[g * maxcnt + (k - bounds[g])];
 }
 
-}  // namespace
+}  // namespace eqe
 
-// ---------------------------------------------------------------------------
-struct equil_matrix {
-  int device = 0, rank = 0, world = 1;
-  bool dense = false;
-  int64_t m = 0, n = 0, nnz = 0;
-  cudaStream_t stream = nullptr;
-  cudaStream_t copy_stream = nullptr;  // uploads that overlap work on `stream`
-  cudaEvent_t ev_vals = nullptr;       // values of A on the device
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  std::mutex mu;
-  ncclComm_t comm = nullptr;
-
-  // sparse shards (local rows, columns in padded coordinates)
-  eqb::DevCsr A, AT;
-  DevBuf<int64_t> a_rp, t_rp;
-  DevBuf<int32_t> a_ci, t_ci;
-  DevBuf<double> a_va, t_va;
-  std::vector<int64_t> a_bounds, t_bounds;  // partitions of rows / columns
-  int64_t a_max = 0, t_max = 0;             // padded slice sizes
-  DevBuf<int64_t> a_bounds_d, t_bounds_d;
-  DevBuf<eqb::Tile> tiles_sgd, tiles_a, tiles_t;
-  DevBuf<int32_t> rowlist_a, rowlist_t;
-  int n_sgd = 0, n_a = 0, n_t = 0;
-  int n_sgd_long = 0;  // leading kind-3 entries of tiles_sgd
-  // column-panel layout of the local A / A^T shards (panel.cu), built when
-  // EQUIL_PANEL=1 at creation; n_pbands == 0 selects the row-slice traversal
-  // above (the default: faster on B200)
-  bool use_panels = false;
-  // hot-first slot layout of the gathered vectors (build_slot_layout): the SGD
-  // passes read CSR copies whose column indices point at slots, and the
-  // epilogues write each row's next value at its slot
-  bool use_slots = true;
-  bool slots = false;
-  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wmap, smap;  // wmap / smap: padded position -> slot
-  DevBuf<double> pval[2];
-  DevBuf<uint16_t> pcol[2];
-  DevBuf<uint32_t> pruns[2];
-  DevBuf<eqb::PanelChunk> pchunks[2];
-  DevBuf<eqb::PanelBand> pbands;
-  int n_pbands = 0;
-
-  // dense
-  DevBuf<double> Ad, colpart;
-
-  // workspaces
-  // padded gathered vectors e.*s (xs) and d.*w (xw), double-buffered, in one
-  // allocation so a single L2 persisting window covers every gather target
-  struct Slot {
-    double* p = nullptr;
-  } xs[2], xw[2];
-  DevBuf<double> xbuf;
-  DevBuf<double> u, ub, v, vb;  // local
-  DevBuf<uint32_t> signs;
-  DevBuf<unsigned char> sign_scratch;
-  DevBuf<unsigned> flags;
-  DevBuf<double> red_part;
-  DevBuf<unsigned> red_counter;
-  DevBuf<double> scal;  // small device scalars
-  DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
-  DevBuf<double> lin_u, lin_v;  // per-coordinate targets (sgd_equilibrate_targets)
-
-  // graph cache for the SGD loop
-  cudaGraphExec_t graph = nullptr;
-  long long graph_launches = 0;  // kernel nodes per replay
-  struct Key {
-    int T = -1;
-    double alpha = 0, beta = 0, gamma = 0, M = 0;
-    bool vec_lin = false;
-    bool operator==(const Key& o) const {
-      return T == o.T && alpha == o.alpha && beta == o.beta && gamma == o.gamma && M == o.M &&
-             vec_lin == o.vec_lin;
-    }
-  } graph_key;
-
-  int64_t m_loc() const { return dense ? m : a_bounds[rank + 1] - a_bounds[rank]; }
-  int64_t n_loc() const { return dense ? n : t_bounds[rank + 1] - t_bounds[rank]; }
-  int64_t a_goff() const { return dense ? 0 : a_bounds[rank]; }
-  int64_t t_goff() const { return dense ? 0 : t_bounds[rank]; }
-  int64_t m_pad() const { return world == 1 ? m : a_max * world; }
-  int64_t n_pad() const { return world == 1 ? n : t_max * world; }
-
-  // events bracketing the T-iteration loop of the last sgd call (also inside
-  // the captured graph), for the live per-kernel roofline in bench.py
-  cudaEvent_t ev_loop0 = nullptr, ev_loop1 = nullptr;
-  double last_loop_ms = 0.0;
-  int last_loop_iters = 0;
-
-  ~equil_matrix() {
-    if (ev_loop0) cudaEventDestroy(ev_loop0);
-    if (ev_loop1) cudaEventDestroy(ev_loop1);
-    if (graph) cudaGraphExecDestroy(graph);
-    if (comm && nccl().ok) nccl().CommDestroy(comm);
-    if (ev_vals) cudaEventDestroy(ev_vals);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (copy_stream) cudaStreamDestroy(copy_stream);
-    if (stream) cudaStreamDestroy(stream);
-  }
-};
-
-namespace {
+namespace eqe {
 
 void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   M->device = cfg ? cfg->device : 0;
@@ -845,7 +489,7 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   if (M->dense) M->colpart.alloc(((M->m + eqb::kChunk - 1) / eqb::kChunk) * M->n);
 }
 
-}  // namespace
+}  // namespace eqe
 
 // ===========================================================================
 // C ABI
@@ -984,7 +628,7 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
 
 }  // extern "C"
 
-namespace {
+namespace eqe {
 // ExplicitMatrix::sparse on the device.  With `lines` (Matrix Market ingest)
 // a duplicate is reported the way read_matrix_market does
 // (src/matrix_market.cpp:142-158): at the line of the later occurrence.
@@ -1053,7 +697,7 @@ void create_coo_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
     *out = M.release();
   }
 }
-}  // namespace
+}  // namespace eqe
 
 extern "C" {
 
@@ -1128,7 +772,7 @@ equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
 // ---------------------------------------------------------------------------
 // SGD driver
 // ---------------------------------------------------------------------------
-namespace {
+namespace eqe {
 
 struct DiagPlan {
   int stride = 0;
@@ -1138,14 +782,14 @@ struct DiagPlan {
 // canonical reduction of x[0, len) into *out (device): kind 0 sum of squares,
 // 1 plain sum, 2 sum of coef * x; optional sqrt of the result
 void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, int kind,
-                  double coef = 0.0, bool sqrt_out = false) {
+                  double coef, bool sqrt_out) {
   CK(eqb::launch_canon_reduce(x, len, kind, coef, M->red_part.p, M->red_counter.p, out,
                               sqrt_out ? 1 : 0, M->stream));
 }
 
-}  // namespace
+}  // namespace eqe
 
-namespace {
+namespace eqe {
 
 // internal::sgd_row_col (src/equilibrate.cpp:138-210).  Uniform targets
 // (lin = alpha^2, beta^2) when lin_u_host / lin_v_host are null, otherwise the
@@ -1580,7 +1224,7 @@ double canon_sum_host(const double* x, int64_t len) {
   return s[0];
 }
 
-}  // namespace
+}  // namespace eqe
 
 extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_params* p,
                                               const equil_diag_cfg* diag,
@@ -1616,7 +1260,7 @@ extern "C" equil_status equil_sgd_equilibrate_targets(equil_matrix* M, const dou
 // LSQR (src/lsqr.cpp:17-138).  Device vectors, canonical norms, host scalar
 // recurrence with std::hypot.
 // ---------------------------------------------------------------------------
-namespace {
+namespace eqe {
 
 // one matvec pass of B (scaled by scale when non-null) in the given mode
 void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
@@ -1880,7 +1524,7 @@ void lsqr_common(equil_matrix* M, const double* b, const equil_params* p, int ma
   out->adjoint_count = st.adjoints;
 }
 
-}  // namespace
+}  // namespace eqe
 
 extern "C" {
 
@@ -2002,987 +1646,3 @@ equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_
 
 }  // extern "C"
 
-// ---------------------------------------------------------------------------
-// Engine variants (src/variants.cpp): symmetric (:35-103) and block
-// (:156-240) equilibration.  Same sign stream, the same projected-SGD update
-// (run_projected_sgd) and the same estimator arithmetic as sgd_row_col, but
-// the passes run as generic pass kernels (kPassEst) between small kernels that
-// form the scalings, sum estimates over blocks and update the block iterates.
-// Single GPU; sparse and dense matrices (history for sparse ones).
-// ---------------------------------------------------------------------------
-namespace {
-
-// SeededRng (src/rng.cpp:9-49) on the host: the symmetry check's probe
-// normals (Box-Muller with the spare kept; glibc log/sin/cos like the
-// reference build).
-struct HostRng {
-  uint64_t mt[eqb::mt::kN];
-  int i = eqb::mt::kN;
-  bool has_spare = false;
-  double spare = 0.0;
-  HostRng(uint64_t seed, uint64_t stream) { eqb::mt::seed_state(seed, stream, mt); }
-  uint64_t next() {
-    if (i >= eqb::mt::kN) {
-      constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL;
-      for (int k = 0; k < eqb::mt::kN; ++k) {
-        const uint64_t x = (mt[k] & kUpper) | (mt[(k + 1) % eqb::mt::kN] & kLower);
-        uint64_t xa = x >> 1;
-        if (x & 1u) xa ^= 0xB5026F5AA96619E9ULL;
-        mt[k] = mt[(k + eqb::mt::kM) % eqb::mt::kN] ^ xa;
-      }
-      i = 0;
-    }
-    return eqb::mt::temper(mt[i++]);
-  }
-  double uniform01() { return (static_cast<double>(next() >> 11) + 0.5) * 0x1.0p-53; }
-  double normal() {
-    if (has_spare) {
-      has_spare = false;
-      return spare;
-    }
-    const double u1 = uniform01(), u2 = uniform01();
-    const double r = std::sqrt(-2.0 * std::log(u1));
-    const double theta = 6.283185307179586476925286766559 * u2;
-    spare = r * std::sin(theta);
-    has_spare = true;
-    return r * std::cos(theta);
-  }
-};
-
-enum class Variant { kSymmetric, kBlock };
-
-// check_symmetry (src/variants.cpp:14-33) with device applies and canonical
-// dots / norms; the probes come from stream 18 (streams::kSymmetryCheck).
-void check_symmetry(equil_matrix* M, uint64_t seed) {
-  const int64_t n = M->n;
-  cudaStream_t s = M->stream;
-  HostRng rng(seed, 18);
-  std::vector<double> x(n), y(n);
-  DevBuf<double> xd, yd, ax, ay, t;
-  xd.alloc(n); yd.alloc(n); ax.alloc(n); ay.alloc(n); t.alloc(n);
-  double* sc = M->scal.p + 32;
-  for (int probe = 0; probe < 3; ++probe) {
-    for (int64_t i = 0; i < n; ++i) x[i] = rng.normal();
-    for (int64_t i = 0; i < n; ++i) y[i] = rng.normal();
-    CK(cudaMemcpyAsync(xd.p, x.data(), n * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(yd.p, y.data(), n * 8, cudaMemcpyHostToDevice, s));
-    apply_pass(M, false, xd.p, ax.p, eqb::kPassPlain, nullptr, nullptr, nullptr);
-    apply_pass(M, false, yd.p, ay.p, eqb::kPassPlain, nullptr, nullptr, nullptr);
-    CK(eqb::launch_mul(t.p, ax.p, yd.p, n, s));
-    canon_reduce(M, t.p, n, sc + 0, 1);  // ax.dot(y)
-    CK(eqb::launch_mul(t.p, xd.p, ay.p, n, s));
-    canon_reduce(M, t.p, n, sc + 1, 1);  // x.dot(ay)
-    canon_reduce(M, ax.p, n, sc + 2, 0, 0.0, true);
-    canon_reduce(M, yd.p, n, sc + 3, 0, 0.0, true);
-    canon_reduce(M, xd.p, n, sc + 4, 0, 0.0, true);
-    canon_reduce(M, ay.p, n, sc + 5, 0, 0.0, true);
-    double r[6];
-    CK(cudaMemcpyAsync(r, sc, sizeof r, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const double scale = r[2] * r[3] + r[4] * r[5] + 1e-30;
-    require(std::abs(r[0] - r[1]) <= 1e-10 * scale,
-            "sgd_equilibrate_symmetric: operator failed symmetry check");
-  }
-}
-
-void sgd_variant(equil_matrix* M, Variant kind, const equil_params* p,
-                 const equil_diag_cfg* diag, equil_scaling_out* out, const int64_t* rb_host,
-                 const int64_t* cb_host, int64_t R, int64_t C) {
-  std::lock_guard<std::mutex> lk(M->mu);
-  DeviceGuard dg(M->device);
-  const bool sym = kind == Variant::kSymmetric;
-  const char* who = sym ? "sgd_equilibrate_symmetric" : "sgd_equilibrate_block";
-  require(M->world == 1, std::string(who) + ": single-GPU matrices only in this build");
-  validate_params(*p);
-  const int64_t m = M->m, n = M->n;
-  double alpha = 0, beta = 0;
-  std::vector<int32_t> rbm, cbm;
-  std::vector<double> rcount, ccount;
-  if (sym) {
-    require(m == n, "sgd_equilibrate_symmetric: operator must be square");
-    check_symmetry(M, p->seed);
-    resolve_targets(*p, n, n, alpha, beta);
-    require(std::abs(alpha - beta) <= 1e-12 * std::max(alpha, beta),
-            "sgd_equilibrate_symmetric: targets must coincide");
-    R = n;
-    C = 0;
-  } else {  // BlockStructure::validate (src/variants.cpp:131-154)
-    require(rb_host != nullptr && cb_host != nullptr, "BlockStructure: assignment length mismatch");
-    require(R > 0 && C > 0, "BlockStructure: block counts must be positive");
-    require(R < (1LL << 31) && C < (1LL << 31), "BlockStructure: too many blocks");
-    rcount.assign(R, 0.0);
-    ccount.assign(C, 0.0);
-    rbm.resize(m);
-    cbm.resize(n);
-    for (int64_t i = 0; i < m; ++i) {
-      require(rb_host[i] >= 0 && rb_host[i] < R, "BlockStructure: row block index out of range");
-      rbm[i] = static_cast<int32_t>(rb_host[i]);
-    }
-    for (int64_t j = 0; j < n; ++j) {
-      require(cb_host[j] >= 0 && cb_host[j] < C, "BlockStructure: col block index out of range");
-      cbm[j] = static_cast<int32_t>(cb_host[j]);
-    }
-    for (int64_t i = 0; i < m; ++i) rcount[rbm[i]] += 1.0;  // :165-169
-    for (int64_t j = 0; j < n; ++j) ccount[cbm[j]] += 1.0;
-    for (int64_t b = 0; b < R; ++b) require(rcount[b] != 0.0, "BlockStructure: empty row block");
-    for (int64_t b = 0; b < C; ++b) require(ccount[b] != 0.0, "BlockStructure: empty col block");
-    resolve_targets(*p, m, n, alpha, beta);
-  }
-  const int stride = diag ? diag->stride : 0;
-  require(stride >= 0, std::string(who) + ": stride must be positive");
-  const int T = p->iterations;
-  const int nrec = stride ? T / stride + 1 : 0;
-  if (stride) {
-    require(!M->dense, std::string(who) + ": history is implemented for sparse matrices");
-    require(out->hist_cap >= nrec, std::string(who) + ": history capacity too small");
-  }
-  cudaStream_t s = M->stream;
-  const double gamma = p->gamma, Mx = p->max_log_scale;
-
-  // signs: n per iteration (symmetric: one probe) or n + m (s then w)
-  const uint64_t per_iter = static_cast<uint64_t>(sym ? n : n + m);
-  const uint64_t total = per_iter * static_cast<uint64_t>(T);
-  if (total > 0) {
-    M->signs.ensure((total + 31) / 32 + 1);
-    const size_t sb = eqb::sign_stream_scratch_bytes(total);
-    M->sign_scratch.ensure(sb);
-    CK(eqb::sign_stream_generate(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb, s));
-  }
-  // block iterates, linear terms, scalings, probes, estimates
-  DevBuf<double> xu, xub, xv, xvb, lu, lv, d, e, xs, xw, er, ec, ebu, ebv;
-  DevBuf<int32_t> rbd, cbd, memr, memc;
-  DevBuf<int64_t> offr, offc;
-  xu.alloc(R); xub.alloc(R); lu.alloc(R);
-  d.alloc(m); e.alloc(n); xs.alloc(n); xw.alloc(m); er.alloc(m); ec.alloc(n);
-  CK(cudaMemsetAsync(xu.p, 0, R * 8, s));
-  CK(cudaMemsetAsync(xub.p, 0, R * 8, s));
-  {
-    std::vector<double> l(R);
-    for (int64_t b = 0; b < R; ++b) l[b] = sym ? alpha * alpha : (alpha * alpha) * rcount[b];
-    CK(cudaMemcpyAsync(lu.p, l.data(), R * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  if (!sym) {
-    xv.alloc(C); xvb.alloc(C); lv.alloc(C); ebu.alloc(R); ebv.alloc(C);
-    CK(cudaMemsetAsync(xv.p, 0, C * 8, s));
-    CK(cudaMemsetAsync(xvb.p, 0, C * 8, s));
-    std::vector<double> l(C);
-    for (int64_t b = 0; b < C; ++b) l[b] = (beta * beta) * ccount[b];
-    CK(cudaMemcpy(lv.p, l.data(), C * 8, cudaMemcpyHostToDevice));
-    // members of every block in ascending index order (stable counting sort)
-    auto members = [](const std::vector<int32_t>& map, int64_t nb, DevBuf<int32_t>& mem,
-                      DevBuf<int64_t>& off) {
-      std::vector<int64_t> o(nb + 1, 0);
-      for (int32_t b : map) ++o[b + 1];
-      for (int64_t b = 0; b < nb; ++b) o[b + 1] += o[b];
-      std::vector<int32_t> list(map.size());
-      std::vector<int64_t> pos(o.begin(), o.end() - 1);
-      for (size_t i = 0; i < map.size(); ++i) list[pos[map[i]]++] = static_cast<int32_t>(i);
-      mem.alloc(list.size());
-      off.alloc(o.size());
-      if (!list.empty())
-        CK(cudaMemcpy(mem.p, list.data(), list.size() * 4, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(off.p, o.data(), o.size() * 8, cudaMemcpyHostToDevice));
-    };
-    members(rbm, R, memr, offr);
-    members(cbm, C, memc, offc);
-    rbd.alloc(m);
-    cbd.alloc(n);
-    if (m) CK(cudaMemcpy(rbd.p, rbm.data(), m * 4, cudaMemcpyHostToDevice));
-    if (n) CK(cudaMemcpy(cbd.p, cbm.data(), n * 4, cudaMemcpyHostToDevice));
-  }
-  CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
-  eqb::SgdBlockConst c{};
-  c.gamma = gamma;
-  c.M = Mx;
-
-  // history (src/variants.cpp:66-86, :197-214) at the expanded averages
-  constexpr int kRec = 6;
-  DevBuf<double> hist, terms, uf, vf, eu, ev;
-  if (nrec) {
-    hist.alloc(kRec * nrec);
-    terms.alloc(m + n);
-    uf.alloc(m); vf.alloc(n); eu.alloc(m); ev.alloc(n);
-  }
-  const double a2 = alpha * alpha, b2 = sym ? alpha * alpha : beta * beta;
-  const double beta_rms = sym ? alpha : beta;
-  auto expand_avg = [&]() {
-    if (sym) {
-      CK(cudaMemcpyAsync(uf.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(vf.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
-    } else {
-      CK(eqb::launch_gather_map(xub.p, rbd.p, m, uf.p, s));
-      CK(eqb::launch_gather_map(xvb.p, cbd.p, n, vf.p, s));
-    }
-  };
-  int rec = 0;
-  auto record = [&]() {
-    double* slot = hist.p + kRec * rec;
-    expand_avg();
-    CK(eqb::launch_exp(uf.p, eu.p, m, 2.0, s));
-    CK(eqb::launch_exp(vf.p, ev.p, n, 2.0, s));
-    CK(eqb::launch_rms_terms(0, M->A, eu.p, ev.p, terms.p, 0, alpha, s));
-    CK(eqb::launch_rms_terms(1, M->AT, eu.p, ev.p, terms.p + m, 0, beta_rms, s));
-    canon_reduce(M, terms.p, m + n, slot + 0, 1);
-    CK(eqb::launch_obj_terms(M->A, uf.p, vf.p, terms.p, s));
-    canon_reduce(M, terms.p, m, slot + 1, 1);
-    canon_reduce(M, uf.p, m, slot + 2, 2, a2);
-    canon_reduce(M, vf.p, n, slot + 3, 2, b2);
-    canon_reduce(M, uf.p, m, slot + 4, 0);
-    canon_reduce(M, vf.p, n, slot + 5, 0);
-    ++rec;
-  };
-  if (stride) record();
-  for (int t = 1; t <= T; ++t) {
-    eqb::SgdStep st;
-    st.step = 2.0 / (gamma * static_cast<double>(t + 1));
-    st.aw = 2.0 / (static_cast<double>(t) + 2.0);
-    st.aw1 = 1.0 - st.aw;
-    st.pad = 0;
-    const int64_t base = static_cast<int64_t>(t - 1) * static_cast<int64_t>(per_iter);
-    if (sym) {  // d = exp(u); est = (d .* A (d .* s))^2 (:60-64)
-      CK(eqb::launch_expand_scale(xu.p, nullptr, n, M->signs.p, base, d.p, xs.p, s));
-      apply_pass(M, false, xs.p, er.p, eqb::kPassEst, d.p, nullptr, nullptr);
-      CK(eqb::launch_sgd_update(xu.p, xub.p, er.p, lu.p, c, st, n, M->flags.p, s));
-    } else {  // :181-194
-      CK(eqb::launch_expand_scale(xv.p, cbd.p, n, M->signs.p, base, e.p, xs.p, s));
-      CK(eqb::launch_expand_scale(xu.p, rbd.p, m, M->signs.p, base + n, d.p, xw.p, s));
-      apply_pass(M, false, xs.p, er.p, eqb::kPassEst, d.p, nullptr, nullptr);
-      apply_pass(M, true, xw.p, ec.p, eqb::kPassEst, e.p, nullptr, nullptr);
-      CK(eqb::launch_block_sum(er.p, memr.p, offr.p, R, ebu.p, s));
-      CK(eqb::launch_block_sum(ec.p, memc.p, offc.p, C, ebv.p, s));
-      CK(eqb::launch_sgd_update(xu.p, xub.p, ebu.p, lu.p, c, st, R, M->flags.p, s));
-      CK(eqb::launch_sgd_update(xv.p, xvb.p, ebv.p, lv.p, c, st, C, M->flags.p, s));
-    }
-    if (stride && t % stride == 0) record();
-  }
-  // result: expanded averages and their exponentials (:93-96, :226-229)
-  DevBuf<double> ufin, vfin, dfin, efin;
-  ufin.alloc(m); vfin.alloc(n); dfin.alloc(m); efin.alloc(n);
-  if (sym) {
-    CK(cudaMemcpyAsync(ufin.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(vfin.p, xub.p, n * 8, cudaMemcpyDeviceToDevice, s));
-  } else {
-    CK(eqb::launch_gather_map(xub.p, rbd.p, m, ufin.p, s));
-    CK(eqb::launch_gather_map(xvb.p, cbd.p, n, vfin.p, s));
-  }
-  CK(eqb::launch_exp(ufin.p, dfin.p, m, 1.0, s));
-  CK(eqb::launch_exp(vfin.p, efin.p, n, 1.0, s));
-  const cudaMemcpyKind k =
-      out->outputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  if (out->u) CK(cudaMemcpyAsync(out->u, ufin.p, m * 8, k, s));
-  if (out->v) CK(cudaMemcpyAsync(out->v, vfin.p, n * 8, k, s));
-  if (out->d) CK(cudaMemcpyAsync(out->d, dfin.p, m * 8, k, s));
-  if (out->e) CK(cudaMemcpyAsync(out->e, efin.p, n * 8, k, s));
-  unsigned flags = 0;
-  CK(cudaMemcpyAsync(&flags, M->flags.p, sizeof flags, cudaMemcpyDeviceToHost, s));
-  std::vector<double> hh(kRec * static_cast<size_t>(std::max(nrec, 1)));
-  if (nrec) CK(cudaMemcpyAsync(hh.data(), hist.p, kRec * nrec * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  out->alpha = alpha;
-  out->beta = sym ? alpha : beta;
-  out->iterate_bound_ok = (flags & 1u) ? 0 : 1;
-  out->box_feasible = (flags & 2u) ? 0 : 1;
-  out->apply_count = T;
-  out->adjoint_count = sym ? 0 : T;
-  out->hist_len = nrec;
-  for (int h = 0; h < nrec; ++h) {
-    const double* r = hh.data() + kRec * h;
-    const double obj = 0.5 * r[1] - r[2] - r[3] + 0.5 * gamma * (r[4] + r[5]);
-    if (out->hist_iter) out->hist_iter[h] = h * stride;
-    if (out->hist_objective)  // symmetric: each unordered pair once (:75-78)
-      out->hist_objective[h] = (diag->want_objective ? (sym ? 0.5 * obj : obj) : 0.0);
-    if (out->hist_rms)
-      out->hist_rms[h] = diag->want_rms ? std::sqrt(r[0] / static_cast<double>(m + n)) : 0.0;
-  }
-}
-
-}  // namespace
-
-extern "C" {
-
-equil_status equil_sgd_equilibrate_symmetric(equil_matrix* M, const equil_params* p,
-                                             const equil_diag_cfg* diag,
-                                             equil_scaling_out* out) {
-  return guarded([&] {
-    require(M != nullptr && p != nullptr && out != nullptr,
-            "sgd_equilibrate_symmetric: null argument");
-    sgd_variant(M, Variant::kSymmetric, p, diag, out, nullptr, nullptr, 0, 0);
-  });
-}
-
-equil_status equil_sgd_equilibrate_block(equil_matrix* M, const int64_t* row_block,
-                                         const int64_t* col_block, int64_t row_blocks,
-                                         int64_t col_blocks, const equil_params* p,
-                                         const equil_diag_cfg* diag, equil_scaling_out* out) {
-  return guarded([&] {
-    require(M != nullptr && p != nullptr && out != nullptr,
-            "sgd_equilibrate_block: null argument");
-    sgd_variant(M, Variant::kBlock, p, diag, out, row_block, col_block, row_blocks, col_blocks);
-  });
-}
-
-}  // extern "C"
-
-// ---------------------------------------------------------------------------
-// spectral_norm (src/lsqr.cpp:140-163) and the Chambolle-Pock lasso
-// (src/ccp.cpp:27-160): the second consumer of the equilibration's d, e.
-// Device vectors, canonical reductions; the lasso objective of every iterate
-// is evaluated on the device into a history array, so a run without an early
-// stop test synchronises only at its end.  Single GPU.
-// ---------------------------------------------------------------------------
-namespace {
-
-// power iteration on diag(d) A diag(e) (d, e null: A), uncharged
-double spectral_norm_dev(equil_matrix* M, const double* d, const double* e, int max_iters,
-                         double rel_tol, uint64_t seed) {
-  require(max_iters > 0, "spectral_norm: max_iters must be positive");
-  const int64_t m = M->m, n = M->n;
-  cudaStream_t s = M->stream;
-  HostRng rng(seed, 19);  // streams::kPowerIteration
-  std::vector<double> xh(n);
-  for (int64_t j = 0; j < n; ++j) xh[j] = rng.normal();
-  DevBuf<double> x, y, z, t;
-  x.alloc(n); y.alloc(m); z.alloc(n); t.alloc(std::max(m, n));
-  double* sc = M->scal.p + 40;
-  CK(cudaMemcpyAsync(x.p, xh.data(), n * 8, cudaMemcpyHostToDevice, s));
-  canon_reduce(M, x.p, n, sc + 0, 0, 0.0, true);
-  const double xn = read_scalar(M, sc + 0);
-  if (!(xn > 0.0)) fail(EQUIL_ERUNTIME, "spectral_norm: degenerate start");
-  CK(eqb::launch_lsqr_normalize(x.p, x.p, sc + 0, nullptr, nullptr, n, nullptr, nullptr, s));
-  double lambda = 0.0;
-  for (int it = 0; it < max_iters; ++it) {
-    const double* xg = x.p;
-    if (e) {
-      CK(eqb::launch_mul(t.p, e, x.p, n, s));
-      xg = t.p;
-    }
-    apply_pass(M, false, xg, y.p, eqb::kPassScaled, d, nullptr, nullptr);
-    canon_reduce(M, y.p, m, sc + 1, 0);
-    const double next = read_scalar(M, sc + 1);
-    if (next == 0.0) return 0.0;
-    const bool settled = std::abs(next - lambda) <= rel_tol * next;
-    lambda = next;
-    if (settled) break;
-    const double* yg = y.p;
-    if (d) {
-      CK(eqb::launch_mul(t.p, d, y.p, m, s));
-      yg = t.p;
-    }
-    apply_pass(M, true, yg, z.p, eqb::kPassScaled, e, nullptr, nullptr);
-    canon_reduce(M, z.p, n, sc + 2, 0, 0.0, true);
-    const double zn = read_scalar(M, sc + 2);
-    if (zn == 0.0) break;
-    CK(eqb::launch_lsqr_normalize(x.p, z.p, sc + 2, nullptr, nullptr, n, nullptr, nullptr, s));
-  }
-  return std::sqrt(lambda);
-}
-
-// lasso_objective (src/ccp.cpp:115-123) of device x into *out (device)
-void lasso_value_dev(equil_matrix* M, const double* b_d, double sqrt_lambda, const double* x,
-                     const double* absx, double* r, double* out) {
-  apply_pass(M, false, x, r, eqb::kPassResid, nullptr, b_d, nullptr);  // b - Ax: same squares
-  double* sc = M->scal.p + 44;
-  canon_reduce(M, r, M->m, sc + 0, 0);
-  canon_reduce(M, absx, M->n, sc + 1, 1);
-  CK(eqb::launch_lasso_value(sc + 0, sc + 1, sqrt_lambda, out, M->stream));
-}
-
-void ccp_common(equil_matrix* M, const double* b, double lambda, const equil_params* p,
-                const equil_ccp_options* o, equil_ccp_out* out, const char* who) {
-  require(M != nullptr && o != nullptr && out != nullptr, std::string(who) + ": null argument");
-  require(b != nullptr, "lasso: rhs length mismatch");
-  std::lock_guard<std::mutex> lk(M->mu);
-  DeviceGuard dg(M->device);
-  require(M->world == 1, std::string(who) + ": single-GPU matrices only in this build");
-  cudaStream_t s = M->stream;
-  const int64_t m = M->m, n = M->n;
-  // validate_problem (:11-17)
-  require(lambda > 0.0, "lasso: lambda must be positive");
-  DevBuf<double> b_d;
-  b_d.alloc(m);
-  CK(cudaMemcpyAsync(b_d.p, b, m * 8, cudaMemcpyHostToDevice, s));
-  canon_reduce(M, b_d.p, m, M->scal.p + 48, 0, 0.0, true);
-  require(read_scalar(M, M->scal.p + 48) > 0.0, "lasso: rhs must be nonzero");
-  require(o->max_iters >= 0, std::string(who) + ": max_iters must be nonnegative");
-  const int T = p ? p->iterations : 0;
-  require(out->objective_history != nullptr &&
-              out->hist_cap >= std::max(o->max_iters, 0) + 1 + std::max(T, 0),
-          std::string(who) + ": history capacity too small");
-  const bool track = std::isfinite(o->p_star);
-  require(!track || out->gap_history != nullptr, std::string(who) + ": gap_history missing");
-
-  long long applies = 0, adjoints = 0;
-  DevBuf<double> dd, ed;
-  const double* d = nullptr;
-  const double* e = nullptr;
-  if (p) {  // sgd_equilibrate on the charged operator (:139)
-    dd.alloc(m);
-    ed.alloc(n);
-    equil_scaling_out so{};
-    so.d = dd.p;
-    so.e = ed.p;
-    so.outputs_on_device = 1;
-    M->mu.unlock();
-    const equil_status rc = equil_sgd_equilibrate(M, p, nullptr, &so);
-    M->mu.lock();
-    if (rc != EQUIL_OK) fail(rc, g_err);
-    applies = so.apply_count;
-    adjoints = so.adjoint_count;
-    d = dd.p;
-    e = ed.p;
-  }
-  // ccp_core (:27-110)
-  const double sl = std::sqrt(lambda);
-  double tau, sigma;
-  if (o->tau > 0.0 && o->sigma > 0.0) {
-    tau = o->tau;
-    sigma = o->sigma;
-  } else {
-    const double norm2 = spectral_norm_dev(M, d, e, 100, 1e-9, 0);
-    if (!(norm2 > 0.0)) fail(EQUIL_ERUNTIME, "ccp_lasso: zero operator");
-    tau = 0.9 / norm2;
-    sigma = 0.9 / norm2;
-  }
-  const double f0 = [&] {
-    DevBuf<double> zero, r, v;
-    zero.alloc(n);
-    r.alloc(m);
-    v.alloc(1);
-    CK(cudaMemsetAsync(zero.p, 0, n * 8, s));
-    lasso_value_dev(M, b_d.p, sl, zero.p, zero.p, r.p, v.p);
-    return read_scalar(M, v.p);
-  }();
-  int hl = 0, gl = 0;
-  bool reached = false;
-  auto push = [&](double f) {
-    out->objective_history[hl++] = f;
-    if (track) out->gap_history[gl++] = (f - o->p_star) / f0;
-  };
-  for (int t = 0; t <= T; ++t) push(f0);
-  if (track && o->gap_tol > 0.0 && out->gap_history[gl - 1] <= o->gap_tol) reached = true;
-
-  DevBuf<double> y, kz, dy, z, ezt, g, x, absx, r, fh;
-  y.alloc(m); kz.alloc(m); dy.alloc(m); r.alloc(m);
-  z.alloc(n); ezt.alloc(n); g.alloc(n); x.alloc(n); absx.alloc(n);
-  const int iters = std::max(o->max_iters, 0);
-  fh.alloc(std::max(iters, 1));
-  CK(cudaMemsetAsync(y.p, 0, m * 8, s));
-  CK(cudaMemsetAsync(z.p, 0, n * 8, s));
-  CK(cudaMemsetAsync(ezt.p, 0, n * 8, s));
-  CK(cudaMemsetAsync(x.p, 0, n * 8, s));
-  const bool early = track && o->gap_tol > 0.0;  // stop test needs f on the host
-  int done = 0;
-  for (int t = 1; t <= iters && !reached; ++t) {
-    apply_pass(M, false, ezt.p, kz.p, eqb::kPassScaled, d, nullptr, nullptr);  // K z~
-    ++applies;
-    CK(eqb::launch_ccp_dual(y.p, kz.p, d, b_d.p, sigma, sl, m, dy.p, s));
-    apply_pass(M, true, dy.p, g.p, eqb::kPassScaled, e, nullptr, nullptr);  // K^T y
-    ++adjoints;
-    CK(eqb::launch_ccp_primal(z.p, ezt.p, g.p, e, tau, tau * sl, o->theta, n, x.p, absx.p, s));
-    lasso_value_dev(M, b_d.p, sl, x.p, absx.p, r.p, fh.p + (t - 1));  // uncharged probe
-    done = t;
-    if (early) {
-      push(read_scalar(M, fh.p + (t - 1)));
-      if (out->gap_history[gl - 1] <= o->gap_tol) reached = true;
-    }
-  }
-  if (!early && done > 0) {
-    std::vector<double> f(done);
-    CK(cudaMemcpyAsync(f.data(), fh.p, done * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (double v : f) push(v);
-  }
-  if (out->x) CK(cudaMemcpyAsync(out->x, x.p, n * 8, cudaMemcpyDeviceToHost, s));  // e .* z
-  CK(cudaStreamSynchronize(s));
-  out->hist_len = hl;
-  out->gap_len = gl;
-  out->tau = tau;
-  out->sigma = sigma;
-  out->theta = o->theta;
-  out->iterations = done;
-  out->equil_iterations = T;
-  out->reached_tol = reached ? 1 : 0;
-  out->apply_count = applies;
-  out->adjoint_count = adjoints;
-}
-
-}  // namespace
-
-extern "C" {
-
-equil_status equil_spectral_norm(equil_matrix* M, int max_iters, double rel_tol, uint64_t seed,
-                                 double* out) {
-  return guarded([&] {
-    require(M != nullptr && out != nullptr, "spectral_norm: null argument");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    require(M->world == 1, "spectral_norm: single-GPU matrices only in this build");
-    *out = spectral_norm_dev(M, nullptr, nullptr, max_iters, rel_tol, seed);
-  });
-}
-
-equil_status equil_lasso_objective(equil_matrix* M, const double* b, double lambda,
-                                   const double* x, double* out) {
-  return guarded([&] {
-    require(M != nullptr && b != nullptr && x != nullptr && out != nullptr,
-            "lasso_objective: null argument");
-    require(lambda > 0.0, "lasso_objective: malformed problem");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    require(M->world == 1, "lasso_objective: single-GPU matrices only in this build");
-    cudaStream_t s = M->stream;
-    DevBuf<double> b_d, x_d, ax, r, v;
-    b_d.alloc(M->m); x_d.alloc(M->n); ax.alloc(M->n); r.alloc(M->m); v.alloc(1);
-    CK(cudaMemcpyAsync(b_d.p, b, M->m * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(x_d.p, x, M->n * 8, cudaMemcpyHostToDevice, s));
-    CK(eqb::launch_abs(x_d.p, M->n, ax.p, s));
-    lasso_value_dev(M, b_d.p, std::sqrt(lambda), x_d.p, ax.p, r.p, v.p);
-    *out = read_scalar(M, v.p);
-  });
-}
-
-equil_status equil_ccp_lasso(equil_matrix* M, const double* b, double lambda,
-                             const equil_ccp_options* o, equil_ccp_out* out) {
-  return guarded([&] { ccp_common(M, b, lambda, nullptr, o, out, "ccp_lasso"); });
-}
-
-equil_status equil_ccp_lasso_preconditioned(equil_matrix* M, const double* b, double lambda,
-                                            const equil_params* p, const equil_ccp_options* o,
-                                            equil_ccp_out* out) {
-  return guarded([&] {
-    require(p != nullptr, "ccp_lasso_preconditioned: null params");
-    ccp_common(M, b, lambda, p, o, out, "ccp_lasso_preconditioned");
-  });
-}
-
-}  // extern "C"
-
-// ---------------------------------------------------------------------------
-// Matrix store ingest: Matrix Market files
-// (src/matrix_market.cpp) parsed on host threads, sorted / checked / converted
-// to CSR on the device; a binary CSR file for fast reloads; host export.
-// ---------------------------------------------------------------------------
-namespace {
-
-// the local CSR(A) (world 1) or dense A on the host
-void export_host(equil_matrix* M, std::vector<int64_t>& rp, std::vector<int32_t>& ci,
-                 std::vector<double>& va, std::vector<double>& dense) {
-  require(M->world == 1, "export: single-GPU matrices only");
-  cudaStream_t s = M->stream;
-  if (M->dense) {
-    dense.resize(static_cast<size_t>(M->m * M->n));
-    CK(cudaMemcpyAsync(dense.data(), M->Ad.p, M->m * M->n * 8, cudaMemcpyDeviceToHost, s));
-  } else {
-    rp.resize(M->m + 1);
-    ci.resize(static_cast<size_t>(M->nnz));
-    va.resize(static_cast<size_t>(M->nnz));
-    CK(cudaMemcpyAsync(rp.data(), M->A.row_ptr, (M->m + 1) * 8, cudaMemcpyDeviceToHost, s));
-    if (M->nnz) {
-      CK(cudaMemcpyAsync(ci.data(), M->A.col, M->nnz * 4, cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(va.data(), M->A.val, M->nnz * 8, cudaMemcpyDeviceToHost, s));
-    }
-  }
-  CK(cudaStreamSynchronize(s));
-}
-
-}  // namespace
-
-extern "C" {
-
-equil_status equil_matrix_read_matrix_market(const char* path, const equil_device_cfg* cfg,
-                                             equil_matrix** out) {
-  return guarded([&] {
-    require(path != nullptr && out != nullptr, "matrix market: null argument");
-    *out = nullptr;
-    std::string buf;
-    eqb::mm::read_file(path, buf);
-    eqb::mm::Matrix mm;
-    eqb::mm::parse(buf.data(), buf.size(), mm);
-    buf.clear();
-    buf.shrink_to_fit();
-    if (mm.dense) {
-      const equil_status rc =
-          equil_matrix_create_dense(mm.m, mm.n, mm.dense_rowmajor.data(), cfg, out);
-      if (rc != EQUIL_OK) fail(rc, g_err);
-      return;
-    }
-    create_coo_impl(mm.m, mm.n, mm.nnz, mm.row.data(), mm.col.data(), mm.val.data(),
-                    mm.line.data(), cfg, out);
-  });
-}
-
-equil_status equil_matrix_write_matrix_market(equil_matrix* M, const char* path) {
-  return guarded([&] {
-    require(M != nullptr && path != nullptr, "matrix market: null argument");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    std::vector<int64_t> rp;
-    std::vector<int32_t> ci;
-    std::vector<double> va, dense;
-    export_host(M, rp, ci, va, dense);
-    if (M->dense)
-      eqb::mm::write_array(path, M->m, M->n, dense.data());
-    else
-      eqb::mm::write_coordinate(path, M->m, M->n, rp.data(), ci.data(), va.data());
-  });
-}
-
-equil_status equil_matrix_save_binary(equil_matrix* M, const char* path) {
-  return guarded([&] {
-    require(M != nullptr && path != nullptr, "binary csr: null argument");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    std::vector<int64_t> rp;
-    std::vector<int32_t> ci;
-    std::vector<double> va, dense;
-    export_host(M, rp, ci, va, dense);
-    eqb::mm::write_binary(path, M->m, M->n, M->dense, rp.data(), ci.data(), va.data(),
-                          dense.data());
-  });
-}
-
-equil_status equil_matrix_load_binary(const char* path, const equil_device_cfg* cfg,
-                                      equil_matrix** out) {
-  return guarded([&] {
-    require(path != nullptr && out != nullptr, "binary csr: null argument");
-    *out = nullptr;
-    FILE* f = std::fopen(path, "rb");
-    if (!f) throw std::runtime_error(std::string("binary csr: cannot open '") + path + "'");
-    struct Closer {
-      FILE* f;
-      ~Closer() { std::fclose(f); }
-    } closer{f};
-    int64_t hdr[4];
-    eqb::mm::read_binary_header(f, path, hdr);
-    const int64_t m = hdr[0], n = hdr[1], nnz = hdr[2];
-    // read straight into pinned host buffers (fast H2D in the create call)
-    auto pinned = [](size_t bytes) {
-      void* p = nullptr;
-      CK(cudaMallocHost(&p, std::max<size_t>(bytes, 8)));
-      return p;
-    };
-    struct Pinned {
-      void* p;
-      ~Pinned() { if (p) cudaFreeHost(p); }
-    };
-    equil_status rc;
-    if (hdr[3]) {
-      Pinned a{pinned(static_cast<size_t>(nnz) * 8)};
-      eqb::mm::read_exact(f, a.p, 8, static_cast<size_t>(nnz), path);
-      rc = equil_matrix_create_dense(m, n, static_cast<const double*>(a.p), cfg, out);
-    } else {
-      Pinned rp{pinned(static_cast<size_t>(m + 1) * 8)};
-      Pinned ci{pinned(static_cast<size_t>(nnz) * 4)};
-      Pinned va{pinned(static_cast<size_t>(nnz) * 8)};
-      eqb::mm::read_exact(f, rp.p, 8, static_cast<size_t>(m + 1), path);
-      eqb::mm::read_exact(f, ci.p, 4, static_cast<size_t>(nnz), path);
-      eqb::mm::read_exact(f, va.p, 8, static_cast<size_t>(nnz), path);
-      rc = equil_matrix_create_csr(m, n, static_cast<const int64_t*>(rp.p),
-                                   static_cast<const int32_t*>(ci.p),
-                                   static_cast<const double*>(va.p), cfg, out);
-    }
-    if (rc != EQUIL_OK) fail(rc, g_err);
-  });
-}
-
-equil_status equil_matrix_export_csr(equil_matrix* M, int64_t* row_ptr, int32_t* col,
-                                     double* val) {
-  return guarded([&] {
-    require(M != nullptr && row_ptr != nullptr, "export_csr: null argument");
-    require(!M->dense, "export_csr: dense matrix");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    std::vector<int64_t> rp;
-    std::vector<int32_t> ci;
-    std::vector<double> va, dense;
-    export_host(M, rp, ci, va, dense);
-    std::memcpy(row_ptr, rp.data(), rp.size() * 8);
-    if (M->nnz) {
-      std::memcpy(col, ci.data(), ci.size() * 4);
-      std::memcpy(val, va.data(), va.size() * 8);
-    }
-  });
-}
-
-equil_status equil_matrix_export_dense(equil_matrix* M, double* rowmajor) {
-  return guarded([&] {
-    require(M != nullptr && rowmajor != nullptr, "export_dense: null argument");
-    require(M->dense, "export_dense: sparse matrix");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    std::vector<int64_t> rp;
-    std::vector<int32_t> ci;
-    std::vector<double> va, dense;
-    export_host(M, rp, ci, va, dense);
-    std::memcpy(rowmajor, dense.data(), dense.size() * 8);
-  });
-}
-
-int equil_matrix_is_dense(const equil_matrix* M) { return M && M->dense ? 1 : 0; }
-
-}  // extern "C"
-
-// Host-only Matrix Market access (no device needed): parse into a handle,
-// fetch the entries, write a host CSR / dense array.
-extern "C" {
-
-equil_status equil_mm_parse(const char* path, int64_t* m, int64_t* n, int64_t* nnz, int* dense,
-                            void** handle) {
-  return guarded([&] {
-    require(path && m && n && nnz && dense && handle, "matrix market: null argument");
-    *handle = nullptr;
-    std::string buf;
-    eqb::mm::read_file(path, buf);
-    auto mm = std::make_unique<eqb::mm::Matrix>();
-    eqb::mm::parse(buf.data(), buf.size(), *mm);
-    *m = mm->m;
-    *n = mm->n;
-    *nnz = mm->nnz;
-    *dense = mm->dense ? 1 : 0;
-    *handle = mm.release();
-  });
-}
-
-equil_status equil_mm_fetch(void* handle, int64_t* rows, int64_t* cols, double* vals,
-                            int64_t* lines) {
-  return guarded([&] {
-    require(handle != nullptr, "matrix market: null handle");
-    const auto* mm = static_cast<const eqb::mm::Matrix*>(handle);
-    if (mm->dense) {
-      if (vals) std::memcpy(vals, mm->dense_rowmajor.data(), mm->dense_rowmajor.size() * 8);
-      return;
-    }
-    if (rows) std::memcpy(rows, mm->row.data(), mm->row.size() * 8);
-    if (cols) std::memcpy(cols, mm->col.data(), mm->col.size() * 8);
-    if (vals) std::memcpy(vals, mm->val.data(), mm->val.size() * 8);
-    if (lines) std::memcpy(lines, mm->line.data(), mm->line.size() * 8);
-  });
-}
-
-void equil_mm_free(void* handle) { delete static_cast<eqb::mm::Matrix*>(handle); }
-
-equil_status equil_mm_write_csr(const char* path, int64_t m, int64_t n, const int64_t* row_ptr,
-                                const int32_t* col, const double* val) {
-  return guarded([&] {
-    require(path && row_ptr && m > 0 && n > 0, "matrix market: null argument");
-    eqb::mm::write_coordinate(path, m, n, row_ptr, col, val);
-  });
-}
-
-equil_status equil_mm_write_dense(const char* path, int64_t m, int64_t n,
-                                  const double* rowmajor) {
-  return guarded([&] {
-    require(path && rowmajor && m > 0 && n > 0, "matrix market: null argument");
-    eqb::mm::write_array(path, m, n, rowmajor);
-  });
-}
-
-}  // extern "C"
-
-// ---------------------------------------------------------------------------
-// Public helpers of include/equil/equilibrate.hpp and metrics.hpp on the device
-// matrix: objective / gradient (weighted and plain), the one-sample stochastic
-// gradient estimate, rms_error, project_box.  Per-row sums follow CSR order
-// (A's rows for u, A^T's rows = ascending original rows for v); whole-vector
-// sums use the canonical reduction; exp is det_exp (the numerics contract).
-// Single GPU, sparse matrices (the estimate also takes dense ones).
-// ---------------------------------------------------------------------------
-namespace {
-
-struct HelperCtx {
-  equil_matrix* M;
-  cudaStream_t s;
-  DevBuf<double> u, v, lu, lv, tm, tn;
-  HelperCtx(equil_matrix* m, const double* uh, const double* vh, const char* who,
-            bool need_csr = true)
-      : M(m), s(m->stream) {
-    require(M->world == 1, std::string(who) + ": single-GPU matrices only in this build");
-    require(!need_csr || !M->dense, std::string(who) + ": sparse matrices only in this build");
-    u.alloc(M->m);
-    v.alloc(M->n);
-    tm.alloc(M->m);
-    tn.alloc(M->n);
-    CK(cudaMemcpyAsync(u.p, uh, M->m * 8, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(v.p, vh, M->n * 8, cudaMemcpyHostToDevice, s));
-  }
-  const double* upload_lin(DevBuf<double>& b, const double* h, int64_t len) {
-    if (!h) return nullptr;
-    b.alloc(len);
-    CK(cudaMemcpyAsync(b.p, h, len * 8, cudaMemcpyHostToDevice, s));
-    return b.p;
-  }
-};
-
-// objective_weighted (src/equilibrate.cpp:10-22); lin arrays null: constants
-double objective_dev(HelperCtx& c, const double* lin_u, double lu_c, const double* lin_v,
-                     double lv_c, double gamma) {
-  equil_matrix* M = c.M;
-  double* sc = M->scal.p + 52;
-  CK(eqb::launch_obj_terms(M->A, c.u.p, c.v.p, c.tm.p, c.s));
-  canon_reduce(M, c.tm.p, M->m, sc + 0, 1);
-  if (lin_u) {
-    CK(eqb::launch_mul(c.tm.p, lin_u, c.u.p, M->m, c.s));
-    canon_reduce(M, c.tm.p, M->m, sc + 1, 1);
-  } else {
-    canon_reduce(M, c.u.p, M->m, sc + 1, 2, lu_c);
-  }
-  if (lin_v) {
-    CK(eqb::launch_mul(c.tn.p, lin_v, c.v.p, M->n, c.s));
-    canon_reduce(M, c.tn.p, M->n, sc + 2, 1);
-  } else {
-    canon_reduce(M, c.v.p, M->n, sc + 2, 2, lv_c);
-  }
-  canon_reduce(M, c.u.p, M->m, sc + 3, 0);
-  canon_reduce(M, c.v.p, M->n, sc + 4, 0);
-  double r[5];
-  CK(cudaMemcpyAsync(r, sc, sizeof r, cudaMemcpyDeviceToHost, c.s));
-  CK(cudaStreamSynchronize(c.s));
-  return 0.5 * r[0] - r[1] - r[2] + 0.5 * gamma * (r[3] + r[4]);
-}
-
-// gradient_weighted (src/equilibrate.cpp:24-37)
-void gradient_dev(HelperCtx& c, const double* lin_u, double lu_c, const double* lin_v,
-                  double lv_c, double gamma, double* gu_h, double* gv_h) {
-  equil_matrix* M = c.M;
-  CK(eqb::launch_obj_terms(M->A, c.u.p, c.v.p, c.tm.p, c.s));   // sum_j a^2 e^{2(u_i+v_j)}
-  CK(eqb::launch_obj_terms(M->AT, c.v.p, c.u.p, c.tn.p, c.s));  // ascending i per column
-  CK(eqb::launch_grad_finish(c.tm.p, c.u.p, lin_u, lu_c, gamma, M->m, c.s));
-  CK(eqb::launch_grad_finish(c.tn.p, c.v.p, lin_v, lv_c, gamma, M->n, c.s));
-  CK(cudaMemcpyAsync(gu_h, c.tm.p, M->m * 8, cudaMemcpyDeviceToHost, c.s));
-  CK(cudaMemcpyAsync(gv_h, c.tn.p, M->n * 8, cudaMemcpyDeviceToHost, c.s));
-  CK(cudaStreamSynchronize(c.s));
-}
-
-}  // namespace
-
-extern "C" {
-
-equil_status equil_objective_weighted(equil_matrix* M, const double* u, const double* v,
-                                      const double* lin_u, const double* lin_v, double gamma,
-                                      double* out) {
-  return guarded([&] {
-    require(M && u && v && lin_u && lin_v && out, "objective: null argument");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    HelperCtx c(M, u, v, "objective");
-    const double* lu = c.upload_lin(c.lu, lin_u, M->m);
-    const double* lv = c.upload_lin(c.lv, lin_v, M->n);
-    *out = objective_dev(c, lu, 0.0, lv, 0.0, gamma);
-  });
-}
-
-equil_status equil_objective(equil_matrix* M, const double* u, const double* v,
-                             const equil_params* p, double* out) {
-  return guarded([&] {
-    require(M && u && v && p && out, "objective: null argument");
-    validate_params(*p);
-    double alpha = 0, beta = 0;
-    resolve_targets(*p, M->m, M->n, alpha, beta);
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    HelperCtx c(M, u, v, "objective");
-    *out = objective_dev(c, nullptr, alpha * alpha, nullptr, beta * beta, p->gamma);
-  });
-}
-
-equil_status equil_gradient_weighted(equil_matrix* M, const double* u, const double* v,
-                                     const double* lin_u, const double* lin_v, double gamma,
-                                     double* grad_u, double* grad_v) {
-  return guarded([&] {
-    require(M && u && v && lin_u && lin_v && grad_u && grad_v, "gradient: null argument");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    HelperCtx c(M, u, v, "gradient");
-    const double* lu = c.upload_lin(c.lu, lin_u, M->m);
-    const double* lv = c.upload_lin(c.lv, lin_v, M->n);
-    gradient_dev(c, lu, 0.0, lv, 0.0, gamma, grad_u, grad_v);
-  });
-}
-
-equil_status equil_gradient(equil_matrix* M, const double* u, const double* v,
-                            const equil_params* p, double* grad_u, double* grad_v) {
-  return guarded([&] {
-    require(M && u && v && p && grad_u && grad_v, "gradient: null argument");
-    validate_params(*p);
-    double alpha = 0, beta = 0;
-    resolve_targets(*p, M->m, M->n, alpha, beta);
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    HelperCtx c(M, u, v, "gradient");
-    gradient_dev(c, nullptr, alpha * alpha, nullptr, beta * beta, p->gamma, grad_u, grad_v);
-  });
-}
-
-// stochastic_gradient_estimate (src/equilibrate.cpp:60-71): the probes are
-// outputs [offset, offset + n + m) of SeededRng(seed, stream) (s then w)
-equil_status equil_stochastic_gradient_estimate(equil_matrix* M, const double* u,
-                                                const double* v, const equil_params* p,
-                                                uint64_t seed, uint64_t stream, uint64_t offset,
-                                                double* g_u, double* g_v) {
-  return guarded([&] {
-    require(M && u && v && p && g_u && g_v, "stochastic_gradient_estimate: null argument");
-    validate_params(*p);
-    double alpha = 0, beta = 0;
-    resolve_targets(*p, M->m, M->n, alpha, beta);
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    HelperCtx c(M, u, v, "stochastic_gradient_estimate", false);
-    const int64_t m = M->m, n = M->n;
-    const uint64_t total = offset + static_cast<uint64_t>(m + n);
-    DevBuf<uint32_t> bits;
-    DevBuf<unsigned char> scratch;
-    bits.alloc((total + 31) / 32 + 1);
-    const size_t sb = eqb::sign_stream_scratch_bytes(total);
-    scratch.alloc(sb);
-    CK(eqb::sign_stream_generate(seed, stream, total, bits.p, scratch.p, sb, c.s));
-    DevBuf<double> d, e, xs, xw;
-    d.alloc(m); e.alloc(n); xs.alloc(n); xw.alloc(m);
-    // d = exp(u), e = exp(v); xs = e .* s; xw = d .* w
-    CK(eqb::launch_expand_scale(c.v.p, nullptr, n, bits.p, static_cast<int64_t>(offset), e.p,
-                                xs.p, c.s));
-    CK(eqb::launch_expand_scale(c.u.p, nullptr, m, bits.p, static_cast<int64_t>(offset) + n,
-                                d.p, xw.p, c.s));
-    apply_pass(M, false, xs.p, c.tm.p, eqb::kPassEst, d.p, nullptr, nullptr);
-    apply_pass(M, true, xw.p, c.tn.p, eqb::kPassEst, e.p, nullptr, nullptr);
-    CK(eqb::launch_sge_finish(c.tm.p, c.u.p, -alpha * alpha, p->gamma, m, c.s));
-    CK(eqb::launch_sge_finish(c.tn.p, c.v.p, -beta * beta, p->gamma, n, c.s));
-    CK(cudaMemcpyAsync(g_u, c.tm.p, m * 8, cudaMemcpyDeviceToHost, c.s));
-    CK(cudaMemcpyAsync(g_v, c.tn.p, n * 8, cudaMemcpyDeviceToHost, c.s));
-    CK(cudaStreamSynchronize(c.s));
-  });
-}
-
-// rms_error (src/metrics.cpp:41-56)
-equil_status equil_rms_error(equil_matrix* M, const double* u, const double* v, double alpha,
-                             double beta, double* out) {
-  return guarded([&] {
-    require(M && u && v && out, "rms_error: null argument");
-    require(alpha > 0.0 && beta > 0.0, "rms_error: targets must be positive");
-    std::lock_guard<std::mutex> lk(M->mu);
-    DeviceGuard dg(M->device);
-    HelperCtx c(M, u, v, "rms_error");
-    DevBuf<double> terms;
-    terms.alloc(M->m + M->n);
-    CK(eqb::launch_exp(c.u.p, c.tm.p, M->m, 2.0, c.s));
-    CK(eqb::launch_exp(c.v.p, c.tn.p, M->n, 2.0, c.s));
-    CK(eqb::launch_rms_terms(0, M->A, c.tm.p, c.tn.p, terms.p, 0, alpha, c.s));
-    CK(eqb::launch_rms_terms(1, M->AT, c.tm.p, c.tn.p, terms.p + M->m, 0, beta, c.s));
-    canon_reduce(M, terms.p, M->m + M->n, M->scal.p + 58, 1);
-    *out = std::sqrt(read_scalar(M, M->scal.p + 58) / static_cast<double>(M->m + M->n));
-  });
-}
-
-// project_box (src/equilibrate.cpp:73-76), host
-equil_status equil_project_box(const double* x, int64_t n, double bound, double* out) {
-  return guarded([&] {
-    require(bound >= 0.0, "project_box: bound must be nonnegative");
-    require(n == 0 || (x && out), "project_box: null argument");
-    for (int64_t i = 0; i < n; ++i) {
-      const double lo = x[i] < -bound ? -bound : x[i];  // cwiseMax(-bound)
-      out[i] = bound < lo ? bound : lo;                  // cwiseMin(bound)
-    }
-  });
-}
-
-}  // extern "C"

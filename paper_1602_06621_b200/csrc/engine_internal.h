@@ -1,0 +1,386 @@
+// engine_internal.h -- shared internals of the host engine (engine.cu,
+// engine_ext.cu): error plumbing of the C ABI, pooled device buffers, the
+// parameter rules of src/params.cpp, the traversal plan types and the
+// equil_matrix handle itself.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/equil_b200.h"
+#include "internal.h"
+#include "mmio.h"
+#include "mt64_host.h"
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (the process that drives us -- e.g. torch -- has
+// usually loaded libnccl.so.2 already; dlopen then returns that copy).
+// ---------------------------------------------------------------------------
+namespace eqe {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int ncclUint8 = 1, ncclUint32 = 3, ncclFloat64 = 8, ncclMax = 2;
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+inline NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
+             api.AllReduce;
+  });
+  return api;
+}
+
+inline thread_local std::string g_err;
+
+struct Fail {
+  equil_status code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(equil_status c, const std::string& m) { throw Fail{c, m}; }
+inline void require(bool c, const std::string& m) {
+  if (!c) fail(EQUIL_EINVAL, m);
+}
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? EQUIL_ENOMEM : EQUIL_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) cuda_check((x), #x)
+inline void nccl_check(ncclResult_t r, const char* what) {
+  if (r != 0) {
+    const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
+    fail(EQUIL_ENCCL, std::string(what) + ": " + s);
+  }
+}
+
+template <class F>
+equil_status guarded(F&& f) {
+  try {
+    f();
+    return EQUIL_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return EQUIL_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return EQUIL_ERUNTIME;
+  }
+}
+
+// EQUIL_VERBOSE=1: per-phase wall times of setup calls (synchronizing; debug only)
+struct PhaseTimer {
+  const char* what;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(const char* w)
+      : what(w), on(getenv("EQUIL_VERBOSE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(cudaStream_t s, const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[equil] %s %-14s %8.2f ms\n", what, phase,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
+// Device buffers come from the device's stream-ordered memory pool (release
+// threshold kept at max), allocated on a private per-device stream and made
+// visible before use, so repeated matrix setups reuse already-mapped memory
+// instead of paying cudaMalloc / cudaFree page mapping every time.  Release
+// keeps cudaFree's semantics: the device is synchronised before the memory goes
+// back to the pool.
+inline cudaStream_t alloc_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    cudaGetLastError();
+  }
+  return streams[dev];
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int dev = -1;         // >= 0: pool allocation on alloc_stream(dev)
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    int d = 0;
+    CK(cudaGetDevice(&d));
+    cudaStream_t s = alloc_stream(d);
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    CK(cudaStreamSynchronize(s));
+    dev = d;
+    n = count;
+  }
+  void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'ed array
+    release();
+    p = q;
+    n = count;
+    dev = -1;
+  }
+  void ensure(size_t count) {
+    if (count > n || !p) alloc(count);
+  }
+  void release() {
+    if (p) {
+      if (dev >= 0) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        cudaDeviceSynchronize();  // like cudaFree: nothing may still use p
+        cudaFreeAsync(p, alloc_stream(dev));
+        if (cur != dev) cudaSetDevice(cur);
+      } else {
+        cudaFree(p);
+      }
+    }
+    p = nullptr;
+    n = 0;
+    dev = -1;
+  }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(dev, o.dev);
+  }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---- params (src/params.cpp:7-44) -----------------------------------------
+inline void resolve_targets(const equil_params& p, int64_t rows, int64_t cols,
+                     double& alpha, double& beta) {
+  require(rows > 0 && cols > 0, "resolve_targets: dimensions must be positive");
+  require(p.alpha >= 0.0 && p.beta >= 0.0,
+          "resolve_targets: targets must be positive (or 0 for auto)");
+  const double m = static_cast<double>(rows);
+  const double n = static_cast<double>(cols);
+  alpha = p.alpha;
+  beta = p.beta;
+  if (alpha == 0.0 && beta == 0.0) {
+    alpha = std::pow(n / m, 0.25);
+    beta = std::pow(m / n, 0.25);
+  } else if (beta == 0.0) {
+    beta = alpha * std::sqrt(m / n);
+  } else if (alpha == 0.0) {
+    alpha = beta * std::sqrt(n / m);
+  } else {
+    const double lhs = m * alpha * alpha;
+    const double rhs = n * beta * beta;
+    require(std::abs(lhs - rhs) <= 1e-8 * std::max(lhs, rhs),
+            "resolve_targets: m*alpha^2 == n*beta^2 violated");
+  }
+}
+
+inline void validate_params(const equil_params& p) {
+  require(p.gamma > 0.0, "params: gamma must be positive");
+  require(p.max_log_scale > 0.0, "params: max_log_scale must be positive");
+  require(p.iterations >= 0, "params: iterations must be nonnegative");
+  require(std::isfinite(p.gamma) && std::isfinite(p.max_log_scale),
+          "params: gamma and max_log_scale must be finite");
+}
+
+// ---- traversal plan ---------------------------------------------------------
+// Rows longer than kTileNnz become kind-3 long slices (32 length-sorted rows
+// per CTA); all other rows are grouped into kind-2 slices: within windows of
+// kSliceWindow consecutive rows, rows are sorted by length (longest first) and
+// cut into groups of 32, so the lanes of a slice have similar chain lengths and
+// the epilogue's scattered writes stay inside one window.  The row order never
+// affects results: each row is an independent sequential sum.  Windows are
+// planned in parallel host threads; the result does not depend on the thread
+// count (parts are concatenated in window order, ties keep row order).
+struct Plan {
+  std::vector<eqb::Tile> lng, slices;
+  std::vector<int32_t> rowlist;
+};
+
+Plan plan_tiles(const int64_t* rp, int64_t rows, int mat);
+std::vector<int64_t> partition_rows(const int64_t* rp, int64_t rows, int parts);
+
+}  // namespace eqe
+
+// The device-resident matrix behind the opaque handle of include/equil_b200.h.
+using namespace eqe;
+// ---------------------------------------------------------------------------
+struct equil_matrix {
+  int device = 0, rank = 0, world = 1;
+  bool dense = false;
+  int64_t m = 0, n = 0, nnz = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // uploads that overlap work on `stream`
+  cudaEvent_t ev_vals = nullptr;       // values of A on the device
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::mutex mu;
+  ncclComm_t comm = nullptr;
+
+  // sparse shards (local rows, columns in padded coordinates)
+  eqb::DevCsr A, AT;
+  DevBuf<int64_t> a_rp, t_rp;
+  DevBuf<int32_t> a_ci, t_ci;
+  DevBuf<double> a_va, t_va;
+  std::vector<int64_t> a_bounds, t_bounds;  // partitions of rows / columns
+  int64_t a_max = 0, t_max = 0;             // padded slice sizes
+  DevBuf<int64_t> a_bounds_d, t_bounds_d;
+  DevBuf<eqb::Tile> tiles_sgd, tiles_a, tiles_t;
+  DevBuf<int32_t> rowlist_a, rowlist_t;
+  int n_sgd = 0, n_a = 0, n_t = 0;
+  int n_sgd_long = 0;  // leading kind-3 entries of tiles_sgd
+  // column-panel layout of the local A / A^T shards (panel.cu), built when
+  // EQUIL_PANEL=1 at creation; n_pbands == 0 selects the row-slice traversal
+  // above (the default: faster on B200)
+  bool use_panels = false;
+  // hot-first slot layout of the gathered vectors (build_slot_layout): the SGD
+  // passes read CSR copies whose column indices point at slots, and the
+  // epilogues write each row's next value at its slot
+  bool use_slots = true;
+  bool slots = false;
+  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wmap, smap;  // wmap / smap: padded position -> slot
+  DevBuf<double> pval[2];
+  DevBuf<uint16_t> pcol[2];
+  DevBuf<uint32_t> pruns[2];
+  DevBuf<eqb::PanelChunk> pchunks[2];
+  DevBuf<eqb::PanelBand> pbands;
+  int n_pbands = 0;
+
+  // dense
+  DevBuf<double> Ad, colpart;
+
+  // workspaces
+  // padded gathered vectors e.*s (xs) and d.*w (xw), double-buffered, in one
+  // allocation so a single L2 persisting window covers every gather target
+  struct Slot {
+    double* p = nullptr;
+  } xs[2], xw[2];
+  DevBuf<double> xbuf;
+  DevBuf<double> u, ub, v, vb;  // local
+  DevBuf<uint32_t> signs;
+  DevBuf<unsigned char> sign_scratch;
+  DevBuf<unsigned> flags;
+  DevBuf<double> red_part;
+  DevBuf<unsigned> red_counter;
+  DevBuf<double> scal;  // small device scalars
+  DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
+  DevBuf<double> lin_u, lin_v;  // per-coordinate targets (sgd_equilibrate_targets)
+
+  // graph cache for the SGD loop
+  cudaGraphExec_t graph = nullptr;
+  long long graph_launches = 0;  // kernel nodes per replay
+  struct Key {
+    int T = -1;
+    double alpha = 0, beta = 0, gamma = 0, M = 0;
+    bool vec_lin = false;
+    bool operator==(const Key& o) const {
+      return T == o.T && alpha == o.alpha && beta == o.beta && gamma == o.gamma && M == o.M &&
+             vec_lin == o.vec_lin;
+    }
+  } graph_key;
+
+  int64_t m_loc() const { return dense ? m : a_bounds[rank + 1] - a_bounds[rank]; }
+  int64_t n_loc() const { return dense ? n : t_bounds[rank + 1] - t_bounds[rank]; }
+  int64_t a_goff() const { return dense ? 0 : a_bounds[rank]; }
+  int64_t t_goff() const { return dense ? 0 : t_bounds[rank]; }
+  int64_t m_pad() const { return world == 1 ? m : a_max * world; }
+  int64_t n_pad() const { return world == 1 ? n : t_max * world; }
+
+  // events bracketing the T-iteration loop of the last sgd call (also inside
+  // the captured graph), for the live per-kernel roofline in bench.py
+  cudaEvent_t ev_loop0 = nullptr, ev_loop1 = nullptr;
+  double last_loop_ms = 0.0;
+  int last_loop_iters = 0;
+
+  ~equil_matrix() {
+    if (ev_loop0) cudaEventDestroy(ev_loop0);
+    if (ev_loop1) cudaEventDestroy(ev_loop1);
+    if (graph) cudaGraphExecDestroy(graph);
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
+    if (ev_vals) cudaEventDestroy(ev_vals);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+
+namespace eqe {
+// defined in engine.cu, used by the extension entry points (engine_ext.cu)
+void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, int kind,
+                  double coef = 0.0, bool sqrt_out = false);
+void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
+                const double* scale, const double* prev, const double* coef);
+double read_scalar(equil_matrix* M, const double* dev);
+void create_coo_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                     const int64_t* cols, const double* vals, const int64_t* lines,
+                     const equil_device_cfg* cfg, equil_matrix** out);
+}  // namespace eqe
