@@ -664,3 +664,29 @@ def test_equilibrate_helpers_vs_reference_golden(golden, key):
         eq.project_box(np.zeros(2), -1.0)
     with pytest.raises(eq.InvalidArgument, match="targets must be positive"):
         eq.rms_error(M, u, v, 0.0, 1.0)
+
+
+# ---------------------------------------------------------------- degenerate inputs
+@pytest.mark.parametrize("m,n,entries", [(4, 3, []), (1, 1, [(0, 0, 2.0)]),
+                                         (5, 7, [(4, 6, -1.5)]), (1, 9, [(0, 2, 1.0), (0, 8, 3.0)])])
+def test_degenerate_sparse_inputs_vs_oracle(C, m, n, entries):
+    """No entries at all, a single entry, one row: SGD and LSQR through the
+    CSR and COO constructors agree with the oracle (breakdown included)."""
+    rows = np.array([e[0] for e in entries], np.int64)
+    cols = np.array([e[1] for e in entries], np.int64)
+    vals = np.array([e[2] for e in entries], np.float64)
+    rp = np.zeros(m + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    rp = np.cumsum(rp)
+    A = oracle.CsrArrays(m, n, rp, cols.astype(np.int32), vals)
+    want = C.sgd_equilibrate(A, iterations=25, seed=3)
+    for M in (eq.ExplicitMatrix.from_csr(m, n, rp, cols, vals),
+              eq.ExplicitMatrix.sparse(m, n, (rows, cols, vals))):
+        got = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=25, seed=3))
+        for k in "uvde":
+            assert np.array_equal(getattr(got, k), getattr(want, k)), k
+        b = np.arange(1, m + 1, dtype=np.float64)
+        lw = C.lsqr(A, b, 5, 0.0)
+        lg = eq.lsqr(M, b, 5, 0.0)
+        assert np.array_equal(lg.residual_history, lw.residual_history)
+        assert (lg.iterations, lg.breakdown) == (lw.iterations, lw.breakdown)
