@@ -1297,6 +1297,30 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
   CK(eqb::launch_pass(a, adjoint ? M->n_t : M->n_a, M->stream));
 }
 
+// two passes of A (not the adjoint) sharing one traversal of CSR(A):
+// out0 <- (xg0, mode0, ...), out1 <- (xg1, mode1, ...); dense: two passes
+void apply_pass_dual(equil_matrix* M, const double* xg0, double* out0, int mode0,
+                     const double* scale0, const double* prev0, const double* coef0,
+                     const double* xg1, double* out1, int mode1, const double* scale1,
+                     const double* prev1, const double* coef1) {
+  if (M->dense) {
+    apply_pass(M, false, xg0, out0, mode0, scale0, prev0, coef0);
+    apply_pass(M, false, xg1, out1, mode1, scale1, prev1, coef1);
+    return;
+  }
+  eqb::PassArgs a{}, b{};
+  for (eqb::PassArgs* p : {&a, &b}) {
+    p->rp = M->A.row_ptr;
+    p->ci = M->A.col;
+    p->va = M->A.val;
+    p->tiles = M->tiles_a.p;
+    p->rl = M->rowlist_a.p;
+  }
+  a.xg = xg0; a.out = out0; a.mode = mode0; a.scale = scale0; a.prev = prev0; a.coef = coef0;
+  b.xg = xg1; b.out = out1; b.mode = mode1; b.scale = scale1; b.prev = prev1; b.coef = coef1;
+  CK(eqb::launch_pass_dual(a, b, M->n_a, M->stream));
+}
+
 double read_scalar(equil_matrix* M, const double* dev) {
   double h = 0;
   CK(cudaMemcpyAsync(&h, dev, 8, cudaMemcpyDeviceToHost, M->stream));
@@ -1395,7 +1419,9 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
 
   for (int t = 1; t <= max_iters; ++t) {
     bool invariant = false;
-    apply_pass(M, false, ev.p, unL, eqb::kPassLsqrU, d, u.p, sc + 1);  // Bv - alpha u
+    // un = Bv - alpha u: computed here for t = 1, afterwards by the fused pass at
+    // the end of the previous iteration (same arithmetic, one A traversal less)
+    if (t == 1) apply_pass(M, false, ev.p, unL, eqb::kPassLsqrU, d, u.p, sc + 1);
     ++st.applies;
     L.norm(un.p, true, sc + 0);
     beta = read_scalar(M, sc + 0);
@@ -1428,7 +1454,10 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, exL, L.nL, s));
     L.gather(ex.p, false);
     st.iterations = t;
-    apply_pass(M, false, ex.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr);
+    // residual b - A(e.x) and, in the same traversal of A, the next iteration's
+    // B v - alpha u (its inputs v, alpha, u are final here; unused if we stop)
+    apply_pass_dual(M, ex.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, ev.p, unL,
+                    eqb::kPassLsqrU, d, u.p, sc + 1);
     L.norm(r.p, true, sc + 2);
     const double rel = read_scalar(M, sc + 2) / bnorm;
     if (st.hist_len < hist_cap) hist[st.hist_len] = rel;

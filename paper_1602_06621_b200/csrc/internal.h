@@ -230,6 +230,9 @@ cudaError_t launch_sgd_iter_part(const SgdIterArgs& a, int tile_base, int ntiles
 cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
                        cudaStream_t s);
 cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s);
+// two passes over the same matrix (same tiles) in one traversal: a and b differ
+// only in the gathered vector and the epilogue (LSQR: residual + next B v)
+cudaError_t launch_pass_dual(const PassArgs& a, const PassArgs& b, int ntiles, cudaStream_t s);
 
 // canonical reduction (det_math.cuh) of terms x*x (kind 0), x (kind 1) or
 // coef*x (kind 2); *out (device) = result, or its sqrt when sqrt_out

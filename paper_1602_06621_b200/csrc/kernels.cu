@@ -555,13 +555,16 @@ namespace {
 // (coalesced, aligned chunks) into a padded [32][kLongStride] buffer, then warp
 // 0's 32 lanes each extend one row's sequential sum with conflict-free 16-byte
 // reads -- 32 chains in parallel instead of one lane-0 chain per warp.
-template <class Epi>
+// NV = 2 (LSQR's fused pass): a second gathered vector xg2 rides along; its
+// products go to a second staging buffer and a second sequential chain.
+template <class Epi, int NV = 1>
 __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __restrict__ rp,
                                                const int32_t* __restrict__ ci,
                                                const double* __restrict__ va,
                                                const double* __restrict__ xg,
                                                const int32_t* __restrict__ rowlist,
-                                               double* sp, SliceMeta& sm, Epi& epi) {
+                                               double* sp, SliceMeta& sm, Epi& epi,
+                                               const double* __restrict__ xg2 = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = t.r1;
   int myrow = -1, mk0 = 0, mlen = 0, rounds = 0;
@@ -579,7 +582,8 @@ __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __r
   }
   __syncthreads();
   const int maxr = sm.maxr;
-  double acc = 0.0;
+  double acc = 0.0, acc2 = 0.0;
+  double* sp2 = sp + 32 * kLongStride;  // NV == 2 only
   for (int b = 0; b < maxr; ++b) {
     const int off = b * kLongChunk;
     // warp w stages rows w, w+4, ... : kLongChunk / 32 products per lane per row
@@ -609,26 +613,36 @@ __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __r
       for (int u = 0; u < kLongBatch; ++u)
 #pragma unroll
         for (int h = 0; h < kPer; ++h)
-          if (ok[kPer * u + h])
-            sp[(q0 + 4 * u) * kLongStride + lane + 32 * h] =
-                __dmul_rn(v[kPer * u + h], __ldg(xg + c[kPer * u + h]));
+          if (ok[kPer * u + h]) {
+            const int at = (q0 + 4 * u) * kLongStride + lane + 32 * h;
+            sp[at] = __dmul_rn(v[kPer * u + h], __ldg(xg + c[kPer * u + h]));
+            if constexpr (NV == 2) sp2[at] = __dmul_rn(v[kPer * u + h], __ldg(xg2 + c[kPer * u + h]));
+          }
     }
     __syncthreads();
-    if (warp == 0 && rounds > b)
+    if (warp == 0 && rounds > b) {
       acc = chain_sum(acc, sp + lane * kLongStride, max(0, mk0 - off),
                       min(kLongChunk, mlen - off));
+      if constexpr (NV == 2)
+        acc2 = chain_sum(acc2, sp2 + lane * kLongStride, max(0, mk0 - off),
+                         min(kLongChunk, mlen - off));
+    }
     __syncthreads();
   }
-  if (warp == 0 && myrow >= 0) epi(myrow, acc);
+  if (warp == 0 && myrow >= 0) {
+    if constexpr (NV == 2) epi(myrow, acc, acc2);
+    else epi(myrow, acc);
+  }
 }
 
-template <class Epi>
+template <class Epi, int NV = 1>
 __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restrict__ rp,
                                          const int32_t* __restrict__ ci,
                                          const double* __restrict__ va,
                                          const double* __restrict__ xg,
                                          const int32_t* __restrict__ rowlist, double* sp,
-                                         SliceMeta& sm, int lane, Epi& epi) {
+                                         SliceMeta& sm, int lane, Epi& epi,
+                                         const double* __restrict__ xg2 = nullptr) {
   {
     // Slice: up to 32 rows (sorted by length, longest first), one per lane, in
     // lock-step rounds of kSliceChunk products per row.  Each round the warp
@@ -649,7 +663,8 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
     const int maxr = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(rounds)));
     __syncwarp();
     const int half = lane >> 4, e = lane & 15;
-    double acc = 0.0;
+    double acc = 0.0, acc2 = 0.0;
+    double* sp2 = sp + 32 * kSliceStride;  // NV == 2 only
     for (int b = 0; b < maxr; ++b) {
       const int off = b * kSliceChunk;
 #if EQ_SLICE_PREFETCH
@@ -684,7 +699,10 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
 #pragma unroll
         for (int u = 0; u < kSliceBatch; ++u) {
           const int q = q0 + 2 * u + half;
-          if (ok[u]) sp[q * kSliceStride + e] = __dmul_rn(v[u], __ldg(xg + c[u]));
+          if (ok[u]) {
+            sp[q * kSliceStride + e] = __dmul_rn(v[u], __ldg(xg + c[u]));
+            if constexpr (NV == 2) sp2[q * kSliceStride + e] = __dmul_rn(v[u], __ldg(xg2 + c[u]));
+          }
         }
       }
       __syncwarp();
@@ -692,10 +710,14 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
         const int lo = max(0, mk0 - off);
         const int hi = min(kSliceChunk, mlen - off);
         acc = chain_sum(acc, sp + lane * kSliceStride, lo, hi);
+        if constexpr (NV == 2) acc2 = chain_sum(acc2, sp2 + lane * kSliceStride, lo, hi);
       }
       __syncwarp();
     }
-    if (myrow >= 0) epi(myrow, acc);
+    if (myrow >= 0) {
+      if constexpr (NV == 2) epi(myrow, acc, acc2);
+      else epi(myrow, acc);
+    }
   }
 }
 
@@ -720,11 +742,11 @@ sgd_iter_kernel(const SgdIterArgs a, int tile_base, int ntiles) {
   const int mat = t.mat;
   SgdEpi epi{a, mat, 0u};
   if ((KINDS & 2) && t.kind == 3)  // CTA-cooperative (all 4 warps hold this tile)
-    run_long_slice(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
-                   a.rl[mat], &sp[0][0], sm[0], epi);
+    run_long_slice<SgdEpi, 1>(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
+                              a.rl[mat], &sp[0][0], sm[0], epi);
   else if (KINDS & 1)
-    run_tile(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur, a.rl[mat],
-             sp[warp], sm[warp], lane, epi);
+    run_tile<SgdEpi, 1>(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
+                        a.rl[mat], sp[warp], sm[warp], lane, epi);
   if (epi.fl) atomicOr(a.flags, epi.fl);
 }
 
@@ -911,27 +933,58 @@ struct PassEpi {
   const PassArgs& a;
   __device__ void operator()(int64_t r, double acc) { pass_epilogue(a, r, acc); }
 };
+struct PassEpi2 {
+  const PassArgs& a;
+  const PassArgs& b;
+  __device__ void operator()(int64_t r, double acc, double acc2) {
+    pass_epilogue(a, r, acc);
+    pass_epilogue(b, r, acc2);
+  }
+};
 
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) pass_kernel(const PassArgs a, int ntiles) {
-  __shared__ __align__(16) double sp[kTileWarps][kWarpSmem];
+// NV = 2: two passes over the same matrix in one traversal (shared value and
+// column streams, two gathers per entry, two sequential sums per row)
+template <int NV>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+pass_kernel(const PassArgs a, const PassArgs b, int ntiles) {
+  constexpr int kWarpDoubles = NV == 2 ? 2 * 32 * kSliceStride : kWarpSmem;
+  static_assert(NV == 1 || 2 * 32 * kLongStride <= kTileWarps * kWarpDoubles, "long staging");
+  __shared__ __align__(16) double sp[kTileWarps][kWarpDoubles];
   __shared__ SliceMeta sm[kTileWarps];
   if (a.skip && *a.skip) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = blockIdx.x * kTileWarps + warp;
   if (tid >= ntiles) return;
-  PassEpi epi{a};
   const Tile t = a.tiles[tid];
-  if (t.kind == 3)
-    run_long_slice(t, a.rp, a.ci, a.va, a.xg, a.rl, &sp[0][0], sm[0], epi);
-  else
-    run_tile(t, a.rp, a.ci, a.va, a.xg, a.rl, sp[warp], sm[warp], lane, epi);
+  if constexpr (NV == 1) {
+    PassEpi epi{a};
+    if (t.kind == 3)
+      run_long_slice<PassEpi, 1>(t, a.rp, a.ci, a.va, a.xg, a.rl, &sp[0][0], sm[0], epi);
+    else
+      run_tile<PassEpi, 1>(t, a.rp, a.ci, a.va, a.xg, a.rl, &sp[warp][0], sm[warp], lane, epi);
+  } else {
+    PassEpi2 epi{a, b};
+    if (t.kind == 3)
+      run_long_slice<PassEpi2, 2>(t, a.rp, a.ci, a.va, a.xg, a.rl, &sp[0][0], sm[0], epi, b.xg);
+    else
+      run_tile<PassEpi2, 2>(t, a.rp, a.ci, a.va, a.xg, a.rl, &sp[warp][0], sm[warp], lane, epi,
+                            b.xg);
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s) {
   if (ntiles == 0) return cudaSuccess;
-  pass_kernel<<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, ntiles); count_launch(s);
+  pass_kernel<1><<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, a, ntiles);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pass_dual(const PassArgs& a, const PassArgs& b, int ntiles, cudaStream_t s) {
+  if (ntiles == 0) return cudaSuccess;
+  pass_kernel<2><<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, b, ntiles);
+  count_launch(s);
   return cudaGetLastError();
 }
 
