@@ -233,6 +233,9 @@ cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s);
 // two passes over the same matrix (same tiles) in one traversal: a and b differ
 // only in the gathered vector and the epilogue (LSQR: residual + next B v)
 cudaError_t launch_pass_dual(const PassArgs& a, const PassArgs& b, int ntiles, cudaStream_t s);
+// tiles [tile_base, tile_base + ntiles); b non-null: the dual pass
+cudaError_t launch_pass_range(const PassArgs& a, const PassArgs* b, int tile_base, int ntiles,
+                              cudaStream_t s);
 
 // canonical reduction (det_math.cuh) of terms x*x (kind 0), x (kind 1) or
 // coef*x (kind 2); *out (device) = result, or its sqrt when sqrt_out

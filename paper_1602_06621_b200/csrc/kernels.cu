@@ -946,7 +946,7 @@ struct PassEpi2 {
 // column streams, two gathers per entry, two sequential sums per row)
 template <int NV>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
-pass_kernel(const PassArgs a, const PassArgs b, int ntiles) {
+pass_kernel(const PassArgs a, const PassArgs b, int tile_base, int ntiles) {
   constexpr int kWarpDoubles = NV == 2 ? 2 * 32 * kSliceStride : kWarpSmem;
   static_assert(NV == 1 || 2 * 32 * kLongStride <= kTileWarps * kWarpDoubles, "long staging");
   __shared__ __align__(16) double sp[kTileWarps][kWarpDoubles];
@@ -955,7 +955,7 @@ pass_kernel(const PassArgs a, const PassArgs b, int ntiles) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = blockIdx.x * kTileWarps + warp;
   if (tid >= ntiles) return;
-  const Tile t = a.tiles[tid];
+  const Tile t = a.tiles[tile_base + tid];
   if constexpr (NV == 1) {
     PassEpi epi{a};
     if (t.kind == 3)
@@ -974,18 +974,24 @@ pass_kernel(const PassArgs a, const PassArgs b, int ntiles) {
 
 }  // namespace
 
-cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s) {
-  if (ntiles == 0) return cudaSuccess;
-  pass_kernel<1><<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, a, ntiles);
+cudaError_t launch_pass_range(const PassArgs& a, const PassArgs* b, int tile_base, int ntiles,
+                              cudaStream_t s) {
+  if (ntiles <= 0) return cudaSuccess;
+  const unsigned g = static_cast<unsigned>((ntiles + kTileWarps - 1) / kTileWarps);
+  if (b)
+    pass_kernel<2><<<g, kTileThreads, 0, s>>>(a, *b, tile_base, ntiles);
+  else
+    pass_kernel<1><<<g, kTileThreads, 0, s>>>(a, a, tile_base, ntiles);
   count_launch(s);
   return cudaGetLastError();
 }
 
+cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s) {
+  return launch_pass_range(a, nullptr, 0, ntiles, s);
+}
+
 cudaError_t launch_pass_dual(const PassArgs& a, const PassArgs& b, int ntiles, cudaStream_t s) {
-  if (ntiles == 0) return cudaSuccess;
-  pass_kernel<2><<<(ntiles + kTileWarps - 1) / kTileWarps, kTileThreads, 0, s>>>(a, b, ntiles);
-  count_launch(s);
-  return cudaGetLastError();
+  return launch_pass_range(a, &b, 0, ntiles, s);
 }
 
 // ---------------------------------------------------------------------------
