@@ -547,6 +547,7 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
                                      const int32_t* col, const double* val,
                                      const equil_device_cfg* cfg, equil_matrix** out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:create_csr");
     require(out != nullptr, "ExplicitMatrix::sparse: null output handle");
     *out = nullptr;
     require(m > 0 && n > 0, "ExplicitMatrix::sparse: dimensions must be positive");
@@ -704,12 +705,16 @@ extern "C" {
 equil_status equil_matrix_create_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
                                      const int64_t* cols, const double* vals,
                                      const equil_device_cfg* cfg, equil_matrix** out) {
-  return guarded([&] { create_coo_impl(m, n, nnz, rows, cols, vals, nullptr, cfg, out); });
+  return guarded([&] {
+    NvtxRange nvtx_("equil:create_coo");
+    create_coo_impl(m, n, nnz, rows, cols, vals, nullptr, cfg, out);
+  });
 }
 
 equil_status equil_matrix_create_dense(int64_t m, int64_t n, const double* rowmajor,
                                        const equil_device_cfg* cfg, equil_matrix** out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:create_dense");
     require(out != nullptr, "ExplicitMatrix::dense: null output handle");
     *out = nullptr;
     require(m > 0 && n > 0, "ExplicitMatrix::dense: dimensions must be positive");
@@ -1230,6 +1235,7 @@ extern "C" equil_status equil_sgd_equilibrate(equil_matrix* M, const equil_param
                                               const equil_diag_cfg* diag,
                                               equil_scaling_out* out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:sgd_equilibrate");
     require(M != nullptr && p != nullptr && out != nullptr, "sgd_equilibrate: null argument");
     double alpha = 0, beta = 0;
     resolve_targets(*p, M->m, M->n, alpha, beta);  // src/equilibrate.cpp:216
@@ -1242,6 +1248,7 @@ extern "C" equil_status equil_sgd_equilibrate_targets(equil_matrix* M, const dou
                                                       const equil_diag_cfg* diag,
                                                       equil_scaling_out* out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:sgd_equilibrate_targets");
     require(M != nullptr && p != nullptr && out != nullptr,
             "sgd_equilibrate_targets: null argument");
     require(r != nullptr && c != nullptr, "sgd_equilibrate_targets: target length mismatch");
@@ -1559,13 +1566,17 @@ extern "C" {
 
 equil_status equil_lsqr(equil_matrix* A, const double* b, int max_iters, double tol,
                         equil_lsqr_out* out) {
-  return guarded([&] { lsqr_common(A, b, nullptr, max_iters, tol, out, "lsqr"); });
+  return guarded([&] {
+    NvtxRange nvtx_("equil:lsqr");
+    lsqr_common(A, b, nullptr, max_iters, tol, out, "lsqr");
+  });
 }
 
 equil_status equil_lsqr_preconditioned(equil_matrix* A, const double* b,
                                        const equil_params* p, int max_iters, double tol,
                                        equil_lsqr_out* out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:lsqr_preconditioned");
     require(p != nullptr, "lsqr_preconditioned: null params");
     lsqr_common(A, b, p, max_iters, tol, out, "lsqr_preconditioned");
   });

@@ -308,6 +308,7 @@ equil_status equil_sgd_equilibrate_symmetric(equil_matrix* M, const equil_params
                                              const equil_diag_cfg* diag,
                                              equil_scaling_out* out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:sgd_equilibrate_symmetric");
     require(M != nullptr && p != nullptr && out != nullptr,
             "sgd_equilibrate_symmetric: null argument");
     sgd_variant(M, Variant::kSymmetric, p, diag, out, nullptr, nullptr, 0, 0);
@@ -319,6 +320,7 @@ equil_status equil_sgd_equilibrate_block(equil_matrix* M, const int64_t* row_blo
                                          int64_t col_blocks, const equil_params* p,
                                          const equil_diag_cfg* diag, equil_scaling_out* out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:sgd_equilibrate_block");
     require(M != nullptr && p != nullptr && out != nullptr,
             "sgd_equilibrate_block: null argument");
     sgd_variant(M, Variant::kBlock, p, diag, out, row_block, col_block, row_blocks, col_blocks);
@@ -547,13 +549,17 @@ equil_status equil_lasso_objective(equil_matrix* M, const double* b, double lamb
 
 equil_status equil_ccp_lasso(equil_matrix* M, const double* b, double lambda,
                              const equil_ccp_options* o, equil_ccp_out* out) {
-  return guarded([&] { ccp_common(M, b, lambda, nullptr, o, out, "ccp_lasso"); });
+  return guarded([&] {
+    NvtxRange nvtx_("equil:ccp_lasso");
+    ccp_common(M, b, lambda, nullptr, o, out, "ccp_lasso");
+  });
 }
 
 equil_status equil_ccp_lasso_preconditioned(equil_matrix* M, const double* b, double lambda,
                                             const equil_params* p, const equil_ccp_options* o,
                                             equil_ccp_out* out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:ccp_lasso_preconditioned");
     require(p != nullptr, "ccp_lasso_preconditioned: null params");
     ccp_common(M, b, lambda, p, o, out, "ccp_lasso_preconditioned");
   });
@@ -596,6 +602,7 @@ extern "C" {
 equil_status equil_matrix_read_matrix_market(const char* path, const equil_device_cfg* cfg,
                                              equil_matrix** out) {
   return guarded([&] {
+    NvtxRange nvtx_("equil:read_matrix_market");
     require(path != nullptr && out != nullptr, "matrix market: null argument");
     *out = nullptr;
     std::string buf;

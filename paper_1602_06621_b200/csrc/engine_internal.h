@@ -19,6 +19,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/equil_b200.h"
 #include "internal.h"
 #include "mmio.h"
@@ -114,6 +116,14 @@ equil_status guarded(F&& f) {
   }
 }
 
+// NVTX range for profilers (nsys / ncu --nvtx): one per C ABI call and phase
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // EQUIL_VERBOSE=1: per-phase wall times of setup calls (synchronizing; debug only)
 struct PhaseTimer {
   const char* what;
@@ -122,6 +132,7 @@ struct PhaseTimer {
   explicit PhaseTimer(const char* w)
       : what(w), on(getenv("EQUIL_VERBOSE") != nullptr), t(std::chrono::steady_clock::now()) {}
   void mark(cudaStream_t s, const char* phase) {
+    nvtxMarkA(phase);
     if (!on) return;
     cudaStreamSynchronize(s);
     const auto now = std::chrono::steady_clock::now();
