@@ -252,6 +252,34 @@ void build_panel_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT)
   M->n_pbands = static_cast<int>(h.size());
 }
 
+// Column blocks for gathered vectors larger than L2.  When the vector a pass
+// gathers from (xs for A, xw for A^T) exceeds EQUIL_BLOCK_MB (default 60 MB,
+// measured best on c5 among 20-80 MB: blocks of 40-53 MB), its coordinates are cut
+// into nb contiguous blocks and each iteration visits every row block by block
+// in nb launches, carrying the row's running sum between them (SgdEpi::span).
+// A row's entries of one block are contiguous and blocks ascend, so the sum
+// order is unchanged.  The slot layout is not used with blocks.
+void build_block_layout(equil_matrix* M) {
+  M->nblk[0] = M->nblk[1] = 1;
+  if (M->use_panels) return;
+  double mb = 60.0;
+  if (const char* e = getenv("EQUIL_BLOCK_MB")) mb = std::max(1.0, atof(e));
+  const int64_t lens[2] = {M->n_pad(), M->m_pad()};
+  for (int mat = 0; mat < 2; ++mat) {
+    const double bytes = static_cast<double>(lens[mat]) * 8.0;
+    const int nb = static_cast<int>(std::ceil(bytes / (mb * 1e6)));
+    if (nb <= 1) continue;
+    const eqb::DevCsr& C = mat ? M->AT : M->A;
+    const int64_t width = (lens[mat] + nb - 1) / nb;
+    M->nblk[mat] = nb;
+    M->bwidth[mat] = width;
+    M->bnd[mat].alloc(std::max<int64_t>(1, C.rows * (nb - 1)));
+    M->carry[mat].alloc(std::max<int64_t>(1, C.rows));
+    CK(eqb::launch_block_bounds(C, nb, width, M->bnd[mat].p, M->stream));
+  }
+  if (M->nblk[0] > 1 || M->nblk[1] > 1) M->use_slots = false;
+}
+
 // Hot-first slot layout.  In the A^T pass every entry of A's row i gathers
 // xw[i], so row i is read len(row i) times per iteration; with Zipf row lengths
 // a few thousand rows take most gathers (c3: the 20k longest rows, 156 KB, take
@@ -356,6 +384,7 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
                plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
   build_panel_layout(M, la.data(), lt.data());
+  build_block_layout(M);
   build_slot_layout(M, fullA.row_ptr, fullT.row_ptr);
 }
 
@@ -420,6 +449,7 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     M->t_va.swap(tva);
     M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
     M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
+    build_block_layout(M);
     build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);  // device work
     if (tplanner.joinable()) tplanner.join();  // planned during the transpose
     pt.mark(s, "plan A^T");
@@ -984,6 +1014,11 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     };
     auto iter_args = [&](int t) {
       eqb::SgdIterArgs a{};
+      for (int k = 0; k < 2; ++k) {  // column blocks (round set per launch)
+        a.nblk[k] = M->nblk[k];
+        a.bnd[k] = M->bnd[k].p;
+        a.carry[k] = M->carry[k].p;
+      }
       for (int k = 0; k < 2; ++k) {
         const eqb::DevCsr& C = k ? M->AT : M->A;
         a.rp[k] = C.row_ptr;
@@ -1062,23 +1097,27 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
         CK(eqb::launch_dense_sgd_iter(dense_args(t), s));
       } else {
         static const int conc = getenv("EQUIL_CONC") ? atoi(getenv("EQUIL_CONC")) : 1;
-        if (M->n_pbands) {
-          CK(eqb::launch_sgd_panel(iter_args(t), panel_args, M->n_pbands, s));
-        } else if (conc && M->n_sgd_long > 0 && M->n_sgd_long < M->n_sgd) {
-          // long-row CTA groups and warp tiles as two concurrent kernels (fork /
-          // join on the copy stream): each kernel gets its own residency on the
-          // SMs instead of one launch sized for both (c3: 4-5% faster)
-          const eqb::SgdIterArgs a = iter_args(t);
-          CK(cudaEventRecord(M->ev_fork, s));
-          CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
-          CK(eqb::launch_sgd_iter_part(a, 0, M->n_sgd_long, true, conc >= 2 ? 8 : 6,
-                                       M->copy_stream));
-          CK(eqb::launch_sgd_iter_part(a, M->n_sgd_long, M->n_sgd - M->n_sgd_long, false,
-                                       conc >= 3 ? 8 : 6, s));
-          CK(cudaEventRecord(M->ev_join, M->copy_stream));
-          CK(cudaStreamWaitEvent(s, M->ev_join, 0));
-        } else {
-          CK(eqb::launch_sgd_iter(iter_args(t), M->n_sgd, s));
+        const int rounds = std::max(M->nblk[0], M->nblk[1]);
+        for (int rd = 0; rd < rounds; ++rd) {  // column-block rounds (1 unless blocked)
+          eqb::SgdIterArgs a = iter_args(t);
+          a.round = rd;
+          if (M->n_pbands) {
+            CK(eqb::launch_sgd_panel(a, panel_args, M->n_pbands, s));
+          } else if (conc && M->n_sgd_long > 0 && M->n_sgd_long < M->n_sgd) {
+            // long-row CTA groups and warp tiles as two concurrent kernels (fork /
+            // join on the copy stream): each kernel gets its own residency on the
+            // SMs instead of one launch sized for both (c3: 4-5% faster)
+            CK(cudaEventRecord(M->ev_fork, s));
+            CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+            CK(eqb::launch_sgd_iter_part(a, 0, M->n_sgd_long, true, conc >= 2 ? 8 : 6,
+                                         M->copy_stream));
+            CK(eqb::launch_sgd_iter_part(a, M->n_sgd_long, M->n_sgd - M->n_sgd_long, false,
+                                         conc >= 3 ? 8 : 6, s));
+            CK(cudaEventRecord(M->ev_join, M->copy_stream));
+            CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+          } else {
+            CK(eqb::launch_sgd_iter(a, M->n_sgd, s));
+          }
         }
         if (t < T) {
           allgather_padded(M, M->xs[t & 1].p, M->t_max);

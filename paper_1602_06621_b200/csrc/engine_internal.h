@@ -316,7 +316,12 @@ struct equil_matrix {
   // epilogues write each row's next value at its slot
   bool use_slots = true;
   bool slots = false;
-  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wmap, smap;  // wmap / smap: padded position -> slot
+  DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wmap, smap;
+  // column blocks of the gathered vectors (build_block_layout): per matrix
+  int nblk[2] = {1, 1};
+  int64_t bwidth[2] = {0, 0};
+  DevBuf<int32_t> bnd[2];
+  DevBuf<double> carry[2];  // wmap / smap: padded position -> slot
   DevBuf<double> pval[2];
   DevBuf<uint16_t> pcol[2];
   DevBuf<uint32_t> pruns[2];

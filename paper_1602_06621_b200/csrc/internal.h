@@ -99,6 +99,13 @@ struct SgdIterArgs {
   // A^T rows), or nullptr for the plain padded position poff + r.  A layout
   // with the most-gathered coordinates packed first keeps them L1-resident.
   const int32_t* slot[2];
+  // column blocks of the gathered vectors (gathers larger than L2): this
+  // launch's round, blocks per matrix (1: none), per-row interior block
+  // boundaries (nblk - 1 offsets into the row) and the carried running sums
+  int round;
+  int nblk[2];
+  const int32_t* bnd[2];
+  double* carry[2];
   SgdStep st;
   unsigned* flags;
 };
@@ -221,6 +228,9 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
 // of each rank ordered by decreasing floor(log2(length)), stable
 cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* bounds, int G,
                             int64_t maxcnt, int32_t* map_pad, cudaStream_t s);
+// column-block boundaries of every row (block b = columns [b*width, (b+1)*width))
+cudaError_t launch_block_bounds(const DevCsr& M, int nb, int64_t width, int32_t* bnd,
+                                cudaStream_t s);
 // dst[k] = map[src[k]] (column indices into a slot layout)
 cudaError_t launch_remap_cols(int32_t* dst, const int32_t* src, const int32_t* map, int64_t nnz,
                               cudaStream_t s);

@@ -568,10 +568,11 @@ __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __r
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = t.r1;
   int myrow = -1, mk0 = 0, mlen = 0, rounds = 0;
+  double acc0 = 0.0;  // running sum carried in (column-block rounds)
   if (warp == 0) {
     myrow = lane < cnt ? rowlist[t.r0 + lane] : -1;
-    const int64_t k0 = myrow >= 0 ? rp[myrow] : 0;
-    const int64_t k1 = myrow >= 0 ? rp[myrow + 1] : 0;
+    int64_t k0 = 0, k1 = 0;
+    if (myrow >= 0) epi.span(rp, myrow, k0, k1, acc0);
     const int64_t kb = k0 & ~static_cast<int64_t>(kLongChunk - 1);
     rounds = k1 > k0 ? static_cast<int>((k1 - kb + kLongChunk - 1) / kLongChunk) : 0;
     mk0 = static_cast<int>(k0 - kb);
@@ -582,7 +583,7 @@ __device__ __forceinline__ void run_long_slice(const Tile& t, const int64_t* __r
   }
   __syncthreads();
   const int maxr = sm.maxr;
-  double acc = 0.0, acc2 = 0.0;
+  double acc = acc0, acc2 = 0.0;
   double* sp2 = sp + 32 * kLongStride;  // NV == 2 only
   for (int b = 0; b < maxr; ++b) {
     const int off = b * kLongChunk;
@@ -654,8 +655,9 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
     // (the first and last chunk of a row are partial).
     const int cnt = t.r1;
     const int myrow = lane < cnt ? rowlist[t.r0 + lane] : -1;
-    const int64_t k0 = myrow >= 0 ? rp[myrow] : 0;
-    const int64_t k1 = myrow >= 0 ? rp[myrow + 1] : 0;
+    int64_t k0 = 0, k1 = 0;
+    double acc0 = 0.0;
+    if (myrow >= 0) epi.span(rp, myrow, k0, k1, acc0);
     const int64_t kb = k0 & ~static_cast<int64_t>(kSliceChunk - 1);
     const int rounds = k1 > k0 ? static_cast<int>((k1 - kb + kSliceChunk - 1) / kSliceChunk) : 0;
     const int mk0 = static_cast<int>(k0 - kb), mlen = static_cast<int>(k1 - kb);
@@ -663,7 +665,7 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
     const int maxr = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(rounds)));
     __syncwarp();
     const int half = lane >> 4, e = lane & 15;
-    double acc = 0.0, acc2 = 0.0;
+    double acc = acc0, acc2 = 0.0;
     double* sp2 = sp + 32 * kSliceStride;  // NV == 2 only
     for (int b = 0; b < maxr; ++b) {
       const int off = b * kSliceChunk;
@@ -721,11 +723,36 @@ __device__ __forceinline__ void run_tile(const Tile& t, const int64_t* __restric
   }
 }
 
+// With column blocks (nblk > 1) a row's entries are visited block by block in
+// separate launches (rounds); the running sum waits in `carry` between them and
+// the epilogue runs in the last round.  Blocks are contiguous column ranges and
+// columns ascend within a row, so every row is still summed in CSR order.
 struct SgdEpi {
   const SgdIterArgs& a;
   int mat;
   unsigned fl;
-  __device__ void operator()(int64_t r, double acc) { sgd_epilogue(a, mat, r, acc, fl); }
+  __device__ void span(const int64_t* rp, int64_t r, int64_t& k0, int64_t& k1,
+                       double& acc0) const {
+    const int nb = a.nblk[mat];
+    k0 = rp[r];
+    k1 = rp[r + 1];
+    acc0 = 0.0;
+    if (nb <= 1) return;
+    const int32_t* bb = a.bnd[mat] + r * (nb - 1);
+    const int64_t base = k0;
+    if (a.round > 0) {
+      k0 = base + bb[a.round - 1];
+      acc0 = a.carry[mat][r];
+    }
+    if (a.round < nb - 1) k1 = base + bb[a.round];
+  }
+  __device__ void operator()(int64_t r, double acc) {
+    if (a.round < a.nblk[mat] - 1) {
+      a.carry[mat][r] = acc;
+      return;
+    }
+    sgd_epilogue(a, mat, r, acc, fl);
+  }
 };
 
 // KINDS: bit 0 = warp slices (kind 2), bit 1 = CTA long slices (kind 3);
@@ -740,6 +767,7 @@ sgd_iter_kernel(const SgdIterArgs a, int tile_base, int ntiles) {
   if (tid >= ntiles) return;
   const Tile t = a.tiles[tile_base + tid];
   const int mat = t.mat;
+  if (a.round >= a.nblk[mat]) return;  // this matrix has fewer column blocks
   SgdEpi epi{a, mat, 0u};
   if ((KINDS & 2) && t.kind == 3)  // CTA-cooperative (all 4 warps hold this tile)
     run_long_slice<SgdEpi, 1>(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
@@ -891,6 +919,36 @@ cudaError_t launch_sgd_iter_part(const SgdIterArgs& a, int tile_base, int ntiles
   return cudaGetLastError();
 }
 
+namespace {
+// per row: the nb - 1 interior column-block boundaries as offsets into the row
+// (first entry with column >= b * width), columns ascending within rows
+__global__ void block_bounds_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                    int64_t rows, int nb, int64_t width,
+                                    int32_t* __restrict__ bnd) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t k0 = rp[r], k1 = rp[r + 1];
+  for (int b = 1; b < nb; ++b) {
+    const int64_t key = b * width;
+    int64_t lo = k0, hi = k1;  // lower bound of key in ci[k0, k1)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ci[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    bnd[r * (nb - 1) + (b - 1)] = static_cast<int32_t>(lo - k0);
+  }
+}
+}  // namespace
+
+cudaError_t launch_block_bounds(const DevCsr& M, int nb, int64_t width, int32_t* bnd,
+                                cudaStream_t s) {
+  if (M.rows == 0 || nb <= 1) return cudaSuccess;
+  block_bounds_kernel<<<static_cast<unsigned>((M.rows + 255) / 256), 256, 0, s>>>(
+      M.row_ptr, M.col, M.rows, nb, width, bnd);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
@@ -929,13 +987,27 @@ __device__ __forceinline__ void pass_epilogue(const PassArgs& a, int64_t r,
   }
 }
 
+__device__ __forceinline__ void full_row(const int64_t* rp, int64_t r, int64_t& k0, int64_t& k1,
+                                         double& acc0) {
+  k0 = rp[r];
+  k1 = rp[r + 1];
+  acc0 = 0.0;
+}
 struct PassEpi {
   const PassArgs& a;
+  __device__ void span(const int64_t* rp, int64_t r, int64_t& k0, int64_t& k1,
+                       double& acc0) const {
+    full_row(rp, r, k0, k1, acc0);
+  }
   __device__ void operator()(int64_t r, double acc) { pass_epilogue(a, r, acc); }
 };
 struct PassEpi2 {
   const PassArgs& a;
   const PassArgs& b;
+  __device__ void span(const int64_t* rp, int64_t r, int64_t& k0, int64_t& k1,
+                       double& acc0) const {
+    full_row(rp, r, k0, k1, acc0);
+  }
   __device__ void operator()(int64_t r, double acc, double acc2) {
     pass_epilogue(a, r, acc);
     pass_epilogue(b, r, acc2);

@@ -690,3 +690,27 @@ def test_degenerate_sparse_inputs_vs_oracle(C, m, n, entries):
         lg = eq.lsqr(M, b, 5, 0.0)
         assert np.array_equal(lg.residual_history, lw.residual_history)
         assert (lg.iterations, lg.breakdown) == (lw.iterations, lw.breakdown)
+
+
+@pytest.mark.parametrize("case", ["sp", "lr", "c3"])
+def test_column_block_rounds_bit_exact(C, golden, monkeypatch, case):
+    """Gathered vectors larger than EQUIL_BLOCK_MB are visited in column blocks
+    with the row sums carried between launches (engine.cu build_block_layout).
+    Forcing tiny blocks here: the trajectory must not change by a bit."""
+    monkeypatch.setenv("EQUIL_BLOCK_MB", "0.004")  # 500-coordinate blocks
+    if case == "c3":
+        from paper_1602_06621_b200 import configs
+        inst = configs.config(3, scale=0.02)
+        A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+        want = C.sgd_equilibrate(A, iterations=15, seed=7)
+        got = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(iterations=15, seed=7))
+        want = {k: getattr(want, k) for k in "uvde"}
+    else:
+        A = csr_from_golden(golden, case)
+        got = eq.sgd_equilibrate(device_matrix(A), eq.EquilibrationParams(iterations=40, seed=5),
+                                 eq.DiagnosticsConfig(stride=10))
+        want = {k: golden[f"{case}_sgd_{k}"] for k in "uvde"}
+        np.testing.assert_allclose([h.rms for h in got.history], golden[f"{case}_sgd_hist_rms"],
+                                   rtol=1e-12, atol=0)
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), want[k]), k
