@@ -27,6 +27,7 @@
 // interval the CTA stages round c+1 and chains round c, while the entries of
 // round c+2 and the runs of round c+1 are already in flight into registers.
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -451,15 +452,17 @@ cudaError_t build_panels(const DevCsr& M, int64_t vec_len, const std::vector<int
 cudaError_t launch_sgd_panel(const SgdIterArgs& a, const PanelArgs& p, int nbands,
                              cudaStream_t s) {
   if (nbands == 0) return cudaSuccess;
-  static bool attr_set[64] = {};
+  // the attribute is per device; setting it is idempotent, so racing threads
+  // at worst set it twice
+  static std::atomic<bool> attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 64 && !attr_set[dev]) {
+  if (dev < 64 && !attr_set[dev].load(std::memory_order_acquire)) {
     const cudaError_t e = cudaFuncSetAttribute(
         sgd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
         static_cast<int>(sizeof(PanelSmem)));
     if (e != cudaSuccess) return e;
-    attr_set[dev] = true;
+    attr_set[dev].store(true, std::memory_order_release);
   }
   sgd_panel_kernel<<<nbands, kPanelThreads, sizeof(PanelSmem), s>>>(a, p);
   count_launch(s);
