@@ -241,18 +241,32 @@ cudaError_t dense_cols_partial(const double* A, int64_t m, int64_t n, const doub
 
 }  // namespace
 
-cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s) {
+// rows (u block) and columns (v block) read A independently: with a side
+// stream s2 they run concurrently (fork on ev_fork, join on ev_join)
+cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s, cudaStream_t s2,
+                                  cudaEvent_t ev_fork, cudaEvent_t ev_join) {
   if (a.n > static_cast<int64_t>(kChunk) * 32) return cudaErrorInvalidValue;
+  cudaError_t e = cudaSuccess;
+  cudaStream_t rs = s;
+  if (s2) {
+    if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s2, ev_fork, 0)) != cudaSuccess) return e;
+    rs = s2;
+  }
   dense_sgd_rows_kernel<<<static_cast<unsigned>((a.m + kRowsPerCta - 1) / kRowsPerCta), 256, 0,
-                          s>>>(a);
-  count_launch(s);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+                          rs>>>(a);
+  count_launch(rs);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   e = dense_cols_partial(a.A, a.m, a.n, a.xw_cur, a.colpart, s);
   if (e != cudaSuccess) return e;
   dense_sgd_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
   count_launch(s);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (s2) {
+    if ((e = cudaEventRecord(ev_join, s2)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s) {

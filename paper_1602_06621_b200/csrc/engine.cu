@@ -1094,7 +1094,11 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     };
     auto one_iter = [&](int t) {
       if (M->dense) {
-        CK(eqb::launch_dense_sgd_iter(dense_args(t), s));
+        static const int dconc = getenv("EQUIL_CONC") ? atoi(getenv("EQUIL_CONC")) : 1;
+        if (dconc)
+          CK(eqb::launch_dense_sgd_iter(dense_args(t), s, M->copy_stream, M->ev_fork, M->ev_join));
+        else
+          CK(eqb::launch_dense_sgd_iter(dense_args(t), s));
       } else {
         static const int conc = getenv("EQUIL_CONC") ? atoi(getenv("EQUIL_CONC")) : 1;
         const int rounds = std::max(M->nblk[0], M->nblk[1]);

@@ -281,7 +281,9 @@ struct DenseIterArgs {
   unsigned* flags;
   double* colpart;  // scratch: nchunks_m x n
 };
-cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s);
+// s2 non-null: the row and column halves run concurrently on s2 / s
+cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s, cudaStream_t s2 = nullptr,
+                                  cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr);
 struct DensePassArgs {
   const double* A;
   int64_t m, n;
