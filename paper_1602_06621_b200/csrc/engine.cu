@@ -65,8 +65,23 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   // rows (kind 3), each replicated once per warp of the CTA
   std::stable_sort(longs.begin(), longs.end(),
                    [](const auto& a, const auto& b) { return a.first > b.first; });
-  for (size_t q = 0; q < longs.size(); q += eqb::kLongRows) {
-    const int cnt = static_cast<int>(std::min<size_t>(eqb::kLongRows, longs.size() - q));
+  // mid-length rows (kTileNnz, EQ_MID_MAX]: warp slices of 32 globally
+  // length-sorted rows, placed first among the slices (longest first)
+  size_t nlong = longs.size();
+  if (eqb::kMidMax > eqb::kTileNnz) {
+    size_t first_mid = 0;
+    while (first_mid < longs.size() && longs[first_mid].first > eqb::kMidMax) ++first_mid;
+    std::vector<eqb::Tile> mids;
+    for (size_t q = first_mid; q < longs.size(); q += eqb::kSliceRows) {
+      const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, longs.size() - q));
+      mids.push_back({static_cast<int32_t>(P.rowlist.size()), cnt, 2, static_cast<int16_t>(mat), 0});
+      for (int k = 0; k < cnt; ++k) P.rowlist.push_back(static_cast<int32_t>(longs[q + k].second));
+    }
+    P.slices.insert(P.slices.begin(), mids.begin(), mids.end());
+    nlong = first_mid;
+  }
+  for (size_t q = 0; q < nlong; q += eqb::kLongRows) {
+    const int cnt = static_cast<int>(std::min<size_t>(eqb::kLongRows, nlong - q));
     const eqb::Tile t{static_cast<int32_t>(P.rowlist.size()), cnt, 3,
                       static_cast<int16_t>(mat), 0};
     for (int k = 0; k < cnt; ++k) P.rowlist.push_back(static_cast<int32_t>(longs[q + k].second));

@@ -29,6 +29,10 @@ struct Tile {
 #define EQ_LONG_THRESH 512
 #endif
 constexpr int kTileNnz = EQ_LONG_THRESH;  // longest row of a slice; longer rows: kind 3
+#ifndef EQ_MID_MAX
+#define EQ_MID_MAX 0
+#endif
+constexpr int kMidMax = EQ_MID_MAX;  // rows in (kTileNnz, kMidMax]: globally sorted warp slices
 constexpr int kSliceChunk = 16;  // products per row per lock-step round (kind 2)
 constexpr int kSliceStride = 18; // padded row stride (doubles): conflict-free LDS.128
 constexpr int kSliceBatch = EQ_SLICE_BATCH;  // row pairs staged per batch (loads in flight)

@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for c in 1 1 0; do echo "== conc $c"; EQUIL_CONC=$c timeout 300 python tools/perf_probe.py 3 2>&1 | tail -1 | cut -c1-200; done
+for t in base mid1k mid2k mid4k mid16k base; do
+  if [ $t = base ]; then L=paper_1602_06621_b200/libequil_b200.so; else L=paper_1602_06621_b200/libequil_b200_$t.so; fi
+  echo "== $t"; EQUIL_LIB=$PWD/$L timeout 300 python tools/perf_probe.py 3 2>&1 | tail -1 | cut -c1-200
+done
