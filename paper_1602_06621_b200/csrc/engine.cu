@@ -161,10 +161,15 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   }
   if (M->world > 1) {
     require(cfg->nccl_id != nullptr, "device cfg: world_size > 1 needs nccl_id");
-    if (!nccl().ok) fail(EQUIL_ENCCL, "libnccl.so.2 could not be loaded");
-    ncclUniqueId id;
-    std::memcpy(&id, cfg->nccl_id, sizeof id);
-    nccl_check(nccl().CommInitRank(&M->comm, M->world, id, M->rank), "ncclCommInitRank");
+    const char* hxe = getenv("EQUIL_HOST_EXCHANGE");
+    if (hxe && atoi(hxe) != 0) {  // test transport (HostExchange), no NCCL
+      M->hx = host_exchange(cfg->nccl_id, M->world);
+    } else {
+      if (!nccl().ok) fail(EQUIL_ENCCL, "libnccl.so.2 could not be loaded");
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_id, sizeof id);
+      nccl_check(nccl().CommInitRank(&M->comm, M->world, id, M->rank), "ncclCommInitRank");
+    }
   }
   M->flags.alloc(1);
   M->red_counter.alloc(1);
@@ -203,6 +208,19 @@ void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
 
 void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
   if (M->world == 1) return;
+  if (M->hx) {  // host exchange: own slice out, barrier, peers' slices in, barrier
+    const size_t bytes = static_cast<size_t>(maxcnt) * 8;
+    CK(cudaStreamSynchronize(M->stream));
+    std::vector<char>& mine = M->hx->slot[M->rank];
+    mine.resize(bytes);
+    if (bytes) CK(cudaMemcpy(mine.data(), buf + M->rank * maxcnt, bytes, cudaMemcpyDeviceToHost));
+    M->hx->barrier();
+    for (int g = 0; g < M->world; ++g)
+      if (g != M->rank && bytes)
+        CK(cudaMemcpy(buf + g * maxcnt, M->hx->slot[g].data(), bytes, cudaMemcpyHostToDevice));
+    M->hx->barrier();
+    return;
+  }
   nccl_check(nccl().AllGather(buf + M->rank * maxcnt, buf, static_cast<size_t>(maxcnt),
                               ncclFloat64, M->comm, M->stream),
              "ncclAllGather");
@@ -1145,7 +1163,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       }
     };
 
-    if (dp.stride == 0 && T > 0) {
+    if (dp.stride == 0 && T > 0 && !M->hx) {  // (the host exchange cannot be captured)
       // capture the whole T loop once per (T, targets, gamma, M) and replay it
       equil_matrix::Key key{T, alpha, beta, gamma, Mx, vec_lin};
       if (!M->graph || !(M->graph_key == key)) {
@@ -1199,9 +1217,35 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     CK(eqb::launch_exp(M->ub.p, dloc, ml, 1.0, s));
     CK(eqb::launch_exp(M->vb.p, eloc, nl, 1.0, s));
     unsigned flags = 0;
-    if (M->world > 1) {
-      nccl_check(nccl().AllReduce(M->flags.p, M->flags.p, 1, ncclUint32, ncclMax, M->comm, s),
-                 "ncclAllReduce");
+    if (M->world > 1 && M->hx) {  // host exchange: max of the flag words
+      unsigned mine = 0;
+      CK(cudaMemcpyAsync(&mine, M->flags.p, sizeof mine, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      M->hx->slot[M->rank].assign(reinterpret_cast<char*>(&mine),
+                                  reinterpret_cast<char*>(&mine) + sizeof mine);
+      M->hx->barrier();
+      unsigned all = 0;
+      for (int g = 0; g < M->world; ++g) {
+        unsigned v = 0;
+        std::memcpy(&v, M->hx->slot[g].data(), sizeof v);
+        all |= v;
+      }
+      M->hx->barrier();
+      CK(cudaMemcpyAsync(M->flags.p, &all, sizeof all, cudaMemcpyHostToDevice, s));
+    } else if (M->world > 1) {
+      // the flag words are bit sets (1: iterate bound, 2: box); NCCL has no
+      // bitwise OR, so gather every rank's word and OR them
+      DevBuf<unsigned> words;
+      words.alloc(M->world);
+      nccl_check(nccl().AllGather(M->flags.p, words.p, 1, ncclUint32, M->comm, s),
+                 "ncclAllGather");
+      std::vector<unsigned> w(M->world);
+      CK(cudaMemcpyAsync(w.data(), words.p, M->world * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                         s));
+      CK(cudaStreamSynchronize(s));
+      unsigned all = 0;
+      for (unsigned x : w) all |= x;
+      CK(cudaMemcpyAsync(M->flags.p, &all, sizeof all, cudaMemcpyHostToDevice, s));
     }
     CK(cudaMemcpyAsync(&flags, M->flags.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     const cudaMemcpyKind kind =

@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -281,6 +283,48 @@ std::vector<int64_t> partition_rows(const int64_t* rp, int64_t rows, int parts);
 
 }  // namespace eqe
 
+namespace eqe {
+// In-process rank exchange used instead of NCCL when EQUIL_HOST_EXCHANGE=1:
+// several rank handles of one sharded matrix live in one process (one thread
+// each, e.g. all on one GPU in a test) and meet on the host -- a barrier on a
+// condition variable, slices passed through host buffers.  No kernel ever
+// waits on another rank; the sharded engine's index arithmetic, padding and
+// reductions run exactly as with NCCL.
+struct HostExchange {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<std::vector<char>> slot;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+inline std::shared_ptr<HostExchange> host_exchange(const void* id128, int world) {
+  static std::mutex mu;
+  static std::map<std::string, std::weak_ptr<HostExchange>> reg;
+  std::lock_guard<std::mutex> lk(mu);
+  const std::string key(static_cast<const char*>(id128), 128);
+  auto hx = reg[key].lock();
+  if (!hx) {
+    hx = std::make_shared<HostExchange>();
+    hx->world = world;
+    hx->slot.resize(world);
+    reg[key] = hx;
+  }
+  return hx;
+}
+}  // namespace eqe
+
 // The device-resident matrix behind the opaque handle of include/equil_b200.h.
 using namespace eqe;
 // ---------------------------------------------------------------------------
@@ -294,6 +338,7 @@ struct equil_matrix {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
   ncclComm_t comm = nullptr;
+  std::shared_ptr<eqe::HostExchange> hx;  // EQUIL_HOST_EXCHANGE=1 instead of comm
 
   // sparse shards (local rows, columns in padded coordinates)
   eqb::DevCsr A, AT;

@@ -714,3 +714,61 @@ def test_column_block_rounds_bit_exact(C, golden, monkeypatch, case):
                                    rtol=1e-12, atol=0)
     for k in "uvde":
         assert np.array_equal(getattr(got, k), want[k]), k
+
+
+# ---------------------------------------------------------------- sharded engine
+@pytest.mark.parametrize("case,world", [("lr", 2), ("sp", 3), ("c3", 4)])
+def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, case, world):
+    """The multi-GPU engine (row shards of A and A^T, padded gathered vectors,
+    slot maps, history and LSQR reductions) run as `world` rank handles in one
+    process on one GPU, exchanging through the host (EQUIL_HOST_EXCHANGE=1, a
+    barrier per exchange; no kernel waits on another rank).  Every rank must
+    return the single-GPU result bit for bit."""
+    import os
+    import threading
+    if case == "c3":
+        from paper_1602_06621_b200 import configs
+        inst = configs.config(3, scale=0.02)
+        A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    else:
+        A = csr_from_golden(golden, case)
+    b = np.random.default_rng(4).standard_normal(A.m)
+    p = eq.EquilibrationParams(iterations=20, seed=5)
+    d = eq.DiagnosticsConfig(stride=5)
+    M1 = device_matrix(A)
+    ref_s = eq.sgd_equilibrate(M1, p, d)
+    ref_l = eq.lsqr(M1, b, 12, 0.0)
+    ref_p = eq.lsqr_preconditioned(M1, b, eq.EquilibrationParams(iterations=8, seed=2), 12, 0.0)
+    monkeypatch.setenv("EQUIL_HOST_EXCHANGE", "1")
+    nid = os.urandom(128)
+    Ms = [eq.ExplicitMatrix.from_csr(A.m, A.n, A.row_ptr, A.col, A.val, rank=r, world_size=world,
+                                     nccl_id=nid) for r in range(world)]
+    out = [None] * world
+    errs = []
+
+    def run(r):
+        try:
+            s = eq.sgd_equilibrate(Ms[r], p, d)
+            lp = eq.lsqr(Ms[r], b, 12, 0.0)
+            pp = eq.lsqr_preconditioned(Ms[r], b, eq.EquilibrationParams(iterations=8, seed=2),
+                                        12, 0.0)
+            out[r] = (s, lp, pp)
+        except Exception as ex:  # surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    for s, lp, pp in out:
+        for k in "uvde":
+            assert np.array_equal(getattr(s, k), getattr(ref_s, k)), k
+        assert (s.box_feasible, s.iterate_bound_ok) == (ref_s.box_feasible, ref_s.iterate_bound_ok)
+        assert [h.objective for h in s.history] == [h.objective for h in ref_s.history]
+        assert [h.rms for h in s.history] == [h.rms for h in ref_s.history]
+        assert np.array_equal(lp.residual_history, ref_l.residual_history)
+        assert np.array_equal(lp.x, ref_l.x)
+        assert np.array_equal(pp.residual_history, ref_p.residual_history)
+        assert np.array_equal(pp.x, ref_p.x)
