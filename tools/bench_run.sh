@@ -1,2 +1,5 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err || exit 1
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
+timeout 600 python tools/perf_probe.py 2 4 > gpurun_out/probe24.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
