@@ -248,12 +248,52 @@ def run_ours(args):
                "path": "equil_sgd_equilibrate_csr (upload, device transpose, T iterations, "
                        "download)"}
         del r
+    else:
+        # the same public path at N GPUs: every rank builds its shard from the
+        # pinned host CSR (handle + communicator), runs T iterations and reads
+        # the gathered u, v, d, e back to the host; max over ranks
+        pin_rp = torch.from_numpy(inst.row_ptr).pin_memory()
+        pin_c = torch.from_numpy(inst.col).pin_memory()
+        pin_v = torch.from_numpy(inst.val).pin_memory()
+        ts = []
+        r = None
+        for _ in range(args.e2e_steps):
+            obj = [eq.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            barrier()
+            t0 = time.perf_counter()
+            M2 = eq.ExplicitMatrix.from_csr(inst.m, inst.n, pin_rp.numpy(), pin_c.numpy(),
+                                            pin_v.numpy(), device=local, rank=rank,
+                                            world_size=world, nccl_id=obj[0])
+            r = eq.sgd_equilibrate(M2, p)
+            M2.close()
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            ts.append(float(dt.item()))
+        e2e_s = statistics.mean(ts)
+        h2d = int(inst.row_ptr.nbytes + inst.col.nbytes + inst.val.nbytes) * world
+        d2h = int(8 * 2 * (inst.m + inst.n)) * world
+        e2e = {"value": T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "s_per_step": e2e_s,
+               "samples_s": [round(t, 4) for t in ts],
+               "path": "ExplicitMatrix.from_csr on every rank (upload, device transpose, "
+                       "shard, communicator) + sgd_equilibrate to host"}
+        if rank == 0:  # the sharded result must equal one GPU's bit for bit
+            one = eq.sgd_equilibrate_csr(inst.m, inst.n, pin_rp.numpy(), pin_c.numpy(),
+                                         pin_v.numpy(), p, device=local)
+            check = {"bit_identical_to_1gpu": bool(
+                all(np.array_equal(getattr(r, k), getattr(one, k)) for k in "uvde"))}
+        barrier()
+        del r
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(inst, args.cpu_iters)
 
     if rank == 0:
+        if world == 1:
+            check = None
+        exchange = eq.exchange_mode(M)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -276,6 +316,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
             "flags": {"box_feasible": res.box_feasible, "iterate_bound_ok": res.iterate_bound_ok},
+            "exchange": exchange, "check": check,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -172,6 +172,10 @@ void* equil_matrix_stream(equil_matrix* A);
 /* Device time (CUDA events on the handle's stream) of the T-iteration loop of
  * the last equil_sgd_equilibrate call; *iterations receives T. */
 double equil_last_loop_ms(equil_matrix* A, int* iterations);
+/* How the SGD loop of a sharded handle exchanges the next gathered vectors:
+ * 0 single GPU / not yet negotiated, 1 padded all-gathers (NCCL or host
+ * exchange), 2 fused peer stores from the SGD epilogue + one-word barrier. */
+int equil_exchange_mode(const equil_matrix* A);
 /* Number of this library's kernels launched so far in the process. */
 long long equil_kernel_launches(void);
 

@@ -83,6 +83,7 @@ SIGNATURES = {
     "equil_matrix_shape": (C.c_int, [C.c_void_p, _i64p, _i64p, _i64p]),
     "equil_matrix_stream": (C.c_void_p, [C.c_void_p]),
     "equil_last_loop_ms": (C.c_double, [C.c_void_p, _ip]),
+    "equil_exchange_mode": (C.c_int, [C.c_void_p]),
     "equil_kernel_launches": (C.c_longlong, []),
     "equil_apply": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int]),
     "equil_sgd_equilibrate": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(DiagCfg),

@@ -674,6 +674,12 @@ def last_loop_ms(op: ExplicitMatrix):
     return ms, it.value
 
 
+def exchange_mode(op: ExplicitMatrix) -> str:
+    """How a sharded handle's SGD loop exchanges the gathered vectors:
+    "single" (one GPU or not yet run), "allgather" or "p2p" (fused peer stores)."""
+    return ("single", "allgather", "p2p")[int(L.load().equil_exchange_mode(op._h))]
+
+
 def kernel_launches() -> int:
     return int(L.load().equil_kernel_launches())
 

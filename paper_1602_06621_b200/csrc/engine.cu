@@ -226,6 +226,108 @@ void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
              "ncclAllGather");
 }
 
+// Fused all-gather of the SGD loop.  With world > 1 every rank maps every peer's
+// gathered-vector buffer (xbuf, same layout on all ranks): CUDA IPC handles are
+// all-gathered over NCCL and opened with peer access (NVLink / NVSwitch), or,
+// under the host exchange, the in-process pointers are passed directly.  The SGD
+// epilogue then stores each next value into all copies and the iteration ends
+// with a one-word barrier instead of two padded all-gathers.  Negotiated once
+// (collectively, at the first SGD call); any rank unable to map turns it off
+// for all.  EQUIL_P2P=0 keeps the NCCL all-gathers.
+static int64_t elem_delta(const void* peer, const double* mine) {
+  // both allocations are 256-byte aligned, so the offset is whole doubles
+  return (static_cast<int64_t>(reinterpret_cast<intptr_t>(peer)) -
+          static_cast<int64_t>(reinterpret_cast<intptr_t>(mine))) /
+         static_cast<int64_t>(sizeof(double));
+}
+
+void setup_peers(equil_matrix* M) {
+  M->p2p_state = -1;
+  const int G = M->world, r = M->rank;
+  int want = (!M->use_panels && !M->dense && G - 1 <= EQ_MAX_PEERS) ? 1 : 0;
+  if (const char* e = getenv("EQUIL_P2P")) want = want && atoi(e) != 0;
+  std::vector<int64_t> delta;
+  if (M->hx) {
+    struct Rec {
+      int ok;
+      double* base;
+    } mine{want, M->xbuf.p};
+    CK(cudaStreamSynchronize(M->stream));
+    M->hx->slot[r].assign(reinterpret_cast<char*>(&mine), reinterpret_cast<char*>(&mine + 1));
+    M->hx->barrier();
+    bool ok = true;
+    std::vector<Rec> all(G);
+    for (int g = 0; g < G; ++g) {
+      std::memcpy(&all[g], M->hx->slot[g].data(), sizeof(Rec));
+      ok = ok && all[g].ok;
+    }
+    M->hx->barrier();
+    if (!ok) return;
+    for (int g = 0; g < G; ++g)
+      if (g != r) delta.push_back(elem_delta(all[g].base, M->xbuf.p));
+  } else {
+    struct Rec {
+      int32_t ok;
+      int32_t pad;
+      cudaIpcMemHandle_t h;
+    } mine{};
+    mine.ok = want && cudaIpcGetMemHandle(&mine.h, M->xbuf.p) == cudaSuccess;
+    cudaGetLastError();
+    DevBuf<char> buf;
+    buf.alloc(G * sizeof(Rec));
+    cudaStream_t s = M->stream;
+    CK(cudaMemcpyAsync(buf.p + r * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, s));
+    nccl_check(nccl().AllGather(buf.p + r * sizeof(Rec), buf.p, sizeof(Rec), ncclUint8, M->comm, s),
+               "ncclAllGather");
+    std::vector<Rec> all(G);
+    CK(cudaMemcpyAsync(all.data(), buf.p, G * sizeof(Rec), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    bool ok = true;
+    for (const Rec& x : all) ok = ok && x.ok;
+    if (!ok) return;  // every rank saw the same records
+    unsigned opened = 1;
+    for (int g = 0; g < G; ++g) {
+      if (g == r) continue;
+      void* q = nullptr;
+      if (cudaIpcOpenMemHandle(&q, all[g].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+        M->peer_mapped.push_back(q);
+        delta.push_back(elem_delta(q, M->xbuf.p));
+      } else {
+        opened = 0;
+      }
+      cudaGetLastError();
+    }
+    DevBuf<unsigned> w;  // every rank must have mapped every peer
+    w.alloc(1);
+    CK(cudaMemcpyAsync(w.p, &opened, sizeof opened, cudaMemcpyHostToDevice, s));
+    nccl_check(nccl().AllReduce(w.p, w.p, 1, ncclUint32, ncclMin, M->comm, s), "ncclAllReduce");
+    CK(cudaMemcpyAsync(&opened, w.p, sizeof opened, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!opened) {
+      for (void* q : M->peer_mapped) cudaIpcCloseMemHandle(q);
+      M->peer_mapped.clear();
+      return;
+    }
+  }
+  M->peer_delta = delta;
+  M->bar.alloc(1);
+  CK(cudaMemset(M->bar.p, 0, sizeof(unsigned)));
+  M->p2p_state = 1;
+}
+
+// End of a fused-all-gather iteration: no rank starts iteration t+1 (which
+// overwrites the buffers its peers read in iteration t) before every rank's
+// passes and peer stores of iteration t are complete.
+void rank_barrier(equil_matrix* M) {
+  if (M->hx) {
+    CK(cudaStreamSynchronize(M->stream));
+    M->hx->barrier();
+    return;
+  }
+  nccl_check(nccl().AllReduce(M->bar.p, M->bar.p, 1, ncclUint32, ncclMax, M->comm, M->stream),
+             "ncclAllReduce");
+}
+
 // Bands for the column-panel traversal: consecutive rows, closed before a row
 // that would push the band past `target` entries or kBandRows rows.
 std::vector<int64_t> plan_bands(const int64_t* rp, int64_t rows, int64_t target) {
@@ -509,7 +611,13 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   // each vector padded to whole panels (the panel traversal bulk-copies them)
   auto whole = [](int64_t x) { return (x + eqb::kPanelW - 1) / eqb::kPanelW * eqb::kPanelW; };
   const int64_t np = whole(M->n_pad()), mp = whole(M->m_pad());
-  M->xbuf.alloc(2 * (np + mp));
+  if (M->world > 1 && !M->hx) {  // pool memory cannot be exported over CUDA IPC
+    double* q = nullptr;
+    CK(cudaMalloc(&q, 2 * (np + mp) * sizeof(double)));
+    M->xbuf.adopt(q, 2 * (np + mp));
+  } else {
+    M->xbuf.alloc(2 * (np + mp));
+  }
   CK(cudaMemset(M->xbuf.p, 0, 2 * (np + mp) * sizeof(double)));
   if (pt) pt->mark(M->stream, "xbuf");
   for (int b = 0; b < 2; ++b) {
@@ -825,6 +933,11 @@ double equil_last_loop_ms(equil_matrix* A, int* iterations) {
 
 long long equil_kernel_launches(void) { return eqb::launch_count(); }
 
+int equil_exchange_mode(const equil_matrix* A) {
+  if (!A || A->world == 1 || A->p2p_state == 0) return 0;
+  return A->p2p_state == 1 ? 2 : 1;
+}
+
 equil_status equil_matrix_shape(const equil_matrix* A, int64_t* m, int64_t* n,
                                 int64_t* nnz) {
   return guarded([&] {
@@ -919,6 +1032,8 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
     const int64_t a_poff = M->world == 1 ? M->a_goff() : M->rank * M->a_max;
     const int64_t t_poff = M->world == 1 ? M->t_goff() : M->rank * M->t_max;
+    if (M->world > 1 && M->p2p_state == 0 && T > 0) setup_peers(M);
+    const bool p2p = M->world > 1 && M->p2p_state == 1;
     if (T > 0) {
       CK(eqb::launch_sgd_init(M->xs[0].p, M->xw[0].p, M->u.p, M->ub.p, M->v.p, M->vb.p,
                               M->n_pad(), M->m_pad(), M->signs.p, M->m_loc(), M->n_loc(),
@@ -1089,6 +1204,10 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       }
       a.st = host_step(t);
       a.flags = M->flags.p;
+      if (p2p) {
+        a.npeer = static_cast<int>(M->peer_delta.size());
+        for (int g = 0; g < a.npeer; ++g) a.peer_delta[g] = M->peer_delta[g];
+      }
       return a;
     };
     eqb::PanelArgs panel_args{};
@@ -1156,7 +1275,9 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
             CK(eqb::launch_sgd_iter(a, M->n_sgd, s));
           }
         }
-        if (t < T) {
+        if (t < T && p2p) {
+          rank_barrier(M);  // the epilogue already stored into every peer's copy
+        } else if (t < T) {
           allgather_padded(M, M->xs[t & 1].p, M->t_max);
           allgather_padded(M, M->xw[t & 1].p, M->a_max);
         }

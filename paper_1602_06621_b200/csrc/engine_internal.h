@@ -38,7 +38,7 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;
-constexpr int ncclUint8 = 1, ncclUint32 = 3, ncclFloat64 = 8, ncclMax = 2;
+constexpr int ncclUint8 = 1, ncclUint32 = 3, ncclFloat64 = 8, ncclMax = 2, ncclMin = 3;
 
 struct NcclApi {
   void* h = nullptr;
@@ -383,7 +383,13 @@ struct equil_matrix {
   struct Slot {
     double* p = nullptr;
   } xs[2], xw[2];
-  DevBuf<double> xbuf;
+  DevBuf<double> xbuf;  // cudaMalloc'ed when world > 1 (exportable over CUDA IPC)
+  // fused all-gather of the SGD loop (setup_peers): every peer's xbuf as an
+  // element offset from ours; p2p_state 0: not negotiated, 1: on, -1: off
+  int p2p_state = 0;
+  std::vector<int64_t> peer_delta;
+  std::vector<void*> peer_mapped;  // IPC mappings, closed on destroy
+  DevBuf<unsigned> bar;            // barrier word
   DevBuf<double> u, ub, v, vb;  // local
   DevBuf<uint32_t> signs;
   DevBuf<unsigned char> sign_scratch;
@@ -424,6 +430,7 @@ struct equil_matrix {
     if (ev_loop0) cudaEventDestroy(ev_loop0);
     if (ev_loop1) cudaEventDestroy(ev_loop1);
     if (graph) cudaGraphExecDestroy(graph);
+    for (void* q : peer_mapped) cudaIpcCloseMemHandle(q);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (ev_vals) cudaEventDestroy(ev_vals);
     if (ev_fork) cudaEventDestroy(ev_fork);

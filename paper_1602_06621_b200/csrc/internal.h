@@ -20,6 +20,9 @@ struct Tile {
   int32_t pad;
 };
 #ifndef EQ_SLICE_BATCH
+#ifndef EQ_MAX_PEERS
+#define EQ_MAX_PEERS 7  // fused all-gather up to 8 ranks (one NVSwitch node)
+#endif
 #define EQ_SLICE_BATCH 6
 #endif
 #ifndef EQ_LONG_BATCH
@@ -112,6 +115,12 @@ struct SgdIterArgs {
   double* carry[2];
   SgdStep st;
   unsigned* flags;
+  // fused all-gather (world > 1, EQUIL_P2P): the epilogue also stores each next
+  // value at the same position of every peer rank's gathered vector, over
+  // NVLink through CUDA IPC mappings (peer buffer = local buffer + peer_delta[g]
+  // elements), so the exchange overlaps the passes; a one-word barrier follows
+  int npeer;
+  int64_t peer_delta[EQ_MAX_PEERS];
 };
 
 // ---- column-panel traversal (panel.cu) ------------------------------------

@@ -775,6 +775,9 @@ sgd_iter_kernel(const SgdIterArgs a, int tile_base, int ntiles) {
   else if (KINDS & 1)
     run_tile<SgdEpi, 1>(t, a.rp[mat], a.ci[mat], a.va[mat], mat ? a.xw_cur : a.xs_cur,
                         a.rl[mat], sp[warp], sm[warp], lane, epi);
+  // peer stores performed system-wide before the kernel completes (the
+  // barrier that follows orders every peer's next reads after them)
+  if (a.npeer) __threadfence_system();
   if (epi.fl) atomicOr(a.flags, epi.fl);
 }
 

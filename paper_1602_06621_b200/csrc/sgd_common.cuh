@@ -75,7 +75,10 @@ __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
   if (a.has_next) {  // next iteration's e.*s (from v) / d.*w (from u)
     const double dn = det_exp(xn);
     const bool pos = sign_bit(a.signs, a.sign_next[mat] + r);
-    (mat ? a.xs_next : a.xw_next)[pi] = pos ? dn : -dn;
+    double* dst = (mat ? a.xs_next : a.xw_next) + pi;
+    const double val = pos ? dn : -dn;
+    *dst = val;
+    for (int g = 0; g < a.npeer; ++g) dst[a.peer_delta[g]] = val;  // peers' copies
   }
 }
 __device__ __forceinline__ uint32_t ld_na(const uint32_t* p) {

@@ -717,13 +717,16 @@ def test_column_block_rounds_bit_exact(C, golden, monkeypatch, case):
 
 
 # ---------------------------------------------------------------- sharded engine
+@pytest.mark.parametrize("p2p", ["1", "0"])
 @pytest.mark.parametrize("case,world", [("lr", 2), ("sp", 3), ("c3", 4)])
-def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, case, world):
+def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, case, world, p2p):
     """The multi-GPU engine (row shards of A and A^T, padded gathered vectors,
     slot maps, history and LSQR reductions) run as `world` rank handles in one
     process on one GPU, exchanging through the host (EQUIL_HOST_EXCHANGE=1, a
     barrier per exchange; no kernel waits on another rank).  Every rank must
-    return the single-GPU result bit for bit."""
+    return the single-GPU result bit for bit, both with the fused all-gather
+    (EQUIL_P2P=1: the SGD epilogue stores into every rank's gathered vector)
+    and with the padded all-gathers."""
     import os
     import threading
     if case == "c3":
@@ -740,6 +743,7 @@ def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, 
     ref_l = eq.lsqr(M1, b, 12, 0.0)
     ref_p = eq.lsqr_preconditioned(M1, b, eq.EquilibrationParams(iterations=8, seed=2), 12, 0.0)
     monkeypatch.setenv("EQUIL_HOST_EXCHANGE", "1")
+    monkeypatch.setenv("EQUIL_P2P", p2p)
     nid = os.urandom(128)
     Ms = [eq.ExplicitMatrix.from_csr(A.m, A.n, A.row_ptr, A.col, A.val, rank=r, world_size=world,
                                      nccl_id=nid) for r in range(world)]
@@ -762,6 +766,7 @@ def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, 
     for t in th:
         t.join(timeout=600)
     assert not errs, errs
+    assert {eq.exchange_mode(M) for M in Ms} == {"p2p" if p2p == "1" else "allgather"}
     for s, lp, pp in out:
         for k in "uvde":
             assert np.array_equal(getattr(s, k), getattr(ref_s, k)), k
