@@ -19,10 +19,10 @@ struct Tile {
   int16_t kind, mat;
   int32_t pad;
 };
-#ifndef EQ_SLICE_BATCH
 #ifndef EQ_MAX_PEERS
 #define EQ_MAX_PEERS 7  // fused all-gather up to 8 ranks (one NVSwitch node)
 #endif
+#ifndef EQ_SLICE_BATCH
 #define EQ_SLICE_BATCH 6
 #endif
 #ifndef EQ_LONG_BATCH
