@@ -141,6 +141,9 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   M->world = cfg ? std::max(1, cfg->world_size) : 1;
   if (const char* e = getenv("EQUIL_PANEL")) M->use_panels = atoi(e) != 0;  // A/B knob
   if (const char* e = getenv("EQUIL_SLOTS")) M->use_slots = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_SELL")) M->use_sell = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_SELL_VARIANT")) M->sell_variant = atoi(e);
+  if (const char* e = getenv("EQUIL_SELL_LONG")) M->sell_long = atoi(e) != 0;
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -183,7 +186,100 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
 // Upload the traversal plans of the local CSR(A) / CSR(A^T) shards.  The SGD
 // launch covers both matrices: every long row (longest first, so the longest
 // sequential chains start first), then the slices of A and of A^T.
-void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
+// The interleaved-slice plan (sell.cu) reuses the same row groups: every
+// kind-3 group and kind-2 slice becomes one slice, and the slices of both
+// matrices are ordered longest first (ties keep plan order).
+void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt, const int64_t* rpa,
+               const int64_t* rpt) {
+  equil_matrix::SellHost& H = M->sell_host;
+  H = equil_matrix::SellHost{};
+  struct Ent {
+    int32_t maxlen;
+    int16_t mat, cnt;
+    int32_t r0;
+  };
+  std::vector<Ent> ents;
+  for (int mat = 0; mat < 2; ++mat) {
+    const Plan& P = mat ? pt : pa;
+    const int64_t* rp = mat ? rpt : rpa;
+    auto add = [&](const eqb::Tile& t) {
+      int32_t mx = 0;
+      for (int k = 0; k < t.r1; ++k) {
+        const int32_t r = P.rowlist[t.r0 + k];
+        mx = std::max<int32_t>(mx, static_cast<int32_t>(rp[r + 1] - rp[r]));
+      }
+      ents.push_back({mx, static_cast<int16_t>(mat), static_cast<int16_t>(t.r1), t.r0});
+    };
+    if (M->sell_long)
+      for (size_t q = 0; q < P.lng.size(); q += eqb::kTileWarps) add(P.lng[q]);
+    for (const eqb::Tile& t : P.slices) add(t);
+  }
+  std::stable_sort(ents.begin(), ents.end(),
+                   [](const Ent& a, const Ent& b) { return a.maxlen > b.maxlen; });
+  H.slices.resize(ents.size());
+  H.row.assign(32 * ents.size(), 0);
+  H.len.assign(32 * ents.size(), 0);
+  for (size_t w = 0; w < ents.size(); ++w) {
+    const Ent& e = ents[w];
+    const Plan& P = e.mat ? pt : pa;
+    const int64_t* rp = e.mat ? rpt : rpa;
+    H.slices[w] = {H.total[e.mat], e.maxlen, e.cnt, e.mat};
+    H.total[e.mat] += 32 * static_cast<int64_t>(e.maxlen);
+    for (int k = 0; k < e.cnt; ++k) {
+      const int32_t r = P.rowlist[e.r0 + k];
+      H.row[32 * w + k] = r;
+      H.len[32 * w + k] = static_cast<int32_t>(rp[r + 1] - rp[r]);
+    }
+  }
+}
+
+// Device arrays of the interleaved slices, from the slot-remapped columns (the
+// slot layout must be built).  The slot copies of the columns are then dropped.
+void build_sell_layout(equil_matrix* M) {
+  M->sell = false;
+  if (!M->use_sell || !M->slots || M->use_panels || M->nblk[0] > 1 || M->nblk[1] > 1) return;
+  const equil_matrix::SellHost& H = M->sell_host;
+  cudaStream_t s = M->stream;
+  auto upload = [&](auto& d, const auto& h) {
+    d.alloc(h.size());
+    if (!h.empty())
+      CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice, s));
+  };
+  upload(M->sell_slices, H.slices);
+  upload(M->sell_row, H.row);
+  upload(M->sell_len, H.len);
+  M->n_sell = static_cast<int>(H.slices.size());
+  for (int mat = 0; mat < 2; ++mat) {
+    std::vector<int64_t> moff;
+    std::vector<int32_t> midx;
+    for (size_t w = 0; w < H.slices.size(); ++w)
+      if (H.slices[w].mat == mat && H.slices[w].maxlen > 0) {
+        moff.push_back(H.slices[w].off);
+        midx.push_back(static_cast<int32_t>(w));
+      }
+    M->sell_ci[mat].alloc(H.total[mat]);
+    M->sell_va[mat].alloc(H.total[mat]);
+    DevBuf<int64_t> doff;
+    DevBuf<int32_t> didx;
+    upload(doff, moff);
+    upload(didx, midx);
+    const eqb::DevCsr& C = mat ? M->AT : M->A;
+    CK(eqb::build_sell(C.row_ptr, mat ? M->t_ci_sgd.p : M->a_ci_sgd.p, C.val, doff.p, didx.p,
+                       static_cast<int>(moff.size()), M->sell_row.p, M->sell_len.p,
+                       H.total[mat], M->sell_ci[mat].p, M->sell_va[mat].p, s));
+    CK(cudaStreamSynchronize(s));  // before doff / didx go
+  }
+  if (M->sell_long || M->n_sgd_long == 0) {  // the staged kernel no longer runs
+    M->a_ci_sgd.release();
+    M->t_ci_sgd.release();
+  }
+  M->sell_host = equil_matrix::SellHost{};
+  M->sell = true;
+}
+
+void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt, const int64_t* rpa,
+                  const int64_t* rpt) {
+  if (M->use_sell) plan_sell(M, pa, pt, rpa, rpt);
   // kind-3 groups (4 entries each) first, so every group starts on a CTA
   std::vector<eqb::Tile> sgd = pa.lng;
   sgd.insert(sgd.end(), pt.lng.begin(), pt.lng.end());
@@ -517,10 +613,12 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   const std::vector<int64_t> la = local_rp(rpA_host, M->a_bounds);
   const std::vector<int64_t> lt = local_rp(rpT_host, M->t_bounds);
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
-               plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
+               plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1), la.data(),
+               lt.data());
   build_panel_layout(M, la.data(), lt.data());
   build_block_layout(M);
   build_slot_layout(M, fullA.row_ptr, fullT.row_ptr);
+  build_sell_layout(M);
 }
 
 void alloc_workspaces(equil_matrix* M, PhaseTimer* pt = nullptr);
@@ -591,12 +689,14 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     if (planner && planner->joinable()) planner->join();
     pt.mark(s, "plan A (join)");
     if (planA)  // computed concurrently by the caller
-      upload_plans(M, *planA, planT);
+      upload_plans(M, *planA, planT, row_ptr, rpT.data());
     else
-      upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
+      upload_plans(M, plan_tiles(row_ptr, m, 0), planT, row_ptr, rpT.data());
     pt.mark(s, "upload plans");
     build_panel_layout(M, row_ptr, rpT.data());
     pt.mark(s, "panels");
+    build_sell_layout(M);
+    pt.mark(s, "sell");
   } else {
     const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
     shard_sparse(M, fullA, fullT, rpA, rpT);
@@ -1259,6 +1359,28 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
           a.round = rd;
           if (M->n_pbands) {
             CK(eqb::launch_sgd_panel(a, panel_args, M->n_pbands, s));
+          } else if (M->sell) {
+            eqb::SellArgs sa{};
+            sa.slices = M->sell_slices.p;
+            sa.nslices = M->n_sell;
+            sa.row = M->sell_row.p;
+            sa.len = M->sell_len.p;
+            for (int k = 0; k < 2; ++k) {
+              sa.ci[k] = M->sell_ci[k].p;
+              sa.va[k] = M->sell_va[k].p;
+            }
+            if (M->sell_long || M->n_sgd_long == 0) {
+              CK(eqb::launch_sgd_sell(a, sa, M->sell_variant, s));
+            } else {
+              // rows longer than a tile stay CTA-cooperative (their sequential
+              // chains would otherwise wait on every load round trip)
+              CK(cudaEventRecord(M->ev_fork, s));
+              CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+              CK(eqb::launch_sgd_iter_part(a, 0, M->n_sgd_long, true, 6, M->copy_stream));
+              CK(eqb::launch_sgd_sell(a, sa, M->sell_variant, s));
+              CK(cudaEventRecord(M->ev_join, M->copy_stream));
+              CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+            }
           } else if (conc && M->n_sgd_long > 0 && M->n_sgd_long < M->n_sgd) {
             // long-row CTA groups and warp tiles as two concurrent kernels (fork /
             // join on the copy stream): each kernel gets its own residency on the

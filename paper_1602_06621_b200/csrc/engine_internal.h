@@ -362,6 +362,22 @@ struct equil_matrix {
   bool use_slots = true;
   bool slots = false;
   DevBuf<int32_t> a_ci_sgd, t_ci_sgd, wmap, smap;
+  // interleaved row slices of the SGD passes (sell.cu, build_sell_layout):
+  // the default traversal when the slot layout is on and nothing is blocked;
+  // EQUIL_SELL=0 keeps the staged warp tiles / CTA long slices
+  bool use_sell = true;
+  bool sell = false;
+  bool sell_long = false;  // rows longer than kTileNnz too (else kind-3 CTA groups)
+  int sell_variant = 0;
+  struct SellHost {
+    std::vector<eqb::SellSlice> slices;
+    std::vector<int32_t> row, len;
+    int64_t total[2] = {0, 0};
+  } sell_host;
+  DevBuf<eqb::SellSlice> sell_slices;
+  DevBuf<int32_t> sell_row, sell_len, sell_ci[2];
+  DevBuf<double> sell_va[2];
+  int n_sell = 0;
   // column blocks of the gathered vectors (build_block_layout): per matrix
   int nblk[2] = {1, 1};
   int64_t bwidth[2] = {0, 0};

@@ -123,6 +123,39 @@ struct SgdIterArgs {
   int64_t peer_delta[EQ_MAX_PEERS];
 };
 
+// ---- interleaved row slices (sell.cu) --------------------------------------
+// The SGD passes' own copy of CSR(A) / CSR(A^T) with the entries of each slice
+// of <= 32 length-sorted rows interleaved: entry k of lane l's row sits at
+// off + 32 k + l.  A warp streams a slice with fully coalesced 256-byte value
+// and 128-byte column loads, and every lane owns one row, so its sequential
+// CSR-order sum runs in registers (no shared-memory staging).  Column indices
+// are slots of the gathered vector (build_slot_layout).
+struct SellSlice {
+  int64_t off;     // first element (multiple of 32) in its matrix's arrays
+  int32_t maxlen;  // entries of the slice's longest row
+  int16_t cnt;     // rows (<= 32)
+  int16_t mat;     // 0: A (u block), 1: A^T (v block)
+};
+struct SellArgs {
+  const SellSlice* slices;  // both matrices, longest slices first
+  int nslices;
+  const int32_t* row;       // local row of lane l of slice w at 32 w + l
+  const int32_t* len;       // its length (0 for empty lanes)
+  const int32_t* ci[2];     // interleaved slot columns
+  const double* va[2];      // interleaved values
+};
+// Fill matrix `mat`'s interleaved arrays (total elements) from CSR rows whose
+// columns are already slots (ci_slot); moff / midx: that matrix's slices in
+// offset order and their indices into the slice list.
+cudaError_t build_sell(const int64_t* rp, const int32_t* ci_slot, const double* val,
+                       const int64_t* moff, const int32_t* midx, int nmat_slices,
+                       const int32_t* row, const int32_t* len, int64_t total,
+                       int32_t* out_ci, double* out_va, cudaStream_t s);
+// one SGD iteration over every slice (both matrices); variant selects the
+// compiled batch / pipelining / occupancy point (EQUIL_SELL_VARIANT)
+cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,
+                            cudaStream_t s);
+
 // ---- column-panel traversal (panel.cu) ------------------------------------
 // The gathered vector is cut into panels of kPanelW coordinates and the rows
 // into bands of <= kBandRows rows.  Each band's entries are stored panel-major

@@ -1,0 +1,207 @@
+// sell.cu -- the SGD iteration over interleaved row slices (K3/K4, default).
+//
+// Layout (internal.h SellSlice): the rows of a slice (<= 32, length-sorted by
+// plan_tiles) are stored interleaved, entry k of lane l at off + 32 k + l, so
+// the warp that owns the slice reads entry k of all its rows with one 128-byte
+// column load and one 256-byte value load.  Each lane owns one row: it forms
+// the products val * x[slot] (one rounded multiply each) and extends its row's
+// sum in CSR order with rounded adds, exactly explicit_matrix.cpp:73-75 for
+// CSR(A) and, on CSR(A^T) whose rows hold ascending original rows,
+// explicit_matrix.cpp:86-91.  There is no shared-memory staging, no barrier and
+// no cross-lane step: the only limit is how many column / value loads and
+// gathers each SM keeps in flight.
+//
+// Slices of both matrices run in one launch, longest first (a greedy
+// longest-processing-time order: the 10^4-entry rows of a Zipf matrix start at
+// once instead of trailing the launch).  The epilogue is the same fused
+// sgd_epilogue as the staged traversal (sgd_common.cuh).
+#include "sgd_common.cuh"
+
+namespace eqb {
+namespace {
+
+__global__ void build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ val,
+                                  const int64_t* __restrict__ moff,
+                                  const int32_t* __restrict__ midx, int nms,
+                                  const int32_t* __restrict__ row,
+                                  const int32_t* __restrict__ len, int64_t total,
+                                  int32_t* __restrict__ oc, double* __restrict__ ov) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= total) return;
+  int lo = 0, hi = nms;  // last slice with moff <= e
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (moff[mid] <= e) lo = mid; else hi = mid;
+  }
+  const int64_t rel = e - moff[lo];
+  const int lane = static_cast<int>(rel & 31);
+  const int64_t k = rel >> 5;
+  const int64_t q = 32 * static_cast<int64_t>(midx[lo]) + lane;
+  int32_t c = 0;
+  double v = 0.0;
+  if (k < len[q]) {
+    const int64_t src = rp[row[q]] + k;
+    c = ci[src];
+    v = val[src];
+  }
+  oc[e] = c;
+  ov[e] = v;
+}
+
+// L2 prefetch of the slice's interleaved entries [k, k + B) (one bulk request
+// per array, issued by one lane): the column / value loads of a later batch
+// then wait on L2 instead of DRAM, without holding registers.
+template <int B>
+__device__ __forceinline__ void prefetch_batch(const int32_t* cbase, const double* vbase, int k) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cbase + 32 * k),
+               "r"(B * 32 * 4) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vbase + 32 * k),
+               "r"(B * 32 * 8) : "memory");
+}
+
+// One warp per slice.  B entries per lane per batch: B column loads and B
+// value loads, then B gathers, then B dependent adds.  PIPE: the next batch's
+// column / value loads are issued before this batch's gathers (one batch of
+// CSR stream in flight behind the gathers).  PF > 0: lane 0 keeps the slice's
+// stream PF batches ahead in L2 (the batch loop is then the critical path of
+// the slice's longest row: an L2 load and a gather per batch).
+template <int B, bool PIPE, int MINB, int PF = 0>
+__global__ void __launch_bounds__(128, MINB) sgd_sell_kernel(const SgdIterArgs a,
+                                                             const SellArgs sa) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (w >= sa.nslices) return;
+  const SellSlice sd = sa.slices[w];
+  const int mat = sd.mat;
+  const int q = 32 * w + lane;
+  const int len = __ldg(sa.len + q);
+  const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
+  const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
+  const double* __restrict__ x = mat ? a.xw_cur : a.xs_cur;
+  double acc = 0.0;
+  int k = 0;
+  const int maxlen = sd.maxlen;
+  const int32_t* cb = sa.ci[mat] + sd.off;
+  const double* vb = sa.va[mat] + sd.off;
+  if constexpr (PF > 0) {
+    if (lane == 0)
+      for (int j = 0; j < PF && j * B < maxlen; ++j) prefetch_batch<B>(cb, vb, j * B);
+  }
+  if constexpr (!PIPE) {
+    for (; k + B <= len; k += B) {
+      if constexpr (PF > 0) {
+        if (lane == 0 && k + PF * B < maxlen) prefetch_batch<B>(cb, vb, k + PF * B);
+      }
+      int32_t c[B];
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * (k + b));
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * (k + b));
+      double g[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) g[b] = __ldg(x + c[b]);
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
+    }
+  } else {
+    if (k + B <= len) {
+      int32_t c[B];
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * b);
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * b);
+      for (;;) {
+        const int kn = k + B;
+        const bool more = kn + B <= len;
+        int32_t cn[B];
+        double vn[B];
+        if (more) {
+#pragma unroll
+          for (int b = 0; b < B; ++b) cn[b] = ld_na(cp + 32 * (kn + b));
+#pragma unroll
+          for (int b = 0; b < B; ++b) vn[b] = ld_na(vp + 32 * (kn + b));
+        }
+        double g[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) g[b] = __ldg(x + c[b]);
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
+        k = kn;
+        if (!more) break;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          c[b] = cn[b];
+          v[b] = vn[b];
+        }
+      }
+    }
+  }
+  if (k < len) {  // tail: fewer than B entries left
+    int32_t c[B];
+    double v[B], g[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (k + b < len) {
+        c[b] = ld_na(cp + 32 * (k + b));
+        v[b] = ld_na(vp + 32 * (k + b));
+      }
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (k + b < len) g[b] = __ldg(x + c[b]);
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (k + b < len) acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
+  }
+  unsigned fl = 0;
+  if (lane < sd.cnt) sgd_epilogue(a, mat, __ldg(sa.row + q), acc, fl);
+  // peer stores performed system-wide before the kernel completes (the
+  // barrier that follows orders every peer's next reads after them)
+  if (a.npeer) __threadfence_system();
+  if (fl) atomicOr(a.flags, fl);
+}
+
+template <int B, bool PIPE, int MINB, int PF = 0>
+void launch_variant(const SgdIterArgs& a, const SellArgs& sa, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>((sa.nslices + 3) / 4);
+  sgd_sell_kernel<B, PIPE, MINB, PF><<<g, 128, 0, s>>>(a, sa);
+}
+
+}  // namespace
+
+cudaError_t build_sell(const int64_t* rp, const int32_t* ci_slot, const double* val,
+                       const int64_t* moff, const int32_t* midx, int nmat_slices,
+                       const int32_t* row, const int32_t* len, int64_t total,
+                       int32_t* out_ci, double* out_va, cudaStream_t s) {
+  if (total == 0 || nmat_slices == 0) return cudaSuccess;
+  build_sell_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+      rp, ci_slot, val, moff, midx, nmat_slices, row, len, total, out_ci, out_va);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,
+                            cudaStream_t s) {
+  if (sa.nslices == 0) return cudaSuccess;
+  switch (variant) {  // EQUIL_SELL_VARIANT (A/B knob); 0 = measured best on c3
+    case 1: launch_variant<4, false, 12>(a, sa, s); break;
+    case 2: launch_variant<8, false, 8>(a, sa, s); break;
+    case 3: launch_variant<16, false, 6>(a, sa, s); break;
+    case 4: launch_variant<4, true, 8>(a, sa, s); break;
+    case 5: launch_variant<8, true, 8>(a, sa, s); break;
+    case 6: launch_variant<6, true, 8>(a, sa, s); break;
+    case 7: launch_variant<12, true, 5>(a, sa, s); break;
+    case 8: launch_variant<16, false, 6, 2>(a, sa, s); break;
+    case 9: launch_variant<16, false, 6, 4>(a, sa, s); break;
+    case 10: launch_variant<8, false, 8, 4>(a, sa, s); break;
+    case 11: launch_variant<8, false, 8, 8>(a, sa, s); break;
+    case 12: launch_variant<16, false, 4, 4>(a, sa, s); break;
+    default: launch_variant<8, true, 6>(a, sa, s); break;
+  }
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+}  // namespace eqb
