@@ -77,7 +77,7 @@ def peaks():
 
 
 def ncu_traffic():
-    """DRAM bytes per SGD iteration (both sgd_iter_kernel parts) from the
+    """DRAM bytes per SGD iteration (both SGD kernel launches) from the
     committed ncu --set full capture (profiles/ncu_summary.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
@@ -309,9 +309,10 @@ def run_ours(args):
             "achieved_GBps": B * value / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sgd_iter_kernel: one iteration = A and A^T passes with "
-                                   "the fused u/v epilogue (long-row and slice parts as two "
-                                   "concurrent launches)",
+                         "kernel": "sgd_sell_kernel + sgd_sell_long_kernel: one iteration = "
+                                   "A and A^T passes over interleaved row slices with the fused "
+                                   "u/v epilogue (warp slices and warp-specialised long-row "
+                                   "CTAs as two concurrent launches)",
                          "bytes_per_launch": per_gpu_bytes, "launch_ms": kern_s * 1e3,
                          "peak_source": peak_src},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,

@@ -143,7 +143,8 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SLOTS")) M->use_slots = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL")) M->use_sell = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL_VARIANT")) M->sell_variant = atoi(e);
-  if (const char* e = getenv("EQUIL_SELL_LONG")) M->sell_long = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_SELL_LONG")) M->sell_long = atoi(e);
+  if (const char* e = getenv("EQUIL_SELL_LVARIANT")) M->sell_lvariant = atoi(e);
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -249,6 +250,9 @@ void build_sell_layout(equil_matrix* M) {
   upload(M->sell_row, H.row);
   upload(M->sell_len, H.len);
   M->n_sell = static_cast<int>(H.slices.size());
+  M->n_sell_long = 0;
+  while (M->n_sell_long < M->n_sell && H.slices[M->n_sell_long].maxlen > eqb::kTileNnz)
+    ++M->n_sell_long;
   for (int mat = 0; mat < 2; ++mat) {
     std::vector<int64_t> moff;
     std::vector<int32_t> midx;
@@ -1369,7 +1373,19 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               sa.ci[k] = M->sell_ci[k].p;
               sa.va[k] = M->sell_va[k].p;
             }
-            if (M->sell_long || M->n_sgd_long == 0) {
+            if (M->sell_long == 2 && M->n_sell_long > 0) {
+              // long slices on warp-specialised CTAs, the rest on warps,
+              // concurrently (fork / join on the copy stream)
+              CK(cudaEventRecord(M->ev_fork, s));
+              CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+              eqb::SellArgs sl = sa;
+              sl.nslices = M->n_sell_long;
+              CK(eqb::launch_sgd_sell_long(a, sl, M->sell_lvariant, M->copy_stream));
+              sa.first = M->n_sell_long;
+              CK(eqb::launch_sgd_sell(a, sa, M->sell_variant, s));
+              CK(cudaEventRecord(M->ev_join, M->copy_stream));
+              CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+            } else if (M->sell_long || M->n_sgd_long == 0) {
               CK(eqb::launch_sgd_sell(a, sa, M->sell_variant, s));
             } else {
               // rows longer than a tile stay CTA-cooperative (their sequential

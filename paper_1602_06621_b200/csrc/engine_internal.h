@@ -367,8 +367,12 @@ struct equil_matrix {
   // EQUIL_SELL=0 keeps the staged warp tiles / CTA long slices
   bool use_sell = true;
   bool sell = false;
-  bool sell_long = false;  // rows longer than kTileNnz too (else kind-3 CTA groups)
-  int sell_variant = 0;
+  // rows longer than kTileNnz (EQUIL_SELL_LONG): 0 kind-3 CTA groups on the
+  // CSR arrays, 1 lane chains in the warp kernel, 2 warp-specialised CTAs
+  // (sgd_sell_long_kernel) on the interleaved arrays
+  int sell_long = 2;
+  int sell_variant = 0, sell_lvariant = 0;
+  int n_sell_long = 0;  // leading slices with rows longer than kTileNnz
   struct SellHost {
     std::vector<eqb::SellSlice> slices;
     std::vector<int32_t> row, len;

@@ -138,7 +138,7 @@ struct SellSlice {
 };
 struct SellArgs {
   const SellSlice* slices;  // both matrices, longest slices first
-  int nslices;
+  int first, nslices;       // a launch covers slices [first, nslices)
   const int32_t* row;       // local row of lane l of slice w at 32 w + l
   const int32_t* len;       // its length (0 for empty lanes)
   const int32_t* ci[2];     // interleaved slot columns
@@ -155,6 +155,9 @@ cudaError_t build_sell(const int64_t* rp, const int32_t* ci_slot, const double* 
 // compiled batch / pipelining / occupancy point (EQUIL_SELL_VARIANT)
 cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,
                             cudaStream_t s);
+// the long slices (one warp-specialised CTA each, EQUIL_SELL_LVARIANT)
+cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int variant,
+                                 cudaStream_t s);
 
 // ---- column-panel traversal (panel.cu) ------------------------------------
 // The gathered vector is cut into panels of kPanelW coordinates and the rows

@@ -70,7 +70,7 @@ template <int B, bool PIPE, int MINB, int PF = 0>
 __global__ void __launch_bounds__(128, MINB) sgd_sell_kernel(const SgdIterArgs a,
                                                              const SellArgs sa) {
   const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int w = sa.first + blockIdx.x * 4 + (threadIdx.x >> 5);
   if (w >= sa.nslices) return;
   const SellSlice sd = sa.slices[w];
   const int mat = sd.mat;
@@ -163,9 +163,129 @@ __global__ void __launch_bounds__(128, MINB) sgd_sell_kernel(const SgdIterArgs a
   if (fl) atomicOr(a.flags, fl);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Long slices (rows longer than kTileNnz): one CTA per slice, warp-specialised.
+// A lane-per-row chain that waits on its own loads would make the slice's
+// longest row (10^4 entries on c3) the critical path of the whole launch, so
+// S stager warps run ahead: stager s takes rounds s, s + S, ... (B entries of
+// every row per round: coalesced interleaved loads, gathers, rounded products)
+// into a ring of S + 1 shared-memory stages, and warp 0's lanes extend their
+// rows' sequential sums from the ring (conflict-free: lane l reads column l).
+// Stages hand over on mbarriers (full: 32 stager lanes arrive; empty: 32 chain
+// lanes arrive).  PIPE: a stager issues its next round's loads before this
+// round's gathers.  Products are formed in any order; the adds are the
+// reference's CSR-order chain.
+template <int B, int S, bool PIPE, int MINB>
+__global__ void __launch_bounds__(32 * (S + 1), MINB)
+sgd_sell_long_kernel(const SgdIterArgs a, const SellArgs sa) {
+  constexpr int R = S + 1;
+  __shared__ __align__(16) double buf[R][B * 32];
+  __shared__ __align__(8) unsigned long long full[R], empty[R];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = sa.first + blockIdx.x;
+  if (threadIdx.x < R) {
+    mbar_init(&full[threadIdx.x], 32);
+    mbar_init(&empty[threadIdx.x], 32);
+  }
+  __syncthreads();
+  if (w >= sa.nslices) return;
+  const SellSlice sd = sa.slices[w];
+  const int mat = sd.mat;
+  const int q = 32 * w + lane;
+  const int len = __ldg(sa.len + q);
+  const int rounds = (sd.maxlen + B - 1) / B;
+  if (warp > 0) {
+    const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
+    const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
+    const double* __restrict__ x = mat ? a.xw_cur : a.xs_cur;
+    int r = warp - 1;
+    int32_t c[B];
+    double v[B];
+    auto load = [&](int rr, int32_t* cc, double* vv) {
+      const int k0 = rr * B;
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (k0 + b < len) cc[b] = ld_na(cp + 32 * (k0 + b));
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (k0 + b < len) vv[b] = ld_na(vp + 32 * (k0 + b));
+    };
+    if (PIPE && r < rounds) load(r, c, v);
+    for (; r < rounds; r += S) {
+      const int k0 = r * B;
+      int32_t cn[B];
+      double vn[B];
+      if constexpr (PIPE) {
+        if (r + S < rounds) load(r + S, cn, vn);
+      } else {
+        load(r, c, v);
+      }
+      double g[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (k0 + b < len) g[b] = __ldg(x + c[b]);
+      const int bi = r % R;
+      if (r >= R) mbar_wait(&empty[bi], ((r / R) - 1) & 1);
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (k0 + b < len) buf[bi][32 * b + lane] = __dmul_rn(v[b], g[b]);
+      mbar_arrive(&full[bi]);
+      if constexpr (PIPE) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          c[b] = cn[b];
+          v[b] = vn[b];
+        }
+      }
+    }
+    return;
+  }
+  double acc = 0.0;
+  for (int r = 0; r < rounds; ++r) {
+    const int bi = r % R;
+    mbar_wait(&full[bi], (r / R) & 1);
+    const int k0 = r * B;
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (k0 + b < len) acc = __dadd_rn(acc, buf[bi][32 * b + lane]);
+    mbar_arrive(&empty[bi]);
+  }
+  unsigned fl = 0;
+  if (lane < sd.cnt) sgd_epilogue(a, mat, __ldg(sa.row + q), acc, fl);
+  if (a.npeer) __threadfence_system();
+  if (fl) atomicOr(a.flags, fl);
+}
+
+template <int B, int S, bool PIPE, int MINB>
+void launch_long_variant(const SgdIterArgs& a, const SellArgs& sa, cudaStream_t s) {
+  sgd_sell_long_kernel<B, S, PIPE, MINB>
+      <<<static_cast<unsigned>(sa.nslices - sa.first), 32 * (S + 1), 0, s>>>(a, sa);
+}
+
 template <int B, bool PIPE, int MINB, int PF = 0>
 void launch_variant(const SgdIterArgs& a, const SellArgs& sa, cudaStream_t s) {
-  const unsigned g = static_cast<unsigned>((sa.nslices + 3) / 4);
+  const unsigned g = static_cast<unsigned>((sa.nslices - sa.first + 3) / 4);
   sgd_sell_kernel<B, PIPE, MINB, PF><<<g, 128, 0, s>>>(a, sa);
 }
 
@@ -182,22 +302,29 @@ cudaError_t build_sell(const int64_t* rp, const int32_t* ci_slot, const double* 
   return cudaGetLastError();
 }
 
+cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int variant,
+                                 cudaStream_t s) {
+  if (sa.nslices <= sa.first) return cudaSuccess;
+  switch (variant) {  // EQUIL_SELL_LVARIANT (A/B knob); 0 = measured best on c3
+    case 1: launch_long_variant<8, 7, true, 2>(a, sa, s); break;
+    case 2: launch_long_variant<4, 7, true, 3>(a, sa, s); break;
+    case 3: launch_long_variant<2, 15, true, 2>(a, sa, s); break;
+    case 4: launch_long_variant<8, 7, false, 2>(a, sa, s); break;
+    default: launch_long_variant<4, 15, true, 1>(a, sa, s); break;
+  }
+  count_launch(s);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,
                             cudaStream_t s) {
-  if (sa.nslices == 0) return cudaSuccess;
+  if (sa.nslices <= sa.first) return cudaSuccess;
   switch (variant) {  // EQUIL_SELL_VARIANT (A/B knob); 0 = measured best on c3
     case 1: launch_variant<4, false, 12>(a, sa, s); break;
     case 2: launch_variant<8, false, 8>(a, sa, s); break;
     case 3: launch_variant<16, false, 6>(a, sa, s); break;
-    case 4: launch_variant<4, true, 8>(a, sa, s); break;
-    case 5: launch_variant<8, true, 8>(a, sa, s); break;
-    case 6: launch_variant<6, true, 8>(a, sa, s); break;
-    case 7: launch_variant<12, true, 5>(a, sa, s); break;
-    case 8: launch_variant<16, false, 6, 2>(a, sa, s); break;
-    case 9: launch_variant<16, false, 6, 4>(a, sa, s); break;
-    case 10: launch_variant<8, false, 8, 4>(a, sa, s); break;
-    case 11: launch_variant<8, false, 8, 8>(a, sa, s); break;
-    case 12: launch_variant<16, false, 4, 4>(a, sa, s); break;
+    case 4: launch_variant<8, true, 8>(a, sa, s); break;
+    case 5: launch_variant<16, false, 6, 2>(a, sa, s); break;
     default: launch_variant<8, true, 6>(a, sa, s); break;
   }
   count_launch(s);
