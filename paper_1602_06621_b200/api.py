@@ -651,10 +651,19 @@ def sgd_equilibrate_device(op: ExplicitMatrix, params: EquilibrationParams,
 
 
 def sgd_equilibrate_csr(rows: int, cols: int, row_ptr, col, val,
-                        params: EquilibrationParams, device: int = 0) -> ScalingResult:
+                        params: EquilibrationParams, device: int = 0,
+                        out=None) -> ScalingResult:
     """One-shot C-ABI entry (equil_sgd_equilibrate_csr): host CSR in, host
-    scaling out; upload, device transpose, equilibration and download inside."""
-    u, v, d, e = np.zeros(rows), np.zeros(cols), np.zeros(rows), np.zeros(cols)
+    scaling out; upload, device transpose, equilibration and download inside.
+    out: optional (u, v, d, e) float64 host arrays (e.g. pinned) to write into."""
+    if out is None:
+        u, v, d, e = np.zeros(rows), np.zeros(cols), np.zeros(rows), np.zeros(cols)
+    else:
+        u, v, d, e = out
+        for a, ln in ((u, rows), (v, cols), (d, rows), (e, cols)):
+            if a.dtype != np.float64 or a.shape != (ln,) or not a.flags.c_contiguous:
+                raise ValueError("sgd_equilibrate_csr: out arrays must be contiguous float64 "
+                                 "of lengths (rows, cols, rows, cols)")
     out = L.ScalingOut(L.ptr(u, L._dp), L.ptr(v, L._dp), L.ptr(d, L._dp), L.ptr(e, L._dp), 0,
                        0.0, 0.0, 0, 0, 0, 0, None, None, None, 0, 0)
     p = params._c()

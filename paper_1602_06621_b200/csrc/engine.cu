@@ -87,6 +87,21 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
     for (int k = 0; k < cnt; ++k) P.rowlist.push_back(static_cast<int32_t>(longs[q + k].second));
     for (int w = 0; w < eqb::kTileWarps; ++w) P.lng.push_back(t);
   }
+  // interleaved-slice entries, longest first
+  auto ent = [&](const eqb::Tile& t, int lng) {
+    int64_t mx = 0;
+    for (int k = 0; k < t.r1; ++k) {
+      const int32_t r = P.rowlist[t.r0 + k];
+      mx = std::max<int64_t>(mx, rp[r + 1] - rp[r]);
+    }
+    return SellEnt{static_cast<int32_t>(mx), static_cast<int16_t>(t.r1),
+                   static_cast<int16_t>(lng), t.r0};
+  };
+  P.sell.reserve(P.lng.size() / eqb::kTileWarps + P.slices.size());
+  for (size_t q = 0; q < P.lng.size(); q += eqb::kTileWarps) P.sell.push_back(ent(P.lng[q], 1));
+  for (const eqb::Tile& t : P.slices) P.sell.push_back(ent(t, 0));
+  std::stable_sort(P.sell.begin(), P.sell.end(),
+                   [](const SellEnt& a, const SellEnt& b) { return a.maxlen > b.maxlen; });
   return P;
 }
 
@@ -187,55 +202,53 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
 // Upload the traversal plans of the local CSR(A) / CSR(A^T) shards.  The SGD
 // launch covers both matrices: every long row (longest first, so the longest
 // sequential chains start first), then the slices of A and of A^T.
-// The interleaved-slice plan (sell.cu) reuses the same row groups: every
-// kind-3 group and kind-2 slice becomes one slice, and the slices of both
-// matrices are ordered longest first (ties keep plan order).
-void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt, const int64_t* rpa,
-               const int64_t* rpt) {
+// Merge the two matrices' interleaved-slice lists (both longest first; ties
+// take A first) into the launch order, and lay out each matrix's arrays in it.
+void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
   equil_matrix::SellHost& H = M->sell_host;
   H = equil_matrix::SellHost{};
-  struct Ent {
-    int32_t maxlen;
-    int16_t mat, cnt;
-    int32_t r0;
+  struct Src {
+    const SellEnt* e;
+    int mat;
   };
-  std::vector<Ent> ents;
-  for (int mat = 0; mat < 2; ++mat) {
-    const Plan& P = mat ? pt : pa;
-    const int64_t* rp = mat ? rpt : rpa;
-    auto add = [&](const eqb::Tile& t) {
-      int32_t mx = 0;
-      for (int k = 0; k < t.r1; ++k) {
-        const int32_t r = P.rowlist[t.r0 + k];
-        mx = std::max<int32_t>(mx, static_cast<int32_t>(rp[r + 1] - rp[r]));
-      }
-      ents.push_back({mx, static_cast<int16_t>(mat), static_cast<int16_t>(t.r1), t.r0});
+  std::vector<Src> order;
+  order.reserve(pa.sell.size() + pt.sell.size());
+  {
+    size_t i = 0, j = 0;
+    auto skip = [&](const std::vector<SellEnt>& v, size_t& k) {
+      while (k < v.size() && v[k].lng && !M->sell_long) ++k;
     };
-    if (M->sell_long)
-      for (size_t q = 0; q < P.lng.size(); q += eqb::kTileWarps) add(P.lng[q]);
-    for (const eqb::Tile& t : P.slices) add(t);
-  }
-  std::stable_sort(ents.begin(), ents.end(),
-                   [](const Ent& a, const Ent& b) { return a.maxlen > b.maxlen; });
-  H.slices.resize(ents.size());
-  H.row.assign(32 * ents.size(), 0);
-  H.len.assign(32 * ents.size(), 0);
-  for (size_t w = 0; w < ents.size(); ++w) {
-    const Ent& e = ents[w];
-    const Plan& P = e.mat ? pt : pa;
-    const int64_t* rp = e.mat ? rpt : rpa;
-    H.slices[w] = {H.total[e.mat], e.maxlen, e.cnt, e.mat};
-    H.total[e.mat] += 32 * static_cast<int64_t>(e.maxlen);
-    for (int k = 0; k < e.cnt; ++k) {
-      const int32_t r = P.rowlist[e.r0 + k];
-      H.row[32 * w + k] = r;
-      H.len[32 * w + k] = static_cast<int32_t>(rp[r + 1] - rp[r]);
+    skip(pa.sell, i);
+    skip(pt.sell, j);
+    while (i < pa.sell.size() || j < pt.sell.size()) {
+      if (j >= pt.sell.size() || (i < pa.sell.size() && pa.sell[i].maxlen >= pt.sell[j].maxlen)) {
+        order.push_back({&pa.sell[i++], 0});
+        skip(pa.sell, i);
+      } else {
+        order.push_back({&pt.sell[j++], 1});
+        skip(pt.sell, j);
+      }
     }
   }
+  const size_t ns = order.size();
+  H.slices.resize(ns);
+  for (int mat = 0; mat < 2; ++mat) H.kbp[mat].assign(1, 0);
+  for (size_t w = 0; w < ns; ++w) {
+    const SellEnt& e = *order[w].e;
+    const int mat = order[w].mat;
+    H.slices[w] = {H.total[mat], e.maxlen, e.cnt, static_cast<int16_t>(mat)};
+    H.total[mat] += 32 * static_cast<int64_t>(e.maxlen);
+    if (e.maxlen > 0) {
+      H.midx[mat].push_back(static_cast<int32_t>(w));
+      H.kbp[mat].push_back(H.kbp[mat].back() + (e.maxlen + 31) / 32);
+    }
+  }
+  H.r0.resize(ns);
+  for (size_t w = 0; w < ns; ++w) H.r0[w] = order[w].e->r0;
 }
 
-// Device arrays of the interleaved slices, from the slot-remapped columns (the
-// slot layout must be built).  The slot copies of the columns are then dropped.
+// Device arrays of the interleaved slices, columns mapped to slots on the way
+// (the slot layout must be built).
 void build_sell_layout(equil_matrix* M) {
   M->sell = false;
   if (!M->use_sell || !M->slots || M->use_panels || M->nblk[0] > 1 || M->nblk[1] > 1) return;
@@ -247,31 +260,33 @@ void build_sell_layout(equil_matrix* M) {
       CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice, s));
   };
   upload(M->sell_slices, H.slices);
-  upload(M->sell_row, H.row);
-  upload(M->sell_len, H.len);
   M->n_sell = static_cast<int>(H.slices.size());
+  {  // lane -> row and length, from the device row lists
+    DevBuf<int32_t> dr0;
+    upload(dr0, H.r0);
+    M->sell_row.alloc(32 * static_cast<size_t>(M->n_sell));
+    M->sell_len.alloc(32 * static_cast<size_t>(M->n_sell));
+    CK(eqb::launch_sell_rows(M->sell_slices.p, dr0.p, M->n_sell, M->rowlist_a.p,
+                             M->rowlist_t.p, M->A.row_ptr, M->AT.row_ptr, M->sell_row.p,
+                             M->sell_len.p, s));
+    CK(cudaStreamSynchronize(s));
+  }
   M->n_sell_long = 0;
   while (M->n_sell_long < M->n_sell && H.slices[M->n_sell_long].maxlen > eqb::kTileNnz)
     ++M->n_sell_long;
   for (int mat = 0; mat < 2; ++mat) {
-    std::vector<int64_t> moff;
-    std::vector<int32_t> midx;
-    for (size_t w = 0; w < H.slices.size(); ++w)
-      if (H.slices[w].mat == mat && H.slices[w].maxlen > 0) {
-        moff.push_back(H.slices[w].off);
-        midx.push_back(static_cast<int32_t>(w));
-      }
     M->sell_ci[mat].alloc(H.total[mat]);
     M->sell_va[mat].alloc(H.total[mat]);
-    DevBuf<int64_t> doff;
+    DevBuf<int64_t> dkbp;
     DevBuf<int32_t> didx;
-    upload(doff, moff);
-    upload(didx, midx);
+    upload(dkbp, H.kbp[mat]);
+    upload(didx, H.midx[mat]);
     const eqb::DevCsr& C = mat ? M->AT : M->A;
-    CK(eqb::build_sell(C.row_ptr, mat ? M->t_ci_sgd.p : M->a_ci_sgd.p, C.val, doff.p, didx.p,
-                       static_cast<int>(moff.size()), M->sell_row.p, M->sell_len.p,
-                       H.total[mat], M->sell_ci[mat].p, M->sell_va[mat].p, s));
-    CK(cudaStreamSynchronize(s));  // before doff / didx go
+    // columns of A index xs (slot map smap), columns of A^T index xw (wmap)
+    CK(eqb::build_sell(C.row_ptr, C.col, mat ? M->wmap.p : M->smap.p, C.val, dkbp.p, didx.p,
+                       static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
+                       M->sell_len.p, M->sell_ci[mat].p, M->sell_va[mat].p, s));
+    CK(cudaStreamSynchronize(s));  // before dkbp / didx go
   }
   if (M->sell_long || M->n_sgd_long == 0) {  // the staged kernel no longer runs
     M->a_ci_sgd.release();
@@ -281,9 +296,8 @@ void build_sell_layout(equil_matrix* M) {
   M->sell = true;
 }
 
-void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt, const int64_t* rpa,
-                  const int64_t* rpt) {
-  if (M->use_sell) plan_sell(M, pa, pt, rpa, rpt);
+void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
+  if (M->use_sell) plan_sell(M, pa, pt);
   // kind-3 groups (4 entries each) first, so every group starts on a CTA
   std::vector<eqb::Tile> sgd = pa.lng;
   sgd.insert(sgd.end(), pt.lng.begin(), pt.lng.end());
@@ -545,10 +559,12 @@ void build_slot_layout(equil_matrix* M, const int64_t* rpA_dev, const int64_t* r
   M->smap.alloc(M->n_pad());
   CK(eqb::launch_slot_map(rpA_dev, M->m, abd, G, M->a_max, M->wmap.p, s));
   CK(eqb::launch_slot_map(rpT_dev, M->n, tbd, G, M->t_max, M->smap.p, s));
-  M->a_ci_sgd.alloc(M->A.nnz);
-  M->t_ci_sgd.alloc(M->AT.nnz);
-  CK(eqb::launch_remap_cols(M->a_ci_sgd.p, M->A.col, M->smap.p, M->A.nnz, s));
-  CK(eqb::launch_remap_cols(M->t_ci_sgd.p, M->AT.col, M->wmap.p, M->AT.nnz, s));
+  if (!M->use_sell || M->sell_long == 0) {  // slot-mapped columns of the staged traversal
+    M->a_ci_sgd.alloc(M->A.nnz);
+    M->t_ci_sgd.alloc(M->AT.nnz);
+    CK(eqb::launch_remap_cols(M->a_ci_sgd.p, M->A.col, M->smap.p, M->A.nnz, s));
+    CK(eqb::launch_remap_cols(M->t_ci_sgd.p, M->AT.col, M->wmap.p, M->AT.nnz, s));
+  }
   M->slots = true;  // complete when `stream` reaches here (setup ends with a sync)
 }
 
@@ -617,8 +633,7 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   const std::vector<int64_t> la = local_rp(rpA_host, M->a_bounds);
   const std::vector<int64_t> lt = local_rp(rpT_host, M->t_bounds);
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
-               plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1), la.data(),
-               lt.data());
+               plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
   build_panel_layout(M, la.data(), lt.data());
   build_block_layout(M);
   build_slot_layout(M, fullA.row_ptr, fullT.row_ptr);
@@ -693,9 +708,9 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     if (planner && planner->joinable()) planner->join();
     pt.mark(s, "plan A (join)");
     if (planA)  // computed concurrently by the caller
-      upload_plans(M, *planA, planT, row_ptr, rpT.data());
+      upload_plans(M, *planA, planT);
     else
-      upload_plans(M, plan_tiles(row_ptr, m, 0), planT, row_ptr, rpT.data());
+      upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
     pt.mark(s, "upload plans");
     build_panel_layout(M, row_ptr, rpT.data());
     pt.mark(s, "panels");
@@ -1422,7 +1437,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       }
     };
 
-    if (dp.stride == 0 && T > 0 && !M->hx) {  // (the host exchange cannot be captured)
+    if (dp.stride == 0 && T > 0 && !M->hx && !M->oneshot) {  // (host exchange: no capture)
       // capture the whole T loop once per (T, targets, gamma, M) and replay it
       equil_matrix::Key key{T, alpha, beta, gamma, Mx, vec_lin};
       if (!M->graph || !(M->graph_key == key)) {
@@ -2040,6 +2055,7 @@ equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_
   equil_matrix* M = nullptr;
   equil_status rc = equil_matrix_create_csr(m, n, row_ptr, col, val, cfg, &M);
   if (rc != EQUIL_OK) return rc;
+  M->oneshot = true;  // one call on this handle: launch the loop directly, no graph
   rc = equil_sgd_equilibrate(M, p, nullptr, out);
   equil_matrix_destroy(M);
   return rc;

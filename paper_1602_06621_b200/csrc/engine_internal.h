@@ -273,9 +273,19 @@ inline void validate_params(const equil_params& p) {
 // affects results: each row is an independent sequential sum.  Windows are
 // planned in parallel host threads; the result does not depend on the thread
 // count (parts are concatenated in window order, ties keep row order).
+// The interleaved-slice plan (sell.cu) reuses the same row groups: every
+// kind-3 group and every kind-2 slice becomes one slice, listed longest first
+// (stable), so merging the two matrices' lists keeps the launch longest first.
+struct SellEnt {
+  int32_t maxlen;  // entries of the group's longest row
+  int16_t cnt;     // rows
+  int16_t lng;     // a kind-3 group (rows longer than kTileNnz)
+  int32_t r0;      // first row in rowlist
+};
 struct Plan {
   std::vector<eqb::Tile> lng, slices;
   std::vector<int32_t> rowlist;
+  std::vector<SellEnt> sell;
 };
 
 Plan plan_tiles(const int64_t* rp, int64_t rows, int mat);
@@ -375,8 +385,12 @@ struct equil_matrix {
   int n_sell_long = 0;  // leading slices with rows longer than kTileNnz
   struct SellHost {
     std::vector<eqb::SellSlice> slices;
-    std::vector<int32_t> row, len;
+    std::vector<int32_t> r0;  // first row of each slice in its matrix's row list
     int64_t total[2] = {0, 0};
+    // per matrix: its slices in launch order (indices into slices) and the
+    // prefix of their 32-entry blocks (the device build's work items)
+    std::vector<int32_t> midx[2];
+    std::vector<int64_t> kbp[2];
   } sell_host;
   DevBuf<eqb::SellSlice> sell_slices;
   DevBuf<int32_t> sell_row, sell_len, sell_ci[2];
@@ -420,7 +434,9 @@ struct equil_matrix {
   DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
   DevBuf<double> lin_u, lin_v;  // per-coordinate targets (sgd_equilibrate_targets)
 
-  // graph cache for the SGD loop
+  // graph cache for the SGD loop (not built for a one-shot handle, whose
+  // single call would pay capture and instantiation for one replay)
+  bool oneshot = false;
   cudaGraphExec_t graph = nullptr;
   long long graph_launches = 0;  // kernel nodes per replay
   struct Key {

@@ -144,13 +144,19 @@ struct SellArgs {
   const int32_t* ci[2];     // interleaved slot columns
   const double* va[2];      // interleaved values
 };
-// Fill matrix `mat`'s interleaved arrays (total elements) from CSR rows whose
-// columns are already slots (ci_slot); moff / midx: that matrix's slices in
-// offset order and their indices into the slice list.
-cudaError_t build_sell(const int64_t* rp, const int32_t* ci_slot, const double* val,
-                       const int64_t* moff, const int32_t* midx, int nmat_slices,
-                       const int32_t* row, const int32_t* len, int64_t total,
+// Fill one matrix's interleaved arrays from its CSR rows, columns mapped
+// through map (slots; nullptr: unchanged).  midx: that matrix's slices (indices
+// into slices) in launch order; kbp: prefix of their 32-entry blocks.
+cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
+                       const int64_t* kbp, const int32_t* midx, int nmat_slices,
+                       const SellSlice* slices, const int32_t* row, const int32_t* len,
                        int32_t* out_ci, double* out_va, cudaStream_t s);
+// row[32 w + l] / len[32 w + l] of every slice lane from the plans' row lists
+// (slice w lists rows rowlist_{mat}[r0[w] ...]); empty lanes get 0 / 0
+cudaError_t launch_sell_rows(const SellSlice* slices, const int32_t* r0, int nslices,
+                             const int32_t* rowlist_a, const int32_t* rowlist_t,
+                             const int64_t* rp_a, const int64_t* rp_t, int32_t* row,
+                             int32_t* len, cudaStream_t s);
 // one SGD iteration over every slice (both matrices); variant selects the
 // compiled batch / pipelining / occupancy point (EQUIL_SELL_VARIANT)
 cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,

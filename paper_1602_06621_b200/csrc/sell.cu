@@ -20,33 +20,70 @@
 namespace eqb {
 namespace {
 
-__global__ void build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                  const double* __restrict__ val,
-                                  const int64_t* __restrict__ moff,
-                                  const int32_t* __restrict__ midx, int nms,
-                                  const int32_t* __restrict__ row,
-                                  const int32_t* __restrict__ len, int64_t total,
-                                  int32_t* __restrict__ oc, double* __restrict__ ov) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= total) return;
-  int lo = 0, hi = nms;  // last slice with moff <= e
+// One warp per work item = (slice, block of 32 entries per row): the rows'
+// entries are read row by row (coalesced along the row, columns mapped to
+// slots), transposed through shared memory and written interleaved (coalesced
+// along the lanes).  Lanes past a row's end write zero padding.
+__global__ void __launch_bounds__(64)
+build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                  const int32_t* __restrict__ map, const double* __restrict__ val,
+                  const int64_t* __restrict__ kbp, const int32_t* __restrict__ midx, int nms,
+                  const SellSlice* __restrict__ slices, const int32_t* __restrict__ row,
+                  const int32_t* __restrict__ len, int32_t* __restrict__ oc,
+                  double* __restrict__ ov) {
+  __shared__ int32_t tc[2][32][33];
+  __shared__ double tv[2][32][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = blockIdx.x * 2LL + warp;
+  if (item >= kbp[nms]) return;
+  int lo = 0, hi = nms;  // last slice with kbp[j] <= item
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (moff[mid] <= e) lo = mid; else hi = mid;
+    if (kbp[mid] <= item) lo = mid; else hi = mid;
   }
-  const int64_t rel = e - moff[lo];
-  const int lane = static_cast<int>(rel & 31);
-  const int64_t k = rel >> 5;
-  const int64_t q = 32 * static_cast<int64_t>(midx[lo]) + lane;
-  int32_t c = 0;
-  double v = 0.0;
-  if (k < len[q]) {
-    const int64_t src = rp[row[q]] + k;
-    c = ci[src];
-    v = val[src];
+  const int w = midx[lo];
+  const int k0 = static_cast<int>(item - kbp[lo]) * 32;
+  const SellSlice sd = slices[w];
+  const int mylen = len[32 * w + lane];
+  const int64_t mystart = lane < sd.cnt ? rp[row[32 * w + lane]] : 0;
+  for (int r = 0; r < sd.cnt; ++r) {
+    const int64_t st = __shfl_sync(0xffffffffu, mystart, r);
+    const int ln = __shfl_sync(0xffffffffu, mylen, r);
+    const int k = k0 + lane;
+    if (k < ln) {
+      const int32_t c = ci[st + k];
+      tc[warp][lane][r] = map ? map[c] : c;
+      tv[warp][lane][r] = val[st + k];
+    }
   }
-  oc[e] = c;
-  ov[e] = v;
+  __syncwarp();
+  const int kend = min(32, sd.maxlen - k0);
+  for (int kk = 0; kk < kend; ++kk) {
+    const int64_t dst = sd.off + static_cast<int64_t>(k0 + kk) * 32 + lane;
+    const bool ok = lane < sd.cnt && k0 + kk < mylen;
+    oc[dst] = ok ? tc[warp][kk][lane] : 0;
+    ov[dst] = ok ? tv[warp][kk][lane] : 0.0;
+  }
+}
+
+__global__ void sell_rows_kernel(const SellSlice* __restrict__ slices,
+                                 const int32_t* __restrict__ r0, int nslices,
+                                 const int32_t* __restrict__ rla, const int32_t* __restrict__ rlt,
+                                 const int64_t* __restrict__ rpa, const int64_t* __restrict__ rpt,
+                                 int32_t* __restrict__ row, int32_t* __restrict__ len) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= 32LL * nslices) return;
+  const int64_t w = q >> 5;
+  const int lane = static_cast<int>(q & 31);
+  const SellSlice sd = slices[w];
+  int32_t r = 0, l = 0;
+  if (lane < sd.cnt) {
+    r = (sd.mat ? rlt : rla)[r0[w] + lane];
+    const int64_t* rp = sd.mat ? rpt : rpa;
+    l = static_cast<int32_t>(rp[r + 1] - rp[r]);
+  }
+  row[q] = r;
+  len[q] = l;
 }
 
 // L2 prefetch of the slice's interleaved entries [k, k + B) (one bulk request
@@ -291,13 +328,30 @@ void launch_variant(const SgdIterArgs& a, const SellArgs& sa, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t build_sell(const int64_t* rp, const int32_t* ci_slot, const double* val,
-                       const int64_t* moff, const int32_t* midx, int nmat_slices,
-                       const int32_t* row, const int32_t* len, int64_t total,
+cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
+                       const int64_t* kbp, const int32_t* midx, int nmat_slices,
+                       const SellSlice* slices, const int32_t* row, const int32_t* len,
                        int32_t* out_ci, double* out_va, cudaStream_t s) {
-  if (total == 0 || nmat_slices == 0) return cudaSuccess;
-  build_sell_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-      rp, ci_slot, val, moff, midx, nmat_slices, row, len, total, out_ci, out_va);
+  if (nmat_slices == 0) return cudaSuccess;
+  int64_t items = 0;
+  cudaError_t e = cudaMemcpyAsync(&items, kbp + nmat_slices, sizeof items,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess || items == 0) return e;
+  build_sell_kernel<<<static_cast<unsigned>((items + 1) / 2), 64, 0, s>>>(
+      rp, ci, map, val, kbp, midx, nmat_slices, slices, row, len, out_ci, out_va);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sell_rows(const SellSlice* slices, const int32_t* r0, int nslices,
+                             const int32_t* rowlist_a, const int32_t* rowlist_t,
+                             const int64_t* rp_a, const int64_t* rp_t, int32_t* row,
+                             int32_t* len, cudaStream_t s) {
+  if (nslices == 0) return cudaSuccess;
+  const int64_t n = 32LL * nslices;
+  sell_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      slices, r0, nslices, rowlist_a, rowlist_t, rp_a, rp_t, row, len);
   count_launch(s);
   return cudaGetLastError();
 }
