@@ -160,6 +160,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SELL_VARIANT")) M->sell_variant = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_LONG")) M->sell_long = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_LVARIANT")) M->sell_lvariant = atoi(e);
+  if (const char* e = getenv("EQUIL_SELL_PASSES")) M->sell_passes = atoi(e) != 0;
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -244,7 +245,75 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
     }
   }
   H.r0.resize(ns);
-  for (size_t w = 0; w < ns; ++w) H.r0[w] = order[w].e->r0;
+  for (size_t w = 0; w < ns; ++w) {
+    H.r0[w] = order[w].e->r0;
+    const int mat = order[w].mat;
+    H.pidx[mat].push_back(static_cast<int32_t>(w));
+    if (order[w].e->maxlen > eqb::kTileNnz) ++H.plong[mat];
+  }
+}
+
+// The generic passes' column arrays (padded coordinates) and per-matrix slice
+// orders, on first use.
+void ensure_sell_pass(equil_matrix* M) {
+  if (M->sell_pass || !M->sell) return;
+  const equil_matrix::SellHost& H = M->sell_host;
+  cudaStream_t s = M->stream;
+  for (int mat = 0; mat < 2; ++mat) {
+    M->sell_pci[mat].alloc(H.total[mat]);
+    M->sell_pidx[mat].alloc(H.pidx[mat].size());
+    if (!H.pidx[mat].empty())
+      CK(cudaMemcpyAsync(M->sell_pidx[mat].p, H.pidx[mat].data(), H.pidx[mat].size() * 4,
+                         cudaMemcpyHostToDevice, s));
+    DevBuf<int64_t> dkbp;
+    DevBuf<int32_t> didx;
+    dkbp.alloc(H.kbp[mat].size());
+    didx.alloc(H.midx[mat].size());
+    CK(cudaMemcpyAsync(dkbp.p, H.kbp[mat].data(), H.kbp[mat].size() * 8, cudaMemcpyHostToDevice,
+                       s));
+    if (!H.midx[mat].empty())
+      CK(cudaMemcpyAsync(didx.p, H.midx[mat].data(), H.midx[mat].size() * 4,
+                         cudaMemcpyHostToDevice, s));
+    const eqb::DevCsr& C = mat ? M->AT : M->A;
+    CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, didx.p,
+                       static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
+                       M->sell_len.p, M->sell_pci[mat].p, nullptr, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  M->sell_pass = true;
+}
+
+// One generic pass (b: the dual pass) over matrix `mat` on the interleaved
+// slices: long slices on the copy stream, warp slices on the main stream.
+void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::PassArgs* b) {
+  ensure_sell_pass(M);
+  const equil_matrix::SellHost& H = M->sell_host;
+  cudaStream_t s = M->stream;
+  eqb::SellArgs sa{};
+  sa.slices = M->sell_slices.p;
+  sa.order = M->sell_pidx[mat].p;
+  sa.row = M->sell_row.p;
+  sa.len = M->sell_len.p;
+  for (int k = 0; k < 2; ++k) {
+    sa.ci[k] = M->sell_pci[k].p;
+    sa.va[k] = M->sell_va[k].p;
+  }
+  const int nl = H.plong[mat], nall = static_cast<int>(H.pidx[mat].size());
+  if (nl > 0) {
+    CK(cudaEventRecord(M->ev_fork, s));
+    CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+    eqb::SellArgs sl = sa;
+    sl.first = 0;
+    sl.nslices = nl;
+    CK(eqb::launch_sell_pass(a, b, sl, true, M->copy_stream));
+  }
+  sa.first = nl;
+  sa.nslices = nall;
+  CK(eqb::launch_sell_pass(a, b, sa, false, s));
+  if (nl > 0) {
+    CK(cudaEventRecord(M->ev_join, M->copy_stream));
+    CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+  }
 }
 
 // Device arrays of the interleaved slices, columns mapped to slots on the way
@@ -292,8 +361,9 @@ void build_sell_layout(equil_matrix* M) {
     M->a_ci_sgd.release();
     M->t_ci_sgd.release();
   }
-  M->sell_host = equil_matrix::SellHost{};
   M->sell = true;
+  M->sell_pass = false;
+  if (M->sell_long == 0) M->sell_passes = false;  // long rows are not in the slices
 }
 
 void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
@@ -1677,6 +1747,10 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
   a.prev = prev;
   a.coef = coef;
   a.mode = mode;
+  if (M->sell && M->sell_passes) {
+    sell_pass(M, adjoint ? 1 : 0, a, nullptr);
+    return;
+  }
   CK(eqb::launch_pass(a, adjoint ? M->n_t : M->n_a, M->stream));
 }
 
@@ -1701,6 +1775,10 @@ void apply_pass_dual(equil_matrix* M, const double* xg0, double* out0, int mode0
   }
   a.xg = xg0; a.out = out0; a.mode = mode0; a.scale = scale0; a.prev = prev0; a.coef = coef0;
   b.xg = xg1; b.out = out1; b.mode = mode1; b.scale = scale1; b.prev = prev1; b.coef = coef1;
+  if (M->sell && M->sell_passes) {
+    sell_pass(M, 0, a, &b);
+    return;
+  }
   CK(eqb::launch_pass_dual(a, b, M->n_a, M->stream));
 }
 

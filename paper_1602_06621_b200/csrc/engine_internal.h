@@ -391,11 +391,21 @@ struct equil_matrix {
     // prefix of their 32-entry blocks (the device build's work items)
     std::vector<int32_t> midx[2];
     std::vector<int64_t> kbp[2];
+    // per matrix: every slice in launch order (passes over one matrix) and
+    // how many of them lead with rows longer than kTileNnz
+    std::vector<int32_t> pidx[2];
+    int plong[2] = {0, 0};
   } sell_host;
   DevBuf<eqb::SellSlice> sell_slices;
   DevBuf<int32_t> sell_row, sell_len, sell_ci[2];
   DevBuf<double> sell_va[2];
   int n_sell = 0;
+  // the generic passes (LSQR, apply, variants) over the same slices: columns
+  // in padded coordinates (their vectors are not in slot layout), built on
+  // first use; values shared with the SGD arrays
+  bool sell_passes = true;  // EQUIL_SELL_PASSES=0: generic passes on the staged kernels
+  bool sell_pass = false;
+  DevBuf<int32_t> sell_pci[2], sell_pidx[2];
   // column blocks of the gathered vectors (build_block_layout): per matrix
   int nblk[2] = {1, 1};
   int64_t bwidth[2] = {0, 0};

@@ -138,7 +138,8 @@ struct SellSlice {
 };
 struct SellArgs {
   const SellSlice* slices;  // both matrices, longest slices first
-  int first, nslices;       // a launch covers slices [first, nslices)
+  int first, nslices;       // a launch covers positions [first, nslices)
+  const int32_t* order;     // position -> slice (nullptr: identity)
   const int32_t* row;       // local row of lane l of slice w at 32 w + l
   const int32_t* len;       // its length (0 for empty lanes)
   const int32_t* ci[2];     // interleaved slot columns
@@ -298,6 +299,11 @@ cudaError_t launch_pass(const PassArgs& a, int ntiles, cudaStream_t s);
 // two passes over the same matrix (same tiles) in one traversal: a and b differ
 // only in the gathered vector and the epilogue (LSQR: residual + next B v)
 cudaError_t launch_pass_dual(const PassArgs& a, const PassArgs& b, int ntiles, cudaStream_t s);
+// a pass over the interleaved slices listed in sa (one matrix; columns in
+// padded coordinates): lng selects the warp-specialised long-slice kernel;
+// b non-null: the dual pass
+cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArgs& sa, bool lng,
+                             cudaStream_t s);
 // tiles [tile_base, tile_base + ntiles); b non-null: the dual pass
 cudaError_t launch_pass_range(const PassArgs& a, const PassArgs* b, int tile_base, int ntiles,
                               cudaStream_t s);

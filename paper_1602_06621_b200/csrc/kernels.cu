@@ -964,32 +964,6 @@ cudaError_t launch_exp(const double* x, double* y, int64_t n, double scale,
 // ---------------------------------------------------------------------------
 namespace {
 
-__device__ __forceinline__ void pass_epilogue(const PassArgs& a, int64_t r,
-                                              double acc) {
-  switch (a.mode) {
-    case kPassPlain:
-      a.out[r] = acc;
-      break;
-    case kPassLsqrU:
-    case kPassLsqrV: {  // B.apply(v) - alpha*u  (lsqr.cpp:39, :49)
-      const double bv = a.scale ? __dmul_rn(a.scale[r], acc) : acc;
-      a.out[r] = __dsub_rn(bv, __dmul_rn(*a.coef, a.prev[r]));
-      break;
-    }
-    case kPassResid:  // b - A x  (lsqr.cpp:97, :131)
-      a.out[r] = __dsub_rn(a.prev[r], acc);
-      break;
-    case kPassScaled:
-      a.out[r] = a.scale ? __dmul_rn(a.scale[r], acc) : acc;
-      break;
-    case kPassEst: {  // estimate_row_norms_sq: y = s_i * acc, y * y (estimator.cpp:5-9)
-      const double y = __dmul_rn(a.scale[r], acc);
-      a.out[r] = __dmul_rn(y, y);
-      break;
-    }
-  }
-}
-
 __device__ __forceinline__ void full_row(const int64_t* rp, int64_t r, int64_t& k0, int64_t& k1,
                                          double& acc0) {
   k0 = rp[r];

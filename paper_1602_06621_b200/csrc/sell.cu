@@ -53,7 +53,7 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
     if (k < ln) {
       const int32_t c = ci[st + k];
       tc[warp][lane][r] = map ? map[c] : c;
-      tv[warp][lane][r] = val[st + k];
+      if (ov) tv[warp][lane][r] = val[st + k];
     }
   }
   __syncwarp();
@@ -62,7 +62,7 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
     const int64_t dst = sd.off + static_cast<int64_t>(k0 + kk) * 32 + lane;
     const bool ok = lane < sd.cnt && k0 + kk < mylen;
     oc[dst] = ok ? tc[warp][kk][lane] : 0;
-    ov[dst] = ok ? tv[warp][kk][lane] : 0.0;
+    if (ov) ov[dst] = ok ? tv[warp][kk][lane] : 0.0;
   }
 }
 
@@ -84,120 +84,6 @@ __global__ void sell_rows_kernel(const SellSlice* __restrict__ slices,
   }
   row[q] = r;
   len[q] = l;
-}
-
-// L2 prefetch of the slice's interleaved entries [k, k + B) (one bulk request
-// per array, issued by one lane): the column / value loads of a later batch
-// then wait on L2 instead of DRAM, without holding registers.
-template <int B>
-__device__ __forceinline__ void prefetch_batch(const int32_t* cbase, const double* vbase, int k) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cbase + 32 * k),
-               "r"(B * 32 * 4) : "memory");
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vbase + 32 * k),
-               "r"(B * 32 * 8) : "memory");
-}
-
-// One warp per slice.  B entries per lane per batch: B column loads and B
-// value loads, then B gathers, then B dependent adds.  PIPE: the next batch's
-// column / value loads are issued before this batch's gathers (one batch of
-// CSR stream in flight behind the gathers).  PF > 0: lane 0 keeps the slice's
-// stream PF batches ahead in L2 (the batch loop is then the critical path of
-// the slice's longest row: an L2 load and a gather per batch).
-template <int B, bool PIPE, int MINB, int PF = 0>
-__global__ void __launch_bounds__(128, MINB) sgd_sell_kernel(const SgdIterArgs a,
-                                                             const SellArgs sa) {
-  const int lane = threadIdx.x & 31;
-  const int w = sa.first + blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (w >= sa.nslices) return;
-  const SellSlice sd = sa.slices[w];
-  const int mat = sd.mat;
-  const int q = 32 * w + lane;
-  const int len = __ldg(sa.len + q);
-  const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
-  const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
-  const double* __restrict__ x = mat ? a.xw_cur : a.xs_cur;
-  double acc = 0.0;
-  int k = 0;
-  const int maxlen = sd.maxlen;
-  const int32_t* cb = sa.ci[mat] + sd.off;
-  const double* vb = sa.va[mat] + sd.off;
-  if constexpr (PF > 0) {
-    if (lane == 0)
-      for (int j = 0; j < PF && j * B < maxlen; ++j) prefetch_batch<B>(cb, vb, j * B);
-  }
-  if constexpr (!PIPE) {
-    for (; k + B <= len; k += B) {
-      if constexpr (PF > 0) {
-        if (lane == 0 && k + PF * B < maxlen) prefetch_batch<B>(cb, vb, k + PF * B);
-      }
-      int32_t c[B];
-      double v[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * (k + b));
-#pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * (k + b));
-      double g[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) g[b] = __ldg(x + c[b]);
-#pragma unroll
-      for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
-    }
-  } else {
-    if (k + B <= len) {
-      int32_t c[B];
-      double v[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * b);
-#pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * b);
-      for (;;) {
-        const int kn = k + B;
-        const bool more = kn + B <= len;
-        int32_t cn[B];
-        double vn[B];
-        if (more) {
-#pragma unroll
-          for (int b = 0; b < B; ++b) cn[b] = ld_na(cp + 32 * (kn + b));
-#pragma unroll
-          for (int b = 0; b < B; ++b) vn[b] = ld_na(vp + 32 * (kn + b));
-        }
-        double g[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) g[b] = __ldg(x + c[b]);
-#pragma unroll
-        for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
-        k = kn;
-        if (!more) break;
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          c[b] = cn[b];
-          v[b] = vn[b];
-        }
-      }
-    }
-  }
-  if (k < len) {  // tail: fewer than B entries left
-    int32_t c[B];
-    double v[B], g[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (k + b < len) {
-        c[b] = ld_na(cp + 32 * (k + b));
-        v[b] = ld_na(vp + 32 * (k + b));
-      }
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (k + b < len) g[b] = __ldg(x + c[b]);
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (k + b < len) acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
-  }
-  unsigned fl = 0;
-  if (lane < sd.cnt) sgd_epilogue(a, mat, __ldg(sa.row + q), acc, fl);
-  // peer stores performed system-wide before the kernel completes (the
-  // barrier that follows orders every peer's next reads after them)
-  if (a.npeer) __threadfence_system();
-  if (fl) atomicOr(a.flags, fl);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -222,6 +108,136 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
   } while (!done);
 }
 
+// What a traversal does with its row sums.  NV gathered vectors per entry (2:
+// LSQR's fused residual + next B v pass, one value / column stream, two
+// sequential sums per row).
+struct SgdOp {  // the fused u / v update of one SGD iteration
+  static constexpr int NV = 1;
+  SgdIterArgs a;
+  __device__ bool skip() const { return false; }
+  __device__ const double* x(int mat) const { return mat ? a.xw_cur : a.xs_cur; }
+  __device__ const double* x2(int) const { return nullptr; }
+  __device__ void finish(int mat, int32_t r, double acc, double, unsigned& fl) const {
+    sgd_epilogue(a, mat, r, acc, fl);
+  }
+  __device__ void end(unsigned fl) const {
+    // peer stores performed system-wide before the kernel completes (the
+    // barrier that follows orders every peer's next reads after them)
+    if (a.npeer) __threadfence_system();
+    if (fl) atomicOr(a.flags, fl);
+  }
+};
+template <int NV_>
+struct PassOp {  // generic passes (pass_epilogue); one matrix per launch
+  static constexpr int NV = NV_;
+  PassArgs p, q;
+  __device__ bool skip() const { return p.skip && *p.skip; }
+  __device__ const double* x(int) const { return p.xg; }
+  __device__ const double* x2(int) const { return q.xg; }
+  __device__ void finish(int, int32_t r, double acc, double acc2, unsigned&) const {
+    pass_epilogue(p, r, acc);
+    if constexpr (NV == 2) pass_epilogue(q, r, acc2);
+  }
+  __device__ void end(unsigned) const {}
+};
+
+__device__ __forceinline__ int slice_at(const SellArgs& sa, int i) {
+  return sa.order ? __ldg(sa.order + i) : i;
+}
+
+// One warp per slice (rows <= kTileNnz).  B entries per lane per batch: B
+// column loads and B value loads, then the gathers, then the dependent adds.
+// PIPE: the next batch's column / value loads are issued before this batch's
+// gathers (one batch of CSR stream in flight behind the gathers).
+template <class Op, int B, bool PIPE, int MINB>
+__global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const SellArgs sa) {
+  constexpr int NV = Op::NV;
+  if (op.skip()) return;
+  const int lane = threadIdx.x & 31;
+  const int i = sa.first + blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (i >= sa.nslices) return;
+  const int w = slice_at(sa, i);
+  const SellSlice sd = sa.slices[w];
+  const int mat = sd.mat;
+  const int q = 32 * w + lane;
+  const int len = __ldg(sa.len + q);
+  const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
+  const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
+  const double* __restrict__ x = op.x(mat);
+  const double* __restrict__ x2 = op.x2(mat);
+  double acc = 0.0, acc2 = 0.0;
+  auto consume = [&](const int32_t* c, const double* v, int k0, bool full) {
+    double g[B], g2[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (full || k0 + b < len) {
+        g[b] = __ldg(x + c[b]);
+        if constexpr (NV == 2) g2[b] = __ldg(x2 + c[b]);
+      }
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (full || k0 + b < len) {
+        acc = __dadd_rn(acc, __dmul_rn(v[b], g[b]));
+        if constexpr (NV == 2) acc2 = __dadd_rn(acc2, __dmul_rn(v[b], g2[b]));
+      }
+  };
+  int k = 0;
+  if constexpr (!PIPE) {
+    for (; k + B <= len; k += B) {
+      int32_t c[B];
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * (k + b));
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * (k + b));
+      consume(c, v, k, true);
+    }
+  } else {
+    if (k + B <= len) {
+      int32_t c[B];
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * b);
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * b);
+      for (;;) {
+        const int kn = k + B;
+        const bool more = kn + B <= len;
+        int32_t cn[B];
+        double vn[B];
+        if (more) {
+#pragma unroll
+          for (int b = 0; b < B; ++b) cn[b] = ld_na(cp + 32 * (kn + b));
+#pragma unroll
+          for (int b = 0; b < B; ++b) vn[b] = ld_na(vp + 32 * (kn + b));
+        }
+        consume(c, v, k, true);
+        k = kn;
+        if (!more) break;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          c[b] = cn[b];
+          v[b] = vn[b];
+        }
+      }
+    }
+  }
+  if (k < len) {  // tail: fewer than B entries left
+    int32_t c[B];
+    double v[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (k + b < len) {
+        c[b] = ld_na(cp + 32 * (k + b));
+        v[b] = ld_na(vp + 32 * (k + b));
+      }
+    consume(c, v, k, false);
+  }
+  unsigned fl = 0;
+  if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl);
+  op.end(fl);
+}
+
 // Long slices (rows longer than kTileNnz): one CTA per slice, warp-specialised.
 // A lane-per-row chain that waits on its own loads would make the slice's
 // longest row (10^4 entries on c3) the critical path of the whole launch, so
@@ -233,20 +249,23 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // lanes arrive).  PIPE: a stager issues its next round's loads before this
 // round's gathers.  Products are formed in any order; the adds are the
 // reference's CSR-order chain.
-template <int B, int S, bool PIPE, int MINB>
+template <class Op, int B, int S, bool PIPE, int MINB>
 __global__ void __launch_bounds__(32 * (S + 1), MINB)
-sgd_sell_long_kernel(const SgdIterArgs a, const SellArgs sa) {
+sell_long_kernel(const Op op, const SellArgs sa) {
+  constexpr int NV = Op::NV;
   constexpr int R = S + 1;
-  __shared__ __align__(16) double buf[R][B * 32];
+  __shared__ __align__(16) double buf[NV][R][B * 32];
   __shared__ __align__(8) unsigned long long full[R], empty[R];
+  if (op.skip()) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = sa.first + blockIdx.x;
+  const int i = sa.first + blockIdx.x;
   if (threadIdx.x < R) {
     mbar_init(&full[threadIdx.x], 32);
     mbar_init(&empty[threadIdx.x], 32);
   }
   __syncthreads();
-  if (w >= sa.nslices) return;
+  if (i >= sa.nslices) return;
+  const int w = slice_at(sa, i);
   const SellSlice sd = sa.slices[w];
   const int mat = sd.mat;
   const int q = 32 * w + lane;
@@ -255,7 +274,8 @@ sgd_sell_long_kernel(const SgdIterArgs a, const SellArgs sa) {
   if (warp > 0) {
     const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
     const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
-    const double* __restrict__ x = mat ? a.xw_cur : a.xs_cur;
+    const double* __restrict__ x = op.x(mat);
+    const double* __restrict__ x2 = op.x2(mat);
     int r = warp - 1;
     int32_t c[B];
     double v[B];
@@ -278,15 +298,21 @@ sgd_sell_long_kernel(const SgdIterArgs a, const SellArgs sa) {
       } else {
         load(r, c, v);
       }
-      double g[B];
+      double g[B], g2[B];
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (k0 + b < len) g[b] = __ldg(x + c[b]);
+        if (k0 + b < len) {
+          g[b] = __ldg(x + c[b]);
+          if constexpr (NV == 2) g2[b] = __ldg(x2 + c[b]);
+        }
       const int bi = r % R;
       if (r >= R) mbar_wait(&empty[bi], ((r / R) - 1) & 1);
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (k0 + b < len) buf[bi][32 * b + lane] = __dmul_rn(v[b], g[b]);
+        if (k0 + b < len) {
+          buf[0][bi][32 * b + lane] = __dmul_rn(v[b], g[b]);
+          if constexpr (NV == 2) buf[NV - 1][bi][32 * b + lane] = __dmul_rn(v[b], g2[b]);
+        }
       mbar_arrive(&full[bi]);
       if constexpr (PIPE) {
 #pragma unroll
@@ -298,32 +324,34 @@ sgd_sell_long_kernel(const SgdIterArgs a, const SellArgs sa) {
     }
     return;
   }
-  double acc = 0.0;
+  double acc = 0.0, acc2 = 0.0;
   for (int r = 0; r < rounds; ++r) {
     const int bi = r % R;
     mbar_wait(&full[bi], (r / R) & 1);
     const int k0 = r * B;
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (k0 + b < len) acc = __dadd_rn(acc, buf[bi][32 * b + lane]);
+      if (k0 + b < len) {
+        acc = __dadd_rn(acc, buf[0][bi][32 * b + lane]);
+        if constexpr (NV == 2) acc2 = __dadd_rn(acc2, buf[NV - 1][bi][32 * b + lane]);
+      }
     mbar_arrive(&empty[bi]);
   }
   unsigned fl = 0;
-  if (lane < sd.cnt) sgd_epilogue(a, mat, __ldg(sa.row + q), acc, fl);
-  if (a.npeer) __threadfence_system();
-  if (fl) atomicOr(a.flags, fl);
+  if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl);
+  op.end(fl);
 }
 
-template <int B, int S, bool PIPE, int MINB>
-void launch_long_variant(const SgdIterArgs& a, const SellArgs& sa, cudaStream_t s) {
-  sgd_sell_long_kernel<B, S, PIPE, MINB>
-      <<<static_cast<unsigned>(sa.nslices - sa.first), 32 * (S + 1), 0, s>>>(a, sa);
+template <class Op, int B, int S, bool PIPE, int MINB>
+void launch_long(const Op& op, const SellArgs& sa, cudaStream_t s) {
+  sell_long_kernel<Op, B, S, PIPE, MINB>
+      <<<static_cast<unsigned>(sa.nslices - sa.first), 32 * (S + 1), 0, s>>>(op, sa);
 }
 
-template <int B, bool PIPE, int MINB, int PF = 0>
-void launch_variant(const SgdIterArgs& a, const SellArgs& sa, cudaStream_t s) {
+template <class Op, int B, bool PIPE, int MINB>
+void launch_warp(const Op& op, const SellArgs& sa, cudaStream_t s) {
   const unsigned g = static_cast<unsigned>((sa.nslices - sa.first + 3) / 4);
-  sgd_sell_kernel<B, PIPE, MINB, PF><<<g, 128, 0, s>>>(a, sa);
+  sell_warp_kernel<Op, B, PIPE, MINB><<<g, 128, 0, s>>>(op, sa);
 }
 
 }  // namespace
@@ -359,12 +387,13 @@ cudaError_t launch_sell_rows(const SellSlice* slices, const int32_t* r0, int nsl
 cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int variant,
                                  cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
+  const SgdOp op{a};
   switch (variant) {  // EQUIL_SELL_LVARIANT (A/B knob); 0 = measured best on c3
-    case 1: launch_long_variant<8, 7, true, 2>(a, sa, s); break;
-    case 2: launch_long_variant<4, 7, true, 3>(a, sa, s); break;
-    case 3: launch_long_variant<2, 15, true, 2>(a, sa, s); break;
-    case 4: launch_long_variant<8, 7, false, 2>(a, sa, s); break;
-    default: launch_long_variant<4, 15, true, 1>(a, sa, s); break;
+    case 1: launch_long<SgdOp, 8, 7, true, 2>(op, sa, s); break;
+    case 2: launch_long<SgdOp, 4, 7, true, 3>(op, sa, s); break;
+    case 3: launch_long<SgdOp, 2, 15, true, 2>(op, sa, s); break;
+    case 4: launch_long<SgdOp, 8, 7, false, 2>(op, sa, s); break;
+    default: launch_long<SgdOp, 4, 15, true, 1>(op, sa, s); break;
   }
   count_launch(s);
   return cudaGetLastError();
@@ -373,13 +402,29 @@ cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int v
 cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,
                             cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
+  const SgdOp op{a};
   switch (variant) {  // EQUIL_SELL_VARIANT (A/B knob); 0 = measured best on c3
-    case 1: launch_variant<4, false, 12>(a, sa, s); break;
-    case 2: launch_variant<8, false, 8>(a, sa, s); break;
-    case 3: launch_variant<16, false, 6>(a, sa, s); break;
-    case 4: launch_variant<8, true, 8>(a, sa, s); break;
-    case 5: launch_variant<16, false, 6, 2>(a, sa, s); break;
-    default: launch_variant<8, true, 6>(a, sa, s); break;
+    case 1: launch_warp<SgdOp, 4, false, 12>(op, sa, s); break;
+    case 2: launch_warp<SgdOp, 8, false, 8>(op, sa, s); break;
+    case 3: launch_warp<SgdOp, 16, false, 6>(op, sa, s); break;
+    case 4: launch_warp<SgdOp, 8, true, 8>(op, sa, s); break;
+    default: launch_warp<SgdOp, 8, true, 6>(op, sa, s); break;
+  }
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArgs& sa, bool lng,
+                             cudaStream_t s) {
+  if (sa.nslices <= sa.first) return cudaSuccess;
+  if (b) {
+    const PassOp<2> op{a, *b};
+    if (lng) launch_long<PassOp<2>, 4, 15, true, 1>(op, sa, s);
+    else launch_warp<PassOp<2>, 4, true, 6>(op, sa, s);
+  } else {
+    const PassOp<1> op{a, a};
+    if (lng) launch_long<PassOp<1>, 4, 15, true, 1>(op, sa, s);
+    else launch_warp<PassOp<1>, 8, true, 6>(op, sa, s);
   }
   count_launch(s);
   return cudaGetLastError();

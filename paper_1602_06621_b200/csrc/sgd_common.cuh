@@ -81,6 +81,33 @@ __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
     for (int g = 0; g < a.npeer; ++g) dst[a.peer_delta[g]] = val;  // peers' copies
   }
 }
+// epilogues of the generic passes (LSQR, variants, apply)
+__device__ __forceinline__ void pass_epilogue(const PassArgs& a, int64_t r,
+                                              double acc) {
+  switch (a.mode) {
+    case kPassPlain:
+      a.out[r] = acc;
+      break;
+    case kPassLsqrU:
+    case kPassLsqrV: {  // B.apply(v) - alpha*u  (lsqr.cpp:39, :49)
+      const double bv = a.scale ? __dmul_rn(a.scale[r], acc) : acc;
+      a.out[r] = __dsub_rn(bv, __dmul_rn(*a.coef, a.prev[r]));
+      break;
+    }
+    case kPassResid:  // b - A x  (lsqr.cpp:97, :131)
+      a.out[r] = __dsub_rn(a.prev[r], acc);
+      break;
+    case kPassScaled:
+      a.out[r] = a.scale ? __dmul_rn(a.scale[r], acc) : acc;
+      break;
+    case kPassEst: {  // estimate_row_norms_sq: y = s_i * acc, y * y (estimator.cpp:5-9)
+      const double y = __dmul_rn(a.scale[r], acc);
+      a.out[r] = __dmul_rn(y, y);
+      break;
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t ld_na(const uint32_t* p) {
   uint32_t v;
   asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
