@@ -777,3 +777,51 @@ def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, 
         assert np.array_equal(lp.x, ref_l.x)
         assert np.array_equal(pp.residual_history, ref_p.residual_history)
         assert np.array_equal(pp.x, ref_p.x)
+
+
+TRAVERSALS = [
+    {},                                                    # interleaved slices (default)
+    {"EQUIL_SELL_LONG": "1"},                              # long rows as lane chains
+    {"EQUIL_SELL_LONG": "0"},                              # long rows on the staged CTAs
+    {"EQUIL_SELL": "0"},                                   # staged traversal throughout
+    {"EQUIL_SELL_PASSES": "0"},                            # generic passes staged
+    {"EQUIL_SELL_VARIANT": "1", "EQUIL_SELL_LVARIANT": "3"},
+    {"EQUIL_SELL_VARIANT": "3", "EQUIL_SELL_LVARIANT": "4"},
+]
+
+
+@pytest.mark.parametrize("env", TRAVERSALS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items())
+                         or "default")
+def test_traversals_bit_exact_on_boundary_row_lengths(C, monkeypatch, env):
+    """Every SGD traversal and pass (sell.cu warp slices / warp-specialised
+    long slices, their variants, the staged kernels) against the oracle on
+    rows whose lengths sit on the boundaries of batches, rounds, the 512-entry
+    long-row threshold and partial slices, plus empty rows inside long slices."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(5)
+    n = 6000
+    lens = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 511, 512, 513, 514,
+            515, 1000, 1023, 4099, 5999, 6000]
+    lens = lens * 3 + list(rng.integers(0, 40, 250)) + [0] * 20
+    rng.shuffle(lens)
+    m = len(lens)
+    cols = [np.sort(rng.choice(n, size=int(L), replace=False)) for L in lens]
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = np.concatenate(cols).astype(np.int32)
+    val = rng.standard_normal(int(rp[-1])) * np.exp(rng.standard_normal(int(rp[-1])))
+    A = oracle.CsrArrays(m, n, rp, col, val)
+    M = device_matrix(A)
+    w = C.sgd_equilibrate(A, iterations=12, seed=3)
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=12, seed=3))
+    for k in "uvde":
+        assert np.array_equal(getattr(r, k), getattr(w, k)), k
+    b = rng.standard_normal(m)
+    run = eq.lsqr(M, b, 8, 0.0)
+    ref = C.lsqr(A, b, 8, 0.0)
+    assert np.array_equal(np.array(run.residual_history), ref.residual_history)
+    assert np.array_equal(run.x, ref.x)
+    pre = eq.lsqr_preconditioned(M, b, eq.EquilibrationParams(iterations=6, seed=4), 8, 0.0)
+    pref = C.lsqr_preconditioned(A, b, 8, 0.0, iterations=6, seed=4)
+    assert np.array_equal(np.array(pre.residual_history), pref.residual_history)
+    assert np.array_equal(pre.x, pref.x)
