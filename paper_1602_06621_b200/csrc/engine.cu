@@ -171,6 +171,12 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   CK(cudaEventCreateWithFlags(&M->ev_vals, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&M->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&M->ev_join, cudaEventDisableTiming));
+  {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&M->sign_stream, cudaStreamNonBlocking, hi));
+    for (cudaEvent_t& e : M->sign_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   {  // keep stream-ordered scratch (transpose, reductions) cached across calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, M->device) == cudaSuccess) {
@@ -1210,13 +1216,21 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     };
     const eqb::SgdBlockConst cu = block_const(lin_u), cv = block_const(lin_v);
 
+    PhaseTimer pt("sgd");
+    std::vector<std::pair<uint64_t, int>> sign_ready;
     // K1: all T*(n+m) signs up front (never depends on the iterate)
     if (total > 0) {
       M->signs.ensure((total + 31) / 32 + 1);
       const size_t sb = eqb::sign_stream_scratch_bytes(total);
       M->sign_scratch.ensure(sb);
-      CK(eqb::sign_stream_generate(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb, s));
+      // the first two iterations' signs on s, the rest on the side stream
+      // while the loop runs (one_iter waits where it needs them)
+      CK(eqb::sign_stream_generate_staged(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb,
+                                          s, std::min<uint64_t>(total, 2 * per_iter),
+                                          M->sign_stream, M->sign_ev, equil_matrix::kSignEvents,
+                                          &sign_ready));
     }
+    pt.mark(s, "signs");
     // init: u = v = 0, ubar = vbar = 0, xs = s_1, xw = w_1
     CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
     const int64_t a_poff = M->world == 1 ? M->a_goff() : M->rank * M->a_max;
@@ -1433,7 +1447,20 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       a.colpart = M->colpart.p;
       return a;
     };
+    // iteration t's epilogue writes iteration t+1's probes: outputs up to
+    // (t + 1)(m + n) must be ready (staged sign generation)
+    size_t sign_li = 0;
+    bool capturing = false;
+    auto await_signs = [&](int t) {
+      if (t >= T || sign_ready.empty()) return;
+      const uint64_t need = std::min<uint64_t>(total, static_cast<uint64_t>(t + 1) * per_iter);
+      if (sign_ready[sign_li].first >= need) return;
+      while (sign_ready[sign_li].first < need) ++sign_li;
+      CK(cudaStreamWaitEvent(s, M->sign_ev[sign_ready[sign_li].second],
+                             capturing ? cudaEventWaitExternal : cudaEventWaitDefault));
+    };
     auto one_iter = [&](int t) {
+      await_signs(t);
       if (M->dense) {
         static const int dconc = getenv("EQUIL_CONC") ? atoi(getenv("EQUIL_CONC")) : 1;
         if (dconc)
@@ -1517,6 +1544,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
         }
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
         try {
           // external event-record nodes: the graph itself timestamps the loop
           CK(cudaEventRecordWithFlags(M->ev_loop0, s, cudaEventRecordExternal));
@@ -1527,6 +1555,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
           throw;
         }
         CK(cudaStreamEndCapture(s, &g));
+        capturing = false;
         {  // kernel nodes of one replay, for the launch accounting
           size_t nn = 0;
           CK(cudaGraphGetNodes(g, nullptr, &nn));
@@ -1554,6 +1583,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       CK(cudaEventRecord(M->ev_loop1, s));
     }
     M->last_loop_iters = T;
+    pt.mark(s, "loop");
 
     // finalize: u = ubar, v = vbar, d = exp(ubar), e = exp(vbar) (:201-204)
     double* dloc = M->tmp_m.p;
@@ -1623,6 +1653,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     if (nrec)
       CK(cudaMemcpyAsync(hh.data(), hist.p, kRec * nrec * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    pt.mark(s, "finalize");
     M->last_loop_ms = 0.0;
     if (T > 0) {
       float ms = 0.f;
