@@ -175,7 +175,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&M->sign_stream, cudaStreamNonBlocking, hi));
-    for (cudaEvent_t& e : M->sign_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&M->sign_ev, cudaEventDisableTiming));
   }
   {  // keep stream-ordered scratch (transpose, reductions) cached across calls
     cudaMemPool_t pool;
@@ -909,9 +909,18 @@ equil_status equil_nccl_unique_id(void* out128) {
   });
 }
 
-equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_ptr,
-                                     const int32_t* col, const double* val,
-                                     const equil_device_cfg* cfg, equil_matrix** out) {
+}  // extern "C"
+
+namespace eqe {
+struct PreSigns {
+  uint64_t seed, total;
+};
+}  // namespace eqe
+
+static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr,
+                                    const int32_t* col, const double* val,
+                                    const equil_device_cfg* cfg, equil_matrix** out,
+                                    const eqe::PreSigns* pre) {
   return guarded([&] {
     NvtxRange nvtx_("equil:create_csr");
     require(out != nullptr, "ExplicitMatrix::sparse: null output handle");
@@ -935,6 +944,17 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     M->nnz = nnz;
     DeviceGuard dg(M->device);
     cudaStream_t s = M->stream;
+    if (pre && pre->total > 0) {  // overlaps the uploads and the transpose below
+      M->signs.ensure((pre->total + 31) / 32 + 1);
+      const size_t sb = eqb::sign_stream_scratch_bytes(pre->total);
+      M->sign_scratch.ensure(sb);
+      CK(eqb::sign_stream_generate(pre->seed, 17, pre->total, M->signs.p, M->sign_scratch.p, sb,
+                                   M->sign_stream));
+      CK(cudaEventRecord(M->sign_ev, M->sign_stream));
+      M->pre_signs = true;
+      M->pre_seed = pre->seed;
+      M->pre_total = pre->total;
+    }
     pt.mark(s, "setup");
     // full A on device (uploaded once; shards are sliced from it)
     DevBuf<int64_t> rp;
@@ -991,6 +1011,14 @@ equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_pt
     finish_sparse(M.get(), rp, ci, va, row_ptr, pt, &planA, &planner);
     *out = M.release();
   });
+}
+
+extern "C" {
+
+equil_status equil_matrix_create_csr(int64_t m, int64_t n, const int64_t* row_ptr,
+                                     const int32_t* col, const double* val,
+                                     const equil_device_cfg* cfg, equil_matrix** out) {
+  return create_csr_impl(m, n, row_ptr, col, val, cfg, out, nullptr);
 }
 
 }  // extern "C"
@@ -1217,18 +1245,16 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     const eqb::SgdBlockConst cu = block_const(lin_u), cv = block_const(lin_v);
 
     PhaseTimer pt("sgd");
-    std::vector<std::pair<uint64_t, int>> sign_ready;
-    // K1: all T*(n+m) signs up front (never depends on the iterate)
-    if (total > 0) {
+    // K1: all T*(n+m) signs up front (never depends on the iterate); a
+    // one-shot call generated them during the matrix setup
+    if (total > 0 && M->pre_signs && M->pre_seed == p->seed && M->pre_total == total) {
+      CK(cudaStreamWaitEvent(s, M->sign_ev, 0));
+      M->pre_signs = false;
+    } else if (total > 0) {
       M->signs.ensure((total + 31) / 32 + 1);
       const size_t sb = eqb::sign_stream_scratch_bytes(total);
       M->sign_scratch.ensure(sb);
-      // the first two iterations' signs on s, the rest on the side stream
-      // while the loop runs (one_iter waits where it needs them)
-      CK(eqb::sign_stream_generate_staged(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb,
-                                          s, std::min<uint64_t>(total, 2 * per_iter),
-                                          M->sign_stream, M->sign_ev, equil_matrix::kSignEvents,
-                                          &sign_ready));
+      CK(eqb::sign_stream_generate(p->seed, 17, total, M->signs.p, M->sign_scratch.p, sb, s));
     }
     pt.mark(s, "signs");
     // init: u = v = 0, ubar = vbar = 0, xs = s_1, xw = w_1
@@ -1447,20 +1473,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       a.colpart = M->colpart.p;
       return a;
     };
-    // iteration t's epilogue writes iteration t+1's probes: outputs up to
-    // (t + 1)(m + n) must be ready (staged sign generation)
-    size_t sign_li = 0;
-    bool capturing = false;
-    auto await_signs = [&](int t) {
-      if (t >= T || sign_ready.empty()) return;
-      const uint64_t need = std::min<uint64_t>(total, static_cast<uint64_t>(t + 1) * per_iter);
-      if (sign_ready[sign_li].first >= need) return;
-      while (sign_ready[sign_li].first < need) ++sign_li;
-      CK(cudaStreamWaitEvent(s, M->sign_ev[sign_ready[sign_li].second],
-                             capturing ? cudaEventWaitExternal : cudaEventWaitDefault));
-    };
     auto one_iter = [&](int t) {
-      await_signs(t);
       if (M->dense) {
         static const int dconc = getenv("EQUIL_CONC") ? atoi(getenv("EQUIL_CONC")) : 1;
         if (dconc)
@@ -1544,7 +1557,6 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
         }
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        capturing = true;
         try {
           // external event-record nodes: the graph itself timestamps the loop
           CK(cudaEventRecordWithFlags(M->ev_loop0, s, cudaEventRecordExternal));
@@ -1555,7 +1567,6 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
           throw;
         }
         CK(cudaStreamEndCapture(s, &g));
-        capturing = false;
         {  // kernel nodes of one replay, for the launch accounting
           size_t nn = 0;
           CK(cudaGraphGetNodes(g, nullptr, &nn));
@@ -2162,7 +2173,12 @@ equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_
                                        const equil_params* p, const equil_device_cfg* cfg,
                                        equil_scaling_out* out) {
   equil_matrix* M = nullptr;
-  equil_status rc = equil_matrix_create_csr(m, n, row_ptr, col, val, cfg, &M);
+  // the sign stream depends only on (seed, T, m + n): generate it while the
+  // matrix is built (invalid parameters are reported by the call below first)
+  eqe::PreSigns pre{0, 0};
+  if (p && equil_validate_params(p) == EQUIL_OK && m > 0 && n > 0)
+    pre = {p->seed, static_cast<uint64_t>(m + n) * static_cast<uint64_t>(p->iterations)};
+  equil_status rc = create_csr_impl(m, n, row_ptr, col, val, cfg, &M, &pre);
   if (rc != EQUIL_OK) return rc;
   M->oneshot = true;  // one call on this handle: launch the loop directly, no graph
   rc = equil_sgd_equilibrate(M, p, nullptr, out);

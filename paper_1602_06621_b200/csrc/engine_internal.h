@@ -346,11 +346,14 @@ struct equil_matrix {
   cudaStream_t copy_stream = nullptr;  // uploads that overlap work on `stream`
   cudaEvent_t ev_vals = nullptr;       // values of A on the device
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  // staged sign generation: the jump-tree levels past the first iterations run
-  // on a high-priority side stream while the SGD loop starts (sgd_row_col)
-  static constexpr int kSignEvents = 16;
+  // one-shot calls (equil_sgd_equilibrate_csr) know the seed and T before the
+  // matrix is built: the sign stream is generated on a high-priority side
+  // stream while the matrix uploads and transposes; sgd_row_col then only
+  // waits on sign_ev (pre_* describe what was generated)
   cudaStream_t sign_stream = nullptr;
-  cudaEvent_t sign_ev[kSignEvents] = {};
+  cudaEvent_t sign_ev = nullptr;
+  bool pre_signs = false;
+  uint64_t pre_seed = 0, pre_total = 0;
   std::mutex mu;
   ncclComm_t comm = nullptr;
   std::shared_ptr<eqe::HostExchange> hx;  // EQUIL_HOST_EXCHANGE=1 instead of comm
@@ -486,8 +489,7 @@ struct equil_matrix {
     if (ev_vals) cudaEventDestroy(ev_vals);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
-    for (cudaEvent_t e : sign_ev)
-      if (e) cudaEventDestroy(e);
+    if (sign_ev) cudaEventDestroy(sign_ev);
     if (sign_stream) cudaStreamDestroy(sign_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (stream) cudaStreamDestroy(stream);

@@ -319,15 +319,6 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
                                  uint32_t* bits, void* scratch,
                                  size_t scratch_bytes, cudaStream_t s);
 size_t sign_stream_scratch_bytes(uint64_t total);
-// Staged: the outputs [0, >= first_need) are produced on s; the rest on `side`
-// in jump-tree levels.  ready[0] = {outputs complete on s, -1}; ready[i > 0] =
-// {outputs complete once event events[ready[i].second] fires} (ascending).
-// events[0] forks the side stream; nev >= 2.  side == nullptr: all on s.
-cudaError_t sign_stream_generate_staged(uint64_t seed, uint64_t stream, uint64_t total,
-                                        uint32_t* bits, void* scratch, size_t scratch_bytes,
-                                        cudaStream_t s, uint64_t first_need,
-                                        cudaStream_t side, cudaEvent_t* events, int nev,
-                                        std::vector<std::pair<uint64_t, int>>* ready);
 
 // dense
 struct DenseIterArgs {

@@ -119,11 +119,11 @@ mt_jump_kernel(uint64_t* __restrict__ windows, int src0, int dst0,
 // One CTA per segment: outputs [g*L, min((g+1)*L, total)) -> sign bits.
 __global__ void __launch_bounds__(kMtThreads)
 mt_gen_kernel(const uint64_t* __restrict__ windows, uint64_t seg_len,
-              uint64_t total, uint32_t* __restrict__ bits, uint64_t g0) {
+              uint64_t total, uint32_t* __restrict__ bits) {
   __shared__ uint64_t ring[2 * mt::kN];
   __shared__ uint8_t sbit[kPackOutputs];
   const int tid = threadIdx.x;
-  const uint64_t g = g0 + blockIdx.x;
+  const uint64_t g = blockIdx.x;
   const uint64_t start = g * seg_len;
   const uint64_t len = min(seg_len, total - start);
   for (int j = tid; j < mt::kN; j += blockDim.x)
@@ -211,15 +211,6 @@ size_t sign_stream_scratch_bytes(uint64_t total) {
 cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
                                  uint32_t* bits, void* scratch,
                                  size_t scratch_bytes, cudaStream_t s) {
-  return sign_stream_generate_staged(seed, stream, total, bits, scratch, scratch_bytes, s,
-                                     total, nullptr, nullptr, 0, nullptr);
-}
-
-cudaError_t sign_stream_generate_staged(uint64_t seed, uint64_t stream, uint64_t total,
-                                        uint32_t* bits, void* scratch, size_t scratch_bytes,
-                                        cudaStream_t s, uint64_t first_need,
-                                        cudaStream_t side, cudaEvent_t* events, int nev,
-                                        std::vector<std::pair<uint64_t, int>>* ready) {
   if (total == 0) return cudaSuccess;
   if (scratch_bytes < sign_stream_scratch_bytes(total)) return cudaErrorInvalidValue;
   const int k = choose_seg_log2(total);
@@ -256,18 +247,7 @@ cudaError_t sign_stream_generate_staged(uint64_t seed, uint64_t stream, uint64_t
                                      static_cast<int>(smem)));
     attr = true;
   }
-  // Level a of the jump tree makes segment starts [2^a, 2^(a+1)) from [0, 2^a).
-  // Staged: the levels whose segments cover the first `first_need` outputs
-  // (and their generation) run on s; the remaining levels run on `side`, each
-  // followed by the generation of its segments and an event, so the caller's
-  // work on s can start on the first outputs while the rest is produced.
-  int a0 = levels;  // levels [0, a0) on s
-  if (side && events && nev > 0) {
-    a0 = 0;
-    while (a0 < levels && (1ULL << a0) * L < first_need) ++a0;
-    a0 = std::max(a0, levels - (nev - 1));  // events[1..nev): one per side level
-  }
-  for (int a = 0; a < a0; ++a) {
+  for (int a = 0; a < levels; ++a) {
     const uint64_t lo = 1ULL << a;
     const uint64_t cnt = std::min(lo, G - lo);
     mt_jump_kernel<<<static_cast<unsigned>(cnt), kMtThreads, smem, s>>>(
@@ -276,33 +256,8 @@ cudaError_t sign_stream_generate_staged(uint64_t seed, uint64_t stream, uint64_t
     count_launch(s);
     EQ_CUDA_TRY(cudaGetLastError());
   }
-  const uint64_t g_main = std::min<uint64_t>(G, 1ULL << a0);  // segments ready on s
-  if (a0 < levels) {  // fork the side stream off s before generating on s
-    EQ_CUDA_TRY(cudaEventRecord(events[0], s));
-    EQ_CUDA_TRY(cudaStreamWaitEvent(side, events[0], 0));
-  }
-  mt_gen_kernel<<<static_cast<unsigned>(g_main), kMtThreads, 0, s>>>(windows, L, total, bits, 0);
-  count_launch(s);
-  EQ_CUDA_TRY(cudaGetLastError());
-  if (ready) {
-    ready->clear();
-    ready->push_back({std::min(total, g_main * L), -1});  // on s
-  }
-  for (int a = a0; a < levels; ++a) {
-    const uint64_t lo = 1ULL << a;
-    const uint64_t cnt = std::min(lo, G - lo);
-    mt_jump_kernel<<<static_cast<unsigned>(cnt), kMtThreads, smem, side>>>(
-        windows, 0, static_cast<int>(lo),
-        reinterpret_cast<const uint4*>(pos + static_cast<size_t>(a) * kPosCap), npos8[a]);
-    count_launch(side);
-    mt_gen_kernel<<<static_cast<unsigned>(cnt), kMtThreads, 0, side>>>(windows, L, total, bits,
-                                                                       lo);
-    count_launch(side);
-    EQ_CUDA_TRY(cudaGetLastError());
-    const int ev = a - a0 + 1;
-    EQ_CUDA_TRY(cudaEventRecord(events[ev], side));
-    if (ready) ready->push_back({std::min(total, (lo + cnt) * L), ev});
-  }
+  mt_gen_kernel<<<static_cast<unsigned>(G), kMtThreads, 0, s>>>(windows, L, total,
+                                                                bits); count_launch(s);
   return cudaGetLastError();
 }
 

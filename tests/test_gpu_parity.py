@@ -825,3 +825,21 @@ def test_traversals_bit_exact_on_boundary_row_lengths(C, monkeypatch, env):
     pref = C.lsqr_preconditioned(A, b, 8, 0.0, iterations=6, seed=4)
     assert np.array_equal(np.array(pre.residual_history), pref.residual_history)
     assert np.array_equal(pre.x, pref.x)
+
+
+def test_one_shot_entry_bit_exact_vs_oracle(C):
+    """equil_sgd_equilibrate_csr generates the sign stream while the matrix is
+    built (seed and T are known up front): same trajectory as the oracle, and
+    invalid parameters still fail with the reference's message."""
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(1)
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    for seed, T in [(0, 50), (9, 7), (3, 0)]:
+        p = eq.EquilibrationParams(alpha=inst.alpha, beta=inst.beta, iterations=T, seed=seed)
+        got = eq.sgd_equilibrate_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val, p)
+        want = C.sgd_equilibrate(A, alpha=inst.alpha, beta=inst.beta, iterations=T, seed=seed)
+        for k in "uvde":
+            assert np.array_equal(getattr(got, k), getattr(want, k)), (seed, T, k)
+    with pytest.raises(ValueError, match="gamma must be positive"):
+        eq.sgd_equilibrate_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val,
+                               eq.EquilibrationParams(gamma=0.0))

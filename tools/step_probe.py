@@ -14,7 +14,7 @@ inst = configs.config(3)
 M = eq.ExplicitMatrix.from_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
 p = eq.EquilibrationParams(alpha=inst.alpha, beta=inst.beta, iterations=100, seed=0)
 bufs = [torch.empty(k, dtype=torch.float64, device="cuda") for k in (inst.m, inst.n, inst.m, inst.n)]
-for k in range(4):
+for k in range(int(os.environ.get("STEPS", "4"))):
     t0 = time.perf_counter()
     eq.sgd_equilibrate_device(M, p, *[b.data_ptr() for b in bufs])
     t1 = time.perf_counter()
