@@ -97,11 +97,10 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
     return SellEnt{static_cast<int32_t>(mx), static_cast<int16_t>(t.r1),
                    static_cast<int16_t>(lng), t.r0};
   };
+  // (long groups first, longest first; then the warp slices in window order)
   P.sell.reserve(P.lng.size() / eqb::kTileWarps + P.slices.size());
   for (size_t q = 0; q < P.lng.size(); q += eqb::kTileWarps) P.sell.push_back(ent(P.lng[q], 1));
   for (const eqb::Tile& t : P.slices) P.sell.push_back(ent(t, 0));
-  std::stable_sort(P.sell.begin(), P.sell.end(),
-                   [](const SellEnt& a, const SellEnt& b) { return a.maxlen > b.maxlen; });
   return P;
 }
 
@@ -161,6 +160,8 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SELL_LONG")) M->sell_long = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_LVARIANT")) M->sell_lvariant = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_PASSES")) M->sell_passes = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_SELL_ORDER")) M->sell_order = atoi(e);
+  if (const char* e = getenv("EQUIL_SELL_BLOCKED")) M->sell_blocked = atoi(e) != 0;
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -218,25 +219,22 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
     const SellEnt* e;
     int mat;
   };
+  // Launch order: the long groups of both matrices longest first, then the
+  // warp slices -- longest first (EQUIL_SELL_ORDER=0, default; c3: 1.5% faster)
+  // or in window order (1: the epilogues' row accesses stay local, which
+  // matters once u, v and the gathered vectors outgrow L2, e.g. with blocks).
   std::vector<Src> order;
   order.reserve(pa.sell.size() + pt.sell.size());
-  {
-    size_t i = 0, j = 0;
-    auto skip = [&](const std::vector<SellEnt>& v, size_t& k) {
-      while (k < v.size() && v[k].lng && !M->sell_long) ++k;
-    };
-    skip(pa.sell, i);
-    skip(pt.sell, j);
-    while (i < pa.sell.size() || j < pt.sell.size()) {
-      if (j >= pt.sell.size() || (i < pa.sell.size() && pa.sell[i].maxlen >= pt.sell[j].maxlen)) {
-        order.push_back({&pa.sell[i++], 0});
-        skip(pa.sell, i);
-      } else {
-        order.push_back({&pt.sell[j++], 1});
-        skip(pt.sell, j);
-      }
-    }
-  }
+  for (int mat = 0; mat < 2; ++mat)
+    for (const SellEnt& e : mat ? pt.sell : pa.sell)
+      if (e.lng && M->sell_long) order.push_back({&e, mat});
+  const size_t nlong = order.size();
+  for (int mat = 0; mat < 2; ++mat)
+    for (const SellEnt& e : mat ? pt.sell : pa.sell)
+      if (!e.lng) order.push_back({&e, mat});
+  auto by_len = [](const Src& a, const Src& b) { return a.e->maxlen > b.e->maxlen; };
+  std::stable_sort(order.begin(), order.begin() + nlong, by_len);
+  if (M->sell_order == 0) std::stable_sort(order.begin() + nlong, order.end(), by_len);
   const size_t ns = order.size();
   H.slices.resize(ns);
   for (int mat = 0; mat < 2; ++mat) H.kbp[mat].assign(1, 0);
@@ -283,7 +281,7 @@ void ensure_sell_pass(equil_matrix* M) {
     const eqb::DevCsr& C = mat ? M->AT : M->A;
     CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, didx.p,
                        static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
-                       M->sell_len.p, M->sell_pci[mat].p, nullptr, s));
+                       M->sell_len.p, nullptr, M->sell_pci[mat].p, nullptr, s));
     CK(cudaStreamSynchronize(s));
   }
   M->sell_pass = true;
@@ -324,9 +322,86 @@ void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::Pass
 
 // Device arrays of the interleaved slices, columns mapped to slots on the way
 // (the slot layout must be built).
+// Column blocks (build_block_layout): the interleaved arrays are laid out
+// block-major -- block b holds, per slice, each lane's entries with columns in
+// block b, interleaved and padded to the slice's longest range -- so round b of
+// an iteration streams exactly the entries whose gathers fall in block b.
+// Columns stay in padded coordinates (blocks are column ranges).
+void build_sell_blocked(equil_matrix* M) {
+  const equil_matrix::SellHost& H = M->sell_host;
+  cudaStream_t s = M->stream;
+  const int ns = M->n_sell;
+  const int nbm = std::max(M->nblk[0], M->nblk[1]);
+  const int64_t nq = 32LL * ns;
+  DevBuf<int32_t> kst, maxb;
+  kst.alloc(nbm * nq);
+  maxb.alloc(static_cast<size_t>(nbm) * ns);
+  M->sell_bln.alloc(nbm * nq);
+  CK(eqb::launch_sell_block_lanes(M->sell_slices.p, ns, M->sell_row.p, M->sell_len.p,
+                                  M->A.row_ptr, M->A.col, M->AT.row_ptr, M->AT.col, M->nblk[0],
+                                  M->nblk[1], M->bwidth[0], M->bwidth[1], nbm, kst.p,
+                                  M->sell_bln.p, maxb.p, s));
+  std::vector<int32_t> hm(static_cast<size_t>(nbm) * ns);
+  CK(cudaMemcpyAsync(hm.data(), maxb.p, hm.size() * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<eqb::SellSlice> tab(static_cast<size_t>(nbm) * ns);
+  int64_t tot[2] = {0, 0};
+  std::vector<std::vector<int64_t>> kbp[2];
+  std::vector<std::vector<int32_t>> midx[2];
+  for (int mat = 0; mat < 2; ++mat) {
+    kbp[mat].resize(nbm);
+    midx[mat].resize(nbm);
+  }
+  for (int b = 0; b < nbm; ++b)
+    for (int w = 0; w < ns; ++w) {
+      const int mat = H.slices[w].mat;
+      eqb::SellSlice& e = tab[static_cast<size_t>(b) * ns + w];
+      e = {0, 0, 0, static_cast<int16_t>(mat)};
+      if (b >= M->nblk[mat]) continue;  // this matrix has fewer blocks
+      const int32_t ml = hm[static_cast<size_t>(b) * ns + w];
+      e = {tot[mat], ml, H.slices[w].cnt, static_cast<int16_t>(mat)};
+      tot[mat] += 32 * static_cast<int64_t>(ml);
+      if (kbp[mat][b].empty()) kbp[mat][b].push_back(0);
+      if (ml > 0) {
+        midx[mat][b].push_back(w);
+        kbp[mat][b].push_back(kbp[mat][b].back() + (ml + 31) / 32);
+      }
+    }
+  M->sell_bslices.alloc(tab.size());
+  CK(cudaMemcpyAsync(M->sell_bslices.p, tab.data(), tab.size() * sizeof(tab[0]),
+                     cudaMemcpyHostToDevice, s));
+  for (int mat = 0; mat < 2; ++mat) {
+    M->sell_ci[mat].alloc(tot[mat]);
+    M->sell_va[mat].alloc(tot[mat]);
+    const eqb::DevCsr& C = mat ? M->AT : M->A;
+    for (int b = 0; b < M->nblk[mat]; ++b) {
+      if (midx[mat][b].empty()) continue;
+      DevBuf<int64_t> dkbp;
+      DevBuf<int32_t> didx;
+      dkbp.alloc(kbp[mat][b].size());
+      didx.alloc(midx[mat][b].size());
+      CK(cudaMemcpyAsync(dkbp.p, kbp[mat][b].data(), kbp[mat][b].size() * 8,
+                         cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(didx.p, midx[mat][b].data(), midx[mat][b].size() * 4,
+                         cudaMemcpyHostToDevice, s));
+      CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, didx.p,
+                         static_cast<int>(midx[mat][b].size()),
+                         M->sell_bslices.p + static_cast<size_t>(b) * ns, M->sell_row.p,
+                         M->sell_bln.p + b * nq, kst.p + b * nq, M->sell_ci[mat].p,
+                         M->sell_va[mat].p, s));
+      CK(cudaStreamSynchronize(s));
+    }
+  }
+  M->sell_carry.alloc(nq);
+  M->sell_nb = nbm;
+}
+
 void build_sell_layout(equil_matrix* M) {
   M->sell = false;
-  if (!M->use_sell || !M->slots || M->use_panels || M->nblk[0] > 1 || M->nblk[1] > 1) return;
+  M->sell_nb = 1;
+  const bool blocked = M->nblk[0] > 1 || M->nblk[1] > 1;
+  if (!M->use_sell || M->use_panels || (!M->slots && !blocked)) return;
+  if (blocked && (!M->sell_blocked || M->sell_long == 0)) return;
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
   auto upload = [&](auto& d, const auto& h) {
@@ -349,7 +424,7 @@ void build_sell_layout(equil_matrix* M) {
   M->n_sell_long = 0;
   while (M->n_sell_long < M->n_sell && H.slices[M->n_sell_long].maxlen > eqb::kTileNnz)
     ++M->n_sell_long;
-  for (int mat = 0; mat < 2; ++mat) {
+  for (int mat = 0; mat < 2 && !blocked; ++mat) {
     M->sell_ci[mat].alloc(H.total[mat]);
     M->sell_va[mat].alloc(H.total[mat]);
     DevBuf<int64_t> dkbp;
@@ -360,9 +435,10 @@ void build_sell_layout(equil_matrix* M) {
     // columns of A index xs (slot map smap), columns of A^T index xw (wmap)
     CK(eqb::build_sell(C.row_ptr, C.col, mat ? M->wmap.p : M->smap.p, C.val, dkbp.p, didx.p,
                        static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
-                       M->sell_len.p, M->sell_ci[mat].p, M->sell_va[mat].p, s));
+                       M->sell_len.p, nullptr, M->sell_ci[mat].p, M->sell_va[mat].p, s));
     CK(cudaStreamSynchronize(s));  // before dkbp / didx go
   }
+  if (blocked) build_sell_blocked(M);
   if (M->sell_long || M->n_sgd_long == 0) {  // the staged kernel no longer runs
     M->a_ci_sgd.release();
     M->t_ci_sgd.release();
@@ -370,6 +446,7 @@ void build_sell_layout(equil_matrix* M) {
   M->sell = true;
   M->sell_pass = false;
   if (M->sell_long == 0) M->sell_passes = false;  // long rows are not in the slices
+  if (blocked) M->sell_passes = false;            // the passes' arrays are not blocked
 }
 
 void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
@@ -588,7 +665,7 @@ void build_block_layout(equil_matrix* M) {
   M->nblk[0] = M->nblk[1] = 1;
   if (M->use_panels) return;
   double mb = 60.0;
-  if (const char* e = getenv("EQUIL_BLOCK_MB")) mb = std::max(1.0, atof(e));
+  if (const char* e = getenv("EQUIL_BLOCK_MB")) mb = std::max(1e-6, atof(e));
   const int64_t lens[2] = {M->n_pad(), M->m_pad()};
   for (int mat = 0; mat < 2; ++mat) {
     const double bytes = static_cast<double>(lens[mat]) * 8.0;
@@ -1494,6 +1571,11 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
             sa.nslices = M->n_sell;
             sa.row = M->sell_row.p;
             sa.len = M->sell_len.p;
+            if (M->sell_nb > 1) {  // column block rd of every slice, sums carried per lane
+              sa.slices = M->sell_bslices.p + static_cast<size_t>(rd) * M->n_sell;
+              sa.len = M->sell_bln.p + static_cast<size_t>(rd) * 32 * M->n_sell;
+              a.carry[0] = a.carry[1] = M->sell_carry.p;
+            }
             for (int k = 0; k < 2; ++k) {
               sa.ci[k] = M->sell_ci[k].p;
               sa.va[k] = M->sell_va[k].p;

@@ -148,10 +148,19 @@ struct SellArgs {
 // Fill one matrix's interleaved arrays from its CSR rows, columns mapped
 // through map (slots; nullptr: unchanged).  midx: that matrix's slices (indices
 // into slices) in launch order; kbp: prefix of their 32-entry blocks.
+// kst (nullable): each lane's first entry within its row (column blocks).
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
                        const int64_t* kbp, const int32_t* midx, int nmat_slices,
                        const SellSlice* slices, const int32_t* row, const int32_t* len,
-                       int32_t* out_ci, double* out_va, cudaStream_t s);
+                       const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s);
+// column blocks: per block b and slice lane q, the lane's first entry and
+// entry count in block b (kst / bln[b * 32 nslices + q]) and the per-block
+// slice maxima maxb[b * nslices + w]
+cudaError_t launch_sell_block_lanes(const SellSlice* slices, int nslices, const int32_t* row,
+                                    const int32_t* len, const int64_t* rpa, const int32_t* cia,
+                                    const int64_t* rpt, const int32_t* cit, int nba, int nbt,
+                                    int64_t wa, int64_t wt, int nbmax, int32_t* kst, int32_t* bln,
+                                    int32_t* maxb, cudaStream_t s);
 // row[32 w + l] / len[32 w + l] of every slice lane from the plans' row lists
 // (slice w lists rows rowlist_{mat}[r0[w] ...]); empty lanes get 0 / 0
 cudaError_t launch_sell_rows(const SellSlice* slices, const int32_t* r0, int nslices,

@@ -29,8 +29,8 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
                   const int32_t* __restrict__ map, const double* __restrict__ val,
                   const int64_t* __restrict__ kbp, const int32_t* __restrict__ midx, int nms,
                   const SellSlice* __restrict__ slices, const int32_t* __restrict__ row,
-                  const int32_t* __restrict__ len, int32_t* __restrict__ oc,
-                  double* __restrict__ ov) {
+                  const int32_t* __restrict__ len, const int32_t* __restrict__ kst,
+                  int32_t* __restrict__ oc, double* __restrict__ ov) {
   __shared__ int32_t tc[2][32][33];
   __shared__ double tv[2][32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -45,7 +45,8 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
   const int k0 = static_cast<int>(item - kbp[lo]) * 32;
   const SellSlice sd = slices[w];
   const int mylen = len[32 * w + lane];
-  const int64_t mystart = lane < sd.cnt ? rp[row[32 * w + lane]] : 0;
+  const int64_t mystart =
+      lane < sd.cnt ? rp[row[32 * w + lane]] + (kst ? kst[32 * w + lane] : 0) : 0;
   for (int r = 0; r < sd.cnt; ++r) {
     const int64_t st = __shfl_sync(0xffffffffu, mystart, r);
     const int ln = __shfl_sync(0xffffffffu, mylen, r);
@@ -63,6 +64,57 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
     const bool ok = lane < sd.cnt && k0 + kk < mylen;
     oc[dst] = ok ? tc[warp][kk][lane] : 0;
     if (ov) ov[dst] = ok ? tv[warp][kk][lane] : 0.0;
+  }
+}
+
+// Column blocks (gathered vectors larger than L2): for every slice lane, the
+// range of its row's entries in each block of `width` columns (columns
+// ascend within a row) -- kst / bln[b * 32 nslices + q] -- and per block the
+// slice's longest range, maxb[b * nslices + w].  Blocks past a matrix's count
+// are empty.
+__global__ void sell_block_lanes_kernel(const SellSlice* __restrict__ slices, int nslices,
+                                        const int32_t* __restrict__ row,
+                                        const int32_t* __restrict__ len,
+                                        const int64_t* __restrict__ rpa,
+                                        const int32_t* __restrict__ cia,
+                                        const int64_t* __restrict__ rpt,
+                                        const int32_t* __restrict__ cit, int nba, int nbt,
+                                        int64_t wa, int64_t wt, int nbmax,
+                                        int32_t* __restrict__ kst, int32_t* __restrict__ bln,
+                                        int32_t* __restrict__ maxb) {
+  const int64_t gt = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t w = gt >> 5;
+  if (w >= nslices) return;
+  const int lane = static_cast<int>(gt & 31);
+  const int64_t q = 32 * w + lane;
+  const int64_t nq = 32LL * nslices;
+  const SellSlice sd = slices[w];
+  const int mat = sd.mat;
+  const int nb = mat ? nbt : nba;
+  const int64_t width = mat ? wt : wa;
+  const int L = lane < sd.cnt ? len[q] : 0;
+  const int32_t* c = L > 0 ? (mat ? cit + rpt[row[q]] : cia + rpa[row[q]]) : nullptr;
+  int k0 = 0;
+  for (int b = 0; b < nbmax; ++b) {
+    int k1 = k0;
+    if (b < nb) {
+      if (b == nb - 1) {
+        k1 = L;
+      } else {  // first entry with column >= (b + 1) * width
+        const int64_t key = (b + 1) * width;
+        int lo = k0, hi = L;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (c[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        k1 = lo;
+      }
+    }
+    kst[b * nq + q] = k0;
+    bln[b * nq + q] = k1 - k0;
+    const unsigned mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(k1 - k0));
+    if (lane == 0) maxb[static_cast<int64_t>(b) * nslices + w] = static_cast<int32_t>(mx);
+    k0 = k1;
   }
 }
 
@@ -117,7 +169,15 @@ struct SgdOp {  // the fused u / v update of one SGD iteration
   __device__ bool skip() const { return false; }
   __device__ const double* x(int mat) const { return mat ? a.xw_cur : a.xs_cur; }
   __device__ const double* x2(int) const { return nullptr; }
-  __device__ void finish(int mat, int32_t r, double acc, double, unsigned& fl) const {
+  // column-block rounds: the running sum of lane q waits in carry[0][q]
+  __device__ double start(int mat, int64_t q) const {
+    return a.round > 0 && a.round < a.nblk[mat] ? a.carry[0][q] : 0.0;
+  }
+  __device__ void finish(int mat, int32_t r, double acc, double, unsigned& fl, int64_t q) const {
+    if (a.round < a.nblk[mat] - 1) {
+      a.carry[0][q] = acc;
+      return;
+    }
     sgd_epilogue(a, mat, r, acc, fl);
   }
   __device__ void end(unsigned fl) const {
@@ -134,7 +194,8 @@ struct PassOp {  // generic passes (pass_epilogue); one matrix per launch
   __device__ bool skip() const { return p.skip && *p.skip; }
   __device__ const double* x(int) const { return p.xg; }
   __device__ const double* x2(int) const { return q.xg; }
-  __device__ void finish(int, int32_t r, double acc, double acc2, unsigned&) const {
+  __device__ double start(int, int64_t) const { return 0.0; }
+  __device__ void finish(int, int32_t r, double acc, double acc2, unsigned&, int64_t) const {
     pass_epilogue(p, r, acc);
     if constexpr (NV == 2) pass_epilogue(q, r, acc2);
   }
@@ -165,7 +226,7 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
   const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
   const double* __restrict__ x = op.x(mat);
   const double* __restrict__ x2 = op.x2(mat);
-  double acc = 0.0, acc2 = 0.0;
+  double acc = op.start(mat, q), acc2 = 0.0;
   auto consume = [&](const int32_t* c, const double* v, int k0, bool full) {
     double g[B], g2[B];
 #pragma unroll
@@ -234,7 +295,7 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
     consume(c, v, k, false);
   }
   unsigned fl = 0;
-  if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl);
+  if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl, q);
   op.end(fl);
 }
 
@@ -324,7 +385,7 @@ sell_long_kernel(const Op op, const SellArgs sa) {
     }
     return;
   }
-  double acc = 0.0, acc2 = 0.0;
+  double acc = op.start(mat, q), acc2 = 0.0;
   for (int r = 0; r < rounds; ++r) {
     const int bi = r % R;
     mbar_wait(&full[bi], (r / R) & 1);
@@ -338,7 +399,7 @@ sell_long_kernel(const Op op, const SellArgs sa) {
     mbar_arrive(&empty[bi]);
   }
   unsigned fl = 0;
-  if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl);
+  if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl, q);
   op.end(fl);
 }
 
@@ -359,7 +420,7 @@ void launch_warp(const Op& op, const SellArgs& sa, cudaStream_t s) {
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
                        const int64_t* kbp, const int32_t* midx, int nmat_slices,
                        const SellSlice* slices, const int32_t* row, const int32_t* len,
-                       int32_t* out_ci, double* out_va, cudaStream_t s) {
+                       const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s) {
   if (nmat_slices == 0) return cudaSuccess;
   int64_t items = 0;
   cudaError_t e = cudaMemcpyAsync(&items, kbp + nmat_slices, sizeof items,
@@ -367,7 +428,7 @@ cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map,
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess || items == 0) return e;
   build_sell_kernel<<<static_cast<unsigned>((items + 1) / 2), 64, 0, s>>>(
-      rp, ci, map, val, kbp, midx, nmat_slices, slices, row, len, out_ci, out_va);
+      rp, ci, map, val, kbp, midx, nmat_slices, slices, row, len, kst, out_ci, out_va);
   count_launch(s);
   return cudaGetLastError();
 }
@@ -380,6 +441,19 @@ cudaError_t launch_sell_rows(const SellSlice* slices, const int32_t* r0, int nsl
   const int64_t n = 32LL * nslices;
   sell_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
       slices, r0, nslices, rowlist_a, rowlist_t, rp_a, rp_t, row, len);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sell_block_lanes(const SellSlice* slices, int nslices, const int32_t* row,
+                                    const int32_t* len, const int64_t* rpa, const int32_t* cia,
+                                    const int64_t* rpt, const int32_t* cit, int nba, int nbt,
+                                    int64_t wa, int64_t wt, int nbmax, int32_t* kst, int32_t* bln,
+                                    int32_t* maxb, cudaStream_t s) {
+  if (nslices == 0) return cudaSuccess;
+  const int64_t n = 32LL * nslices;
+  sell_block_lanes_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      slices, nslices, row, len, rpa, cia, rpt, cit, nba, nbt, wa, wt, nbmax, kst, bln, maxb);
   count_launch(s);
   return cudaGetLastError();
 }
