@@ -162,6 +162,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SELL_PASSES")) M->sell_passes = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL_ORDER")) M->sell_order = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_BLOCKED")) M->sell_blocked = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_BLOCK_WIN")) M->block_win = atoi(e) != 0;
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -467,6 +468,8 @@ void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
   };
   M->n_sgd = upload(M->tiles_sgd, sgd);
   M->n_sgd_long = static_cast<int>(pa.lng.size() + pt.lng.size());
+  M->n_la = static_cast<int>(pa.lng.size());
+  M->n_sa = static_cast<int>(pa.slices.size());
   M->n_a = upload(M->tiles_a, ta);
   M->n_t = upload(M->tiles_t, tt);
   upload(M->rowlist_a, pa.rowlist);
@@ -879,6 +882,28 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
   pt.mark(s, "workspaces");
 }
 
+// L2 access-policy window of stream st: [base, base + bytes) persisting (as much
+// of it as the carve-out holds), or with bytes == 0 the handle's default
+// (base == xbuf: the gathered vectors; nullptr: none).
+void set_l2_window(equil_matrix* M, cudaStream_t st, const void* base, size_t bytes) {
+  if (M->l2_carve == 0) return;
+  cudaStreamAttrValue attr{};
+  if (bytes == 0 && base) {
+    bytes = M->l2_default_bytes;
+  }
+  if (base && bytes) {
+    const size_t win = std::min(bytes, M->l2_max_window);
+    attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio =
+        static_cast<float>(std::min(1.0, static_cast<double>(M->l2_carve) / win));
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr);
+  cudaGetLastError();  // a hint; never fail on it
+}
+
 void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   // each vector padded to whole panels (the panel traversal bulk-copies them)
   auto whole = [](int64_t x) { return (x + eqb::kPanelW - 1) / eqb::kPanelW * eqb::kPanelW; };
@@ -906,7 +931,10 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   if (l2win && max_persist > 0 && max_window > 0) {
     const size_t win = std::min(bytes, static_cast<size_t>(max_window));
     const size_t carve = std::min(win, static_cast<size_t>(max_persist));
+    M->l2_max_window = static_cast<size_t>(max_window);
+    M->l2_default_bytes = bytes;
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+      M->l2_carve = carve;
       cudaStreamAttrValue attr{};
       attr.accessPolicyWindow.base_ptr = M->xbuf.p;
       attr.accessPolicyWindow.num_bytes = win;
@@ -1603,6 +1631,35 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               CK(eqb::launch_sgd_sell(a, sa, M->sell_variant, s));
               CK(cudaEventRecord(M->ev_join, M->copy_stream));
               CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+            }
+          } else if (rounds > 1) {
+            // column blocks: one launch pair per (round, matrix), so each launch
+            // gathers from one block, which the L2 access-policy window on both
+            // streams keeps persisting (EQUIL_BLOCK_WIN=0: the whole-buffer window)
+            for (int mat = 0; mat < 2; ++mat) {
+              if (rd >= M->nblk[mat]) continue;
+              if (M->block_win) {
+                const int64_t len = mat ? M->m_pad() : M->n_pad();
+                const int64_t b0 = rd * M->bwidth[mat];
+                const double* base = (mat ? a.xw_cur : a.xs_cur) + b0;
+                const size_t bytes = static_cast<size_t>(std::min(M->bwidth[mat], len - b0)) * 8;
+                set_l2_window(M, s, base, bytes);
+                set_l2_window(M, M->copy_stream, base, bytes);
+              }
+              const int lb = mat ? M->n_la : 0;
+              const int ln = mat ? M->n_sgd_long - M->n_la : M->n_la;
+              const int sb = M->n_sgd_long + (mat ? M->n_sa : 0);
+              const int sn = mat ? M->n_sgd - M->n_sgd_long - M->n_sa : M->n_sa;
+              CK(cudaEventRecord(M->ev_fork, s));
+              CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+              if (ln > 0) CK(eqb::launch_sgd_iter_part(a, lb, ln, true, 6, M->copy_stream));
+              if (sn > 0) CK(eqb::launch_sgd_iter_part(a, sb, sn, false, 6, s));
+              CK(cudaEventRecord(M->ev_join, M->copy_stream));
+              CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+            }
+            if (M->block_win && rd == rounds - 1) {  // back to the default windows
+              set_l2_window(M, s, M->xbuf.p, 0);
+              set_l2_window(M, M->copy_stream, nullptr, 0);
             }
           } else if (conc && M->n_sgd_long > 0 && M->n_sgd_long < M->n_sgd) {
             // long-row CTA groups and warp tiles as two concurrent kernels (fork /

@@ -369,6 +369,12 @@ struct equil_matrix {
   DevBuf<int32_t> rowlist_a, rowlist_t;
   int n_sgd = 0, n_a = 0, n_t = 0;
   int n_sgd_long = 0;  // leading kind-3 entries of tiles_sgd
+  int n_la = 0, n_sa = 0;  // A's kind-3 entries / A's warp slices in tiles_sgd
+  // L2 persisting window of the gathered vectors (alloc_workspaces): carve-out,
+  // device maximum window, default window bytes (xbuf); with column blocks each
+  // launch's window is its block (EQUIL_BLOCK_WIN)
+  size_t l2_carve = 0, l2_max_window = 0, l2_default_bytes = 0;
+  bool block_win = true;
   // column-panel layout of the local A / A^T shards (panel.cu), built when
   // EQUIL_PANEL=1 at creation; n_pbands == 0 selects the row-slice traversal
   // above (the default: faster on B200)
@@ -508,6 +514,7 @@ struct equil_matrix {
 
 namespace eqe {
 // defined in engine.cu, used by the extension entry points (engine_ext.cu)
+void set_l2_window(equil_matrix* M, cudaStream_t st, const void* base, size_t bytes);
 void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, int kind,
                   double coef = 0.0, bool sqrt_out = false);
 void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
