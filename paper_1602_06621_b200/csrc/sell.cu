@@ -138,6 +138,37 @@ __global__ void sell_rows_kernel(const SellSlice* __restrict__ slices,
   len[q] = l;
 }
 
+// streamed interleaved entries (read once per iteration)
+#ifndef EQ_STREAM_HINT
+#define EQ_STREAM_HINT 0  // 1: L2::128B, 2: L2::256B prefetch-size hint on the stream loads
+#endif
+__device__ __forceinline__ double ld_st(const double* p) {
+#if EQ_STREAM_HINT == 1
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#elif EQ_STREAM_HINT == 2
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return ld_na(p);
+#endif
+}
+__device__ __forceinline__ int32_t ld_st(const int32_t* p) {
+#if EQ_STREAM_HINT == 1
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::128B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#elif EQ_STREAM_HINT == 2
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return ld_na(p);
+#endif
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -248,9 +279,9 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
       int32_t c[B];
       double v[B];
 #pragma unroll
-      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * (k + b));
+      for (int b = 0; b < B; ++b) c[b] = ld_st(cp + 32 * (k + b));
 #pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * (k + b));
+      for (int b = 0; b < B; ++b) v[b] = ld_st(vp + 32 * (k + b));
       consume(c, v, k, true);
     }
   } else {
@@ -258,9 +289,9 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
       int32_t c[B];
       double v[B];
 #pragma unroll
-      for (int b = 0; b < B; ++b) c[b] = ld_na(cp + 32 * b);
+      for (int b = 0; b < B; ++b) c[b] = ld_st(cp + 32 * b);
 #pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = ld_na(vp + 32 * b);
+      for (int b = 0; b < B; ++b) v[b] = ld_st(vp + 32 * b);
       for (;;) {
         const int kn = k + B;
         const bool more = kn + B <= len;
@@ -268,9 +299,9 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
         double vn[B];
         if (more) {
 #pragma unroll
-          for (int b = 0; b < B; ++b) cn[b] = ld_na(cp + 32 * (kn + b));
+          for (int b = 0; b < B; ++b) cn[b] = ld_st(cp + 32 * (kn + b));
 #pragma unroll
-          for (int b = 0; b < B; ++b) vn[b] = ld_na(vp + 32 * (kn + b));
+          for (int b = 0; b < B; ++b) vn[b] = ld_st(vp + 32 * (kn + b));
         }
         consume(c, v, k, true);
         k = kn;
@@ -289,8 +320,8 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
 #pragma unroll
     for (int b = 0; b < B; ++b)
       if (k + b < len) {
-        c[b] = ld_na(cp + 32 * (k + b));
-        v[b] = ld_na(vp + 32 * (k + b));
+        c[b] = ld_st(cp + 32 * (k + b));
+        v[b] = ld_st(vp + 32 * (k + b));
       }
     consume(c, v, k, false);
   }
@@ -344,10 +375,10 @@ sell_long_kernel(const Op op, const SellArgs sa) {
       const int k0 = rr * B;
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (k0 + b < len) cc[b] = ld_na(cp + 32 * (k0 + b));
+        if (k0 + b < len) cc[b] = ld_st(cp + 32 * (k0 + b));
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (k0 + b < len) vv[b] = ld_na(vp + 32 * (k0 + b));
+        if (k0 + b < len) vv[b] = ld_st(vp + 32 * (k0 + b));
     };
     if (PIPE && r < rounds) load(r, c, v);
     for (; r < rounds; r += S) {
