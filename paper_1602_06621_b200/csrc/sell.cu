@@ -200,7 +200,19 @@ struct SgdOp {  // the fused u / v update of one SGD iteration
   __device__ bool skip() const { return false; }
   __device__ const double* x(int mat) const { return mat ? a.xw_cur : a.xs_cur; }
   __device__ const double* x2(int) const { return nullptr; }
-  // column-block rounds: the running sum of lane q waits in carry[0][q]
+  __device__ double start(int, int64_t) const { return 0.0; }
+  __device__ void finish(int mat, int32_t r, double acc, double, unsigned& fl, int64_t) const {
+    sgd_epilogue(a, mat, r, acc, fl);
+  }
+  __device__ void end(unsigned fl) const {
+    // peer stores performed system-wide before the kernel completes (the
+    // barrier that follows orders every peer's next reads after them)
+    if (a.npeer) __threadfence_system();
+    if (fl) atomicOr(a.flags, fl);
+  }
+};
+// column-block rounds: the running sum of lane q waits in carry[0][q]
+struct SgdBlockOp : SgdOp {
   __device__ double start(int mat, int64_t q) const {
     return a.round > 0 && a.round < a.nblk[mat] ? a.carry[0][q] : 0.0;
   }
@@ -210,12 +222,6 @@ struct SgdOp {  // the fused u / v update of one SGD iteration
       return;
     }
     sgd_epilogue(a, mat, r, acc, fl);
-  }
-  __device__ void end(unsigned fl) const {
-    // peer stores performed system-wide before the kernel completes (the
-    // barrier that follows orders every peer's next reads after them)
-    if (a.npeer) __threadfence_system();
-    if (fl) atomicOr(a.flags, fl);
   }
 };
 template <int NV_>
@@ -492,6 +498,11 @@ cudaError_t launch_sell_block_lanes(const SellSlice* slices, int nslices, const 
 cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int variant,
                                  cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
+  if (a.nblk[0] > 1 || a.nblk[1] > 1) {
+    launch_long<SgdBlockOp, 4, 15, true, 1>(SgdBlockOp{{a}}, sa, s);
+    count_launch(s);
+    return cudaGetLastError();
+  }
   const SgdOp op{a};
   switch (variant) {  // EQUIL_SELL_LVARIANT (A/B knob); 0 = measured best on c3
     case 1: launch_long<SgdOp, 8, 7, true, 2>(op, sa, s); break;
@@ -507,6 +518,11 @@ cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int v
 cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int variant,
                             cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
+  if (a.nblk[0] > 1 || a.nblk[1] > 1) {
+    launch_warp<SgdBlockOp, 8, true, 6>(SgdBlockOp{{a}}, sa, s);
+    count_launch(s);
+    return cudaGetLastError();
+  }
   const SgdOp op{a};
   switch (variant) {  // EQUIL_SELL_VARIANT (A/B knob); 0 = measured best on c3
     case 1: launch_warp<SgdOp, 4, false, 12>(op, sa, s); break;
