@@ -15,6 +15,9 @@
 // longest-processing-time order: the 10^4-entry rows of a Zipf matrix start at
 // once instead of trailing the launch).  The epilogue is the same fused
 // sgd_epilogue as the staged traversal (sgd_common.cuh).
+#include <cstdlib>
+#include <type_traits>
+
 #include "sgd_common.cuh"
 
 namespace eqb {
@@ -440,8 +443,31 @@ sell_long_kernel(const Op op, const SellArgs sa) {
   op.end(fl);
 }
 
+// Preferred shared-memory carveout (percent of the maximum), once per kernel
+// instantiation.  The SGD long slices need 16.6 KB per CTA: 22% (~50 KB, three
+// CTAs) leaves the rest of each SM's 256 KB to L1, where xw's hot slots live
+// (c3: 1.158 -> 1.117-1.128 ms; 8% starves the long kernel, 30-50% shrinks L1).
+// EQUIL_CARVE_LONG / EQUIL_CARVE_WARP override (-1: the driver's choice).
+template <class K>
+void carveout(K kernel, const char* env, int dflt) {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int pct = dflt;
+  if (const char* e = getenv(env)) pct = atoi(e);
+  if (pct >= 0) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
+  }
+}
+template <class Op>
+constexpr int carve_long() { return std::is_same<Op, SgdOp>::value ? 22 : -1; }
+template <class Op>
+constexpr int carve_warp() { return std::is_same<Op, SgdOp>::value ? 0 : -1; }
+
 template <class Op, int B, int S, bool PIPE, int MINB>
 void launch_long(const Op& op, const SellArgs& sa, cudaStream_t s) {
+  carveout(sell_long_kernel<Op, B, S, PIPE, MINB>, "EQUIL_CARVE_LONG", carve_long<Op>());
   sell_long_kernel<Op, B, S, PIPE, MINB>
       <<<static_cast<unsigned>(sa.nslices - sa.first), 32 * (S + 1), 0, s>>>(op, sa);
 }
@@ -449,6 +475,7 @@ void launch_long(const Op& op, const SellArgs& sa, cudaStream_t s) {
 template <class Op, int B, bool PIPE, int MINB>
 void launch_warp(const Op& op, const SellArgs& sa, cudaStream_t s) {
   const unsigned g = static_cast<unsigned>((sa.nslices - sa.first + 3) / 4);
+  carveout(sell_warp_kernel<Op, B, PIPE, MINB>, "EQUIL_CARVE_WARP", carve_warp<Op>());
   sell_warp_kernel<Op, B, PIPE, MINB><<<g, 128, 0, s>>>(op, sa);
 }
 
