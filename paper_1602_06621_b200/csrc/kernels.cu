@@ -78,10 +78,13 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
 // One CTA per jump: W[dst0 + b] = sum_i r_i W_{p+i}, p = position of W[src0 + b].
 // The set bits of r are given as a host-expanded list of positions (uint16,
 // padded to a multiple of 8 with kJumpWords, whose window reads zeros).
-__global__ void __launch_bounds__(kMtThreads)
+// kJumpGroups thread groups of kMtThreads split the position list and XOR
+// their partial sums (GF(2): any order gives the same words).
+constexpr int kJumpGroups = 3;
+__global__ void __launch_bounds__(kMtThreads * kJumpGroups)
 mt_jump_kernel(uint64_t* __restrict__ windows, int src0, int dst0,
                const uint4* __restrict__ pos8, int npos8) {
-  extern __shared__ uint64_t sx[];  // kJumpWords + kN zero words
+  extern __shared__ uint64_t sx[];  // kJumpWords + kN zero words, then the partials
   const int tid = threadIdx.x;
   const uint64_t* src = windows + static_cast<size_t>(src0 + blockIdx.x) * mt::kN;
   for (int j = tid; j < mt::kN; j += blockDim.x) {
@@ -98,10 +101,13 @@ mt_jump_kernel(uint64_t* __restrict__ windows, int src0, int dst0,
       sx[q + mt::kN + j] = mt_next(sx[q + j], sx[q + j + 1], sx[q + mt::kM + j]);
     __syncthreads();
   }
-  if (tid < mt::kN) {
+  const int grp = tid / kMtThreads, t = tid - grp * kMtThreads;
+  uint64_t* part = sx + kJumpWords + mt::kN;  // [kJumpGroups - 1][kN]
+  if (t < mt::kN) {
     uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    const uint64_t* x = sx + tid;
-    for (int q = 0; q < npos8; ++q) {
+    const uint64_t* x = sx + t;
+    const int q0 = npos8 * grp / kJumpGroups, q1 = npos8 * (grp + 1) / kJumpGroups;
+    for (int q = q0; q < q1; ++q) {
       const uint4 p = __ldg(pos8 + q);  // 8 positions, warp-uniform (broadcast)
       a0 ^= x[p.x & 0xffff];
       a1 ^= x[p.x >> 16];
@@ -112,7 +118,17 @@ mt_jump_kernel(uint64_t* __restrict__ windows, int src0, int dst0,
       a2 ^= x[p.w & 0xffff];
       a3 ^= x[p.w >> 16];
     }
-    windows[static_cast<size_t>(dst0 + blockIdx.x) * mt::kN + tid] = (a0 ^ a1) ^ (a2 ^ a3);
+    if (grp > 0) part[(grp - 1) * mt::kN + t] = (a0 ^ a1) ^ (a2 ^ a3);
+    a0 ^= a1;
+    a2 ^= a3;
+    a0 ^= a2;
+    if (grp == 0) part[(kJumpGroups - 1) * mt::kN + t] = a0;
+  }
+  __syncthreads();
+  if (grp == 0 && t < mt::kN) {
+    uint64_t w = part[(kJumpGroups - 1) * mt::kN + t];
+    for (int g = 0; g < kJumpGroups - 1; ++g) w ^= part[g * mt::kN + t];
+    windows[static_cast<size_t>(dst0 + blockIdx.x) * mt::kN + t] = w;
   }
 }
 
@@ -174,18 +190,24 @@ int ceil_log2(uint64_t x) {
   return k;
 }
 
-// Segment length L = 2^k: trade jump levels (one ~wave each) against the
-// sequential length each segment generates.
+// Segment length L = 2^k: trade jump-tree levels against the sequential length
+// each segment generates.  Model (B200, measured): a jump wave (one CTA per SM,
+// 172 KB of shared memory) ~0.09 ms; generation ~0.76 us per 1000 outputs per
+// CTA, six CTAs per SM.
 int choose_seg_log2(uint64_t total) {
   int best = 14;
   double best_cost = 1e300;
   for (int k = 14; k <= 40; ++k) {
     const uint64_t L = 1ULL << k;
     const uint64_t G = (total + L - 1) / L;
-    const double levels = static_cast<double>(ceil_log2(G));
-    const double waves = static_cast<double>((G + 147) / 148);
-    const double cost = levels * 1.0 + (waves - 1) * 0.5 +
-                        static_cast<double>(std::min(L, total)) / 312.0 * 8e-4;
+    const int levels = ceil_log2(G);
+    double cost = 0.0;
+    for (int a = 0; a < levels; ++a) {
+      const uint64_t cnt = std::min<uint64_t>(1ULL << a, G - (1ULL << a));
+      cost += static_cast<double>((cnt + 147) / 148) * 0.09;
+    }
+    cost += static_cast<double>((G + 148 * 6 - 1) / (148 * 6)) *
+            static_cast<double>(std::min(L, total)) * 7.6e-7;
     if (cost < best_cost) {
       best_cost = cost;
       best = k;
@@ -239,7 +261,7 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
   if (levels > 0)
     EQ_CUDA_TRY(cudaMemcpyAsync(pos, hpos.data(), hpos.size() * sizeof(uint16_t),
                                 cudaMemcpyHostToDevice, s));
-  const size_t smem = (kJumpWords + mt::kN) * sizeof(uint64_t);
+  const size_t smem = (kJumpWords + mt::kN + kJumpGroups * mt::kN) * sizeof(uint64_t);
   static bool attr = false;
   if (!attr) {
     EQ_CUDA_TRY(cudaFuncSetAttribute(mt_jump_kernel,
@@ -250,7 +272,7 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
   for (int a = 0; a < levels; ++a) {
     const uint64_t lo = 1ULL << a;
     const uint64_t cnt = std::min(lo, G - lo);
-    mt_jump_kernel<<<static_cast<unsigned>(cnt), kMtThreads, smem, s>>>(
+    mt_jump_kernel<<<static_cast<unsigned>(cnt), kMtThreads * kJumpGroups, smem, s>>>(
         windows, 0, static_cast<int>(lo),
         reinterpret_cast<const uint4*>(pos + static_cast<size_t>(a) * kPosCap), npos8[a]);
     count_launch(s);
