@@ -7,7 +7,31 @@
 
 namespace eqb {
 
-// read-only load that does not allocate in L1 (streamed CSR arrays)
+// read-only load that does not allocate in L1 (streamed CSR arrays).
+// EQ_STREAM_EF: the stream is also marked evict-first in L2, so a column block
+// of the gathered vector (EQUIL_BLOCK_MB) is not pushed out by it.
+#ifndef EQ_STREAM_EF
+#define EQ_STREAM_EF 1
+#endif
+#if EQ_STREAM_EF
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+      : "=d"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_na(const int32_t* p) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+      : "=r"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+#else
 __device__ __forceinline__ double ld_na(const double* p) {
   double v;
   asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -18,6 +42,7 @@ __device__ __forceinline__ int32_t ld_na(const int32_t* p) {
   asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+#endif
 
 __device__ __forceinline__ bool sign_bit(const uint32_t* bits, int64_t b) {
   return (__ldg(bits + (b >> 5)) >> (b & 31)) & 1u;
