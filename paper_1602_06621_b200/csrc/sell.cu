@@ -50,15 +50,34 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
   const int mylen = len[32 * w + lane];
   const int64_t mystart =
       lane < sd.cnt ? rp[row[32 * w + lane]] + (kst ? kst[32 * w + lane] : 0) : 0;
-  for (int r = 0; r < sd.cnt; ++r) {
-    const int64_t st = __shfl_sync(0xffffffffu, mystart, r);
-    const int ln = __shfl_sync(0xffffffffu, mylen, r);
-    const int k = k0 + lane;
-    if (k < ln) {
-      const int32_t c = ci[st + k];
-      tc[warp][lane][r] = map ? map[c] : c;
-      if (ov) tv[warp][lane][r] = val[st + k];
+  // eight rows per batch: their loads (and then their slot lookups) are issued
+  // together instead of one dependent round trip per row
+  const int k = k0 + lane;
+  for (int r0 = 0; r0 < sd.cnt; r0 += 8) {
+    int32_t c[8];
+    double v[8];
+    bool ok[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t st = __shfl_sync(0xffffffffu, mystart, r0 + j);
+      const int ln = __shfl_sync(0xffffffffu, mylen, r0 + j);
+      ok[j] = r0 + j < sd.cnt && k < ln;
+      if (ok[j]) {
+        c[j] = ci[st + k];
+        if (ov) v[j] = val[st + k];
+      }
     }
+    if (map) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (ok[j]) c[j] = map[c[j]];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (ok[j]) {
+        tc[warp][lane][r0 + j] = c[j];
+        if (ov) tv[warp][lane][r0 + j] = v[j];
+      }
   }
   __syncwarp();
   const int kend = min(32, sd.maxlen - k0);
