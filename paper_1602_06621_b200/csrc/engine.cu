@@ -163,6 +163,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SELL_ORDER")) M->sell_order = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_BLOCKED")) M->sell_blocked = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_BLOCK_WIN")) M->block_win = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_SPLIT_EPI")) M->split_epi = atoi(e) != 0;
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -947,6 +948,7 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
     cudaGetLastError();  // the window is a hint; never fail on it
   }
   if (pt) pt->mark(M->stream, "l2 window");
+  M->rowacc.alloc(M->m_loc() + M->n_loc());
   M->u.alloc(M->m_loc());
   M->ub.alloc(M->m_loc());
   M->v.alloc(M->n_loc());
@@ -1608,7 +1610,21 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               sa.ci[k] = M->sell_ci[k].p;
               sa.va[k] = M->sell_va[k].p;
             }
-            if (M->sell_long == 2 && M->n_sell_long > 0) {
+            if (M->split_epi && M->sell_nb == 1 && M->sell_long == 2) {
+              // row sums from both kernels (concurrent), then one update pass
+              a.carry[0] = M->rowacc.p;
+              a.carry[1] = M->rowacc.p + M->m_loc();
+              CK(cudaEventRecord(M->ev_fork, s));
+              CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
+              eqb::SellArgs sl = sa;
+              sl.nslices = M->n_sell_long;
+              CK(eqb::launch_sgd_sell_split(a, sl, true, M->copy_stream));
+              sa.first = M->n_sell_long;
+              CK(eqb::launch_sgd_sell_split(a, sa, false, s));
+              CK(cudaEventRecord(M->ev_join, M->copy_stream));
+              CK(cudaStreamWaitEvent(s, M->ev_join, 0));
+              CK(eqb::launch_sgd_update_rows(a, M->m_loc(), M->n_loc(), s));
+            } else if (M->sell_long == 2 && M->n_sell_long > 0) {
               // long slices on warp-specialised CTAs, the rest on warps,
               // concurrently (fork / join on the copy stream)
               CK(cudaEventRecord(M->ev_fork, s));

@@ -426,6 +426,9 @@ struct equil_matrix {
   // the generic passes (LSQR, apply, variants) over the same slices: columns
   // in padded coordinates (their vectors are not in slot layout), built on
   // first use; values shared with the SGD arrays
+  // split epilogue (EQUIL_SPLIT_EPI): row sums to rowacc, then one update pass
+  bool split_epi = true;
+  DevBuf<double> rowacc;
   bool sell_passes = true;  // EQUIL_SELL_PASSES=0: generic passes on the staged kernels
   bool sell_pass = false;
   DevBuf<int32_t> sell_pci[2], sell_pidx[2];

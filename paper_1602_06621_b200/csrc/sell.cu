@@ -140,6 +140,21 @@ __global__ void sell_block_lanes_kernel(const SellSlice* __restrict__ slices, in
   }
 }
 
+// the split epilogue: rows [0, m_loc) of A then [0, n_loc) of A^T, in order
+__global__ void __launch_bounds__(256) sgd_update_rows_kernel(const SgdIterArgs a, int64_t m_loc,
+                                                              int64_t n_loc) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned fl = 0;
+  if (k < m_loc + n_loc) {
+    const int mat = k >= m_loc ? 1 : 0;
+    const int64_t r = mat ? k - m_loc : k;
+    sgd_epilogue(a, mat, r, a.carry[mat][r], fl);
+  }
+  if (a.npeer) __threadfence_system();
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if (fl && (threadIdx.x & 31) == 0) atomicOr(a.flags, fl);
+}
+
 __global__ void sell_rows_kernel(const SellSlice* __restrict__ slices,
                                  const int32_t* __restrict__ r0, int nslices,
                                  const int32_t* __restrict__ rla, const int32_t* __restrict__ rlt,
@@ -232,6 +247,15 @@ struct SgdOp {  // the fused u / v update of one SGD iteration
     if (a.npeer) __threadfence_system();
     if (fl) atomicOr(a.flags, fl);
   }
+};
+// split epilogue: the traversal only stores each row's sum (carry[mat][row]);
+// sgd_update_rows_kernel applies the update afterwards with full occupancy, so
+// the epilogue's dependent loads no longer hold the traversal's warps
+struct SgdSplitOp : SgdOp {
+  __device__ void finish(int mat, int32_t r, double acc, double, unsigned&, int64_t) const {
+    a.carry[mat][r] = acc;
+  }
+  __device__ void end(unsigned) const {}
 };
 // column-block rounds: the running sum of lane q waits in carry[0][q]
 struct SgdBlockOp : SgdOp {
@@ -480,9 +504,11 @@ void carveout(K kernel, const char* env, int dflt) {
   }
 }
 template <class Op>
-constexpr int carve_long() { return std::is_same<Op, SgdOp>::value ? 22 : -1; }
+constexpr bool is_sgd() { return std::is_same<Op, SgdOp>::value || std::is_same<Op, SgdSplitOp>::value; }
 template <class Op>
-constexpr int carve_warp() { return std::is_same<Op, SgdOp>::value ? 0 : -1; }
+constexpr int carve_long() { return is_sgd<Op>() ? 22 : -1; }
+template <class Op>
+constexpr int carve_warp() { return is_sgd<Op>() ? 0 : -1; }
 
 template <class Op, int B, int S, bool PIPE, int MINB>
 void launch_long(const Op& op, const SellArgs& sa, cudaStream_t s) {
@@ -557,6 +583,25 @@ cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int v
     case 4: launch_long<SgdOp, 8, 7, false, 2>(op, sa, s); break;
     default: launch_long<SgdOp, 4, 15, true, 1>(op, sa, s); break;
   }
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_update_rows(const SgdIterArgs& a, int64_t m_loc, int64_t n_loc,
+                                   cudaStream_t s) {
+  const int64_t n = m_loc + n_loc;
+  if (n == 0) return cudaSuccess;
+  sgd_update_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(a, m_loc, n_loc);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_sell_split(const SgdIterArgs& a, const SellArgs& sa, bool lng,
+                                  cudaStream_t s) {
+  if (sa.nslices <= sa.first) return cudaSuccess;
+  const SgdSplitOp op{{a}};
+  if (lng) launch_long<SgdSplitOp, 4, 15, true, 1>(op, sa, s);
+  else launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s);
   count_launch(s);
   return cudaGetLastError();
 }
