@@ -1618,9 +1618,9 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
               eqb::SellArgs sl = sa;
               sl.nslices = M->n_sell_long;
-              CK(eqb::launch_sgd_sell_split(a, sl, true, M->copy_stream));
+              CK(eqb::launch_sgd_sell_split(a, sl, true, M->sell_lvariant, M->copy_stream));
               sa.first = M->n_sell_long;
-              CK(eqb::launch_sgd_sell_split(a, sa, false, s));
+              CK(eqb::launch_sgd_sell_split(a, sa, false, M->sell_variant, s));
               CK(cudaEventRecord(M->ev_join, M->copy_stream));
               CK(cudaStreamWaitEvent(s, M->ev_join, 0));
               CK(eqb::launch_sgd_update_rows(a, M->m_loc(), M->n_loc(), s));

@@ -174,7 +174,7 @@ cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int varian
 // split epilogue: the traversal stores row sums in a.carry[mat][row] (lng: the
 // long-slice kernel), then the update runs over all local rows
 cudaError_t launch_sgd_sell_split(const SgdIterArgs& a, const SellArgs& sa, bool lng,
-                                  cudaStream_t s);
+                                  int variant, cudaStream_t s);
 cudaError_t launch_sgd_update_rows(const SgdIterArgs& a, int64_t m_loc, int64_t n_loc,
                                    cudaStream_t s);
 // the long slices (one warp-specialised CTA each, EQUIL_SELL_LVARIANT)

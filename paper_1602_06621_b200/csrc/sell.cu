@@ -597,11 +597,26 @@ cudaError_t launch_sgd_update_rows(const SgdIterArgs& a, int64_t m_loc, int64_t 
 }
 
 cudaError_t launch_sgd_sell_split(const SgdIterArgs& a, const SellArgs& sa, bool lng,
-                                  cudaStream_t s) {
+                                  int variant, cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
   const SgdSplitOp op{{a}};
-  if (lng) launch_long<SgdSplitOp, 4, 15, true, 1>(op, sa, s);
-  else launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s);
+  if (lng) {
+    switch (variant) {  // EQUIL_SELL_LVARIANT
+      case 1: launch_long<SgdSplitOp, 4, 15, true, 2>(op, sa, s); break;
+      case 2: launch_long<SgdSplitOp, 2, 15, true, 2>(op, sa, s); break;
+      case 3: launch_long<SgdSplitOp, 4, 7, true, 4>(op, sa, s); break;
+      default: launch_long<SgdSplitOp, 4, 15, true, 1>(op, sa, s); break;
+    }
+  } else {
+    switch (variant) {  // EQUIL_SELL_VARIANT
+      case 1: launch_warp<SgdSplitOp, 8, true, 8>(op, sa, s); break;
+      case 2: launch_warp<SgdSplitOp, 8, true, 10>(op, sa, s); break;
+      case 3: launch_warp<SgdSplitOp, 4, true, 12>(op, sa, s); break;
+      case 4: launch_warp<SgdSplitOp, 16, false, 8>(op, sa, s); break;
+      case 5: launch_warp<SgdSplitOp, 8, false, 10>(op, sa, s); break;
+      default: launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s); break;
+    }
+  }
   count_launch(s);
   return cudaGetLastError();
 }
