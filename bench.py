@@ -312,10 +312,11 @@ def run_ours(args):
             "achieved_GBps": B * value / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sgd_sell_kernel + sgd_sell_long_kernel: one iteration = "
-                                   "A and A^T passes over interleaved row slices with the fused "
-                                   "u/v epilogue (warp slices and warp-specialised long-row "
-                                   "CTAs as two concurrent launches)",
+                         "kernel": "sell_warp_kernel + sell_long_kernel + "
+                                   "sgd_update_rows_kernel: one iteration = A and A^T passes "
+                                   "over interleaved row slices (warp slices and "
+                                   "warp-specialised long-row CTAs, concurrent), then the u/v "
+                                   "update of every row",
                          "bytes_per_launch": per_gpu_bytes, "launch_ms": kern_s * 1e3,
                          "peak_source": peak_src},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
