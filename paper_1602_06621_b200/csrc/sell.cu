@@ -11,10 +11,15 @@
 // no cross-lane step: the only limit is how many column / value loads and
 // gathers each SM keeps in flight.
 //
-// Slices of both matrices run in one launch, longest first (a greedy
+// Slices of both matrices are ordered longest first (a greedy
 // longest-processing-time order: the 10^4-entry rows of a Zipf matrix start at
-// once instead of trailing the launch).  The epilogue is the same fused
-// sgd_epilogue as the staged traversal (sgd_common.cuh).
+// once instead of trailing the launch).  Rows longer than kTileNnz go to the
+// warp-specialised sell_long_kernel, the rest to sell_warp_kernel; the two run
+// concurrently.  By default (SgdSplitOp) both only store each row's sum and
+// sgd_update_rows_kernel then applies the SGD update (sgd_epilogue,
+// sgd_common.cuh) to every row; SgdOp fuses the epilogue instead, SgdBlockOp
+// carries sums between column-block rounds, PassOp<NV> runs the generic passes
+// (LSQR, variants) with one or two gathered vectors.
 #include <cstdlib>
 #include <type_traits>
 
