@@ -102,3 +102,19 @@ def test_host_side_preconditions_need_no_gpu():
         eq.ExplicitMatrix.sparse(0, 2, [])
     with pytest.raises(eq.InvalidArgument, match="row_ptr"):
         eq.ExplicitMatrix.from_csr(2, 2, [0, 2, 1], [0, 1], [1.0, 1.0])
+
+
+def test_one_shot_result_buffers_are_checked_before_any_device_work():
+    # sgd_equilibrate_csr(out=...): caller-owned (e.g. pinned) result arrays must
+    # be contiguous float64 of lengths (rows, cols, rows, cols)
+    import numpy as np
+    rp = np.array([0, 1, 2], np.int64)
+    col = np.array([0, 1], np.int32)
+    val = np.array([1.0, 2.0])
+    p = eq.EquilibrationParams(iterations=1)
+    bad = [(np.zeros(2), np.zeros(2), np.zeros(2), np.zeros(3)),
+           (np.zeros(2, np.float32), np.zeros(2), np.zeros(2), np.zeros(2)),
+           (np.zeros(4)[::2], np.zeros(2), np.zeros(2), np.zeros(2))]
+    for out in bad:
+        with pytest.raises(ValueError, match="out arrays"):
+            eq.sgd_equilibrate_csr(2, 2, rp, col, val, p, out=out)
