@@ -669,11 +669,15 @@ void build_block_layout(equil_matrix* M) {
   M->nblk[0] = M->nblk[1] = 1;
   if (M->use_panels) return;
   double mb = 60.0;
-  if (const char* e = getenv("EQUIL_BLOCK_MB")) mb = std::max(1e-6, atof(e));
+  if (const char* e = getenv("EQUIL_BLOCK_MB")) {
+    const double v = atof(e);
+    if (v > 0.0) mb = v;
+  }
   const int64_t lens[2] = {M->n_pad(), M->m_pad()};
   for (int mat = 0; mat < 2; ++mat) {
     const double bytes = static_cast<double>(lens[mat]) * 8.0;
-    const int nb = static_cast<int>(std::ceil(bytes / (mb * 1e6)));
+    // (at most 1024 blocks: the per-row block boundaries take rows * (nb - 1) ints)
+    const int nb = static_cast<int>(std::min(1024.0, std::ceil(bytes / (mb * 1e6))));
     if (nb <= 1) continue;
     const eqb::DevCsr& C = mat ? M->AT : M->A;
     const int64_t width = (lens[mat] + nb - 1) / nb;
