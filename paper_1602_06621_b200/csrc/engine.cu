@@ -291,7 +291,8 @@ void ensure_sell_pass(equil_matrix* M) {
 
 // One generic pass (b: the dual pass) over matrix `mat` on the interleaved
 // slices: long slices on the copy stream, warp slices on the main stream.
-void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::PassArgs* b) {
+void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::PassArgs* b,
+               bool pair = false) {
   ensure_sell_pass(M);
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
@@ -311,11 +312,11 @@ void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::Pass
     eqb::SellArgs sl = sa;
     sl.first = 0;
     sl.nslices = nl;
-    CK(eqb::launch_sell_pass(a, b, sl, true, M->copy_stream));
+    CK(eqb::launch_sell_pass(a, b, sl, true, pair, M->copy_stream));
   }
   sa.first = nl;
   sa.nslices = nall;
-  CK(eqb::launch_sell_pass(a, b, sa, false, s));
+  CK(eqb::launch_sell_pass(a, b, sa, false, pair, s));
   if (nl > 0) {
     CK(cudaEventRecord(M->ev_join, M->copy_stream));
     CK(cudaStreamWaitEvent(s, M->ev_join, 0));
@@ -957,7 +958,9 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   M->ub.alloc(M->m_loc());
   M->v.alloc(M->n_loc());
   M->vb.alloc(M->n_loc());
-  const int64_t big = std::max(M->m_pad(), M->n_pad());
+  // the longest canonical reduction runs over m + n terms (the history's RMS
+  // spread, equil_rms_error); padded vectors are at most m_pad / n_pad long
+  const int64_t big = std::max(M->m_pad() + M->n_pad(), M->m + M->n);
   M->red_part.alloc((big + eqb::kChunk - 1) / eqb::kChunk + 1);
   M->tmp_m.alloc(M->m_pad());
   M->tmp_n.alloc(M->n_pad());
@@ -1298,6 +1301,14 @@ struct DiagPlan {
 // 1 plain sum, 2 sum of coef * x; optional sqrt of the result
 void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, int kind,
                   double coef, bool sqrt_out) {
+  const size_t parts = static_cast<size_t>((len + eqb::kChunk - 1) / eqb::kChunk) + 1;
+  if (parts > M->red_part.n) {  // never inside a captured graph: setup sizes it for m + n
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(M->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      throw std::runtime_error("canon_reduce: partials buffer too small during capture");
+    M->red_part.ensure(parts);
+  }
   CK(eqb::launch_canon_reduce(x, len, kind, coef, M->red_part.p, M->red_counter.p, out,
                               sqrt_out ? 1 : 0, M->stream));
 }
@@ -1918,7 +1929,8 @@ namespace eqe {
 
 // one matvec pass of B (scaled by scale when non-null) in the given mode
 void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
-                const double* scale, const double* prev, const double* coef) {
+                const double* scale, const double* prev, const double* coef,
+                const int* skip) {
   if (M->dense) {
     eqb::DensePassArgs a{};
     a.A = M->Ad.p;
@@ -1931,6 +1943,7 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
     a.prev = prev;
     a.coef = coef;
     a.mode = mode;
+    a.skip = skip;
     a.colpart = M->colpart.p;
     CK(eqb::launch_dense_pass(a, M->stream));
     return;
@@ -1948,6 +1961,7 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
   a.prev = prev;
   a.coef = coef;
   a.mode = mode;
+  a.skip = skip;
   if (M->sell && M->sell_passes) {
     sell_pass(M, adjoint ? 1 : 0, a, nullptr);
     return;
@@ -1956,11 +1970,15 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
 }
 
 // two passes of A (not the adjoint) sharing one traversal of CSR(A):
-// out0 <- (xg0, mode0, ...), out1 <- (xg1, mode1, ...); dense: two passes
+// out0 <- (xg0, mode0, ...), out1 <- (xg1, mode1, ...); dense: two passes.
+// pair (interleaved slices only, pair_layout): xg0 holds both gathered vectors
+// interleaved, xg0[2c] for pass 0 and xg0[2c + 1] for pass 1; xg1 is ignored.
+bool pair_layout(const equil_matrix* M) { return !M->dense && M->sell && M->sell_passes; }
+
 void apply_pass_dual(equil_matrix* M, const double* xg0, double* out0, int mode0,
                      const double* scale0, const double* prev0, const double* coef0,
                      const double* xg1, double* out1, int mode1, const double* scale1,
-                     const double* prev1, const double* coef1) {
+                     const double* prev1, const double* coef1, bool pair = false) {
   if (M->dense) {
     apply_pass(M, false, xg0, out0, mode0, scale0, prev0, coef0);
     apply_pass(M, false, xg1, out1, mode1, scale1, prev1, coef1);
@@ -1977,9 +1995,10 @@ void apply_pass_dual(equil_matrix* M, const double* xg0, double* out0, int mode0
   a.xg = xg0; a.out = out0; a.mode = mode0; a.scale = scale0; a.prev = prev0; a.coef = coef0;
   b.xg = xg1; b.out = out1; b.mode = mode1; b.scale = scale1; b.prev = prev1; b.coef = coef1;
   if (M->sell && M->sell_passes) {
-    sell_pass(M, 0, a, &b);
+    sell_pass(M, 0, a, &b, pair);
     return;
   }
+  if (pair) throw std::runtime_error("apply_pass_dual: interleaved pair without slices");
   CK(eqb::launch_pass_dual(a, b, M->n_a, M->stream));
 }
 
@@ -2047,19 +2066,41 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
                double* hist, int hist_cap, LsqrState& st, DevBuf<double>& x) {
   cudaStream_t s = M->stream;
   LsqrLayout L(M);
-  DevBuf<double> u, v, w, un, du, vn, ev, ex, r;
+  // pair: the two vectors the fused residual + B v pass gathers, e.x and e.v,
+  // live interleaved in one padded array (xv[2c], xv[2c + 1]) so that pass
+  // makes one 16-byte gather per entry; it is all-gathered once per iteration,
+  // after the x update (e.v is only read by that pass)
+  const bool pair = pair_layout(M);
+  const int64_t os = pair ? 2 : 1;
+  DevBuf<double> u, v, w, un, du, vn, ev, ex, xv, r;
   u.alloc(L.mL); v.alloc(L.nL); w.alloc(L.nL); x.alloc(L.nL);
   un.alloc(L.mP); du.alloc(L.mP); r.alloc(L.mP);
-  vn.alloc(L.nP); ev.alloc(L.nP); ex.alloc(L.nP);
+  vn.alloc(L.nP);
+  if (pair) {
+    xv.alloc(2 * L.nP);
+    CK(cudaMemsetAsync(xv.p, 0, 2 * L.nP * 8, s));  // e.x = 0 for the first pass
+  } else {
+    ev.alloc(L.nP);
+    ex.alloc(L.nP);
+  }
   double* unL = un.p + L.pa;
   double* duL = du.p + L.pa;
   double* rL = r.p + L.pa;
   double* vnL = vn.p + L.pt;
-  double* evL = ev.p + L.pt;
-  double* exL = ex.p + L.pt;
+  double* evL = pair ? xv.p + 2 * L.pt + 1 : ev.p + L.pt;
+  double* exL = pair ? xv.p + 2 * L.pt : ex.p + L.pt;
+  auto gather_ev = [&] {
+    if (pair) allgather_padded(M, xv.p, 2 * M->t_max);
+    else L.gather(ev.p, false);
+  };
+  auto gather_ex = [&] {
+    if (pair) allgather_padded(M, xv.p, 2 * M->t_max);
+    else L.gather(ex.p, false);
+  };
   CK(cudaMemsetAsync(x.p, 0, L.nL * 8, s));
   double* sc = M->scal.p;  // [0] beta, [1] alpha, [2] residual norm
   int* dummy = reinterpret_cast<int*>(sc + 8);
+  int* inv = reinterpret_cast<int*>(sc + 9);  // this iteration's invariant flag
 
   CK(cudaMemcpyAsync(unL, c, L.mL * 8, cudaMemcpyDeviceToDevice, s));
   L.norm(un.p, true, sc + 0);  // beta = |c|
@@ -2074,38 +2115,75 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     st.breakdown = true;
     return;
   }
-  CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, dummy, nullptr, s));
-  L.gather(ev.p, false);
+  CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, dummy, nullptr, s, os));
+  gather_ev();
   CK(cudaMemcpyAsync(w.p, v.p, L.nL * 8, cudaMemcpyDeviceToDevice, s));
   double phibar = beta, rhobar = alpha;
 
-  for (int t = 1; t <= max_iters; ++t) {
-    bool invariant = false;
-    // un = Bv - alpha u: computed here for t = 1, afterwards by the fused pass at
-    // the end of the previous iteration (same arithmetic, one A traversal less)
-    if (t == 1) apply_pass(M, false, ev.p, unL, eqb::kPassLsqrU, d, u.p, sc + 1);
-    ++st.applies;
-    L.norm(un.p, true, sc + 0);
-    beta = read_scalar(M, sc + 0);
-    if (beta > 0.0) {
-      CK(eqb::launch_lsqr_normalize(u.p, unL, sc + 0, duL, d, L.mL, nullptr, nullptr, s));
-      L.gather(du.p, true);
-    } else {
-      invariant = true;
+  // One host synchronisation per iteration.  The device runs the first half of
+  // iteration t (B v - alpha u is already there, |u'|, u = u'/beta, B^T u -
+  // beta v, |v'|, v = v'/alpha) with the reference's invariant branches
+  // (:41-52) as device flags: a normalisation whose norm is not positive sets
+  // `inv` and every later step of the iteration is skipped.  The host then
+  // reads beta, alpha, the flag and iteration t-1's residual norm in one copy,
+  // records t-1 (and stops where the reference stops after t-1: tol reached or
+  // invariant), and runs the scalar recurrence with std::hypot exactly as
+  // :58-64 before the x / w update and the fused residual + next B v pass.
+  // A stop found at that point discards only the speculative first half of
+  // iteration t (u, v, not outputs); counts are committed per accepted iteration.
+  if (!M->lsqr_sync) {
+    void* q = nullptr;
+    CK(cudaHostAlloc(&q, sizeof(equil_matrix::LsqrSync), cudaHostAllocDefault));
+    M->lsqr_sync = static_cast<equil_matrix::LsqrSync*>(q);
+  }
+  equil_matrix::LsqrSync* hs = M->lsqr_sync;
+  auto record = [&](double rnorm) -> bool {  // true: stop after this iteration
+    const double rel = rnorm / bnorm;
+    if (st.hist_len < hist_cap) hist[st.hist_len] = rel;
+    ++st.hist_len;
+    if (rel <= tol) {
+      st.reached_tol = true;
+      return true;
     }
-    alpha = 0.0;
-    if (!invariant) {
-      apply_pass(M, true, du.p, vnL, eqb::kPassLsqrV, e, v.p, sc + 0);  // B^T u - beta v
-      ++st.adjoints;
-      L.norm(vn.p, false, sc + 1);
-      alpha = read_scalar(M, sc + 1);
-      if (alpha > 0.0) {
-        CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, nullptr, nullptr, s));
-        L.gather(ev.p, false);
-      } else {
-        invariant = true;
+    return false;
+  };
+  bool prev_invariant = false;
+  for (int t = 1; t <= max_iters; ++t) {
+    // un = Bv - alpha u: computed here for t = 1, afterwards by the fused pass at
+    // the end of the previous iteration (same arithmetic, one A traversal less).
+    // With the pair layout the first one is the fused pass too, its residual
+    // half (b - A 0, into r) discarded.
+    if (t == 1) {
+      if (pair)
+        apply_pass_dual(M, xv.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, nullptr, unL,
+                        eqb::kPassLsqrU, d, u.p, sc + 1, true);
+      else
+        apply_pass(M, false, ev.p, unL, eqb::kPassLsqrU, d, u.p, sc + 1);
+    }
+    CK(cudaMemsetAsync(inv, 0, sizeof(int), s));
+    L.norm(un.p, true, sc + 0);
+    CK(eqb::launch_lsqr_normalize(u.p, unL, sc + 0, duL, d, L.mL, inv, nullptr, s));
+    L.gather(du.p, true);
+    apply_pass(M, true, du.p, vnL, eqb::kPassLsqrV, e, v.p, sc + 0, inv);  // B^T u - beta v
+    L.norm(vn.p, false, sc + 1);
+    CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, inv, inv, s, os));
+    if (!pair) gather_ev();  // pair: travels with e.x below
+    CK(cudaMemcpyAsync(hs, sc, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs->inv, inv, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (t > 1) {  // iteration t-1's residual (:66-78)
+      if (record(hs->rnorm)) return;
+      if (prev_invariant) {
+        st.breakdown = true;
+        return;
       }
     }
+    ++st.applies;
+    beta = hs->beta;
+    const bool u_inv = !(beta > 0.0);
+    alpha = u_inv ? 0.0 : hs->alpha;
+    if (!u_inv) ++st.adjoints;
+    const bool invariant = u_inv || !(alpha > 0.0);
     const double rho = std::hypot(rhobar, beta);  // :58-64
     const double cs = rhobar / rho;
     const double sn = beta / rho;
@@ -2113,25 +2191,24 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     rhobar = -cs * alpha;
     const double phi = cs * phibar;
     phibar = sn * phibar;
-    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, exL, L.nL, s));
-    L.gather(ex.p, false);
+    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, exL, L.nL, s, os));
+    gather_ex();
     st.iterations = t;
     // residual b - A(e.x) and, in the same traversal of A, the next iteration's
     // B v - alpha u (its inputs v, alpha, u are final here; unused if we stop)
-    apply_pass_dual(M, ex.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, ev.p, unL,
-                    eqb::kPassLsqrU, d, u.p, sc + 1);
+    if (pair)
+      apply_pass_dual(M, xv.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, nullptr, unL,
+                      eqb::kPassLsqrU, d, u.p, sc + 1, true);
+    else
+      apply_pass_dual(M, ex.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, ev.p, unL,
+                      eqb::kPassLsqrU, d, u.p, sc + 1);
     L.norm(r.p, true, sc + 2);
-    const double rel = read_scalar(M, sc + 2) / bnorm;
-    if (st.hist_len < hist_cap) hist[st.hist_len] = rel;
-    ++st.hist_len;
-    if (rel <= tol) {
-      st.reached_tol = true;
-      break;
-    }
-    if (invariant) {
-      st.breakdown = true;
-      break;
-    }
+    prev_invariant = invariant;
+  }
+  if (st.iterations > 0) {  // the last iteration's residual
+    const double rnorm = read_scalar(M, sc + 2);
+    if (record(rnorm)) return;
+    if (prev_invariant) st.breakdown = true;
   }
 }
 

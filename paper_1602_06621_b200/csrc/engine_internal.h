@@ -467,6 +467,11 @@ struct equil_matrix {
   DevBuf<double> red_part;
   DevBuf<unsigned> red_counter;
   DevBuf<double> scal;  // small device scalars
+  struct LsqrSync {     // LSQR's per-iteration host read (pinned)
+    double beta, alpha, rnorm;
+    int inv;
+  };
+  LsqrSync* lsqr_sync = nullptr;
   DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
   DevBuf<double> lin_u, lin_v;  // per-coordinate targets (sgd_equilibrate_targets)
 
@@ -499,6 +504,7 @@ struct equil_matrix {
   int last_loop_iters = 0;
 
   ~equil_matrix() {
+    if (lsqr_sync) cudaFreeHost(lsqr_sync);
     if (ev_loop0) cudaEventDestroy(ev_loop0);
     if (ev_loop1) cudaEventDestroy(ev_loop1);
     if (graph) cudaGraphExecDestroy(graph);
@@ -521,7 +527,8 @@ void set_l2_window(equil_matrix* M, cudaStream_t st, const void* base, size_t by
 void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, int kind,
                   double coef = 0.0, bool sqrt_out = false);
 void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
-                const double* scale, const double* prev, const double* coef);
+                const double* scale, const double* prev, const double* coef,
+                const int* skip = nullptr);
 double read_scalar(equil_matrix* M, const double* dev);
 void create_coo_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
                      const int64_t* cols, const double* vals, const int64_t* lines,

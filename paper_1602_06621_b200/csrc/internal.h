@@ -318,6 +318,7 @@ cudaError_t launch_pass_dual(const PassArgs& a, const PassArgs& b, int ntiles, c
 // padded coordinates): lng selects the warp-specialised long-slice kernel;
 // b non-null: the dual pass
 cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArgs& sa, bool lng,
+                             bool pair,
                              cudaStream_t s);
 // tiles [tile_base, tile_base + ntiles); b non-null: the dual pass
 cudaError_t launch_pass_range(const PassArgs& a, const PassArgs* b, int tile_base, int ntiles,
@@ -413,10 +414,11 @@ cudaError_t launch_lsqr_normalize(double* dst, const double* src,
                                   const double* norm_dev, double* scaled_out,
                                   const double* scale, int64_t len,
                                   int* invariant, int* skip_in,
-                                  cudaStream_t s);
+                                  cudaStream_t s, int64_t ostride = 1);
+// ostride: scaled_out / ex element stride (2: one half of an interleaved pair)
 cudaError_t launch_lsqr_xw_update(double* x, double* w, const double* v,
                                   double c1, double c2, const double* e,
-                                  double* ex, int64_t n, cudaStream_t s);
+                                  double* ex, int64_t n, cudaStream_t s, int64_t ostride = 1);
 cudaError_t launch_rms_terms(int mat, const DevCsr& M, const double* eu,
                              const double* ev, double* out, int64_t goff,
                              double target, cudaStream_t s);

@@ -20,6 +20,7 @@
 // sgd_common.cuh) to every row; SgdOp fuses the epilogue instead, SgdBlockOp
 // carries sums between column-block rounds, PassOp<NV> runs the generic passes
 // (LSQR, variants) with one or two gathered vectors.
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -238,6 +239,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // sequential sums per row).
 struct SgdOp {  // the fused u / v update of one SGD iteration
   static constexpr int NV = 1;
+  static constexpr bool PAIR = false;
   SgdIterArgs a;
   __device__ bool skip() const { return false; }
   __device__ const double* x(int mat) const { return mat ? a.xw_cur : a.xs_cur; }
@@ -278,6 +280,7 @@ struct SgdBlockOp : SgdOp {
 template <int NV_>
 struct PassOp {  // generic passes (pass_epilogue); one matrix per launch
   static constexpr int NV = NV_;
+  static constexpr bool PAIR = false;
   PassArgs p, q;
   __device__ bool skip() const { return p.skip && *p.skip; }
   __device__ const double* x(int) const { return p.xg; }
@@ -289,6 +292,26 @@ struct PassOp {  // generic passes (pass_epilogue); one matrix per launch
   }
   __device__ void end(unsigned) const {}
 };
+// LSQR's fused residual + next B v pass with its two gathered vectors stored
+// interleaved (p.xg[2 c] = (e.x)_c, p.xg[2 c + 1] = (e.v)_c): one 16-byte
+// gather (one L2 sector) per entry instead of two 8-byte gathers from two arrays
+struct PassPairOp : PassOp<2> {
+  static constexpr bool PAIR = true;
+};
+
+// the gathered value(s) of slot c: one vector, two vectors, or one interleaved pair
+template <class Op>
+__device__ __forceinline__ void gather_x(const double* __restrict__ x, const double* __restrict__ x2,
+                                         int32_t c, double& g, double& g2) {
+  if constexpr (Op::PAIR) {
+    const double2 p = __ldg(reinterpret_cast<const double2*>(x) + c);
+    g = p.x;
+    g2 = p.y;
+  } else {
+    g = __ldg(x + c);
+    if constexpr (Op::NV == 2) g2 = __ldg(x2 + c);
+  }
+}
 
 __device__ __forceinline__ int slice_at(const SellArgs& sa, int i) {
   return sa.order ? __ldg(sa.order + i) : i;
@@ -319,10 +342,7 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
     double g[B], g2[B];
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (full || k0 + b < len) {
-        g[b] = __ldg(x + c[b]);
-        if constexpr (NV == 2) g2[b] = __ldg(x2 + c[b]);
-      }
+      if (full || k0 + b < len) gather_x<Op>(x, x2, c[b], g[b], g2[b]);
 #pragma unroll
     for (int b = 0; b < B; ++b)
       if (full || k0 + b < len) {
@@ -450,10 +470,7 @@ sell_long_kernel(const Op op, const SellArgs sa) {
       double g[B], g2[B];
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (k0 + b < len) {
-          g[b] = __ldg(x + c[b]);
-          if constexpr (NV == 2) g2[b] = __ldg(x2 + c[b]);
-        }
+        if (k0 + b < len) gather_x<Op>(x, x2, c[b], g[b], g2[b]);
       const int bi = r % R;
       if (r >= R) mbar_wait(&empty[bi], ((r / R) - 1) & 1);
 #pragma unroll
@@ -498,9 +515,15 @@ sell_long_kernel(const Op op, const SellArgs sa) {
 // EQUIL_CARVE_LONG / EQUIL_CARVE_WARP override (-1: the driver's choice).
 template <class K>
 void carveout(K kernel, const char* env, int dflt) {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  // once per (instantiation, device): the attribute is per device context
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (done.fetch_or(bit) & bit) return;
   int pct = dflt;
   if (const char* e = getenv(env)) pct = atoi(e);
   if (pct >= 0) {
@@ -647,10 +670,26 @@ cudaError_t launch_sgd_sell(const SgdIterArgs& a, const SellArgs& sa, int varian
 }
 
 cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArgs& sa, bool lng,
-                             cudaStream_t s) {
+                             bool pair, cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
   static const int pv = getenv("EQUIL_PASS_VARIANT") ? atoi(getenv("EQUIL_PASS_VARIANT")) : 0;
-  if (b) {
+  if (b && pair) {
+    PassPairOp op;
+    op.p = a;
+    op.q = *b;
+    if (lng) {
+      switch (pv) {  // EQUIL_PASS_VARIANT
+        case 1: launch_long<PassPairOp, 4, 15, true, 1>(op, sa, s); break;
+        case 2: launch_long<PassPairOp, 4, 7, true, 2>(op, sa, s); break;
+        default: launch_long<PassPairOp, 2, 15, true, 1>(op, sa, s); break;
+      }
+    } else {
+      switch (pv) {
+        case 4: launch_warp<PassPairOp, 8, true, 6>(op, sa, s); break;
+        default: launch_warp<PassPairOp, 4, true, 6>(op, sa, s); break;
+      }
+    }
+  } else if (b) {
     const PassOp<2> op{a, *b};
     if (lng) {
       switch (pv) {  // EQUIL_PASS_VARIANT; 0 = measured best on c4 (1.82 vs 1.86 ms)

@@ -24,7 +24,7 @@ def main(rep, dst):
     peak = 6443.8
     try:
         peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-                     .get("hbm_copy_GBps", peak))
+                     .get("hbm_gbs", peak))
     except Exception:
         pass
     agg = {}
