@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c4 LSQR and c2 dense keys")
+    ap.add_argument("--ref-iters", type=int, default=3,
+                    help="reference arm: SGD iterations per step (one sgd_equilibrate call)")
     return ap.parse_args()
 
 
@@ -137,6 +140,132 @@ class Clocks:
                 "samples": len(rows)}
 
 
+def workload_config(inst, world: int) -> dict:
+    """config dict shared by both arms (the driver compares them)."""
+    return {"workload": "c3: sparse CSR 2e6 x 1e6, Zipf(1.5) rows on [1,1e4], "
+                        "exp(N(0,1.5)) scalings, T=100, seed 0, auto targets",
+            "m": inst.m, "n": inst.n, "nnz": inst.nnz, "iterations_per_step": inst.iterations,
+            "l2": "inputs larger than L2 (CSR(A)+CSR(A^T) = 3.7 GB >> 126 MB)",
+            "parallelism": f"rows of A and A^T sharded over {world} GPU(s)"}
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+FIXTURE = os.path.join(ROOT, "tests", "golden", "fullsize_c3.json")
+
+
+def sha(a) -> str:
+    import hashlib
+
+    import numpy as np
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def check_vs_fixture(inst, vecs: dict) -> dict:
+    """Compare u, v, d, e of the benched run (c3, T=100, seed 0) with the digest
+    the oracle and the reference's own sources produced (tests/golden/
+    make_fullsize.py); the matrix digest proves it is the same instance."""
+    try:
+        with open(FIXTURE) as f:
+            fx = json.load(f)
+    except OSError:
+        return {"bit_identical_to_oracle": None, "why": "fixture missing"}
+    want = fx["instance"]
+    same_inst = (sha(inst.row_ptr), sha(inst.col), sha(inst.val)) == (
+        want["row_ptr"], want["col"], want["val"])
+    ok = same_inst and inst.iterations == fx["config"]["iterations"] and all(
+        sha(vecs[k]) == fx["result"][k] for k in "uvde")
+    return {"bit_identical_to_oracle": bool(ok), "fixture": "tests/golden/fullsize_c3.json",
+            "same_instance": bool(same_inst)}
+
+
+def lsqr_bytes(inst) -> float:
+    """Bytes one LSQR iteration must move: A and A^T once
+    (24 B/nnz), row pointers, m-side u, d, b read + d.u gathered + u written,
+    n-side v, e, x, w read + e.v, e.x gathered + v, x, w written."""
+    m, n, nnz = inst.m, inst.n, inst.nnz
+    return 24.0 * nnz + 4.0 * (m + n) + 8.0 * (5 * m + 9 * n)
+
+
+def c4_experiment(eq, M, inst, peak: float, curve_every: int = 25) -> dict:
+    """BASELINE configs[3] on the resident c3 matrix: plain lsqr (500) and
+    lsqr_preconditioned (T=50 + 500), tol 0 -- run_lsqr_experiment's two
+    variants (src/experiments.cpp:234-281).  Per-iteration time from the
+    difference of a 500- and a 0-iteration solve; residual curves sampled every
+    `curve_every` iterations; every history entry and x checked against the
+    fixtures tests/golden/fullsize_c4{p,q}.json."""
+    from paper_1602_06621_b200 import configs
+    b = configs.rhs(inst)
+    iters, T = 500, 50
+    pe = eq.EquilibrationParams(iterations=T, seed=0)
+    eq.lsqr(M, b, 2, 0.0)  # warm
+    t0 = time.perf_counter()
+    eq.lsqr(M, b, 0, 0.0)
+    t_zero = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plain = eq.lsqr(M, b, iters, 0.0)
+    t_plain = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pre = eq.lsqr_preconditioned(M, b, pe, iters, 0.0)
+    t_pre = time.perf_counter() - t0
+    per_it = (t_plain - t_zero) / iters
+    B = lsqr_bytes(inst)
+    check = {}
+    for tag, run in (("c4p", plain), ("c4q", pre)):
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", f"fullsize_{tag}.json")) as f:
+                fx = json.load(f)["result"]
+            hist = [float.fromhex(x) for x in fx["residual_history"]]
+            check[tag] = bool(list(run.residual_history) == hist and sha(run.x) == fx["x"])
+        except OSError:
+            check[tag] = None
+
+    def curve(h, offset=0):
+        return {str(k): h[k] for k in range(0, len(h), curve_every)} | {str(len(h) - 1): h[-1]}
+
+    return {"workload": "c4: c3's A, b = A x_true + 0.01 N(0,1); plain lsqr 500 iterations and "
+                        "lsqr_preconditioned T=50 + 500, tol 0",
+            "ms_per_lsqr_iteration": per_it * 1e3,
+            "lsqr_s": {"plain": t_plain, "preconditioned": t_pre, "zero_iterations": t_zero},
+            "roofline": {"bound": "hbm", "bytes_per_iteration": B,
+                         "achieved": B / per_it / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": B / per_it / 1e9 / peak},
+            "residual_vs_total_iteration": {"plain": curve(list(plain.residual_history)),
+                                            f"equil{T}": curve(list(pre.residual_history))},
+            "check": {"bit_identical_to_oracle": check}}
+
+
+def c2_dense(eq, peak: float) -> dict:
+    """BASELINE configs[1]: dense 4096 x 2048, T=100, seed 1 (matrix resident)."""
+    from paper_1602_06621_b200 import configs
+    inst = configs.config(2)
+    D = eq.ExplicitMatrix.dense(inst.dense)
+    p = eq.EquilibrationParams(iterations=inst.iterations, seed=inst.seed)
+    ms = []
+    for _ in range(5):
+        eq.sgd_equilibrate(D, p)
+        ms.append(eq.last_loop_ms(D)[0])
+    D.close()
+    per = statistics.median(ms[1:]) / 1e3 / inst.iterations
+    B = 8.0 * inst.m * inst.n + 48.125 * (inst.m + inst.n)
+    return {"workload": "c2: dense 4096 x 2048 fp64 row-major, T=100, seed 1",
+            "us_per_iteration": per * 1e6, "iterations_per_s": 1.0 / per,
+            "roofline": {"bound": "hbm", "bytes_per_iteration": B, "achieved": B / per / 1e9,
+                         "peak": peak, "unit": "GB/s", "frac": B / per / 1e9 / peak,
+                         "note": "single-pass bytes; A (67 MB) is L2-resident across iterations"}}
+
+
 def cpu_baseline(inst, iters: int):
     import numpy as np  # noqa: F401
     import oracle
@@ -147,7 +276,8 @@ def cpu_baseline(inst, iters: int):
     dt = time.perf_counter() - t0
     return {"value": iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{iters} SGD iterations of the full c3 matrix (oracle/equil_oracle.c, "
-                      f"bit-identical to the reference's sources), 1 thread, {dt:.2f} s"}
+                      f"bit-identical to the reference's sources), 1 thread, {dt:.2f} s",
+            **host_cpu()}
 
 
 def run_ours(args):
@@ -289,13 +419,23 @@ def run_ours(args):
         barrier()
         del r
 
+    extra = {}
+    if world == 1:
+        # the benched result (device buffers of the last timed step) and the e2e
+        # result, against the oracle / reference digest of this exact run
+        vecs = {k: t.cpu().numpy() for k, t in zip("uvde", (u, v, d, e))}
+        check = check_vs_fixture(inst, vecs)
+        check["e2e_bit_identical_to_oracle"] = check_vs_fixture(
+            inst, dict(zip("uvde", pin_out)))["bit_identical_to_oracle"]
+        if not args.no_extras:
+            extra["c4_lsqr"] = c4_experiment(eq, M, inst, peak)
+            extra["c2_dense"] = c2_dense(eq, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(inst, args.cpu_iters)
 
     if rank == 0:
-        if world == 1:
-            check = None
         exchange = eq.exchange_mode(M)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -303,11 +443,7 @@ def run_ours(args):
             "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator restating BASELINE configs[2])",
-            "config": {"workload": "c3: sparse CSR 2e6 x 1e6, Zipf(1.5) rows on [1,1e4], "
-                                   "exp(N(0,1.5)) scalings, T=100, seed 0, auto targets",
-                       "m": inst.m, "n": inst.n, "nnz": inst.nnz, "iterations_per_step": T,
-                       "l2": "inputs larger than L2 (CSR(A)+CSR(A^T) = 3.7 GB >> 126 MB)",
-                       "parallelism": f"rows of A and A^T sharded over {world} GPU(s)"},
+            "config": workload_config(inst, world),
             "ms_per_iteration": elapsed / args.steps / T * 1e3,
             "achieved_GBps": B * value / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -321,7 +457,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
             "flags": {"box_feasible": res.box_feasible, "iterate_bound_ok": res.iterate_bound_ok},
-            "exchange": exchange, "check": check,
+            "exchange": exchange, "check": check, **extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -329,22 +465,45 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def load_instance_without_repo_libs(tmp: str):
+    """c3 generated in a CHILD process (which loads the repo's generator
+    library) and read back here from raw files, so the reference process maps
+    no repo shared object -- only oracle/_ref/libequil_ref.so."""
+    import numpy as np
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); "
+            "from paper_1602_06621_b200 import configs; i = configs.config(%d); "
+            "[np.save(%r + '/' + k + '.npy', getattr(i, k)) for k in ('row_ptr', 'col', 'val')]; "
+            "print(i.m, i.n, i.iterations, i.seed, i.alpha, i.beta)") % (ROOT, CONFIG_ID, tmp)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True)
+    m, n, T, seed, alpha, beta = out.stdout.split()
+
+    class Inst:
+        pass
+    inst = Inst()
+    inst.m, inst.n, inst.iterations, inst.seed = int(m), int(n), int(T), int(seed)
+    inst.alpha, inst.beta = float(alpha), float(beta)
+    for k in ("row_ptr", "col", "val"):
+        setattr(inst, k, np.load(os.path.join(tmp, k + ".npy")))
+    inst.nnz = int(inst.row_ptr[-1])
+    return inst
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import oracle
-    from paper_1602_06621_b200 import configs
     if not os.path.exists(oracle.REF_PATH):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libequil_ref.so was "
                           "not built (needs /root/reference at build time)"}))
         return
-    inst = configs.config(CONFIG_ID)
+    with tempfile.TemporaryDirectory() as tmp:
+        inst = load_instance_without_repo_libs(tmp)
     R = oracle.ref_oracle()
     t0 = time.perf_counter()
     RM = R.matrix(oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val))
     build_s = time.perf_counter() - t0
-    T = 1  # one SGD iteration of the full matrix per step (bounded sample)
+    T = max(1, args.ref_iters)  # SGD iterations of the full matrix per step (bounded sample)
     for _ in range(args.warmup):
         RM.sgd_equilibrate(alpha=inst.alpha, beta=inst.beta, iterations=T, seed=inst.seed)
     t0 = time.perf_counter()
@@ -354,16 +513,18 @@ def run_reference(args):
     value = T * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3 * inst.iterations / T,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator restating BASELINE configs[2])",
-        "config": {"workload": "c3: sparse CSR 2e6 x 1e6, Zipf(1.5) rows on [1,1e4], "
-                               "exp(N(0,1.5)) scalings, T=100, seed 0, auto targets",
-                   "m": inst.m, "n": inst.n, "nnz": inst.nnz},
+        "config": workload_config(inst, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
-                         "sample": f"sgd_equilibrate with T={T} per step on the full c3 matrix; "
-                                   "reference sources (oracle/_ref) on eigen-lite, 1 thread "
-                                   f"(ExplicitMatrix::sparse build {build_s:.1f} s untimed)"},
+                         "sample": f"sgd_equilibrate with T={T} per call on the full c3 matrix "
+                                   f"({args.steps} timed calls; ms_per_step scaled to T="
+                                   f"{inst.iterations}); the reference's sources (oracle/_ref) "
+                                   "on eigen-lite, 1 thread (the reference has no threading; "
+                                   f"ExplicitMatrix::sparse build {build_s:.1f} s untimed)",
+                         **host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

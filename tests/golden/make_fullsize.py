@@ -10,6 +10,9 @@ GPU tests / bench.py compare against them:
   fullsize_c4p.json    config 4 plain lsqr, 500 iterations, tol 0: the whole
                        residual history (exact, float.hex) and SHA-256 of x
   fullsize_c4q.json    config 4 lsqr_preconditioned, T=50, 500 iterations
+  fullsize_c3h.json    config 3, T=20 with diagnostics every 5 iterations: the
+                       per-iteration objective and RMS row/column-norm spread
+                       (src/equilibrate.cpp:174-195, src/metrics.cpp:24-56)
 
 Each part is computed twice, by the C restatement (oracle/liboracle.so) and by
 the reference's own translation units (oracle/_ref/libequil_ref.so, built
@@ -70,7 +73,7 @@ def run_part(part: str, who: str) -> dict:
     import oracle
     from paper_1602_06621_b200 import configs
     t0 = time.time()
-    inst = configs.config(3 if part == "c3" else 4)
+    inst = configs.config(3 if part in ("c3", "c3h") else 4)
     A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
     rec = {"instance": instance_digest(inst), "who": who}
     if who == "ref":
@@ -84,6 +87,16 @@ def run_part(part: str, who: str) -> dict:
         r = (M.sgd_equilibrate(iterations=T_C3, seed=0) if who == "ref"
              else Co.sgd_equilibrate(A, iterations=T_C3, seed=0))
         rec["result"] = scaling_record(r)
+    elif part == "c3h":
+        rec["config"] = {"iterations": 20, "seed": 0, "diag_stride": 5}
+        r = (M.sgd_equilibrate(iterations=20, seed=0, diag_stride=5) if who == "ref"
+             else Co.sgd_equilibrate(A, iterations=20, seed=0, diag_stride=5))
+        rec["result"] = scaling_record(r)
+        # diagnostics do not feed back; compared at 1e-12 relative,
+        # so the two implementations are recorded separately
+        rec["history"] = {"iter": [int(x) for x in r.hist_iter],
+                          "objective": [float(x).hex() for x in r.hist_objective],
+                          "rms": [float(x).hex() for x in r.hist_rms]}
     else:
         b = configs.rhs(inst)
         rec["b"] = sha(b)
@@ -101,7 +114,8 @@ def run_part(part: str, who: str) -> dict:
 
 
 def merge() -> None:
-    names = {"c3": "fullsize_c3.json", "c4p": "fullsize_c4p.json", "c4q": "fullsize_c4q.json"}
+    names = {"c3": "fullsize_c3.json", "c3h": "fullsize_c3h.json",
+             "c4p": "fullsize_c4p.json", "c4q": "fullsize_c4q.json"}
     for part, name in names.items():
         recs = {}
         for who in ("oracle", "ref"):
@@ -119,6 +133,14 @@ def merge() -> None:
         if a.get("b") != b.get("b"):
             raise SystemExit(f"{part}: rhs differs")
         out = {k: a[k] for k in ("instance", "config", "result") if k in a}
+        if "history" in a:
+            ha = [float.fromhex(x) for x in a["history"]["objective"] + a["history"]["rms"]]
+            hb = [float.fromhex(x) for x in b["history"]["objective"] + b["history"]["rms"]]
+            if a["history"]["iter"] != b["history"]["iter"] or any(
+                    abs(x - y) > 1e-12 * max(abs(x), abs(y)) for x, y in zip(ha, hb)):
+                raise SystemExit(f"{part}: histories differ beyond 1e-12")
+            out["history"] = a["history"]
+            out["history_reference"] = b["history"]
         if "b" in a:
             out["b"] = a["b"]
         out["generated_by"] = ("tests/golden/make_fullsize.py: oracle/liboracle.so and "

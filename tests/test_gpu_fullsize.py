@@ -1,0 +1,147 @@
+"""Parity at BASELINE.json's own sizes (GPU, through the C ABI).
+
+The oracle needs minutes per run at these sizes, so configs 3 and 4 compare
+against fixtures committed under tests/golden/ (fullsize_*.json, made by
+tests/golden/make_fullsize.py from BOTH the C restatement and the reference's
+own translation units, which agree bit for bit).  Config 2 (dense 4096x2048)
+runs the oracle live.
+
+  c3  2e6 x 1e6, nnz 1.535e8, T = 100, seed 0: u, v, d, e bit for bit (the
+      benched run itself), through the matrix handle and the one-shot entry
+      (src/equilibrate.cpp:138-221);
+  c3h T = 20 with diagnostics every 5 iterations: the objective / RMS spread
+      history within north_star's 1e-9 relative (src/equilibrate.cpp:174-195);
+  c2  dense, T = 100, seed 1, vs the oracle live (src/explicit_matrix.cpp:69,84
+      in the shim-defined order);
+  c4  plain lsqr (500 iterations) and lsqr_preconditioned (T = 50 + 500) on c3's
+      A: every residual-history entry and x bit for bit (src/lsqr.cpp:85-138).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1602_06621_b200 as eq
+from paper_1602_06621_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def fixture(name):
+    path = os.path.join(GOLD, f"fullsize_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    with open(path) as f:
+        return json.load(f)
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def c3():
+    inst = configs.config(3)
+    M = eq.ExplicitMatrix.from_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    yield inst, M
+    M.close()
+
+
+def check_instance(inst, rec):
+    want = rec["instance"]
+    assert (inst.m, inst.n, inst.nnz) == (want["m"], want["n"], want["nnz"])
+    # the generator on this host produced the matrix the fixture was made from
+    assert sha(inst.row_ptr) == want["row_ptr"]
+    assert sha(inst.col) == want["col"]
+    assert sha(inst.val) == want["val"]
+
+
+def check_scaling(r, want):
+    for k in "uvde":
+        got = getattr(r, k)
+        if sha(got) != want[k]:
+            head = [float.fromhex(x) for x in want["head"][k]]
+            raise AssertionError(f"{k} differs from the oracle (head {got[:4]} vs {head})")
+    assert float(r.alpha).hex() == want["alpha"] and float(r.beta).hex() == want["beta"]
+    assert (r.box_feasible, r.iterate_bound_ok) == (want["box_feasible"],
+                                                    want["iterate_bound_ok"])
+    assert (r.apply_count, r.adjoint_count) == (want["apply_count"], want["adjoint_count"])
+
+
+def test_c3_full_size_T100_bit_exact(c3):
+    inst, M = c3
+    rec = fixture("c3")
+    check_instance(inst, rec)
+    p = eq.EquilibrationParams(iterations=rec["config"]["iterations"], seed=rec["config"]["seed"])
+    check_scaling(eq.sgd_equilibrate(M, p), rec["result"])
+    # again from the captured graph's replay, then through the one-shot entry
+    check_scaling(eq.sgd_equilibrate(M, p), rec["result"])
+    check_scaling(eq.sgd_equilibrate_csr(inst.m, inst.n, inst.row_ptr, inst.col, inst.val, p),
+                  rec["result"])
+
+
+def test_c3_full_size_history_within_tolerance(c3):
+    inst, M = c3
+    rec = fixture("c3h")
+    check_instance(inst, rec)
+    cfg = rec["config"]
+    r = eq.sgd_equilibrate(M, eq.EquilibrationParams(iterations=cfg["iterations"], seed=cfg["seed"]),
+                           eq.DiagnosticsConfig(stride=cfg["diag_stride"]))
+    check_scaling(r, rec["result"])
+    # Diagnostics do not feed back into the trajectory.  The reference sums
+    # 1.5e8 terms sequentially with glibc exp; the device uses det_exp and the
+    # canonical tree, so they agree to the sequential sum's rounding error
+    # (measured <= 4e-11 relative here), inside north_star's 1e-9 bar.  Checked
+    # against both the C restatement's and the reference's own history.
+    for hist in (rec["history"], rec["history_reference"]):
+        assert [x.iter for x in r.history] == hist["iter"]
+        for key, got in (("objective", [x.objective for x in r.history]),
+                         ("rms", [x.rms for x in r.history])):
+            want = np.array([float.fromhex(x) for x in hist[key]])
+            np.testing.assert_allclose(np.array(got), want, rtol=1e-9, atol=0, err_msg=key)
+
+
+def check_lsqr(run, want):
+    hist = [float.fromhex(x) for x in want["residual_history"]]
+    got = list(run.residual_history)
+    assert len(got) == len(hist)
+    bad = [k for k, (a, b) in enumerate(zip(got, hist)) if a != b]
+    assert not bad, f"residual history differs first at entry {bad[0]}: {got[bad[0]]} vs {hist[bad[0]]}"
+    assert sha(run.x) == want["x"], f"x differs (head {run.x[:4]})"
+    assert (run.iterations, run.reached_tol, run.breakdown) == (
+        want["iterations"], want["reached_tol"], want["breakdown"])
+    assert (run.apply_count, run.adjoint_count) == (want["apply_count"], want["adjoint_count"])
+
+
+@pytest.mark.parametrize("part", ["c4p", "c4q"])
+def test_c4_lsqr_500_iterations_bit_exact(c3, part):
+    inst, M = c3
+    rec = fixture(part)
+    check_instance(inst, rec)
+    b = configs.rhs(inst)
+    assert sha(b) == rec["b"]
+    cfg = rec["config"]
+    if part == "c4p":
+        run = eq.lsqr(M, b, cfg["max_iters"], cfg["tol"])
+    else:
+        run = eq.lsqr_preconditioned(M, b, eq.EquilibrationParams(iterations=cfg["iterations"],
+                                                                  seed=cfg["seed"]),
+                                     cfg["max_iters"], cfg["tol"])
+    check_lsqr(run, rec["result"])
+
+
+def test_c2_dense_full_size_T100_vs_oracle(C):
+    import oracle
+    inst = configs.config(2)
+    A = oracle.CsrArrays(inst.m, inst.n, dense=inst.dense)
+    M = eq.ExplicitMatrix.dense(inst.dense)
+    p = eq.EquilibrationParams(iterations=inst.iterations, seed=inst.seed)
+    got = eq.sgd_equilibrate(M, p)
+    want = C.sgd_equilibrate(A, iterations=inst.iterations, seed=inst.seed)
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert (got.box_feasible, got.iterate_bound_ok) == (want.box_feasible, want.iterate_bound_ok)
