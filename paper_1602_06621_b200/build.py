@@ -27,7 +27,7 @@ LIB = os.path.join(HERE, "libequil_b200" + (f"_{TAG}" if TAG else "") + ".so")
 GEN_LIB = os.path.join(HERE, "libequil_gen.so")  # synthetic inputs (bench/tests)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["kernels.cu", "sell.cu", "panel.cu", "variants.cu", "dense.cu", "engine.cu", "engine_ext.cu"]
+CU_SOURCES = ["kernels.cu", "transpose.cu", "sell.cu", "panel.cu", "variants.cu", "dense.cu", "engine.cu", "engine_ext.cu"]
 CXX_SOURCES = ["mt64_host.cpp", "mmio.cpp"]
 HEADERS = ["det_math.cuh", "internal.h", "mt64_host.h", "sgd_common.cuh", "mmio.h",
            "engine_internal.h"]

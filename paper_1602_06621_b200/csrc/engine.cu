@@ -11,6 +11,62 @@
 
 namespace eqe {
 
+// Grow-only mapped pinned staging for h2d's pull copies, one per host thread.
+// A block is reused only by the next setup on the same thread, which starts
+// after the previous one synchronised its stream.
+struct PullArena {
+  struct Block {
+    char* host = nullptr;
+    char* dev = nullptr;
+    size_t cap = 0, used = 0;
+  };
+  std::vector<Block> blocks;
+  ~PullArena() {
+    for (Block& b : blocks) cudaFreeHost(b.host);
+  }
+  char* take(size_t bytes, char** dev) {
+    bytes = (bytes + 255) & ~static_cast<size_t>(255);
+    for (Block& b : blocks)
+      if (b.cap - b.used >= bytes) {
+        *dev = b.dev + b.used;
+        char* h = b.host + b.used;
+        b.used += bytes;
+        return h;
+      }
+    Block b;
+    b.cap = std::max<size_t>(bytes, 32u << 20);
+    void* hp = nullptr;
+    CK(cudaHostAlloc(&hp, b.cap, cudaHostAllocMapped | cudaHostAllocPortable));
+    b.host = static_cast<char*>(hp);
+    void* dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, hp, 0));
+    b.dev = static_cast<char*>(dp);
+    b.used = bytes;
+    blocks.push_back(b);
+    *dev = b.dev;
+    return b.host;
+  }
+};
+static PullArena& pull_arena() {
+  thread_local PullArena a;
+  return a;
+}
+void pull_arena_reset() {
+  for (PullArena::Block& b : pull_arena().blocks) b.used = 0;
+}
+
+void h2d(equil_matrix* M, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  if (!M->pull_uploads) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, M->stream));
+    return;
+  }
+  char* dev = nullptr;
+  char* h = pull_arena().take(bytes, &dev);
+  std::memcpy(h, src, bytes);
+  CK(eqb::launch_pull_copy(dst, dev, bytes, M->stream));
+}
+
 Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   Plan P;
   const int64_t nwin = (rows + eqb::kSliceWindow - 1) / eqb::kSliceWindow;
@@ -281,7 +337,7 @@ void ensure_sell_pass(equil_matrix* M) {
       CK(cudaMemcpyAsync(didx.p, H.midx[mat].data(), H.midx[mat].size() * 4,
                          cudaMemcpyHostToDevice, s));
     const eqb::DevCsr& C = mat ? M->AT : M->A;
-    CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, didx.p,
+    CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, H.kbp[mat].back(), didx.p,
                        static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
                        M->sell_len.p, nullptr, M->sell_pci[mat].p, nullptr, s));
     CK(cudaStreamSynchronize(s));
@@ -387,7 +443,7 @@ void build_sell_blocked(equil_matrix* M) {
                          cudaMemcpyHostToDevice, s));
       CK(cudaMemcpyAsync(didx.p, midx[mat][b].data(), midx[mat][b].size() * 4,
                          cudaMemcpyHostToDevice, s));
-      CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, didx.p,
+      CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, kbp[mat][b].back(), didx.p,
                          static_cast<int>(midx[mat][b].size()),
                          M->sell_bslices.p + static_cast<size_t>(b) * ns, M->sell_row.p,
                          M->sell_bln.p + b * nq, kst.p + b * nq, M->sell_ci[mat].p,
@@ -399,8 +455,35 @@ void build_sell_blocked(equil_matrix* M) {
   M->sell_nb = nbm;
 }
 
-void build_sell_layout(equil_matrix* M) {
+// interleaved arrays of matrix `mat`: columns (mapped to slots) and / or values
+void build_sell_arrays(equil_matrix* M, int mat, bool cols, bool vals) {
+  const equil_matrix::SellHost& H = M->sell_host;
+  cudaStream_t s = M->stream;
+  DevBuf<int64_t> dkbp;
+  DevBuf<int32_t> didx;
+  dkbp.alloc_on(H.kbp[mat].size(), s);
+  didx.alloc_on(H.midx[mat].size(), s);
+  h2d(M, dkbp.p, H.kbp[mat].data(), H.kbp[mat].size() * 8);
+  h2d(M, didx.p, H.midx[mat].data(), H.midx[mat].size() * 4);
+  const eqb::DevCsr& C = mat ? M->AT : M->A;
+  CK(eqb::build_sell(C.row_ptr, C.col, mat ? M->wmap.p : M->smap.p, C.val, dkbp.p,
+                     H.kbp[mat].back(), didx.p,
+                     static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
+                     M->sell_len.p, nullptr, cols ? M->sell_ci[mat].p : nullptr,
+                     vals ? M->sell_va[mat].p : nullptr, s));
+}
+
+// the values half of build_sell_layout(M, false), after A's values (and
+// CSR(A^T)'s) are on the device
+void build_sell_values(equil_matrix* M) {
+  if (!M->sell_values_pending) return;
+  for (int mat = 0; mat < 2; ++mat) build_sell_arrays(M, mat, false, true);
+  M->sell_values_pending = false;
+}
+
+void build_sell_layout(equil_matrix* M, bool with_values) {
   M->sell = false;
+  M->sell_values_pending = false;
   M->sell_nb = 1;
   const bool blocked = M->nblk[0] > 1 || M->nblk[1] > 1;
   if (!M->use_sell || M->use_panels || (!M->slots && !blocked)) return;
@@ -409,20 +492,19 @@ void build_sell_layout(equil_matrix* M) {
   cudaStream_t s = M->stream;
   auto upload = [&](auto& d, const auto& h) {
     d.alloc(h.size());
-    if (!h.empty())
-      CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice, s));
+    h2d(M, d.p, h.data(), h.size() * sizeof(h[0]));
   };
   upload(M->sell_slices, H.slices);
   M->n_sell = static_cast<int>(H.slices.size());
   {  // lane -> row and length, from the device row lists
     DevBuf<int32_t> dr0;
-    upload(dr0, H.r0);
+    dr0.alloc_on(H.r0.size(), s);
+    h2d(M, dr0.p, H.r0.data(), H.r0.size() * 4);
     M->sell_row.alloc(32 * static_cast<size_t>(M->n_sell));
     M->sell_len.alloc(32 * static_cast<size_t>(M->n_sell));
     CK(eqb::launch_sell_rows(M->sell_slices.p, dr0.p, M->n_sell, M->rowlist_a.p,
                              M->rowlist_t.p, M->A.row_ptr, M->AT.row_ptr, M->sell_row.p,
                              M->sell_len.p, s));
-    CK(cudaStreamSynchronize(s));
   }
   M->n_sell_long = 0;
   while (M->n_sell_long < M->n_sell && H.slices[M->n_sell_long].maxlen > eqb::kTileNnz)
@@ -430,17 +512,11 @@ void build_sell_layout(equil_matrix* M) {
   for (int mat = 0; mat < 2 && !blocked; ++mat) {
     M->sell_ci[mat].alloc(H.total[mat]);
     M->sell_va[mat].alloc(H.total[mat]);
-    DevBuf<int64_t> dkbp;
-    DevBuf<int32_t> didx;
-    upload(dkbp, H.kbp[mat]);
-    upload(didx, H.midx[mat]);
-    const eqb::DevCsr& C = mat ? M->AT : M->A;
-    // columns of A index xs (slot map smap), columns of A^T index xw (wmap)
-    CK(eqb::build_sell(C.row_ptr, C.col, mat ? M->wmap.p : M->smap.p, C.val, dkbp.p, didx.p,
-                       static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
-                       M->sell_len.p, nullptr, M->sell_ci[mat].p, M->sell_va[mat].p, s));
-    CK(cudaStreamSynchronize(s));  // before dkbp / didx go
+    // columns of A index xs (slot map smap), columns of A^T index xw (wmap);
+    // the values follow in build_sell_values once they are on the device
+    build_sell_arrays(M, mat, true, with_values);
   }
+  M->sell_values_pending = !blocked && !with_values;
   if (blocked) build_sell_blocked(M);
   if (M->sell_long || M->n_sgd_long == 0) {  // the staged kernel no longer runs
     M->a_ci_sgd.release();
@@ -464,8 +540,7 @@ void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
   tt.insert(tt.end(), pt.slices.begin(), pt.slices.end());
   auto upload = [&](auto& d, const auto& h) {
     d.alloc(h.size());
-    if (!h.empty())
-      CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+    h2d(M, d.p, h.data(), h.size() * sizeof(h[0]));
     return static_cast<int>(h.size());
   };
   M->n_sgd = upload(M->tiles_sgd, sgd);
@@ -709,11 +784,11 @@ void build_slot_layout(equil_matrix* M, const int64_t* rpA_dev, const int64_t* r
   const int64_t* abd = M->a_bounds_d.p;
   const int64_t* tbd = M->t_bounds_d.p;
   if (G == 1) {  // bounds {0, rows}
-    ab.alloc(2);
-    tb.alloc(2);
+    ab.alloc_on(2, s);
+    tb.alloc_on(2, s);
     const int64_t a2[2] = {0, M->m}, t2[2] = {0, M->n};
-    CK(cudaMemcpy(ab.p, a2, 16, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(tb.p, t2, 16, cudaMemcpyHostToDevice));
+    h2d(M, ab.p, a2, 16);
+    h2d(M, tb.p, t2, 16);
     abd = ab.p;
     tbd = tb.p;
   }
@@ -799,7 +874,7 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   build_panel_layout(M, la.data(), lt.data());
   build_block_layout(M);
   build_slot_layout(M, fullA.row_ptr, fullT.row_ptr);
-  build_sell_layout(M);
+  build_sell_layout(M, true);
 }
 
 void alloc_workspaces(equil_matrix* M, PhaseTimer* pt = nullptr);
@@ -842,13 +917,40 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
   } tj{tplanner};
   if (M->world == 1)
     tplanner = std::thread([&] {
-      if (cudaEventSynchronize(ev_rp) == cudaSuccess) planT = plan_tiles(rpT.data(), n, 1);
+      if (cudaEventSynchronize(ev_rp) != cudaSuccess) return;
+      const auto t0 = std::chrono::steady_clock::now();
+      planT = plan_tiles(rpT.data(), n, 1);
+      if (pt.mode == 2)
+        fprintf(stderr, "[equil] plan_tiles(A^T) %.2f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     });
-  CK(eqb::transpose_csr(fullA, fullT, s, M->ev_vals));
-  CK(cudaStreamWaitEvent(s, M->ev_vals, 0));  // every later use of A's values
-  pt.mark(s, "transpose");
+  // K2's structure needs only the columns (and CSR(A^T)'s row pointers, which
+  // the partition plan reads on the host); A's values may still be uploading
   CK(cudaEventSynchronize(ev_rp));
-  pt.mark(s, "rowptr copy");
+  // until the values have arrived, uploads must not queue behind them on the
+  // copy engine: plans go up through pull kernels
+  struct PullScope {
+    equil_matrix* M;
+    explicit PullScope(equil_matrix* m) : M(m) {
+      pull_arena_reset();
+      M->pull_uploads = M->world == 1;
+    }
+    ~PullScope() {
+      M->pull_uploads = false;
+      cudaStreamSynchronize(M->stream);  // nothing may still read the arena
+    }
+  } pull_scope(M);
+  eqb::TransposeWork tw;
+  CK(eqb::transpose_structure(fullA, fullT, rpT.data(), tw, s,
+                              [M](void* d, const void* h, size_t b) { h2d(M, d, h, b); }));
+  pt.mark(s, "transpose");
+  // everything below until the values step reads only row pointers and columns
+  auto values_arrived = [&] {
+    CK(cudaStreamWaitEvent(s, M->ev_vals, 0));  // every later use of A's values
+    CK(eqb::transpose_values(fullA, fullT, tw, s));
+    M->pull_uploads = false;
+    pt.mark(s, "values");
+  };
   if (M->world == 1) {
     // adopt the full arrays as the shard (no copy)
     M->a_bounds = {0, m};
@@ -863,6 +965,8 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     M->t_va.swap(tva);
     M->A = {m, n, nnz, M->a_rp.p, M->a_ci.p, M->a_va.p};
     M->AT = {n, m, nnz, M->t_rp.p, M->t_ci.p, M->t_va.p};
+    fullA = M->A;
+    fullT = M->AT;
     build_block_layout(M);
     build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);  // device work
     if (tplanner.joinable()) tplanner.join();  // planned during the transpose
@@ -874,11 +978,20 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     else
       upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
     pt.mark(s, "upload plans");
+    // values are needed from here on only by the opt-in panel / blocked layouts
+    const bool late_values = !M->use_panels && M->nblk[0] <= 1 && M->nblk[1] <= 1;
+    if (!late_values) values_arrived();
     build_panel_layout(M, row_ptr, rpT.data());
     pt.mark(s, "panels");
-    build_sell_layout(M);
+    build_sell_layout(M, !late_values);
     pt.mark(s, "sell");
+    if (late_values) {
+      values_arrived();
+      build_sell_values(M);
+      pt.mark(s, "sell values");
+    }
   } else {
+    values_arrived();
     const std::vector<int64_t> rpA(row_ptr, row_ptr + m + 1);
     shard_sparse(M, fullA, fullT, rpA, rpT);
   }
@@ -1086,6 +1199,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
       CK(cudaStreamWaitEvent(M->copy_stream, M->ev_vals, 0));
       CK(cudaMemcpyAsync(va.p, val, nnz * 8, cudaMemcpyHostToDevice, M->copy_stream));
       CK(cudaEventRecord(M->ev_vals, M->copy_stream));
+      if (pt.mode == 2) pt.mark(M->copy_stream, "values in");
     } else {
       CK(cudaEventRecord(M->ev_vals, s));
     }
@@ -1099,7 +1213,14 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
         if (t.joinable()) t.join();
       }
     } joiner{planner};
-    if (M->world == 1) planner = std::thread([&] { planA = plan_tiles(row_ptr, m, 0); });
+    if (M->world == 1)
+      planner = std::thread([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        planA = plan_tiles(row_ptr, m, 0);
+        if (pt.mode == 2)
+          fprintf(stderr, "[equil] plan_tiles(A) %.2f ms\n",
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      });
     pt.mark(s, "upload");
     // validation (explicit_matrix.cpp:21-39 for canonical CSR); the deterministic
     // first error: out of range, then duplicate, then unsorted columns

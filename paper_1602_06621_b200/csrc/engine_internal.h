@@ -126,21 +126,59 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
-// EQUIL_VERBOSE=1: per-phase wall times of setup calls (synchronizing; debug only)
+// EQUIL_VERBOSE=1: per-phase wall times of setup calls (synchronizing; debug
+// only).  EQUIL_VERBOSE=2: a non-synchronizing timeline instead -- each mark
+// records the host time and an event on the given stream; at the end every
+// mark prints both, relative to the first (the device times need the events
+// to have completed, so they are printed when the timer goes out of scope).
 struct PhaseTimer {
   const char* what;
-  bool on;
-  std::chrono::steady_clock::time_point t;
+  int mode;
+  std::chrono::steady_clock::time_point t, t0;
+  struct Rec {
+    const char* phase;
+    double host_ms;
+    cudaEvent_t ev;
+  };
+  std::vector<Rec> recs;
+  cudaEvent_t e0 = nullptr;
   explicit PhaseTimer(const char* w)
-      : what(w), on(getenv("EQUIL_VERBOSE") != nullptr), t(std::chrono::steady_clock::now()) {}
+      : what(w), mode(getenv("EQUIL_VERBOSE") ? atoi(getenv("EQUIL_VERBOSE")) : 0),
+        t(std::chrono::steady_clock::now()), t0(t) {
+    if (getenv("EQUIL_VERBOSE") && mode == 0) mode = 1;
+  }
   void mark(cudaStream_t s, const char* phase) {
     nvtxMarkA(phase);
-    if (!on) return;
-    cudaStreamSynchronize(s);
+    if (mode == 0) return;
     const auto now = std::chrono::steady_clock::now();
+    if (mode == 2) {
+      cudaEvent_t e = nullptr;
+      if (!e0) {
+        cudaEventCreate(&e0);
+        cudaEventRecord(e0, s);
+      }
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      recs.push_back({phase, std::chrono::duration<double, std::milli>(now - t0).count(), e});
+      return;
+    }
+    cudaStreamSynchronize(s);
+    const auto after = std::chrono::steady_clock::now();
     fprintf(stderr, "[equil] %s %-14s %8.2f ms\n", what, phase,
-            std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
+            std::chrono::duration<double, std::milli>(after - t).count());
+    t = after;
+  }
+  ~PhaseTimer() {
+    if (mode != 2) return;
+    for (const Rec& r : recs) {
+      float ms = -1.0f;
+      if (cudaEventSynchronize(r.ev) == cudaSuccess) cudaEventElapsedTime(&ms, e0, r.ev);
+      fprintf(stderr, "[equil] %s %-14s host %8.2f ms  device %8.2f ms\n", what, r.phase,
+              r.host_ms, static_cast<double>(ms));
+      cudaEventDestroy(r.ev);
+    }
+    if (e0) cudaEventDestroy(e0);
+    cudaGetLastError();
   }
 };
 
@@ -160,6 +198,10 @@ inline cudaStream_t alloc_stream(int dev) {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t keep = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      // an allocation must never wait on another stream's pending frees (setup
+      // allocates on alloc_stream while the matrix stream is busy)
+      int no = 0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
     cudaGetLastError();
@@ -172,6 +214,16 @@ struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   int dev = -1;         // >= 0: pool allocation on alloc_stream(dev)
+  cudaStream_t own = nullptr;  // alloc_on: stream-ordered on this stream
+  // a temporary used only on stream s (setup): stream-ordered allocation and
+  // free, no synchronisation on either side; s must outlive the buffer
+  void alloc_on(size_t count, cudaStream_t s) {
+    release();
+    if (count == 0) count = 1;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    own = s;
+    n = count;
+  }
   void alloc(size_t count) {
     release();
     if (count == 0) count = 1;
@@ -193,6 +245,13 @@ struct DevBuf {
     if (count > n || !p) alloc(count);
   }
   void release() {
+    if (p && own) {
+      cudaFreeAsync(p, own);
+      p = nullptr;
+      own = nullptr;
+      n = 0;
+      return;
+    }
     if (p) {
       if (dev >= 0) {
         int cur = 0;
@@ -213,6 +272,7 @@ struct DevBuf {
     std::swap(p, o.p);
     std::swap(n, o.n);
     std::swap(dev, o.dev);
+    std::swap(own, o.own);
   }
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
@@ -429,7 +489,8 @@ struct equil_matrix {
   // split epilogue (EQUIL_SPLIT_EPI): row sums to rowacc, then one update pass
   bool split_epi = true;
   DevBuf<double> rowacc;
-  bool sell_passes = true;  // EQUIL_SELL_PASSES=0: generic passes on the staged kernels
+  bool sell_passes = true;
+  bool sell_values_pending = false;  // interleaved values not built yet (setup)  // EQUIL_SELL_PASSES=0: generic passes on the staged kernels
   bool sell_pass = false;
   DevBuf<int32_t> sell_pci[2], sell_pidx[2];
   // column blocks of the gathered vectors (build_block_layout): per matrix
@@ -472,6 +533,7 @@ struct equil_matrix {
     int inv;
   };
   LsqrSync* lsqr_sync = nullptr;
+  bool pull_uploads = false;  // setup: host -> device copies by pull kernels (h2d)
   DevBuf<double> tmp_m, tmp_n, tmp_m2, tmp_n2;
   DevBuf<double> lin_u, lin_v;  // per-coordinate targets (sgd_equilibrate_targets)
 
@@ -530,6 +592,11 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
                 const double* scale, const double* prev, const double* coef,
                 const int* skip = nullptr);
 double read_scalar(equil_matrix* M, const double* dev);
+// host -> device copy on M->stream: a pull kernel from a thread-local mapped
+// pinned arena while M->pull_uploads (setup, A's values on the copy engine),
+// else cudaMemcpyAsync
+void h2d(equil_matrix* M, void* dst, const void* src, size_t bytes);
+void pull_arena_reset();
 void create_coo_impl(int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
                      const int64_t* cols, const double* vals, const int64_t* lines,
                      const equil_device_cfg* cfg, equil_matrix** out);

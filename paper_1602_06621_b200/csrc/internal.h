@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "det_math.cuh"
@@ -149,8 +150,11 @@ struct SellArgs {
 // through map (slots; nullptr: unchanged).  midx: that matrix's slices (indices
 // into slices) in launch order; kbp: prefix of their 32-entry blocks.
 // kst (nullable): each lane's first entry within its row (column blocks).
+// host -> device copy by a kernel reading mapped pinned memory (setup)
+cudaError_t launch_pull_copy(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
+// items: kbp[nmat_slices] (known on the host)
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
-                       const int64_t* kbp, const int32_t* midx, int nmat_slices,
+                       const int64_t* kbp, int64_t items, const int32_t* midx, int nmat_slices,
                        const SellSlice* slices, const int32_t* row, const int32_t* len,
                        const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s);
 // column blocks: per block b and slice lane q, the lane's first entry and
@@ -277,9 +281,32 @@ cudaError_t launch_validate_csr(const DevCsr& A, int* err, unsigned long long* w
 // before the transpose itself
 cudaError_t launch_col_rowptr(const int32_t* col, int64_t nnz, int64_t cols, int64_t* rp,
                               cudaStream_t s);
-// val_ready (optional): event the value gather waits on (values still uploading)
-cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s,
+// K2 (transpose.cu).  transpose_structure needs AT.row_ptr (launch_col_rowptr)
+// and A's columns only: it writes AT.col and records the value permutations in
+// w; transpose_values then moves the values (after they have arrived).
+// transpose_csr = both (val_ready: event the value step waits on).
+struct TransposeWork {
+  int64_t nnz = 0;
+  cudaStream_t stream = nullptr;
+  int32_t* srcT = nullptr;  // source entry of every CSR(A^T) entry
+  TransposeWork() = default;
+  TransposeWork(const TransposeWork&) = delete;
+  TransposeWork& operator=(const TransposeWork&) = delete;
+  ~TransposeWork();
+  void release();
+};
+// rpT_host: CSR(A^T)'s row pointers on the host (the partition plan);
+// upload (optional): the host -> device copy to use for the plan
+using HostUpload = std::function<void(void* dst, const void* src, size_t bytes)>;
+cudaError_t transpose_structure(const DevCsr& A, DevCsr& AT, const int64_t* rpT_host,
+                                TransposeWork& w, cudaStream_t s,
+                                const HostUpload& upload = nullptr);
+cudaError_t transpose_values(const DevCsr& A, DevCsr& AT, TransposeWork& w, cudaStream_t s);
+cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, const int64_t* rpT_host, cudaStream_t s,
                           cudaEvent_t val_ready = nullptr);
+// hand-written exclusive scan (transpose.cu); in == out allowed
+template <class T>
+cudaError_t exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t s);
 // ExplicitMatrix::sparse on device from COO (rows/cols int64, device); out
 // arrays preallocated (row_ptr m+1, col/val nnz).  On a precondition failure
 // *bad_kind = 1 (out of range: *bad = first entry index in input order) or

@@ -336,128 +336,33 @@ cudaError_t launch_validate_csr(const DevCsr& A, int* err, unsigned long long* w
 }
 
 // ---------------------------------------------------------------------------
-// K2: bit-exact transpose.  transposed() emits {j, i, v} in CSR order and
-// sparse() sorts by (j, i); because CSR order is ascending in i, a STABLE sort
-// by column alone yields the identical arrays.
+// Host -> device copy pulled by the SMs from mapped pinned memory: during
+// matrix setup the copy engine is busy with A's values, and a small plan
+// upload queued behind them would wait for the whole transfer.
 // ---------------------------------------------------------------------------
 namespace {
-__global__ void iota_kernel(int32_t* v, int64_t n) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k < n) v[k] = static_cast<int32_t>(k);
-}
-// row index of every entry: each thread binary-searches the row of its first
-// entry, then walks 32 consecutive entries (streaming writes)
-constexpr int kExpand = 32;
-__global__ void expand_rows_kernel(const int64_t* __restrict__ rp, int64_t rows, int64_t nnz,
-                                   int32_t* __restrict__ rowidx) {
-  const int64_t k0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * kExpand;
-  if (k0 >= nnz) return;
-  int64_t lo = 0, hi = rows;  // rp[lo] <= k0 < rp[hi]
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (rp[mid] <= k0) lo = mid; else hi = mid;
-  }
-  int64_t next = rp[lo + 1];
-  const int64_t k1 = imin64(nnz, k0 + kExpand);
-  for (int64_t k = k0; k < k1; ++k) {
-    while (k >= next) next = rp[++lo + 1];  // skips empty rows
-    rowidx[k] = static_cast<int32_t>(lo);
-  }
-}
-__global__ void transpose_gather_kernel(const int32_t* __restrict__ rowidx,
-                                        const double* __restrict__ val,
-                                        const int32_t* __restrict__ perm,
-                                        int64_t nnz, int32_t* __restrict__ tcol,
-                                        double* __restrict__ tval) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (p >= nnz) return;
-  const int64_t k = perm[p];
-  tcol[p] = rowidx[k];
-  tval[p] = val[k];
-}
-__global__ void transpose_rowptr_kernel(const int32_t* __restrict__ skey, int64_t nnz,
-                                        int64_t cols, int64_t* __restrict__ trp) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (p > nnz) return;
-  const int64_t prev = (p == 0) ? -1 : skey[p - 1];
-  const int64_t cur = (p == nnz) ? cols : skey[p];
-  for (int64_t j = prev + 1; j <= cur && j <= cols; ++j) trp[j] = p;
+__global__ void pull_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                 int64_t n16, unsigned char* __restrict__ dtail,
+                                 const unsigned char* __restrict__ stail, int tail) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t k = t0; k < n16; k += stride) dst[k] = src[k];
+  if (t0 < tail) dtail[t0] = stail[t0];
 }
 }  // namespace
 
-namespace {
-__global__ void col_count_kernel(const int32_t* __restrict__ col, int64_t nnz,
-                                 unsigned long long* __restrict__ cnt) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k < nnz) atomicAdd(cnt + col[k] + 1, 1ull);
-}
-}  // namespace
-
-cudaError_t launch_col_rowptr(const int32_t* col, int64_t nnz, int64_t cols, int64_t* rp,
-                              cudaStream_t s) {
-  void* temp = nullptr;
-  size_t tb = 0;
-  cudaError_t e = cudaMemsetAsync(rp, 0, (cols + 1) * 8, s);
-  if (e) return e;
-  if (nnz > 0) {
-    col_count_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
-        col, nnz, reinterpret_cast<unsigned long long*>(rp));
-    count_launch(s);
-  }
-  e = cub::DeviceScan::InclusiveSum(nullptr, tb, rp, rp, cols + 1, s);
-  if (e) return e;
-  e = cudaMallocAsync(&temp, tb, s);
-  if (e) return e;
-  e = cub::DeviceScan::InclusiveSum(temp, tb, rp, rp, cols + 1, s);
-  cudaFreeAsync(temp, s);
-  return e;
-}
-
-cudaError_t transpose_csr(const DevCsr& A, DevCsr& AT, cudaStream_t s, cudaEvent_t val_ready) {
-  const int64_t nnz = A.nnz;
-  AT.rows = A.cols;
-  AT.cols = A.rows;
-  AT.nnz = nnz;
-  if (nnz >= (1LL << 31)) return cudaErrorInvalidValue;
-  int32_t *perm_in = nullptr, *perm_out = nullptr, *keys_out = nullptr;
-  void* temp = nullptr;
-  size_t temp_bytes = 0;
-  const int end_bit = std::max(1, ceil_log2(static_cast<uint64_t>(A.cols) + 1));
-  cudaError_t e = cudaSuccess;
-  do {
-    if (nnz > 0) {
-      e = cudaMallocAsync(&perm_in, nnz * sizeof(int32_t), s); if (e) break;
-      e = cudaMallocAsync(&perm_out, nnz * sizeof(int32_t), s); if (e) break;
-      e = cudaMallocAsync(&keys_out, nnz * sizeof(int32_t), s); if (e) break;
-      iota_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(perm_in, nnz); count_launch(s);
-      e = cudaGetLastError(); if (e) break;
-      e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, A.col, keys_out, perm_in,
-                                          perm_out, nnz, 0, end_bit, s);
-      if (e) break;
-      e = cudaMallocAsync(&temp, temp_bytes, s); if (e) break;
-      e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, A.col, keys_out, perm_in,
-                                          perm_out, nnz, 0, end_bit, s);
-      if (e) break;
-      // perm_in is free once the sort has run: reuse it for the row index of each entry
-      const int64_t nexp = (nnz + kExpand - 1) / kExpand;
-      expand_rows_kernel<<<static_cast<unsigned>((nexp + 255) / 256), 256, 0, s>>>(
-          A.row_ptr, A.rows, nnz, perm_in); count_launch(s);
-      if (val_ready) {
-        e = cudaStreamWaitEvent(s, val_ready, 0); if (e) break;
-      }
-      transpose_gather_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(
-          perm_in, A.val, perm_out, nnz, AT.col, AT.val); count_launch(s);
-      e = cudaGetLastError(); if (e) break;
-    }
-    transpose_rowptr_kernel<<<static_cast<unsigned>((nnz + 1 + 255) / 256), 256, 0, s>>>(
-        keys_out, nnz, A.cols, AT.row_ptr); count_launch(s);
-    e = cudaGetLastError();
-  } while (0);
-  if (temp) cudaFreeAsync(temp, s);
-  if (perm_in) cudaFreeAsync(perm_in, s);
-  if (perm_out) cudaFreeAsync(perm_out, s);
-  if (keys_out) cudaFreeAsync(keys_out, s);
-  return e;
+cudaError_t launch_pull_copy(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  // both 16-byte aligned (pool / arena allocations)
+  const int64_t n16 = static_cast<int64_t>(bytes / 16);
+  const int tail = static_cast<int>(bytes % 16);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, 1184));
+  pull_copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+      static_cast<uint4*>(dst), static_cast<const uint4*>(src_mapped), n16,
+      static_cast<unsigned char*>(dst) + n16 * 16,
+      static_cast<const unsigned char*>(src_mapped) + n16 * 16, tail);
+  count_launch(s);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

@@ -69,11 +69,11 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
       const int ln = __shfl_sync(0xffffffffu, mylen, r0 + j);
       ok[j] = r0 + j < sd.cnt && k < ln;
       if (ok[j]) {
-        c[j] = ci[st + k];
+        if (oc) c[j] = ci[st + k];
         if (ov) v[j] = val[st + k];
       }
     }
-    if (map) {
+    if (map && oc) {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (ok[j]) c[j] = map[c[j]];
@@ -81,7 +81,7 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (ok[j]) {
-        tc[warp][lane][r0 + j] = c[j];
+        if (oc) tc[warp][lane][r0 + j] = c[j];
         if (ov) tv[warp][lane][r0 + j] = v[j];
       }
   }
@@ -90,7 +90,7 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
   for (int kk = 0; kk < kend; ++kk) {
     const int64_t dst = sd.off + static_cast<int64_t>(k0 + kk) * 32 + lane;
     const bool ok = lane < sd.cnt && k0 + kk < mylen;
-    oc[dst] = ok ? tc[warp][kk][lane] : 0;
+    if (oc) oc[dst] = ok ? tc[warp][kk][lane] : 0;
     if (ov) ov[dst] = ok ? tv[warp][kk][lane] : 0.0;
   }
 }
@@ -555,15 +555,10 @@ void launch_warp(const Op& op, const SellArgs& sa, cudaStream_t s) {
 }  // namespace
 
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
-                       const int64_t* kbp, const int32_t* midx, int nmat_slices,
+                       const int64_t* kbp, int64_t items, const int32_t* midx, int nmat_slices,
                        const SellSlice* slices, const int32_t* row, const int32_t* len,
                        const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s) {
-  if (nmat_slices == 0) return cudaSuccess;
-  int64_t items = 0;
-  cudaError_t e = cudaMemcpyAsync(&items, kbp + nmat_slices, sizeof items,
-                                  cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess || items == 0) return e;
+  if (nmat_slices == 0 || items == 0) return cudaSuccess;
   build_sell_kernel<<<static_cast<unsigned>((items + 1) / 2), 64, 0, s>>>(
       rp, ci, map, val, kbp, midx, nmat_slices, slices, row, len, kst, out_ci, out_va);
   count_launch(s);

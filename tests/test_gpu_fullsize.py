@@ -145,3 +145,16 @@ def test_c2_dense_full_size_T100_vs_oracle(C):
     for k in "uvde":
         assert np.array_equal(getattr(got, k), getattr(want, k)), k
     assert (got.box_feasible, got.iterate_bound_ok) == (want.box_feasible, want.iterate_bound_ok)
+
+
+def test_c3_transpose_bit_exact_vs_oracle(c3, C):
+    """K2 at full size: CSR(A^T) of the benched matrix equals the oracle's
+    restatement of ExplicitMatrix::transposed() (src/explicit_matrix.cpp:117-125)
+    array for array."""
+    import oracle
+    inst, M = c3
+    trp, tc, tv = M.transposed_csr()
+    want = C.transpose(oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val))
+    assert np.array_equal(trp, want.row_ptr)
+    assert np.array_equal(tc, want.col)
+    assert np.array_equal(tv, want.val)
