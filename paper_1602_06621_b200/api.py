@@ -131,7 +131,18 @@ class ExplicitMatrix:
         """Canonical CSR (columns strictly ascending per row); validated and
         transposed on the device."""
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
-        ci = np.ascontiguousarray(col, dtype=np.int32)
+        c_in = np.asarray(col)
+        if c_in.dtype != np.int32 and c_in.size:
+            # wider indices must not wrap into range on the int32 cast: report
+            # the first out-of-range entry as ExplicitMatrix::sparse does
+            # (src/explicit_matrix.cpp:23-28)
+            bad = np.flatnonzero((c_in < 0) | (c_in >= cols))
+            if bad.size:
+                k = int(bad[0])
+                i = int(np.searchsorted(rp, k, side="right")) - 1
+                raise InvalidArgument(f"ExplicitMatrix::sparse: entry ({i}, {int(c_in[k])}) "
+                                      "out of range")
+        ci = np.ascontiguousarray(c_in, dtype=np.int32)
         va = np.ascontiguousarray(val, dtype=np.float64)
         if rp.size != rows + 1 and rows > 0:
             raise InvalidArgument("ExplicitMatrix::sparse: row_ptr must have rows + 1 entries")

@@ -9,6 +9,13 @@
 // variants, the lasso, the public helpers and file I/O are in engine_ext.cu.
 #include "engine_internal.h"
 
+#include <fcntl.h>
+#include <pthread.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <atomic>
+
 namespace eqe {
 
 // Grow-only mapped pinned staging for h2d's pull copies, one per host thread.
@@ -247,7 +254,9 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (M->world > 1) {
     require(cfg->nccl_id != nullptr, "device cfg: world_size > 1 needs nccl_id");
     const char* hxe = getenv("EQUIL_HOST_EXCHANGE");
-    if (hxe && atoi(hxe) != 0) {  // test transport (HostExchange), no NCCL
+    if (hxe && atoi(hxe) == 2) {  // processes, shared memory + CUDA IPC, no NCCL
+      M->hx = shm_exchange(cfg->nccl_id, M->world, M->rank);
+    } else if (hxe && atoi(hxe) != 0) {  // test transport (ThreadExchange), no NCCL
       M->hx = host_exchange(cfg->nccl_id, M->world);
     } else {
       if (!nccl().ok) fail(EQUIL_ENCCL, "libnccl.so.2 could not be loaded");
@@ -558,13 +567,13 @@ void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
   if (M->hx) {  // host exchange: own slice out, barrier, peers' slices in, barrier
     const size_t bytes = static_cast<size_t>(maxcnt) * 8;
     CK(cudaStreamSynchronize(M->stream));
-    std::vector<char>& mine = M->hx->slot[M->rank];
-    mine.resize(bytes);
+    std::vector<char> mine(bytes);
     if (bytes) CK(cudaMemcpy(mine.data(), buf + M->rank * maxcnt, bytes, cudaMemcpyDeviceToHost));
+    M->hx->put(M->rank, mine.data(), bytes);
     M->hx->barrier();
     for (int g = 0; g < M->world; ++g)
       if (g != M->rank && bytes)
-        CK(cudaMemcpy(buf + g * maxcnt, M->hx->slot[g].data(), bytes, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(buf + g * maxcnt, M->hx->slot(g), bytes, cudaMemcpyHostToDevice));
     M->hx->barrier();
     return;
   }
@@ -588,91 +597,188 @@ static int64_t elem_delta(const void* peer, const double* mine) {
          static_cast<int64_t>(sizeof(double));
 }
 
+// Cross-process host exchange (EQUIL_HOST_EXCHANGE=2): one POSIX shared-memory
+// segment per communicator id -- a header with a process-shared barrier, then
+// one slot of EQUIL_SHM_SLOT_MB (default 8) per rank.  Rank 0 initialises the
+// header; the others wait for its magic word.  The name is unlinked once every
+// rank has attached (the mappings stay valid).
+struct ShmExchange : HostExchange {
+  struct Header {
+    std::atomic<unsigned long long> magic;
+    pthread_barrier_t bar;
+    int world;
+    size_t cap;
+  };
+  static constexpr unsigned long long kMagic = 0x6571756c73686d31ULL;  // "equlshm1"
+  Header* h = nullptr;
+  char* base = nullptr;
+  size_t total = 0;
+  size_t cap = 0;
+  std::string name;
+  ShmExchange(const void* id128, int world_, int rank) {
+    world = world_;
+    const unsigned char* id = static_cast<const unsigned char*>(id128);
+    uint64_t hsh = 1469598103934665603ULL;  // FNV-1a of the id
+    for (int k = 0; k < 128; ++k) hsh = (hsh ^ id[k]) * 1099511628211ULL;
+    char nm[64];
+    snprintf(nm, sizeof nm, "/equil_%016llx", static_cast<unsigned long long>(hsh));
+    name = nm;
+    double mb = 8.0;
+    if (const char* e = getenv("EQUIL_SHM_SLOT_MB")) mb = std::max(0.001, atof(e));
+    cap = static_cast<size_t>(mb * (1 << 20));
+    total = 4096 + cap * world;
+    const int fd = shm_open(name.c_str(), O_CREAT | O_RDWR, 0600);
+    if (fd < 0) fail(EQUIL_ERUNTIME, "host exchange: shm_open failed");
+    if (ftruncate(fd, static_cast<off_t>(total)) != 0) {
+      close(fd);
+      fail(EQUIL_ERUNTIME, "host exchange: ftruncate failed");
+    }
+    void* p = mmap(nullptr, total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) fail(EQUIL_ERUNTIME, "host exchange: mmap failed");
+    h = static_cast<Header*>(p);
+    base = static_cast<char*>(p) + 4096;
+    if (rank == 0) {
+      pthread_barrierattr_t at;
+      pthread_barrierattr_init(&at);
+      pthread_barrierattr_setpshared(&at, PTHREAD_PROCESS_SHARED);
+      pthread_barrier_init(&h->bar, &at, static_cast<unsigned>(world));
+      pthread_barrierattr_destroy(&at);
+      h->world = world;
+      h->cap = cap;
+      h->magic.store(kMagic, std::memory_order_release);
+    } else {
+      for (int k = 0; h->magic.load(std::memory_order_acquire) != kMagic; ++k) {
+        if (k > 600000) fail(EQUIL_ERUNTIME, "host exchange: rank 0 never attached");
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+      }
+    }
+    barrier();
+    if (rank == 0) shm_unlink(name.c_str());
+  }
+  ~ShmExchange() override {
+    if (h) munmap(h, total);
+  }
+  void barrier() override { pthread_barrier_wait(&h->bar); }
+  void put(int rank, const void* data, size_t bytes) override {
+    if (bytes > cap) fail(EQUIL_ERUNTIME, "host exchange: slot too small (EQUIL_SHM_SLOT_MB)");
+    std::memcpy(base + rank * cap, data, bytes);
+  }
+  const char* slot(int g) override { return base + g * cap; }
+  bool in_process() const override { return false; }
+};
+
+std::shared_ptr<HostExchange> shm_exchange(const void* id128, int world, int rank) {
+  return std::make_shared<ShmExchange>(id128, world, rank);
+}
+
+// bytes of every rank, in rank order, through the handle's transport
+static std::vector<char> allgather_bytes(equil_matrix* M, const void* mine, size_t bytes) {
+  const int G = M->world;
+  std::vector<char> all(G * bytes);
+  if (M->hx) {
+    M->hx->put(M->rank, mine, bytes);
+    M->hx->barrier();
+    for (int g = 0; g < G; ++g) std::memcpy(all.data() + g * bytes, M->hx->slot(g), bytes);
+    M->hx->barrier();
+    return all;
+  }
+  DevBuf<char> buf;
+  buf.alloc(G * bytes);
+  cudaStream_t s = M->stream;
+  CK(cudaMemcpyAsync(buf.p + M->rank * bytes, mine, bytes, cudaMemcpyHostToDevice, s));
+  nccl_check(nccl().AllGather(buf.p + M->rank * bytes, buf.p, bytes, ncclUint8, M->comm, s),
+             "ncclAllGather");
+  CK(cudaMemcpyAsync(all.data(), buf.p, G * bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return all;
+}
+
 void setup_peers(equil_matrix* M) {
   M->p2p_state = -1;
   const int G = M->world, r = M->rank;
   int want = (!M->use_panels && !M->dense && G - 1 <= EQ_MAX_PEERS) ? 1 : 0;
   if (const char* e = getenv("EQUIL_P2P")) want = want && atoi(e) != 0;
-  std::vector<int64_t> delta;
-  if (M->hx) {
-    struct Rec {
-      int ok;
-      double* base;
-    } mine{want, M->xbuf.p};
-    CK(cudaStreamSynchronize(M->stream));
-    M->hx->slot[r].assign(reinterpret_cast<char*>(&mine), reinterpret_cast<char*>(&mine + 1));
-    M->hx->barrier();
-    bool ok = true;
-    std::vector<Rec> all(G);
-    for (int g = 0; g < G; ++g) {
-      std::memcpy(&all[g], M->hx->slot[g].data(), sizeof(Rec));
-      ok = ok && all[g].ok;
-    }
-    M->hx->barrier();
-    if (!ok) return;
-    for (int g = 0; g < G; ++g)
-      if (g != r) delta.push_back(elem_delta(all[g].base, M->xbuf.p));
-  } else {
-    struct Rec {
-      int32_t ok;
-      int32_t pad;
-      cudaIpcMemHandle_t h;
-    } mine{};
-    mine.ok = want && cudaIpcGetMemHandle(&mine.h, M->xbuf.p) == cudaSuccess;
+  CK(cudaStreamSynchronize(M->stream));
+  const bool local = M->hx && M->hx->in_process();
+  struct Rec {
+    int32_t ok;
+    int32_t pad;
+    double* base;  // in-process transport: the buffer itself
+    cudaIpcMemHandle_t h;
+  } mine{};
+  mine.ok = want;
+  mine.base = M->xbuf.p;
+  if (want && !local) {
+    mine.ok = cudaIpcGetMemHandle(&mine.h, M->xbuf.p) == cudaSuccess;
     cudaGetLastError();
-    DevBuf<char> buf;
-    buf.alloc(G * sizeof(Rec));
-    cudaStream_t s = M->stream;
-    CK(cudaMemcpyAsync(buf.p + r * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, s));
-    nccl_check(nccl().AllGather(buf.p + r * sizeof(Rec), buf.p, sizeof(Rec), ncclUint8, M->comm, s),
-               "ncclAllGather");
-    std::vector<Rec> all(G);
-    CK(cudaMemcpyAsync(all.data(), buf.p, G * sizeof(Rec), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    bool ok = true;
-    for (const Rec& x : all) ok = ok && x.ok;
-    if (!ok) return;  // every rank saw the same records
-    unsigned opened = 1;
-    for (int g = 0; g < G; ++g) {
-      if (g == r) continue;
-      void* q = nullptr;
-      if (cudaIpcOpenMemHandle(&q, all[g].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
-        M->peer_mapped.push_back(q);
-        delta.push_back(elem_delta(q, M->xbuf.p));
-      } else {
-        opened = 0;
-      }
-      cudaGetLastError();
+  }
+  std::vector<char> raw = allgather_bytes(M, &mine, sizeof mine);
+  std::vector<Rec> all(G);
+  std::memcpy(all.data(), raw.data(), G * sizeof(Rec));
+  bool ok = true;
+  for (const Rec& x : all) ok = ok && x.ok;
+  if (!ok) return;  // every rank saw the same records
+  std::vector<int64_t> delta;
+  unsigned opened = 1;
+  for (int g = 0; g < G; ++g) {
+    if (g == r) continue;
+    if (local) {
+      delta.push_back(elem_delta(all[g].base, M->xbuf.p));
+      continue;
     }
-    DevBuf<unsigned> w;  // every rank must have mapped every peer
-    w.alloc(1);
-    CK(cudaMemcpyAsync(w.p, &opened, sizeof opened, cudaMemcpyHostToDevice, s));
-    nccl_check(nccl().AllReduce(w.p, w.p, 1, ncclUint32, ncclMin, M->comm, s), "ncclAllReduce");
-    CK(cudaMemcpyAsync(&opened, w.p, sizeof opened, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (!opened) {
-      for (void* q : M->peer_mapped) cudaIpcCloseMemHandle(q);
-      M->peer_mapped.clear();
-      return;
+    void* q = nullptr;
+    if (cudaIpcOpenMemHandle(&q, all[g].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+      M->peer_mapped.push_back(q);
+      delta.push_back(elem_delta(q, M->xbuf.p));
+    } else {
+      opened = 0;
     }
+    cudaGetLastError();
+  }
+  // every rank must have mapped every peer
+  raw = allgather_bytes(M, &opened, sizeof opened);
+  for (int g = 0; g < G; ++g) {
+    unsigned v = 0;
+    std::memcpy(&v, raw.data() + g * sizeof v, sizeof v);
+    opened = opened && v;
+  }
+  if (!opened) {
+    for (void* q : M->peer_mapped) cudaIpcCloseMemHandle(q);
+    M->peer_mapped.clear();
+    return;
   }
   M->peer_delta = delta;
   M->bar.alloc(1);
-  CK(cudaMemset(M->bar.p, 0, sizeof(unsigned)));
+  CK(cudaMemsetAsync(M->bar.p, 0, sizeof(unsigned), M->stream));
+  CK(cudaMemsetAsync(M->xbar(), 0, eqb::kBarWords * sizeof(unsigned long long), M->stream));
+  CK(cudaStreamSynchronize(M->stream));
+  allgather_bytes(M, &opened, sizeof opened);  // no rank signals before all flags are zero
   M->p2p_state = 1;
 }
 
 // End of a fused-all-gather iteration: no rank starts iteration t+1 (which
 // overwrites the buffers its peers read in iteration t) before every rank's
-// passes and peer stores of iteration t are complete.
+// passes and peer stores of iteration t are complete.  Host transports: a host
+// barrier.  NCCL: a device flag barrier on the peer-mapped buffers
+// (peer_barrier_kernel: release-store of the epoch into every peer's flag for
+// this rank, acquire-spin on the own flags), graph-capturable and without a
+// collective; EQUIL_P2P_BARRIER=nccl keeps a one-word ncclAllReduce instead.
 void rank_barrier(equil_matrix* M) {
   if (M->hx) {
     CK(cudaStreamSynchronize(M->stream));
     M->hx->barrier();
     return;
   }
-  nccl_check(nccl().AllReduce(M->bar.p, M->bar.p, 1, ncclUint32, ncclMax, M->comm, M->stream),
-             "ncclAllReduce");
+  static const bool use_nccl = getenv("EQUIL_P2P_BARRIER") &&
+                               std::string(getenv("EQUIL_P2P_BARRIER")) == "nccl";
+  if (use_nccl) {
+    nccl_check(nccl().AllReduce(M->bar.p, M->bar.p, 1, ncclUint32, ncclMax, M->comm, M->stream),
+               "ncclAllReduce");
+    return;
+  }
+  CK(eqb::launch_peer_barrier(M->xbar(), M->rank, M->world, M->peer_delta.data(),
+                              static_cast<int>(M->peer_delta.size()), M->stream));
 }
 
 // Bands for the column-panel traversal: consecutive rows, closed before a row
@@ -1027,14 +1133,18 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   // each vector padded to whole panels (the panel traversal bulk-copies them)
   auto whole = [](int64_t x) { return (x + eqb::kPanelW - 1) / eqb::kPanelW * eqb::kPanelW; };
   const int64_t np = whole(M->n_pad()), mp = whole(M->m_pad());
-  if (M->world > 1 && !M->hx) {  // pool memory cannot be exported over CUDA IPC
+  // the gathered vectors, then the device barrier words (fused all-gather)
+  const int64_t xlen = 2 * (np + mp) + eqb::kBarWords;
+  M->xbar_off = 2 * (np + mp);
+  if (M->world > 1 && !(M->hx && M->hx->in_process())) {
+    // pool memory cannot be exported over CUDA IPC
     double* q = nullptr;
-    CK(cudaMalloc(&q, 2 * (np + mp) * sizeof(double)));
-    M->xbuf.adopt(q, 2 * (np + mp));
+    CK(cudaMalloc(&q, xlen * sizeof(double)));
+    M->xbuf.adopt(q, xlen);
   } else {
-    M->xbuf.alloc(2 * (np + mp));
+    M->xbuf.alloc(xlen);
   }
-  CK(cudaMemset(M->xbuf.p, 0, 2 * (np + mp) * sizeof(double)));
+  CK(cudaMemset(M->xbuf.p, 0, xlen * sizeof(double)));
   if (pt) pt->mark(M->stream, "xbuf");
   for (int b = 0; b < 2; ++b) {
     M->xs[b].p = M->xbuf.p + b * np;
@@ -1746,7 +1856,10 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               sa.ci[k] = M->sell_ci[k].p;
               sa.va[k] = M->sell_va[k].p;
             }
-            if (M->split_epi && M->sell_nb == 1 && M->sell_long == 2) {
+            // with peer stores (p2p) the fused epilogue sends each row's next
+            // value as soon as its sum is done, overlapping the exchange with
+            // the passes; the split epilogue would send them all afterwards
+            if (M->split_epi && M->sell_nb == 1 && M->sell_long == 2 && !p2p) {
               // row sums from both kernels (concurrent), then one update pass
               a.carry[0] = M->rowacc.p;
               a.carry[1] = M->rowacc.p + M->m_loc();
@@ -1892,18 +2005,23 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
     double* eloc = M->tmp_n.p;
     CK(eqb::launch_exp(M->ub.p, dloc, ml, 1.0, s));
     CK(eqb::launch_exp(M->vb.p, eloc, nl, 1.0, s));
+    if (p2p && !M->hx) {  // a timed-out device barrier leaves the ranks out of step
+      unsigned long long err = 0;
+      CK(cudaMemcpyAsync(&err, M->xbar() + eqb::kBarError, sizeof err, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (err) fail(EQUIL_ERUNTIME, "sgd_equilibrate: peer barrier timed out (a rank stalled)");
+    }
     unsigned flags = 0;
     if (M->world > 1 && M->hx) {  // host exchange: max of the flag words
       unsigned mine = 0;
       CK(cudaMemcpyAsync(&mine, M->flags.p, sizeof mine, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      M->hx->slot[M->rank].assign(reinterpret_cast<char*>(&mine),
-                                  reinterpret_cast<char*>(&mine) + sizeof mine);
+      M->hx->put(M->rank, &mine, sizeof mine);
       M->hx->barrier();
       unsigned all = 0;
       for (int g = 0; g < M->world; ++g) {
         unsigned v = 0;
-        std::memcpy(&v, M->hx->slot[g].data(), sizeof v);
+        std::memcpy(&v, M->hx->slot(g), sizeof v);
         all |= v;
       }
       M->hx->barrier();

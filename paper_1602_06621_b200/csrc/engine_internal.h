@@ -359,14 +359,28 @@ namespace eqe {
 // condition variable, slices passed through host buffers.  No kernel ever
 // waits on another rank; the sharded engine's index arithmetic, padding and
 // reductions run exactly as with NCCL.
+// Host-side exchange among the ranks of a sharded matrix for tests and
+// single-GPU runs of the sharded engine (no NCCL): put() publishes this rank's
+// bytes, barrier(), then slot(g) reads rank g's.  ThreadExchange: ranks are
+// threads of one process (EQUIL_HOST_EXCHANGE=1).  ShmExchange: ranks are
+// processes (EQUIL_HOST_EXCHANGE=2), POSIX shared memory + a process-shared
+// barrier; peers' gathered-vector buffers are then mapped over CUDA IPC, as
+// they are with NCCL.
 struct HostExchange {
   int world = 0;
+  virtual ~HostExchange() = default;
+  virtual void barrier() = 0;
+  virtual void put(int rank, const void* data, size_t bytes) = 0;
+  virtual const char* slot(int g) = 0;
+  virtual bool in_process() const = 0;
+};
+struct ThreadExchange : HostExchange {
   std::mutex mu;
   std::condition_variable cv;
   int arrived = 0;
   long long gen = 0;
-  std::vector<std::vector<char>> slot;
-  void barrier() {
+  std::vector<std::vector<char>> slots;
+  void barrier() override {
     std::unique_lock<std::mutex> lk(mu);
     const long long g = gen;
     if (++arrived == world) {
@@ -377,7 +391,13 @@ struct HostExchange {
       cv.wait(lk, [&] { return gen != g; });
     }
   }
+  void put(int rank, const void* data, size_t bytes) override {
+    slots[rank].assign(static_cast<const char*>(data), static_cast<const char*>(data) + bytes);
+  }
+  const char* slot(int g) override { return slots[g].data(); }
+  bool in_process() const override { return true; }
 };
+std::shared_ptr<HostExchange> shm_exchange(const void* id128, int world, int rank);
 inline std::shared_ptr<HostExchange> host_exchange(const void* id128, int world) {
   static std::mutex mu;
   static std::map<std::string, std::weak_ptr<HostExchange>> reg;
@@ -385,9 +405,10 @@ inline std::shared_ptr<HostExchange> host_exchange(const void* id128, int world)
   const std::string key(static_cast<const char*>(id128), 128);
   auto hx = reg[key].lock();
   if (!hx) {
-    hx = std::make_shared<HostExchange>();
-    hx->world = world;
-    hx->slot.resize(world);
+    auto t = std::make_shared<ThreadExchange>();
+    t->world = world;
+    t->slots.resize(world);
+    hx = t;
     reg[key] = hx;
   }
   return hx;
@@ -520,7 +541,9 @@ struct equil_matrix {
   int p2p_state = 0;
   std::vector<int64_t> peer_delta;
   std::vector<void*> peer_mapped;  // IPC mappings, closed on destroy
-  DevBuf<unsigned> bar;            // barrier word
+  DevBuf<unsigned> bar;            // barrier word (EQUIL_P2P_BARRIER=nccl)
+  int64_t xbar_off = 0;            // device barrier words: xbuf tail (eqb::kBarWords)
+  unsigned long long* xbar() { return reinterpret_cast<unsigned long long*>(xbuf.p + xbar_off); }
   DevBuf<double> u, ub, v, vb;  // local
   DevBuf<uint32_t> signs;
   DevBuf<unsigned char> sign_scratch;

@@ -150,6 +150,16 @@ struct SellArgs {
 // through map (slots; nullptr: unchanged).  midx: that matrix's slices (indices
 // into slices) in launch order; kbp: prefix of their 32-entry blocks.
 // kst (nullable): each lane's first entry within its row (column blocks).
+// Device flag barrier of the fused all-gather (world > 1, NCCL transport): a
+// tail of kBarWords 64-bit words behind the gathered vectors in xbuf (mapped by
+// every peer): [0, world) the last epoch each rank signalled, [kBarEpoch] this
+// rank's epoch counter, [kBarError] set if a wait timed out.  peer_delta: the
+// peers' xbuf minus this rank's, in 8-byte words (npeer = world - 1).
+constexpr int kBarWords = 16;
+constexpr int kBarEpoch = 8;
+constexpr int kBarError = 9;
+cudaError_t launch_peer_barrier(unsigned long long* bar, int rank, int world,
+                                const int64_t* peer_delta, int npeer, cudaStream_t s);
 // host -> device copy by a kernel reading mapped pinned memory (setup)
 cudaError_t launch_pull_copy(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
 // items: kbp[nmat_slices] (known on the host)

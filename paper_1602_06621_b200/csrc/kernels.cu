@@ -336,6 +336,56 @@ cudaError_t launch_validate_csr(const DevCsr& A, int* err, unsigned long long* w
 }
 
 // ---------------------------------------------------------------------------
+// Device flag barrier across the ranks of a fused all-gather (one CTA).  Stream
+// order puts it after this rank's SGD kernels, whose threads fenced their peer
+// stores system-wide (__threadfence_system) before exiting.  Each rank bumps its
+// epoch, release-stores it into flag[rank] of every peer, and acquire-spins
+// until every other rank's flag in its own array has reached the epoch; the
+// kernels after it (a new launch: L1 starts empty) then read the peers' stores.
+// A wait longer than ~6 s gives up and sets the error word (checked on the host
+// after the loop) instead of hanging.
+// ---------------------------------------------------------------------------
+namespace {
+struct PeerDeltas {
+  int64_t d[EQ_MAX_PEERS];
+};
+__global__ void peer_barrier_kernel(unsigned long long* bar, int rank, int world,
+                                    PeerDeltas pd, int npeer) {
+  __shared__ unsigned long long ep;
+  if (threadIdx.x == 0) {
+    ep = bar[kBarEpoch] + 1;
+    bar[kBarEpoch] = ep;
+  }
+  __syncthreads();
+  const unsigned long long e = ep;
+  if (static_cast<int>(threadIdx.x) < npeer) {
+    unsigned long long* dst = bar + rank + pd.d[threadIdx.x];
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(e) : "memory");
+  }
+  if (static_cast<int>(threadIdx.x) < world && static_cast<int>(threadIdx.x) != rank) {
+    unsigned long long v = 0;
+    for (long long spin = 0; spin < (1LL << 26); ++spin) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(bar + threadIdx.x) : "memory");
+      if (v >= e) break;
+      __nanosleep(100);
+    }
+    if (v < e) atomicExch(bar + kBarError, 1ULL);
+  }
+  __syncthreads();
+}
+}  // namespace
+
+cudaError_t launch_peer_barrier(unsigned long long* bar, int rank, int world,
+                                const int64_t* peer_delta, int npeer, cudaStream_t s) {
+  if (npeer > EQ_MAX_PEERS || world > kBarEpoch) return cudaErrorInvalidValue;
+  PeerDeltas pd{};
+  for (int g = 0; g < npeer; ++g) pd.d[g] = peer_delta[g];
+  peer_barrier_kernel<<<1, 32, 0, s>>>(bar, rank, world, pd, npeer);
+  count_launch(s);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Host -> device copy pulled by the SMs from mapped pinned memory: during
 // matrix setup the copy engine is busy with A's values, and a small plan
 // upload queued behind them would wait for the whole transfer.
