@@ -178,6 +178,9 @@ double equil_last_loop_ms(equil_matrix* A, int* iterations);
 int equil_exchange_mode(const equil_matrix* A);
 /* Number of this library's kernels launched so far in the process. */
 long long equil_kernel_launches(void);
+/* Build flags of the loaded library: bit 0 = checked build (EQ_CHECK device
+ * assertions, libequil_b200_checked.so).  No reference counterpart. */
+int equil_build_flags(void);
 
 /* LinearOperator::apply / apply_adjoint (include/equil/linop.hpp:13-25,
  * src/explicit_matrix.cpp:67-93): y = A x or x = A^T y, host vectors. */

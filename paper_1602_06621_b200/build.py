@@ -24,10 +24,13 @@ TAG = os.environ.get("EQUIL_TAG", "")
 DEFS = os.environ.get("EQUIL_DEFS", "").split()
 OBJ = os.path.join(CSRC, "build" + (f"_{TAG}" if TAG else ""))
 LIB = os.path.join(HERE, "libequil_b200" + (f"_{TAG}" if TAG else "") + ".so")
+# the checked build: device-side bounds / ring-protocol assertions (EQ_CHECK),
+# run by tests/test_gpu_checked.py in place of compute-sanitizer
+CHECKED_LIB = os.path.join(HERE, "libequil_b200_checked.so")
 GEN_LIB = os.path.join(HERE, "libequil_gen.so")  # synthetic inputs (bench/tests)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["kernels.cu", "transpose.cu", "sell.cu", "panel.cu", "variants.cu", "dense.cu", "engine.cu", "engine_ext.cu"]
+CU_SOURCES = ["engine.cu", "engine_ext.cu", "kernels.cu", "transpose.cu", "sell.cu", "panel.cu", "variants.cu", "dense.cu"]
 CXX_SOURCES = ["mt64_host.cpp", "mmio.cpp"]
 HEADERS = ["det_math.cuh", "internal.h", "mt64_host.h", "sgd_common.cuh", "mmio.h",
            "engine_internal.h"]
@@ -56,31 +59,45 @@ def _run(cmd: list[str], log: str | None = None) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ...")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = True) -> str:
+    lib = _build(OBJ, LIB, DEFS, force, verbose)
+    if checked and not TAG:
+        _build(os.path.join(CSRC, "build_checked"), CHECKED_LIB, ["-DEQ_CHECKED"], force, verbose)
+    gsrc = os.path.join(CSRC, "gen.cpp")
+    if force or _stale(GEN_LIB, [gsrc]):
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", gsrc, "-o", GEN_LIB])
+    return lib
+
+
+def _build(OBJ: str, LIB: str, DEFS: list, force: bool, verbose: bool) -> str:
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(OBJ, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "equil_b200.h")]
-    objs = []
+    objs, jobs = [], []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         if force or _stale(o, [s, *hdrs]):
-            if verbose:
-                print("nvcc", src, flush=True)
-            _run([NVCC, *ARCH, *NVFLAGS, *DEFS, "-c", s, "-o", o], log=o + ".ptxas.log")
+            jobs.append((src, [NVCC, *ARCH, *NVFLAGS, *DEFS, "-c", s, "-o", o], o + ".ptxas.log"))
         objs.append(o)
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         if force or _stale(o, [s, *hdrs]):
-            if verbose:
-                print("g++", src, flush=True)
-            _run(["g++", *CXXFLAGS, "-c", s, "-o", o])
+            jobs.append((src, ["g++", *CXXFLAGS, "-c", s, "-o", o], None))
         objs.append(o)
+
+    def one(job):
+        src, cmd, log = job
+        if verbose:
+            print(("nvcc " if cmd[0] == NVCC else "g++ ") + src + (" " + " ".join(DEFS) if DEFS else ""),
+                  flush=True)
+        _run(cmd, log=log)
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        list(ex.map(one, jobs))
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lpthread"])
-    gsrc = os.path.join(CSRC, "gen.cpp")
-    if force or _stale(GEN_LIB, [gsrc]):
-        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", gsrc, "-o", GEN_LIB])
     return LIB
 
 

@@ -362,6 +362,7 @@ void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::Pass
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
   eqb::SellArgs sa{};
+  sa.xlen[0] = sa.xlen[1] = mat ? M->m_pad() : M->n_pad();  // padded coordinates
   sa.slices = M->sell_slices.p;
   sa.order = M->sell_pidx[mat].p;
   sa.row = M->sell_row.p;
@@ -1150,28 +1151,36 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
     M->xs[b].p = M->xbuf.p + b * np;
     M->xw[b].p = M->xbuf.p + 2 * np + b * mp;
   }
-  // Keep the gather targets resident in L2 while CSR(A)/CSR(A^T) stream past.
+  // Keep the gather targets resident in L2 while CSR(A)/CSR(A^T) stream past;
+  // dense: keep A itself (c2: 67 MB, read twice per iteration) persisting.
   int dev = 0, max_persist = 0, max_window = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-  const size_t bytes = static_cast<size_t>(2 * (np + mp)) * sizeof(double);
+  const void* wbase = M->dense ? static_cast<const void*>(M->Ad.p) : M->xbuf.p;
+  const size_t bytes = M->dense ? static_cast<size_t>(M->m * M->n) * sizeof(double)
+                                : static_cast<size_t>(2 * (np + mp)) * sizeof(double);
   static const bool l2win = !getenv("EQUIL_L2WIN") || atoi(getenv("EQUIL_L2WIN")) != 0;
-  if (l2win && max_persist > 0 && max_window > 0) {
+  if (l2win && max_persist > 0 && max_window > 0 && bytes > 0) {
     const size_t win = std::min(bytes, static_cast<size_t>(max_window));
     const size_t carve = std::min(win, static_cast<size_t>(max_persist));
     M->l2_max_window = static_cast<size_t>(max_window);
     M->l2_default_bytes = bytes;
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
+    // the limit is device-wide and setting it is slow (~2 ms): only when it changes
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur == carve || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) == cudaSuccess) {
       M->l2_carve = carve;
       cudaStreamAttrValue attr{};
-      attr.accessPolicyWindow.base_ptr = M->xbuf.p;
+      attr.accessPolicyWindow.base_ptr = const_cast<void*>(wbase);
       attr.accessPolicyWindow.num_bytes = win;
       attr.accessPolicyWindow.hitRatio =
           static_cast<float>(std::min(1.0, static_cast<double>(carve) / win));
       attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       cudaStreamSetAttribute(M->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+      if (M->dense)  // the column half runs on the copy stream
+        cudaStreamSetAttribute(M->copy_stream, cudaStreamAttributeAccessPolicyWindow, &attr);
     }
     cudaGetLastError();  // the window is a hint; never fail on it
   }
@@ -1501,6 +1510,14 @@ double equil_last_loop_ms(equil_matrix* A, int* iterations) {
 
 long long equil_kernel_launches(void) { return eqb::launch_count(); }
 
+int equil_build_flags(void) {
+#ifdef EQ_CHECKED
+  return 1;
+#else
+  return 0;
+#endif
+}
+
 int equil_exchange_mode(const equil_matrix* A) {
   if (!A || A->world == 1 || A->p2p_state == 0) return 0;
   return A->p2p_state == 1 ? 2 : 1;
@@ -1541,7 +1558,7 @@ void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, in
     M->red_part.ensure(parts);
   }
   CK(eqb::launch_canon_reduce(x, len, kind, coef, M->red_part.p, M->red_counter.p, out,
-                              sqrt_out ? 1 : 0, M->stream));
+                              sqrt_out ? 1 : 0, M->stream, static_cast<int64_t>(M->red_part.n)));
 }
 
 }  // namespace eqe
@@ -1843,6 +1860,8 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
             CK(eqb::launch_sgd_panel(a, panel_args, M->n_pbands, s));
           } else if (M->sell) {
             eqb::SellArgs sa{};
+            sa.xlen[0] = M->n_pad();  // A's rows gather xs, A^T's xw
+            sa.xlen[1] = M->m_pad();
             sa.slices = M->sell_slices.p;
             sa.nslices = M->n_sell;
             sa.row = M->sell_row.p;

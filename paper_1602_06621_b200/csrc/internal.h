@@ -4,12 +4,31 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <functional>
 #include <vector>
 
 #include "det_math.cuh"
 
 namespace eqb {
+
+// Checked build (EQUIL_DEFS=-DEQ_CHECKED, libequil_b200_checked.so): device-side
+// bounds / protocol assertions that trap on failure.  compute-sanitizer is not
+// available on the GPU pool, so tests/test_gpu_checked.py runs the workloads on
+// this build instead.
+#ifdef EQ_CHECKED
+#define EQ_CHECK(c)                                                              \
+  do {                                                                           \
+    if (!(c)) {                                                                  \
+      printf("EQ_CHECK failed at %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define EQ_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 
 // Sparse traversal tile.  kind 2 (one warp): a slice of r1 (<= 32) rows listed
 // at rowlist[r0 ...], sorted by length (longest first), summed one row per lane
@@ -145,11 +164,8 @@ struct SellArgs {
   const int32_t* len;       // its length (0 for empty lanes)
   const int32_t* ci[2];     // interleaved slot columns
   const double* va[2];      // interleaved values
+  int64_t xlen[2];          // length of the gathered vector(s) (checked builds)
 };
-// Fill one matrix's interleaved arrays from its CSR rows, columns mapped
-// through map (slots; nullptr: unchanged).  midx: that matrix's slices (indices
-// into slices) in launch order; kbp: prefix of their 32-entry blocks.
-// kst (nullable): each lane's first entry within its row (column blocks).
 // Device flag barrier of the fused all-gather (world > 1, NCCL transport): a
 // tail of kBarWords 64-bit words behind the gathered vectors in xbuf (mapped by
 // every peer): [0, world) the last epoch each rank signalled, [kBarEpoch] this
@@ -162,6 +178,10 @@ cudaError_t launch_peer_barrier(unsigned long long* bar, int rank, int world,
                                 const int64_t* peer_delta, int npeer, cudaStream_t s);
 // host -> device copy by a kernel reading mapped pinned memory (setup)
 cudaError_t launch_pull_copy(void* dst, const void* src_mapped, size_t bytes, cudaStream_t s);
+// Fill one matrix's interleaved arrays from its CSR rows, columns mapped
+// through map (slots; nullptr: unchanged).  midx: that matrix's slices (indices
+// into slices) in launch order; kbp: prefix of their 32-entry blocks.
+// kst (nullable): each lane's first entry within its row (column blocks).
 // items: kbp[nmat_slices] (known on the host)
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
                        const int64_t* kbp, int64_t items, const int32_t* midx, int nmat_slices,
@@ -363,9 +383,10 @@ cudaError_t launch_pass_range(const PassArgs& a, const PassArgs* b, int tile_bas
 
 // canonical reduction (det_math.cuh) of terms x*x (kind 0), x (kind 1) or
 // coef*x (kind 2); *out (device) = result, or its sqrt when sqrt_out
+// part_cap: capacity of partials (checked builds; < 0: unknown)
 cudaError_t launch_canon_reduce(const double* x, int64_t len, int kind, double coef,
                                 double* partials, unsigned* counter, double* out,
-                                int sqrt_out, cudaStream_t s);
+                                int sqrt_out, cudaStream_t s, int64_t part_cap = -1);
 
 // signs: MT19937-64 device generation
 cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,

@@ -1038,8 +1038,9 @@ __device__ double block_fold(double* s, int lanes) {
 __global__ void __launch_bounds__(256)
 canon_reduce_kernel(const double* __restrict__ x, int64_t len, int kind, double coef,
                     double* __restrict__ part, unsigned* counter,
-                    double* __restrict__ out, int sqrt_out) {
+                    double* __restrict__ out, int sqrt_out, int64_t part_cap) {
   __shared__ double s[kLanes2];
+  EQ_CHECK(part_cap < 0 || static_cast<int64_t>(blockIdx.x) < part_cap);
   __shared__ bool last;
   const int64_t nc = (len + kChunk - 1) / kChunk;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk;
@@ -1080,10 +1081,10 @@ canon_reduce_kernel(const double* __restrict__ x, int64_t len, int kind, double 
 
 cudaError_t launch_canon_reduce(const double* x, int64_t len, int kind, double coef,
                                 double* partials, unsigned* counter, double* out,
-                                int sqrt_out, cudaStream_t s) {
+                                int sqrt_out, cudaStream_t s, int64_t part_cap) {
   const int64_t nc = std::max<int64_t>(1, (len + kChunk - 1) / kChunk);
   canon_reduce_kernel<<<static_cast<unsigned>(nc), 256, 0, s>>>(
-      x, len, kind, coef, partials, counter, out, sqrt_out); count_launch(s);
+      x, len, kind, coef, partials, counter, out, sqrt_out, part_cap); count_launch(s);
   return cudaGetLastError();
 }
 

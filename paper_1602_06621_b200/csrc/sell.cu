@@ -342,7 +342,10 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
     double g[B], g2[B];
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (full || k0 + b < len) gather_x<Op>(x, x2, c[b], g[b], g2[b]);
+      if (full || k0 + b < len) {
+        EQ_CHECK(c[b] >= 0 && c[b] < sa.xlen[mat]);
+        gather_x<Op>(x, x2, c[b], g[b], g2[b]);
+      }
 #pragma unroll
     for (int b = 0; b < B; ++b)
       if (full || k0 + b < len) {
@@ -425,6 +428,9 @@ sell_long_kernel(const Op op, const SellArgs sa) {
   constexpr int R = S + 1;
   __shared__ __align__(16) double buf[NV][R][B * 32];
   __shared__ __align__(8) unsigned long long full[R], empty[R];
+#ifdef EQ_CHECKED
+  __shared__ int tag[R];  // round whose products a stage holds (ring protocol check)
+#endif
   if (op.skip()) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = sa.first + blockIdx.x;
@@ -470,9 +476,15 @@ sell_long_kernel(const Op op, const SellArgs sa) {
       double g[B], g2[B];
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (k0 + b < len) gather_x<Op>(x, x2, c[b], g[b], g2[b]);
+        if (k0 + b < len) {
+          EQ_CHECK(c[b] >= 0 && c[b] < sa.xlen[mat]);
+          gather_x<Op>(x, x2, c[b], g[b], g2[b]);
+        }
       const int bi = r % R;
       if (r >= R) mbar_wait(&empty[bi], ((r / R) - 1) & 1);
+#ifdef EQ_CHECKED
+      if (lane == 0) tag[bi] = r;
+#endif
 #pragma unroll
       for (int b = 0; b < B; ++b)
         if (k0 + b < len) {
@@ -494,6 +506,9 @@ sell_long_kernel(const Op op, const SellArgs sa) {
   for (int r = 0; r < rounds; ++r) {
     const int bi = r % R;
     mbar_wait(&full[bi], (r / R) & 1);
+#ifdef EQ_CHECKED
+    EQ_CHECK(tag[bi] == r);  // the stage holds this round's products
+#endif
     const int k0 = r * B;
 #pragma unroll
     for (int b = 0; b < B; ++b)

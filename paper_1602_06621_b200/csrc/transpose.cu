@@ -234,7 +234,7 @@ part_scatter_kernel(const int32_t* __restrict__ col, const int32_t* __restrict__
                     const int32_t* __restrict__ src, const PartChunk* __restrict__ chunks,
                     int nchunks, int shift, int bits, const int32_t* __restrict__ off,
                     int32_t* __restrict__ ocol, int32_t* __restrict__ orow,
-                    int32_t* __restrict__ osrc) {
+                    int32_t* __restrict__ osrc, int64_t total) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ScatterSmem& S = reinterpret_cast<ScatterSmem*>(smraw)[warp];
@@ -274,6 +274,7 @@ part_scatter_kernel(const int32_t* __restrict__ col, const int32_t* __restrict__
     if (ok && lane == leader) base = S.cur[bk];
     base = __shfl_sync(0xffffffffu, base, leader);
     const int32_t pos = base + __popc(peers & lt);
+    EQ_CHECK(!ok || (pos >= 0 && pos < total));
     const int32_t l0 = base / kLine;  // positions are >= 0
     // a bucket's entries of this step span at most 3 granules: fill, flush full ones
     for (int ph = 0; ph < 3; ++ph) {
@@ -480,7 +481,7 @@ cudaError_t transpose_structure(const DevCsr& A, DevCsr& AT, const int64_t* rpT_
       int32_t* orow = final ? AT.col : bufr[o];
       int32_t* osrc = final ? w.srcT : bufs[o];
       part_scatter_kernel<<<grid, 32 * kPartWarps, kPartWarps * sizeof(ScatterSmem), s>>>(
-          icol, irow, isrc, dch, nchunks, shift, bits, cnt, oc, orow, osrc);
+          icol, irow, isrc, dch, nchunks, shift, bits, cnt, oc, orow, osrc, nnz);
       count_launch(s);
       if ((e = cudaGetLastError())) break;
       icol = oc;
