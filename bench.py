@@ -364,8 +364,9 @@ def run_ours(args):
         # pinned result buffers: the device->host read of u, v, d, e is inside the step
         pin_out = tuple(torch.empty(k, dtype=torch.float64).pin_memory().numpy()
                         for k in (inst.m, inst.n, inst.m, inst.n))
-        eq.sgd_equilibrate_csr(inst.m, inst.n, pin_rp.numpy(), pin_c.numpy(), pin_v.numpy(),
-                               p, device=local, out=pin_out)  # warm (module load, jump polys)
+        for _ in range(2):  # warm (module load, jump polys, pool growth, pinned mappings)
+            eq.sgd_equilibrate_csr(inst.m, inst.n, pin_rp.numpy(), pin_c.numpy(), pin_v.numpy(),
+                                   p, device=local, out=pin_out)
         ts = []
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()

@@ -193,6 +193,33 @@ __global__ void remap_cols_kernel(int32_t* col, int64_t nnz, const int64_t* boun
   col[k] = static_cast<int32_t>(g * maxcnt + (j - bounds[g]));
 }
 
+// sharded setup: a constant added to every column (local A row -> padded slot)
+__global__ void add_cols_kernel(int32_t* col, int64_t nnz, int64_t delta) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < nnz) col[k] = static_cast<int32_t>(col[k] + delta);
+}
+// row lengths from row pointers
+__global__ void row_counts_kernel(const int64_t* rp, int64_t rows, int32_t* cnt) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k < rows) cnt[k] = static_cast<int32_t>(rp[k + 1] - rp[k]);
+}
+// Merge of the received CSR(A^T) pieces: run (source g, local row j) of cnt
+// entries moves from src_off to dst_off.  Sources arrive in rank order and each
+// holds ascending rows of A, so row j's entries end up in ascending original
+// row order -- CSR(A^T)'s order (explicit_matrix.cpp:117-125).
+__global__ void merge_runs_kernel(const int64_t* src_off, const int64_t* dst_off,
+                                  const int32_t* cnt, int64_t runs, const int32_t* ci_in,
+                                  const double* va_in, int32_t* ci_out, double* va_out) {
+  const int64_t q = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;  // 8 threads per run
+  if (q >= runs) return;
+  const int64_t s0 = src_off[q], d0 = dst_off[q];
+  for (int k = sub; k < cnt[q]; k += 8) {
+    ci_out[d0 + k] = ci_in[s0 + k];
+    va_out[d0 + k] = va_in[s0 + k];
+  }
+}
+
 __global__ void rebase_rowptr_kernel(int64_t* dst, const int64_t* src, int64_t cnt,
                                      int64_t base) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -216,7 +243,6 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   M->device = cfg ? cfg->device : 0;
   M->rank = cfg ? cfg->rank : 0;
   M->world = cfg ? std::max(1, cfg->world_size) : 1;
-  if (const char* e = getenv("EQUIL_PANEL")) M->use_panels = atoi(e) != 0;  // A/B knob
   if (const char* e = getenv("EQUIL_SLOTS")) M->use_slots = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL")) M->use_sell = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL_VARIANT")) M->sell_variant = atoi(e);
@@ -326,16 +352,27 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
 
 // The generic passes' column arrays (padded coordinates) and per-matrix slice
 // orders, on first use.
+// per-matrix slice orders of the generic passes (both column flavours)
+void ensure_sell_order(equil_matrix* M) {
+  if (M->sell_order_up || !M->sell) return;
+  const equil_matrix::SellHost& H = M->sell_host;
+  for (int mat = 0; mat < 2; ++mat) {
+    M->sell_pidx[mat].alloc(H.pidx[mat].size());
+    if (!H.pidx[mat].empty())
+      CK(cudaMemcpyAsync(M->sell_pidx[mat].p, H.pidx[mat].data(), H.pidx[mat].size() * 4,
+                         cudaMemcpyHostToDevice, M->stream));
+  }
+  CK(cudaStreamSynchronize(M->stream));
+  M->sell_order_up = true;
+}
+
 void ensure_sell_pass(equil_matrix* M) {
   if (M->sell_pass || !M->sell) return;
+  ensure_sell_order(M);
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
   for (int mat = 0; mat < 2; ++mat) {
     M->sell_pci[mat].alloc(H.total[mat]);
-    M->sell_pidx[mat].alloc(H.pidx[mat].size());
-    if (!H.pidx[mat].empty())
-      CK(cudaMemcpyAsync(M->sell_pidx[mat].p, H.pidx[mat].data(), H.pidx[mat].size() * 4,
-                         cudaMemcpyHostToDevice, s));
     DevBuf<int64_t> dkbp;
     DevBuf<int32_t> didx;
     dkbp.alloc(H.kbp[mat].size());
@@ -356,9 +393,15 @@ void ensure_sell_pass(equil_matrix* M) {
 
 // One generic pass (b: the dual pass) over matrix `mat` on the interleaved
 // slices: long slices on the copy stream, warp slices on the main stream.
+// slotted: the gathered vector is in the hot-first slot layout, so the SGD
+// passes' slot-mapped column arrays serve (LSQR, engine.cu lsqr_core).
 void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::PassArgs* b,
-               bool pair = false) {
-  ensure_sell_pass(M);
+               bool pair = false, bool slotted = false) {
+  if (slotted) {
+    ensure_sell_order(M);
+  } else {
+    ensure_sell_pass(M);
+  }
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
   eqb::SellArgs sa{};
@@ -368,7 +411,7 @@ void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::Pass
   sa.row = M->sell_row.p;
   sa.len = M->sell_len.p;
   for (int k = 0; k < 2; ++k) {
-    sa.ci[k] = M->sell_pci[k].p;
+    sa.ci[k] = slotted ? M->sell_ci[k].p : M->sell_pci[k].p;
     sa.va[k] = M->sell_va[k].p;
   }
   const int nl = H.plong[mat], nall = static_cast<int>(H.pidx[mat].size());
@@ -496,7 +539,7 @@ void build_sell_layout(equil_matrix* M, bool with_values) {
   M->sell_values_pending = false;
   M->sell_nb = 1;
   const bool blocked = M->nblk[0] > 1 || M->nblk[1] > 1;
-  if (!M->use_sell || M->use_panels || (!M->slots && !blocked)) return;
+  if (!M->use_sell || (!M->slots && !blocked)) return;
   if (blocked && (!M->sell_blocked || M->sell_long == 0)) return;
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
@@ -667,6 +710,7 @@ struct ShmExchange : HostExchange {
   }
   const char* slot(int g) override { return base + g * cap; }
   bool in_process() const override { return false; }
+  size_t capacity() const override { return cap; }
 };
 
 std::shared_ptr<HostExchange> shm_exchange(const void* id128, int world, int rank) {
@@ -698,7 +742,7 @@ static std::vector<char> allgather_bytes(equil_matrix* M, const void* mine, size
 void setup_peers(equil_matrix* M) {
   M->p2p_state = -1;
   const int G = M->world, r = M->rank;
-  int want = (!M->use_panels && !M->dense && G - 1 <= EQ_MAX_PEERS) ? 1 : 0;
+  int want = (!M->dense && G - 1 <= EQ_MAX_PEERS) ? 1 : 0;
   if (const char* e = getenv("EQUIL_P2P")) want = want && atoi(e) != 0;
   CK(cudaStreamSynchronize(M->stream));
   const bool local = M->hx && M->hx->in_process();
@@ -782,65 +826,6 @@ void rank_barrier(equil_matrix* M) {
                               static_cast<int>(M->peer_delta.size()), M->stream));
 }
 
-// Bands for the column-panel traversal: consecutive rows, closed before a row
-// that would push the band past `target` entries or kBandRows rows.
-std::vector<int64_t> plan_bands(const int64_t* rp, int64_t rows, int64_t target) {
-  std::vector<int64_t> b{0};
-  for (int64_t i = 0; i < rows; ++i) {
-    const int64_t r0 = b.back();
-    if (i > r0 && (i - r0 >= eqb::kBandRows || rp[i + 1] - rp[r0] > target)) b.push_back(i);
-  }
-  if (rows > 0) b.push_back(rows);
-  return b;
-}
-
-// Panel-major copies of the local A / A^T shards and the band list of the SGD
-// launch (both matrices, largest bands first).  Band size targets about
-// EQUIL_BANDS_PER_SM (default 2) bands per SM over the whole launch.
-void build_panel_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT) {
-  M->n_pbands = 0;
-  if (!M->use_panels) return;
-  int dev = 0, sms = 148;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  double per_sm = 2.0;
-  if (const char* e = getenv("EQUIL_BANDS_PER_SM")) per_sm = std::max(0.1, atof(e));
-  const int64_t total = M->A.nnz + M->AT.nnz;
-  const int64_t target = std::max<int64_t>(1, static_cast<int64_t>(total / (per_sm * sms)));
-  std::vector<std::pair<int64_t, eqb::PanelBand>> all;
-  for (int mat = 0; mat < 2; ++mat) {
-    const eqb::DevCsr& C = mat ? M->AT : M->A;
-    const int64_t* rp = mat ? rpT : rpA;
-    const std::vector<int64_t> bounds = plan_bands(rp, C.rows, target);
-    const int nb = static_cast<int>(bounds.size()) - 1;
-    if (nb <= 0) continue;
-    M->pval[mat].alloc(C.nnz);
-    M->pcol[mat].alloc(C.nnz);
-    eqb::PanelChunk* ch = nullptr;
-    uint32_t* runs = nullptr;
-    int64_t nch = 0, nruns = 0;
-    std::vector<int64_t> bc;
-    CK(eqb::build_panels(C, mat ? M->m_pad() : M->n_pad(), bounds, M->pval[mat].p,
-                         M->pcol[mat].p, &runs, &nruns, &ch, &nch, &bc, M->stream));
-    M->pchunks[mat].adopt(ch, static_cast<size_t>(std::max<int64_t>(1, nch)));
-    M->pruns[mat].adopt(runs, static_cast<size_t>(std::max<int64_t>(1, nruns)));
-    for (int b = 0; b < nb; ++b) {
-      eqb::PanelBand pb{static_cast<int32_t>(bounds[b]),
-                        static_cast<int32_t>(bounds[b + 1] - bounds[b]),
-                        static_cast<int32_t>(bc[b]), static_cast<int32_t>(bc[b + 1]), mat, 0};
-      all.push_back({rp[bounds[b + 1]] - rp[bounds[b]], pb});
-    }
-  }
-  std::stable_sort(all.begin(), all.end(),
-                   [](const auto& x, const auto& y) { return x.first > y.first; });
-  std::vector<eqb::PanelBand> h;
-  for (const auto& x : all) h.push_back(x.second);
-  M->pbands.alloc(h.size());
-  if (!h.empty())
-    CK(cudaMemcpy(M->pbands.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
-  M->n_pbands = static_cast<int>(h.size());
-}
-
 // Column blocks for gathered vectors larger than L2.  When the vector a pass
 // gathers from (xs for A, xw for A^T) exceeds EQUIL_BLOCK_MB (default 60 MB,
 // measured best on c5 among 20-80 MB: blocks of 40-53 MB), its coordinates are cut
@@ -850,7 +835,6 @@ void build_panel_layout(equil_matrix* M, const int64_t* rpA, const int64_t* rpT)
 // order is unchanged.  The slot layout is not used with blocks.
 void build_block_layout(equil_matrix* M) {
   M->nblk[0] = M->nblk[1] = 1;
-  if (M->use_panels) return;
   double mb = 60.0;
   if (const char* e = getenv("EQUIL_BLOCK_MB")) {
     const double v = atof(e);
@@ -884,7 +868,7 @@ void build_block_layout(equil_matrix* M) {
 // the global row pointers (a 7-bit stable radix sort per matrix).
 void build_slot_layout(equil_matrix* M, const int64_t* rpA_dev, const int64_t* rpT_dev) {
   M->slots = false;
-  if (!M->use_slots || M->use_panels) return;
+  if (!M->use_slots) return;
   cudaStream_t s = M->stream;
   const int G = M->world;
   DevBuf<int64_t> ab, tb;
@@ -978,10 +962,302 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   const std::vector<int64_t> lt = local_rp(rpT_host, M->t_bounds);
   upload_plans(M, plan_tiles(la.data(), static_cast<int64_t>(la.size()) - 1, 0),
                plan_tiles(lt.data(), static_cast<int64_t>(lt.size()) - 1, 1));
-  build_panel_layout(M, la.data(), lt.data());
   build_block_layout(M);
   build_slot_layout(M, fullA.row_ptr, fullT.row_ptr);
   build_sell_layout(M, true);
+}
+
+// ---- rank collectives of the sharded setup ---------------------------------
+// Every transport: NCCL (grouped send / receive, all-reduce) or the host
+// exchange (one process per GPU over shared memory, or ranks as threads of one
+// process; chunked through the exchange slots).
+
+// Device all-to-all of bytes: send[soff[h], soff[h+1]) goes to rank h, and
+// recv[roff[g], roff[g+1]) arrives from rank g.
+void alltoallv_bytes(equil_matrix* M, const char* send, const std::vector<int64_t>& soff,
+                     char* recv, const std::vector<int64_t>& roff) {
+  const int G = M->world, r = M->rank;
+  cudaStream_t s = M->stream;
+  if (!M->hx) {
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    for (int h = 0; h < G; ++h) {
+      const size_t sb = static_cast<size_t>(soff[h + 1] - soff[h]);
+      const size_t rb = static_cast<size_t>(roff[h + 1] - roff[h]);
+      if (h == r) {
+        if (sb) CK(cudaMemcpyAsync(recv + roff[h], send + soff[h], sb, cudaMemcpyDeviceToDevice, s));
+        continue;
+      }
+      if (sb) nccl_check(nccl().Send(send + soff[h], sb, ncclUint8, h, M->comm, s), "ncclSend");
+      if (rb) nccl_check(nccl().Recv(recv + roff[h], rb, ncclUint8, h, M->comm, s), "ncclRecv");
+    }
+    nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  // host exchange: every rank's whole send buffer passes through its slot in
+  // chunks of the slot capacity; each rank copies out the part addressed to it
+  CK(cudaStreamSynchronize(s));
+  const size_t total = static_cast<size_t>(soff[G]);
+  std::vector<char> host(total);
+  if (total) CK(cudaMemcpy(host.data(), send, total, cudaMemcpyDeviceToHost));
+  // everyone's send offsets (to find the piece addressed to this rank)
+  const std::vector<char> offs =
+      allgather_bytes(M, soff.data(), static_cast<size_t>(G + 1) * sizeof(int64_t));
+  auto off_of = [&](int g, int h) {
+    int64_t v;
+    std::memcpy(&v, offs.data() + (static_cast<size_t>(g) * (G + 1) + h) * sizeof(int64_t), 8);
+    return v;
+  };
+  const size_t cap = std::min<size_t>(M->hx->capacity(), size_t(1) << 30);
+  int64_t maxtot = 0;
+  for (int g = 0; g < G; ++g) maxtot = std::max(maxtot, off_of(g, G));
+  const int64_t rounds = (maxtot + static_cast<int64_t>(cap) - 1) / static_cast<int64_t>(cap);
+  std::vector<char> mine(static_cast<size_t>(roff[G]));
+  for (int64_t c = 0; c < rounds; ++c) {
+    const int64_t lo = c * static_cast<int64_t>(cap);
+    const int64_t hi = std::min<int64_t>(lo + static_cast<int64_t>(cap), static_cast<int64_t>(total));
+    M->hx->put(r, host.data() + std::min<int64_t>(lo, total), hi > lo ? static_cast<size_t>(hi - lo) : 0);
+    M->hx->barrier();
+    for (int g = 0; g < G; ++g) {
+      const int64_t a = std::max(off_of(g, r), lo);
+      const int64_t b = std::min(off_of(g, r + 1), lo + static_cast<int64_t>(cap));
+      if (b > a)
+        std::memcpy(mine.data() + roff[g] + (a - off_of(g, r)), M->hx->slot(g) + (a - lo),
+                    static_cast<size_t>(b - a));
+    }
+    M->hx->barrier();
+  }
+  if (roff[G]) CK(cudaMemcpy(recv, mine.data(), static_cast<size_t>(roff[G]), cudaMemcpyHostToDevice));
+}
+
+// In-place sum of an int64 device array over the ranks.
+void allreduce_sum_i64(equil_matrix* M, int64_t* dev, int64_t count) {
+  cudaStream_t s = M->stream;
+  if (!M->hx) {
+    nccl_check(nccl().AllReduce(dev, dev, static_cast<size_t>(count), ncclInt64, ncclSum, M->comm, s),
+               "ncclAllReduce");
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  CK(cudaStreamSynchronize(s));
+  const size_t bytes = static_cast<size_t>(count) * 8;
+  const size_t cap = std::min<size_t>(M->hx->capacity(), size_t(1) << 30) / 8 * 8;
+  std::vector<int64_t> mine(static_cast<size_t>(count)), sum(static_cast<size_t>(count), 0);
+  CK(cudaMemcpy(mine.data(), dev, bytes, cudaMemcpyDeviceToHost));
+  for (size_t lo = 0; lo < bytes; lo += cap) {
+    const size_t len = std::min(cap, bytes - lo);
+    M->hx->put(M->rank, reinterpret_cast<const char*>(mine.data()) + lo, len);
+    M->hx->barrier();
+    for (int g = 0; g < M->world; ++g) {
+      const int64_t* p = reinterpret_cast<const int64_t*>(M->hx->slot(g));
+      for (size_t k = 0; k < len / 8; ++k) sum[lo / 8 + k] += p[k];
+    }
+    M->hx->barrier();
+  }
+  CK(cudaMemcpy(dev, sum.data(), bytes, cudaMemcpyHostToDevice));
+}
+
+// ExplicitMatrix::sparse's message for the first invalid entry (class, global
+// entry index), in the reference's order of checks (explicit_matrix.cpp:21-39)
+[[noreturn]] void fail_invalid_entry(unsigned long long wh, const int64_t* row_ptr, int64_t m,
+                                     const int32_t* col) {
+  const int cls = static_cast<int>(wh >> 40);
+  const int64_t k = static_cast<int64_t>(wh & ((1ULL << 40) - 1));
+  const int64_t i = std::upper_bound(row_ptr, row_ptr + m + 1, k) - row_ptr - 1;
+  const std::string at = "(" + std::to_string(i) + ", " + std::to_string(col[k]) + ")";
+  if (cls == 0) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry " + at + " out of range");
+  if (cls == 1) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry " + at);
+  fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: columns not ascending at entry " + at +
+                         " (canonical CSR required)");
+}
+
+// Sharded setup (world > 1).  Rank r uploads only its rows [a0, a1) of A,
+// validates them (the first error over all ranks wins, so every rank throws
+// the single-GPU message), and transposes them locally.  CSR(A^T)'s global
+// row pointers are the sum of the ranks' local prefix sums (one all-reduce),
+// which fixes the A^T partition.  An all-to-all then sends every rank the rows
+// of its A^T range from every other rank's local transpose (counts, columns,
+// values), and a merge lays them out in rank order -- ascending original row,
+// CSR(A^T)'s own order -- so the shards equal those cut from the full
+// transpose, bit for bit, with 1/world of the upload and transpose work.
+void create_sharded(equil_matrix* M, const int64_t* row_ptr, const int32_t* col,
+                    const double* val, PhaseTimer& pt) {
+  const int G = M->world, r = M->rank;
+  const int64_t m = M->m, n = M->n;
+  cudaStream_t s = M->stream;
+  M->a_bounds = partition_rows(row_ptr, m, G);
+  const int64_t a0 = M->a_bounds[r], a1 = M->a_bounds[r + 1];
+  const int64_t k0 = row_ptr[a0], k1 = row_ptr[a1];
+  const int64_t ml = a1 - a0, nl = k1 - k0;
+  // this rank's rows of A (row pointers rebased) and the global row pointers
+  // (the slot layout of the gathered vectors needs every row's length)
+  DevBuf<int64_t> rpA_full;
+  rpA_full.alloc(m + 1);
+  CK(cudaMemcpyAsync(rpA_full.p, row_ptr, (m + 1) * 8, cudaMemcpyHostToDevice, s));
+  std::vector<int64_t> rph(static_cast<size_t>(ml) + 1);
+  for (int64_t i = 0; i <= ml; ++i) rph[i] = row_ptr[a0 + i] - k0;
+  M->a_rp.alloc(ml + 1);
+  M->a_ci.alloc(nl);
+  M->a_va.alloc(nl);
+  CK(cudaMemcpyAsync(M->a_rp.p, rph.data(), (ml + 1) * 8, cudaMemcpyHostToDevice, s));
+  if (nl) {
+    CK(cudaMemcpyAsync(M->a_ci.p, col + k0, nl * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(M->a_va.p, val + k0, nl * 8, cudaMemcpyHostToDevice, s));
+  }
+  eqb::DevCsr locA{ml, n, nl, M->a_rp.p, M->a_ci.p, M->a_va.p};
+  pt.mark(s, "upload (shard)");
+  // validation of the local rows; the smallest (class, global entry) over ranks
+  DevBuf<unsigned long long> where;
+  where.alloc(1);
+  CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
+  CK(cudaMemsetAsync(where.p, 0xff, 8, s));
+  CK(eqb::launch_validate_csr(locA, reinterpret_cast<int*>(M->flags.p), where.p, s));
+  unsigned long long wh = ~0ULL;
+  CK(cudaMemcpyAsync(&wh, where.p, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (wh != ~0ULL) wh += static_cast<unsigned long long>(k0);  // class bits untouched
+  {
+    const std::vector<char> all = allgather_bytes(M, &wh, 8);
+    for (int g = 0; g < G; ++g) {
+      unsigned long long o;
+      std::memcpy(&o, all.data() + 8 * g, 8);
+      wh = std::min(wh, o);
+    }
+  }
+  if (wh != ~0ULL) fail_invalid_entry(wh, row_ptr, m, col);
+  pt.mark(s, "validate (shard)");
+  // local transpose: n rows (A's columns) x ml (this rank's rows of A)
+  DevBuf<int64_t> trl;
+  DevBuf<int32_t> tcl;
+  DevBuf<double> tvl;
+  trl.alloc(n + 1);
+  tcl.alloc(nl);
+  tvl.alloc(nl);
+  CK(eqb::launch_col_rowptr(M->a_ci.p, nl, n, trl.p, s));
+  std::vector<int64_t> trl_h(static_cast<size_t>(n) + 1);
+  CK(cudaMemcpyAsync(trl_h.data(), trl.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  eqb::DevCsr locT{n, ml, nl, trl.p, tcl.p, tvl.p};
+  {
+    eqb::TransposeWork tw;
+    CK(eqb::transpose_structure(locA, locT, trl_h.data(), tw, s));
+    CK(eqb::transpose_values(locA, locT, tw, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  pt.mark(s, "transpose (shard)");
+  // CSR(A^T)'s global row pointers: the sum of the local prefix sums
+  DevBuf<int64_t> rpT_full;
+  rpT_full.alloc(n + 1);
+  CK(cudaMemcpyAsync(rpT_full.p, trl.p, (n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  allreduce_sum_i64(M, rpT_full.p, n + 1);
+  std::vector<int64_t> rpT(static_cast<size_t>(n) + 1);
+  CK(cudaMemcpy(rpT.data(), rpT_full.p, (n + 1) * 8, cudaMemcpyDeviceToHost));
+  M->t_bounds = partition_rows(rpT.data(), n, G);
+  M->a_max = 0;
+  M->t_max = 0;
+  for (int g = 0; g < G; ++g) {
+    M->a_max = std::max(M->a_max, M->a_bounds[g + 1] - M->a_bounds[g]);
+    M->t_max = std::max(M->t_max, M->t_bounds[g + 1] - M->t_bounds[g]);
+  }
+  M->a_bounds_d.alloc(G + 1);
+  M->t_bounds_d.alloc(G + 1);
+  CK(cudaMemcpy(M->a_bounds_d.p, M->a_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(M->t_bounds_d.p, M->t_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+  // A^T's columns are A's rows: local row -> this rank's padded slot range
+  if (nl)
+    add_cols_kernel<<<static_cast<unsigned>((nl + 255) / 256), 256, 0, s>>>(tcl.p, nl,
+                                                                        r * M->a_max);
+  // A's columns are A^T's rows: global column -> padded slot
+  if (nl)
+    remap_cols_kernel<<<static_cast<unsigned>((nl + 255) / 256), 256, 0, s>>>(
+        M->a_ci.p, nl, M->t_bounds_d.p, G, M->t_max);
+  CK(cudaGetLastError());
+  // all-to-all: rank h gets rows [t_bounds[h], t_bounds[h+1]) of every local
+  // transpose -- first each row's count, then the columns and the values
+  const int64_t t0 = M->t_bounds[r], t1 = M->t_bounds[r + 1], tl = t1 - t0;
+  DevBuf<int32_t> cnt_all;
+  cnt_all.alloc(n);
+  row_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(trl.p, n, cnt_all.p);
+  CK(cudaGetLastError());
+  std::vector<int64_t> so(G + 1), ro(G + 1);
+  for (int h = 0; h <= G; ++h) so[h] = M->t_bounds[h] * 4;
+  for (int g = 0; g <= G; ++g) ro[g] = static_cast<int64_t>(g) * tl * 4;
+  DevBuf<int32_t> cnt_in;
+  cnt_in.alloc(static_cast<size_t>(G) * tl);
+  CK(cudaStreamSynchronize(s));
+  alltoallv_bytes(M, reinterpret_cast<const char*>(cnt_all.p), so,
+                  reinterpret_cast<char*>(cnt_in.p), ro);
+  // entry offsets: what this rank sends to h, and (counts summed) what it gets
+  std::vector<int32_t> cin(static_cast<size_t>(G) * tl);
+  if (!cin.empty())
+    CK(cudaMemcpy(cin.data(), cnt_in.p, cin.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> se(G + 1), re(G + 1, 0);
+  for (int h = 0; h <= G; ++h) se[h] = trl_h[M->t_bounds[h]];
+  for (int g = 0; g < G; ++g) {
+    int64_t c = 0;
+    for (int64_t j = 0; j < tl; ++j) c += cin[static_cast<size_t>(g) * tl + j];
+    re[g + 1] = re[g] + c;
+  }
+  const int64_t nt = re[G];  // this rank's entries of A^T
+  require(nt == rpT[t1] - rpT[t0], "sharded setup: A^T entry count mismatch");
+  DevBuf<int32_t> ci_in;
+  DevBuf<double> va_in;
+  ci_in.alloc(nt);
+  va_in.alloc(nt);
+  {
+    std::vector<int64_t> sb(G + 1), rb(G + 1);
+    for (int h = 0; h <= G; ++h) sb[h] = se[h] * 4, rb[h] = re[h] * 4;
+    alltoallv_bytes(M, reinterpret_cast<const char*>(tcl.p), sb,
+                    reinterpret_cast<char*>(ci_in.p), rb);
+    for (int h = 0; h <= G; ++h) sb[h] = se[h] * 8, rb[h] = re[h] * 8;
+    alltoallv_bytes(M, reinterpret_cast<const char*>(tvl.p), sb,
+                    reinterpret_cast<char*>(va_in.p), rb);
+  }
+  pt.mark(s, "all-to-all");
+  // merge: row j of the shard = the runs of sources 0, 1, ..., G-1 in order
+  std::vector<int64_t> src_off(static_cast<size_t>(G) * tl), dst_off(src_off.size());
+  {
+    std::vector<int64_t> pos(static_cast<size_t>(tl));
+    for (int64_t j = 0; j < tl; ++j) pos[j] = rpT[t0 + j] - rpT[t0];
+    for (int g = 0; g < G; ++g) {
+      int64_t sp = re[g];
+      for (int64_t j = 0; j < tl; ++j) {
+        const size_t q = static_cast<size_t>(g) * tl + j;
+        src_off[q] = sp;
+        dst_off[q] = pos[j];
+        sp += cin[q];
+        pos[j] += cin[q];
+      }
+    }
+  }
+  DevBuf<int64_t> so_d, do_d;
+  so_d.alloc(src_off.size());
+  do_d.alloc(dst_off.size());
+  M->t_rp.alloc(tl + 1);
+  M->t_ci.alloc(nt);
+  M->t_va.alloc(nt);
+  std::vector<int64_t> trp(static_cast<size_t>(tl) + 1);
+  for (int64_t j = 0; j <= tl; ++j) trp[j] = rpT[t0 + j] - rpT[t0];
+  CK(cudaMemcpyAsync(M->t_rp.p, trp.data(), (tl + 1) * 8, cudaMemcpyHostToDevice, s));
+  if (!src_off.empty()) {
+    CK(cudaMemcpyAsync(so_d.p, src_off.data(), src_off.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(do_d.p, dst_off.data(), dst_off.size() * 8, cudaMemcpyHostToDevice, s));
+    const int64_t runs = static_cast<int64_t>(src_off.size());
+    merge_runs_kernel<<<static_cast<unsigned>((runs * 8 + 255) / 256), 256, 0, s>>>(
+        so_d.p, do_d.p, cnt_in.p, runs, ci_in.p, va_in.p, M->t_ci.p, M->t_va.p);
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(s));
+  pt.mark(s, "merge");
+  M->A = {ml, n, nl, M->a_rp.p, M->a_ci.p, M->a_va.p};
+  M->AT = {tl, m, nt, M->t_rp.p, M->t_ci.p, M->t_va.p};
+  const std::vector<int64_t>& la = rph;
+  upload_plans(M, plan_tiles(la.data(), ml, 0), plan_tiles(trp.data(), tl, 1));
+  build_block_layout(M);
+  build_slot_layout(M, rpA_full.p, rpT_full.p);
+  build_sell_layout(M, true);
+  CK(cudaStreamSynchronize(s));
+  pt.mark(s, "plan");
 }
 
 void alloc_workspaces(equil_matrix* M, PhaseTimer* pt = nullptr);
@@ -1085,11 +1361,9 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     else
       upload_plans(M, plan_tiles(row_ptr, m, 0), planT);
     pt.mark(s, "upload plans");
-    // values are needed from here on only by the opt-in panel / blocked layouts
-    const bool late_values = !M->use_panels && M->nblk[0] <= 1 && M->nblk[1] <= 1;
+    // values are needed from here on only by the blocked layouts
+    const bool late_values = M->nblk[0] <= 1 && M->nblk[1] <= 1;
     if (!late_values) values_arrived();
-    build_panel_layout(M, row_ptr, rpT.data());
-    pt.mark(s, "panels");
     build_sell_layout(M, !late_values);
     pt.mark(s, "sell");
     if (late_values) {
@@ -1131,8 +1405,8 @@ void set_l2_window(equil_matrix* M, cudaStream_t st, const void* base, size_t by
 }
 
 void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
-  // each vector padded to whole panels (the panel traversal bulk-copies them)
-  auto whole = [](int64_t x) { return (x + eqb::kPanelW - 1) / eqb::kPanelW * eqb::kPanelW; };
+  // each vector padded to whole 32 KB granules (aligned bases for every copy)
+  auto whole = [](int64_t x) { return (x + 4095) / 4096 * 4096; };
   const int64_t np = whole(M->n_pad()), mp = whole(M->m_pad());
   // the gathered vectors, then the device barrier words (fused all-gather)
   const int64_t xlen = 2 * (np + mp) + eqb::kBarWords;
@@ -1302,7 +1576,14 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
       M->pre_total = pre->total;
     }
     pt.mark(s, "setup");
-    // full A on device (uploaded once; shards are sliced from it)
+    if (M->world > 1) {  // each rank uploads and transposes only its rows
+      create_sharded(M.get(), row_ptr, col, val, pt);
+      alloc_workspaces(M.get(), &pt);
+      CK(cudaStreamSynchronize(s));
+      *out = M.release();
+      return;
+    }
+    // full A on device (uploaded once)
     DevBuf<int64_t> rp;
     DevBuf<int32_t> ci;
     DevBuf<double> va;
@@ -1352,16 +1633,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     CK(cudaMemcpyAsync(&wh, where.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     pt.mark(s, "validate");
-    if (wh != ~0ULL) {
-      const int cls = static_cast<int>(wh >> 40);
-      const int64_t k = static_cast<int64_t>(wh & ((1ULL << 40) - 1));
-      const int64_t i = std::upper_bound(row_ptr, row_ptr + m + 1, k) - row_ptr - 1;
-      const std::string at = "(" + std::to_string(i) + ", " + std::to_string(col[k]) + ")";
-      if (cls == 0) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: entry " + at + " out of range");
-      if (cls == 1) fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: duplicate entry " + at);
-      fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: columns not ascending at entry " + at +
-                             " (canonical CSR required)");
-    }
+    if (wh != ~0ULL) fail_invalid_entry(wh, row_ptr, m, col);
     finish_sparse(M.get(), rp, ci, va, row_ptr, pt, &planA, &planner);
     *out = M.release();
   });
@@ -1809,14 +2081,6 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       }
       return a;
     };
-    eqb::PanelArgs panel_args{};
-    panel_args.bands = M->pbands.p;
-    for (int k = 0; k < 2; ++k) {
-      panel_args.chunks[k] = M->pchunks[k].p;
-      panel_args.val[k] = M->pval[k].p;
-      panel_args.col[k] = M->pcol[k].p;
-      panel_args.runs[k] = M->pruns[k].p;
-    }
     auto dense_args = [&](int t) {
       eqb::DenseIterArgs a{};
       a.A = M->Ad.p;
@@ -1856,9 +2120,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
         for (int rd = 0; rd < rounds; ++rd) {  // column-block rounds (1 unless blocked)
           eqb::SgdIterArgs a = iter_args(t);
           a.round = rd;
-          if (M->n_pbands) {
-            CK(eqb::launch_sgd_panel(a, panel_args, M->n_pbands, s));
-          } else if (M->sell) {
+          if (M->sell) {
             eqb::SellArgs sa{};
             sa.xlen[0] = M->n_pad();  // A's rows gather xs, A^T's xw
             sa.xlen[1] = M->m_pad();
@@ -2188,7 +2450,7 @@ namespace eqe {
 // one matvec pass of B (scaled by scale when non-null) in the given mode
 void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
                 const double* scale, const double* prev, const double* coef,
-                const int* skip) {
+                const int* skip, bool slotted) {
   if (M->dense) {
     eqb::DensePassArgs a{};
     a.A = M->Ad.p;
@@ -2221,7 +2483,7 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
   a.mode = mode;
   a.skip = skip;
   if (M->sell && M->sell_passes) {
-    sell_pass(M, adjoint ? 1 : 0, a, nullptr);
+    sell_pass(M, adjoint ? 1 : 0, a, nullptr, false, slotted);
     return;
   }
   CK(eqb::launch_pass(a, adjoint ? M->n_t : M->n_a, M->stream));
@@ -2236,7 +2498,8 @@ bool pair_layout(const equil_matrix* M) { return !M->dense && M->sell && M->sell
 void apply_pass_dual(equil_matrix* M, const double* xg0, double* out0, int mode0,
                      const double* scale0, const double* prev0, const double* coef0,
                      const double* xg1, double* out1, int mode1, const double* scale1,
-                     const double* prev1, const double* coef1, bool pair = false) {
+                     const double* prev1, const double* coef1, bool pair = false,
+                     bool slotted = false) {
   if (M->dense) {
     apply_pass(M, false, xg0, out0, mode0, scale0, prev0, coef0);
     apply_pass(M, false, xg1, out1, mode1, scale1, prev1, coef1);
@@ -2253,7 +2516,7 @@ void apply_pass_dual(equil_matrix* M, const double* xg0, double* out0, int mode0
   a.xg = xg0; a.out = out0; a.mode = mode0; a.scale = scale0; a.prev = prev0; a.coef = coef0;
   b.xg = xg1; b.out = out1; b.mode = mode1; b.scale = scale1; b.prev = prev1; b.coef = coef1;
   if (M->sell && M->sell_passes) {
-    sell_pass(M, 0, a, &b, pair);
+    sell_pass(M, 0, a, &b, pair, slotted);
     return;
   }
   if (pair) throw std::runtime_error("apply_pass_dual: interleaved pair without slices");
@@ -2330,6 +2593,13 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
   // after the x update (e.v is only read by that pass)
   const bool pair = pair_layout(M);
   const int64_t os = pair ? 2 : 1;
+  // slotted: the gathered vectors (d.u for the A^T pass, the (e.x, e.v) pair
+  // for the A pass) are written in the SGD loop's hot-first slot layout, so
+  // the passes run on the SGD's slot-mapped interleaved columns and A's
+  // longest rows -- gathered by most rows of A^T -- stay L1-resident
+  const bool slotted = pair && M->slots && M->sell_nb == 1;
+  const int32_t* slot_u = slotted ? M->wmap.p + L.pa : nullptr;  // local A row -> slot
+  const int32_t* slot_v = slotted ? M->smap.p + L.pt : nullptr;  // local A^T row -> slot
   DevBuf<double> u, v, w, un, du, vn, ev, ex, xv, r;
   u.alloc(L.mL); v.alloc(L.nL); w.alloc(L.nL); x.alloc(L.nL);
   un.alloc(L.mP); du.alloc(L.mP); r.alloc(L.mP);
@@ -2342,11 +2612,11 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     ex.alloc(L.nP);
   }
   double* unL = un.p + L.pa;
-  double* duL = du.p + L.pa;
+  double* duL = slotted ? du.p : du.p + L.pa;  // slotted: slot maps hold absolute positions
   double* rL = r.p + L.pa;
   double* vnL = vn.p + L.pt;
-  double* evL = pair ? xv.p + 2 * L.pt + 1 : ev.p + L.pt;
-  double* exL = pair ? xv.p + 2 * L.pt : ex.p + L.pt;
+  double* evL = pair ? xv.p + (slotted ? 0 : 2 * L.pt) + 1 : ev.p + L.pt;
+  double* exL = pair ? xv.p + (slotted ? 0 : 2 * L.pt) : ex.p + L.pt;
   auto gather_ev = [&] {
     if (pair) allgather_padded(M, xv.p, 2 * M->t_max);
     else L.gather(ev.p, false);
@@ -2362,9 +2632,10 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
 
   CK(cudaMemcpyAsync(unL, c, L.mL * 8, cudaMemcpyDeviceToDevice, s));
   L.norm(un.p, true, sc + 0);  // beta = |c|
-  CK(eqb::launch_lsqr_normalize(u.p, c, sc + 0, duL, d, L.mL, nullptr, nullptr, s));
+  CK(eqb::launch_lsqr_normalize(u.p, c, sc + 0, duL, d, L.mL, nullptr, nullptr, s, 1, slot_u));
   L.gather(du.p, true);
-  apply_pass(M, true, du.p, vnL, eqb::kPassScaled, e, nullptr, nullptr);  // v = B^T u
+  apply_pass(M, true, du.p, vnL, eqb::kPassScaled, e, nullptr, nullptr, nullptr,
+             slotted);  // v = B^T u
   ++st.adjoints;
   L.norm(vn.p, false, sc + 1);
   double beta = read_scalar(M, sc + 0);
@@ -2373,7 +2644,7 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     st.breakdown = true;
     return;
   }
-  CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, dummy, nullptr, s, os));
+  CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, dummy, nullptr, s, os, slot_v));
   gather_ev();
   CK(cudaMemcpyAsync(w.p, v.p, L.nL * 8, cudaMemcpyDeviceToDevice, s));
   double phibar = beta, rhobar = alpha;
@@ -2414,17 +2685,18 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     if (t == 1) {
       if (pair)
         apply_pass_dual(M, xv.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, nullptr, unL,
-                        eqb::kPassLsqrU, d, u.p, sc + 1, true);
+                        eqb::kPassLsqrU, d, u.p, sc + 1, true, slotted);
       else
         apply_pass(M, false, ev.p, unL, eqb::kPassLsqrU, d, u.p, sc + 1);
     }
     CK(cudaMemsetAsync(inv, 0, sizeof(int), s));
     L.norm(un.p, true, sc + 0);
-    CK(eqb::launch_lsqr_normalize(u.p, unL, sc + 0, duL, d, L.mL, inv, nullptr, s));
+    CK(eqb::launch_lsqr_normalize(u.p, unL, sc + 0, duL, d, L.mL, inv, nullptr, s, 1, slot_u));
     L.gather(du.p, true);
-    apply_pass(M, true, du.p, vnL, eqb::kPassLsqrV, e, v.p, sc + 0, inv);  // B^T u - beta v
+    apply_pass(M, true, du.p, vnL, eqb::kPassLsqrV, e, v.p, sc + 0, inv,
+               slotted);  // B^T u - beta v
     L.norm(vn.p, false, sc + 1);
-    CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, inv, inv, s, os));
+    CK(eqb::launch_lsqr_normalize(v.p, vnL, sc + 1, evL, e, L.nL, inv, inv, s, os, slot_v));
     if (!pair) gather_ev();  // pair: travels with e.x below
     CK(cudaMemcpyAsync(hs, sc, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&hs->inv, inv, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2449,14 +2721,15 @@ void lsqr_core(equil_matrix* M, const double* c, const double* b_loc, double bno
     rhobar = -cs * alpha;
     const double phi = cs * phibar;
     phibar = sn * phibar;
-    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, exL, L.nL, s, os));
+    CK(eqb::launch_lsqr_xw_update(x.p, w.p, v.p, phi / rho, theta / rho, e, exL, L.nL, s, os,
+                                  slot_v));
     gather_ex();
     st.iterations = t;
     // residual b - A(e.x) and, in the same traversal of A, the next iteration's
     // B v - alpha u (its inputs v, alpha, u are final here; unused if we stop)
     if (pair)
       apply_pass_dual(M, xv.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, nullptr, unL,
-                      eqb::kPassLsqrU, d, u.p, sc + 1, true);
+                      eqb::kPassLsqrU, d, u.p, sc + 1, true, slotted);
     else
       apply_pass_dual(M, ex.p, rL, eqb::kPassResid, nullptr, b_loc, nullptr, ev.p, unL,
                       eqb::kPassLsqrU, d, u.p, sc + 1);

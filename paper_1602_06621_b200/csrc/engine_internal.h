@@ -38,7 +38,8 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 typedef int ncclResult_t;
-constexpr int ncclUint8 = 1, ncclUint32 = 3, ncclFloat64 = 8, ncclMax = 2, ncclMin = 3;
+constexpr int ncclUint8 = 1, ncclInt32 = 2, ncclUint32 = 3, ncclInt64 = 4, ncclFloat64 = 8;
+constexpr int ncclSum = 0, ncclMax = 2, ncclMin = 3;
 
 struct NcclApi {
   void* h = nullptr;
@@ -49,6 +50,10 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
 };
@@ -68,9 +73,13 @@ inline NcclApi& nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(api.h, "ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(api.h, "ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(api.h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(api.h, "ncclGroupEnd"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
-             api.AllReduce;
+             api.AllReduce && api.Send && api.Recv && api.GroupStart && api.GroupEnd;
   });
   return api;
 }
@@ -373,6 +382,7 @@ struct HostExchange {
   virtual void put(int rank, const void* data, size_t bytes) = 0;
   virtual const char* slot(int g) = 0;
   virtual bool in_process() const = 0;
+  virtual size_t capacity() const = 0;  // bytes one put may carry
 };
 struct ThreadExchange : HostExchange {
   std::mutex mu;
@@ -396,6 +406,7 @@ struct ThreadExchange : HostExchange {
   }
   const char* slot(int g) override { return slots[g].data(); }
   bool in_process() const override { return true; }
+  size_t capacity() const override { return SIZE_MAX; }
 };
 std::shared_ptr<HostExchange> shm_exchange(const void* id128, int world, int rank);
 inline std::shared_ptr<HostExchange> host_exchange(const void* id128, int world) {
@@ -456,10 +467,6 @@ struct equil_matrix {
   // launch's window is its block (EQUIL_BLOCK_WIN)
   size_t l2_carve = 0, l2_max_window = 0, l2_default_bytes = 0;
   bool block_win = true;
-  // column-panel layout of the local A / A^T shards (panel.cu), built when
-  // EQUIL_PANEL=1 at creation; n_pbands == 0 selects the row-slice traversal
-  // above (the default: faster on B200)
-  bool use_panels = false;
   // hot-first slot layout of the gathered vectors (build_slot_layout): the SGD
   // passes read CSR copies whose column indices point at slots, and the
   // epilogues write each row's next value at its slot
@@ -513,18 +520,13 @@ struct equil_matrix {
   bool sell_passes = true;
   bool sell_values_pending = false;  // interleaved values not built yet (setup)  // EQUIL_SELL_PASSES=0: generic passes on the staged kernels
   bool sell_pass = false;
+  bool sell_order_up = false;  // sell_pidx uploaded
   DevBuf<int32_t> sell_pci[2], sell_pidx[2];
   // column blocks of the gathered vectors (build_block_layout): per matrix
   int nblk[2] = {1, 1};
   int64_t bwidth[2] = {0, 0};
   DevBuf<int32_t> bnd[2];
   DevBuf<double> carry[2];  // wmap / smap: padded position -> slot
-  DevBuf<double> pval[2];
-  DevBuf<uint16_t> pcol[2];
-  DevBuf<uint32_t> pruns[2];
-  DevBuf<eqb::PanelChunk> pchunks[2];
-  DevBuf<eqb::PanelBand> pbands;
-  int n_pbands = 0;
 
   // dense
   DevBuf<double> Ad, colpart;
@@ -613,7 +615,7 @@ void canon_reduce(equil_matrix* M, const double* x, int64_t len, double* out, in
                   double coef = 0.0, bool sqrt_out = false);
 void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, int mode,
                 const double* scale, const double* prev, const double* coef,
-                const int* skip = nullptr);
+                const int* skip = nullptr, bool slotted = false);
 double read_scalar(equil_matrix* M, const double* dev);
 // host -> device copy on M->stream: a pull kernel from a thread-local mapped
 // pinned arena while M->pull_uploads (setup, A's values on the copy engine),

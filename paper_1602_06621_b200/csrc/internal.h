@@ -215,58 +215,6 @@ cudaError_t launch_sgd_update_rows(const SgdIterArgs& a, int64_t m_loc, int64_t 
 cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int variant,
                                  cudaStream_t s);
 
-// ---- column-panel traversal (panel.cu) ------------------------------------
-// The gathered vector is cut into panels of kPanelW coordinates and the rows
-// into bands of <= kBandRows rows.  Each band's entries are stored panel-major
-// (band, panel, row, column): one CTA walks its band panel by panel with the
-// panel resident in shared memory (bulk-copied, double-buffered) and the
-// band's running row sums in shared memory.  Within a row the entries are
-// still visited in ascending column order, so every row sum is the same
-// sequential CSR-order chain as the reference's.
-#ifndef EQ_PANEL_W
-#define EQ_PANEL_W 4096
-#endif
-constexpr int kPanelW = EQ_PANEL_W;        // coordinates per panel (power of two)
-constexpr int kPanelChunk = 4096;          // entries staged per round
-constexpr int kBandRows = 12288;           // running sums held in shared memory
-constexpr int kPanelThreads = 1024;
-static_assert((kPanelW & (kPanelW - 1)) == 0 && kPanelW <= 65536, "panel width");
-static_assert(kBandRows < 65536, "row index packs into 16 bits");
-
-// A round of <= kPanelChunk consecutive entries of one (band, panel) segment,
-// and the row runs inside it (maximal stretches of one row, in order).
-struct PanelChunk {
-  int64_t e0;          // first entry (index into the panel-major arrays)
-  int32_t q0;          // first run (index into the run list)
-  int32_t len;         // entries
-  int32_t nruns;
-  int32_t panel;
-  int32_t next_panel;  // next panel this band visits after `panel`, or -1
-  int32_t band;
-};
-struct PanelBand {
-  int32_t r0, rows;  // local rows [r0, r0 + rows)
-  int32_t c0, c1;    // chunks [c0, c1) of matrix `mat`
-  int32_t mat, pad;
-};
-struct PanelArgs {
-  const PanelBand* bands;
-  const PanelChunk* chunks[2];
-  const double* val[2];     // panel-major values
-  const uint16_t* col[2];   // column - panel * kPanelW
-  const uint32_t* runs[2];  // (start within the round) << 16 | (row - band r0)
-};
-// Build the panel-major copy of a CSR matrix whose columns index a gathered
-// vector of length vec_len; band_r0 = nbands + 1 row boundaries.  out_val /
-// out_col hold nnz entries; *runs and *chunks are cudaMalloc'ed (caller
-// frees); band_c receives the nbands + 1 chunk boundaries.
-cudaError_t build_panels(const DevCsr& M, int64_t vec_len, const std::vector<int64_t>& band_r0,
-                         double* out_val, uint16_t* out_col, uint32_t** runs, int64_t* nruns,
-                         PanelChunk** chunks, int64_t* nchunks, std::vector<int64_t>* band_c,
-                         cudaStream_t s);
-cudaError_t launch_sgd_panel(const SgdIterArgs& a, const PanelArgs& p, int nbands,
-                             cudaStream_t s);
-
 enum PassMode : int {
   kPassPlain = 0,    // y = acc
   kPassLsqrU = 1,    // out = s_i*acc - alpha*u_i   (s = d or 1)
@@ -472,11 +420,15 @@ cudaError_t launch_lsqr_normalize(double* dst, const double* src,
                                   const double* norm_dev, double* scaled_out,
                                   const double* scale, int64_t len,
                                   int* invariant, int* skip_in,
-                                  cudaStream_t s, int64_t ostride = 1);
-// ostride: scaled_out / ex element stride (2: one half of an interleaved pair)
+                                  cudaStream_t s, int64_t ostride = 1,
+                                  const int32_t* slot = nullptr);
+// ostride: scaled_out / ex element stride (2: one half of an interleaved pair);
+// slot (nullable): element k goes to position slot[k] (the hot-first slot
+// layout of the gathered vectors, engine.cu build_slot_layout), else to k
 cudaError_t launch_lsqr_xw_update(double* x, double* w, const double* v,
                                   double c1, double c2, const double* e,
-                                  double* ex, int64_t n, cudaStream_t s, int64_t ostride = 1);
+                                  double* ex, int64_t n, cudaStream_t s, int64_t ostride = 1,
+                                  const int32_t* slot = nullptr);
 cudaError_t launch_rms_terms(int mat, const DevCsr& M, const double* eu,
                              const double* ev, double* out, int64_t goff,
                              double target, cudaStream_t s);

@@ -1098,7 +1098,8 @@ namespace {
 __global__ void lsqr_normalize_kernel(double* dst, const double* src,
                                       const double* norm_dev, double* scaled_out,
                                       const double* scale, int64_t len,
-                                      int* invariant, int* skip_in, int64_t ostride) {
+                                      int* invariant, int* skip_in, int64_t ostride,
+                                      const int32_t* slot) {
   if (skip_in && *skip_in) return;
   const double nrm = *norm_dev;
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -1109,19 +1110,21 @@ __global__ void lsqr_normalize_kernel(double* dst, const double* src,
   if (k >= len) return;
   const double q = __ddiv_rn(src[k], nrm);
   dst[k] = q;
-  if (scaled_out) scaled_out[k * ostride] = scale ? __dmul_rn(scale[k], q) : q;
+  const int64_t o = slot ? static_cast<int64_t>(slot[k]) : k;
+  if (scaled_out) scaled_out[o * ostride] = scale ? __dmul_rn(scale[k], q) : q;
 }
 
 __global__ void lsqr_xw_kernel(double* x, double* w, const double* v, double c1,
                                double c2, const double* e, double* ex, int64_t n,
-                               int64_t ostride) {
+                               int64_t ostride, const int32_t* slot) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= n) return;
   const double wk = w[k];
   const double xk = __dadd_rn(x[k], __dmul_rn(c1, wk));  // x += (phi/rho) w
   x[k] = xk;
   w[k] = __dsub_rn(v[k], __dmul_rn(c2, wk));           // w = v - (theta/rho) w
-  if (ex) ex[k * ostride] = e ? __dmul_rn(e[k], xk) : xk;
+  const int64_t o = slot ? static_cast<int64_t>(slot[k]) : k;
+  if (ex) ex[o * ostride] = e ? __dmul_rn(e[k], xk) : xk;
 }
 
 }  // namespace
@@ -1130,19 +1133,20 @@ cudaError_t launch_lsqr_normalize(double* dst, const double* src,
                                   const double* norm_dev, double* scaled_out,
                                   const double* scale, int64_t len,
                                   int* invariant, int* skip_in, cudaStream_t s,
-                                  int64_t ostride) {
+                                  int64_t ostride, const int32_t* slot) {
   const int64_t nb = std::max<int64_t>(1, (len + 255) / 256);
   lsqr_normalize_kernel<<<static_cast<unsigned>(nb), 256, 0, s>>>(
-      dst, src, norm_dev, scaled_out, scale, len, invariant, skip_in, ostride); count_launch(s);
+      dst, src, norm_dev, scaled_out, scale, len, invariant, skip_in, ostride, slot); count_launch(s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lsqr_xw_update(double* x, double* w, const double* v,
                                   double c1, double c2, const double* e,
-                                  double* ex, int64_t n, cudaStream_t s, int64_t ostride) {
+                                  double* ex, int64_t n, cudaStream_t s, int64_t ostride,
+                                  const int32_t* slot) {
   if (n == 0) return cudaSuccess;
   lsqr_xw_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, w, v, c1, c2,
-                                                                        e, ex, n, ostride); count_launch(s);
+                                                                        e, ex, n, ostride, slot); count_launch(s);
   return cudaGetLastError();
 }
 

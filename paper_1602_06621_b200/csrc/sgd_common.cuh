@@ -1,5 +1,5 @@
 // sgd_common.cuh -- device helpers shared by the SGD traversals (kernels.cu:
-// warp tiles / long slices, panel.cu: column panels): streamed loads, the
+// staged warp tiles / long rows, sell.cu: interleaved slices): streamed loads, the
 // sequential row sum and the fused u/v epilogue.
 #pragma once
 

@@ -291,11 +291,13 @@ def test_sgd_scaled_config3_bit_exact(C):
 
 
 @pytest.mark.parametrize("case", ["sp", "lr", "c3"])
-def test_panel_traversal_bit_exact(C, golden, monkeypatch, case):
-    """The opt-in column-panel traversal (panel.cu, EQUIL_PANEL=1): same
-    trajectory bit for bit -- golden cases (rows crossing panels and rounds)
-    and c3's generator at 2% scale (bands, many panels, long rows)."""
-    monkeypatch.setenv("EQUIL_PANEL", "1")
+@pytest.mark.parametrize("lvariant", ["2", "3"])
+def test_long_slice_variants_bit_exact(C, golden, monkeypatch, case, lvariant):
+    """The long-slice ring at other shapes than the default (EQUIL_SELL_LVARIANT:
+    2 entries x 15 stagers, 4 x 7 with four CTAs per SM): same trajectory bit for
+    bit -- golden cases and c3's generator at 2% scale (rows of up to 10^4
+    entries), so the ring protocol does not depend on its shape."""
+    monkeypatch.setenv("EQUIL_SELL_LVARIANT", lvariant)
     if case == "c3":
         from paper_1602_06621_b200 import configs
         inst = configs.config(3, scale=0.02)
@@ -745,13 +747,16 @@ def test_sharded_engine_bit_identical_via_host_exchange(C, golden, monkeypatch, 
     monkeypatch.setenv("EQUIL_HOST_EXCHANGE", "1")
     monkeypatch.setenv("EQUIL_P2P", p2p)
     nid = os.urandom(128)
-    Ms = [eq.ExplicitMatrix.from_csr(A.m, A.n, A.row_ptr, A.col, A.val, rank=r, world_size=world,
-                                     nccl_id=nid) for r in range(world)]
+    # creation is collective (sharded setup: all-reduce and all-to-all between
+    # the ranks), so every rank creates its handle on its own thread
+    Ms = [None] * world
     out = [None] * world
     errs = []
 
     def run(r):
         try:
+            Ms[r] = eq.ExplicitMatrix.from_csr(A.m, A.n, A.row_ptr, A.col, A.val, rank=r,
+                                               world_size=world, nccl_id=nid)
             s = eq.sgd_equilibrate(Ms[r], p, d)
             lp = eq.lsqr(Ms[r], b, 12, 0.0)
             pp = eq.lsqr_preconditioned(Ms[r], b, eq.EquilibrationParams(iterations=8, seed=2),

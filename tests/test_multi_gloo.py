@@ -252,3 +252,74 @@ def test_sharded_lsqr_bit_identical_world2(golden):
         assert p.exitcode == 0
     assert np.array_equal(hist, want.residual_history)
     assert np.array_equal(X, want.x)
+
+
+def _transpose_worker(rank, world, port, A_arrays, out_q):
+    """The sharded setup of engine.cu create_sharded on CPU: local rows of A,
+    local transpose, global A^T row pointers as the all-reduced sum of the local
+    prefix sums, all-to-all of the A^T row ranges (counts, columns, values), and
+    the rank-order merge."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    import paper_1602_06621_b200 as eq
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, n, rp, col, val = A_arrays
+    O = oracle.c_oracle()
+    ab = eq.partition_rows(rp, world)
+    a0, a1 = ab[rank], ab[rank + 1]
+    k0, k1 = rp[a0], rp[a1]
+    Al = oracle.CsrArrays(a1 - a0, n, rp[a0:a1 + 1] - k0, col[k0:k1], val[k0:k1])
+    Tl = O.transpose(Al)  # n x (a1 - a0), columns = local rows
+    glob = torch.from_numpy(Tl.row_ptr.astype(np.int64).copy())
+    dist.all_reduce(glob)  # sum of prefix sums = CSR(A^T)'s row pointers
+    rpT = glob.numpy()
+    tb = eq.partition_rows(rpT, world)
+    cnt = np.diff(Tl.row_ptr)
+    pieces = [(cnt[tb[h]:tb[h + 1]], Tl.col[Tl.row_ptr[tb[h]]:Tl.row_ptr[tb[h + 1]]] + a0,
+               Tl.val[Tl.row_ptr[tb[h]]:Tl.row_ptr[tb[h + 1]]]) for h in range(world)]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, pieces)  # all-to-all through a gather
+    t0, t1 = tb[rank], tb[rank + 1]
+    rows = []
+    offs = [0] * world
+    for j in range(t1 - t0):
+        cs, vs = [], []
+        for g in range(world):
+            c, cc, vv = gathered[g][rank]
+            o, k = offs[g], int(c[j])
+            cs.append(cc[o:o + k])
+            vs.append(vv[o:o + k])
+            offs[g] += k
+        rows.append((np.concatenate(cs), np.concatenate(vs)))
+    out_q.put((rank, t0, t1, rpT, rows))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_setup_transpose_alltoall(golden, world):
+    """Each rank's merged A^T shard equals the rows cut from the full
+    transpose, bit for bit (explicit_matrix.cpp:117-125)."""
+    from conftest import csr_from_golden
+    import oracle
+    A = csr_from_golden(golden, "sp")
+    full = oracle.c_oracle().transpose(A)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transpose_worker,
+                         args=(r, world, port, (A.m, A.n, A.row_ptr, A.col, A.val), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, t0, t1, rpT, rows in got:
+        assert np.array_equal(rpT, full.row_ptr)
+        for j, (c, v) in enumerate(rows):
+            k0, k1 = full.row_ptr[t0 + j], full.row_ptr[t0 + j + 1]
+            assert np.array_equal(c, full.col[k0:k1]) and np.array_equal(v, full.val[k0:k1])
