@@ -298,31 +298,17 @@ struct PassOp {  // generic passes (pass_epilogue); one matrix per launch
 struct PassPairOp : PassOp<2> {
   static constexpr bool PAIR = true;
 };
-template <class Op>
-__host__ __device__ constexpr bool is_sgd_pass() { return Op::NV == 1 && !std::is_base_of<PassOp<1>, Op>::value; }
-
-// EQ_XS_NA (A/B build knob): gathers of A's rows (xs: uniform columns, no
-// reuse) do not allocate in L1, leaving it to the hot slots of xw -- 1: in the
-// long-slice kernel, 2: in both kernels
-#ifndef EQ_XS_NA
-#define EQ_XS_NA 0
-#endif
-__device__ __forceinline__ double ld_gather_na(const double* p) {
-  double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
 
 // the gathered value(s) of slot c: one vector, two vectors, or one interleaved pair
 template <class Op>
 __device__ __forceinline__ void gather_x(const double* __restrict__ x, const double* __restrict__ x2,
-                                         int32_t c, double& g, double& g2, bool na = false) {
+                                         int32_t c, double& g, double& g2) {
   if constexpr (Op::PAIR) {
     const double2 p = __ldg(reinterpret_cast<const double2*>(x) + c);
     g = p.x;
     g2 = p.y;
   } else {
-    g = na ? ld_gather_na(x + c) : __ldg(x + c);
+    g = __ldg(x + c);
     if constexpr (Op::NV == 2) g2 = __ldg(x2 + c);
   }
 }
@@ -358,7 +344,7 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
     for (int b = 0; b < B; ++b)
       if (full || k0 + b < len) {
         EQ_CHECK(c[b] >= 0 && c[b] < sa.xlen[mat]);
-        gather_x<Op>(x, x2, c[b], g[b], g2[b], EQ_XS_NA >= 2 && is_sgd_pass<Op>() && mat == 0);
+        gather_x<Op>(x, x2, c[b], g[b], g2[b]);
       }
 #pragma unroll
     for (int b = 0; b < B; ++b)
@@ -492,7 +478,7 @@ sell_long_kernel(const Op op, const SellArgs sa) {
       for (int b = 0; b < B; ++b)
         if (k0 + b < len) {
           EQ_CHECK(c[b] >= 0 && c[b] < sa.xlen[mat]);
-          gather_x<Op>(x, x2, c[b], g[b], g2[b], EQ_XS_NA >= 1 && is_sgd_pass<Op>() && mat == 0);
+          gather_x<Op>(x, x2, c[b], g[b], g2[b]);
         }
       const int bi = r % R;
       if (r >= R) mbar_wait(&empty[bi], ((r / R) - 1) & 1);
