@@ -247,6 +247,7 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SELL")) M->use_sell = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL_VARIANT")) M->sell_variant = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_LONG")) M->sell_long = atoi(e);
+  if (const char* e = getenv("EQUIL_SELL_QUAD")) M->sell_quad = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL_LVARIANT")) M->sell_lvariant = atoi(e);
   if (const char* e = getenv("EQUIL_SELL_PASSES")) M->sell_passes = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SELL_ORDER")) M->sell_order = atoi(e);
@@ -335,7 +336,10 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
     const SellEnt& e = *order[w].e;
     const int mat = order[w].mat;
     H.slices[w] = {H.total[mat], e.maxlen, e.cnt, static_cast<int16_t>(mat)};
-    H.total[mat] += 32 * static_cast<int64_t>(e.maxlen);
+    // long slices read by the warp-specialised kernel are stored in the quad
+    // layout (128-bit stream loads), padded to a multiple of 4 entries
+    const bool quad = M->sell_long == 2 && M->sell_quad && e.maxlen > eqb::kTileNnz;
+    H.total[mat] += 32 * (quad ? eqb::sell_quad_len(e.maxlen) : static_cast<int64_t>(e.maxlen));
     if (e.maxlen > 0) {
       H.midx[mat].push_back(static_cast<int32_t>(w));
       H.kbp[mat].push_back(H.kbp[mat].back() + (e.maxlen + 31) / 32);
@@ -352,6 +356,11 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
 
 // The generic passes' column arrays (padded coordinates) and per-matrix slice
 // orders, on first use.
+// long slices are in the quad layout when the warp-specialised kernel reads them
+int quad_min(const equil_matrix* M) {
+  return M->sell_long == 2 && M->sell_quad ? eqb::kTileNnz + 1 : 0x7fffffff;
+}
+
 // per-matrix slice orders of the generic passes (both column flavours)
 void ensure_sell_order(equil_matrix* M) {
   if (M->sell_order_up || !M->sell) return;
@@ -385,7 +394,7 @@ void ensure_sell_pass(equil_matrix* M) {
     const eqb::DevCsr& C = mat ? M->AT : M->A;
     CK(eqb::build_sell(C.row_ptr, C.col, nullptr, C.val, dkbp.p, H.kbp[mat].back(), didx.p,
                        static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
-                       M->sell_len.p, nullptr, M->sell_pci[mat].p, nullptr, s));
+                       M->sell_len.p, nullptr, M->sell_pci[mat].p, nullptr, s, quad_min(M)));
     CK(cudaStreamSynchronize(s));
   }
   M->sell_pass = true;
@@ -406,6 +415,7 @@ void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::Pass
   cudaStream_t s = M->stream;
   eqb::SellArgs sa{};
   sa.xlen[0] = sa.xlen[1] = mat ? M->m_pad() : M->n_pad();  // padded coordinates
+  sa.quad = M->sell_long == 2 && M->sell_quad;
   sa.slices = M->sell_slices.p;
   sa.order = M->sell_pidx[mat].p;
   sa.row = M->sell_row.p;
@@ -523,7 +533,7 @@ void build_sell_arrays(equil_matrix* M, int mat, bool cols, bool vals) {
                      H.kbp[mat].back(), didx.p,
                      static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
                      M->sell_len.p, nullptr, cols ? M->sell_ci[mat].p : nullptr,
-                     vals ? M->sell_va[mat].p : nullptr, s));
+                     vals ? M->sell_va[mat].p : nullptr, s, quad_min(M)));
 }
 
 // the values half of build_sell_layout(M, false), after A's values (and
@@ -2124,6 +2134,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
             eqb::SellArgs sa{};
             sa.xlen[0] = M->n_pad();  // A's rows gather xs, A^T's xw
             sa.xlen[1] = M->m_pad();
+            sa.quad = M->sell_long == 2 && M->sell_quad && M->sell_nb == 1;  // see plan_sell
             sa.slices = M->sell_slices.p;
             sa.nslices = M->n_sell;
             sa.row = M->sell_row.p;

@@ -482,6 +482,8 @@ struct equil_matrix {
   // CSR arrays, 1 lane chains in the warp kernel, 2 warp-specialised CTAs
   // (sgd_sell_long_kernel) on the interleaved arrays
   int sell_long = 2;
+  // long slices in the quad layout (128-bit stream loads; EQUIL_SELL_QUAD=0: 1-wide)
+  bool sell_quad = true;
   int sell_variant = 0, sell_lvariant = 0;
   int n_sell_long = 0;  // leading slices with rows longer than kTileNnz
   int sell_order = 0;   // EQUIL_SELL_ORDER: warp slices longest first (0) / in window order (1)

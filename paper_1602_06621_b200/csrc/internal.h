@@ -165,7 +165,14 @@ struct SellArgs {
   const int32_t* ci[2];     // interleaved slot columns
   const double* va[2];      // interleaved values
   int64_t xlen[2];          // length of the gathered vector(s) (checked builds)
+  int quad;                 // 1: long slices (maxlen > kTileNnz) in the quad layout
 };
+// Quad layout of a long slice: entries 4q .. 4q+3 of lane l are adjacent, at
+// off + 128 q + 4 l + (k % 4), so a lane streams its row with 128-bit loads
+// (four columns, two pairs of values); the slice is padded to a multiple of 4
+// entries.  Short slices keep entry k of lane l at off + 32 k + l.
+constexpr int kQuad = 4;
+__host__ __device__ inline int64_t sell_quad_len(int64_t maxlen) { return (maxlen + 3) & ~int64_t(3); }
 // Device flag barrier of the fused all-gather (world > 1, NCCL transport): a
 // tail of kBarWords 64-bit words behind the gathered vectors in xbuf (mapped by
 // every peer): [0, world) the last epoch each rank signalled, [kBarEpoch] this
@@ -186,7 +193,8 @@ cudaError_t launch_pull_copy(void* dst, const void* src_mapped, size_t bytes, cu
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
                        const int64_t* kbp, int64_t items, const int32_t* midx, int nmat_slices,
                        const SellSlice* slices, const int32_t* row, const int32_t* len,
-                       const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s);
+                       const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s,
+                       int quad_min = 0x7fffffff);  // slices with maxlen >= quad_min: quad layout
 // column blocks: per block b and slice lane q, the lane's first entry and
 // entry count in block b (kst / bln[b * 32 nslices + q]) and the per-block
 // slice maxima maxb[b * nslices + w]

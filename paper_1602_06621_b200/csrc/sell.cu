@@ -39,7 +39,7 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
                   const int64_t* __restrict__ kbp, const int32_t* __restrict__ midx, int nms,
                   const SellSlice* __restrict__ slices, const int32_t* __restrict__ row,
                   const int32_t* __restrict__ len, const int32_t* __restrict__ kst,
-                  int32_t* __restrict__ oc, double* __restrict__ ov) {
+                  int32_t* __restrict__ oc, double* __restrict__ ov, int quad_min) {
   __shared__ int32_t tc[2][32][33];
   __shared__ double tv[2][32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -86,10 +86,13 @@ build_sell_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci
       }
   }
   __syncwarp();
-  const int kend = min(32, sd.maxlen - k0);
+  const bool quad = sd.maxlen >= quad_min;
+  const int kend = min(32, static_cast<int>(quad ? sell_quad_len(sd.maxlen) : sd.maxlen) - k0);
   for (int kk = 0; kk < kend; ++kk) {
-    const int64_t dst = sd.off + static_cast<int64_t>(k0 + kk) * 32 + lane;
-    const bool ok = lane < sd.cnt && k0 + kk < mylen;
+    const int k = k0 + kk;
+    const int64_t dst = sd.off + (quad ? static_cast<int64_t>(k >> 2) * 128 + 4 * lane + (k & 3)
+                                       : static_cast<int64_t>(k) * 32 + lane);
+    const bool ok = lane < sd.cnt && k < mylen;
     if (oc) oc[dst] = ok ? tc[warp][kk][lane] : 0;
     if (ov) ov[dst] = ok ? tv[warp][kk][lane] : 0.0;
   }
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(256) sgd_update_rows_kernel(const SgdIterArgs 
   if (k < m_loc + n_loc) {
     const int mat = k >= m_loc ? 1 : 0;
     const int64_t r = mat ? k - m_loc : k;
-    sgd_epilogue(a, mat, r, a.carry[mat][r], fl);
+    sgd_epilogue(a, mat, r, pick(a.carry, mat)[r], fl);
   }
   if (a.npeer) __threadfence_system();
   fl = __reduce_or_sync(0xffffffffu, fl);
@@ -212,6 +215,27 @@ __device__ __forceinline__ int32_t ld_st(const int32_t* p) {
 #endif
 }
 
+// 128-bit / 64-bit streamed loads of the quad layout (same qualifiers as ld_na:
+// no L1 allocation, L2 evict-first)
+__device__ __forceinline__ int4 ld_st4(const int32_t* p) {
+  int4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+__device__ __forceinline__ int2 ld_st2(const int32_t* p) {
+  int2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+__device__ __forceinline__ double2 ld_st2(const double* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+      : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -260,17 +284,17 @@ struct SgdOp {  // the fused u / v update of one SGD iteration
 // the epilogue's dependent loads no longer hold the traversal's warps
 struct SgdSplitOp : SgdOp {
   __device__ void finish(int mat, int32_t r, double acc, double, unsigned&, int64_t) const {
-    a.carry[mat][r] = acc;
+    pick(a.carry, mat)[r] = acc;
   }
   __device__ void end(unsigned) const {}
 };
 // column-block rounds: the running sum of lane q waits in carry[0][q]
 struct SgdBlockOp : SgdOp {
   __device__ double start(int mat, int64_t q) const {
-    return a.round > 0 && a.round < a.nblk[mat] ? a.carry[0][q] : 0.0;
+    return a.round > 0 && a.round < pick(a.nblk, mat) ? a.carry[0][q] : 0.0;
   }
   __device__ void finish(int mat, int32_t r, double acc, double, unsigned& fl, int64_t q) const {
-    if (a.round < a.nblk[mat] - 1) {
+    if (a.round < pick(a.nblk, mat) - 1) {
       a.carry[0][q] = acc;
       return;
     }
@@ -333,8 +357,8 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
   const int mat = sd.mat;
   const int q = 32 * w + lane;
   const int len = __ldg(sa.len + q);
-  const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
-  const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
+  const int32_t* __restrict__ cp = pick(sa.ci, mat) + sd.off + lane;
+  const double* __restrict__ vp = pick(sa.va, mat) + sd.off + lane;
   const double* __restrict__ x = op.x(mat);
   const double* __restrict__ x2 = op.x2(mat);
   double acc = op.start(mat, q), acc2 = 0.0;
@@ -343,7 +367,7 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
 #pragma unroll
     for (int b = 0; b < B; ++b)
       if (full || k0 + b < len) {
-        EQ_CHECK(c[b] >= 0 && c[b] < sa.xlen[mat]);
+        EQ_CHECK(c[b] >= 0 && c[b] < pick(sa.xlen, mat));
         gather_x<Op>(x, x2, c[b], g[b], g2[b]);
       }
 #pragma unroll
@@ -421,9 +445,10 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
 // lanes arrive).  PIPE: a stager issues its next round's loads before this
 // round's gathers.  Products are formed in any order; the adds are the
 // reference's CSR-order chain.
-template <class Op, int B, int S, bool PIPE, int MINB>
+template <class Op, int B, int S, bool PIPE, int MINB, int Q>
 __global__ void __launch_bounds__(32 * (S + 1), MINB)
 sell_long_kernel(const Op op, const SellArgs sa) {
+  static_assert(Q == 1 || (Q == kQuad && (B == 2 || B == 4)), "quad rounds: 2 or 4 entries");
   constexpr int NV = Op::NV;
   constexpr int R = S + 1;
   __shared__ __align__(16) double buf[NV][R][B * 32];
@@ -447,8 +472,8 @@ sell_long_kernel(const Op op, const SellArgs sa) {
   const int len = __ldg(sa.len + q);
   const int rounds = (sd.maxlen + B - 1) / B;
   if (warp > 0) {
-    const int32_t* __restrict__ cp = sa.ci[mat] + sd.off + lane;
-    const double* __restrict__ vp = sa.va[mat] + sd.off + lane;
+    const int32_t* __restrict__ cp = pick(sa.ci, mat) + sd.off + lane;
+    const double* __restrict__ vp = pick(sa.va, mat) + sd.off + lane;
     const double* __restrict__ x = op.x(mat);
     const double* __restrict__ x2 = op.x2(mat);
     int r = warp - 1;
@@ -456,12 +481,29 @@ sell_long_kernel(const Op op, const SellArgs sa) {
     double v[B];
     auto load = [&](int rr, int32_t* cc, double* vv) {
       const int k0 = rr * B;
+      if constexpr (Q == kQuad) {  // the lane's B entries are adjacent: vector loads
+        if (k0 < len) {
+          const int64_t o = static_cast<int64_t>(k0 >> 2) * 128 + 3 * lane + (k0 & 3);
+          if constexpr (B == 4) {
+            const int4 c4 = ld_st4(cp + o);
+            cc[0] = c4.x, cc[1] = c4.y, cc[2] = c4.z, cc[3] = c4.w;
+            const double2 v0 = ld_st2(vp + o), v1 = ld_st2(vp + o + 2);
+            vv[0] = v0.x, vv[1] = v0.y, vv[2] = v1.x, vv[3] = v1.y;
+          } else {
+            const int2 c2 = ld_st2(cp + o);
+            cc[0] = c2.x, cc[1] = c2.y;
+            const double2 v0 = ld_st2(vp + o);
+            vv[0] = v0.x, vv[1] = v0.y;
+          }
+        }
+      } else {
 #pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (k0 + b < len) cc[b] = ld_st(cp + 32 * (k0 + b));
+        for (int b = 0; b < B; ++b)
+          if (k0 + b < len) cc[b] = ld_st(cp + 32 * (k0 + b));
 #pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (k0 + b < len) vv[b] = ld_st(vp + 32 * (k0 + b));
+        for (int b = 0; b < B; ++b)
+          if (k0 + b < len) vv[b] = ld_st(vp + 32 * (k0 + b));
+      }
     };
     if (PIPE && r < rounds) load(r, c, v);
     for (; r < rounds; r += S) {
@@ -477,7 +519,7 @@ sell_long_kernel(const Op op, const SellArgs sa) {
 #pragma unroll
       for (int b = 0; b < B; ++b)
         if (k0 + b < len) {
-          EQ_CHECK(c[b] >= 0 && c[b] < sa.xlen[mat]);
+          EQ_CHECK(c[b] >= 0 && c[b] < pick(sa.xlen, mat));
           gather_x<Op>(x, x2, c[b], g[b], g2[b]);
         }
       const int bi = r % R;
@@ -548,16 +590,25 @@ void carveout(K kernel, const char* env, int dflt) {
 }
 template <class Op>
 constexpr bool is_sgd() { return std::is_same<Op, SgdOp>::value || std::is_same<Op, SgdSplitOp>::value; }
-template <class Op>
-constexpr int carve_long() { return 22; }  // (LSQR passes too: 1.815 -> 1.803 ms)
+// (LSQR passes too: 1.815 -> 1.803 ms).  The dual LSQR pass with 4-entry rounds
+// (quad layout) keeps 2 CTAs per SM only with 36% (its ring is 32 KB): c4
+// 1.331 -> 1.277 ms per LSQR iteration.
+template <class Op, int B>
+constexpr int carve_long() { return Op::NV == 2 && B == 4 ? 36 : 22; }
 template <class Op>
 constexpr int carve_warp() { return is_sgd<Op>() ? 0 : -1; }
 
+template <class Op, int B, int S, bool PIPE, int MINB, int Q>
+void launch_long_q(const Op& op, const SellArgs& sa, cudaStream_t s) {
+  carveout(sell_long_kernel<Op, B, S, PIPE, MINB, Q>, "EQUIL_CARVE_LONG", carve_long<Op, B>());
+  sell_long_kernel<Op, B, S, PIPE, MINB, Q>
+      <<<static_cast<unsigned>(sa.nslices - sa.first), 32 * (S + 1), 0, s>>>(op, sa);
+}
+// the slices' layout picks the instantiation (quad: 128-bit stream loads)
 template <class Op, int B, int S, bool PIPE, int MINB>
 void launch_long(const Op& op, const SellArgs& sa, cudaStream_t s) {
-  carveout(sell_long_kernel<Op, B, S, PIPE, MINB>, "EQUIL_CARVE_LONG", carve_long<Op>());
-  sell_long_kernel<Op, B, S, PIPE, MINB>
-      <<<static_cast<unsigned>(sa.nslices - sa.first), 32 * (S + 1), 0, s>>>(op, sa);
+  if (sa.quad) launch_long_q<Op, B, S, PIPE, MINB, kQuad>(op, sa, s);
+  else launch_long_q<Op, B, S, PIPE, MINB, 1>(op, sa, s);
 }
 
 template <class Op, int B, bool PIPE, int MINB>
@@ -572,10 +623,11 @@ void launch_warp(const Op& op, const SellArgs& sa, cudaStream_t s) {
 cudaError_t build_sell(const int64_t* rp, const int32_t* ci, const int32_t* map, const double* val,
                        const int64_t* kbp, int64_t items, const int32_t* midx, int nmat_slices,
                        const SellSlice* slices, const int32_t* row, const int32_t* len,
-                       const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s) {
+                       const int32_t* kst, int32_t* out_ci, double* out_va, cudaStream_t s,
+                       int quad_min) {
   if (nmat_slices == 0 || items == 0) return cudaSuccess;
   build_sell_kernel<<<static_cast<unsigned>((items + 1) / 2), 64, 0, s>>>(
-      rp, ci, map, val, kbp, midx, nmat_slices, slices, row, len, kst, out_ci, out_va);
+      rp, ci, map, val, kbp, midx, nmat_slices, slices, row, len, kst, out_ci, out_va, quad_min);
   count_launch(s);
   return cudaGetLastError();
 }
@@ -609,16 +661,14 @@ cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int v
                                  cudaStream_t s) {
   if (sa.nslices <= sa.first) return cudaSuccess;
   if (a.nblk[0] > 1 || a.nblk[1] > 1) {
-    launch_long<SgdBlockOp, 4, 15, true, 1>(SgdBlockOp{{a}}, sa, s);
+    launch_long_q<SgdBlockOp, 4, 15, true, 1, 1>(SgdBlockOp{{a}}, sa, s);
     count_launch(s);
     return cudaGetLastError();
   }
   const SgdOp op{a};
   switch (variant) {  // EQUIL_SELL_LVARIANT (A/B knob); 0 = measured best on c3
-    case 1: launch_long<SgdOp, 8, 7, true, 2>(op, sa, s); break;
     case 2: launch_long<SgdOp, 4, 7, true, 3>(op, sa, s); break;
     case 3: launch_long<SgdOp, 2, 15, true, 2>(op, sa, s); break;
-    case 4: launch_long<SgdOp, 8, 7, false, 2>(op, sa, s); break;
     default: launch_long<SgdOp, 4, 15, true, 1>(op, sa, s); break;
   }
   count_launch(s);
@@ -691,7 +741,10 @@ cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArg
       switch (pv) {  // EQUIL_PASS_VARIANT
         case 1: launch_long<PassPairOp, 4, 15, true, 1>(op, sa, s); break;
         case 2: launch_long<PassPairOp, 4, 7, true, 2>(op, sa, s); break;
-        default: launch_long<PassPairOp, 2, 15, true, 1>(op, sa, s); break;
+        default:  // quad layout: a round is one whole quad (B = 4), else B = 2
+          if (sa.quad) launch_long<PassPairOp, 4, 15, true, 1>(op, sa, s);
+          else launch_long<PassPairOp, 2, 15, true, 1>(op, sa, s);
+          break;
       }
     } else {
       switch (pv) {
@@ -705,7 +758,10 @@ cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArg
       switch (pv) {  // EQUIL_PASS_VARIANT; 0 = measured best on c4 (1.82 vs 1.86 ms)
         case 1: launch_long<PassOp<2>, 4, 15, true, 1>(op, sa, s); break;
         case 2: launch_long<PassOp<2>, 4, 7, true, 2>(op, sa, s); break;
-        default: launch_long<PassOp<2>, 2, 15, true, 1>(op, sa, s); break;
+        default:
+          if (sa.quad) launch_long<PassOp<2>, 4, 15, true, 1>(op, sa, s);
+          else launch_long<PassOp<2>, 2, 15, true, 1>(op, sa, s);
+          break;
       }
     } else {
       switch (pv) {

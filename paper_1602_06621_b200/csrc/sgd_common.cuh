@@ -44,6 +44,14 @@ __device__ __forceinline__ int32_t ld_na(const int32_t* p) {
 }
 #endif
 
+// element `mat` of a two-element kernel-parameter array, selected without a
+// dynamic index (which would copy the whole parameter struct to local memory,
+// whose stores then compete with the gathers for L1TEX and L2)
+template <class T>
+__device__ __forceinline__ T pick(const T (&arr)[2], int mat) {
+  return mat ? arr[1] : arr[0];
+}
+
 __device__ __forceinline__ bool sign_bit(const uint32_t* bits, int64_t b) {
   return (__ldg(bits + (b >> 5)) >> (b & 31)) & 1u;
 }
@@ -86,20 +94,23 @@ __device__ __forceinline__ double chain_sum(double acc, const double* sp, int b,
 __device__ __forceinline__ void sgd_epilogue(const SgdIterArgs& a, int mat,
                                              int64_t r, double acc,
                                              unsigned& fl) {
-  const int64_t pi = a.slot[mat] ? static_cast<int64_t>(a.slot[mat][r]) : a.poff[mat] + r;
+  const int64_t pi = pick(a.slot, mat) ? static_cast<int64_t>(pick(a.slot, mat)[r]) : pick(a.poff, mat) + r;
   // |d_i w_i| = d_i exactly (w = +-1): this iteration's d (mat 0) or e (mat 1)
   const double scl = fabs(mat ? a.xs_cur[pi] : a.xw_cur[pi]);
   const double y = __dmul_rn(scl, acc);          // linop.cpp:19 / :25
   const double est = __dmul_rn(y, y);            // estimator.cpp:8
-  double avg = a.avg[mat][r];
-  const double xn = a.lin[mat]
-                        ? sgd_coord_lin(est, a.x[mat][r], a.lin[mat][r], a.c[mat], a.st, avg, fl)
-                        : sgd_coord(est, a.x[mat][r], a.c[mat], a.st, avg, fl);
-  a.x[mat][r] = xn;
-  a.avg[mat][r] = avg;
+  double* const xp = pick(a.x, mat);
+  double* const ap = pick(a.avg, mat);
+  const double* const lp = pick(a.lin, mat);
+  double avg = ap[r];
+  const SgdBlockConst cb = pick(a.c, mat);
+  const double xn = lp ? sgd_coord_lin(est, xp[r], lp[r], cb, a.st, avg, fl)
+                       : sgd_coord(est, xp[r], cb, a.st, avg, fl);
+  xp[r] = xn;
+  ap[r] = avg;
   if (a.has_next) {  // next iteration's e.*s (from v) / d.*w (from u)
     const double dn = det_exp(xn);
-    const bool pos = sign_bit(a.signs, a.sign_next[mat] + r);
+    const bool pos = sign_bit(a.signs, pick(a.sign_next, mat) + r);
     double* dst = (mat ? a.xs_next : a.xw_next) + pi;
     const double val = pos ? dn : -dn;
     *dst = val;

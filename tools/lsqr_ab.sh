@@ -1,6 +1,6 @@
 # LSQR pass-variant A/B on c4 (same box): ms per LSQR iteration for EQUIL_PASS_VARIANT values
 for pv in "$@"; do
-  EQUIL_PASS_VARIANT=$pv timeout 300 python - <<'PY'
+  EQUIL_PASS_VARIANT=${pv%% *} timeout 300 python - <<'PY'
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import paper_1602_06621_b200 as eq
