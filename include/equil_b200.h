@@ -298,6 +298,35 @@ equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_
                                        const equil_device_cfg* cfg,
                                        equil_scaling_out* out);
 
+/* ---- matrix-free operators ------------------------------------------------
+ * The reference's plugin interface is LinearOperator (include/equil/linop.hpp:
+ * 13-25): rows(), cols(), apply(x), apply_adjoint(y).  On the device it is a
+ * pair of callbacks: apply(ctx, x, y, stream) computes y = A x (x: cols
+ * doubles, y: rows doubles, device pointers); apply_adjoint(ctx, y, x, stream)
+ * computes x = A^T y.  They are called from the calling thread and must
+ * enqueue their work on `stream` (a cudaStream_t) or finish it before
+ * returning. */
+typedef void (*equil_device_apply_fn)(void* ctx, const double* in, double* out, void* stream);
+typedef struct {
+  int64_t rows;
+  int64_t cols;
+  equil_device_apply_fn apply;
+  equil_device_apply_fn apply_adjoint;
+  void* ctx;
+  int device;
+} equil_device_operator;
+/* sgd_equilibrate(op, params) on a matrix-free operator (include/equil/
+ * equilibrate.hpp:89-91, src/equilibrate.cpp:138-221): T applies and T
+ * adjoints of op, probes, estimate, update and averaging on the device.
+ * Single GPU; no history (the reference needs the explicit matrix for it). */
+equil_status equil_sgd_equilibrate_operator(const equil_device_operator* op,
+                                            const equil_params* p, equil_scaling_out* out);
+/* y = A x (adjoint: x = A^T y) on device pointers, ordered on `stream`:
+ * an explicit matrix's own traversal, usable as a device operator
+ * (LinearOperator::apply / apply_adjoint, include/equil/linop.hpp:20-24). */
+equil_status equil_apply_device(equil_matrix* A, const double* x, double* y, int adjoint,
+                                void* stream);
+
 /* ---- verification hooks -------------------------------------------------- */
 /* Sign bits of SeededRng(seed, stream) outputs [start, start+count), generated
  * on device (K1); bit k of the packed u32 words = MSB of output start+k. */

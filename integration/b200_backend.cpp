@@ -8,9 +8,12 @@
 
 #include <cstdint>
 #include <cstring>
+#include <exception>
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime_api.h>
 
 #include "equil_b200.h"
 
@@ -32,9 +35,47 @@ const ExplicitMatrix& explicit_of(const LinearOperator& op) {
   const auto* A = dynamic_cast<const ExplicitMatrix*>(&op);
   if (A == nullptr)
     throw std::invalid_argument(
-        "b200 backend: the operator must be an ExplicitMatrix (a matrix-free "
-        "LinearOperator has no device form)");
+        "b200 backend: LSQR needs an ExplicitMatrix (matrix-free operators: sgd_equilibrate)");
   return *A;
+}
+
+void cuda_ok(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("b200 backend: ") + cudaGetErrorString(e));
+}
+
+// A matrix-free LinearOperator whose apply is host code (the user's plugin):
+// the device SGD loop calls it through the device-operator ABI, with the
+// probe copied to the host and the result copied back.  The operator's own
+// apply runs unchanged, so the result is the reference's bit for bit; the
+// PCIe round trips bound its speed, and an operator with a device apply
+// should implement equil_device_operator directly.
+struct HostBridge {
+  const LinearOperator* op;
+  Vec in_m, in_n;
+  std::exception_ptr error;
+};
+void bridge(void* ctx, const double* in, double* out, void* stream, bool adjoint) {
+  auto* b = static_cast<HostBridge*>(ctx);
+  if (b->error) return;
+  try {
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Vec& x = adjoint ? b->in_m : b->in_n;
+    cuda_ok(cudaMemcpyAsync(x.data(), in, static_cast<size_t>(x.size()) * 8,
+                            cudaMemcpyDeviceToHost, s));
+    cuda_ok(cudaStreamSynchronize(s));
+    const Vec y = adjoint ? b->op->apply_adjoint(x) : b->op->apply(x);
+    cuda_ok(cudaMemcpyAsync(out, y.data(), static_cast<size_t>(y.size()) * 8,
+                            cudaMemcpyHostToDevice, s));
+    cuda_ok(cudaStreamSynchronize(s));
+  } catch (...) {
+    b->error = std::current_exception();
+  }
+}
+void bridge_apply(void* ctx, const double* in, double* out, void* stream) {
+  bridge(ctx, in, out, stream, false);
+}
+void bridge_adjoint(void* ctx, const double* in, double* out, void* stream) {
+  bridge(ctx, in, out, stream, true);
 }
 
 Vec to_vec(const std::vector<double>& v) {
@@ -174,7 +215,42 @@ LsqrRun lsqr_preconditioned(const Device& A, const Vec& b, const EquilibrationPa
 
 ScalingResult sgd_equilibrate(const LinearOperator& op, const EquilibrationParams& params,
                               const DiagnosticsConfig& diag) {
-  return sgd_equilibrate(Device(explicit_of(op)), params, diag);
+  if (const auto* A = dynamic_cast<const ExplicitMatrix*>(&op))
+    return sgd_equilibrate(Device(*A), params, diag);
+  // matrix-free: the device loop around the operator's own apply
+  // (equil_sgd_equilibrate_operator); diagnostics need the explicit matrix
+  const equil_params cp = to_c(params);
+  double alpha = 0.0, beta = 0.0;
+  check(equil_resolve_targets(&cp, op.rows(), op.cols(), &alpha, &beta));
+  check(equil_validate_params(&cp));
+  if (diag.matrix != nullptr)
+    throw std::invalid_argument(
+        "b200 backend: diagnostics of a matrix-free operator need sgd_equilibrate on the "
+        "explicit matrix");
+  HostBridge hb{&op, Vec(op.rows()), Vec(op.cols()), nullptr};
+  const equil_device_operator dop{op.rows(), op.cols(), &bridge_apply, &bridge_adjoint, &hb, 0};
+  std::vector<double> u(static_cast<size_t>(op.rows())), d(u.size());
+  std::vector<double> v(static_cast<size_t>(op.cols())), e(v.size());
+  equil_scaling_out o{};
+  o.u = u.data();
+  o.v = v.data();
+  o.d = d.data();
+  o.e = e.data();
+  const equil_status st = equil_sgd_equilibrate_operator(&dop, &cp, &o);
+  if (hb.error) std::rethrow_exception(hb.error);  // the operator's own exception
+  check(st);
+  ScalingResult r;
+  r.u = to_vec(u);
+  r.v = to_vec(v);
+  r.d = to_vec(d);
+  r.e = to_vec(e);
+  r.alpha = o.alpha;
+  r.beta = o.beta;
+  r.box_feasible = o.box_feasible != 0;
+  r.iterate_bound_ok = o.iterate_bound_ok != 0;
+  r.apply_count = o.apply_count;
+  r.adjoint_count = o.adjoint_count;
+  return r;
 }
 
 LsqrRun lsqr(const LinearOperator& op, const Vec& b, int max_iters, double rel_residual_tol) {

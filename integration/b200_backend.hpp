@@ -11,9 +11,11 @@
 //
 // Same arguments, same results (bit for bit: tests run by integration/
 // test_backend.cpp), same exception types and messages
-// (include/equil/common.hpp:16-22).  The operator must be an ExplicitMatrix:
-// a matrix-free LinearOperator has no device form, and the backend says so
-// (std::invalid_argument) instead of running anything on the host.
+// (include/equil/common.hpp:16-22).  sgd_equilibrate takes any LinearOperator:
+// an ExplicitMatrix runs on its device copy (CSR(A) and CSR(A^T), or the dense
+// array); a matrix-free operator runs through the device-operator ABI
+// (equil_sgd_equilibrate_operator) with its own host apply bridged in each
+// iteration.  LSQR needs an ExplicitMatrix (std::invalid_argument otherwise).
 #pragma once
 
 #include <memory>

@@ -9,7 +9,9 @@
 // charged apply/adjoint counts, history on the stride grid, box feasibility,
 // LSQR on the identity / a diagonal / a random square system, the charged
 // counts, the zero right-hand side, breakdown, a singular system, the trivial
-// and badly scaled preconditioned runs.  Every case asserts bit equality of
+// and badly scaled preconditioned runs, and a matrix-free operator (the
+// reference's LinearOperator plugin) through the device loop.  Every case
+// asserts bit equality of
 // the outputs with the reference's (history values within 1e-12 relative:
 // the reference evaluates them with sequential sums and std::exp), plus the
 // case's own property.  Prints "OK" when every check passes.
@@ -341,20 +343,43 @@ void lsqr_cases() {
 }
 
 void operator_case() {
-  // a matrix-free operator has no device form: refused, nothing runs on the host
-  struct Neg final : LinearOperator {
-    Index rows() const override { return 2; }
-    Index cols() const override { return 2; }
-    Vec apply(const Vec& x) const override { return -x; }
-    Vec apply_adjoint(const Vec& y) const override { return -y; }
-  } op;
+  // a matrix-free operator (the reference's plugin interface): B = A diag(c),
+  // applied as A (c .* x) / c .* A^T y -- no explicit form exists; the device
+  // loop around its own apply must reproduce the reference's run bit for bit
+  struct ColumnScaled final : LinearOperator {
+    const ExplicitMatrix* A;
+    Vec c;
+    Index rows() const override { return A->rows(); }
+    Index cols() const override { return A->cols(); }
+    Vec apply(const Vec& x) const override {
+      Vec t(x.size());
+      for (Index j = 0; j < x.size(); ++j) t[j] = c[j] * x[j];
+      return A->apply(t);
+    }
+    Vec apply_adjoint(const Vec& y) const override {
+      Vec z = A->apply_adjoint(y);
+      for (Index j = 0; j < z.size(); ++j) z[j] = c[j] * z[j];
+      return z;
+    }
+  };
+  SeededRng rng(107, 0);
+  const ExplicitMatrix A = scaled_sparse(80, 50, 0.1, 0, rng);
+  ColumnScaled op;
+  op.A = &A;
+  op.c = Vec(50);
+  for (Index j = 0; j < 50; ++j) op.c[j] = std::exp(rng.normal());
+  EquilibrationParams p;
+  p.iterations = 120;
+  p.seed = 9;
+  const ScalingResult g = b200::sgd_equilibrate(op, p);
+  compare_scaling(g, sgd_equilibrate(op, p), "sgd matrix-free operator");
   bool threw = false;
   try {
-    b200::sgd_equilibrate(op, EquilibrationParams{});
+    b200::lsqr(op, Vec::Ones(80), 5, 0.0);
   } catch (const std::invalid_argument&) {
     threw = true;
   }
-  expect(threw, "matrix-free operator refused with std::invalid_argument");
+  expect(threw, "lsqr on a matrix-free operator refused with std::invalid_argument");
 }
 
 }  // namespace

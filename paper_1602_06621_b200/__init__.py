@@ -16,7 +16,8 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   last_loop_ms, exchange_mode, lsqr, lsqr_preconditioned, nccl_unique_id,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
                   sgd_equilibrate_block, sgd_equilibrate_symmetric, sgd_equilibrate_targets,
-                  sgd_equilibrate_device, sign_bits, validate_params)
+                  sgd_equilibrate_device, sign_bits, validate_params,
+                  DeviceOperator, sgd_equilibrate_operator)
 
 __all__ = [
     "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "BlockStructure",
@@ -32,4 +33,5 @@ __all__ = [
     "partition_rows", "resolve_targets", "sgd_equilibrate", "sgd_equilibrate_csr",
     "sgd_equilibrate_block", "sgd_equilibrate_device", "sgd_equilibrate_symmetric",
     "sgd_equilibrate_targets", "sign_bits", "validate_params",
+    "DeviceOperator", "sgd_equilibrate_operator",
 ]

@@ -68,6 +68,15 @@ class CcpOut(C.Structure):
                 ("adjoint_count", C.c_longlong)]
 
 
+# matrix-free operator (equil_device_operator): apply(ctx, in, out, stream)
+DeviceApplyFn = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class DeviceOperator(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("apply", DeviceApplyFn),
+                ("apply_adjoint", DeviceApplyFn), ("ctx", C.c_void_p), ("device", C.c_int)]
+
+
 # every exported symbol of include/equil_b200.h with (restype, argtypes)
 SIGNATURES = {
     "equil_params_default": (None, [C.POINTER(Params)]),
@@ -87,6 +96,9 @@ SIGNATURES = {
     "equil_kernel_launches": (C.c_longlong, []),
     "equil_build_flags": (C.c_int, []),
     "equil_apply": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int]),
+    "equil_apply_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "equil_sgd_equilibrate_operator": (C.c_int, [C.POINTER(DeviceOperator), C.POINTER(Params),
+                                                 C.POINTER(ScalingOut)]),
     "equil_sgd_equilibrate": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(DiagCfg),
                                         C.POINTER(ScalingOut)]),
     "equil_sgd_equilibrate_targets": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params),

@@ -321,6 +321,56 @@ def sgd_equilibrate(op: ExplicitMatrix, params: EquilibrationParams | None = Non
                          bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
 
 
+class DeviceOperator:
+    """A matrix-free LinearOperator on the device (include/equil/linop.hpp:13-25).
+
+    apply(x_ptr, y_ptr, stream) must compute y = A x and apply_adjoint(y_ptr,
+    x_ptr, stream) x = A^T y, on device pointers (ints) of cols / rows doubles,
+    enqueued on the CUDA stream handle `stream` (or finished before returning).
+    """
+
+    def __init__(self, rows: int, cols: int, apply, apply_adjoint, device: int = 0):
+        self.rows_, self.cols_, self.device = int(rows), int(cols), int(device)
+        # keep the ctypes trampolines alive as long as the operator
+        self._fa = L.DeviceApplyFn(lambda ctx, i, o, s: apply(i, o, s))
+        self._fb = L.DeviceApplyFn(lambda ctx, i, o, s: apply_adjoint(i, o, s))
+
+    @classmethod
+    def from_matrix(cls, M: ExplicitMatrix, device: int = 0) -> "DeviceOperator":
+        """An explicit matrix's own device apply / adjoint as an operator."""
+        lib = L.load()
+        return cls(M.rows(), M.cols(),
+                   lambda x, y, s: _check(lib.equil_apply_device(M._h, x, y, 0, s)),
+                   lambda y, x, s: _check(lib.equil_apply_device(M._h, y, x, 1, s)),
+                   device=device)
+
+    def rows(self) -> int:
+        return self.rows_
+
+    def cols(self) -> int:
+        return self.cols_
+
+    def _c(self):
+        return L.DeviceOperator(self.rows_, self.cols_, self._fa, self._fb, None, self.device)
+
+
+def sgd_equilibrate_operator(op: DeviceOperator,
+                             params: EquilibrationParams | None = None) -> ScalingResult:
+    """sgd_equilibrate (include/equil/equilibrate.hpp:89-91) on a matrix-free
+    device operator: T applies and T adjoints of op, everything else on the
+    device.  No history (the reference needs the explicit matrix for it)."""
+    params = params or EquilibrationParams()
+    m, n = op.rows(), op.cols()
+    u, v, d, e = np.zeros(m), np.zeros(n), np.zeros(m), np.zeros(n)
+    out = L.ScalingOut(L.ptr(u, L._dp), L.ptr(v, L._dp), L.ptr(d, L._dp), L.ptr(e, L._dp), 0,
+                       0.0, 0.0, 0, 0, 0, 0, None, None, None, 0, 0)
+    p = params._c()
+    c_op = op._c()
+    _check(L.load().equil_sgd_equilibrate_operator(C.byref(c_op), C.byref(p), C.byref(out)))
+    return ScalingResult(u, v, d, e, out.alpha, out.beta, [], bool(out.box_feasible),
+                         bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
+
+
 def sgd_equilibrate_targets(op: ExplicitMatrix, r, c, params: EquilibrationParams | None = None,
                             diag: DiagnosticsConfig | None = None) -> ScalingResult:
     """sgd_equilibrate_targets (include/equil/variants.hpp:24-27): row i aims
