@@ -627,7 +627,7 @@ void allgather_padded(equil_matrix* M, double* buf, int64_t maxcnt) {
     M->hx->barrier();
     for (int g = 0; g < M->world; ++g)
       if (g != M->rank && bytes)
-        CK(cudaMemcpy(buf + g * maxcnt, M->hx->slot(g), bytes, cudaMemcpyHostToDevice));
+        h2d_sync(M->stream, buf + g * maxcnt, M->hx->slot(g), bytes);
     M->hx->barrier();
     return;
   }
@@ -923,8 +923,8 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
   }
   M->a_bounds_d.alloc(G + 1);
   M->t_bounds_d.alloc(G + 1);
-  CK(cudaMemcpy(M->a_bounds_d.p, M->a_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(M->t_bounds_d.p, M->t_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+  h2d_sync(M->stream, M->a_bounds_d.p, M->a_bounds.data(), (G + 1) * 8);
+  h2d_sync(M->stream, M->t_bounds_d.p, M->t_bounds.data(), (G + 1) * 8);
 
   auto take = [&](eqb::DevCsr& full, const std::vector<int64_t>& rph,
                   const std::vector<int64_t>& bounds, const std::vector<int64_t>& colb,
@@ -947,7 +947,7 @@ void shard_sparse(equil_matrix* M, eqb::DevCsr& fullA, eqb::DevCsr& fullT,
       if (G > 1) {
         DevBuf<int64_t> cb;
         cb.alloc(G + 1);
-        CK(cudaMemcpy(cb.p, colb.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+        h2d_sync(M->stream, cb.p, colb.data(), (G + 1) * 8);
         remap_cols_kernel<<<static_cast<unsigned>((out.nnz + 255) / 256), 256, 0,
                             M->stream>>>(ci.p, out.nnz, cb.p, G, colmax);
         CK(cudaGetLastError());
@@ -1037,7 +1037,7 @@ void alltoallv_bytes(equil_matrix* M, const char* send, const std::vector<int64_
     }
     M->hx->barrier();
   }
-  if (roff[G]) CK(cudaMemcpy(recv, mine.data(), static_cast<size_t>(roff[G]), cudaMemcpyHostToDevice));
+  h2d_sync(s, recv, mine.data(), static_cast<size_t>(roff[G]));
 }
 
 // In-place sum of an int64 device array over the ranks.
@@ -1064,7 +1064,7 @@ void allreduce_sum_i64(equil_matrix* M, int64_t* dev, int64_t count) {
     }
     M->hx->barrier();
   }
-  CK(cudaMemcpy(dev, sum.data(), bytes, cudaMemcpyHostToDevice));
+  h2d_sync(s, dev, sum.data(), bytes);
 }
 
 // ExplicitMatrix::sparse's message for the first invalid entry (class, global
@@ -1171,8 +1171,8 @@ void create_sharded(equil_matrix* M, const int64_t* row_ptr, const int32_t* col,
   }
   M->a_bounds_d.alloc(G + 1);
   M->t_bounds_d.alloc(G + 1);
-  CK(cudaMemcpy(M->a_bounds_d.p, M->a_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(M->t_bounds_d.p, M->t_bounds.data(), (G + 1) * 8, cudaMemcpyHostToDevice));
+  h2d_sync(M->stream, M->a_bounds_d.p, M->a_bounds.data(), (G + 1) * 8);
+  h2d_sync(M->stream, M->t_bounds_d.p, M->t_bounds.data(), (G + 1) * 8);
   // A^T's columns are A's rows: local row -> this rank's padded slot range
   if (nl)
     add_cols_kernel<<<static_cast<unsigned>((nl + 255) / 256), 256, 0, s>>>(tcl.p, nl,

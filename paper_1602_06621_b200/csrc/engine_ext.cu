@@ -171,9 +171,9 @@ void sgd_variant(equil_matrix* M, Variant kind, const equil_params* p,
     CK(cudaMemsetAsync(xvb.p, 0, C * 8, s));
     std::vector<double> l(C);
     for (int64_t b = 0; b < C; ++b) l[b] = (beta * beta) * ccount[b];
-    CK(cudaMemcpy(lv.p, l.data(), C * 8, cudaMemcpyHostToDevice));
+    h2d_sync(s, lv.p, l.data(), C * 8);
     // members of every block in ascending index order (stable counting sort)
-    auto members = [](const std::vector<int32_t>& map, int64_t nb, DevBuf<int32_t>& mem,
+    auto members = [s](const std::vector<int32_t>& map, int64_t nb, DevBuf<int32_t>& mem,
                       DevBuf<int64_t>& off) {
       std::vector<int64_t> o(nb + 1, 0);
       for (int32_t b : map) ++o[b + 1];
@@ -183,16 +183,15 @@ void sgd_variant(equil_matrix* M, Variant kind, const equil_params* p,
       for (size_t i = 0; i < map.size(); ++i) list[pos[map[i]]++] = static_cast<int32_t>(i);
       mem.alloc(list.size());
       off.alloc(o.size());
-      if (!list.empty())
-        CK(cudaMemcpy(mem.p, list.data(), list.size() * 4, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(off.p, o.data(), o.size() * 8, cudaMemcpyHostToDevice));
+      h2d_sync(s, mem.p, list.data(), list.size() * 4);
+      h2d_sync(s, off.p, o.data(), o.size() * 8);
     };
     members(rbm, R, memr, offr);
     members(cbm, C, memc, offc);
     rbd.alloc(m);
     cbd.alloc(n);
-    if (m) CK(cudaMemcpy(rbd.p, rbm.data(), m * 4, cudaMemcpyHostToDevice));
-    if (n) CK(cudaMemcpy(cbd.p, cbm.data(), n * 4, cudaMemcpyHostToDevice));
+    h2d_sync(s, rbd.p, rbm.data(), m * 4);
+    h2d_sync(s, cbd.p, cbm.data(), n * 4);
   }
   CK(cudaMemsetAsync(M->flags.p, 0, sizeof(unsigned), s));
   eqb::SgdBlockConst c{};

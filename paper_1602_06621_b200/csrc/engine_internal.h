@@ -103,6 +103,14 @@ inline void cuda_check(cudaError_t e, const char* what) {
   }
 }
 #define CK(x) cuda_check((x), #x)
+// Host -> device copy ordered on stream s and complete on return.  A plain
+// cudaMemcpy from pageable memory may return before its DMA has landed, and it
+// runs on the legacy stream, which our non-blocking streams do not wait for.
+inline void h2d_sync(cudaStream_t s, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+  cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
 inline void nccl_check(ncclResult_t r, const char* what) {
   if (r != 0) {
     const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
