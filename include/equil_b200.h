@@ -321,6 +321,13 @@ typedef struct {
  * Single GPU; no history (the reference needs the explicit matrix for it). */
 equil_status equil_sgd_equilibrate_operator(const equil_device_operator* op,
                                             const equil_params* p, equil_scaling_out* out);
+/* lsqr(op, b, max_iters, tol) (p == NULL) or lsqr_preconditioned(op, b, *p,
+ * max_iters, tol) (src/lsqr.cpp:85-138) on a matrix-free operator: b and
+ * out->x on the host; three operator calls per iteration (B v, B^T u and the
+ * uncharged residual probe A x).  Single GPU. */
+equil_status equil_lsqr_operator(const equil_device_operator* op, const double* b,
+                                 const equil_params* p, int max_iters, double tol,
+                                 equil_lsqr_out* out);
 /* y = A x (adjoint: x = A^T y) on device pointers, ordered on `stream`:
  * an explicit matrix's own traversal, usable as a device operator
  * (LinearOperator::apply / apply_adjoint, include/equil/linop.hpp:20-24). */

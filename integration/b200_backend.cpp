@@ -31,14 +31,6 @@ equil_params to_c(const EquilibrationParams& p) {
   return {p.alpha, p.beta, p.gamma, p.max_log_scale, p.iterations, p.seed};
 }
 
-const ExplicitMatrix& explicit_of(const LinearOperator& op) {
-  const auto* A = dynamic_cast<const ExplicitMatrix*>(&op);
-  if (A == nullptr)
-    throw std::invalid_argument(
-        "b200 backend: LSQR needs an ExplicitMatrix (matrix-free operators: sgd_equilibrate)");
-  return *A;
-}
-
 void cuda_ok(cudaError_t e) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("b200 backend: ") + cudaGetErrorString(e));
 }
@@ -253,14 +245,53 @@ ScalingResult sgd_equilibrate(const LinearOperator& op, const EquilibrationParam
   return r;
 }
 
+namespace {
+// lsqr / lsqr_preconditioned of a matrix-free operator: the device loop
+// (equil_lsqr_operator) around the operator's own host apply
+LsqrRun lsqr_bridged(const LinearOperator& op, const Vec& b, const EquilibrationParams* p,
+                     int max_iters, double tol) {
+  if (b.size() != op.rows())
+    throw std::invalid_argument(p ? "lsqr_preconditioned: rhs length mismatch"
+                                  : "lsqr: rhs length mismatch");
+  HostBridge hb{&op, Vec(op.rows()), Vec(op.cols()), nullptr};
+  const equil_device_operator dop{op.rows(), op.cols(), &bridge_apply, &bridge_adjoint, &hb, 0};
+  std::vector<double> x(static_cast<size_t>(op.cols()));
+  std::vector<double> hist(static_cast<size_t>((max_iters > 0 ? max_iters : 0) +
+                                               (p && p->iterations > 0 ? p->iterations : 0) + 2));
+  equil_lsqr_out o{};
+  o.x = x.data();
+  o.residual_history = hist.data();
+  o.residual_cap = static_cast<int>(hist.size());
+  equil_params cp{};
+  if (p) cp = to_c(*p);
+  const equil_status st = equil_lsqr_operator(&dop, b.data(), p ? &cp : nullptr, max_iters, tol, &o);
+  if (hb.error) std::rethrow_exception(hb.error);
+  check(st);
+  LsqrRun r;
+  r.x = to_vec(x);
+  r.residual_history.assign(hist.begin(), hist.begin() + o.hist_len);
+  r.iterations = o.iterations;
+  r.equil_iterations = o.equil_iterations;
+  r.reached_tol = o.reached_tol != 0;
+  r.breakdown = o.breakdown != 0;
+  r.apply_count = o.apply_count;
+  r.adjoint_count = o.adjoint_count;
+  return r;
+}
+}  // namespace
+
 LsqrRun lsqr(const LinearOperator& op, const Vec& b, int max_iters, double rel_residual_tol) {
-  return lsqr(Device(explicit_of(op)), b, max_iters, rel_residual_tol);
+  if (const auto* A = dynamic_cast<const ExplicitMatrix*>(&op))
+    return lsqr(Device(*A), b, max_iters, rel_residual_tol);
+  return lsqr_bridged(op, b, nullptr, max_iters, rel_residual_tol);
 }
 
 LsqrRun lsqr_preconditioned(const LinearOperator& op, const Vec& b,
                             const EquilibrationParams& p, int max_iters,
                             double rel_residual_tol) {
-  return lsqr_preconditioned(Device(explicit_of(op)), b, p, max_iters, rel_residual_tol);
+  if (const auto* A = dynamic_cast<const ExplicitMatrix*>(&op))
+    return lsqr_preconditioned(Device(*A), b, p, max_iters, rel_residual_tol);
+  return lsqr_bridged(op, b, &p, max_iters, rel_residual_tol);
 }
 
 }  // namespace equil::b200

@@ -14,8 +14,8 @@
 // (include/equil/common.hpp:16-22).  sgd_equilibrate takes any LinearOperator:
 // an ExplicitMatrix runs on its device copy (CSR(A) and CSR(A^T), or the dense
 // array); a matrix-free operator runs through the device-operator ABI
-// (equil_sgd_equilibrate_operator) with its own host apply bridged in each
-// iteration.  LSQR needs an ExplicitMatrix (std::invalid_argument otherwise).
+// (equil_sgd_equilibrate_operator, equil_lsqr_operator) with its own host apply
+// bridged in each call.
 #pragma once
 
 #include <memory>

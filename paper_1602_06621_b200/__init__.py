@@ -17,7 +17,7 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
                   sgd_equilibrate_block, sgd_equilibrate_symmetric, sgd_equilibrate_targets,
                   sgd_equilibrate_device, sign_bits, validate_params,
-                  DeviceOperator, sgd_equilibrate_operator)
+                  DeviceOperator, sgd_equilibrate_operator, lsqr_operator)
 
 __all__ = [
     "DEFAULT_MAX_LOG_SCALE", "K_AUTO_TARGET", "SGD_PROBE_STREAM", "BlockStructure",
@@ -33,5 +33,5 @@ __all__ = [
     "partition_rows", "resolve_targets", "sgd_equilibrate", "sgd_equilibrate_csr",
     "sgd_equilibrate_block", "sgd_equilibrate_device", "sgd_equilibrate_symmetric",
     "sgd_equilibrate_targets", "sign_bits", "validate_params",
-    "DeviceOperator", "sgd_equilibrate_operator",
+    "DeviceOperator", "sgd_equilibrate_operator", "lsqr_operator",
 ]

@@ -99,6 +99,8 @@ SIGNATURES = {
     "equil_apply_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "equil_sgd_equilibrate_operator": (C.c_int, [C.POINTER(DeviceOperator), C.POINTER(Params),
                                                  C.POINTER(ScalingOut)]),
+    "equil_lsqr_operator": (C.c_int, [C.POINTER(DeviceOperator), _dp, C.POINTER(Params),
+                                      C.c_int, C.c_double, C.POINTER(LsqrOut)]),
     "equil_sgd_equilibrate": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(DiagCfg),
                                         C.POINTER(ScalingOut)]),
     "equil_sgd_equilibrate_targets": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(Params),

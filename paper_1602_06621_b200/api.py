@@ -371,6 +371,26 @@ def sgd_equilibrate_operator(op: DeviceOperator,
                          bool(out.iterate_bound_ok), out.apply_count, out.adjoint_count)
 
 
+def lsqr_operator(op: DeviceOperator, b, max_iters: int, rel_residual_tol: float,
+                  equil_params: EquilibrationParams | None = None) -> LsqrRun:
+    """lsqr (equil_params None) or lsqr_preconditioned (include/equil/lsqr.hpp:
+    30-40) on a matrix-free device operator."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    who = "lsqr_preconditioned" if equil_params is not None else "lsqr"
+    if b.size != op.rows():
+        raise InvalidArgument(f"{who}: rhs length mismatch")
+    x = np.zeros(op.cols())
+    T = max(int(equil_params.iterations), 0) if equil_params is not None else 0
+    h = np.zeros(max(max_iters, 0) + T + 2)
+    out = L.LsqrOut(L.ptr(x, L._dp), L.ptr(h, L._dp), h.size, 0, 0, 0, 0, 0, 0, 0)
+    p = equil_params._c() if equil_params is not None else None
+    c_op = op._c()
+    _check(L.load().equil_lsqr_operator(C.byref(c_op), L.ptr(b, L._dp),
+                                        C.byref(p) if p is not None else None, int(max_iters),
+                                        float(rel_residual_tol), C.byref(out)))
+    return _lsqr_run(x, h, out)
+
+
 def sgd_equilibrate_targets(op: ExplicitMatrix, r, c, params: EquilibrationParams | None = None,
                             diag: DiagnosticsConfig | None = None) -> ScalingResult:
     """sgd_equilibrate_targets (include/equil/variants.hpp:24-27): row i aims

@@ -82,3 +82,51 @@ def test_operator_parameter_errors_match_the_reference_messages():
         eq.sgd_equilibrate_operator(op, eq.EquilibrationParams(alpha=1.0, beta=1.0))
     r = eq.sgd_equilibrate_operator(op, eq.EquilibrationParams(iterations=0))
     assert np.all(r.u == 0) and np.all(r.d == 1) and r.apply_count == 0
+
+
+@pytest.mark.parametrize("case", ["sp", "lr", "dn"])
+def test_operator_lsqr_bit_exact(golden, case):
+    """lsqr / lsqr_preconditioned on the operator (src/lsqr.cpp:17-138 step by
+    step: three operator calls per iteration) equal the explicit path, which
+    is pinned to the reference's golden runs."""
+    A = csr_from_golden(golden, case)
+    M = _matrix(A)
+    op = eq.DeviceOperator.from_matrix(M)
+    b = np.random.default_rng(11).standard_normal(A.m)
+    got = eq.lsqr_operator(op, b, 25, 0.0)
+    want = eq.lsqr(M, b, 25, 0.0)
+    assert np.array_equal(got.x, want.x)
+    assert got.residual_history == want.residual_history
+    assert (got.iterations, got.breakdown, got.reached_tol) == \
+        (want.iterations, want.breakdown, want.reached_tol)
+    assert (got.apply_count, got.adjoint_count) == (want.apply_count, want.adjoint_count)
+    p = eq.EquilibrationParams(iterations=15, seed=3)
+    got = eq.lsqr_operator(op, b, 25, 0.0, p)
+    want = eq.lsqr_preconditioned(M, b, p, 25, 0.0)
+    assert np.array_equal(got.x, want.x)
+    assert got.residual_history == want.residual_history
+    assert (got.iterations, got.equil_iterations) == (want.iterations, want.equil_iterations)
+    assert (got.apply_count, got.adjoint_count) == (want.apply_count, want.adjoint_count)
+
+
+def test_operator_lsqr_errors_and_breakdown():
+    rt = _cudart()
+    rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                   ctypes.c_int, ctypes.c_void_p]
+    rt.cudaMemsetAsync.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t,
+                                   ctypes.c_void_p]
+    n = 6
+    ident = eq.DeviceOperator(n, n, lambda i, o, s: rt.cudaMemcpyAsync(o, i, n * 8, 3, s),
+                              lambda i, o, s: rt.cudaMemcpyAsync(o, i, n * 8, 3, s))
+    b = np.arange(1.0, n + 1)
+    r = eq.lsqr_operator(ident, b, 10, 1e-12)  # test_itersolvers.cpp:36-46
+    assert r.reached_tol and r.iterations == 1 and r.residual_history[0] == 1.0
+    assert np.allclose(r.x, b)
+    with pytest.raises(eq.InvalidArgument, match="rhs must be nonzero"):
+        eq.lsqr_operator(ident, np.zeros(n), 5, 0.0)
+    with pytest.raises(eq.InvalidArgument, match="max_iters must be nonnegative"):
+        eq.lsqr_operator(ident, b, -1, 0.0)
+    zero = eq.DeviceOperator(n, n, lambda i, o, s: rt.cudaMemsetAsync(o, 0, n * 8, s),
+                             lambda i, o, s: rt.cudaMemsetAsync(o, 0, n * 8, s))
+    r = eq.lsqr_operator(zero, b, 10, 0.0)  # A^T b = 0: breakdown at setup
+    assert r.breakdown and r.iterations == 0 and np.all(r.x == 0)
