@@ -106,11 +106,25 @@ dense_sgd_rows_kernel(const DenseIterArgs a) {
   }
 }
 
+// level 2 over chunk partials for column j (nc <= 64, see create_dense)
+__device__ double dense_col_level2(const double* colpart, int64_t nc, int64_t n, int64_t j) {
+  if (nc == 1) return colpart[j];
+  double s[64];
+  int lanes = 1;
+  while (lanes < nc) lanes <<= 1;
+  for (int q = 0; q < lanes; ++q) s[q] = q < nc ? __dadd_rn(0.0, __ldcg(colpart + q * n + j)) : 0.0;
+  for (int h = lanes / 2; h >= 1; h >>= 1)
+    for (int q = 0; q < h; ++q) s[q] = __dadd_rn(s[q], s[q + h]);
+  return s[0];
+}
+
 // partial column sums of one (16-column strip, 2048-row chunk): colpart[c*n + j].
 // Thread (g, jj): column j0 + jj, canonical lanes L = g + 32q (q < 8), g < 32.
+template <class Epi>
 __global__ void __launch_bounds__(512, 2)
-dense_cols_partial_kernel(const double* __restrict__ A, int64_t m, int64_t n,
-                          const double* __restrict__ w, double* __restrict__ colpart) {
+dense_cols_kernel(const double* __restrict__ A, int64_t m, int64_t n,
+                  const double* __restrict__ w, double* __restrict__ colpart,
+                  unsigned* __restrict__ colcnt, const Epi epi) {
   __shared__ double sc[32][16];
   const int jj = threadIdx.x & 15, g = threadIdx.x >> 4;  // g: 0..31
   const int64_t j = static_cast<int64_t>(blockIdx.x) * 16 + jj;
@@ -158,41 +172,45 @@ dense_cols_partial_kernel(const double* __restrict__ A, int64_t m, int64_t n,
     if (g < h) sc[g][jj] = __dadd_rn(sc[g][jj], sc[g + h][jj]);
     __syncthreads();
   }
-  if (g == 0 && j < n) colpart[c * n + j] = sc[0][jj];
-}
-
-// level 2 over chunk partials for column j (nc <= 64, see create_dense)
-__device__ double dense_col_level2(const double* colpart, int64_t nc, int64_t n, int64_t j) {
-  if (nc == 1) return colpart[j];
-  double s[64];
-  int lanes = 1;
-  while (lanes < nc) lanes <<= 1;
-  for (int q = 0; q < lanes; ++q) s[q] = q < nc ? __dadd_rn(0.0, colpart[q * n + j]) : 0.0;
-  for (int h = lanes / 2; h >= 1; h >>= 1)
-    for (int q = 0; q < h; ++q) s[q] = __dadd_rn(s[q], s[q + h]);
-  return s[0];
-}
-
-__global__ void dense_sgd_cols_final_kernel(const DenseIterArgs a) {
-  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (j >= a.n) return;
-  const int64_t nc = (a.m + kChunk - 1) / kChunk;
-  const double acc = dense_col_level2(a.colpart, nc, a.n, j);
-  unsigned fl = 0;  // v epilogue
-  const double e = fabs(a.xs_cur[j]);
-  const double z = __dmul_rn(e, acc);
-  const double est = __dmul_rn(z, z);
-  double avg = a.vb[j];
-  const double xn = a.lin_v ? sgd_coord_lin(est, a.v[j], a.lin_v[j], a.cv, a.st, avg, fl)
-                            : sgd_coord(est, a.v[j], a.cv, a.st, avg, fl);
-  a.v[j] = xn;
-  a.vb[j] = avg;
-  if (a.has_next) {
-    const double dn = det_exp(xn);
-    a.xs_next[j] = dsign_bit(a.signs, a.sign_next_s + j) ? dn : -dn;
+  const int nc = static_cast<int>(gridDim.y);
+  if (nc == 1) {  // one chunk: the partial is the column sum
+    if (g == 0 && j < n) epi(j, sc[0][jj]);
+    return;
   }
-  if (fl) atomicOr(a.flags, fl);
+  if (g == 0 && j < n) colpart[c * n + j] = sc[0][jj];
+  // the strip's last chunk CTA folds level 2 and runs the epilogue (one launch
+  // instead of a partial kernel plus a final kernel)
+  __shared__ unsigned ticket;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(colcnt + blockIdx.x, 1u);
+  __syncthreads();
+  if (ticket != static_cast<unsigned>(nc - 1)) return;
+  __threadfence();
+  if (g == 0 && j < n) epi(j, dense_col_level2(colpart, nc, n, j));
+  if (threadIdx.x == 0) colcnt[blockIdx.x] = 0;  // ready for the next launch
 }
+
+// v epilogue of the dense SGD iteration (src/equilibrate.cpp:113-128) for column j
+struct ColsSgdEpi {
+  DenseIterArgs a;
+  __device__ void operator()(int64_t j, double acc) const {
+    unsigned fl = 0;
+    const double e = fabs(a.xs_cur[j]);
+    const double z = __dmul_rn(e, acc);
+    const double est = __dmul_rn(z, z);
+    double avg = a.vb[j];
+    const double xn = a.lin_v ? sgd_coord_lin(est, a.v[j], a.lin_v[j], a.cv, a.st, avg, fl)
+                              : sgd_coord(est, a.v[j], a.cv, a.st, avg, fl);
+    a.v[j] = xn;
+    a.vb[j] = avg;
+    if (a.has_next) {
+      const double dn = det_exp(xn);
+      a.xs_next[j] = dsign_bit(a.signs, a.sign_next_s + j) ? dn : -dn;
+    }
+    if (fl) atomicOr(a.flags, fl);
+  }
+};
 
 __device__ __forceinline__ void dense_pass_epi(const DensePassArgs& a, int64_t r, double acc) {
   switch (a.mode) {
@@ -222,19 +240,20 @@ __global__ void __launch_bounds__(256) dense_pass_rows_kernel(const DensePassArg
   if (lane == 0) dense_pass_epi(a, i, acc);
 }
 
-__global__ void dense_pass_cols_final_kernel(const DensePassArgs a) {
-  if (a.skip && *a.skip) return;
-  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (j >= a.n) return;
-  const int64_t nc = (a.m + kChunk - 1) / kChunk;
-  dense_pass_epi(a, j, dense_col_level2(a.colpart, nc, a.n, j));
-}
+struct ColsPassEpi {
+  DensePassArgs a;
+  __device__ void operator()(int64_t j, double acc) const {
+    if (a.skip && *a.skip) return;  // the counters still run, so they reset
+    dense_pass_epi(a, j, acc);
+  }
+};
 
-cudaError_t dense_cols_partial(const double* A, int64_t m, int64_t n, const double* w,
-                               double* colpart, cudaStream_t s) {
+template <class Epi>
+cudaError_t dense_cols(const double* A, int64_t m, int64_t n, const double* w, double* colpart,
+                       unsigned* colcnt, const Epi& epi, cudaStream_t s) {
   const dim3 grid(static_cast<unsigned>((n + 15) / 16),
                   static_cast<unsigned>((m + kChunk - 1) / kChunk));
-  dense_cols_partial_kernel<<<grid, 512, 0, s>>>(A, m, n, w, colpart);
+  dense_cols_kernel<Epi><<<grid, 512, 0, s>>>(A, m, n, w, colpart, colcnt, epi);
   count_launch(s);
   return cudaGetLastError();
 }
@@ -257,11 +276,8 @@ cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s, cudaSt
                           rs>>>(a);
   count_launch(rs);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  e = dense_cols_partial(a.A, a.m, a.n, a.xw_cur, a.colpart, s);
+  e = dense_cols(a.A, a.m, a.n, a.xw_cur, a.colpart, a.colcnt, ColsSgdEpi{a}, s);
   if (e != cudaSuccess) return e;
-  dense_sgd_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
-  count_launch(s);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (s2) {
     if ((e = cudaEventRecord(ev_join, s2)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return e;
@@ -277,11 +293,7 @@ cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s) {
     count_launch(s);
     return cudaGetLastError();
   }
-  const cudaError_t e = dense_cols_partial(a.A, a.m, a.n, a.xg, a.colpart, s);
-  if (e != cudaSuccess) return e;
-  dense_pass_cols_final_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
-  count_launch(s);
-  return cudaGetLastError();
+  return dense_cols(a.A, a.m, a.n, a.xg, a.colpart, a.colcnt, ColsPassEpi{a}, s);
 }
 
 }  // namespace eqb

@@ -1482,7 +1482,12 @@ void alloc_workspaces(equil_matrix* M, PhaseTimer* pt) {
   M->tmp_n.alloc(M->n_pad());
   M->tmp_m2.alloc(M->m_pad());
   M->tmp_n2.alloc(M->n_pad());
-  if (M->dense) M->colpart.alloc(((M->m + eqb::kChunk - 1) / eqb::kChunk) * M->n);
+  if (M->dense) {
+    M->colpart.alloc(((M->m + eqb::kChunk - 1) / eqb::kChunk) * M->n);
+    M->colcnt.alloc((M->n + 15) / 16);
+    CK(cudaMemsetAsync(M->colcnt.p, 0, ((M->n + 15) / 16) * sizeof(unsigned), M->stream));
+    CK(cudaStreamSynchronize(M->stream));
+  }
 }
 
 }  // namespace eqe
@@ -2115,6 +2120,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
       a.st = host_step(t);
       a.flags = M->flags.p;
       a.colpart = M->colpart.p;
+      a.colcnt = M->colcnt.p;
       return a;
     };
     auto one_iter = [&](int t) {
@@ -2476,6 +2482,7 @@ void apply_pass(equil_matrix* M, bool adjoint, const double* xg, double* out, in
     a.mode = mode;
     a.skip = skip;
     a.colpart = M->colpart.p;
+    a.colcnt = M->colcnt.p;
     CK(eqb::launch_dense_pass(a, M->stream));
     return;
   }

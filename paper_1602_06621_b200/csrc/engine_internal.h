@@ -540,6 +540,7 @@ struct equil_matrix {
 
   // dense
   DevBuf<double> Ad, colpart;
+  DevBuf<unsigned> colcnt;  // dense column strips: chunk CTAs done (dense.cu)
 
   // workspaces
   // padded gathered vectors e.*s (xs) and d.*w (xw), double-buffered, in one

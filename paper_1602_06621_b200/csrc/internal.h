@@ -370,7 +370,8 @@ struct DenseIterArgs {
   const double* lin_v;
   SgdStep st;
   unsigned* flags;
-  double* colpart;  // scratch: nchunks_m x n
+  double* colpart;   // scratch: nchunks_m x n
+  unsigned* colcnt;  // per 16-column strip: chunk CTAs done (zero between launches)
 };
 // s2 non-null: the row and column halves run concurrently on s2 / s
 cudaError_t launch_dense_sgd_iter(const DenseIterArgs& a, cudaStream_t s, cudaStream_t s2 = nullptr,
@@ -387,6 +388,7 @@ struct DensePassArgs {
   const int* skip;
   int mode;
   double* colpart;
+  unsigned* colcnt;
 };
 cudaError_t launch_dense_pass(const DensePassArgs& a, cudaStream_t s);
 
