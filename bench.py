@@ -50,6 +50,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c4 LSQR and c2 dense keys")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for the timing barriers (gloo + "
+                         "EQUIL_HOST_EXCHANGE=2 + --device 0: several ranks on one GPU, "
+                         "a test of the N > 1 path)")
+    ap.add_argument("--device", type=int, default=-1, help="GPU of every rank (default LOCAL_RANK)")
     ap.add_argument("--ref-iters", type=int, default=3,
                     help="reference arm: SGD iterations per step (one sgd_equilibrate call)")
     return ap.parse_args()
@@ -291,9 +296,21 @@ def run_ours(args):
     rank, world, local = dist_env()
     if args.gpus != world and world == 1 and args.gpus > 1:
         raise SystemExit("run N>1 under torch.distributed.run (one process per GPU)")
+    if args.device >= 0:
+        local = args.device
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=torch.device("cuda", local) if args.dist_backend == "nccl"
+                         else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     inst = configs.config(CONFIG_ID)
     T = inst.iterations
@@ -342,9 +359,7 @@ def run_ours(args):
     clk = clocks.stop()
     elapsed = ev0.elapsed_time(ev1) / 1e3
     if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+        elapsed = max_over_ranks(elapsed)
     value = T * args.steps / elapsed
 
     # ---- roofline of the dominant kernel (fused SGD pass), live CUDA events
@@ -401,9 +416,7 @@ def run_ours(args):
                                             world_size=world, nccl_id=obj[0])
             r = eq.sgd_equilibrate(M2, p)
             M2.close()
-            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-            ts.append(float(dt.item()))
+            ts.append(max_over_ranks(time.perf_counter() - t0))
         e2e_s = statistics.mean(ts)
         h2d = int(inst.row_ptr.nbytes + inst.col.nbytes + inst.val.nbytes) * world
         d2h = int(8 * 2 * (inst.m + inst.n)) * world
