@@ -306,6 +306,14 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
 // sequential chains start first), then the slices of A and of A^T.
 // Merge the two matrices' interleaved-slice lists (both longest first; ties
 // take A first) into the launch order, and lay out each matrix's arrays in it.
+// slices of at least this many entries per row are stored in the quad layout
+// (EQUIL_SELL_QUAD=0: none; EQUIL_QUAD_MIN: the threshold, default 64)
+int quad_min(const equil_matrix* M) {
+  if (!M->sell_quad) return 0x7fffffff;
+  static const int qm = getenv("EQUIL_QUAD_MIN") ? std::max(4, atoi(getenv("EQUIL_QUAD_MIN"))) : 64;
+  return qm;
+}
+
 void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
   equil_matrix::SellHost& H = M->sell_host;
   H = equil_matrix::SellHost{};
@@ -338,7 +346,7 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
     H.slices[w] = {H.total[mat], e.maxlen, e.cnt, static_cast<int16_t>(mat)};
     // long slices read by the warp-specialised kernel are stored in the quad
     // layout (128-bit stream loads), padded to a multiple of 4 entries
-    const bool quad = M->sell_long == 2 && M->sell_quad && e.maxlen > eqb::kTileNnz;
+    const bool quad = e.maxlen >= quad_min(M);
     H.total[mat] += 32 * (quad ? eqb::sell_quad_len(e.maxlen) : static_cast<int64_t>(e.maxlen));
     if (e.maxlen > 0) {
       H.midx[mat].push_back(static_cast<int32_t>(w));
@@ -356,10 +364,6 @@ void plan_sell(equil_matrix* M, const Plan& pa, const Plan& pt) {
 
 // The generic passes' column arrays (padded coordinates) and per-matrix slice
 // orders, on first use.
-// long slices are in the quad layout when the warp-specialised kernel reads them
-int quad_min(const equil_matrix* M) {
-  return M->sell_long == 2 && M->sell_quad ? eqb::kTileNnz + 1 : 0x7fffffff;
-}
 
 // per-matrix slice orders of the generic passes (both column flavours)
 void ensure_sell_order(equil_matrix* M) {
@@ -415,7 +419,7 @@ void sell_pass(equil_matrix* M, int mat, const eqb::PassArgs& a, const eqb::Pass
   cudaStream_t s = M->stream;
   eqb::SellArgs sa{};
   sa.xlen[0] = sa.xlen[1] = mat ? M->m_pad() : M->n_pad();  // padded coordinates
-  sa.quad = M->sell_long == 2 && M->sell_quad;
+  sa.quad_min = quad_min(M);
   sa.slices = M->sell_slices.p;
   sa.order = M->sell_pidx[mat].p;
   sa.row = M->sell_row.p;
@@ -2140,7 +2144,7 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
             eqb::SellArgs sa{};
             sa.xlen[0] = M->n_pad();  // A's rows gather xs, A^T's xw
             sa.xlen[1] = M->m_pad();
-            sa.quad = M->sell_long == 2 && M->sell_quad && M->sell_nb == 1;  // see plan_sell
+            sa.quad_min = M->sell_nb == 1 ? quad_min(M) : 0x7fffffff;  // see plan_sell
             sa.slices = M->sell_slices.p;
             sa.nslices = M->n_sell;
             sa.row = M->sell_row.p;

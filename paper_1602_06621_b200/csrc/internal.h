@@ -165,12 +165,13 @@ struct SellArgs {
   const int32_t* ci[2];     // interleaved slot columns
   const double* va[2];      // interleaved values
   int64_t xlen[2];          // length of the gathered vector(s) (checked builds)
-  int quad;                 // 1: long slices (maxlen > kTileNnz) in the quad layout
+  int quad_min;             // slices with maxlen >= quad_min are in the quad layout
 };
-// Quad layout of a long slice: entries 4q .. 4q+3 of lane l are adjacent, at
+// Quad layout of a slice: entries 4q .. 4q+3 of lane l are adjacent, at
 // off + 128 q + 4 l + (k % 4), so a lane streams its row with 128-bit loads
 // (four columns, two pairs of values); the slice is padded to a multiple of 4
-// entries.  Short slices keep entry k of lane l at off + 32 k + l.
+// entries.  Slices shorter than quad_min keep entry k of lane l at
+// off + 32 k + l (short rows would pay more padding than the loads save).
 constexpr int kQuad = 4;
 __host__ __device__ inline int64_t sell_quad_len(int64_t maxlen) { return (maxlen + 3) & ~int64_t(3); }
 // Device flag barrier of the fused all-gather (world > 1, NCCL transport): a

@@ -229,6 +229,13 @@ __device__ __forceinline__ int2 ld_st2(const int32_t* p) {
       : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_evict_first()));
   return v;
 }
+// 256-bit load (sm_100: LDG.E.NA.ENL2.256): a lane's whole quad of values in one
+// access, so a warp's value load is 1 KB contiguous (two 128-bit loads would
+// each touch every sector half-used, and without L1 allocation fetch it twice)
+__device__ __forceinline__ void ld_st4(const double* p, double* v) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p), "l"(l2_evict_first()));
+}
 __device__ __forceinline__ double2 ld_st2(const double* p) {
   double2 v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
@@ -341,27 +348,42 @@ __device__ __forceinline__ int slice_at(const SellArgs& sa, int i) {
   return sa.order ? __ldg(sa.order + i) : i;
 }
 
-// One warp per slice (rows <= kTileNnz).  B entries per lane per batch: B
-// column loads and B value loads, then the gathers, then the dependent adds.
-// PIPE: the next batch's column / value loads are issued before this batch's
-// gathers (one batch of CSR stream in flight behind the gathers).
-template <class Op, int B, bool PIPE, int MINB>
-__global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const SellArgs sa) {
+// The traversal of one warp slice, for its layout: Q = 1 (entry k of lane l
+// at 32 k + l: one 32-bit column and one 64-bit value load per entry) or
+// Q = kQuad (the lane's entries 4 at a time: one 128-bit column load and two
+// 128-bit value loads per quad).
+template <class Op, int B, bool PIPE, int Q>
+__device__ __forceinline__ void warp_slice(const Op& op, const SellArgs& sa, const SellSlice& sd,
+                                           int mat, int q, int len, int lane) {
+  static_assert(Q == 1 || B % kQuad == 0, "quad batches: whole quads");
   constexpr int NV = Op::NV;
-  if (op.skip()) return;
-  const int lane = threadIdx.x & 31;
-  const int i = sa.first + blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (i >= sa.nslices) return;
-  const int w = slice_at(sa, i);
-  const SellSlice sd = sa.slices[w];
-  const int mat = sd.mat;
-  const int q = 32 * w + lane;
-  const int len = __ldg(sa.len + q);
-  const int32_t* __restrict__ cp = pick(sa.ci, mat) + sd.off + lane;
-  const double* __restrict__ vp = pick(sa.va, mat) + sd.off + lane;
+  const int32_t* __restrict__ cp = pick(sa.ci, mat) + sd.off + (Q == 1 ? lane : 4 * lane);
+  const double* __restrict__ vp = pick(sa.va, mat) + sd.off + (Q == 1 ? lane : 4 * lane);
   const double* __restrict__ x = op.x(mat);
   const double* __restrict__ x2 = op.x2(mat);
   double acc = op.start(mat, q), acc2 = 0.0;
+  // entries k .. k + B - 1 of the lane's row (full: all within the row)
+  auto load = [&](int k, int32_t* c, double* v, bool full) {
+    if constexpr (Q == 1) {
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (full || k + b < len) c[b] = ld_st(cp + 32 * (k + b));
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (full || k + b < len) v[b] = ld_st(vp + 32 * (k + b));
+    } else {
+#pragma unroll
+      for (int t = 0; t < B / kQuad; ++t) {
+        const int kk = k + kQuad * t;  // a multiple of 4: whole quads
+        if (full || kk < len) {
+          const int64_t o = static_cast<int64_t>(kk >> 2) * 128;
+          const int4 c4 = ld_st4(cp + o);
+          c[4 * t] = c4.x, c[4 * t + 1] = c4.y, c[4 * t + 2] = c4.z, c[4 * t + 3] = c4.w;
+          ld_st4(vp + o, v + 4 * t);
+        }
+      }
+    }
+  };
   auto consume = [&](const int32_t* c, const double* v, int k0, bool full) {
     double g[B], g2[B];
 #pragma unroll
@@ -382,31 +404,20 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
     for (; k + B <= len; k += B) {
       int32_t c[B];
       double v[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) c[b] = ld_st(cp + 32 * (k + b));
-#pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = ld_st(vp + 32 * (k + b));
+      load(k, c, v, true);
       consume(c, v, k, true);
     }
   } else {
     if (k + B <= len) {
       int32_t c[B];
       double v[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) c[b] = ld_st(cp + 32 * b);
-#pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = ld_st(vp + 32 * b);
+      load(0, c, v, true);
       for (;;) {
         const int kn = k + B;
         const bool more = kn + B <= len;
         int32_t cn[B];
         double vn[B];
-        if (more) {
-#pragma unroll
-          for (int b = 0; b < B; ++b) cn[b] = ld_st(cp + 32 * (kn + b));
-#pragma unroll
-          for (int b = 0; b < B; ++b) vn[b] = ld_st(vp + 32 * (kn + b));
-        }
+        if (more) load(kn, cn, vn, true);
         consume(c, v, k, true);
         k = kn;
         if (!more) break;
@@ -421,17 +432,32 @@ __global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const
   if (k < len) {  // tail: fewer than B entries left
     int32_t c[B];
     double v[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (k + b < len) {
-        c[b] = ld_st(cp + 32 * (k + b));
-        v[b] = ld_st(vp + 32 * (k + b));
-      }
+    load(k, c, v, false);
     consume(c, v, k, false);
   }
   unsigned fl = 0;
   if (lane < sd.cnt) op.finish(mat, __ldg(sa.row + q), acc, acc2, fl, q);
   op.end(fl);
+}
+
+// One warp per slice (rows <= kTileNnz).  B entries per lane per batch: B
+// column loads and B value loads, then the gathers, then the dependent adds.
+// PIPE: the next batch's column / value loads are issued before this batch's
+// gathers (one batch of CSR stream in flight behind the gathers).  Slices with
+// maxlen >= sa.quad_min are in the quad layout (uniform branch per warp).
+template <class Op, int B, bool PIPE, int MINB>
+__global__ void __launch_bounds__(128, MINB) sell_warp_kernel(const Op op, const SellArgs sa) {
+  if (op.skip()) return;
+  const int lane = threadIdx.x & 31;
+  const int i = sa.first + blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (i >= sa.nslices) return;
+  const int w = slice_at(sa, i);
+  const SellSlice sd = sa.slices[w];
+  const int mat = sd.mat;
+  const int q = 32 * w + lane;
+  const int len = __ldg(sa.len + q);
+  if (sd.maxlen >= sa.quad_min) warp_slice<Op, B, PIPE, kQuad>(op, sa, sd, mat, q, len, lane);
+  else warp_slice<Op, B, PIPE, 1>(op, sa, sd, mat, q, len, lane);
 }
 
 // Long slices (rows longer than kTileNnz): one CTA per slice, warp-specialised.
@@ -487,8 +513,7 @@ sell_long_kernel(const Op op, const SellArgs sa) {
           if constexpr (B == 4) {
             const int4 c4 = ld_st4(cp + o);
             cc[0] = c4.x, cc[1] = c4.y, cc[2] = c4.z, cc[3] = c4.w;
-            const double2 v0 = ld_st2(vp + o), v1 = ld_st2(vp + o + 2);
-            vv[0] = v0.x, vv[1] = v0.y, vv[2] = v1.x, vv[3] = v1.y;
+            ld_st4(vp + o, vv);
           } else {
             const int2 c2 = ld_st2(cp + o);
             cc[0] = c2.x, cc[1] = c2.y;
@@ -607,7 +632,7 @@ void launch_long_q(const Op& op, const SellArgs& sa, cudaStream_t s) {
 // the slices' layout picks the instantiation (quad: 128-bit stream loads)
 template <class Op, int B, int S, bool PIPE, int MINB>
 void launch_long(const Op& op, const SellArgs& sa, cudaStream_t s) {
-  if (sa.quad) launch_long_q<Op, B, S, PIPE, MINB, kQuad>(op, sa, s);
+  if (sa.quad_min <= kTileNnz + 1) launch_long_q<Op, B, S, PIPE, MINB, kQuad>(op, sa, s);
   else launch_long_q<Op, B, S, PIPE, MINB, 1>(op, sa, s);
 }
 
@@ -742,7 +767,7 @@ cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArg
         case 1: launch_long<PassPairOp, 4, 15, true, 1>(op, sa, s); break;
         case 2: launch_long<PassPairOp, 4, 7, true, 2>(op, sa, s); break;
         default:  // quad layout: a round is one whole quad (B = 4), else B = 2
-          if (sa.quad) launch_long<PassPairOp, 4, 15, true, 1>(op, sa, s);
+          if (sa.quad_min <= kTileNnz + 1) launch_long<PassPairOp, 4, 15, true, 1>(op, sa, s);
           else launch_long<PassPairOp, 2, 15, true, 1>(op, sa, s);
           break;
       }
@@ -759,7 +784,7 @@ cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArg
         case 1: launch_long<PassOp<2>, 4, 15, true, 1>(op, sa, s); break;
         case 2: launch_long<PassOp<2>, 4, 7, true, 2>(op, sa, s); break;
         default:
-          if (sa.quad) launch_long<PassOp<2>, 4, 15, true, 1>(op, sa, s);
+          if (sa.quad_min <= kTileNnz + 1) launch_long<PassOp<2>, 4, 15, true, 1>(op, sa, s);
           else launch_long<PassOp<2>, 2, 15, true, 1>(op, sa, s);
           break;
       }
