@@ -727,7 +727,18 @@ cudaError_t launch_sgd_sell_split(const SgdIterArgs& a, const SellArgs& sa, bool
       case 3: launch_warp<SgdSplitOp, 4, true, 12>(op, sa, s); break;
       case 4: launch_warp<SgdSplitOp, 16, false, 8>(op, sa, s); break;
       case 5: launch_warp<SgdSplitOp, 8, false, 10>(op, sa, s); break;
-      default: launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s); break;
+      case 6: launch_warp<SgdSplitOp, 8, true, 7>(op, sa, s); break;
+      case 7: launch_warp<SgdSplitOp, 4, true, 8>(op, sa, s); break;
+      case 8: launch_warp<SgdSplitOp, 4, true, 10>(op, sa, s); break;
+      case 9: launch_warp<SgdSplitOp, 8, false, 8>(op, sa, s); break;
+      case 10: launch_warp<SgdSplitOp, 4, true, 14>(op, sa, s); break;
+      case 11: launch_warp<SgdSplitOp, 4, true, 11>(op, sa, s); break;
+      case 12: launch_warp<SgdSplitOp, 8, true, 9>(op, sa, s); break;
+      case 13: launch_warp<SgdSplitOp, 4, false, 12>(op, sa, s); break;
+      case 14: launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s); break;
+      // quad layout (256-bit value loads): 56 registers, 9 CTAs per SM (c3:
+      // 0.997-1.010 vs 1.067-1.083 ms at <8, true, 6>)
+      default: launch_warp<SgdSplitOp, 8, true, 9>(op, sa, s); break;
     }
   }
   count_launch(s);
@@ -774,7 +785,11 @@ cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArg
     } else {
       switch (pv) {
         case 4: launch_warp<PassPairOp, 8, true, 6>(op, sa, s); break;
-        default: launch_warp<PassPairOp, 4, true, 6>(op, sa, s); break;
+        case 5: launch_warp<PassPairOp, 4, true, 10>(op, sa, s); break;
+        case 6: launch_warp<PassPairOp, 4, true, 6>(op, sa, s); break;
+        case 7: launch_warp<PassPairOp, 8, true, 8>(op, sa, s); break;
+        // 8 CTAs per SM on the quad layout (c4: 1.208-1.211 vs 1.227-1.228 ms at 6)
+        default: launch_warp<PassPairOp, 4, true, 8>(op, sa, s); break;
       }
     }
   } else if (b) {
@@ -796,8 +811,16 @@ cudaError_t launch_sell_pass(const PassArgs& a, const PassArgs* b, const SellArg
     }
   } else {
     const PassOp<1> op{a, a};
-    if (lng) launch_long<PassOp<1>, 4, 15, true, 1>(op, sa, s);
-    else launch_warp<PassOp<1>, 8, true, 6>(op, sa, s);
+    if (lng) {
+      launch_long<PassOp<1>, 4, 15, true, 1>(op, sa, s);
+    } else {
+      switch (pv) {
+        case 5: launch_warp<PassOp<1>, 8, true, 9>(op, sa, s); break;
+        case 6: launch_warp<PassOp<1>, 8, true, 6>(op, sa, s); break;
+        case 7: launch_warp<PassOp<1>, 4, true, 10>(op, sa, s); break;
+        default: launch_warp<PassOp<1>, 8, true, 8>(op, sa, s); break;
+      }
+    }
   }
   count_launch(s);
   return cudaGetLastError();
