@@ -262,12 +262,16 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
     EQ_CUDA_TRY(cudaMemcpyAsync(pos, hpos.data(), hpos.size() * sizeof(uint16_t),
                                 cudaMemcpyHostToDevice, s));
   const size_t smem = (kJumpWords + mt::kN + kJumpGroups * mt::kN) * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
+  // the attribute belongs to the device context: set it once per device
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  EQ_CUDA_TRY(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ULL << (dev & 63);
+  if (!(attr_done.load() & bit)) {
     EQ_CUDA_TRY(cudaFuncSetAttribute(mt_jump_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    attr = true;
+    attr_done.fetch_or(bit);
   }
   for (int a = 0; a < levels; ++a) {
     const uint64_t lo = 1ULL << a;
