@@ -203,7 +203,25 @@ def lsqr_bytes(inst) -> float:
     return 24.0 * nnz + 4.0 * (m + n) + 8.0 * (5 * m + 9 * n)
 
 
-def c4_experiment(eq, M, inst, peak: float, curve_every: int = 25) -> dict:
+def c4_cpu_lsqr(inst, b) -> dict:
+    """The reference's LSQR per iteration on the host: the oracle
+    C port (bit-identical to the reference's sources), 1 thread, on the full c3
+    matrix; the difference of a 3- and a 1-iteration solve."""
+    import oracle
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    O = oracle.c_oracle()
+    t0 = time.perf_counter()
+    O.lsqr(A, b, 1, 0.0)
+    t1 = time.perf_counter()
+    O.lsqr(A, b, 3, 0.0)
+    t2 = time.perf_counter()
+    per = ((t2 - t1) - (t1 - t0)) / 2
+    return {"ms_per_lsqr_iteration": per * 1e3, "cores": 1, "kind": "port",
+            "sample": "oracle lsqr on the full c3 matrix, 3 minus 1 iterations, 1 thread",
+            **host_cpu()}
+
+
+def c4_experiment(eq, M, inst, peak: float, curve_every: int = 25, cpu: bool = False) -> dict:
     """BASELINE configs[3] on the resident c3 matrix: plain lsqr (500) and
     lsqr_preconditioned (T=50 + 500), tol 0 -- run_lsqr_experiment's two
     variants (src/experiments.cpp:234-281).  Per-iteration time from the
@@ -248,7 +266,8 @@ def c4_experiment(eq, M, inst, peak: float, curve_every: int = 25) -> dict:
                          "frac": B / per_it / 1e9 / peak},
             "residual_vs_total_iteration": {"plain": curve(list(plain.residual_history)),
                                             f"equil{T}": curve(list(pre.residual_history))},
-            "check": {"bit_identical_to_oracle": check}}
+            "check": {"bit_identical_to_oracle": check},
+            "cpu_baseline": c4_cpu_lsqr(inst, b) if cpu else None}
 
 
 def c2_dense(eq, peak: float) -> dict:
@@ -442,7 +461,8 @@ def run_ours(args):
         check["e2e_bit_identical_to_oracle"] = check_vs_fixture(
             inst, dict(zip("uvde", pin_out)))["bit_identical_to_oracle"]
         if not args.no_extras:
-            extra["c4_lsqr"] = c4_experiment(eq, M, inst, peak)
+            extra["c4_lsqr"] = c4_experiment(eq, M, inst, peak,
+                                             cpu=rank == 0 and not args.no_cpu_baseline)
             extra["c2_dense"] = c2_dense(eq, peak)
 
     cpu = None
@@ -459,6 +479,10 @@ def run_ours(args):
             "data": "synthetic (seeded generator restating BASELINE configs[2])",
             "config": workload_config(inst, world),
             "ms_per_iteration": elapsed / args.steps / T * 1e3,
+            # a step = sign stream (K1, all T iterations) + init + the T-iteration
+            # loop + final exp (signs reported apart, and inside value)
+            "step_breakdown_ms": {"loop": kern_s * 1e3 * T,
+                                  "signs_init_final": elapsed / args.steps * 1e3 - kern_s * 1e3 * T},
             "achieved_GBps": B * value / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
