@@ -15,6 +15,8 @@
 // round-to-nearest intrinsic; the library is also built with --fmad=false.
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -243,18 +245,38 @@ cudaError_t sign_stream_generate(uint64_t seed, uint64_t stream, uint64_t total,
   uint16_t* pos = reinterpret_cast<uint16_t*>(windows + G * mt::kN);
   // host: seeding state and, per tree level, the set-bit positions of the
   // jump polynomial x^(2^(k+a)) mod phi
-  static thread_local std::vector<uint64_t> seedw(mt::kN), poly(mt::kPolyWords);
+  static thread_local std::vector<uint64_t> seedw(mt::kN);
   static thread_local std::vector<uint16_t> hpos;
   std::vector<int> npos8(levels);
   hpos.assign(static_cast<size_t>(levels) * kPosCap, static_cast<uint16_t>(kJumpWords));
   mt::seed_state(seed, stream, seedw.data());
-  for (int a = 0; a < levels; ++a) {
-    if (!mt::jump_poly_pow2(k + a, poly.data())) return cudaErrorUnknown;
-    uint16_t* dst = hpos.data() + static_cast<size_t>(a) * kPosCap;
+  // set-bit positions of x^(2^j) mod phi: constants of the generator, computed
+  // once per j and process (the per-call scan of 19937 bits per level was
+  // host time the device waited for)
+  struct JumpPositions {
+    std::vector<uint16_t> pos;
     int cnt = 0;
-    for (int i = 0; i < mt::kDegree; ++i)
-      if ((poly[i >> 6] >> (i & 63)) & 1ULL) dst[cnt++] = static_cast<uint16_t>(i);
-    npos8[a] = (cnt + 7) / 8;  // tail slots keep the zero-window sentinel
+  };
+  static std::mutex jp_mu;
+  static std::map<int, JumpPositions> jp_cache;
+  for (int a = 0; a < levels; ++a) {
+    const JumpPositions* jp = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(jp_mu);
+      auto it = jp_cache.find(k + a);
+      if (it == jp_cache.end()) {
+        std::vector<uint64_t> poly(mt::kPolyWords);
+        if (!mt::jump_poly_pow2(k + a, poly.data())) return cudaErrorUnknown;
+        JumpPositions j;
+        for (int i = 0; i < mt::kDegree; ++i)
+          if ((poly[i >> 6] >> (i & 63)) & 1ULL) j.pos.push_back(static_cast<uint16_t>(i));
+        j.cnt = static_cast<int>(j.pos.size());
+        it = jp_cache.emplace(k + a, std::move(j)).first;
+      }
+      jp = &it->second;  // map nodes are stable
+    }
+    std::copy(jp->pos.begin(), jp->pos.end(), hpos.begin() + static_cast<size_t>(a) * kPosCap);
+    npos8[a] = (jp->cnt + 7) / 8;  // tail slots keep the zero-window sentinel
   }
   EQ_CUDA_TRY(cudaMemcpyAsync(windows, seedw.data(), mt::kN * sizeof(uint64_t),
                               cudaMemcpyHostToDevice, s));
