@@ -131,6 +131,41 @@ int main() {
     printf("no cuTensorMapEncodeTiled\n");
     return 1;
   }
+  // concurrency: LSU gathers (stream a) and TMA gather4 (stream b) at the same
+  // time -- does the TMA unit add gather capacity beside the LSU / L1TEX path?
+  auto concurrent = [&](const CUtensorMap& tm, const double* x, int lsu_ctas, int tma_ctas) {
+    cudaStream_t sa, sb;
+    cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking);
+    constexpr int ROWS = 32 * 1 * 4;
+    const int64_t per = (n / tma_ctas) / ROWS * ROWS;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaDeviceSynchronize();
+      cudaEventRecord(a, 0);
+      cudaStreamWaitEvent(sa, a, 0);
+      cudaStreamWaitEvent(sb, a, 0);
+      lsu_gather<<<lsu_ctas, 256, 0, sa>>>(idx, x, n, out);
+      if (tma_ctas) tma_gather<1, 4, 3><<<tma_ctas, 128, 0, sb>>>(tm, idx, per, out);
+      cudaEvent_t ea, eb;
+      cudaEventCreate(&ea);
+      cudaEventCreate(&eb);
+      cudaEventRecord(ea, sa);
+      cudaEventRecord(eb, sb);
+      cudaStreamWaitEvent(0, ea, 0);
+      cudaStreamWaitEvent(0, eb, 0);
+      cudaEventRecord(b, 0);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      const double tot = static_cast<double>(n) + (tma_ctas ? static_cast<double>(per) * tma_ctas : 0.0);
+      if (rep == 1)
+        printf("concurrent lsu ctas %5d + tma ctas %5d: %.3f ms for %.0fM + %.0fM gathers = %.1f G/s total\n",
+               lsu_ctas, tma_ctas, ms, n / 1e6, tma_ctas ? per * tma_ctas / 1e6 : 0.0, tot / ms / 1e6);
+    }
+  };
   for (int range : {1000000, 2000000}) {  // doubles (8 / 16 MB)
     double* x;
     cudaMalloc(&x, (size_t)range * 8);
@@ -162,13 +197,10 @@ int main() {
       printf("lsu ldg 8B gathers (one per 32-byte row): %.3f ms  %.1f G/s\n", ms / 5, n / (ms / 5) / 1e6);
     }
     run_tma<1, 4, 3>(tm, idx, n, 148 * 12, out, "");
-    run_tma<1, 8, 3>(tm, idx, n, 148 * 7, out, "");
-    run_tma<1, 4, 1>(tm, idx, n, 148 * 16, out, "");
-    run_tma<1, 2, 1>(tm, idx, n, 148 * 24, out, "");
-    run_tma<1, 4, 7>(tm, idx, n, 148 * 8, out, "");
-    run_tma<1, 8, 7>(tm, idx, n, 148 * 4, out, "");
-    run_tma<1, 8, 15>(tm, idx, n, 148 * 2, out, "");
-    run_tma<2, 4, 7>(tm, idx, n, 148 * 3, out, "");
+    concurrent(tm, x, 148 * 8, 0);
+    concurrent(tm, x, 148 * 4, 148 * 8);
+    concurrent(tm, x, 148 * 6, 148 * 6);
+    concurrent(tm, x, 148 * 8, 148 * 4);
     cudaFree(x);
   }
   return 0;
