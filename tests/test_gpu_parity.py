@@ -793,6 +793,8 @@ TRAVERSALS = [
     {"EQUIL_SELL_VARIANT": "1", "EQUIL_SELL_LVARIANT": "3"},
     {"EQUIL_SELL_VARIANT": "3", "EQUIL_SELL_LVARIANT": "4"},
     {"EQUIL_SELL_ORDER": "1"},                             # warp slices in window order
+    {"EQUIL_SELL_QUAD": "0"},                              # every slice 1-wide (no 128/256-bit loads)
+    {"EQUIL_SELL_VARIANT": "14"},                          # warp slices at 6 CTAs/SM (80 registers)
     {"EQUIL_SPLIT_EPI": "0"},                              # SGD update fused into the traversals
     {"EQUIL_BLOCK_MB": "0.004"},                           # 500-coordinate column blocks
     {"EQUIL_BLOCK_MB": "0.004", "EQUIL_SELL_BLOCKED": "1"},  # same on interleaved slices
