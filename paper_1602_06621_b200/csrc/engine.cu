@@ -81,6 +81,7 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
       1, std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), nwin / 8)));
   struct Part {
     std::vector<eqb::Tile> slices;
+    std::vector<int32_t> maxlen;  // of each slice: its first row's length
     std::vector<int32_t> rowlist;
     std::vector<std::pair<int64_t, int64_t>> longs;
   };
@@ -88,25 +89,46 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   auto work = [&](int t) {
     Part& pt = parts[t];
     const int64_t wa = nwin * t / nth, wb = nwin * (t + 1) / nth;
-    std::vector<std::pair<int64_t, int32_t>> win;
+    pt.rowlist.reserve(static_cast<size_t>((wb - wa) * eqb::kSliceWindow));
+    pt.slices.reserve(static_cast<size_t>((wb - wa) * (eqb::kSliceWindow / eqb::kSliceRows + 1)));
+    pt.maxlen.reserve(pt.slices.capacity());
+    // a window's rows by decreasing length, ties in row order (a stable
+    // counting sort: lengths are at most kTileNnz)
+    std::vector<int32_t> start(eqb::kTileNnz + 2);
+    std::vector<int32_t> wlen(eqb::kSliceWindow);
     for (int64_t w = wa; w < wb; ++w) {
       const int64_t w0 = w * eqb::kSliceWindow;
       const int64_t w1 = std::min<int64_t>(rows, w0 + eqb::kSliceWindow);
-      win.clear();
+      std::fill(start.begin(), start.end(), 0);
+      int nshort = 0;
       for (int64_t i = w0; i < w1; ++i) {
         const int64_t len = rp[i + 1] - rp[i];
-        if (len > eqb::kTileNnz)
+        if (len > eqb::kTileNnz) {
           pt.longs.push_back({len, i});
-        else
-          win.push_back({len, static_cast<int32_t>(i)});
+          wlen[i - w0] = -1;
+        } else {
+          wlen[i - w0] = static_cast<int32_t>(len);
+          ++start[len];
+          ++nshort;
+        }
       }
-      std::stable_sort(win.begin(), win.end(),
-                       [](const auto& a, const auto& b) { return a.first > b.first; });
-      for (size_t q = 0; q < win.size(); q += eqb::kSliceRows) {
-        const int cnt = static_cast<int>(std::min<size_t>(eqb::kSliceRows, win.size() - q));
-        pt.slices.push_back({static_cast<int32_t>(pt.rowlist.size()), cnt, 2,
-                             static_cast<int16_t>(mat), 0});
-        for (int k = 0; k < cnt; ++k) pt.rowlist.push_back(win[q + k].second);
+      int32_t run = 0;  // start[l] = rows longer than l
+      for (int l = eqb::kTileNnz; l >= 0; --l) {
+        const int32_t c = start[l];
+        start[l] = run;
+        run += c;
+      }
+      const size_t base = pt.rowlist.size();
+      pt.rowlist.resize(base + nshort);
+      for (int64_t i = w0; i < w1; ++i) {
+        const int32_t l = wlen[i - w0];
+        if (l >= 0) pt.rowlist[base + start[l]++] = static_cast<int32_t>(i);
+      }
+      for (int q = 0; q < nshort; q += eqb::kSliceRows) {
+        const int cnt = std::min<int>(eqb::kSliceRows, nshort - q);
+        pt.slices.push_back({static_cast<int32_t>(base + q), cnt, 2, static_cast<int16_t>(mat), 0});
+        const int32_t r = pt.rowlist[base + q];
+        pt.maxlen.push_back(static_cast<int32_t>(rp[r + 1] - rp[r]));
       }
     }
   };
@@ -115,12 +137,22 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   work(0);
   for (auto& x : th) x.join();
   std::vector<std::pair<int64_t, int64_t>> longs;
+  std::vector<int32_t> slice_max;  // parallel to P.slices until the mids are inserted
+  {
+    size_t ns = 0, nr = 0;
+    for (const Part& pt : parts) ns += pt.slices.size(), nr += pt.rowlist.size();
+    P.slices.reserve(ns);
+    slice_max.reserve(ns);
+    P.rowlist.reserve(static_cast<size_t>(rows));
+    (void)nr;
+  }
   for (Part& pt : parts) {
     const int32_t base = static_cast<int32_t>(P.rowlist.size());
     for (eqb::Tile s : pt.slices) {
       s.r0 += base;
       P.slices.push_back(s);
     }
+    slice_max.insert(slice_max.end(), pt.maxlen.begin(), pt.maxlen.end());
     P.rowlist.insert(P.rowlist.end(), pt.rowlist.begin(), pt.rowlist.end());
     longs.insert(longs.end(), pt.longs.begin(), pt.longs.end());
   }
@@ -141,6 +173,11 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
       for (int k = 0; k < cnt; ++k) P.rowlist.push_back(static_cast<int32_t>(longs[q + k].second));
     }
     P.slices.insert(P.slices.begin(), mids.begin(), mids.end());
+    // globally sorted: a mid slice's first row is its longest
+    std::vector<int32_t> mmax;
+    for (size_t q = first_mid; q < longs.size(); q += eqb::kSliceRows)
+      mmax.push_back(static_cast<int32_t>(longs[q].first));
+    slice_max.insert(slice_max.begin(), mmax.begin(), mmax.end());
     nlong = first_mid;
   }
   for (size_t q = 0; q < nlong; q += eqb::kLongRows) {
@@ -163,7 +200,11 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
   // (long groups first, longest first; then the warp slices in window order)
   P.sell.reserve(P.lng.size() / eqb::kTileWarps + P.slices.size());
   for (size_t q = 0; q < P.lng.size(); q += eqb::kTileWarps) P.sell.push_back(ent(P.lng[q], 1));
-  for (const eqb::Tile& t : P.slices) P.sell.push_back(ent(t, 0));
+  // (every slice is sorted longest first, so its first row gives maxlen)
+  for (size_t q = 0; q < P.slices.size(); ++q) {
+    const eqb::Tile& t = P.slices[q];
+    P.sell.push_back(SellEnt{slice_max[q], static_cast<int16_t>(t.r1), 0, t.r0});
+  }
   return P;
 }
 
@@ -557,8 +598,11 @@ void build_sell_layout(equil_matrix* M, bool with_values) {
   if (blocked && (!M->sell_blocked || M->sell_long == 0)) return;
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
+  // (allocations ordered on s: the host may be ahead of the device here, and a
+  // host-synchronous pool allocation would grow the pool instead of reusing what
+  // the transpose's temporaries free in stream order)
   auto upload = [&](auto& d, const auto& h) {
-    d.alloc(h.size());
+    d.alloc_async(h.size(), s);
     h2d(M, d.p, h.data(), h.size() * sizeof(h[0]));
   };
   upload(M->sell_slices, H.slices);
@@ -567,8 +611,8 @@ void build_sell_layout(equil_matrix* M, bool with_values) {
     DevBuf<int32_t> dr0;
     dr0.alloc_on(H.r0.size(), s);
     h2d(M, dr0.p, H.r0.data(), H.r0.size() * 4);
-    M->sell_row.alloc(32 * static_cast<size_t>(M->n_sell));
-    M->sell_len.alloc(32 * static_cast<size_t>(M->n_sell));
+    M->sell_row.alloc_async(32 * static_cast<size_t>(M->n_sell), s);
+    M->sell_len.alloc_async(32 * static_cast<size_t>(M->n_sell), s);
     CK(eqb::launch_sell_rows(M->sell_slices.p, dr0.p, M->n_sell, M->rowlist_a.p,
                              M->rowlist_t.p, M->A.row_ptr, M->AT.row_ptr, M->sell_row.p,
                              M->sell_len.p, s));
@@ -577,8 +621,8 @@ void build_sell_layout(equil_matrix* M, bool with_values) {
   while (M->n_sell_long < M->n_sell && H.slices[M->n_sell_long].maxlen > eqb::kTileNnz)
     ++M->n_sell_long;
   for (int mat = 0; mat < 2 && !blocked; ++mat) {
-    M->sell_ci[mat].alloc(H.total[mat]);
-    M->sell_va[mat].alloc(H.total[mat]);
+    M->sell_ci[mat].alloc_async(H.total[mat], s);
+    M->sell_va[mat].alloc_async(H.total[mat], s);
     // columns of A index xs (slot map smap), columns of A^T index xw (wmap);
     // the values follow in build_sell_values once they are on the device
     build_sell_arrays(M, mat, true, with_values);

@@ -252,6 +252,19 @@ struct DevBuf {
     dev = d;
     n = count;
   }
+  // A persistent buffer first used on stream s (setup): the allocation is
+  // ordered on s, so it reuses memory that earlier temporaries of s freed and
+  // the host does not wait; other streams must be ordered after this point of
+  // s before they touch it.  Freed like alloc()'s buffers (device sync first).
+  void alloc_async(size_t count, cudaStream_t s) {
+    release();
+    if (count == 0) count = 1;
+    int d = 0;
+    CK(cudaGetDevice(&d));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    dev = d;
+    n = count;
+  }
   void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'ed array
     release();
     p = q;
