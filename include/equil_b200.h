@@ -176,6 +176,11 @@ double equil_last_loop_ms(equil_matrix* A, int* iterations);
  * 0 single GPU / not yet negotiated, 1 padded all-gathers (NCCL or host
  * exchange), 2 fused peer stores from the SGD epilogue + one-word barrier. */
 int equil_exchange_mode(const equil_matrix* A);
+/* How the SGD passes traverse the rows of A longer than 512 entries: 0 the
+ * warp-specialised long-slice kernel (or no such rows), 1 the column sweep
+ * (one persistent CTA per SM, gathered vector in shared-memory panels).  No
+ * reference counterpart (the result is the same bit for bit). */
+int equil_sweep_active(const equil_matrix* A);
 /* Number of this library's kernels launched so far in the process. */
 long long equil_kernel_launches(void);
 /* Build flags of the loaded library: bit 0 = checked build (EQ_CHECK device

@@ -13,7 +13,7 @@ from .api import (DEFAULT_MAX_LOG_SCALE, K_AUTO_TARGET, SGD_PROBE_STREAM,
                   lasso_objective, spectral_norm, det_exp_device, kernel_launches,
                   SeededRng, gradient, gradient_weighted, objective, objective_weighted,
                   project_box, rms_error, stochastic_gradient_estimate,
-                  last_loop_ms, exchange_mode, lsqr, lsqr_preconditioned, nccl_unique_id,
+                  last_loop_ms, exchange_mode, sweep_active, lsqr, lsqr_preconditioned, nccl_unique_id,
                   partition_rows, resolve_targets, sgd_equilibrate, sgd_equilibrate_csr,
                   sgd_equilibrate_block, sgd_equilibrate_symmetric, sgd_equilibrate_targets,
                   sgd_equilibrate_device, sign_bits, validate_params,
@@ -29,7 +29,7 @@ __all__ = [
     "DiagnosticsConfig",
     "EquilibrationParams", "EquilRuntimeError", "ExplicitMatrix", "InvalidArgument",
     "IterationRecord", "LsqrRun", "ScalingResult", "canon_sumsq_device", "det_exp_device",
-    "kernel_launches", "last_loop_ms", "exchange_mode", "lsqr", "lsqr_preconditioned", "nccl_unique_id",
+    "kernel_launches", "last_loop_ms", "exchange_mode", "sweep_active", "lsqr", "lsqr_preconditioned", "nccl_unique_id",
     "partition_rows", "resolve_targets", "sgd_equilibrate", "sgd_equilibrate_csr",
     "sgd_equilibrate_block", "sgd_equilibrate_device", "sgd_equilibrate_symmetric",
     "sgd_equilibrate_targets", "sign_bits", "validate_params",

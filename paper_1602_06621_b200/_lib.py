@@ -93,6 +93,7 @@ SIGNATURES = {
     "equil_matrix_stream": (C.c_void_p, [C.c_void_p]),
     "equil_last_loop_ms": (C.c_double, [C.c_void_p, _ip]),
     "equil_exchange_mode": (C.c_int, [C.c_void_p]),
+    "equil_sweep_active": (C.c_int, [C.c_void_p]),
     "equil_kernel_launches": (C.c_longlong, []),
     "equil_build_flags": (C.c_int, []),
     "equil_apply": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int]),

@@ -770,6 +770,12 @@ def exchange_mode(op: ExplicitMatrix) -> str:
     return ("single", "allgather", "p2p")[int(L.load().equil_exchange_mode(op._h))]
 
 
+def sweep_active(op: ExplicitMatrix) -> bool:
+    """True if the SGD passes run A's rows of more than 512 entries on the
+    column sweep (csrc/sweep.cu) rather than the long-slice kernel."""
+    return bool(L.load().equil_sweep_active(op._h))
+
+
 def kernel_launches() -> int:
     return int(L.load().equil_kernel_launches())
 

@@ -30,7 +30,7 @@ CHECKED_LIB = os.path.join(HERE, "libequil_b200_checked.so")
 GEN_LIB = os.path.join(HERE, "libequil_gen.so")  # synthetic inputs (bench/tests)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["engine.cu", "engine_ext.cu", "engine_op.cu", "kernels.cu", "transpose.cu", "sell.cu", "variants.cu", "dense.cu"]
+CU_SOURCES = ["engine.cu", "engine_ext.cu", "engine_op.cu", "kernels.cu", "transpose.cu", "sell.cu", "sweep.cu", "variants.cu", "dense.cu"]
 CXX_SOURCES = ["mt64_host.cpp", "mmio.cpp"]
 HEADERS = ["det_math.cuh", "internal.h", "mt64_host.h", "sgd_common.cuh", "mmio.h",
            "engine_internal.h"]

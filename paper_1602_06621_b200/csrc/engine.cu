@@ -180,6 +180,7 @@ Plan plan_tiles(const int64_t* rp, int64_t rows, int mat) {
     slice_max.insert(slice_max.begin(), mmax.begin(), mmax.end());
     nlong = first_mid;
   }
+  for (size_t q = 0; q < nlong; ++q) P.long_nnz += longs[q].first;
   for (size_t q = 0; q < nlong; q += eqb::kLongRows) {
     const int cnt = static_cast<int>(std::min<size_t>(eqb::kLongRows, nlong - q));
     const eqb::Tile t{static_cast<int32_t>(P.rowlist.size()), cnt, 3,
@@ -295,6 +296,13 @@ void setup_common(equil_matrix* M, const equil_device_cfg* cfg) {
   if (const char* e = getenv("EQUIL_SELL_BLOCKED")) M->sell_blocked = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_BLOCK_WIN")) M->block_win = atoi(e) != 0;
   if (const char* e = getenv("EQUIL_SPLIT_EPI")) M->split_epi = atoi(e) != 0;
+  if (const char* e = getenv("EQUIL_SWEEP")) {
+    M->use_sweep = atoi(e) != 0;
+    M->sweep_forced = M->use_sweep;
+  }
+  if (const char* e = getenv("EQUIL_SWEEP_WIDTH")) M->sweep_width = std::max(256, atoi(e) & ~1);
+  if (const char* e = getenv("EQUIL_SWEEP_STAGES")) M->sweep_stages = std::max(2, atoi(e));
+
   require(M->rank >= 0 && M->rank < M->world, "device cfg: rank out of range");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -639,8 +647,132 @@ void build_sell_layout(equil_matrix* M, bool with_values) {
   if (blocked) M->sell_passes = false;            // the passes' arrays are not blocked
 }
 
+// Column sweep of A's long rows (sweep.cu): deal the rows to one CTA per SM
+// (longest first, boustrophedon, so every CTA gets the same count and a similar
+// number of entries), cut each row into its runs per panel, sort every (CTA,
+// panel)'s rows by run length and lay the blobs out.  The values follow in
+// build_sweep_values once they are on the device.
+void build_sweep_values(equil_matrix* M) {
+  if (!M->sweep || !M->sweep_values_pending) return;
+  const eqb::SweepArgs& sw = M->sweep_args;
+  CK(eqb::launch_sweep_fill(M->A.row_ptr, M->A.col, M->A.val, M->sweep_crow.p, sw.nctas, sw.rmax,
+                            sw.npanels, sw.width, M->sweep_perm.p, M->sweep_srun.p,
+                            M->sweep_gbase.p, M->sweep_nepad.p, M->sweep_rstart.p, M->sweep_off.p,
+                            M->sweep_blobs.p, false, true, M->stream));
+  M->sweep_values_pending = false;
+}
+
+void build_sweep_layout(equil_matrix* M, bool with_values) {
+  M->sweep = false;
+  M->sweep_values_pending = false;
+  if (!M->sweep_candidate || !M->sell || M->sell_nb != 1 || M->sell_long != 2 || !M->split_epi)
+    return;
+  const equil_matrix::SellHost& H = M->sell_host;
+  const std::vector<int32_t>& rows = M->sweep_rows_host;
+  if (rows.empty() || H.plong[1] != 0) return;  // (A^T's long rows stay on the long kernel)
+  cudaStream_t s = M->stream;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, M->device));
+  const int G = static_cast<int>(std::min<size_t>(nsm, rows.size()));
+  const int per = static_cast<int>((rows.size() + G - 1) / G);
+  const int R = (per + 127) / 128 * 128;
+  if (R > 896) return;  // 32 producer + R consumer threads per CTA
+  const int NG = R / 32;
+  std::vector<int32_t> crow(static_cast<size_t>(G) * R, -1);
+  for (size_t i = 0; i < rows.size(); ++i) {
+    const size_t round = i / G, pos = i % G;
+    const size_t c = (round & 1) ? G - 1 - pos : pos;
+    crow[c * R + round] = rows[i];
+  }
+  M->sweep_crow.alloc_async(crow.size(), s);
+  h2d(M, M->sweep_crow.p, crow.data(), crow.size() * 4);
+  // Panel width: two stages of (panel + the CTA's largest blob) must fit in
+  // shared memory.  A CTA's blob holds about W / n of its entries at 10 bytes
+  // each plus padding; start from that estimate and narrow if the layout
+  // disagrees (EQUIL_SWEEP_WIDTH fixes the first try).
+  const int64_t hdr = 16 + 4 * NG + 4 * R;
+  int W = M->sweep_width;
+  if (W <= 0) {
+    const double ent_per_col = static_cast<double>(M->sweep_long_nnz) / G / static_cast<double>(M->n);
+    const double budget = 227.0 * 1024 / 2 - hdr - 4.0 * R - 4096;
+    W = static_cast<int>(budget / (8.0 + 15.0 * ent_per_col));
+    W = std::max(128, std::min(W, 16384) / 512 * 512);
+  }
+  eqb::SweepArgs sw{};
+  std::vector<int64_t> off;
+  size_t ncp = 0;
+  int P = 0;
+  for (int attempt = 0;; ++attempt) {
+    if (attempt == 6) return;  // the rows do not fit this scheme
+    P = static_cast<int>((M->n + W - 1) / W);
+    ncp = static_cast<size_t>(G) * P;
+    DevBuf<uint16_t> runl;
+    runl.alloc_on(ncp * R, s);
+    M->sweep_rstart.alloc_async(ncp * R, s);
+    M->sweep_perm.alloc_async(ncp * R, s);
+    M->sweep_srun.alloc_async(ncp * R, s);
+    M->sweep_gbase.alloc_async(ncp * NG, s);
+    M->sweep_nepad.alloc_async(ncp, s);
+    CK(eqb::launch_sweep_runs(M->A.row_ptr, M->A.col, M->sweep_crow.p, G, R, P, W, runl.p,
+                              M->sweep_rstart.p, s));
+    CK(eqb::launch_sweep_sort(runl.p, G, R, P, M->sweep_perm.p, M->sweep_srun.p, M->sweep_gbase.p,
+                              M->sweep_nepad.p, s));
+    std::vector<uint32_t> ne(ncp);
+    CK(cudaMemcpyAsync(ne.data(), M->sweep_nepad.p, ncp * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    off.assign(ncp + 1, 0);
+    int64_t bmax = 0;
+    for (size_t q = 0; q < ncp; ++q) {
+      const int64_t b = hdr + 10 * static_cast<int64_t>(ne[q]);
+      off[q + 1] = off[q] + b;
+      bmax = std::max(bmax, b);
+    }
+    sw = eqb::SweepArgs{};
+    sw.nctas = G;
+    sw.rmax = R;
+    sw.npanels = P;
+    sw.width = W;
+    sw.ncols = M->n;
+    sw.blob_max = static_cast<unsigned>(bmax);
+    sw.stages = M->sweep_stages;
+    while (sw.stages > 2 && eqb::sweep_smem_bytes(sw) > 227 * 1024) --sw.stages;
+    if (eqb::sweep_smem_bytes(sw) <= 227 * 1024) break;
+    // narrower panels, smaller blobs: scale by what the largest blob may take
+    const double room = 227.0 * 1024 / 2 - 4.0 * R - 4.0 * P - 256 - 8.0 * W;
+    const double f = room > 4096 ? room / static_cast<double>(bmax) : 0.25;
+    const int Wn = static_cast<int>(W * std::min(0.8, 0.9 * f)) / 64 * 64;
+    if (Wn < 128) return;
+    W = Wn;
+  }
+  M->sweep_off.alloc_async(off.size(), s);
+  h2d(M, M->sweep_off.p, off.data(), off.size() * 8);
+  M->sweep_blobs.alloc_async(static_cast<size_t>(off[ncp]), s);
+  CK(cudaMemsetAsync(M->sweep_blobs.p, 0, static_cast<size_t>(off[ncp]), s));
+  CK(eqb::launch_sweep_fill(M->A.row_ptr, M->A.col, M->A.val, M->sweep_crow.p, G, R, P, W,
+                            M->sweep_perm.p, M->sweep_srun.p, M->sweep_gbase.p, M->sweep_nepad.p,
+                            M->sweep_rstart.p, M->sweep_off.p, M->sweep_blobs.p, true, with_values,
+                            s));
+  // h2d may have staged the host vectors in the pull arena; they are copied by now
+  CK(cudaStreamSynchronize(s));
+  sw.blobs = M->sweep_blobs.p;
+  sw.blob_off = M->sweep_off.p;
+  sw.crow = M->sweep_crow.p;
+  M->sweep_args = sw;
+  M->sweep = true;
+  M->sweep_values_pending = !with_values;
+  if (getenv("EQUIL_VERBOSE"))
+    fprintf(stderr, "[equil] sweep: %d CTAs x %d rows, %d panels of %d, %d stages, blobs %.1f MB (max %u B)\n",
+            G, R, P, W, sw.stages, off[ncp] / 1048576.0, sw.blob_max);
+}
+
 void upload_plans(equil_matrix* M, const Plan& pa, const Plan& pt) {
   if (M->use_sell) plan_sell(M, pa, pt);
+  M->sweep_rows_host.clear();
+  M->sweep_long_nnz = pa.long_nnz;
+  if (M->sweep_candidate)  // A's long rows, longest first (each group is listed once per warp)
+    for (size_t q = 0; q < pa.lng.size(); q += eqb::kTileWarps)
+      for (int k = 0; k < pa.lng[q].r1; ++k)
+        M->sweep_rows_host.push_back(pa.rowlist[pa.lng[q].r0 + k]);
   // kind-3 groups (4 entries each) first, so every group starts on a CTA
   std::vector<eqb::Tile> sgd = pa.lng;
   sgd.insert(sgd.end(), pt.lng.begin(), pt.lng.end());
@@ -944,7 +1076,8 @@ void build_slot_layout(equil_matrix* M, const int64_t* rpA_dev, const int64_t* r
   M->wmap.alloc(M->m_pad());
   M->smap.alloc(M->n_pad());
   CK(eqb::launch_slot_map(rpA_dev, M->m, abd, G, M->a_max, M->wmap.p, s));
-  CK(eqb::launch_slot_map(rpT_dev, M->n, tbd, G, M->t_max, M->smap.p, s));
+  // the column sweep walks xs in column order: A's columns keep their positions
+  CK(eqb::launch_slot_map(rpT_dev, M->n, tbd, G, M->t_max, M->smap.p, s, M->sweep_candidate));
   if (!M->use_sell || M->sell_long == 0) {  // slot-mapped columns of the staged traversal
     M->a_ci_sgd.alloc(M->A.nnz);
     M->t_ci_sgd.alloc(M->AT.nnz);
@@ -1409,6 +1542,14 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     fullA = M->A;
     fullT = M->AT;
     build_block_layout(M);
+    // column sweep of A's long rows (sweep.cu): decided here because it wants xs
+    // in column order (identity slot map); needs long rows in A, one GPU, no
+    // column blocks, and an even n (16-byte aligned panels of both xs buffers)
+    M->sweep_candidate = false;
+    if (M->use_sweep && M->use_sell && M->use_slots && M->sell_long == 2 && M->split_epi &&
+        M->nblk[0] <= 1 && M->nblk[1] <= 1 && (n & 1) == 0)
+      for (int64_t i = 0; i < m && !M->sweep_candidate; ++i)
+        M->sweep_candidate = row_ptr[i + 1] - row_ptr[i] > eqb::kTileNnz;
     build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);  // device work
     if (tplanner.joinable()) tplanner.join();  // planned during the transpose
     pt.mark(s, "plan A^T");
@@ -1423,10 +1564,12 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     const bool late_values = M->nblk[0] <= 1 && M->nblk[1] <= 1;
     if (!late_values) values_arrived();
     build_sell_layout(M, !late_values);
+    build_sweep_layout(M, !late_values);
     pt.mark(s, "sell");
     if (late_values) {
       values_arrived();
       build_sell_values(M);
+      build_sweep_values(M);
       pt.mark(s, "sell values");
     }
   } else {
@@ -1627,6 +1770,11 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     M->nnz = nnz;
     DeviceGuard dg(M->device);
     cudaStream_t s = M->stream;
+    // The sweep layout costs about as much to build as it saves in ~100
+    // iterations of c3: a one-shot call of fewer iterations keeps the long-slice kernel
+    if (pre && pre->total > 0 && !M->sweep_forced &&
+        pre->total / static_cast<uint64_t>(m + n) < 200)
+      M->use_sweep = false;
     if (pre && pre->total > 0) {  // overlaps the uploads and the transpose below
       M->signs.ensure((pre->total + 31) / 32 + 1);
       const size_t sb = eqb::sign_stream_scratch_bytes(pre->total);
@@ -1852,6 +2000,8 @@ int equil_build_flags(void) {
   return 0;
 #endif
 }
+
+int equil_sweep_active(const equil_matrix* A) { return A && A->sweep ? 1 : 0; }
 
 int equil_exchange_mode(const equil_matrix* A) {
   if (!A || A->world == 1 || A->p2p_state == 0) return 0;
@@ -2213,7 +2363,14 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               CK(cudaStreamWaitEvent(M->copy_stream, M->ev_fork, 0));
               eqb::SellArgs sl = sa;
               sl.nslices = M->n_sell_long;
-              CK(eqb::launch_sgd_sell_split(a, sl, true, M->sell_lvariant, M->copy_stream));
+              // A's long rows: the column sweep (all long slices are A's), ahead of
+              // the warp slices on the same stream -- its shared-memory stages leave
+              // the concurrent warp kernel too little L1 for xw's hot slots (c3:
+              // 1.09-1.17 concurrent vs 0.92 serial)
+              if (M->sweep)
+                CK(eqb::launch_sweep(a.xs_cur, a.carry[0], M->sweep_args, s));
+              else
+                CK(eqb::launch_sgd_sell_split(a, sl, true, M->sell_lvariant, M->copy_stream));
               sa.first = M->n_sell_long;
               CK(eqb::launch_sgd_sell_split(a, sa, false, M->sell_variant, s));
               CK(cudaEventRecord(M->ev_join, M->copy_stream));

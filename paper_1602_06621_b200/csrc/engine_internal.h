@@ -372,6 +372,7 @@ struct SellEnt {
   int32_t r0;      // first row in rowlist
 };
 struct Plan {
+  int64_t long_nnz = 0;  // entries of the rows longer than kTileNnz
   std::vector<eqb::Tile> lng, slices;
   std::vector<int32_t> rowlist;
   std::vector<SellEnt> sell;
@@ -540,6 +541,22 @@ struct equil_matrix {
   // split epilogue (EQUIL_SPLIT_EPI): row sums to rowacc, then one update pass
   bool split_epi = true;
   DevBuf<double> rowacc;
+  // column-synchronous sweep of A's long rows (sweep.cu, build_sweep_layout;
+  // EQUIL_SWEEP=0 keeps the warp-specialised long-slice kernel for them)
+  bool use_sweep = true;
+  bool sweep_forced = false;  // EQUIL_SWEEP=1: also for one-shot calls of few iterations
+  bool sweep = false;
+  bool sweep_values_pending = false;
+  int sweep_width = 0, sweep_stages = 2;  // width 0: sized from the rows (EQUIL_SWEEP_WIDTH)
+  bool sweep_candidate = false;  // decided before the slot maps: xs keeps column order
+  int64_t sweep_long_nnz = 0;
+  std::vector<int32_t> sweep_rows_host;  // A's rows longer than kTileNnz, longest first
+  eqb::SweepArgs sweep_args{};
+  DevBuf<unsigned char> sweep_blobs;
+  DevBuf<int64_t> sweep_off;
+  DevBuf<int32_t> sweep_crow, sweep_rstart;
+  DevBuf<uint16_t> sweep_perm, sweep_srun;
+  DevBuf<uint32_t> sweep_gbase, sweep_nepad;
   bool sell_passes = true;
   bool sell_values_pending = false;  // interleaved values not built yet (setup)  // EQUIL_SELL_PASSES=0: generic passes on the staged kernels
   bool sell_pass = false;

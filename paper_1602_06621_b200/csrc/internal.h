@@ -224,6 +224,31 @@ cudaError_t launch_sgd_update_rows(const SgdIterArgs& a, int64_t m_loc, int64_t 
 cudaError_t launch_sgd_sell_long(const SgdIterArgs& a, const SellArgs& sa, int variant,
                                  cudaStream_t s);
 
+// ---- column-synchronous sweep of A's long rows (sweep.cu) --------------------
+struct SweepArgs {
+  const unsigned char* blobs;  // per (cta, panel): header | perm | runs | cols | vals
+  const int64_t* blob_off;     // [nctas * npanels + 1] byte offsets (multiples of 16)
+  const int32_t* crow;         // [nctas * rmax] local row of A, -1: none
+  int nctas, rmax;             // persistent CTAs (one per SM), row slots per CTA (multiple of 128)
+  int npanels, width;          // panels of `width` columns (even)
+  int64_t ncols;               // length of the gathered vector
+  int stages;                  // shared-memory stages (panel + blob each)
+  unsigned blob_max;           // largest blob (bytes)
+};
+size_t sweep_smem_bytes(const SweepArgs& sw);
+// rowsum[row] = sum_k val * x[col] of every swept row, CSR order
+cudaError_t launch_sweep(const double* x, double* rowsum, const SweepArgs& sw, cudaStream_t s);
+cudaError_t launch_sweep_runs(const int64_t* rp, const int32_t* ci, const int32_t* crow, int ncta,
+                              int R, int P, int W, uint16_t* runl, int32_t* rstart,
+                              cudaStream_t s);
+cudaError_t launch_sweep_sort(const uint16_t* runl, int ncta, int R, int P, uint16_t* perm,
+                              uint16_t* srun, uint32_t* gbase, uint32_t* nepad, cudaStream_t s);
+cudaError_t launch_sweep_fill(const int64_t* rp, const int32_t* ci, const double* va,
+                              const int32_t* crow, int ncta, int R, int P, int W,
+                              const uint16_t* perm, const uint16_t* srun, const uint32_t* gbase,
+                              const uint32_t* nepad, const int32_t* rstart, const int64_t* blob_off,
+                              unsigned char* blobs, bool do_struct, bool do_vals, cudaStream_t s);
+
 enum PassMode : int {
   kPassPlain = 0,    // y = acc
   kPassLsqrU = 1,    // out = s_i*acc - alpha*u_i   (s = d or 1)
@@ -312,7 +337,7 @@ cudaError_t launch_sgd_init(double* xs, double* xw, double* u, double* ub,
 // (G + 1 device values): map_pad[padded position of row i] = its slot, rows
 // of each rank ordered by decreasing floor(log2(length)), stable
 cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* bounds, int G,
-                            int64_t maxcnt, int32_t* map_pad, cudaStream_t s);
+                            int64_t maxcnt, int32_t* map_pad, cudaStream_t s, bool flat = false);
 // column-block boundaries of every row (block b = columns [b*width, (b+1)*width))
 cudaError_t launch_block_bounds(const DevCsr& M, int nb, int64_t width, int32_t* bnd,
                                 cudaStream_t s);

@@ -834,14 +834,16 @@ namespace {
 // key of row i of rank g: g * 128 + (len == 0 ? 64 : clz(len)) -> longest rows first
 __global__ void slot_keys_kernel(const int64_t* __restrict__ rp, int64_t rows,
                                  const int64_t* __restrict__ bounds, int G,
-                                 uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
+                                 uint32_t* __restrict__ key, int32_t* __restrict__ idx, int flat) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= rows) return;
   int g = 0;
   while (g + 1 < G && bounds[g + 1] <= i) ++g;
   const int64_t len = rp[i + 1] - rp[i];
+  // flat: every row of a rank gets the same key, so the (stable) sort keeps
+  // the row order and the slot map is the identity
   key[i] = static_cast<uint32_t>(g) * 128u +
-           (len <= 0 ? 64u : static_cast<uint32_t>(__clzll(static_cast<long long>(len))));
+           (flat || len <= 0 ? 64u : static_cast<uint32_t>(__clzll(static_cast<long long>(len))));
   idx[i] = static_cast<int32_t>(i);
 }
 // sorted position s holds row perm[s]: map[pad(perm[s])] = g * maxcnt + (s - bounds[g])
@@ -859,7 +861,7 @@ __global__ void slot_map_kernel(const int32_t* __restrict__ perm, int64_t rows,
 }  // namespace
 
 cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* bounds, int G,
-                            int64_t maxcnt, int32_t* map_pad, cudaStream_t s) {
+                            int64_t maxcnt, int32_t* map_pad, cudaStream_t s, bool flat) {
   if (rows == 0) return cudaSuccess;
   uint32_t *k0 = nullptr, *k1 = nullptr;
   int32_t *i0 = nullptr, *i1 = nullptr;
@@ -874,7 +876,7 @@ cudaError_t launch_slot_map(const int64_t* rp, int64_t rows, const int64_t* boun
     e = cudaMallocAsync(&i0, rows * 4, s); if (e) break;
     e = cudaMallocAsync(&i1, rows * 4, s); if (e) break;
     const unsigned grid = static_cast<unsigned>((rows + 255) / 256);
-    slot_keys_kernel<<<grid, 256, 0, s>>>(rp, rows, bounds, G, k0, i0);
+    slot_keys_kernel<<<grid, 256, 0, s>>>(rp, rows, bounds, G, k0, i0, flat ? 1 : 0);
     count_launch(s);
     e = cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, i1, rows, 0, bits, s);
     if (e) break;
