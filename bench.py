@@ -471,6 +471,7 @@ def run_ours(args):
 
     if rank == 0:
         exchange = eq.exchange_mode(M)
+        sweep = eq.sweep_active(M)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -486,11 +487,17 @@ def run_ours(args):
             "achieved_GBps": B * value / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sell_warp_kernel + sell_long_kernel + "
-                                   "sgd_update_rows_kernel: one iteration = A and A^T passes "
-                                   "over interleaved row slices (warp slices and "
-                                   "warp-specialised long-row CTAs, concurrent), then the u/v "
-                                   "update of every row",
+                         "kernel": ("sweep_kernel + sell_warp_kernel + sgd_update_rows_kernel: "
+                                    "one iteration = A's rows of > 512 entries on the column "
+                                    "sweep (xs in shared-memory panels), every other row of A "
+                                    "and A^T on interleaved warp slices, then the u/v update "
+                                    "of every row") if sweep else
+                                   ("sell_warp_kernel + sell_long_kernel + "
+                                    "sgd_update_rows_kernel: one iteration = A and A^T passes "
+                                    "over interleaved row slices (warp slices and "
+                                    "warp-specialised long-row CTAs, concurrent), then the u/v "
+                                    "update of every row"),
+                         "long_rows": "column sweep" if sweep else "long-slice kernel",
                          "bytes_per_launch": per_gpu_bytes, "launch_ms": kern_s * 1e3,
                          "peak_source": peak_src},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
