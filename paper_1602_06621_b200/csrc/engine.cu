@@ -662,10 +662,54 @@ void build_sweep_values(equil_matrix* M) {
   M->sweep_values_pending = false;
 }
 
-void build_sweep_layout(equil_matrix* M, bool with_values) {
+// First half (plan_sweep_layout): deal the rows, pick the panel width, enqueue the
+// run / sort kernels and the copy of the blob sizes to the host, and record an
+// event -- no host wait, so the interleaved layout can be enqueued behind it.
+// Second half (build_sweep_layout): wait for that event only, lay the blobs out
+// and fill them.
+namespace {
+struct SweepPlan {
+  bool ok = false;
+  int G = 0, R = 0, NG = 0, W = 0, P = 0;
+  size_t ncp = 0;
+  int64_t hdr = 0;
+};
+
+void sweep_enqueue_runs(equil_matrix* M, SweepPlan& sp) {
+  cudaStream_t s = M->stream;
+  sp.P = static_cast<int>((M->n + sp.W - 1) / sp.W);
+  sp.ncp = static_cast<size_t>(sp.G) * sp.P;
+  DevBuf<int32_t> rowlen;
+  rowlen.alloc_on(static_cast<size_t>(sp.G) * sp.R, s);
+  M->sweep_rstart.alloc_async(sp.ncp * sp.R, s);
+  M->sweep_perm.alloc_async(sp.ncp * sp.R, s);
+  M->sweep_srun.alloc_async(sp.ncp * sp.R, s);
+  M->sweep_gbase.alloc_async(sp.ncp * sp.NG, s);
+  M->sweep_nepad.alloc_async(sp.ncp, s);
+  CK(eqb::launch_sweep_runs(M->A.row_ptr, M->A.col, M->sweep_crow.p, sp.G, sp.R, sp.P, sp.W,
+                            M->sweep_rstart.p, rowlen.p, s));
+  CK(eqb::launch_sweep_sort(M->sweep_rstart.p, rowlen.p, sp.G, sp.R, sp.P, M->sweep_perm.p,
+                            M->sweep_srun.p, M->sweep_gbase.p, M->sweep_nepad.p, s));
+  if (M->sweep_ne_cap < sp.ncp) {
+    if (M->sweep_ne_host) cudaFreeHost(M->sweep_ne_host);
+    M->sweep_ne_host = nullptr;
+    void* q = nullptr;
+    CK(cudaHostAlloc(&q, sp.ncp * 4, cudaHostAllocDefault));
+    M->sweep_ne_host = static_cast<uint32_t*>(q);
+    M->sweep_ne_cap = sp.ncp;
+  }
+  CK(cudaMemcpyAsync(M->sweep_ne_host, M->sweep_nepad.p, sp.ncp * 4, cudaMemcpyDeviceToHost, s));
+  if (!M->ev_sweep) CK(cudaEventCreateWithFlags(&M->ev_sweep, cudaEventDisableTiming));
+  CK(cudaEventRecord(M->ev_sweep, s));
+}
+}  // namespace
+
+void plan_sweep_layout(equil_matrix* M) {
   M->sweep = false;
   M->sweep_values_pending = false;
-  if (!M->sweep_candidate || !M->sell || M->sell_nb != 1 || M->sell_long != 2 || !M->split_epi)
+  M->sweep_plan_ok = false;
+  if (!M->sweep_candidate || !M->use_sell || !M->slots || M->sell_long != 2 || !M->split_epi ||
+      M->nblk[0] > 1 || M->nblk[1] > 1)
     return;
   const equil_matrix::SellHost& H = M->sell_host;
   const std::vector<int32_t>& rows = M->sweep_rows_host;
@@ -673,11 +717,13 @@ void build_sweep_layout(equil_matrix* M, bool with_values) {
   cudaStream_t s = M->stream;
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, M->device));
-  const int G = static_cast<int>(std::min<size_t>(nsm, rows.size()));
-  const int per = static_cast<int>((rows.size() + G - 1) / G);
-  const int R = (per + 127) / 128 * 128;
-  if (R > 896) return;  // 32 producer + R consumer threads per CTA
-  const int NG = R / 32;
+  SweepPlan sp;
+  sp.G = static_cast<int>(std::min<size_t>(nsm, rows.size()));
+  const int per = static_cast<int>((rows.size() + sp.G - 1) / sp.G);
+  sp.R = (per + 127) / 128 * 128;
+  if (sp.R > 896) return;  // 32 producer + R consumer threads per CTA
+  sp.NG = sp.R / 32;
+  const int G = sp.G, R = sp.R;
   std::vector<int32_t> crow(static_cast<size_t>(G) * R, -1);
   for (size_t i = 0; i < rows.size(); ++i) {
     const size_t round = i / G, pos = i % G;
@@ -686,64 +732,74 @@ void build_sweep_layout(equil_matrix* M, bool with_values) {
   }
   M->sweep_crow.alloc_async(crow.size(), s);
   h2d(M, M->sweep_crow.p, crow.data(), crow.size() * 4);
+  if (!M->pull_uploads) CK(cudaStreamSynchronize(s));  // crow is a local (pageable) vector
   // Panel width: two stages of (panel + the CTA's largest blob) must fit in
   // shared memory.  A CTA's blob holds about W / n of its entries at 10 bytes
   // each plus padding; start from that estimate and narrow if the layout
   // disagrees (EQUIL_SWEEP_WIDTH fixes the first try).
-  const int64_t hdr = 16 + 4 * NG + 4 * R;
-  int W = M->sweep_width;
-  if (W <= 0) {
+  sp.hdr = 16 + 4 * sp.NG + 4 * R;
+  sp.W = M->sweep_width;
+  if (sp.W <= 0) {
     const double ent_per_col = static_cast<double>(M->sweep_long_nnz) / G / static_cast<double>(M->n);
-    const double budget = 227.0 * 1024 / 2 - hdr - 4.0 * R - 4096;
-    W = static_cast<int>(budget / (8.0 + 15.0 * ent_per_col));
-    W = std::max(128, std::min(W, 16384) / 512 * 512);
+    const double budget = 227.0 * 1024 / 2 - sp.hdr - 4.0 * R - 4096;
+    sp.W = static_cast<int>(budget / (8.0 + 15.0 * ent_per_col));
+    sp.W = std::max(128, std::min(sp.W, 16384) / 512 * 512);
   }
+  sweep_enqueue_runs(M, sp);
+  sp.ok = true;
+  M->sweep_plan_ok = true;
+  M->sweep_plan_G = sp.G;
+  M->sweep_plan_R = sp.R;
+  M->sweep_plan_W = sp.W;
+}
+
+void build_sweep_layout(equil_matrix* M, bool with_values) {
+  if (!M->sweep_plan_ok) return;
+  M->sweep_plan_ok = false;
+  if (!M->sell || M->sell_nb != 1) return;
+  cudaStream_t s = M->stream;
+  SweepPlan sp;
+  sp.G = M->sweep_plan_G;
+  sp.R = M->sweep_plan_R;
+  sp.W = M->sweep_plan_W;
+  sp.NG = sp.R / 32;
+  sp.hdr = 16 + 4 * sp.NG + 4 * sp.R;
+  sp.P = static_cast<int>((M->n + sp.W - 1) / sp.W);
+  sp.ncp = static_cast<size_t>(sp.G) * sp.P;
+  const int G = sp.G, R = sp.R;
   eqb::SweepArgs sw{};
   std::vector<int64_t> off;
-  size_t ncp = 0;
-  int P = 0;
   for (int attempt = 0;; ++attempt) {
     if (attempt == 6) return;  // the rows do not fit this scheme
-    P = static_cast<int>((M->n + W - 1) / W);
-    ncp = static_cast<size_t>(G) * P;
-    DevBuf<uint16_t> runl;
-    runl.alloc_on(ncp * R, s);
-    M->sweep_rstart.alloc_async(ncp * R, s);
-    M->sweep_perm.alloc_async(ncp * R, s);
-    M->sweep_srun.alloc_async(ncp * R, s);
-    M->sweep_gbase.alloc_async(ncp * NG, s);
-    M->sweep_nepad.alloc_async(ncp, s);
-    CK(eqb::launch_sweep_runs(M->A.row_ptr, M->A.col, M->sweep_crow.p, G, R, P, W, runl.p,
-                              M->sweep_rstart.p, s));
-    CK(eqb::launch_sweep_sort(runl.p, G, R, P, M->sweep_perm.p, M->sweep_srun.p, M->sweep_gbase.p,
-                              M->sweep_nepad.p, s));
-    std::vector<uint32_t> ne(ncp);
-    CK(cudaMemcpyAsync(ne.data(), M->sweep_nepad.p, ncp * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    off.assign(ncp + 1, 0);
+    CK(cudaEventSynchronize(M->ev_sweep));  // the blob sizes are on the host
+    const uint32_t* ne = M->sweep_ne_host;
+    off.assign(sp.ncp + 1, 0);
     int64_t bmax = 0;
-    for (size_t q = 0; q < ncp; ++q) {
-      const int64_t b = hdr + 10 * static_cast<int64_t>(ne[q]);
+    for (size_t q = 0; q < sp.ncp; ++q) {
+      const int64_t b = sp.hdr + 10 * static_cast<int64_t>(ne[q]);
       off[q + 1] = off[q] + b;
       bmax = std::max(bmax, b);
     }
     sw = eqb::SweepArgs{};
     sw.nctas = G;
     sw.rmax = R;
-    sw.npanels = P;
-    sw.width = W;
+    sw.npanels = sp.P;
+    sw.width = sp.W;
     sw.ncols = M->n;
     sw.blob_max = static_cast<unsigned>(bmax);
     sw.stages = M->sweep_stages;
     while (sw.stages > 2 && eqb::sweep_smem_bytes(sw) > 227 * 1024) --sw.stages;
     if (eqb::sweep_smem_bytes(sw) <= 227 * 1024) break;
     // narrower panels, smaller blobs: scale by what the largest blob may take
-    const double room = 227.0 * 1024 / 2 - 4.0 * R - 4.0 * P - 256 - 8.0 * W;
+    const double room = 227.0 * 1024 / 2 - 4.0 * R - 4.0 * sp.P - 256 - 8.0 * sp.W;
     const double f = room > 4096 ? room / static_cast<double>(bmax) : 0.25;
-    const int Wn = static_cast<int>(W * std::min(0.8, 0.9 * f)) / 64 * 64;
+    const int Wn = static_cast<int>(sp.W * std::min(0.8, 0.9 * f)) / 64 * 64;
     if (Wn < 128) return;
-    W = Wn;
+    sp.W = Wn;
+    sweep_enqueue_runs(M, sp);
   }
+  const int P = sp.P, W = sp.W;
+  const size_t ncp = sp.ncp;
   M->sweep_off.alloc_async(off.size(), s);
   h2d(M, M->sweep_off.p, off.data(), off.size() * 8);
   M->sweep_blobs.alloc_async(static_cast<size_t>(off[ncp]), s);
@@ -752,8 +808,7 @@ void build_sweep_layout(equil_matrix* M, bool with_values) {
                             M->sweep_perm.p, M->sweep_srun.p, M->sweep_gbase.p, M->sweep_nepad.p,
                             M->sweep_rstart.p, M->sweep_off.p, M->sweep_blobs.p, true, with_values,
                             s));
-  // h2d may have staged the host vectors in the pull arena; they are copied by now
-  CK(cudaStreamSynchronize(s));
+  if (!M->pull_uploads) CK(cudaStreamSynchronize(s));  // off is a local (pageable) vector
   sw.blobs = M->sweep_blobs.p;
   sw.blob_off = M->sweep_off.p;
   sw.crow = M->sweep_crow.p;
@@ -1563,6 +1618,7 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     // values are needed from here on only by the blocked layouts
     const bool late_values = M->nblk[0] <= 1 && M->nblk[1] <= 1;
     if (!late_values) values_arrived();
+    plan_sweep_layout(M);  // (its kernels run ahead of the interleaved layout's)
     build_sell_layout(M, !late_values);
     build_sweep_layout(M, !late_values);
     pt.mark(s, "sell");
@@ -1770,10 +1826,10 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     M->nnz = nnz;
     DeviceGuard dg(M->device);
     cudaStream_t s = M->stream;
-    // The sweep layout costs about as much to build as it saves in ~100
-    // iterations of c3: a one-shot call of fewer iterations keeps the long-slice kernel
+    // The sweep layout adds ~4 ms to a pipelined c3 setup and saves ~0.09 ms per
+    // iteration: a one-shot call of few iterations keeps the long-slice kernel
     if (pre && pre->total > 0 && !M->sweep_forced &&
-        pre->total / static_cast<uint64_t>(m + n) < 200)
+        pre->total / static_cast<uint64_t>(m + n) < 64)
       M->use_sweep = false;
     if (pre && pre->total > 0) {  // overlaps the uploads and the transpose below
       M->signs.ensure((pre->total + 31) / 32 + 1);

@@ -239,10 +239,11 @@ size_t sweep_smem_bytes(const SweepArgs& sw);
 // rowsum[row] = sum_k val * x[col] of every swept row, CSR order
 cudaError_t launch_sweep(const double* x, double* rowsum, const SweepArgs& sw, cudaStream_t s);
 cudaError_t launch_sweep_runs(const int64_t* rp, const int32_t* ci, const int32_t* crow, int ncta,
-                              int R, int P, int W, uint16_t* runl, int32_t* rstart,
+                              int R, int P, int W, int32_t* rstart, int32_t* rowlen,
                               cudaStream_t s);
-cudaError_t launch_sweep_sort(const uint16_t* runl, int ncta, int R, int P, uint16_t* perm,
-                              uint16_t* srun, uint32_t* gbase, uint32_t* nepad, cudaStream_t s);
+cudaError_t launch_sweep_sort(const int32_t* rstart, const int32_t* rowlen, int ncta, int R, int P,
+                              uint16_t* perm, uint16_t* srun, uint32_t* gbase, uint32_t* nepad,
+                              cudaStream_t s);
 cudaError_t launch_sweep_fill(const int64_t* rp, const int32_t* ci, const double* va,
                               const int32_t* crow, int ncta, int R, int P, int W,
                               const uint16_t* perm, const uint16_t* srun, const uint32_t* gbase,

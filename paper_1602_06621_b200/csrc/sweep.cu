@@ -184,38 +184,38 @@ sweep_kernel(const double* __restrict__ x, double* __restrict__ rowsum, const Sw
 }
 
 // ---- layout construction ------------------------------------------------------
-// per (cta, local row): run length and first entry (relative to the row start)
-// of the row in every panel.  Columns ascend within a row.
+// per (cta, panel, local row): the first entry of the row with column >= p W,
+// relative to the row start (columns ascend within a row); the run of the row
+// in panel p is the difference to panel p + 1 (the row length after the last)
 __global__ void sweep_runs_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                   const int32_t* __restrict__ crow, int ncta, int R, int P, int W,
-                                  uint16_t* __restrict__ runl, int32_t* __restrict__ rstart) {
-  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (q >= static_cast<int64_t>(ncta) * R) return;
-  const int c = static_cast<int>(q / R), lr = static_cast<int>(q % R);
-  const int32_t row = crow[q];
-  const int64_t k0 = row >= 0 ? rp[row] : 0, k1 = row >= 0 ? rp[row + 1] : 0;
-  int64_t pos = k0;
-  for (int p = 0; p < P; ++p) {
-    int64_t nxt = k1;
-    if (p + 1 < P) {  // first entry with column >= (p + 1) W
-      const int64_t key = static_cast<int64_t>(p + 1) * W;
-      int64_t lo = pos, hi = k1;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (ci[mid] < key) lo = mid + 1; else hi = mid;
-      }
-      nxt = lo;
-    }
-    const int64_t o = (static_cast<int64_t>(c) * P + p) * R + lr;
-    runl[o] = static_cast<uint16_t>(nxt - pos);
-    rstart[o] = static_cast<int32_t>(pos - k0);
-    pos = nxt;
+                                  int32_t* __restrict__ rstart, int32_t* __restrict__ rowlen) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<int64_t>(ncta) * P * R) return;
+  const int lr = static_cast<int>(idx % R);
+  const int64_t cp = idx / R;
+  const int p = static_cast<int>(cp % P), c = static_cast<int>(cp / P);
+  const int32_t row = crow[static_cast<int64_t>(c) * R + lr];
+  if (row < 0) {
+    rstart[idx] = 0;
+    if (p == 0) rowlen[static_cast<int64_t>(c) * R + lr] = 0;
+    return;
   }
+  const int64_t k0 = rp[row], k1 = rp[row + 1];
+  const int64_t key = static_cast<int64_t>(p) * W;
+  int64_t lo = k0, hi = k1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ci[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  rstart[idx] = static_cast<int32_t>(lo - k0);
+  if (p == 0) rowlen[static_cast<int64_t>(c) * R + lr] = static_cast<int32_t>(k1 - k0);
 }
 
 // one CTA per (cta, panel): rows by decreasing run length (stable), the group
 // bases and the padded entry count
-__global__ void sweep_sort_kernel(const uint16_t* __restrict__ runl, int R,
+__global__ void sweep_sort_kernel(const int32_t* __restrict__ rstart,
+                                  const int32_t* __restrict__ rowlen, int R, int P,
                                   uint16_t* __restrict__ perm, uint16_t* __restrict__ srun,
                                   uint32_t* __restrict__ gbase, uint32_t* __restrict__ nepad) {
   extern __shared__ uint16_t sh[];  // runs[R], sorted[R]
@@ -223,7 +223,9 @@ __global__ void sweep_sort_kernel(const uint16_t* __restrict__ runl, int R,
   uint16_t* sorted = sh + R;
   const int64_t cp = blockIdx.x;
   const int t = threadIdx.x;
-  const int r = runl[cp * R + t];
+  const int p = static_cast<int>(cp % P);
+  const int r = (p + 1 < P ? rstart[(cp + 1) * R + t] : rowlen[(cp / P) * R + t]) -
+                rstart[cp * R + t];
   runs[t] = static_cast<uint16_t>(r);
   __syncthreads();
   int rank = 0;
@@ -322,21 +324,23 @@ cudaError_t launch_sweep(const double* x, double* rowsum, const SweepArgs& sw, c
 }
 
 cudaError_t launch_sweep_runs(const int64_t* rp, const int32_t* ci, const int32_t* crow, int ncta,
-                              int R, int P, int W, uint16_t* runl, int32_t* rstart,
+                              int R, int P, int W, int32_t* rstart, int32_t* rowlen,
                               cudaStream_t s) {
-  const int64_t n = static_cast<int64_t>(ncta) * R;
+  const int64_t n = static_cast<int64_t>(ncta) * R * P;
   if (n == 0) return cudaSuccess;
-  sweep_runs_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(rp, ci, crow, ncta, R, P,
-                                                                          W, runl, rstart);
+  sweep_runs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(rp, ci, crow, ncta, R, P,
+                                                                          W, rstart, rowlen);
   count_launch(s);
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep_sort(const uint16_t* runl, int ncta, int R, int P, uint16_t* perm,
-                              uint16_t* srun, uint32_t* gbase, uint32_t* nepad, cudaStream_t s) {
+cudaError_t launch_sweep_sort(const int32_t* rstart, const int32_t* rowlen, int ncta, int R, int P,
+                              uint16_t* perm, uint16_t* srun, uint32_t* gbase, uint32_t* nepad,
+                              cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(ncta) * P;
   if (n == 0) return cudaSuccess;
-  sweep_sort_kernel<<<static_cast<unsigned>(n), R, 4 * R, s>>>(runl, R, perm, srun, gbase, nepad);
+  sweep_sort_kernel<<<static_cast<unsigned>(n), R, 4 * R, s>>>(rstart, rowlen, R, P, perm, srun,
+                                                              gbase, nepad);
   count_launch(s);
   return cudaGetLastError();
 }
