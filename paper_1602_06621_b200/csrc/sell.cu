@@ -721,21 +721,10 @@ cudaError_t launch_sgd_sell_split(const SgdIterArgs& a, const SellArgs& sa, bool
       default: launch_long<SgdSplitOp, 4, 15, true, 1>(op, sa, s); break;
     }
   } else {
-    switch (variant) {  // EQUIL_SELL_VARIANT
+    switch (variant) {  // EQUIL_SELL_VARIANT: <batch, pipelined, CTAs per SM> (DESIGN §3 has the sweep)
       case 1: launch_warp<SgdSplitOp, 8, true, 8>(op, sa, s); break;
-      case 2: launch_warp<SgdSplitOp, 8, true, 10>(op, sa, s); break;
-      case 3: launch_warp<SgdSplitOp, 4, true, 12>(op, sa, s); break;
-      case 4: launch_warp<SgdSplitOp, 16, false, 8>(op, sa, s); break;
-      case 5: launch_warp<SgdSplitOp, 8, false, 10>(op, sa, s); break;
-      case 6: launch_warp<SgdSplitOp, 8, true, 7>(op, sa, s); break;
-      case 7: launch_warp<SgdSplitOp, 4, true, 8>(op, sa, s); break;
-      case 8: launch_warp<SgdSplitOp, 4, true, 10>(op, sa, s); break;
-      case 9: launch_warp<SgdSplitOp, 8, false, 8>(op, sa, s); break;
-      case 10: launch_warp<SgdSplitOp, 4, true, 14>(op, sa, s); break;
-      case 11: launch_warp<SgdSplitOp, 4, true, 11>(op, sa, s); break;
-      case 12: launch_warp<SgdSplitOp, 8, true, 9>(op, sa, s); break;
-      case 13: launch_warp<SgdSplitOp, 4, false, 12>(op, sa, s); break;
-      case 14: launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s); break;
+      case 2: launch_warp<SgdSplitOp, 4, true, 10>(op, sa, s); break;
+      case 3: launch_warp<SgdSplitOp, 8, true, 6>(op, sa, s); break;
       // quad layout (256-bit value loads): 56 registers, 9 CTAs per SM (c3:
       // 0.997-1.010 vs 1.067-1.083 ms at <8, true, 6>)
       default: launch_warp<SgdSplitOp, 8, true, 9>(op, sa, s); break;

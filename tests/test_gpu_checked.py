@@ -29,7 +29,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     ("c3s", {}),
     ("c3s", {"EQUIL_BLOCK_MB": "0.1"}),         # column-block rounds and their carries
     ("c3s", {"EQUIL_SPLIT_EPI": "0"}),         # fused epilogue in the traversals
-    ("c3s", {"EQUIL_SELL_LVARIANT": "3"}),     # another ring shape (batch 2, 15 stagers)
+    ("c3s", {"EQUIL_SWEEP": "0"}),             # long rows on the long-slice kernel's ring
+    ("c3s", {"EQUIL_SWEEP": "0", "EQUIL_SELL_LVARIANT": "3"}),  # another ring shape (batch 2, 15 stagers)
+    ("c3s", {"EQUIL_SWEEP_WIDTH": "700", "EQUIL_SWEEP_STAGES": "3"}),  # narrow sweep panels
 ])
 def test_checked_build_clean(case, env):
     if not os.path.exists(B.CHECKED_LIB):

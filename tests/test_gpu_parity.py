@@ -298,6 +298,7 @@ def test_long_slice_variants_bit_exact(C, golden, monkeypatch, case, lvariant):
     bit -- golden cases and c3's generator at 2% scale (rows of up to 10^4
     entries), so the ring protocol does not depend on its shape."""
     monkeypatch.setenv("EQUIL_SELL_LVARIANT", lvariant)
+    monkeypatch.setenv("EQUIL_SWEEP", "0")  # the SGD's long rows on the long-slice kernel
     if case == "c3":
         from paper_1602_06621_b200 import configs
         inst = configs.config(3, scale=0.02)
@@ -790,11 +791,14 @@ TRAVERSALS = [
     {"EQUIL_SELL_LONG": "0"},                              # long rows on the staged CTAs
     {"EQUIL_SELL": "0"},                                   # staged traversal throughout
     {"EQUIL_SELL_PASSES": "0"},                            # generic passes staged
-    {"EQUIL_SELL_VARIANT": "1", "EQUIL_SELL_LVARIANT": "3"},
-    {"EQUIL_SELL_VARIANT": "3", "EQUIL_SELL_LVARIANT": "4"},
+    {"EQUIL_SWEEP": "0"},                                  # long rows on the long-slice kernel
+    {"EQUIL_SWEEP": "0", "EQUIL_SELL_VARIANT": "1", "EQUIL_SELL_LVARIANT": "3"},
+    {"EQUIL_SWEEP": "0", "EQUIL_SELL_VARIANT": "2", "EQUIL_SELL_LVARIANT": "2"},
+    {"EQUIL_SWEEP_WIDTH": "300", "EQUIL_SWEEP_STAGES": "3"},  # narrow sweep panels
     {"EQUIL_SELL_ORDER": "1"},                             # warp slices in window order
     {"EQUIL_SELL_QUAD": "0"},                              # every slice 1-wide (no 128/256-bit loads)
-    {"EQUIL_SELL_VARIANT": "14"},                          # warp slices at 6 CTAs/SM (80 registers)
+    {"EQUIL_SELL_QUAD": "0", "EQUIL_SWEEP": "0"},
+    {"EQUIL_SELL_VARIANT": "3"},                           # warp slices at 6 CTAs/SM (80 registers)
     {"EQUIL_SPLIT_EPI": "0"},                              # SGD update fused into the traversals
     {"EQUIL_BLOCK_MB": "0.004"},                           # 500-coordinate column blocks
     {"EQUIL_BLOCK_MB": "0.004", "EQUIL_SELL_BLOCKED": "1"},  # same on interleaved slices
