@@ -652,6 +652,16 @@ void build_sell_layout(equil_matrix* M, bool with_values) {
 // number of entries), cut each row into its runs per panel, sort every (CTA,
 // panel)'s rows by run length and lay the blobs out.  The values follow in
 // build_sweep_values once they are on the device.
+// the layout construction's per-(CTA, panel, row) tables, once the blobs are complete
+void release_sweep_scratch(equil_matrix* M) {
+  cudaStream_t s = M->stream;
+  M->sweep_rstart.release_on(s);
+  M->sweep_perm.release_on(s);
+  M->sweep_srun.release_on(s);
+  M->sweep_gbase.release_on(s);
+  M->sweep_nepad.release_on(s);
+}
+
 void build_sweep_values(equil_matrix* M) {
   if (!M->sweep || !M->sweep_values_pending) return;
   const eqb::SweepArgs& sw = M->sweep_args;
@@ -660,6 +670,7 @@ void build_sweep_values(equil_matrix* M) {
                             M->sweep_gbase.p, M->sweep_nepad.p, M->sweep_rstart.p, M->sweep_off.p,
                             M->sweep_blobs.p, false, true, M->stream));
   M->sweep_values_pending = false;
+  release_sweep_scratch(M);
 }
 
 // First half (plan_sweep_layout): deal the rows, pick the panel width, enqueue the
@@ -815,6 +826,7 @@ void build_sweep_layout(equil_matrix* M, bool with_values) {
   M->sweep_args = sw;
   M->sweep = true;
   M->sweep_values_pending = !with_values;
+  if (with_values) release_sweep_scratch(M);
   if (getenv("EQUIL_VERBOSE"))
     fprintf(stderr, "[equil] sweep: %d CTAs x %d rows, %d panels of %d, %d stages, blobs %.1f MB (max %u B)\n",
             G, R, P, W, sw.stages, off[ncp] / 1048576.0, sw.blob_max);

@@ -265,6 +265,17 @@ struct DevBuf {
     dev = d;
     n = count;
   }
+  // free in the order of stream s (every use of the buffer was on s): no device sync
+  void release_on(cudaStream_t s) {
+    if (p && !own && dev >= 0) {
+      cudaFreeAsync(p, s);
+      p = nullptr;
+      n = 0;
+      dev = -1;
+      return;
+    }
+    release();
+  }
   void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'ed array
     release();
     p = q;
