@@ -2440,7 +2440,10 @@ void sgd_row_col(equil_matrix* M, const equil_params* p, const equil_diag_cfg* d
               else
                 CK(eqb::launch_sgd_sell_split(a, sl, true, M->sell_lvariant, M->copy_stream));
               sa.first = M->n_sell_long;
-              CK(eqb::launch_sgd_sell_split(a, sa, false, M->sell_variant, s));
+              // alone on the SMs (after the sweep) the warp slices do slightly better
+              // with batches of 4 at 10 CTAs per SM (c3: 0.867-0.881 vs 0.880-0.887)
+              CK(eqb::launch_sgd_sell_split(
+                  a, sa, false, M->sweep && M->sell_variant == 0 ? 2 : M->sell_variant, s));
               CK(cudaEventRecord(M->ev_join, M->copy_stream));
               CK(cudaStreamWaitEvent(s, M->ev_join, 0));
               CK(eqb::launch_sgd_update_rows(a, M->m_loc(), M->n_loc(), s));
