@@ -1615,8 +1615,14 @@ void finish_sparse(equil_matrix* M, DevBuf<int64_t>& rp, DevBuf<int32_t>& ci,
     M->sweep_candidate = false;
     if (M->use_sweep && M->use_sell && M->use_slots && M->sell_long == 2 && M->split_epi &&
         M->nblk[0] <= 1 && M->nblk[1] <= 1 && (n & 1) == 0)
+    {
       for (int64_t i = 0; i < m && !M->sweep_candidate; ++i)
         M->sweep_candidate = row_ptr[i + 1] - row_ptr[i] > eqb::kTileNnz;
+      // long rows in A^T need the long-slice kernel, and then the sweep stands down
+      // (plan_sweep_layout): keep the hot-first layout of xs for such matrices
+      for (int64_t j = 0; j < n && M->sweep_candidate; ++j)
+        if (rpT[j + 1] - rpT[j] > eqb::kTileNnz) M->sweep_candidate = false;
+    }
     build_slot_layout(M, M->A.row_ptr, M->AT.row_ptr);  // device work
     if (tplanner.joinable()) tplanner.join();  // planned during the transpose
     pt.mark(s, "plan A^T");
