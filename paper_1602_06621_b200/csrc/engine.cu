@@ -701,14 +701,23 @@ void sweep_enqueue_runs(equil_matrix* M, SweepPlan& sp) {
                             M->sweep_rstart.p, rowlen.p, s));
   CK(eqb::launch_sweep_sort(M->sweep_rstart.p, rowlen.p, sp.G, sp.R, sp.P, M->sweep_perm.p,
                             M->sweep_srun.p, M->sweep_gbase.p, M->sweep_nepad.p, s));
-  if (M->sweep_ne_cap < sp.ncp) {
-    if (M->sweep_ne_host) cudaFreeHost(M->sweep_ne_host);
-    M->sweep_ne_host = nullptr;
+  // pinned landing buffer for the sizes: cached per host thread (pinning and
+  // unpinning memory per handle cost tens of ms now and then, and cudaFreeHost
+  // synchronises the device); build_sweep_layout reads it on the same thread
+  struct PinnedScratch {
+    uint32_t* p = nullptr;
+    size_t cap = 0;
+  };
+  static thread_local PinnedScratch ps;
+  if (ps.cap < sp.ncp) {
+    if (ps.p) cudaFreeHost(ps.p);
+    ps = PinnedScratch{};
     void* q = nullptr;
-    CK(cudaHostAlloc(&q, sp.ncp * 4, cudaHostAllocDefault));
-    M->sweep_ne_host = static_cast<uint32_t*>(q);
-    M->sweep_ne_cap = sp.ncp;
+    CK(cudaHostAlloc(&q, sp.ncp * 4 * 2, cudaHostAllocDefault));
+    ps.p = static_cast<uint32_t*>(q);
+    ps.cap = sp.ncp * 2;
   }
+  M->sweep_ne_host = ps.p;
   CK(cudaMemcpyAsync(M->sweep_ne_host, M->sweep_nepad.p, sp.ncp * 4, cudaMemcpyDeviceToHost, s));
   if (!M->ev_sweep) CK(cudaEventCreateWithFlags(&M->ev_sweep, cudaEventDisableTiming));
   CK(cudaEventRecord(M->ev_sweep, s));

@@ -564,8 +564,7 @@ struct equil_matrix {
   std::vector<int32_t> sweep_rows_host;  // A's rows longer than kTileNnz, longest first
   bool sweep_plan_ok = false;  // plan_sweep_layout enqueued; build_sweep_layout finishes it
   int sweep_plan_G = 0, sweep_plan_R = 0, sweep_plan_W = 0;
-  uint32_t* sweep_ne_host = nullptr;  // pinned: per-(CTA, panel) padded entry counts
-  size_t sweep_ne_cap = 0;
+  uint32_t* sweep_ne_host = nullptr;  // pinned (thread-cached): per-(CTA, panel) padded entry counts
   cudaEvent_t ev_sweep = nullptr;
   eqb::SweepArgs sweep_args{};
   DevBuf<unsigned char> sweep_blobs;
@@ -652,7 +651,6 @@ struct equil_matrix {
     if (ev_loop0) cudaEventDestroy(ev_loop0);
     if (ev_loop1) cudaEventDestroy(ev_loop1);
     if (ev_sweep) cudaEventDestroy(ev_sweep);
-    if (sweep_ne_host) cudaFreeHost(sweep_ne_host);
     if (graph) cudaGraphExecDestroy(graph);
     for (void* q : peer_mapped) cudaIpcCloseMemHandle(q);
     if (comm && nccl().ok) nccl().CommDestroy(comm);

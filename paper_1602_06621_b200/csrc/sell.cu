@@ -15,7 +15,9 @@
 // longest-processing-time order: the 10^4-entry rows of a Zipf matrix start at
 // once instead of trailing the launch).  Rows longer than kTileNnz go to the
 // warp-specialised sell_long_kernel, the rest to sell_warp_kernel; the two run
-// concurrently.  By default (SgdSplitOp) both only store each row's sum and
+// concurrently.  (On one GPU the SGD passes run A's long rows on the column
+// sweep of sweep.cu instead, when the matrix allows it; sell_long_kernel then
+// serves the generic passes.)  By default (SgdSplitOp) both only store each row's sum and
 // sgd_update_rows_kernel then applies the SGD update (sgd_epilogue,
 // sgd_common.cuh) to every row; SgdOp fuses the epilogue instead, SgdBlockOp
 // carries sums between column-block rounds, PassOp<NV> runs the generic passes

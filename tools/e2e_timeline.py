@@ -17,7 +17,7 @@ v = torch.from_numpy(inst.val).pin_memory().numpy()
 out = tuple(torch.empty(k, dtype=torch.float64).pin_memory().numpy()
             for k in (inst.m, inst.n, inst.m, inst.n))
 p = eq.EquilibrationParams(alpha=inst.alpha, beta=inst.beta, iterations=100, seed=0)
-for k in range(6):
+for k in range(int(os.environ.get("E2E_REPS", "6"))):
     t0 = time.perf_counter()
     eq.sgd_equilibrate_csr(inst.m, inst.n, rp, c, v, p, out=out)
     print(f"one-shot {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr, flush=True)

@@ -11,3 +11,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --c
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sweep_kernel|sell_warp|sell_long|sgd_update" -s 6 -c 3 -f -o gpurun_out/prof_r2g_sgd python tools/ncu_target.py 3 3 1 > gpurun_out/ncu_f.log 2>&1; echo "ncu full rc=$?"; tail -2 gpurun_out/ncu_f.log
 timeout 300 python tools/lsqr_prof.py 10 > gpurun_out/lp.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_lsqr.csv python tools/lsqr_prof.py 10 > gpurun_out/lp_ncu.log 2>&1; echo "ncu lsqr rc=$?"
+bash tools/sweep_ncu_full.sh
