@@ -23,6 +23,8 @@ if os.environ.get("RESIDENT"):
     for _ in range(3):
         eq.sgd_equilibrate(M, p)
     print("resident handle", stat(), flush=True)
+    if os.environ.get("RESIDENT") == "closed":
+        M.close()
 for k in range(int(os.environ.get("E2E_REPS", "12"))):
     t0 = time.perf_counter()
     eq.sgd_equilibrate_csr(inst.m, inst.n, rp, c, v, p, out=out)
