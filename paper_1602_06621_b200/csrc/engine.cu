@@ -572,19 +572,30 @@ void build_sell_blocked(equil_matrix* M) {
 }
 
 // interleaved arrays of matrix `mat`: columns (mapped to slots) and / or values
-void build_sell_arrays(equil_matrix* M, int mat, bool cols, bool vals) {
+// part 0: every slice of the matrix; 1: only its long slices (rows longer than
+// kTileNnz, the leading entries of the launch order); 2: all but those
+void build_sell_arrays(equil_matrix* M, int mat, bool cols, bool vals, int part = 0) {
   const equil_matrix::SellHost& H = M->sell_host;
   cudaStream_t s = M->stream;
+  // A's long slices are not needed by a one-shot SGD call that runs them on the
+  // column sweep (M->sell_skip_long; build_sweep_layout completes them if the
+  // sweep does not come about)
+  if (part == 0 && mat == 0 && M->sell_skip_long) part = 2;
+  const size_t nl = std::min<size_t>(static_cast<size_t>(H.plong[mat]), H.midx[mat].size());
+  const size_t i0 = part == 2 ? nl : 0, i1 = part == 1 ? nl : H.midx[mat].size();
+  if (i1 <= i0) return;
+  std::vector<int64_t> kbp(H.kbp[mat].begin() + i0, H.kbp[mat].begin() + i1 + 1);
+  for (int64_t& k : kbp) k -= H.kbp[mat][i0];
   DevBuf<int64_t> dkbp;
   DevBuf<int32_t> didx;
-  dkbp.alloc_on(H.kbp[mat].size(), s);
-  didx.alloc_on(H.midx[mat].size(), s);
-  h2d(M, dkbp.p, H.kbp[mat].data(), H.kbp[mat].size() * 8);
-  h2d(M, didx.p, H.midx[mat].data(), H.midx[mat].size() * 4);
+  dkbp.alloc_on(kbp.size(), s);
+  didx.alloc_on(i1 - i0, s);
+  h2d(M, dkbp.p, kbp.data(), kbp.size() * 8);
+  h2d(M, didx.p, H.midx[mat].data() + i0, (i1 - i0) * 4);
+  if (!M->pull_uploads) CK(cudaStreamSynchronize(s));  // kbp is a local (pageable) vector
   const eqb::DevCsr& C = mat ? M->AT : M->A;
-  CK(eqb::build_sell(C.row_ptr, C.col, mat ? M->wmap.p : M->smap.p, C.val, dkbp.p,
-                     H.kbp[mat].back(), didx.p,
-                     static_cast<int>(H.midx[mat].size()), M->sell_slices.p, M->sell_row.p,
+  CK(eqb::build_sell(C.row_ptr, C.col, mat ? M->wmap.p : M->smap.p, C.val, dkbp.p, kbp.back(),
+                     didx.p, static_cast<int>(i1 - i0), M->sell_slices.p, M->sell_row.p,
                      M->sell_len.p, nullptr, cols ? M->sell_ci[mat].p : nullptr,
                      vals ? M->sell_va[mat].p : nullptr, s, quad_min(M)));
 }
@@ -728,6 +739,7 @@ void plan_sweep_layout(equil_matrix* M) {
   M->sweep = false;
   M->sweep_values_pending = false;
   M->sweep_plan_ok = false;
+  M->sell_skip_long = false;
   if (!M->sweep_candidate || !M->use_sell || !M->slots || M->sell_long != 2 || !M->split_epi ||
       M->nblk[0] > 1 || M->nblk[1] > 1)
     return;
@@ -768,15 +780,28 @@ void plan_sweep_layout(equil_matrix* M) {
   sweep_enqueue_runs(M, sp);
   sp.ok = true;
   M->sweep_plan_ok = true;
+  M->sell_skip_long = M->oneshot_hint;  // (see build_sell_arrays)
   M->sweep_plan_G = sp.G;
   M->sweep_plan_R = sp.R;
   M->sweep_plan_W = sp.W;
 }
 
+static void build_sweep_layout_impl(equil_matrix* M, bool with_values);
 void build_sweep_layout(equil_matrix* M, bool with_values) {
   if (!M->sweep_plan_ok) return;
   M->sweep_plan_ok = false;
+  build_sweep_layout_impl(M, with_values);
+  // A's long interleaved slices were left out for the sweep: if it did not come
+  // about, the long-slice kernel needs them after all
+  if (M->sell_skip_long && !M->sweep) {
+    M->sell_skip_long = false;
+    if (M->sell) build_sell_arrays(M, 0, true, with_values, 1);
+  }
+}
+
+static void build_sweep_layout_impl(equil_matrix* M, bool with_values) {
   if (!M->sell || M->sell_nb != 1) return;
+  if (getenv("EQUIL_SWEEP_FAIL")) return;  // test hook: the layout "does not fit"
   cudaStream_t s = M->stream;
   SweepPlan sp;
   sp.G = M->sweep_plan_G;
@@ -1855,6 +1880,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     cudaStream_t s = M->stream;
     // The sweep layout adds ~4 ms to a pipelined c3 setup and saves ~0.09 ms per
     // iteration: a one-shot call of few iterations keeps the long-slice kernel
+    M->oneshot_hint = pre != nullptr;  // the handle serves one SGD call and is destroyed
     if (pre && pre->total > 0 && !M->sweep_forced &&
         pre->total / static_cast<uint64_t>(m + n) < 64)
       M->use_sweep = false;

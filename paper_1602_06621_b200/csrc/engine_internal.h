@@ -562,6 +562,8 @@ struct equil_matrix {
   bool sweep_candidate = false;  // decided before the slot maps: xs keeps column order
   int64_t sweep_long_nnz = 0;
   std::vector<int32_t> sweep_rows_host;  // A's rows longer than kTileNnz, longest first
+  bool oneshot_hint = false;    // created by the one-shot entry point
+  bool sell_skip_long = false;  // A's long interleaved slices not built (the sweep serves them)
   bool sweep_plan_ok = false;  // plan_sweep_layout enqueued; build_sweep_layout finishes it
   int sweep_plan_G = 0, sweep_plan_R = 0, sweep_plan_W = 0;
   uint32_t* sweep_ne_host = nullptr;  // pinned (thread-cached): per-(CTA, panel) padded entry counts

@@ -147,3 +147,19 @@ def test_sweep_few_long_rows_and_boundaries():
         got = _with_env(dict(env, EQUIL_SWEEP="1"), go)
         for k in "uvde":
             assert np.array_equal(getattr(got, k), getattr(want, k)), (env, k)
+
+
+def test_one_shot_call_with_and_without_the_sweep(c3s):
+    """The one-shot entry point (from 64 iterations it plans the sweep and leaves A's
+    long interleaved slices out): with the sweep, with the sweep layout failing after
+    the slices were left out (EQUIL_SWEEP_FAIL: they are completed for the long-slice
+    kernel), and under 64 iterations (no sweep) -- all bit-identical to the oracle."""
+    inst = c3s
+    A = oracle.CsrArrays(inst.m, inst.n, inst.row_ptr, inst.col, inst.val)
+    for T, env in ((64, {}), (64, {"EQUIL_SWEEP_FAIL": "1"}), (20, {})):
+        want = oracle.c_oracle().sgd_equilibrate(A, iterations=T, seed=8)
+        got = _with_env(env, lambda: eq.sgd_equilibrate_csr(
+            inst.m, inst.n, inst.row_ptr, inst.col, inst.val,
+            eq.EquilibrationParams(iterations=T, seed=8)))
+        for k in "uvde":
+            assert np.array_equal(getattr(got, k), getattr(want, k)), (T, env, k)
