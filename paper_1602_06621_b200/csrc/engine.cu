@@ -1864,11 +1864,16 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     require(n < (1LL << 31) && m < (1LL << 31), "ExplicitMatrix::sparse: dimension too large");
     const int64_t nnz = row_ptr[m];
     require(nnz >= 0 && nnz < (1LL << 31), "ExplicitMatrix::sparse: bad nnz");
-    // row_ptr is checked on the host before anything reads the arrays by it
+    // row_ptr is checked on the host before anything reads the arrays by it; the
+    // O(m) monotonicity scan runs below, once the uploads (which need only nnz)
+    // are on their way
     require(row_ptr[0] == 0, "ExplicitMatrix::sparse: row_ptr[0] must be 0");
-    for (int64_t i = 0; i < m; ++i)
-      if (row_ptr[i + 1] < row_ptr[i])
-        fail(EQUIL_EINVAL, "ExplicitMatrix::sparse: row_ptr decreases at row " + std::to_string(i));
+    auto check_monotone = [&] {
+      for (int64_t i = 0; i < m; ++i)
+        if (row_ptr[i + 1] < row_ptr[i])
+          fail(EQUIL_EINVAL,
+               "ExplicitMatrix::sparse: row_ptr decreases at row " + std::to_string(i));
+    };
     require(nnz == 0 || (col && val), "ExplicitMatrix::sparse: null col/val");
     PhaseTimer pt("create_csr");
     auto M = std::make_unique<equil_matrix>();
@@ -1897,6 +1902,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     }
     pt.mark(s, "setup");
     if (M->world > 1) {  // each rank uploads and transposes only its rows
+      check_monotone();
       create_sharded(M.get(), row_ptr, col, val, pt);
       alloc_workspaces(M.get(), &pt);
       CK(cudaStreamSynchronize(s));
@@ -1923,6 +1929,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     } else {
       CK(cudaEventRecord(M->ev_vals, s));
     }
+    check_monotone();  // (while the copies run; nothing has read the arrays by row_ptr yet)
     eqb::DevCsr fullA{m, n, nnz, rp.p, ci.p, va.p};
     // plan CSR(A) on the host while the device validates and transposes
     Plan planA;
@@ -3284,7 +3291,13 @@ equil_status equil_sgd_equilibrate_csr(int64_t m, int64_t n, const int64_t* row_
   if (rc != EQUIL_OK) return rc;
   M->oneshot = true;  // one call on this handle: launch the loop directly, no graph
   rc = equil_sgd_equilibrate(M, p, nullptr, out);
+  const auto t0 = std::chrono::steady_clock::now();
   equil_matrix_destroy(M);
+  if (const char* e = getenv("EQUIL_VERBOSE"))
+    if (atoi(e) >= 2)
+      fprintf(stderr, "[equil] one-shot destroy %.2f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
   return rc;
 }
 
