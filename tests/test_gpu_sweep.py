@@ -163,3 +163,48 @@ def test_one_shot_call_with_and_without_the_sweep(c3s):
             eq.EquilibrationParams(iterations=T, seed=8)))
         for k in "uvde":
             assert np.array_equal(getattr(got, k), getattr(want, k)), (T, env, k)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_sweep_random_instances_match_long_kernel(seed):
+    """Random shapes, long-row counts, panel widths and stage counts: the sweep
+    and the long-slice kernel give the same u, v, d, e bit for bit (both are
+    pinned to the oracle elsewhere; here the two device paths check each other)."""
+    rng = np.random.default_rng(100 + seed)
+    m = int(rng.integers(200, 3000))
+    n = 2 * int(rng.integers(600, 12000))  # even
+    nlong = int(rng.integers(1, 300))
+    rows = []
+    long_at = set(rng.choice(m, size=min(nlong, m), replace=False).tolist())
+    for i in range(m):
+        if i in long_at:
+            L = int(rng.integers(513, min(n, 6000) + 1))
+        else:
+            # keep every column short: few entries per ordinary row
+            L = int(rng.integers(0, 8))
+        c = np.sort(rng.choice(n, size=L, replace=False))
+        rows.append((c, rng.standard_normal(L) * np.exp(rng.standard_normal(L))))
+    rp, ci, va = _csr_from_rows(m, n, rows)
+    # the sweep needs A^T free of long rows: cap the column counts
+    counts = np.bincount(ci, minlength=n)
+    if counts.max() > 512:
+        pytest.skip("instance has a long column")
+    width = [None, 128, 192, 300, 1024, 4096][seed % 6]
+    env = {"EQUIL_SWEEP": "1", "EQUIL_SWEEP_STAGES": str(2 + seed % 3)}
+    if width:
+        env["EQUIL_SWEEP_WIDTH"] = str(width)
+    p = eq.EquilibrationParams(iterations=7, seed=seed)
+
+    def run(envs, expect_on):
+        def go():
+            M = eq.ExplicitMatrix.from_csr(m, n, rp, ci, va)
+            assert eq.sweep_active(M) == expect_on
+            r = eq.sgd_equilibrate(M, p)
+            M.close()
+            return r
+        return _with_env(envs, go)
+
+    got = run(env, True)
+    base = run({"EQUIL_SWEEP": "0"}, False)
+    for k in "uvde":
+        assert np.array_equal(getattr(got, k), getattr(base, k)), (seed, k)
