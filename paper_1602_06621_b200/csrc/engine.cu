@@ -1875,9 +1875,32 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
                "ExplicitMatrix::sparse: row_ptr decreases at row " + std::to_string(i));
     };
     require(nnz == 0 || (col && val), "ExplicitMatrix::sparse: null col/val");
+    // the scan runs on a helper thread from here; its verdict is taken before
+    // anything reads the arrays by row_ptr, and it outranks a device error
+    // (on a box without a GPU a bad row_ptr is still reported as such)
+    std::future<void> mono = std::async(std::launch::async, check_monotone);
+    struct MonoJoin {
+      std::future<void>& f;
+      ~MonoJoin() {
+        if (f.valid()) {
+          try {
+            f.get();
+          } catch (...) {
+          }
+        }
+      }
+    } mono_join{mono};
+    auto mono_get = [&] {
+      if (mono.valid()) mono.get();
+    };
     PhaseTimer pt("create_csr");
     auto M = std::make_unique<equil_matrix>();
-    setup_common(M.get(), cfg);
+    try {
+      setup_common(M.get(), cfg);
+    } catch (...) {
+      mono_get();
+      throw;
+    }
     M->m = m;
     M->n = n;
     M->nnz = nnz;
@@ -1902,7 +1925,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     }
     pt.mark(s, "setup");
     if (M->world > 1) {  // each rank uploads and transposes only its rows
-      check_monotone();
+      mono_get();
       create_sharded(M.get(), row_ptr, col, val, pt);
       alloc_workspaces(M.get(), &pt);
       CK(cudaStreamSynchronize(s));
@@ -1929,7 +1952,7 @@ static equil_status create_csr_impl(int64_t m, int64_t n, const int64_t* row_ptr
     } else {
       CK(cudaEventRecord(M->ev_vals, s));
     }
-    check_monotone();  // (while the copies run; nothing has read the arrays by row_ptr yet)
+    mono_get();  // (the copies are running; nothing has read the arrays by row_ptr yet)
     eqb::DevCsr fullA{m, n, nnz, rp.p, ci.p, va.p};
     // plan CSR(A) on the host while the device validates and transposes
     Plan planA;

@@ -18,6 +18,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <future>
 #include <thread>
 #include <vector>
 
