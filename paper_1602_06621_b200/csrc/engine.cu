@@ -718,11 +718,15 @@ void sweep_enqueue_runs(equil_matrix* M, SweepPlan& sp) {
   struct PinnedScratch {
     uint32_t* p = nullptr;
     size_t cap = 0;
+    ~PinnedScratch() {  // at thread exit (an error after runtime shutdown is moot)
+      if (p) cudaFreeHost(p);
+    }
   };
   static thread_local PinnedScratch ps;
   if (ps.cap < sp.ncp) {
     if (ps.p) cudaFreeHost(ps.p);
-    ps = PinnedScratch{};
+    ps.p = nullptr;
+    ps.cap = 0;
     void* q = nullptr;
     CK(cudaHostAlloc(&q, sp.ncp * 4 * 2, cudaHostAllocDefault));
     ps.p = static_cast<uint32_t*>(q);
